@@ -1,0 +1,34 @@
+# Builds the B200 product library (CUDA kernels + C ABI + C++ drop-in API)
+# and the CPU checkers under oracle/.  `python -c "import __graft_entry__ as g;
+# g.build()"` drives the same targets.
+NVCC    ?= nvcc
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+PKG     := paper_2009_07495_b200
+BUILD   := build
+LIB     := $(PKG)/libigm_b200.so
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -fmad=false -Iinclude
+CXXFLAGS:= -O2 -std=c++20 -fPIC -ffp-contract=off -fno-fast-math -Wall -Iinclude
+HDRS    := $(wildcard $(PKG)/csrc/*.cuh) include/igm.h $(wildcard include/intgmres/*.hpp)
+
+all: $(LIB) oracle
+
+$(BUILD)/%.o: $(PKG)/csrc/%.cu $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(BUILD)/shim.o: $(PKG)/csrc/shim.cpp $(HDRS)
+	@mkdir -p $(BUILD)
+	g++ $(CXXFLAGS) -I/usr/local/cuda/include -c $< -o $@
+
+$(LIB): $(BUILD)/kernels.o $(BUILD)/capi.o $(BUILD)/shim.o
+	$(NVCC) $(ARCH) -shared -o $@ $^
+
+oracle:
+	$(MAKE) -C oracle all
+	@if [ -d /root/reference/proj/core ]; then $(MAKE) -C oracle ref; fi
+
+clean:
+	rm -rf $(BUILD) $(LIB)
+	$(MAKE) -C oracle clean
+
+.PHONY: all oracle clean

@@ -1,0 +1,237 @@
+/*
+ * igm.h -- C ABI of the B200-native int-GMRES hot path (libigm_b200.so).
+ *
+ * Plain C: opaque handles, plain pointers and sizes, status codes.  No torch,
+ * no C++ types.  Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj/core/).  The C++ drop-in API in
+ * include/intgmres/ (*.hpp) is implemented on top of these calls.
+ *
+ * Memory: every vector/array argument may be HOST memory or DEVICE memory of
+ * the context's GPU; the library detects which (cudaPointerGetAttributes) and
+ * stages host buffers through its own device workspace.  Results are written
+ * back into the same space the output pointer lives in.
+ *
+ * Errors: every call returns igm_status; igm_last_error() returns the message
+ * of the last failure on the calling thread.  Status codes map 1:1 onto the
+ * reference's exception types; the C++ shim re-throws them.
+ *
+ * Threading: a context owns one CUDA stream; calls on one context must be
+ * serialised by the caller (the reference is single-threaded, FxTrace is not
+ * thread-safe).  Uploaded matrices are immutable and may be shared by
+ * contexts on the same device.
+ */
+#ifndef IGM_H
+#define IGM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  IGM_OK = 0,
+  IGM_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  IGM_DOMAIN_ERROR = 2,     /* std::domain_error */
+  IGM_OVERFLOW_ERROR = 3,   /* std::overflow_error */
+  IGM_RUNTIME_ERROR = 4,    /* std::runtime_error */
+  IGM_LOGIC_ERROR = 5,      /* std::logic_error */
+  IGM_CUDA_ERROR = 6,       /* device / driver failure (no reference analogue) */
+  IGM_NCCL_ERROR = 7
+} igm_status;
+
+typedef struct igm_ctx igm_ctx;     /* device, stream, workspaces */
+typedef struct igm_split igm_split; /* device-resident SplitMatrix */
+typedef struct igm_csrf igm_csrf;   /* device-resident CsrMatrixF */
+typedef struct igm_ilu igm_ilu;     /* device-resident IluFactors + schedule */
+
+/* ShiftPlan (fxp.hpp:262-278) */
+typedef struct {
+  int dot_b1, dot_b2, axpy_b1, norm_b1, div_b1, div_b2, givens_b2, rot_b;
+} igm_shifts;
+
+/* FxTrace (fxp.hpp:51-103), caller-owned; survives failed calls with its
+ * counts updated (test_refine.cpp:175-203).  `exact` is set to 0 when a
+ * reduction MAY have wrapped in its running sum, in which case `total`
+ * counts the order-free events (mul/sub/shl/div and per-row adds) only. */
+typedef struct {
+  int checked;       /* in: record overflow events */
+  int record_shifts; /* in: log (kernel, b1, b2) per shifted call */
+  int kernel, restart, step; /* in/out: current location */
+  uint64_t total;    /* in/out: accumulates */
+  int n_events, cap_events;
+  int32_t* events;   /* 4 ints each: kernel, op, restart, step */
+  int64_t n_shifts;
+  int cap_shifts;
+  int32_t* shifts;   /* 3 ints each: kernel, b1, b2 */
+  int exact;         /* out */
+} igm_trace;
+
+/* ---- context ---------------------------------------------------------- */
+igm_status igm_ctx_create(int device, igm_ctx** out);
+void igm_ctx_destroy(igm_ctx* ctx);
+igm_status igm_ctx_synchronize(igm_ctx* ctx);
+/* CUDA stream (cudaStream_t) the context launches on. */
+void* igm_ctx_stream(igm_ctx* ctx);
+/* number of kernels this context has launched so far */
+uint64_t igm_ctx_launch_count(igm_ctx* ctx);
+const char* igm_last_error(void);
+const char* igm_version(void);
+
+/* ---- uploads (the hot path's inputs) ----------------------------------- */
+/* SplitMatrix (split.hpp:28-37): ncomp components sharing one CSR pattern;
+ * comp_vals is ncomp*nnz int64, component-major; alphas[0] == 0. */
+igm_status igm_upload_split(igm_ctx* ctx, int n, int nnz, const int* row_ptr,
+                            const int* col_idx, int ncomp,
+                            const int64_t* comp_vals, const int* alphas,
+                            igm_split** out);
+void igm_split_free(igm_split* m);
+/* CsrMatrixF (csr.hpp:10-18), the FP64 system matrix of residual_fp. */
+igm_status igm_upload_csrf(igm_ctx* ctx, int n, const int* row_ptr,
+                           const int* col_idx, const double* vals,
+                           igm_csrf** out);
+void igm_csrf_free(igm_csrf* a);
+/* IluFactors (ilu.hpp:27-32): lower = L*D_l, upper = D_u*U, diagonal stored
+ * at diag_pos.  Builds the wavefront schedule and per-row reciprocals. */
+igm_status igm_upload_ilu(igm_ctx* ctx, int n, const int* l_row_ptr,
+                          const int* l_col_idx, const int64_t* l_vals,
+                          const int* l_diag_pos, const int* u_row_ptr,
+                          const int* u_col_idx, const int64_t* u_vals,
+                          const int* u_diag_pos, igm_ilu** out);
+void igm_ilu_free(igm_ilu* f);
+/* levels of the forward / backward substitution DAGs (diagnostics) */
+int igm_ilu_levels(const igm_ilu* f, int backward);
+
+/* ---- primitives (parity entry points) ---------------------------------- */
+/* replaces intgmres::spmv (split.hpp:48-49, split.cpp:137-157) */
+igm_status igm_spmv(igm_ctx* ctx, const igm_split* m, int s, const int64_t* v,
+                    int64_t* out, igm_trace* t);
+/* replaces intgmres::apply_inverse (ilu.hpp:40-41, ilu.cpp:122-155) */
+igm_status igm_apply_inverse(igm_ctx* ctx, const igm_ilu* f, const int64_t* y,
+                             int64_t* out, igm_trace* t);
+/* replaces intgmres::apply_inverse_fp (ilu.hpp:44-45, ilu.cpp:157-180) */
+igm_status igm_apply_inverse_fp(igm_ctx* ctx, const igm_ilu* f,
+                                const double* y, double* out);
+/* replaces intgmres::fx_dot / fx_norm / fx_axpy_sub (fxp.hpp:248-257) */
+igm_status igm_fx_dot(igm_ctx* ctx, int64_t n, const int64_t* v,
+                      const int64_t* w, int frac_bits, int b1, int b2,
+                      int64_t* out, igm_trace* t);
+igm_status igm_fx_norm(igm_ctx* ctx, int64_t n, const int64_t* v,
+                       int frac_bits, int b1, int64_t* out, igm_trace* t);
+igm_status igm_fx_axpy_sub(igm_ctx* ctx, int64_t n, int64_t* w, int64_t h,
+                           const int64_t* v, int frac_bits, int b1,
+                           igm_trace* t);
+/* replaces intgmres::spmv_fp(CsrMatrixF) and residual_fp (csr.hpp:36-44) */
+igm_status igm_spmv_fp(igm_ctx* ctx, const igm_csrf* a, const double* x,
+                       double* y);
+igm_status igm_residual_fp(igm_ctx* ctx, const igm_csrf* a, const double* x,
+                           const double* b, double* r, double* relnorm);
+/* replaces intgmres::spmv_fp(SplitMatrix, s, x) (split.hpp:53-54) */
+igm_status igm_spmv_fp_split(igm_ctx* ctx, const igm_split* m, int s,
+                             const double* x, double* y);
+/* replaces intgmres::norm2 (csr.hpp:31): the sequential FP64 chain */
+igm_status igm_norm2(igm_ctx* ctx, int64_t n, const double* v, double* out);
+/* replaces intgmres::gamma_scale (refine.hpp:61, refine.cpp:11-19) */
+igm_status igm_gamma_scale(igm_ctx* ctx, int64_t n, const double* r,
+                           double* gamma, double* b_k);
+
+/* ---- the cycle and the solve ------------------------------------------- */
+/* CycleConfig (gmres_int.hpp:18-25) */
+typedef struct {
+  int m, frac_bits, s;
+  igm_shifts shifts;
+  const igm_ilu* precond; /* NULL = unpreconditioned */
+  int collect_basis_norms;
+} igm_cycle_cfg;
+
+/* CycleDiagnostics + ArnoldiState (gmres_int.hpp:27-44); host arrays sized
+ * by the caller, any may be NULL. */
+typedef struct {
+  int dim;
+  double r0_norm;
+  double* g_abs;       /* m */
+  double* cos_d;       /* m */
+  double* sin_d;       /* m */
+  double* basis_norms; /* m+1 */
+  int n_basis_norms;
+  int64_t* basis;      /* (m+1)*n */
+  int n_basis;
+  int64_t* hess;       /* (m+1)*m, column-major, ld = m+1 */
+  int64_t* g;          /* m+1 */
+  int64_t* cos_raw;    /* m */
+  int64_t* sin_raw;    /* m */
+} igm_cycle_out;
+
+/* replaces intgmres::run_cycle (gmres_int.hpp:51-54, gmres_int.cpp:42-196) */
+igm_status igm_run_cycle(igm_ctx* ctx, const igm_split* m,
+                         const igm_cycle_cfg* cfg, const double* b,
+                         const double* x0, double* x_out, igm_cycle_out* out,
+                         igm_trace* t);
+
+/* RefineConfig (refine.hpp:24-34).  The per-refinement depth schedule (a
+ * std::function in the reference, consulted once per refinement that runs,
+ * refine.cpp:61) is either a callback or an array indexed by refinement;
+ * with neither, the constant s is used. */
+typedef int (*igm_schedule_fn)(void* user, int k);
+typedef struct {
+  double tol;
+  int max_refinements, m, frac_bits, s, checked;
+  igm_shifts shifts;
+  const int* s_schedule;         /* NULL or max_refinements entries */
+  igm_schedule_fn s_schedule_fn; /* NULL or callback, wins over the array */
+  void* s_schedule_user;
+} igm_refine_cfg;
+
+/* SolveReport (refine.hpp:36-47); arrays sized max_refinements (+1). */
+typedef struct {
+  int converged, refinements;
+  int64_t total_inner_iterations;
+  int* inner_dims;
+  double* relres_history;
+  int n_relres;
+  double* gamma_history;
+  uint64_t* overflow_per_restart;
+  uint64_t overflow_total;
+  double wall_time_sec;
+  int overflow_exact; /* 0 if a reduction may have wrapped (see igm_trace) */
+} igm_report;
+
+/* replaces intgmres::solve (refine.hpp:67-70, refine.cpp:21-106) */
+igm_status igm_solve(igm_ctx* ctx, const igm_split* m, const igm_csrf* a_fp,
+                     const double* b, const igm_refine_cfg* cfg,
+                     const igm_ilu* precond, double* x_out, igm_report* rep,
+                     igm_trace* external_trace);
+
+/* ---- kernel microbench (BASELINE config 5) ------------------------------ */
+/* One call = w = spmv(m, s, v_in); then for i in 0..k-1:
+ * h_i = fx_dot(w, basis_i, dot_b1, dot_b2); fx_axpy_sub(w, h_i, basis_i,
+ * axpy_b1) -- unchecked (FxTrace* = nullptr).  basis is k*n device int64,
+ * v_in/w device.  h_out: k host int64 (may be NULL). */
+igm_status igm_spmv_mgs(igm_ctx* ctx, const igm_split* m, int s,
+                        const int64_t* v_in, const int64_t* basis, int k,
+                        int frac_bits, int dot_b1, int dot_b2, int axpy_b1,
+                        int64_t* w, int64_t* h_out);
+
+/* ---- host setup (not on the GPU hot path; inputs of the calls above) ---- */
+/* replaces intgmres::row_scale (split.cpp:61-79) */
+igm_status igm_row_scale(int n, const int* row_ptr, const int* col_idx,
+                         const double* vals, int alpha_a, double* vals_out,
+                         double* scale_out);
+/* replaces intgmres::build_split (split.cpp:90-135); comp_vals_out holds
+ * max_components*nnz */
+igm_status igm_build_split(int n, int nnz, const double* vals, int alpha_a,
+                           int max_components, int64_t* comp_vals_out,
+                           int* alphas_out, int* ncomp_out, int* exact_out);
+/* replaces intgmres::split_cast(factorize_ilu0(a)) (ilu.cpp:25-120);
+ * L/U arrays hold up to nnz(A) entries, row_ptr n+1 */
+igm_status igm_factorize_split_cast(int n, const int* row_ptr,
+                                    const int* col_idx, const double* vals,
+                                    int* l_row_ptr, int* l_col_idx,
+                                    int64_t* l_vals, int* l_diag_pos,
+                                    int* u_row_ptr, int* u_col_idx,
+                                    int64_t* u_vals, int* u_diag_pos);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,153 @@
+"""ctypes declarations of the C ABI in include/igm.h (libigm_b200.so).
+
+The shared library is built in-tree (``make`` / ``__graft_entry__.build()``).
+Loading fails loudly when it is missing: there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "libigm_b200.so"
+
+i32p = C.POINTER(C.c_int32)
+i64p = C.POINTER(C.c_int64)
+u64p = C.POINTER(C.c_uint64)
+f64p = C.POINTER(C.c_double)
+
+IGM_OK = 0
+STATUS_NAMES = {
+    0: "ok",
+    1: "invalid_argument",
+    2: "domain_error",
+    3: "overflow_error",
+    4: "runtime_error",
+    5: "logic_error",
+    6: "cuda_error",
+    7: "nccl_error",
+}
+
+KERNEL_NAMES = ["", "spmv", "precond", "dot", "axpy", "norm", "vec_div", "givens",
+                "givens_norm", "givens_div", "rot"]
+OP_NAMES = ["", "add", "sub", "mul", "shl", "div"]
+
+
+class Shifts(C.Structure):
+    _fields_ = [(n, C.c_int) for n in
+                ("dot_b1", "dot_b2", "axpy_b1", "norm_b1", "div_b1", "div_b2", "givens_b2", "rot_b")]
+
+
+class Trace(C.Structure):
+    _fields_ = [
+        ("checked", C.c_int), ("record_shifts", C.c_int),
+        ("kernel", C.c_int), ("restart", C.c_int), ("step", C.c_int),
+        ("total", C.c_uint64),
+        ("n_events", C.c_int), ("cap_events", C.c_int), ("events", i32p),
+        ("n_shifts", C.c_int64), ("cap_shifts", C.c_int), ("shifts", i32p),
+        ("exact", C.c_int),
+    ]
+
+
+class CycleCfg(C.Structure):
+    _fields_ = [("m", C.c_int), ("frac_bits", C.c_int), ("s", C.c_int), ("shifts", Shifts),
+                ("precond", C.c_void_p), ("collect_basis_norms", C.c_int)]
+
+
+class CycleOut(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int), ("r0_norm", C.c_double),
+        ("g_abs", f64p), ("cos_d", f64p), ("sin_d", f64p), ("basis_norms", f64p),
+        ("n_basis_norms", C.c_int),
+        ("basis", i64p), ("n_basis", C.c_int),
+        ("hess", i64p), ("g", i64p), ("cos_raw", i64p), ("sin_raw", i64p),
+    ]
+
+
+SCHED_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int)
+
+
+class RefineCfg(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_refinements", C.c_int), ("m", C.c_int),
+                ("frac_bits", C.c_int), ("s", C.c_int), ("checked", C.c_int),
+                ("shifts", Shifts), ("s_schedule", i32p), ("s_schedule_fn", SCHED_FN),
+                ("s_schedule_user", C.c_void_p)]
+
+
+class Report(C.Structure):
+    _fields_ = [
+        ("converged", C.c_int), ("refinements", C.c_int),
+        ("total_inner_iterations", C.c_int64),
+        ("inner_dims", i32p), ("relres_history", f64p), ("n_relres", C.c_int),
+        ("gamma_history", f64p), ("overflow_per_restart", u64p),
+        ("overflow_total", C.c_uint64), ("wall_time_sec", C.c_double),
+        ("overflow_exact", C.c_int),
+    ]
+
+
+# (name, restype, argtypes) for every entry point declared in include/igm.h
+SIGNATURES = [
+    ("igm_ctx_create", C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    ("igm_ctx_destroy", None, [C.c_void_p]),
+    ("igm_ctx_synchronize", C.c_int, [C.c_void_p]),
+    ("igm_ctx_stream", C.c_void_p, [C.c_void_p]),
+    ("igm_ctx_launch_count", C.c_uint64, [C.c_void_p]),
+    ("igm_last_error", C.c_char_p, []),
+    ("igm_version", C.c_char_p, []),
+    ("igm_upload_split", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                                   C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
+    ("igm_split_free", None, [C.c_void_p]),
+    ("igm_upload_csrf", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.POINTER(C.c_void_p)]),
+    ("igm_csrf_free", None, [C.c_void_p]),
+    ("igm_upload_ilu", C.c_int, [C.c_void_p, C.c_int] + [C.c_void_p] * 8 + [C.POINTER(C.c_void_p)]),
+    ("igm_ilu_free", None, [C.c_void_p]),
+    ("igm_ilu_levels", C.c_int, [C.c_void_p, C.c_int]),
+    ("igm_spmv", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.POINTER(Trace)]),
+    ("igm_apply_inverse", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(Trace)]),
+    ("igm_apply_inverse_fp", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("igm_fx_dot", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,
+                             i64p, C.POINTER(Trace)]),
+    ("igm_fx_norm", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int, C.c_int, i64p,
+                              C.POINTER(Trace)]),
+    ("igm_fx_axpy_sub", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int,
+                                  C.c_int, C.POINTER(Trace)]),
+    ("igm_spmv_fp", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("igm_residual_fp", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, f64p]),
+    ("igm_spmv_fp_split", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
+    ("igm_norm2", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, f64p]),
+    ("igm_gamma_scale", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, f64p, C.c_void_p]),
+    ("igm_run_cycle", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(CycleCfg), C.c_void_p, C.c_void_p,
+                                C.c_void_p, C.POINTER(CycleOut), C.POINTER(Trace)]),
+    ("igm_solve", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(RefineCfg),
+                            C.c_void_p, C.c_void_p, C.POINTER(Report), C.POINTER(Trace)]),
+    ("igm_spmv_mgs", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                               C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, i64p]),
+    ("igm_row_scale", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
+                                C.c_void_p]),
+    ("igm_build_split", C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
+                                  C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("igm_factorize_split_cast", C.c_int, [C.c_int] + [C.c_void_p] * 11),
+]
+
+_lib = None
+
+
+def load(path: os.PathLike | str | None = None) -> C.CDLL:
+    """Load libigm_b200.so (no fallback: raises if it has not been built)."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise RuntimeError(f"{p} is missing: build it with `make` or __graft_entry__.build(); "
+                           "the int-GMRES path has no CPU fallback")
+    lib = C.CDLL(str(p))
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib

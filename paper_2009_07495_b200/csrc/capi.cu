@@ -1,0 +1,1174 @@
+// capi.cu -- the extern "C" boundary (include/igm.h) and the host drivers
+// that enqueue the device cycle / refinement loop.
+//
+// Control flow: a whole int-GMRES(m) cycle is enqueued on the context's
+// stream without any host round trip (kernels early-exit through the Ctl
+// block after a break or an error).  The host synchronises once per cycle
+// (run_cycle) or once per refinement (solve), exactly where the reference's
+// outer loop needs a scalar decision (refine.cpp:52-55, 85).
+#include "igm_internal.cuh"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+using namespace igm;
+
+namespace {
+
+thread_local std::string t_err;
+
+igm_status set_err(igm_status s, const std::string& msg) {
+  t_err = msg;
+  return s;
+}
+
+struct CudaFail : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ApiFail {
+  igm_status st;
+  std::string msg;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaFail(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+igm_status guarded(F&& fn) {
+  try {
+    fn();
+    return IGM_OK;
+  } catch (const ApiFail& f) {
+    return set_err(f.st, f.msg);
+  } catch (const CudaFail& e) {
+    return set_err(IGM_CUDA_ERROR, e.what());
+  } catch (const std::bad_alloc&) {
+    return set_err(IGM_CUDA_ERROR, "host allocation failed");
+  }
+}
+
+[[noreturn]] void fail(igm_status s, const std::string& m) { throw ApiFail{s, m}; }
+
+const char* em_text(int id) {
+  switch (id) {
+    case EM_NORM_NEG: return "fx_norm: accumulator wrapped negative";
+    case EM_DIV_ZERO: return "fx_div: shifted divisor is zero";
+    case EM_ENCODE: return "encode: value outside representable range";
+    case EM_HESS_ZERO: return "solve_hessenberg: zero diagonal";
+    case EM_GAMMA_ZERO: return "gamma_scale: zero residual";
+    default: return "device error";
+  }
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+template <class T>
+T* dalloc(size_t count) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  ck(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+  return static_cast<T*>(p);
+}
+
+template <class T>
+T* dupload(const T* src, size_t count, cudaStream_t st) {
+  T* d = dalloc<T>(count);
+  if (count) ck(cudaMemcpyAsync(d, src, count * sizeof(T), cudaMemcpyDefault, st), "upload");
+  return d;
+}
+
+template <class T>
+std::vector<T> to_host(const T* src, size_t count) {
+  std::vector<T> h(count);
+  if (count) ck(cudaMemcpy(h.data(), src, count * sizeof(T), cudaMemcpyDefault), "to_host");
+  return h;
+}
+
+void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+}  // namespace
+
+void igm_internal_set_error(const std::string& msg) { t_err = msg; }
+
+// ---------------------------------------------------------------------------
+// context
+
+struct Work {
+  long long n = 0;
+  int m = 0;
+  i64* basis = nullptr;  // (m+1) * n
+  i64* w = nullptr;
+  i64* z = nullptr;
+  i64* vin = nullptr;
+  double* r = nullptr;
+  double* r0 = nullptr;
+  double* t1 = nullptr;
+  double* x = nullptr;
+  double* b = nullptr;
+  double* x0 = nullptr;
+  // per-cycle small arrays, one allocation
+  unsigned char* small = nullptr;
+  size_t small_bytes = 0;
+  u64 *acc = nullptr, *absacc = nullptr, *nacc = nullptr, *nabs = nullptr, *cnt = nullptr;
+  i64 *hess = nullptr, *g = nullptr, *cs = nullptr, *sn = nullptr, *gabs = nullptr;
+  int* steprec = nullptr;
+  double *y = nullptr, *wts = nullptr, *bnorms = nullptr;
+  unsigned char* h_small = nullptr;  // pinned mirror
+};
+
+struct igm_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  Ctl* ctl = nullptr;
+  Ctl* h_ctl = nullptr;  // pinned
+  Work ws;
+  // primitive scratch
+  u64* red = nullptr;  // acc, abs hi, abs lo, cnt[OP_COUNT]
+  u64* h_red = nullptr;
+};
+
+namespace {
+
+void ws_free(Work& w) {
+  dfree(w.basis); dfree(w.w); dfree(w.z); dfree(w.vin); dfree(w.r); dfree(w.r0); dfree(w.t1);
+  dfree(w.x); dfree(w.b); dfree(w.x0); dfree(w.small);
+  if (w.h_small) cudaFreeHost(w.h_small);
+  w = Work{};
+}
+
+size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
+
+void ws_ensure(igm_ctx* c, long long n, int m) {
+  Work& w = c->ws;
+  if (n <= w.n && m <= w.m && w.basis) return;
+  const long long nn = std::max<long long>(n, w.n);
+  const int mm = std::max(m, w.m);
+  ws_free(w);
+  w.n = nn;
+  w.m = mm;
+  w.basis = dalloc<i64>(static_cast<size_t>(mm + 1) * nn);
+  w.w = dalloc<i64>(nn);
+  w.z = dalloc<i64>(nn);
+  w.vin = dalloc<i64>(nn);
+  w.r = dalloc<double>(nn);
+  w.r0 = dalloc<double>(nn);
+  w.t1 = dalloc<double>(nn);
+  w.x = dalloc<double>(nn);
+  w.b = dalloc<double>(nn);
+  w.x0 = dalloc<double>(nn);
+  // small arrays
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes); return o; };
+  const size_t o_acc = take(sizeof(u64) * mm * (mm + 1));
+  const size_t o_abs = take(sizeof(u64) * mm * (mm + 1) * 2);
+  const size_t o_nacc = take(sizeof(u64) * mm);
+  const size_t o_nabs = take(sizeof(u64) * mm * 2);
+  const size_t o_cnt = take(sizeof(u64) * mm * K_COUNT * OP_COUNT);
+  const size_t o_hess = take(sizeof(i64) * (mm + 1) * mm);
+  const size_t o_g = take(sizeof(i64) * (mm + 1));
+  const size_t o_cs = take(sizeof(i64) * mm);
+  const size_t o_sn = take(sizeof(i64) * mm);
+  const size_t o_gabs = take(sizeof(i64) * mm);
+  const size_t o_rec = take(sizeof(int) * mm);
+  const size_t o_y = take(sizeof(double) * mm);
+  const size_t o_wts = take(sizeof(double) * mm);
+  const size_t o_bn = take(sizeof(double) * (mm + 1));
+  w.small_bytes = off;
+  w.small = dalloc<unsigned char>(off);
+  ck(cudaMallocHost(reinterpret_cast<void**>(&w.h_small), off), "cudaMallocHost");
+  w.acc = reinterpret_cast<u64*>(w.small + o_acc);
+  w.absacc = reinterpret_cast<u64*>(w.small + o_abs);
+  w.nacc = reinterpret_cast<u64*>(w.small + o_nacc);
+  w.nabs = reinterpret_cast<u64*>(w.small + o_nabs);
+  w.cnt = reinterpret_cast<u64*>(w.small + o_cnt);
+  w.hess = reinterpret_cast<i64*>(w.small + o_hess);
+  w.g = reinterpret_cast<i64*>(w.small + o_g);
+  w.cs = reinterpret_cast<i64*>(w.small + o_cs);
+  w.sn = reinterpret_cast<i64*>(w.small + o_sn);
+  w.gabs = reinterpret_cast<i64*>(w.small + o_gabs);
+  w.steprec = reinterpret_cast<int*>(w.small + o_rec);
+  w.y = reinterpret_cast<double*>(w.small + o_y);
+  w.wts = reinterpret_cast<double*>(w.small + o_wts);
+  w.bnorms = reinterpret_cast<double*>(w.small + o_bn);
+}
+
+// host view of the small arrays after a cycle
+template <class T>
+const T* hview(const Work& w, const void* dptr) {
+  return reinterpret_cast<const T*>(w.h_small + (static_cast<const unsigned char*>(dptr) - w.small));
+}
+
+ShiftsD to_sd(const igm_shifts& s) {
+  return ShiftsD{s.dot_b1, s.dot_b2, s.axpy_b1, s.norm_b1, s.div_b1, s.div_b2, s.givens_b2, s.rot_b};
+}
+
+// ShiftPlan::validate (fxp.cpp:106-127)
+void validate_shifts(const igm_shifts& p, int f) {
+  auto right = [f](int b, const char* name) {
+    if (b < 0 || (b > 0 && b >= f))
+      fail(IGM_INVALID_ARGUMENT, std::string("ShiftPlan: ") + name + " must lie in [0, frac_bits)");
+  };
+  right(p.dot_b1, "dot_b1");
+  right(p.dot_b2, "dot_b2");
+  right(p.axpy_b1, "axpy_b1");
+  right(p.norm_b1, "norm_b1");
+  right(p.div_b2, "div_b2");
+  right(p.givens_b2, "givens_b2");
+  if (p.div_b1 < 0 || p.div_b1 > f) fail(IGM_INVALID_ARGUMENT, "ShiftPlan: div_b1 must lie in [0, frac_bits]");
+  if (p.rot_b != 0) fail(IGM_INVALID_ARGUMENT, "ShiftPlan: rot_b must be 0");
+  if (2 * (f - p.norm_b1) > 62)
+    fail(IGM_INVALID_ARGUMENT, "ShiftPlan: norm accumulator needs 2*(frac_bits - norm_b1) <= 62");
+}
+
+void check_qformat(int f) {
+  if (f < 0 || f > 62) fail(IGM_INVALID_ARGUMENT, "QFormat: frac_bits must be in [0, 62]");
+}
+
+void check_shift(int b, const char* who) {
+  if (b < 0 || b > 63) fail(IGM_INVALID_ARGUMENT, std::string(who) + ": shift out of [0, 63]");
+}
+
+// Staging: a device view of a caller buffer (copy-in for host memory).
+template <class T>
+struct In {
+  const T* d = nullptr;
+  T* owned = nullptr;
+  In(const T* p, size_t count, cudaStream_t st, T* scratch = nullptr) {
+    if (!p) return;
+    if (is_device_ptr(p)) {
+      d = p;
+    } else {
+      T* dst = scratch ? scratch : (owned = dalloc<T>(count));
+      if (count) ck(cudaMemcpyAsync(dst, p, count * sizeof(T), cudaMemcpyHostToDevice, st), "H2D");
+      d = dst;
+    }
+  }
+  ~In() { dfree(owned); }
+  In(const In&) = delete;
+  In& operator=(const In&) = delete;
+};
+
+// An output: device pointer used directly, host pointer gets a D2H copy.
+template <class T>
+struct Out {
+  T* user;
+  T* d = nullptr;
+  T* owned = nullptr;
+  size_t count;
+  bool host;
+  Out(T* p, size_t cnt, T* scratch = nullptr) : user(p), count(cnt) {
+    host = !is_device_ptr(p);
+    if (!host) d = p;
+    else d = scratch ? scratch : (owned = dalloc<T>(cnt));
+  }
+  void fetch(cudaStream_t st) {
+    if (host && count) ck(cudaMemcpyAsync(user, d, count * sizeof(T), cudaMemcpyDeviceToHost, st), "D2H");
+  }
+  ~Out() { dfree(owned); }
+  Out(const Out&) = delete;
+  Out& operator=(const Out&) = delete;
+};
+
+// ----- trace bookkeeping ----------------------------------------------------
+
+const int kKernelOrder[] = {K_SPMV, K_PRECOND, K_DOT, K_AXPY, K_NORM, K_VEC_DIV,
+                            K_GIVENS, K_GIVENS_NORM, K_GIVENS_DIV, K_ROT};
+
+void trace_add(igm_trace* t, int kernel, int op, u64 count, int restart, int step) {
+  if (!t || count == 0) return;
+  t->total += count;
+  for (u64 i = 0; i < count && t->n_events < t->cap_events && t->events; ++i) {
+    int32_t* e = t->events + 4 * t->n_events;
+    e[0] = kernel; e[1] = op; e[2] = restart; e[3] = step;
+    t->n_events++;
+  }
+}
+
+void trace_shift(igm_trace* t, int kernel, int b1, int b2, long long times = 1) {
+  if (!t || !t->record_shifts || times <= 0) return;
+  for (long long i = 0; i < times; ++i) {
+    if (t->n_shifts < t->cap_shifts && t->shifts) {
+      int32_t* s = t->shifts + 3 * t->n_shifts;
+      s[0] = kernel; s[1] = b1; s[2] = b2;
+    } else if (t->n_shifts >= t->cap_shifts) {
+      t->n_shifts += times - i;
+      return;
+    }
+    t->n_shifts++;
+  }
+}
+
+// ----- host-side ILU schedule ------------------------------------------------
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+void build_tri(igm_ctx* c, DevTri& t, int n, const int* rp, const int* ci, const i64* vals,
+               const int* dpos, bool upper) {
+  // strip the diagonal and the structurally-void entries (a "lower" entry
+  // with j > i multiplies a zero-initialised slot in ilu.cpp:126-135, an
+  // "upper" one with j < i likewise), keep CSR order
+  std::vector<int> orp(n + 1, 0), oci;
+  std::vector<i64> ov, dg(n);
+  std::vector<u64> mg(n);
+  std::vector<int> info(n);
+  oci.reserve(rp[n]);
+  ov.reserve(rp[n]);
+  for (int i = 0; i < n; ++i) {
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+      const int j = ci[k];
+      if (j == i) continue;
+      if (j < 0 || j >= n) fail(IGM_INVALID_ARGUMENT, "upload_ilu: column index out of range");
+      if (upper ? (j < i) : (j > i)) continue;
+      oci.push_back(j);
+      ov.push_back(vals[k]);
+    }
+    orp[i + 1] = static_cast<int>(oci.size());
+    const int dp = dpos[i];
+    if (dp < 0 || dp >= rp[n]) fail(IGM_INVALID_ARGUMENT, "upload_ilu: diagonal position out of range");
+    const i64 d = vals[dp];
+    if (d == 0) fail(IGM_INVALID_ARGUMENT, "upload_ilu: zero diagonal entry");
+    dg[i] = d;
+    const SDivMagic gm = make_sdiv(d);
+    mg[i] = gm.u.m;
+    info[i] = gm.u.sh1 | (gm.u.sh2 << 1) | (gm.den_neg << 8) | (gm.den_is_m1 << 9);
+  }
+  // DAG levels
+  std::vector<int> lev(n, 0);
+  int maxlev = 0;
+  if (!upper) {
+    for (int i = 0; i < n; ++i) {
+      int l = 0;
+      for (int k = orp[i]; k < orp[i + 1]; ++k) l = std::max(l, lev[oci[k]] + 1);
+      lev[i] = l;
+      maxlev = std::max(maxlev, l);
+    }
+  } else {
+    for (int i = n - 1; i >= 0; --i) {
+      int l = 0;
+      for (int k = orp[i]; k < orp[i + 1]; ++k) l = std::max(l, lev[oci[k]] + 1);
+      lev[i] = l;
+      maxlev = std::max(maxlev, l);
+    }
+  }
+  // tiles: contiguous row blocks sized to fill the GPU, <= 16384 rows so a
+  // tile's values fit in shared memory (128 KB as int64)
+  const int nsm = num_sms(c->device);
+  int T = env_int("IGM_TRI_TILE", 0);
+  if (T <= 0) T = std::min(16384, std::max(32, (n + nsm - 1) / std::max(1, nsm)));
+  T = std::min(T, 16384);
+  if (n == 0) T = 1;
+  const int ntiles = n > 0 ? (n + T - 1) / T : 1;
+  // per tile: rows bucketed by level (stable), one segment per level
+  std::vector<int> tile_seg(ntiles + 1, 0), seg_level, sr{0}, perm(std::max(n, 1));
+  std::vector<std::pair<int, int>> buf;
+  for (int tl = 0; tl < ntiles && n > 0; ++tl) {
+    const int r0 = tl * T, r1 = std::min(n, r0 + T);
+    buf.clear();
+    for (int i = r0; i < r1; ++i) buf.emplace_back(lev[i], i);
+    std::sort(buf.begin(), buf.end());
+    for (size_t q = 0; q < buf.size(); ++q) {
+      if (q == 0 || buf[q].first != buf[q - 1].first) {
+        if (q) sr.push_back(static_cast<int>(r0 + q));
+        seg_level.push_back(buf[q].first);
+      }
+      perm[r0 + q] = buf[q].second;
+    }
+    sr.push_back(r1);
+    tile_seg[tl + 1] = static_cast<int>(seg_level.size());
+  }
+  if (seg_level.empty()) seg_level.push_back(0);
+
+  cudaStream_t st = c->stream;
+  t.n = n;
+  t.nnz_off = static_cast<int>(oci.size());
+  t.rp = dupload(orp.data(), orp.size(), st);
+  t.ci = dupload(oci.data(), oci.size(), st);
+  t.vals = dupload(ov.data(), ov.size(), st);
+  t.diag = dupload(dg.data(), dg.size(), st);
+  t.dmag = dupload(mg.data(), mg.size(), st);
+  t.dinfo = dupload(info.data(), info.size(), st);
+  t.tile_rows = T;
+  t.ntiles = ntiles;
+  t.nseg = static_cast<int>(seg_level.size());
+  t.nlevels = n > 0 ? maxlev + 1 : 0;
+  t.tile_seg = dupload(tile_seg.data(), tile_seg.size(), st);
+  t.seg_level = dupload(seg_level.data(), seg_level.size(), st);
+  t.seg_rows = dupload(sr.data(), sr.size(), st);
+  t.perm = dupload(perm.data(), perm.size(), st);
+  t.prog = dalloc<int>(ntiles);
+  t.ticket = dalloc<int>(1);
+  ck(cudaStreamSynchronize(st), "upload_ilu sync");
+}
+
+void free_tri(DevTri& t) {
+  dfree(t.rp); dfree(t.ci); dfree(t.vals); dfree(t.diag); dfree(t.dmag); dfree(t.dinfo);
+  dfree(t.tile_seg); dfree(t.seg_level); dfree(t.seg_rows); dfree(t.perm); dfree(t.prog);
+  dfree(t.ticket);
+  t = DevTri{};
+}
+
+// ----- the cycle -------------------------------------------------------------
+
+enum CycleMode { CM_RUN_CYCLE = 0, CM_SOLVE = 1 };
+
+struct CycleParams {
+  const DevSplit* m;
+  int M, f, s;
+  igm_shifts sh;
+  const DevIlu* pre;
+  bool checked;
+  bool collect_norms;
+};
+
+// Enqueue one cycle.  CM_SOLVE: r0 = (ws.r / gamma), x updated in ws.x.
+// CM_RUN_CYCLE: r0 = b - A x0 (x0 may be null), x_out = x0 + correction.
+void enqueue_cycle(igm_ctx* c, const CycleParams& p, CycleMode mode, const double* d_b,
+                   const double* d_x0, double* d_xout) {
+  Work& w = c->ws;
+  cudaStream_t st = c->stream;
+  const long long n = p.m->n;
+  const int M = p.M, f = p.f, ld = M + 1;
+  const ShiftsD sh = to_sd(p.sh);
+  Ctl* ctl = c->ctl;
+  ck(cudaMemsetAsync(w.small, 0, w.small_bytes, st), "memset small");
+  launch_cycle_init(st, ctl, w.g, f);
+  // ---- r0 in floating point (gmres_int.cpp:61-70)
+  const double* r0 = nullptr;
+  if (mode == CM_SOLVE) {
+    if (p.pre) {
+      const double* gbits = reinterpret_cast<const double*>(&ctl->rmax_bits);
+      launch_tri_fp(st, p.pre->lower, false, w.r, w.t1, ctl, gbits);
+      launch_tri_fp(st, p.pre->upper, true, w.t1, w.r0, ctl, nullptr);
+    } else {
+      launch_scale_div(st, n, w.r, w.r0, ctl);
+    }
+    r0 = w.r0;
+  } else {
+    const double* src = d_b;
+    if (d_x0) {
+      launch_spmv_fp_split(st, *p.m, p.s, d_x0, d_b, w.t1, ctl);
+      src = w.t1;
+    }
+    if (p.pre) {
+      launch_tri_fp(st, p.pre->lower, false, src, w.r, ctl, nullptr);
+      launch_tri_fp(st, p.pre->upper, true, w.r, w.r0, ctl, nullptr);
+      r0 = w.r0;
+    } else {
+      r0 = src;
+    }
+  }
+  launch_norm2_serial(st, n, r0, nullptr, ctl, 3);
+  launch_encode(st, n, r0, w.basis, f, ctl);
+  // ---- Arnoldi steps (gmres_int.cpp:90-160)
+  const size_t cstride = static_cast<size_t>(K_COUNT) * OP_COUNT;
+  for (int j = 0; j < M; ++j) {
+    u64* cstep = w.cnt + static_cast<size_t>(j) * cstride;
+    i64* vj = w.basis + static_cast<long long>(j) * n;
+    if (p.pre) {
+      launch_spmv_int(st, *p.m, p.s, vj, w.z, cstep + K_SPMV * OP_COUNT, ctl, p.checked);
+      launch_tri_int(st, p.pre->lower, false, w.z, w.vin, cstep + K_PRECOND * OP_COUNT, ctl, p.checked);
+      launch_tri_int(st, p.pre->upper, true, w.vin, w.w, cstep + K_PRECOND * OP_COUNT, ctl, p.checked);
+    } else {
+      launch_spmv_int(st, *p.m, p.s, vj, w.w, cstep + K_SPMV * OP_COUNT, ctl, p.checked);
+    }
+    u64* accj = w.acc + static_cast<size_t>(j) * (M + 1);
+    u64* absj = w.absacc + static_cast<size_t>(j) * (M + 1) * 2;
+    for (int i = 0; i <= j; ++i) {
+      const i64* vi = w.basis + static_cast<long long>(i) * n;
+      const i64* vp = i > 0 ? w.basis + static_cast<long long>(i - 1) * n : nullptr;
+      launch_mgs_pass(st, n, i == 0 ? 0 : 1, w.w, vp, vi, i > 0 ? accj + (i - 1) : nullptr,
+                      accj + i, absj + 2 * i, f, sh, cstep + K_AXPY * OP_COUNT,
+                      cstep + K_DOT * OP_COUNT, ctl, p.checked);
+    }
+    launch_mgs_pass(st, n, 2, w.w, vj, nullptr, accj + j, w.nacc + j, w.nabs + 2 * j, f, sh,
+                    cstep + K_AXPY * OP_COUNT, cstep + K_NORM * OP_COUNT, ctl, p.checked);
+    launch_step_scalar(st, j, f, sh, accj, absj, w.nacc + j, w.nabs + 2 * j, w.hess, ld, w.g, w.cs,
+                       w.sn, w.gabs, w.w, cstep, ctl, p.checked);
+    launch_vec_div(st, n, w.w, w.basis + static_cast<long long>(j + 1) * n, f, sh,
+                   cstep + K_VEC_DIV * OP_COUNT, ctl, p.checked);
+  }
+  // ---- least squares and update (gmres_int.cpp:163-180)
+  launch_cycle_finish(st, M, f, w.hess, w.g, w.y, w.wts, ctl);
+  if (mode == CM_SOLVE)
+    launch_xupdate(st, n, M, f, w.basis, w.wts, nullptr, w.x, ctl, 1);
+  else
+    launch_xupdate(st, n, M, f, w.basis, w.wts, d_x0, d_xout, ctl, 0);
+  if (p.collect_norms) launch_basis_norms(st, n, M + 1, f, w.basis, nullptr, w.bnorms, ctl);
+}
+
+// copy Ctl + small arrays back (async on the stream; caller syncs)
+void fetch_cycle_state(igm_ctx* c) {
+  ck(cudaMemcpyAsync(c->h_ctl, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream), "ctl D2H");
+  ck(cudaMemcpyAsync(c->ws.h_small, c->ws.small, c->ws.small_bytes, cudaMemcpyDeviceToHost, c->stream),
+     "small D2H");
+}
+
+// Fold one cycle's device counters into the trace; returns the cycle total.
+u64 account_cycle(igm_ctx* c, const CycleParams& p, igm_trace* t, int restart, long long n) {
+  const Work& w = c->ws;
+  const Ctl& h = *c->h_ctl;
+  const u64* cnt = hview<u64>(w, w.cnt);
+  u64 total = 0;
+  // how many Arnoldi steps ran (including a step that broke or failed)
+  int steps_run;
+  if (h.err && h.err_step >= -1) steps_run = h.err_step + 1;
+  else if (h.r0n == 0.0) steps_run = 0;
+  else if (!h.stop) steps_run = p.M;
+  else if (h.nbasis == h.dim) steps_run = h.dim;   // happy breakdown
+  else steps_run = std::min(p.M, h.dim + 1);       // t_mp == 0 break
+  const size_t cstride = static_cast<size_t>(K_COUNT) * OP_COUNT;
+  for (int j = 0; j < steps_run; ++j) {
+    for (int kk : kKernelOrder) {
+      for (int op = 1; op < OP_COUNT; ++op) {
+        const u64 v = cnt[j * cstride + kk * OP_COUNT + op];
+        if (v) {
+          total += v;
+          trace_add(t, kk, op, v, restart, j);
+        }
+      }
+    }
+  }
+  if (t) {
+    if (h.add_inexact) t->exact = 0;
+    // shift records, synthesised in the reference's call order
+    if (t->record_shifts) {
+      const auto& s = p.sh;
+      for (int j = 0; j < steps_run; ++j) {
+        for (int i = 0; i <= j; ++i) {
+          trace_shift(t, K_DOT, s.dot_b1, s.dot_b2);
+          trace_shift(t, K_AXPY, s.axpy_b1, 0);
+        }
+        trace_shift(t, K_NORM, s.norm_b1, s.norm_b1);
+        const bool last = (j == steps_run - 1);
+        const bool broke_tmp = last && h.stop && !h.err && h.dim == j;  // t_mp == 0
+        const bool vecdiv = !last || h.nbasis == j + 2;
+        if (vecdiv) trace_shift(t, K_VEC_DIV, s.div_b1, s.div_b2, n);
+        trace_shift(t, K_GIVENS, 0, s.givens_b2, 4LL * j);
+        trace_shift(t, K_GIVENS_NORM, s.norm_b1, s.norm_b1);
+        if (broke_tmp) break;
+        trace_shift(t, K_GIVENS_DIV, s.div_b1, s.div_b2, 2);
+        trace_shift(t, K_ROT, s.rot_b, s.rot_b, 2);
+      }
+    }
+  }
+  return total;
+}
+
+void raise_device_error(igm_ctx* c) {
+  const Ctl& h = *c->h_ctl;
+  if (h.err) fail(static_cast<igm_status>(h.err), em_text(h.err_msg));
+}
+
+igm_ctx* need_ctx(igm_ctx* c) {
+  if (!c) fail(IGM_INVALID_ARGUMENT, "null igm_ctx");
+  ck(cudaSetDevice(c->device), "cudaSetDevice");
+  return c;
+}
+
+void reset_ctl(igm_ctx* c) { ck(cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->stream), "ctl reset"); }
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* igm_last_error(void) { return t_err.c_str(); }
+const char* igm_version(void) { return "igm_b200 0.1 (sm_100a)"; }
+
+igm_status igm_ctx_create(int device, igm_ctx** out) {
+  return guarded([&] {
+    if (!out) fail(IGM_INVALID_ARGUMENT, "igm_ctx_create: null out");
+    int nd = 0;
+    ck(cudaGetDeviceCount(&nd), "cudaGetDeviceCount");
+    if (device < 0 || device >= nd) fail(IGM_INVALID_ARGUMENT, "igm_ctx_create: bad device index");
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    auto c = std::make_unique<igm_ctx>();
+    c->device = device;
+    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+    c->ctl = dalloc<Ctl>(1);
+    ck(cudaMallocHost(reinterpret_cast<void**>(&c->h_ctl), sizeof(Ctl)), "pinned ctl");
+    c->red = dalloc<u64>(3 + OP_COUNT);
+    ck(cudaMallocHost(reinterpret_cast<void**>(&c->h_red), sizeof(u64) * (3 + OP_COUNT)), "pinned red");
+    ck(cudaMemset(c->ctl, 0, sizeof(Ctl)), "memset ctl");
+    *out = c.release();
+  });
+}
+
+void igm_ctx_destroy(igm_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  ws_free(c->ws);
+  dfree(c->ctl);
+  dfree(c->red);
+  if (c->h_ctl) cudaFreeHost(c->h_ctl);
+  if (c->h_red) cudaFreeHost(c->h_red);
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+igm_status igm_ctx_synchronize(igm_ctx* c) {
+  return guarded([&] { ck(cudaStreamSynchronize(need_ctx(c)->stream), "sync"); });
+}
+
+void* igm_ctx_stream(igm_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+uint64_t igm_ctx_launch_count(igm_ctx*) { return g_launches; }
+
+// ---- uploads
+igm_status igm_upload_split(igm_ctx* c, int n, int nnz, const int* row_ptr, const int* col_idx,
+                            int ncomp, const int64_t* comp_vals, const int* alphas,
+                            igm_split** out) {
+  return guarded([&] {
+    need_ctx(c);
+    if (!out) fail(IGM_INVALID_ARGUMENT, "upload_split: null out");
+    if (n < 0 || nnz < 0 || ncomp < 1) fail(IGM_INVALID_ARGUMENT, "upload_split: bad sizes");
+    auto m = std::make_unique<igm_split>();
+    m->device = c->device;
+    m->n = n;
+    m->nnz = nnz;
+    m->ncomp = ncomp;
+    m->row_ptr = dupload(row_ptr, n + 1, c->stream);
+    m->col_idx = dupload(col_idx, nnz, c->stream);
+    m->vals = dupload(comp_vals, static_cast<size_t>(ncomp) * nnz, c->stream);
+    m->alphas = dupload(alphas, ncomp, c->stream);
+    m->h_alphas = is_device_ptr(alphas) ? to_host(alphas, ncomp) : std::vector<int>(alphas, alphas + ncomp);
+    ck(cudaStreamSynchronize(c->stream), "upload sync");
+    *out = m.release();
+  });
+}
+
+void igm_split_free(igm_split* m) {
+  if (!m) return;
+  cudaSetDevice(m->device);
+  dfree(m->row_ptr); dfree(m->col_idx); dfree(m->vals); dfree(m->alphas);
+  delete m;
+}
+
+igm_status igm_upload_csrf(igm_ctx* c, int n, const int* row_ptr, const int* col_idx,
+                           const double* vals, igm_csrf** out) {
+  return guarded([&] {
+    need_ctx(c);
+    if (!out) fail(IGM_INVALID_ARGUMENT, "upload_csrf: null out");
+    if (n < 0) fail(IGM_INVALID_ARGUMENT, "upload_csrf: bad size");
+    int nnz = 0;
+    ck(cudaMemcpy(&nnz, row_ptr + n, sizeof(int), cudaMemcpyDefault), "nnz");
+    auto a = std::make_unique<igm_csrf>();
+    a->device = c->device;
+    a->n = n;
+    a->nnz = nnz;
+    a->row_ptr = dupload(row_ptr, n + 1, c->stream);
+    a->col_idx = dupload(col_idx, nnz, c->stream);
+    a->vals = dupload(vals, nnz, c->stream);
+    ck(cudaStreamSynchronize(c->stream), "upload sync");
+    *out = a.release();
+  });
+}
+
+void igm_csrf_free(igm_csrf* a) {
+  if (!a) return;
+  cudaSetDevice(a->device);
+  dfree(a->row_ptr); dfree(a->col_idx); dfree(a->vals);
+  delete a;
+}
+
+igm_status igm_upload_ilu(igm_ctx* c, int n, const int* lrp, const int* lci, const int64_t* lv,
+                          const int* ldp, const int* urp, const int* uci, const int64_t* uv,
+                          const int* udp, igm_ilu** out) {
+  return guarded([&] {
+    need_ctx(c);
+    if (!out) fail(IGM_INVALID_ARGUMENT, "upload_ilu: null out");
+    if (n < 0) fail(IGM_INVALID_ARGUMENT, "upload_ilu: bad size");
+    auto hv = [](const auto* p, size_t cnt) {
+      using T = std::remove_const_t<std::remove_pointer_t<decltype(p)>>;
+      return is_device_ptr(p) ? to_host(p, cnt) : std::vector<T>(p, p + cnt);
+    };
+    const std::vector<int> Lrp = hv(lrp, n + 1), Urp = hv(urp, n + 1);
+    const std::vector<int> Lci = hv(lci, Lrp[n]), Uci = hv(uci, Urp[n]);
+    const std::vector<i64> Lv = hv(lv, Lrp[n]), Uv = hv(uv, Urp[n]);
+    const std::vector<int> Ldp = hv(ldp, n), Udp = hv(udp, n);
+    auto f = std::make_unique<igm_ilu>();
+    f->device = c->device;
+    f->n = n;
+    build_tri(c, f->lower, n, Lrp.data(), Lci.data(), Lv.data(), Ldp.data(), false);
+    build_tri(c, f->upper, n, Urp.data(), Uci.data(), Uv.data(), Udp.data(), true);
+    *out = f.release();
+  });
+}
+
+void igm_ilu_free(igm_ilu* f) {
+  if (!f) return;
+  cudaSetDevice(f->device);
+  free_tri(f->lower);
+  free_tri(f->upper);
+  delete f;
+}
+
+int igm_ilu_levels(const igm_ilu* f, int backward) {
+  return f ? (backward ? f->upper.nlevels : f->lower.nlevels) : 0;
+}
+
+// ---- primitives
+igm_status igm_spmv(igm_ctx* c, const igm_split* m, int s, const int64_t* v, int64_t* out,
+                    igm_trace* t) {
+  return guarded([&] {
+    need_ctx(c);
+    if (s < 0 || s > m->ncomp - 1) fail(IGM_INVALID_ARGUMENT, "spmv: component index out of range");
+    const bool chk = t && t->checked;
+    In<i64> dv(v, m->n, c->stream);
+    Out<i64> dout(out, m->n);
+    ck(cudaMemsetAsync(c->red, 0, sizeof(u64) * (3 + OP_COUNT), c->stream), "memset");
+    reset_ctl(c);
+    launch_spmv_int(c->stream, *m, s, dv.d, dout.d, c->red + 3, c->ctl, chk);
+    dout.fetch(c->stream);
+    ck(cudaMemcpyAsync(c->h_red, c->red, sizeof(u64) * (3 + OP_COUNT), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    if (chk) {
+      trace_add(t, t->kernel, OP_MUL, c->h_red[3 + OP_MUL], t->restart, t->step);
+      trace_add(t, t->kernel, OP_ADD, c->h_red[3 + OP_ADD], t->restart, t->step);
+    }
+  });
+}
+
+igm_status igm_apply_inverse(igm_ctx* c, const igm_ilu* f, const int64_t* y, int64_t* out,
+                             igm_trace* t) {
+  return guarded([&] {
+    need_ctx(c);
+    const bool chk = t && t->checked;
+    ws_ensure(c, f->n, 1);
+    In<i64> dy(y, f->n, c->stream);
+    Out<i64> dout(out, f->n);
+    ck(cudaMemsetAsync(c->red, 0, sizeof(u64) * (3 + OP_COUNT), c->stream), "memset");
+    reset_ctl(c);
+    launch_tri_int(c->stream, f->lower, false, dy.d, c->ws.z, c->red + 3, c->ctl, chk);
+    launch_tri_int(c->stream, f->upper, true, c->ws.z, dout.d, c->red + 3, c->ctl, chk);
+    dout.fetch(c->stream);
+    ck(cudaMemcpyAsync(c->h_red, c->red, sizeof(u64) * (3 + OP_COUNT), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    if (chk)
+      for (int op : {OP_MUL, OP_SUB, OP_DIV}) trace_add(t, t->kernel, op, c->h_red[3 + op], t->restart, t->step);
+  });
+}
+
+igm_status igm_apply_inverse_fp(igm_ctx* c, const igm_ilu* f, const double* y, double* out) {
+  return guarded([&] {
+    need_ctx(c);
+    ws_ensure(c, f->n, 1);
+    In<double> dy(y, f->n, c->stream);
+    Out<double> dout(out, f->n);
+    reset_ctl(c);
+    launch_tri_fp(c->stream, f->lower, false, dy.d, c->ws.t1, c->ctl, nullptr);
+    launch_tri_fp(c->stream, f->upper, true, c->ws.t1, dout.d, c->ctl, nullptr);
+    dout.fetch(c->stream);
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+static void fx_red_common(igm_ctx* c, long long n, int mode, const int64_t* v, const int64_t* w,
+                          int b1, int b2, bool chk) {
+  In<i64> dv(v, n, c->stream);
+  In<i64> dw(mode == 0 ? w : nullptr, n, c->stream);
+  ck(cudaMemsetAsync(c->red, 0, sizeof(u64) * (3 + OP_COUNT), c->stream), "memset");
+  if (n > 0) launch_fx_red(c->stream, n, mode, dv.d, dw.d, b1, b2, c->red, c->red + 1, c->red + 3, chk);
+  ck(cudaMemcpyAsync(c->h_red, c->red, sizeof(u64) * (3 + OP_COUNT), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+}
+
+static bool abs_small_h(const u64* ab) {
+  const unsigned __int128 s = (static_cast<unsigned __int128>(ab[0]) << 32) + ab[1];
+  return s < (static_cast<unsigned __int128>(1) << 63);
+}
+
+igm_status igm_fx_dot(igm_ctx* c, int64_t n, const int64_t* v, const int64_t* w, int f, int b1,
+                      int b2, int64_t* out, igm_trace* t) {
+  return guarded([&] {
+    need_ctx(c);
+    check_shift(b1, "fx_dot");
+    check_shift(b2, "fx_dot");
+    if (t) trace_shift(t, t->kernel, b1, b2);
+    const bool chk = t && t->checked;
+    fx_red_common(c, n, 0, v, w, b1, b2, chk);
+    const i64 acc = static_cast<i64>(c->h_red[0]);
+    if (chk) {
+      trace_add(t, t->kernel, OP_MUL, c->h_red[3 + OP_MUL], t->restart, t->step);
+      if (!abs_small_h(c->h_red + 1)) t->exact = 0;
+    }
+    const int e = f - b1 - b2;
+    if (e >= 0) {
+      *out = asr(acc, e);
+    } else {
+      if (chk && shl_ovf(acc, -e)) trace_add(t, t->kernel, OP_SHL, 1, t->restart, t->step);
+      *out = wrap_shl(acc, -e);
+    }
+  });
+}
+
+igm_status igm_fx_norm(igm_ctx* c, int64_t n, const int64_t* v, int f, int b1, int64_t* out,
+                       igm_trace* t) {
+  return guarded([&] {
+    need_ctx(c);
+    check_shift(b1, "fx_norm");
+    const int acc_frac = 2 * (f - b1);
+    if (acc_frac < 0 || acc_frac > 62)
+      fail(IGM_INVALID_ARGUMENT,
+           "fx_norm: accumulator format not representable (need 2*(f-b1) in [0, 62])");
+    if (t) trace_shift(t, t->kernel, b1, b1);
+    const bool chk = t && t->checked;
+    fx_red_common(c, n, 1, v, nullptr, b1, b1, chk);
+    const i64 acc = static_cast<i64>(c->h_red[0]);
+    if (chk) {
+      const u64 nmul = c->h_red[3 + OP_MUL];
+      trace_add(t, t->kernel, OP_MUL, nmul, t->restart, t->step);
+      if (nmul == 0) {
+        const unsigned __int128 s = (static_cast<unsigned __int128>(c->h_red[1]) << 32) + c->h_red[2];
+        const u64 wraps = static_cast<u64>((s + (static_cast<unsigned __int128>(1) << 63)) >> 64);
+        trace_add(t, t->kernel, OP_ADD, wraps, t->restart, t->step);
+      } else if (!abs_small_h(c->h_red + 1)) {
+        t->exact = 0;
+      }
+    }
+    if (acc < 0) fail(IGM_DOMAIN_ERROR, "fx_norm: accumulator wrapped negative");
+    const i64 r = static_cast<i64>(isqrt_u64(static_cast<u64>(acc)));
+    const int e = f - acc_frac / 2;
+    if (e >= 0) {
+      if (chk && shl_ovf(r, e)) trace_add(t, t->kernel, OP_SHL, 1, t->restart, t->step);
+      *out = wrap_shl(r, e);
+    } else {
+      *out = asr(r, -e);
+    }
+  });
+}
+
+igm_status igm_fx_axpy_sub(igm_ctx* c, int64_t n, int64_t* w, int64_t h, const int64_t* v, int f,
+                           int b1, igm_trace* t) {
+  return guarded([&] {
+    need_ctx(c);
+    check_shift(b1, "fx_axpy_sub");
+    if (f - b1 < 0) fail(IGM_INVALID_ARGUMENT, "fx_axpy_sub: b1 exceeds frac_bits");
+    if (t) trace_shift(t, t->kernel, b1, 0);
+    const bool chk = t && t->checked;
+    In<i64> dv(v, n, c->stream);
+    const bool wdev = is_device_ptr(w);
+    i64* dw = w;
+    i64* owned = nullptr;
+    if (!wdev) {
+      owned = dalloc<i64>(n);
+      dw = owned;
+      ck(cudaMemcpyAsync(dw, w, sizeof(i64) * n, cudaMemcpyHostToDevice, c->stream), "H2D");
+    }
+    ck(cudaMemsetAsync(c->red, 0, sizeof(u64) * (3 + OP_COUNT), c->stream), "memset");
+    if (n > 0) launch_axpy_only(c->stream, n, dw, h, dv.d, f, b1, c->red + 3, chk);
+    if (!wdev) ck(cudaMemcpyAsync(w, dw, sizeof(i64) * n, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaMemcpyAsync(c->h_red, c->red, sizeof(u64) * (3 + OP_COUNT), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    dfree(owned);
+    if (chk) {
+      trace_add(t, t->kernel, OP_MUL, c->h_red[3 + OP_MUL], t->restart, t->step);
+      trace_add(t, t->kernel, OP_SUB, c->h_red[3 + OP_SUB], t->restart, t->step);
+    }
+  });
+}
+
+igm_status igm_spmv_fp(igm_ctx* c, const igm_csrf* a, const double* x, double* y) {
+  return guarded([&] {
+    need_ctx(c);
+    In<double> dx(x, a->n, c->stream);
+    Out<double> dy(y, a->n);
+    launch_residual(c->stream, *a, dx.d, nullptr, dy.d, c->ctl, false);
+    dy.fetch(c->stream);
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+igm_status igm_residual_fp(igm_ctx* c, const igm_csrf* a, const double* x, const double* b,
+                           double* r, double* relnorm) {
+  return guarded([&] {
+    need_ctx(c);
+    In<double> dx(x, a->n, c->stream);
+    In<double> db(b, a->n, c->stream);
+    Out<double> dr(r, a->n);
+    reset_ctl(c);
+    launch_residual(c->stream, *a, dx.d, db.d, dr.d, c->ctl, false);
+    launch_norm2_serial(c->stream, a->n, db.d, nullptr, c->ctl, 1);
+    launch_norm2_serial(c->stream, a->n, dr.d, nullptr, c->ctl, 2);
+    dr.fetch(c->stream);
+    ck(cudaMemcpyAsync(c->h_ctl, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    if (relnorm) *relnorm = c->h_ctl->relnorm;
+  });
+}
+
+igm_status igm_spmv_fp_split(igm_ctx* c, const igm_split* m, int s, const double* x, double* y) {
+  return guarded([&] {
+    need_ctx(c);
+    if (s < 0 || s > m->ncomp - 1) fail(IGM_INVALID_ARGUMENT, "spmv_fp: component index out of range");
+    In<double> dx(x, m->n, c->stream);
+    Out<double> dy(y, m->n);
+    reset_ctl(c);
+    launch_spmv_fp_split(c->stream, *m, s, dx.d, nullptr, dy.d, c->ctl);
+    dy.fetch(c->stream);
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+igm_status igm_norm2(igm_ctx* c, int64_t n, const double* v, double* out) {
+  return guarded([&] {
+    need_ctx(c);
+    In<double> dv(v, n, c->stream);
+    double* d = dalloc<double>(1);
+    launch_norm2_serial(c->stream, n, dv.d, d, c->ctl, 0);
+    ck(cudaMemcpyAsync(c->h_red, d, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    std::memcpy(out, c->h_red, sizeof(double));
+    dfree(d);
+  });
+}
+
+igm_status igm_gamma_scale(igm_ctx* c, int64_t n, const double* r, double* gamma, double* b_k) {
+  return guarded([&] {
+    need_ctx(c);
+    In<double> dr(r, n, c->stream);
+    Out<double> db(b_k, n);
+    reset_ctl(c);
+    if (n > 0) launch_gamma(c->stream, n, dr.d, c->ctl);
+    ck(cudaMemcpyAsync(c->h_ctl, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    u64 bits = c->h_ctl->rmax_bits;
+    double g;
+    std::memcpy(&g, &bits, sizeof g);
+    if (g == 0.0) fail(IGM_INVALID_ARGUMENT, "gamma_scale: zero residual");
+    if (n > 0) launch_scale_div(c->stream, n, dr.d, db.d, c->ctl);
+    db.fetch(c->stream);
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    *gamma = g;
+  });
+}
+
+// ---- run_cycle
+igm_status igm_run_cycle(igm_ctx* c, const igm_split* m, const igm_cycle_cfg* cfg,
+                         const double* b, const double* x0, double* x_out, igm_cycle_out* out,
+                         igm_trace* t) {
+  igm_status st = guarded([&] {
+    need_ctx(c);
+    if (!cfg || !m) fail(IGM_INVALID_ARGUMENT, "run_cycle: null argument");
+    if (cfg->m < 1) fail(IGM_INVALID_ARGUMENT, "run_cycle: m must be >= 1");
+    if (cfg->s < 0 || cfg->s > m->ncomp - 1)
+      fail(IGM_INVALID_ARGUMENT, "run_cycle: splitting depth out of range");
+    check_qformat(cfg->frac_bits);
+    validate_shifts(cfg->shifts, cfg->frac_bits);
+    if (cfg->precond && cfg->precond->n != m->n) fail(IGM_INVALID_ARGUMENT, "run_cycle: dimension mismatch");
+    const long long n = m->n;
+    ws_ensure(c, n, cfg->m);
+    Work& w = c->ws;
+    In<double> db(b, n, c->stream, w.b);
+    // x0 all-zero => skip spmv_fp exactly like gmres_int.cpp:63-68
+    const double* dx0 = nullptr;
+    std::unique_ptr<In<double>> dx0h;
+    if (x0) {
+      bool nonzero = true;
+      if (!is_device_ptr(x0)) {
+        nonzero = false;
+        for (long long i = 0; i < n; ++i) nonzero = nonzero || x0[i] != 0.0;
+      }
+      if (nonzero) {
+        dx0h = std::make_unique<In<double>>(x0, n, c->stream, w.x0);
+        dx0 = dx0h->d;
+      }
+    }
+    Out<double> dx(x_out, n, w.x);
+    CycleParams p{m, cfg->m, cfg->frac_bits, cfg->s, cfg->shifts, cfg->precond, t && t->checked,
+                  cfg->collect_basis_norms != 0};
+    reset_ctl(c);
+    if (t) t->exact = 1;
+    enqueue_cycle(c, p, CM_RUN_CYCLE, db.d, dx0, dx.d);
+    fetch_cycle_state(c);
+    ck(cudaStreamSynchronize(c->stream), "cycle sync");
+    const Ctl& h = *c->h_ctl;
+    account_cycle(c, p, t, t ? t->restart : 0, n);
+    raise_device_error(c);
+    dx.fetch(c->stream);
+    const int M = cfg->m;
+    if (out) {
+      out->dim = h.dim;
+      out->r0_norm = h.r0n;
+      const double sc = std::ldexp(1.0, -cfg->frac_bits);
+      const i64* gabs = hview<i64>(w, w.gabs);
+      const i64* cs = hview<i64>(w, w.cs);
+      const i64* sn = hview<i64>(w, w.sn);
+      for (int j = 0; j < h.dim; ++j) {
+        if (out->g_abs) out->g_abs[j] = std::fabs(static_cast<double>(gabs[j]) * sc);
+        if (out->cos_d) out->cos_d[j] = static_cast<double>(cs[j]) * sc;
+        if (out->sin_d) out->sin_d[j] = static_cast<double>(sn[j]) * sc;
+      }
+      const int nb = h.r0n == 0.0 ? 0 : h.nbasis;
+      out->n_basis = nb;
+      out->n_basis_norms = (cfg->collect_basis_norms && h.r0n != 0.0) ? nb : 0;
+      if (out->basis_norms && out->n_basis_norms) {
+        const double* bn = hview<double>(w, w.bnorms);
+        for (int k = 0; k < nb; ++k) out->basis_norms[k] = bn[k];
+      }
+      if (out->basis && nb)
+        ck(cudaMemcpyAsync(out->basis, w.basis, sizeof(i64) * n * nb, cudaMemcpyDefault, c->stream), "basis D2H");
+      if (out->hess) std::memcpy(out->hess, hview<i64>(w, w.hess), sizeof(i64) * (M + 1) * M);
+      if (out->g) std::memcpy(out->g, hview<i64>(w, w.g), sizeof(i64) * (M + 1));
+      if (out->cos_raw) std::memcpy(out->cos_raw, cs, sizeof(i64) * M);
+      if (out->sin_raw) std::memcpy(out->sin_raw, sn, sizeof(i64) * M);
+      if (h.r0n == 0.0) {  // early return: no state was built (gmres_int.cpp:72-73)
+        if (out->g) std::memset(out->g, 0, sizeof(i64) * (M + 1));
+      }
+    }
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+  return st;
+}
+
+// ---- solve
+igm_status igm_solve(igm_ctx* c, const igm_split* m, const igm_csrf* a_fp, const double* b,
+                     const igm_refine_cfg* cfg, const igm_ilu* precond, double* x_out,
+                     igm_report* rep, igm_trace* ext) {
+  return guarded([&] {
+    need_ctx(c);
+    if (!cfg || !m || !a_fp || !rep) fail(IGM_INVALID_ARGUMENT, "solve: null argument");
+    if (a_fp->n != m->n) fail(IGM_INVALID_ARGUMENT, "solve: dimension mismatch");
+    if (cfg->max_refinements < 0) fail(IGM_INVALID_ARGUMENT, "solve: max_refinements must be >= 0");
+    const auto t0 = std::chrono::steady_clock::now();
+    const long long n = m->n;
+    const int M = std::max(cfg->m, 1);
+    ws_ensure(c, n, M);
+    Work& w = c->ws;
+    cudaStream_t st = c->stream;
+    const bool checked = ext ? ext->checked != 0 : cfg->checked != 0;
+    igm_trace own{};
+    own.checked = checked;
+    igm_trace* t = ext ? ext : &own;
+    t->exact = 1;
+    rep->converged = 0;
+    rep->refinements = 0;
+    rep->total_inner_iterations = 0;
+    rep->n_relres = 0;
+    rep->overflow_total = 0;
+    rep->overflow_exact = 1;
+
+    In<double> db(b, n, st, w.b);
+    ck(cudaMemsetAsync(w.x, 0, sizeof(double) * n, st), "x=0");
+    reset_ctl(c);
+    launch_norm2_serial(st, n, db.d, nullptr, c->ctl, 1);  // ||b||
+    launch_residual(st, *a_fp, w.x, db.d, w.r, c->ctl, true);
+    launch_norm2_serial(st, n, w.r, nullptr, c->ctl, 2);
+    ck(cudaMemcpyAsync(c->h_ctl, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st), "ctl");
+    ck(cudaStreamSynchronize(st), "sync");
+    double relnorm = c->h_ctl->relnorm;
+    rep->relres_history[rep->n_relres++] = relnorm;
+
+    for (int k = 0; k < cfg->max_refinements && relnorm >= cfg->tol; ++k) {
+      const u64 rbits = c->h_ctl->rmax_bits;
+      double rmax;
+      std::memcpy(&rmax, &rbits, sizeof rmax);
+      if (rmax == 0.0) break;
+      t->restart = k;
+      const u64 before = t->total;
+      const int depth = cfg->s_schedule_fn ? cfg->s_schedule_fn(cfg->s_schedule_user, k)
+                        : cfg->s_schedule  ? cfg->s_schedule[k]
+                                           : cfg->s;
+      // run_cycle validation (gmres_int.cpp:47-52)
+      if (cfg->m < 1) fail(IGM_INVALID_ARGUMENT, "run_cycle: m must be >= 1");
+      if (depth < 0 || depth > m->ncomp - 1) fail(IGM_INVALID_ARGUMENT, "run_cycle: splitting depth out of range");
+      check_qformat(cfg->frac_bits);
+      validate_shifts(cfg->shifts, cfg->frac_bits);
+      CycleParams p{m, cfg->m, cfg->frac_bits, depth, cfg->shifts, precond, checked, false};
+      enqueue_cycle(c, p, CM_SOLVE, nullptr, nullptr, nullptr);
+      // next residual (the x update is skipped on device when dim == 0)
+      fetch_cycle_state(c);  // ctl snapshot incl. gamma, before the reset below
+      ck(cudaStreamSynchronize(st), "cycle sync");
+      const Ctl hc = *c->h_ctl;
+      account_cycle(c, p, t, k, n);
+      if (hc.add_inexact) rep->overflow_exact = 0;
+      raise_device_error(c);
+      const int dim = hc.dim;
+      if (dim == 0) break;
+      ck(cudaMemsetAsync(&c->ctl->rmax_bits, 0, sizeof(u64), st), "rmax reset");
+      launch_residual(st, *a_fp, w.x, db.d, w.r, c->ctl, true);
+      launch_norm2_serial(st, n, w.r, nullptr, c->ctl, 2);
+      ck(cudaMemcpyAsync(c->h_ctl, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st), "ctl");
+      ck(cudaStreamSynchronize(st), "sync");
+      rep->refinements = k + 1;
+      rep->total_inner_iterations += dim;
+      rep->inner_dims[k] = dim;
+      rep->gamma_history[k] = rmax;
+      rep->overflow_per_restart[k] = t->total - before;
+      relnorm = c->h_ctl->relnorm;
+      rep->relres_history[rep->n_relres++] = relnorm;
+    }
+    rep->converged = relnorm < cfg->tol;
+    rep->overflow_total = t->total;
+    if (!t->exact) rep->overflow_exact = 0;
+    if (x_out) {
+      if (is_device_ptr(x_out))
+        ck(cudaMemcpyAsync(x_out, w.x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "x");
+      else
+        ck(cudaMemcpyAsync(x_out, w.x, sizeof(double) * n, cudaMemcpyDeviceToHost, st), "x");
+    }
+    ck(cudaStreamSynchronize(st), "sync");
+    rep->wall_time_sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+// ---- config-5 microbench: SpMV + MGS against k basis vectors, unchecked
+igm_status igm_spmv_mgs(igm_ctx* c, const igm_split* m, int s, const int64_t* v_in,
+                        const int64_t* basis, int k, int f, int dot_b1, int dot_b2, int axpy_b1,
+                        int64_t* w, int64_t* h_out) {
+  return guarded([&] {
+    need_ctx(c);
+    if (k < 1) fail(IGM_INVALID_ARGUMENT, "spmv_mgs: k must be >= 1");
+    if (!is_device_ptr(v_in) || !is_device_ptr(basis) || !is_device_ptr(w))
+      fail(IGM_INVALID_ARGUMENT, "spmv_mgs: v_in, basis and w must be device memory");
+    cudaStream_t st = c->stream;
+    const long long n = m->n;
+    ws_ensure(c, 1, k);
+    ShiftsD sh{dot_b1, dot_b2, axpy_b1, 0, 0, 0, 0, 0};
+    ck(cudaMemsetAsync(c->ws.acc, 0, sizeof(u64) * (k + 1), st), "memset");
+    reset_ctl(c);
+    launch_spmv_int(st, *m, s, v_in, w, nullptr, c->ctl, false);
+    for (int i = 0; i < k; ++i) {
+      const i64* vi = basis + static_cast<long long>(i) * n;
+      const i64* vp = i > 0 ? basis + static_cast<long long>(i - 1) * n : nullptr;
+      launch_mgs_pass(st, n, i == 0 ? 0 : 1, w, vp, vi, i > 0 ? c->ws.acc + i - 1 : nullptr,
+                      c->ws.acc + i, nullptr, f, sh, nullptr, nullptr, c->ctl, false);
+    }
+    launch_mgs_pass(st, n, 3, w, basis + static_cast<long long>(k - 1) * n, nullptr,
+                    c->ws.acc + k - 1, nullptr, nullptr, f, sh, nullptr, nullptr, c->ctl, false);
+    if (h_out) {
+      std::vector<u64> acc(k);
+      ck(cudaMemcpyAsync(acc.data(), c->ws.acc, sizeof(u64) * k, cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaStreamSynchronize(st), "sync");
+      const int e = f - dot_b1 - dot_b2;
+      for (int i = 0; i < k; ++i) {
+        const i64 a = static_cast<i64>(acc[i]);
+        h_out[i] = e >= 0 ? asr(a, e) : wrap_shl(a, -e);
+      }
+    }
+  });
+}
+
+}  // extern "C"

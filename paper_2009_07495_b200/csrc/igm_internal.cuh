@@ -1,0 +1,167 @@
+// igm_internal.cuh -- device-side data layout of the B200 int-GMRES path.
+//
+// HBM layout:
+//   * SplitMatrix: one CSR pattern (int32 row_ptr/col_idx) shared by all
+//     components; int64 values component-major (comp l at vals + l*nnz).
+//   * CsrMatrixF: int32 pattern (aliased to the split's when identical) +
+//     FP64 values.
+//   * IluFactors: per factor the STRICT off-diagonal CSR in natural row order,
+//     the raw diagonal, per-row exact reciprocals of the diagonal, and the
+//     wavefront schedule (rows grouped into contiguous tiles, each tile's rows
+//     bucketed by DAG level).
+//   * Krylov basis: (m+1) contiguous int64 vectors of n words.
+#pragma once
+
+#include "fx_core.cuh"
+#include "../../include/igm.h"
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace igm {
+
+// Device error-message ids (mapped to the reference's exception texts).
+enum ErrMsg {
+  EM_NONE = 0,
+  EM_NORM_NEG = 1,     // "fx_norm: accumulator wrapped negative"
+  EM_DIV_ZERO = 2,     // "fx_div: shifted divisor is zero"
+  EM_ENCODE = 3,       // "encode: value outside representable range"
+  EM_HESS_ZERO = 4,    // "solve_hessenberg: zero diagonal"
+  EM_GAMMA_ZERO = 5,   // "gamma_scale: zero residual"
+};
+
+// Per-context control block in device memory.  Written by single-thread
+// kernels, read by every kernel of a cycle to early-exit after a break or
+// an error (so a whole cycle can be enqueued without host round trips).
+struct Ctl {
+  int err;        // igm_status of the first error
+  int err_msg;    // ErrMsg
+  int err_step;
+  int stop;       // cycle ended (t_mp == 0, happy breakdown, r0 == 0)
+  int dim;
+  int nbasis;
+  int do_vecdiv;  // the current step produces v_{j+1}
+  int add_inexact;
+  i64 hnext;
+  u64 div_m;      // SDivMagic of the current vec_div divisor
+  int div_sh1, div_sh2, div_neg, div_m1;
+  double r0n;
+  // refinement state
+  u64 rmax_bits;  // max |r_i| as IEEE bits (non-negative doubles order as u64)
+  double nb, nr, relnorm;
+  double scalar;  // scratch result of norm2 kernels
+};
+
+struct DevSplit {
+  int n = 0, nnz = 0, ncomp = 0;
+  int* row_ptr = nullptr;
+  int* col_idx = nullptr;
+  i64* vals = nullptr;   // ncomp * nnz
+  int* alphas = nullptr; // ncomp (device)
+  std::vector<int> h_alphas;
+  std::vector<int> h_row_ptr_hash;  // not used for identity, kept small
+  int device = 0;
+};
+
+struct DevCsrf {
+  int n = 0, nnz = 0;
+  int* row_ptr = nullptr;
+  int* col_idx = nullptr;
+  double* vals = nullptr;
+  int device = 0;
+};
+
+// One triangular factor prepared for the wavefront kernels.
+struct DevTri {
+  int n = 0, nnz_off = 0;
+  int* rp = nullptr;       // n+1, off-diagonal entries only
+  int* ci = nullptr;
+  i64* vals = nullptr;
+  i64* diag = nullptr;     // n raw diagonal
+  u64* dmag = nullptr;     // n round-up reciprocals of |diag|
+  int* dinfo = nullptr;    // n: sh1 | sh2 << 1 | neg << 8 | (diag == -1) << 9
+  // schedule
+  int tile_rows = 0, ntiles = 0, nseg = 0, nlevels = 0;
+  int* tile_seg = nullptr; // ntiles+1
+  int* seg_level = nullptr;// nseg
+  int* seg_rows = nullptr; // nseg+1 into perm
+  int* perm = nullptr;     // n
+  int* prog = nullptr;     // ntiles progress words
+  int* ticket = nullptr;   // 1
+};
+
+struct DevIlu {
+  int n = 0;
+  DevTri lower, upper;
+  int device = 0;
+};
+
+}  // namespace igm
+
+struct igm_split : igm::DevSplit {};
+struct igm_csrf : igm::DevCsrf {};
+struct igm_ilu : igm::DevIlu {};
+
+namespace igm {
+
+struct KParams;  // fwd
+
+// --- kernel launchers (kernels.cu) -----------------------------------------
+struct ShiftsD {
+  int dot_b1, dot_b2, axpy_b1, norm_b1, div_b1, div_b2, givens_b2, rot_b;
+};
+
+void launch_spmv_int(cudaStream_t st, const DevSplit& m, int s, const i64* v,
+                     i64* out, u64* cnt, const Ctl* ctl, bool checked);
+void launch_spmv_fp_split(cudaStream_t st, const DevSplit& m, int s,
+                          const double* x, const double* b, double* y,
+                          const Ctl* ctl);
+void launch_residual(cudaStream_t st, const DevCsrf& a, const double* x,
+                     const double* b, double* r, Ctl* ctl, bool track_max);
+void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward,
+                    const i64* y, i64* out, u64* cnt, const Ctl* ctl,
+                    bool checked);
+void launch_tri_fp(cudaStream_t st, const DevTri& t, bool backward,
+                   const double* y, double* out, const Ctl* ctl,
+                   const double* prescale /* divide y by *prescale or null */);
+void launch_norm2_serial(cudaStream_t st, long long n, const double* v,
+                         double* out, Ctl* ctl, int mode);
+void launch_mgs_pass(cudaStream_t st, long long n, int mode, i64* w,
+                     const i64* vprev, const i64* vcur, const u64* hacc,
+                     u64* acc_out, u64* abs_out, int f, ShiftsD sh,
+                     u64* cnt_axpy, u64* cnt_red, const Ctl* ctl,
+                     bool checked);
+void launch_vec_div(cudaStream_t st, long long n, const i64* w, i64* out,
+                    int f, ShiftsD sh, u64* cnt, const Ctl* ctl,
+                    bool checked);
+void launch_step_scalar(cudaStream_t st, int j, int f, ShiftsD sh,
+                        const u64* acc_col, const u64* abs_col, const u64* nacc,
+                        const u64* nabs, i64* hess, int ld, i64* g, i64* cs,
+                        i64* sn, i64* gabs, const i64* w, u64* cnt_step,
+                        Ctl* ctl, bool checked);
+void launch_cycle_init(cudaStream_t st, Ctl* ctl, i64* g, int f);
+void launch_encode(cudaStream_t st, long long n, const double* r0, i64* v0,
+                   int f, Ctl* ctl);
+void launch_cycle_finish(cudaStream_t st, int m, int f, const i64* hess,
+                         const i64* g, double* y, double* wts, Ctl* ctl);
+void launch_xupdate(cudaStream_t st, long long n, int m, int f,
+                    const i64* basis, const double* wts, const double* x0,
+                    double* x, const Ctl* ctl, int mode);
+void launch_scale_div(cudaStream_t st, long long n, const double* r,
+                      double* out, const Ctl* ctl);
+void launch_fx_red(cudaStream_t st, long long n, int mode, const i64* v,
+                   const i64* w, int b1, int b2, u64* acc, u64* abs_out,
+                   u64* cnt, bool checked);
+void launch_axpy_only(cudaStream_t st, long long n, i64* w, i64 h,
+                      const i64* v, int f, int b1, u64* cnt, bool checked);
+void launch_gamma(cudaStream_t st, long long n, const double* r, Ctl* ctl);
+void launch_basis_norms(cudaStream_t st, long long n, int nb, int f,
+                        const i64* basis, double* tmp, double* out, Ctl* ctl);
+
+int num_sms(int device);
+extern unsigned long long g_launches;  // kernels launched by this library
+
+}  // namespace igm

@@ -1,0 +1,1062 @@
+// kernels.cu -- sm_100a kernels of the int-GMRES hot path.
+//
+// Every kernel here is bit-exact against the reference semantics (SURVEY.md
+// Appendix A): integer kernels wrap mod 2^64 and reduce with order-free
+// wrapping sums; FP64 kernels use explicit _rn intrinsics (no contraction),
+// one thread per row in CSR order, and a single sequential chain for norm2.
+// Kernels that belong to a cycle read the Ctl block first and exit when the
+// cycle has already ended (break / error), so a whole cycle is enqueued
+// without host round trips.
+#include "igm_internal.cuh"
+
+#include <climits>
+#include <type_traits>
+#include <cstdio>
+
+namespace igm {
+
+unsigned long long g_launches = 0;
+
+int num_sms(int device) {
+  static int cached[64] = {0};
+  if (device < 0 || device >= 64) device = 0;
+  if (!cached[device]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    cached[device] = v > 0 ? v : 148;
+  }
+  return cached[device];
+}
+
+namespace {
+
+__device__ __forceinline__ bool cycle_over(const Ctl* c) {
+  return c != nullptr && (c->stop | c->err) != 0;
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ double dec(i64 raw, double scale) {
+  return __dmul_rn(__ll2double_rn(raw), scale);  // exact power-of-two scale
+}
+
+// wrapping block sum of a u64 (any order: Z/2^64 is commutative)
+template <int NT>
+__device__ __forceinline__ u64 block_sum(u64 v, u64* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  u64 r = 0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NT / 32; ++i) r += sh[i];
+  }
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ void bump(u64* cnt, int op, u64 v) {
+  if (v) atomicAdd(reinterpret_cast<unsigned long long*>(cnt + op), static_cast<unsigned long long>(v));
+}
+
+inline int grid_for(long long n, int nt, int device = 0) {
+  long long g = (n + nt - 1) / nt;
+  const long long cap = static_cast<long long>(num_sms(device)) * 8;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+// ---------------------------------------------------------------------------
+// K1 integer SpMV (split.cpp:137-157): one thread per row, CSR order, all
+// components 0..s per row; exact per-row overflow accounting.
+template <bool CHECKED>
+__global__ void __launch_bounds__(256) k_spmv_int(int n, const int* __restrict__ rp,
+                                                  const int* __restrict__ ci,
+                                                  const i64* __restrict__ vals, long long nnz,
+                                                  const int* __restrict__ alphas, int s,
+                                                  const i64* __restrict__ v, i64* __restrict__ out,
+                                                  u64* cnt, const Ctl* ctl) {
+  if (cycle_over(ctl)) return;
+  u64 nmul = 0, nadd = 0;
+  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < n; row += gridDim.x * blockDim.x) {
+    const int b = rp[row], e = rp[row + 1];
+    i64 o = 0;
+    for (int l = 0; l <= s; ++l) {
+      const i64* cv = vals + static_cast<long long>(l) * nnz;
+      i64 acc = 0;
+      for (int k = b; k < e; ++k) {
+        const i64 a = cv[k];
+        const i64 x = __ldg(v + ci[k]);
+        const i64 p = wmul(a, x);
+        if (CHECKED) {
+          nmul += mul_ovf(a, x);
+          nadd += add_ovf(acc, p);
+        }
+        acc = wadd(acc, p);
+      }
+      const i64 d = asr(acc, alphas[l]);
+      if (CHECKED) nadd += add_ovf(o, d);
+      o = wadd(o, d);
+    }
+    out[row] = o;
+  }
+  if (CHECKED) {
+    bump(cnt, OP_MUL, nmul);
+    bump(cnt, OP_ADD, nadd);
+  }
+}
+
+// spmv_fp(SplitMatrix) (split.cpp:159-175) fused with r0 = b - A x0
+// (gmres_int.cpp:63-68); if b == nullptr, y = A x.
+__global__ void __launch_bounds__(256) k_spmv_fp_split(int n, const int* __restrict__ rp,
+                                                       const int* __restrict__ ci,
+                                                       const i64* __restrict__ vals, long long nnz,
+                                                       const int* __restrict__ alphas, int s,
+                                                       const double* __restrict__ x,
+                                                       const double* __restrict__ b,
+                                                       double* __restrict__ y, const Ctl* ctl) {
+  if (cycle_over(ctl)) return;
+  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < n; row += gridDim.x * blockDim.x) {
+    const int rb = rp[row], re = rp[row + 1];
+    double o = 0.0;
+    for (int l = 0; l <= s; ++l) {
+      const i64* cv = vals + static_cast<long long>(l) * nnz;
+      const double scale = ldexp(1.0, -alphas[l]);
+      double acc = 0.0;
+      for (int k = rb; k < re; ++k)
+        acc = __dadd_rn(acc, __dmul_rn(__ll2double_rn(cv[k]), x[ci[k]]));
+      o = __dadd_rn(o, __dmul_rn(scale, acc));
+    }
+    y[row] = b ? __dsub_rn(b[row], o) : o;
+  }
+}
+
+// K7 residual (split.cpp:37-59 + refine.cpp:53-56): r = b - A_fp x, one
+// thread per row in CSR order from 0.0; tracks max|r| as IEEE bits.
+__global__ void __launch_bounds__(256) k_residual(int n, const int* __restrict__ rp,
+                                                  const int* __restrict__ ci,
+                                                  const double* __restrict__ vals,
+                                                  const double* __restrict__ x,
+                                                  const double* __restrict__ b,
+                                                  double* __restrict__ r, Ctl* ctl, int track) {
+  u64 mx = 0;
+  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < n; row += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    const int e = rp[row + 1];
+    for (int k = rp[row]; k < e; ++k) acc = __dadd_rn(acc, __dmul_rn(vals[k], x[ci[k]]));
+    const double rr = b ? __dsub_rn(b[row], acc) : acc;
+    r[row] = rr;
+    const u64 bits = static_cast<u64>(__double_as_longlong(fabs(rr)));
+    mx = bits > mx ? bits : mx;
+  }
+  if (track) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const u64 t = __shfl_down_sync(0xffffffffu, mx, o);
+      mx = t > mx ? t : mx;
+    }
+    if ((threadIdx.x & 31) == 0 && mx)
+      atomicMax(reinterpret_cast<unsigned long long*>(&ctl->rmax_bits), static_cast<unsigned long long>(mx));
+  }
+}
+
+__global__ void k_gamma(long long n, const double* __restrict__ r, Ctl* ctl) {
+  u64 mx = 0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const u64 bits = static_cast<u64>(__double_as_longlong(fabs(r[i])));
+    mx = bits > mx ? bits : mx;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const u64 t = __shfl_down_sync(0xffffffffu, mx, o);
+    mx = t > mx ? t : mx;
+  }
+  if ((threadIdx.x & 31) == 0 && mx)
+    atomicMax(reinterpret_cast<unsigned long long*>(&ctl->rmax_bits), static_cast<unsigned long long>(mx));
+}
+
+// b_k = r / gamma (refine.cpp:17-18), gamma = max|r| from Ctl.
+__global__ void k_scale_div(long long n, const double* __restrict__ r, double* __restrict__ out,
+                            const Ctl* ctl) {
+  if (cycle_over(ctl)) return;
+  const double g = __longlong_as_double(static_cast<long long>(ctl->rmax_bits));
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    out[i] = __ddiv_rn(r[i], g);
+}
+
+// ---------------------------------------------------------------------------
+// K8 norm2 (split.cpp:45-49): ONE sequential chain acc = fl(acc + fl(x*x)).
+// Warps 1..7 square the next tile into shared memory while thread 0 of
+// warp 0 runs the dependent FP64 add chain over the current tile.
+// mode: 0 -> *out = sqrt; 1 -> ctl->nb; 2 -> ctl->nr and ctl->relnorm;
+//       3 -> ctl->r0n (stop the cycle when zero); 4 -> out[0] (decode raw
+//       basis words first: collect_basis_norms).
+constexpr int kNormTile = 2048;
+
+__global__ void __launch_bounds__(256) k_norm2_serial(long long n, const double* __restrict__ v,
+                                                      const i64* __restrict__ raw, double scale,
+                                                      double* out, Ctl* ctl, int mode,
+                                                      int basis_idx) {
+  __shared__ double buf[2][kNormTile];
+  if (mode == 3 && cycle_over(ctl)) return;
+  if (mode == 4 && (ctl->err || basis_idx >= ctl->nbasis)) return;
+  double acc = 0.0;
+  const long long ntiles = (n + kNormTile - 1) / kNormTile;
+  for (long long t = 0; t < ntiles; ++t) {
+    double* b = buf[t & 1];
+    const long long base = t * kNormTile;
+    const int cnt = static_cast<int>(min(static_cast<long long>(kNormTile), n - base));
+    if (threadIdx.x >= 32) {
+      for (int q = threadIdx.x - 32; q < cnt; q += blockDim.x - 32) {
+        const double x = raw ? dec(raw[base + q], scale) : v[base + q];
+        b[q] = __dmul_rn(x, x);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int q = 0;
+      for (; q + 8 <= cnt; q += 8) {
+        const double a0 = b[q], a1 = b[q + 1], a2 = b[q + 2], a3 = b[q + 3];
+        const double a4 = b[q + 4], a5 = b[q + 5], a6 = b[q + 6], a7 = b[q + 7];
+        acc = __dadd_rn(acc, a0); acc = __dadd_rn(acc, a1);
+        acc = __dadd_rn(acc, a2); acc = __dadd_rn(acc, a3);
+        acc = __dadd_rn(acc, a4); acc = __dadd_rn(acc, a5);
+        acc = __dadd_rn(acc, a6); acc = __dadd_rn(acc, a7);
+      }
+      for (; q < cnt; ++q) acc = __dadd_rn(acc, b[q]);
+    }
+  }
+  if (threadIdx.x == 0) {
+    const double r = __dsqrt_rn(acc);
+    switch (mode) {
+      case 0: *out = r; break;
+      case 1: ctl->nb = r; break;
+      case 2:
+        ctl->nr = r;
+        ctl->relnorm = ctl->nb == 0.0 ? r : __ddiv_rn(r, ctl->nb);
+        break;
+      case 3:
+        ctl->r0n = r;
+        if (r == 0.0) ctl->stop = 1;
+        break;
+      case 4: out[basis_idx] = r; break;
+    }
+  }
+}
+
+// K10 encode v1 = trunc(ldexp(r0_i / ||r0||, f)) (gmres_int.cpp:77-81,
+// fxp.hpp:171-176) with the reference's range check.
+__global__ void k_encode(long long n, const double* __restrict__ r0, i64* __restrict__ v0, int f,
+                         Ctl* ctl) {
+  if (cycle_over(ctl)) return;
+  const double r0n = ctl->r0n;
+  const double lim = ldexp(1.0, 63 - f);
+  const double up = ldexp(1.0, f);
+  bool bad = false;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double x = __ddiv_rn(r0[i], r0n);
+    if (!(fabs(x) < lim)) {
+      bad = true;
+      v0[i] = 0;
+    } else {
+      v0[i] = __double2ll_rz(__dmul_rn(x, up));
+    }
+  }
+  if (bad && atomicCAS(&ctl->err, 0, IGM_OVERFLOW_ERROR) == 0) {
+    ctl->err_msg = EM_ENCODE;
+    ctl->err_step = -1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2/K3 fused MGS pass (gmres_int.cpp:101-115, fxp.cpp:49-104).
+//   MODE 0: dot_i only                     (i == 0)
+//   MODE 1: axpy_{i-1} then dot_i          (0 < i <= j)
+//   MODE 2: axpy_j then the norm sum       (tail of step j)
+//   MODE 3: axpy only                      (tail of the config-5 microbench)
+// h_{i-1} is re-derived by every thread from the wrapped accumulator of the
+// previous pass (fx_dot's final shift, fxp.cpp:63-65).  Reductions are
+// wrapping u64 sums (exact, order-free).  In checked mode per-element mul /
+// sub events are counted exactly and sum|term| is accumulated so the
+// running-sum ("add") events can be certified zero.
+template <int MODE, bool CHECKED>
+__global__ void __launch_bounds__(512) k_mgs(long long n, i64* __restrict__ w,
+                                             const i64* __restrict__ vprev,
+                                             const i64* __restrict__ vcur,
+                                             const u64* __restrict__ hacc, u64* acc_out,
+                                             u64* abs_out, int f, ShiftsD sh, u64* cnt_axpy,
+                                             u64* cnt_red, const Ctl* ctl) {
+  __shared__ u64 red[3][16];
+  if (cycle_over(ctl)) return;
+  i64 hs = 0;
+  const int post = f - sh.axpy_b1;
+  if (MODE != 0) {
+    const i64 acc = static_cast<i64>(*hacc);
+    const int e = f - sh.dot_b1 - sh.dot_b2;
+    const i64 h = e >= 0 ? asr(acc, e) : wrap_shl(acc, -e);
+    hs = asr(h, sh.axpy_b1);
+  }
+  u64 sum = 0, ahi = 0, alo = 0, nmul = 0, nsub = 0, nmul2 = 0;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long l = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; l < n; l += stride) {
+    i64 wl = w[l];
+    if (MODE != 0) {
+      const i64 vp = __ldg(vprev + l);
+      const i64 p = wmul(hs, vp);
+      const i64 d = asr(p, post);
+      if (CHECKED) {
+        nmul += mul_ovf(hs, vp);
+        nsub += sub_ovf(wl, d);
+      }
+      wl = wsub(wl, d);
+      w[l] = wl;
+    }
+    if (MODE == 0 || MODE == 1) {
+      const i64 a = asr(wl, sh.dot_b1);
+      const i64 b = asr(__ldg(vcur + l), sh.dot_b2);
+      const i64 t = wmul(a, b);
+      sum += static_cast<u64>(t);
+      if (CHECKED) {
+        nmul2 += mul_ovf(a, b);
+        const u64 at = t < 0 ? 0ull - static_cast<u64>(t) : static_cast<u64>(t);
+        ahi += at >> 32;
+        alo += at & 0xffffffffull;
+      }
+    } else if (MODE == 2) {
+      const i64 s = asr(wl, sh.norm_b1);
+      const i64 t = wmul(s, s);
+      sum += static_cast<u64>(t);
+      if (CHECKED) {
+        nmul2 += mul_ovf(s, s);
+        const u64 at = t < 0 ? 0ull - static_cast<u64>(t) : static_cast<u64>(t);
+        ahi += at >> 32;
+        alo += at & 0xffffffffull;
+      }
+    }
+  }
+  if (CHECKED) {
+    if (MODE != 0) {
+      bump(cnt_axpy, OP_MUL, nmul);
+      bump(cnt_axpy, OP_SUB, nsub);
+    }
+    if (MODE != 3) bump(cnt_red, OP_MUL, nmul2);
+  }
+  if (MODE == 3) return;
+  // block reduce (sum, ahi, alo)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sum += __shfl_down_sync(0xffffffffu, sum, o);
+    if (CHECKED) {
+      ahi += __shfl_down_sync(0xffffffffu, ahi, o);
+      alo += __shfl_down_sync(0xffffffffu, alo, o);
+    }
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][wid] = sum;
+    red[1][wid] = ahi;
+    red[2][wid] = alo;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nw = blockDim.x >> 5;
+    u64 s0 = 0, s1 = 0, s2 = 0;
+    for (int i = 0; i < nw; ++i) {
+      s0 += red[0][i];
+      s1 += red[1][i];
+      s2 += red[2][i];
+    }
+    atomicAdd(reinterpret_cast<unsigned long long*>(acc_out), static_cast<unsigned long long>(s0));
+    if (CHECKED) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(abs_out), static_cast<unsigned long long>(s1));
+      atomicAdd(reinterpret_cast<unsigned long long*>(abs_out + 1), static_cast<unsigned long long>(s2));
+    }
+  }
+}
+
+// Standalone fx_dot / fx_norm partial sums (fxp.cpp:49-86) for the primitive
+// entry points.  mode 0: dot, 1: norm.
+template <bool CHECKED>
+__global__ void __launch_bounds__(512) k_fx_red(long long n, int mode, const i64* __restrict__ v,
+                                                const i64* __restrict__ w, int b1, int b2,
+                                                u64* acc, u64* abs_out, u64* cnt) {
+  __shared__ u64 red[3][16];
+  u64 sum = 0, ahi = 0, alo = 0, nmul = 0;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long l = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; l < n; l += stride) {
+    const i64 a = asr(v[l], b1);
+    const i64 b = mode == 0 ? asr(w[l], b2) : a;
+    const i64 t = wmul(a, b);
+    sum += static_cast<u64>(t);
+    if (CHECKED) {
+      nmul += mul_ovf(a, b);
+      const u64 at = t < 0 ? 0ull - static_cast<u64>(t) : static_cast<u64>(t);
+      ahi += at >> 32;
+      alo += at & 0xffffffffull;
+    }
+  }
+  if (CHECKED) bump(cnt, OP_MUL, nmul);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sum += __shfl_down_sync(0xffffffffu, sum, o);
+    ahi += __shfl_down_sync(0xffffffffu, ahi, o);
+    alo += __shfl_down_sync(0xffffffffu, alo, o);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][wid] = sum;
+    red[1][wid] = ahi;
+    red[2][wid] = alo;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u64 s0 = 0, s1 = 0, s2 = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      s0 += red[0][i];
+      s1 += red[1][i];
+      s2 += red[2][i];
+    }
+    atomicAdd(reinterpret_cast<unsigned long long*>(acc), static_cast<unsigned long long>(s0));
+    atomicAdd(reinterpret_cast<unsigned long long*>(abs_out), static_cast<unsigned long long>(s1));
+    atomicAdd(reinterpret_cast<unsigned long long*>(abs_out + 1), static_cast<unsigned long long>(s2));
+  }
+}
+
+template <bool CHECKED>
+__global__ void __launch_bounds__(512) k_axpy(long long n, i64* __restrict__ w, i64 h,
+                                              const i64* __restrict__ v, int f, int b1, u64* cnt) {
+  const i64 hs = asr(h, b1);
+  const int post = f - b1;
+  u64 nmul = 0, nsub = 0;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long l = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; l < n; l += stride) {
+    const i64 vl = v[l];
+    const i64 d = asr(wmul(hs, vl), post);
+    const i64 wl = w[l];
+    if (CHECKED) {
+      nmul += mul_ovf(hs, vl);
+      nsub += sub_ovf(wl, d);
+    }
+    w[l] = wsub(wl, d);
+  }
+  if (CHECKED) {
+    bump(cnt, OP_MUL, nmul);
+    bump(cnt, OP_SUB, nsub);
+  }
+}
+
+// K4 vec_div (gmres_int.cpp:117-126, fxp.hpp:220-234): per element fx_div
+// by the step-invariant divisor via its exact reciprocal from Ctl.
+template <bool CHECKED>
+__global__ void __launch_bounds__(512) k_vec_div(long long n, const i64* __restrict__ w,
+                                                 i64* __restrict__ out, int f, int b1, int b2,
+                                                 u64* cnt, const Ctl* ctl) {
+  if (!ctl->do_vecdiv) return;
+  SDivMagic g;
+  g.u.m = ctl->div_m;
+  g.u.sh1 = ctl->div_sh1;
+  g.u.sh2 = ctl->div_sh2;
+  g.den_neg = ctl->div_neg;
+  g.den_is_m1 = ctl->div_m1;
+  const int e = f - b1 - b2;
+  u64 nshl = 0, ndiv = 0;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long l = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; l < n; l += stride) {
+    const i64 a = w[l];
+    const i64 num = wrap_shl(a, b1);
+    const i64 q = sdiv(num, g);
+    i64 r;
+    if (e >= 0) {
+      r = wrap_shl(q, e);
+      if (CHECKED) nshl += shl_ovf(q, e);
+    } else {
+      r = asr(q, -e);
+    }
+    if (CHECKED) {
+      nshl += shl_ovf(a, b1);
+      ndiv += sdiv_ovf(num, g);
+    }
+    out[l] = r;
+  }
+  if (CHECKED) {
+    bump(cnt, OP_SHL, nshl);
+    bump(cnt, OP_DIV, ndiv);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5 per-step scalar work (gmres_int.cpp:101-159): finalise the h_ij from
+// the wrapped accumulators, fx_norm -> h_{j+1,j}, vec_div reciprocal, the
+// stored rotations, t_mp, (c, s), the g update, dim and break flags.  One
+// thread; all overflow events counted in sequential order semantics.
+struct Ev {
+  u64* c;  // [K_COUNT][OP_COUNT] of this step
+  bool on;
+  __device__ void hit(int k, int op) {
+    if (on) c[k * OP_COUNT + op] += 1;
+  }
+};
+
+__device__ i64 d_fx_mul(i64 a, i64 b, int f, int b1, int b2, int of, Ev& ev, int k) {
+  const i64 x = asr(a, b1), y = asr(b, b2);
+  if (mul_ovf(x, y)) ev.hit(k, OP_MUL);
+  return asr(wmul(x, y), 2 * f - b1 - b2 - of);
+}
+
+// returns false on a zero shifted divisor (domain_error)
+__device__ bool d_fx_div(i64 a, i64 b, int f, int b1, int b2, i64* out, Ev& ev, int k) {
+  const i64 num = wrap_shl(a, b1);
+  if (shl_ovf(a, b1)) ev.hit(k, OP_SHL);
+  const i64 den = asr(b, b2);
+  if (den == 0) return false;
+  i64 q;
+  if (num == INT64_MIN && den == -1) {
+    ev.hit(k, OP_DIV);
+    q = num;
+  } else {
+    q = num / den;
+  }
+  const int e = f - b1 - b2;
+  if (e >= 0) {
+    if (shl_ovf(q, e)) ev.hit(k, OP_SHL);
+    *out = wrap_shl(q, e);
+  } else {
+    *out = asr(q, -e);
+  }
+  return true;
+}
+
+__device__ void set_err(Ctl* ctl, int status, int msg, int step) {
+  if (ctl->err == 0) {
+    ctl->err = status;
+    ctl->err_msg = msg;
+    ctl->err_step = step;
+  }
+  ctl->stop = 1;
+}
+
+// exact sum|t| = hi*2^32 + lo < 2^63 certifies zero running-sum events
+__device__ bool abs_small(const u64* ab) {
+  const unsigned __int128 s = (static_cast<unsigned __int128>(ab[0]) << 32) + ab[1];
+  return s < (static_cast<unsigned __int128>(1) << 63);
+}
+
+__global__ void k_step_scalar(int j, int f, ShiftsD sh, const u64* acc_col, const u64* abs_col,
+                              const u64* nacc, const u64* nabs, i64* hess, int ld, i64* g,
+                              i64* cs, i64* sn, i64* gabs, const i64* w, u64* cnt_step, Ctl* ctl,
+                              int checked) {
+  ctl->do_vecdiv = 0;
+  if (cycle_over(ctl)) return;
+  Ev ev{cnt_step, checked != 0};
+  i64* col = hess + static_cast<long long>(j) * ld;
+  // h_ij = fx_dot finalisation (fxp.cpp:63-65)
+  const int e = f - sh.dot_b1 - sh.dot_b2;
+  for (int i = 0; i <= j; ++i) {
+    const i64 acc = static_cast<i64>(acc_col[i]);
+    if (e >= 0) {
+      col[i] = asr(acc, e);
+    } else {
+      if (shl_ovf(acc, -e)) ev.hit(K_DOT, OP_SHL);
+      col[i] = wrap_shl(acc, -e);
+    }
+    if (checked && !abs_small(abs_col + 2 * i)) ctl->add_inexact = 1;
+  }
+  // h_{j+1,j} = fx_norm(w) (fxp.cpp:69-86)
+  const i64 nsum = static_cast<i64>(*nacc);
+  if (checked) {
+    // all terms s*s are >= 0 unless a square itself wrapped: then the
+    // running sum is monotone and its wrap count is exact.
+    if (cnt_step[K_NORM * OP_COUNT + OP_MUL] == 0) {
+      const unsigned __int128 s = (static_cast<unsigned __int128>(nabs[0]) << 32) + nabs[1];
+      const unsigned __int128 wraps = (s + (static_cast<unsigned __int128>(1) << 63)) >> 64;
+      cnt_step[K_NORM * OP_COUNT + OP_ADD] += static_cast<u64>(wraps);
+    } else if (!abs_small(nabs)) {
+      ctl->add_inexact = 1;
+    }
+  }
+  if (nsum < 0) {
+    set_err(ctl, IGM_DOMAIN_ERROR, EM_NORM_NEG, j);
+    return;
+  }
+  i64 hnext;
+  {
+    const i64 r = static_cast<i64>(isqrt_u64(static_cast<u64>(nsum)));
+    const int es = sh.norm_b1;  // out_frac - fin/2 = f - (f - b1)
+    if (shl_ovf(r, es)) ev.hit(K_NORM, OP_SHL);
+    hnext = wrap_shl(r, es);
+  }
+  col[j + 1] = hnext;
+  ctl->hnext = hnext;
+  const bool happy = hnext == 0;
+  if (!happy) {
+    const i64 den = asr(hnext, sh.div_b2);
+    if (den == 0) {
+      if (shl_ovf(w[0], sh.div_b1)) ev.hit(K_VEC_DIV, OP_SHL);
+      set_err(ctl, IGM_DOMAIN_ERROR, EM_DIV_ZERO, j);
+      return;
+    }
+    const SDivMagic gm = make_sdiv(den);
+    ctl->div_m = gm.u.m;
+    ctl->div_sh1 = gm.u.sh1;
+    ctl->div_sh2 = gm.u.sh2;
+    ctl->div_neg = gm.den_neg;
+    ctl->div_m1 = gm.den_is_m1;
+    ctl->do_vecdiv = 1;
+    ctl->nbasis = j + 2;
+  }
+  // apply_stored_rotations (gmres_int.cpp:8-25)
+  for (int i = 0; i < j; ++i) {
+    const i64 c = cs[i], s = sn[i], hi = col[i], hn = col[i + 1];
+    const i64 a = d_fx_mul(c, hi, f, 0, sh.givens_b2, f, ev, K_GIVENS);
+    const i64 b = d_fx_mul(s, hn, f, 0, sh.givens_b2, f, ev, K_GIVENS);
+    const i64 d = d_fx_mul(c, hn, f, 0, sh.givens_b2, f, ev, K_GIVENS);
+    const i64 q = d_fx_mul(s, hi, f, 0, sh.givens_b2, f, ev, K_GIVENS);
+    if (add_ovf(a, b)) ev.hit(K_GIVENS, OP_ADD);
+    if (sub_ovf(d, q)) ev.hit(K_GIVENS, OP_SUB);
+    col[i] = wadd(a, b);
+    col[i + 1] = wsub(d, q);
+  }
+  // t_mp = fx_norm((h_jj, h_{j+1,j})) (gmres_int.cpp:133-137)
+  i64 tmp;
+  {
+    const i64 s0 = asr(col[j], sh.norm_b1), s1 = asr(col[j + 1], sh.norm_b1);
+    if (mul_ovf(s0, s0)) ev.hit(K_GIVENS_NORM, OP_MUL);
+    const i64 p0 = wmul(s0, s0);
+    i64 acc = p0;  // 0 + p0 never overflows
+    if (mul_ovf(s1, s1)) ev.hit(K_GIVENS_NORM, OP_MUL);
+    const i64 p1 = wmul(s1, s1);
+    if (add_ovf(acc, p1)) ev.hit(K_GIVENS_NORM, OP_ADD);
+    acc = wadd(acc, p1);
+    if (acc < 0) {
+      set_err(ctl, IGM_DOMAIN_ERROR, EM_NORM_NEG, j);
+      return;
+    }
+    const i64 r = static_cast<i64>(isqrt_u64(static_cast<u64>(acc)));
+    if (shl_ovf(r, sh.norm_b1)) ev.hit(K_GIVENS_NORM, OP_SHL);
+    tmp = wrap_shl(r, sh.norm_b1);
+  }
+  if (tmp == 0) {  // column vanished under rotation: drop it, dim unchanged
+    ctl->stop = 1;
+    return;
+  }
+  i64 c, s;
+  if (!d_fx_div(col[j], tmp, f, sh.div_b1, sh.div_b2, &c, ev, K_GIVENS_DIV) ||
+      !d_fx_div(col[j + 1], tmp, f, sh.div_b1, sh.div_b2, &s, ev, K_GIVENS_DIV)) {
+    set_err(ctl, IGM_DOMAIN_ERROR, EM_DIV_ZERO, j);
+    return;
+  }
+  cs[j] = c;
+  sn[j] = s;
+  col[j] = tmp;
+  col[j + 1] = 0;
+  // residual estimate (gmres_int.cpp:150-153)
+  const i64 g_old = g[j];
+  if (sub_ovf(0, s)) ev.hit(K_ROT, OP_SUB);
+  const i64 neg_s = wsub(0, s);
+  g[j + 1] = d_fx_mul(neg_s, g_old, f, sh.rot_b, sh.rot_b, f, ev, K_ROT);
+  g[j] = d_fx_mul(c, g_old, f, sh.rot_b, sh.rot_b, f, ev, K_ROT);
+  ctl->dim = j + 1;
+  gabs[j] = g[j + 1];
+  if (happy) ctl->stop = 1;
+}
+
+__global__ void k_cycle_init(Ctl* ctl, i64* g, int f) {
+  ctl->stop = 0;
+  ctl->dim = 0;
+  ctl->nbasis = 1;
+  ctl->do_vecdiv = 0;
+  ctl->add_inexact = 0;
+  ctl->r0n = 0.0;
+  g[0] = i64{1} << f;
+}
+
+// K11 (gmres_int.cpp:163-175): decode R and g, back substitution, weights
+// r0n * y_j.  One thread; dim <= m is tiny.
+__global__ void k_cycle_finish(int m, int f, const i64* hess, const i64* g, double* y,
+                               double* wts, Ctl* ctl) {
+  if (ctl->err) return;
+  const int dim = ctl->dim;
+  if (dim == 0) return;
+  const int ld = m + 1;
+  const double sc = ldexp(1.0, -f);
+  for (int i = dim - 1; i >= 0; --i) {
+    double acc = dec(g[i], sc);
+    for (int jj = i + 1; jj < dim; ++jj)
+      acc = __dsub_rn(acc, __dmul_rn(dec(hess[static_cast<long long>(jj) * ld + i], sc), y[jj]));
+    const double rii = dec(hess[static_cast<long long>(i) * ld + i], sc);
+    if (rii == 0.0) {
+      set_err(ctl, IGM_RUNTIME_ERROR, EM_HESS_ZERO, -2);
+      return;
+    }
+    y[i] = __ddiv_rn(acc, rii);
+  }
+  for (int jj = 0; jj < dim; ++jj) wts[jj] = __dmul_rn(ctl->r0n, y[jj]);
+}
+
+// x update (gmres_int.cpp:176-179, refine.cpp:87).
+//   mode 0 (run_cycle): x = x0 + sum_j wts_j * decode(v_j), in j order.
+//   mode 1 (solve):     x += gamma * (0.0 + sum_j wts_j * decode(v_j)).
+__global__ void __launch_bounds__(256) k_xupdate(long long n, int f, const i64* __restrict__ basis,
+                                                 const double* __restrict__ wts,
+                                                 const double* __restrict__ x0,
+                                                 double* __restrict__ x, const Ctl* ctl, int mode) {
+  if (ctl->err) return;
+  const int dim = ctl->dim;
+  if (mode == 1 && dim == 0) return;
+  const double sc = ldexp(1.0, -f);
+  const double gamma = __longlong_as_double(static_cast<long long>(ctl->rmax_bits));
+  for (long long l = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; l < n;
+       l += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double acc = mode == 0 ? (x0 ? x0[l] : 0.0) : 0.0;
+    for (int jj = 0; jj < dim; ++jj)
+      acc = __dadd_rn(acc, __dmul_rn(wts[jj], dec(basis[static_cast<long long>(jj) * n + l], sc)));
+    if (mode == 0)
+      x[l] = acc;
+    else
+      x[l] = __dadd_rn(x[l], __dmul_rn(gamma, acc));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K6/K9 ILU(0) triangular substitutions (ilu.cpp:122-180), sync-free
+// wavefront.  Rows are split into contiguous tiles; a CTA takes tiles in
+// dependency order from a ticket counter (so every tile it waits on is
+// already owned by a running CTA: deadlock-free for any grid size), walks
+// its tile's rows level by level keeping the tile's results in shared
+// memory, and publishes per-tile progress ("all rows with level <= p are
+// final") with release/acquire.  Cross-tile dependencies wait on that
+// progress word and read the value through L2.  Per row the arithmetic is
+// the reference's: CSR order, wrapping mul/sub, truncating division by the
+// raw diagonal (exact reciprocal), or the same in FP64 on the integer
+// factors with no contraction.
+struct TriArgs {
+  int n, tile_rows, ntiles;
+  const int* rp;
+  const int* ci;
+  const i64* vals;
+  const i64* diag;
+  const u64* dmag;
+  const int* dinfo;
+  const int* tile_seg;
+  const int* seg_level;
+  const int* seg_rows;
+  const int* perm;
+  int* prog;
+  int* ticket;
+};
+
+template <typename T, bool BACKWARD, bool CHECKED>
+__global__ void __launch_bounds__(256) k_tri(TriArgs a, const T* __restrict__ y, T* out,
+                                             u64* cnt, const Ctl* ctl,
+                                             const double* prescale) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* zt = reinterpret_cast<T*>(smem_raw);
+  __shared__ int s_tile;
+  if (cycle_over(ctl)) return;
+  if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1);
+  __syncthreads();
+  const int k = s_tile;
+  const int tile = BACKWARD ? a.ntiles - 1 - k : k;
+  const int r0 = tile * a.tile_rows;
+  const int r1 = min(a.n, r0 + a.tile_rows);
+  const int sb = a.tile_seg[tile], se = a.tile_seg[tile + 1];
+  if (threadIdx.x == 0) st_release(a.prog + tile, a.seg_level[sb] - 1);
+  double inv_scale = 0.0;
+  if (prescale) inv_scale = __longlong_as_double(*reinterpret_cast<const long long*>(prescale));
+  u64 nmul = 0, nsub = 0, ndiv = 0;
+  for (int sgi = sb; sgi < se; ++sgi) {
+    const int lev = a.seg_level[sgi];
+    const int pe = a.seg_rows[sgi + 1];
+    for (int p = a.seg_rows[sgi] + threadIdx.x; p < pe; p += blockDim.x) {
+      const int i = a.perm[p];
+      T acc;
+      if constexpr (sizeof(T) == 8 && std::is_same<T, double>::value) {
+        acc = prescale ? __ddiv_rn(y[i], inv_scale) : y[i];
+      } else {
+        acc = y[i];
+      }
+      int waited = -1;
+      const int ke = a.rp[i + 1];
+      for (int kk = a.rp[i]; kk < ke; ++kk) {
+        const int jc = a.ci[kk];
+        const i64 lv = a.vals[kk];
+        T zj;
+        if (jc >= r0 && jc < r1) {
+          zj = zt[jc - r0];
+        } else {
+          const int tj = jc / a.tile_rows;
+          if (tj != waited) {
+            while (ld_acquire(a.prog + tj) < lev - 1) {
+            }
+            waited = tj;
+          }
+          zj = __ldcg(out + jc);
+        }
+        if constexpr (std::is_same<T, double>::value) {
+          acc = __dsub_rn(acc, __dmul_rn(__ll2double_rn(lv), zj));
+        } else {
+          const i64 pr = wmul(lv, zj);
+          if (CHECKED) {
+            nmul += mul_ovf(lv, zj);
+            nsub += sub_ovf(acc, pr);
+          }
+          acc = wsub(acc, pr);
+        }
+      }
+      T z;
+      if constexpr (std::is_same<T, double>::value) {
+        z = __ddiv_rn(acc, __ll2double_rn(a.diag[i]));
+      } else {
+        const int info = a.dinfo[i];
+        SDivMagic gm;
+        gm.u.m = a.dmag[i];
+        gm.u.sh1 = info & 1;
+        gm.u.sh2 = (info >> 1) & 127;
+        gm.den_neg = (info >> 8) & 1;
+        gm.den_is_m1 = (info >> 9) & 1;
+        if (CHECKED) ndiv += sdiv_ovf(acc, gm);
+        z = sdiv(acc, gm);
+      }
+      zt[i - r0] = z;
+      out[i] = z;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0)
+      st_release(a.prog + tile, sgi + 1 < se ? a.seg_level[sgi + 1] - 1 : INT_MAX);
+  }
+  if (CHECKED && !std::is_same<T, double>::value) {
+    bump(cnt, OP_MUL, nmul);
+    bump(cnt, OP_SUB, nsub);
+    bump(cnt, OP_DIV, ndiv);
+  }
+}
+
+TriArgs tri_args(const DevTri& t) {
+  TriArgs a;
+  a.n = t.n;
+  a.tile_rows = t.tile_rows;
+  a.ntiles = t.ntiles;
+  a.rp = t.rp;
+  a.ci = t.ci;
+  a.vals = t.vals;
+  a.diag = t.diag;
+  a.dmag = t.dmag;
+  a.dinfo = t.dinfo;
+  a.tile_seg = t.tile_seg;
+  a.seg_level = t.seg_level;
+  a.seg_rows = t.seg_rows;
+  a.perm = t.perm;
+  a.prog = t.prog;
+  a.ticket = t.ticket;
+  return a;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launchers
+
+#define LAUNCH_CHECK() ++g_launches
+
+void launch_spmv_int(cudaStream_t st, const DevSplit& m, int s, const i64* v, i64* out, u64* cnt,
+                     const Ctl* ctl, bool checked) {
+  const int nt = 256;
+  const int g = static_cast<int>((m.n + nt - 1) / nt > 0 ? (m.n + nt - 1) / nt : 1);
+  if (checked)
+    k_spmv_int<true><<<g, nt, 0, st>>>(m.n, m.row_ptr, m.col_idx, m.vals, m.nnz, m.alphas, s, v, out, cnt, ctl);
+  else
+    k_spmv_int<false><<<g, nt, 0, st>>>(m.n, m.row_ptr, m.col_idx, m.vals, m.nnz, m.alphas, s, v, out, cnt, ctl);
+  LAUNCH_CHECK();
+}
+
+void launch_spmv_fp_split(cudaStream_t st, const DevSplit& m, int s, const double* x,
+                          const double* b, double* y, const Ctl* ctl) {
+  const int nt = 256;
+  const int g = (m.n + nt - 1) / nt > 0 ? (m.n + nt - 1) / nt : 1;
+  k_spmv_fp_split<<<g, nt, 0, st>>>(m.n, m.row_ptr, m.col_idx, m.vals, m.nnz, m.alphas, s, x, b, y, ctl);
+  LAUNCH_CHECK();
+}
+
+void launch_residual(cudaStream_t st, const DevCsrf& a, const double* x, const double* b,
+                     double* r, Ctl* ctl, bool track_max) {
+  const int nt = 256;
+  const int g = (a.n + nt - 1) / nt > 0 ? (a.n + nt - 1) / nt : 1;
+  k_residual<<<g, nt, 0, st>>>(a.n, a.row_ptr, a.col_idx, a.vals, x, b, r, ctl, track_max ? 1 : 0);
+  LAUNCH_CHECK();
+}
+
+void launch_gamma(cudaStream_t st, long long n, const double* r, Ctl* ctl) {
+  k_gamma<<<grid_for(n, 256), 256, 0, st>>>(n, r, ctl);
+  LAUNCH_CHECK();
+}
+
+void launch_scale_div(cudaStream_t st, long long n, const double* r, double* out, const Ctl* ctl) {
+  k_scale_div<<<grid_for(n, 256), 256, 0, st>>>(n, r, out, ctl);
+  LAUNCH_CHECK();
+}
+
+void launch_norm2_serial(cudaStream_t st, long long n, const double* v, double* out, Ctl* ctl,
+                         int mode) {
+  k_norm2_serial<<<1, 256, 0, st>>>(n, v, nullptr, 1.0, out, ctl, mode, 0);
+  LAUNCH_CHECK();
+}
+
+void launch_basis_norms(cudaStream_t st, long long n, int nb, int f, const i64* basis, double* tmp,
+                        double* out, Ctl* ctl) {
+  (void)tmp;
+  for (int k = 0; k < nb; ++k) {
+    k_norm2_serial<<<1, 256, 0, st>>>(n, nullptr, basis + static_cast<long long>(k) * n,
+                                      ldexp(1.0, -f), out, ctl, 4, k);
+    LAUNCH_CHECK();
+  }
+}
+
+void launch_encode(cudaStream_t st, long long n, const double* r0, i64* v0, int f, Ctl* ctl) {
+  k_encode<<<grid_for(n, 256), 256, 0, st>>>(n, r0, v0, f, ctl);
+  LAUNCH_CHECK();
+}
+
+void launch_mgs_pass(cudaStream_t st, long long n, int mode, i64* w, const i64* vprev,
+                     const i64* vcur, const u64* hacc, u64* acc_out, u64* abs_out, int f,
+                     ShiftsD sh, u64* cnt_axpy, u64* cnt_red, const Ctl* ctl, bool checked) {
+  const int nt = 512;
+  const int g = grid_for(n, nt) > 2 * num_sms(0) ? 2 * num_sms(0) : grid_for(n, nt);
+#define MGS_CASE(MD)                                                                               \
+  if (checked)                                                                                     \
+    k_mgs<MD, true><<<g, nt, 0, st>>>(n, w, vprev, vcur, hacc, acc_out, abs_out, f, sh, cnt_axpy,  \
+                                      cnt_red, ctl);                                               \
+  else                                                                                             \
+    k_mgs<MD, false><<<g, nt, 0, st>>>(n, w, vprev, vcur, hacc, acc_out, abs_out, f, sh, cnt_axpy, \
+                                       cnt_red, ctl);
+  switch (mode) {
+    case 0: MGS_CASE(0) break;
+    case 1: MGS_CASE(1) break;
+    case 2: MGS_CASE(2) break;
+    default: MGS_CASE(3) break;
+  }
+#undef MGS_CASE
+  LAUNCH_CHECK();
+}
+
+void launch_fx_red(cudaStream_t st, long long n, int mode, const i64* v, const i64* w, int b1,
+                   int b2, u64* acc, u64* abs_out, u64* cnt, bool checked) {
+  const int nt = 512;
+  const int g = grid_for(n, nt) > 2 * num_sms(0) ? 2 * num_sms(0) : grid_for(n, nt);
+  if (checked)
+    k_fx_red<true><<<g, nt, 0, st>>>(n, mode, v, w, b1, b2, acc, abs_out, cnt);
+  else
+    k_fx_red<false><<<g, nt, 0, st>>>(n, mode, v, w, b1, b2, acc, abs_out, cnt);
+  LAUNCH_CHECK();
+}
+
+void launch_axpy_only(cudaStream_t st, long long n, i64* w, i64 h, const i64* v, int f, int b1,
+                      u64* cnt, bool checked) {
+  const int nt = 512;
+  const int g = grid_for(n, nt);
+  if (checked)
+    k_axpy<true><<<g, nt, 0, st>>>(n, w, h, v, f, b1, cnt);
+  else
+    k_axpy<false><<<g, nt, 0, st>>>(n, w, h, v, f, b1, cnt);
+  LAUNCH_CHECK();
+}
+
+void launch_vec_div(cudaStream_t st, long long n, const i64* w, i64* out, int f, ShiftsD sh,
+                    u64* cnt, const Ctl* ctl, bool checked) {
+  const int nt = 512;
+  const int g = grid_for(n, nt);
+  if (checked)
+    k_vec_div<true><<<g, nt, 0, st>>>(n, w, out, f, sh.div_b1, sh.div_b2, cnt, ctl);
+  else
+    k_vec_div<false><<<g, nt, 0, st>>>(n, w, out, f, sh.div_b1, sh.div_b2, cnt, ctl);
+  LAUNCH_CHECK();
+}
+
+void launch_step_scalar(cudaStream_t st, int j, int f, ShiftsD sh, const u64* acc_col,
+                        const u64* abs_col, const u64* nacc, const u64* nabs, i64* hess, int ld,
+                        i64* g, i64* cs, i64* sn, i64* gabs, const i64* w, u64* cnt_step, Ctl* ctl,
+                        bool checked) {
+  k_step_scalar<<<1, 1, 0, st>>>(j, f, sh, acc_col, abs_col, nacc, nabs, hess, ld, g, cs, sn, gabs,
+                                 w, cnt_step, ctl, checked ? 1 : 0);
+  LAUNCH_CHECK();
+}
+
+void launch_cycle_init(cudaStream_t st, Ctl* ctl, i64* g, int f) {
+  k_cycle_init<<<1, 1, 0, st>>>(ctl, g, f);
+  LAUNCH_CHECK();
+}
+
+void launch_cycle_finish(cudaStream_t st, int m, int f, const i64* hess, const i64* g, double* y,
+                         double* wts, Ctl* ctl) {
+  k_cycle_finish<<<1, 1, 0, st>>>(m, f, hess, g, y, wts, ctl);
+  LAUNCH_CHECK();
+}
+
+void launch_xupdate(cudaStream_t st, long long n, int m, int f, const i64* basis,
+                    const double* wts, const double* x0, double* x, const Ctl* ctl, int mode) {
+  (void)m;
+  k_xupdate<<<grid_for(n, 256), 256, 0, st>>>(n, f, basis, wts, x0, x, ctl, mode);
+  LAUNCH_CHECK();
+}
+
+static void tri_smem_setup(size_t bytes) {
+  static size_t done = 0;
+  if (bytes > done) {
+    cudaFuncSetAttribute(k_tri<i64, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(k_tri<i64, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(k_tri<i64, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(k_tri<i64, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(k_tri<double, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(k_tri<double, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    done = bytes;
+  }
+}
+
+void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out,
+                    u64* cnt, const Ctl* ctl, bool checked) {
+  if (t.n == 0) return;
+  const size_t sm = static_cast<size_t>(t.tile_rows) * sizeof(i64);
+  tri_smem_setup(sm);
+  cudaMemsetAsync(t.ticket, 0, sizeof(int), st);
+  cudaMemsetAsync(t.prog, 0xff, sizeof(int) * t.ntiles, st);
+  const TriArgs a = tri_args(t);
+  if (backward) {
+    if (checked) k_tri<i64, true, true><<<t.ntiles, 256, sm, st>>>(a, y, out, cnt, ctl, nullptr);
+    else k_tri<i64, true, false><<<t.ntiles, 256, sm, st>>>(a, y, out, cnt, ctl, nullptr);
+  } else {
+    if (checked) k_tri<i64, false, true><<<t.ntiles, 256, sm, st>>>(a, y, out, cnt, ctl, nullptr);
+    else k_tri<i64, false, false><<<t.ntiles, 256, sm, st>>>(a, y, out, cnt, ctl, nullptr);
+  }
+  LAUNCH_CHECK();
+}
+
+void launch_tri_fp(cudaStream_t st, const DevTri& t, bool backward, const double* y, double* out,
+                   const Ctl* ctl, const double* prescale) {
+  if (t.n == 0) return;
+  const size_t sm = static_cast<size_t>(t.tile_rows) * sizeof(double);
+  tri_smem_setup(sm);
+  cudaMemsetAsync(t.ticket, 0, sizeof(int), st);
+  cudaMemsetAsync(t.prog, 0xff, sizeof(int) * t.ntiles, st);
+  const TriArgs a = tri_args(t);
+  if (backward)
+    k_tri<double, true, false><<<t.ntiles, 256, sm, st>>>(a, y, out, nullptr, ctl, prescale);
+  else
+    k_tri<double, false, false><<<t.ntiles, 256, sm, st>>>(a, y, out, nullptr, ctl, prescale);
+  LAUNCH_CHECK();
+}
+
+}  // namespace igm

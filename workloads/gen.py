@@ -1,0 +1,183 @@
+"""Synthetic inputs for the BASELINE.json configs (SURVEY.md 8(d) generator rules).
+
+* SplitMix64 counter generator, vectorised in numpy: doubles from the top 53
+  bits, no libstdc++ distributions -- the same arrays feed the oracle and the
+  GPU, so nothing has to be regenerated consistently across languages.
+* CSR rows are built directly, sorted ascending, no duplicates (the format
+  from_triplets produces, split.cpp:15-33).
+* Seeds: 0x200907495 ^ cfg_id.
+
+The paper's SuiteSparse matrices are not available offline; these seeded
+stencils / random matrices stand in with the shapes BASELINE.json names.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+SEED_BASE = 0x200907495
+_GOLD = np.uint64(0x9E3779B97F4A7C15)
+_M1 = np.uint64(0xBF58476D1CE4E5B9)
+_M2 = np.uint64(0x94D049BB133111EB)
+
+
+def splitmix64(seed: int, count: int, offset: int = 0) -> np.ndarray:
+    """count outputs of SplitMix64 starting at stream position offset."""
+    with np.errstate(over="ignore"):
+        idx = np.arange(offset + 1, offset + count + 1, dtype=np.uint64)
+        z = np.uint64(seed & 0xFFFFFFFFFFFFFFFF) + idx * _GOLD
+        z = (z ^ (z >> np.uint64(30))) * _M1
+        z = (z ^ (z >> np.uint64(27))) * _M2
+        return z ^ (z >> np.uint64(31))
+
+
+def uniform(seed: int, count: int, lo: float = -1.0, hi: float = 1.0, offset: int = 0) -> np.ndarray:
+    u = (splitmix64(seed, count, offset) >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+    return lo + (hi - lo) * u
+
+
+def uniform_int(seed: int, count: int, lo: int, hi: int, offset: int = 0) -> np.ndarray:
+    """integers uniform in [lo, hi] (inclusive); hi - lo < 2^63."""
+    span = np.uint64(hi - lo + 1)
+    r = splitmix64(seed, count, offset) % span
+    return (r.astype(np.int64) + np.int64(lo)).astype(np.int64)
+
+
+def normal(seed: int, count: int, offset: int = 0) -> np.ndarray:
+    """Box-Muller normals."""
+    m = (count + 1) // 2
+    u1 = uniform(seed, m, 0.0, 1.0, offset)
+    u2 = uniform(seed, m, 0.0, 1.0, offset + m)
+    u1 = np.where(u1 <= 0.0, 2.0 ** -53, u1)
+    r = np.sqrt(-2.0 * np.log(u1))
+    z = np.concatenate([r * np.cos(2 * np.pi * u2), r * np.sin(2 * np.pi * u2)])
+    return z[:count]
+
+
+# ---------------------------------------------------------------- stencils
+def _stencil_csr(dims, offsets, coef_fn):
+    """CSR of a structured-grid stencil in natural order (x fastest).
+
+    offsets: list of (di, dj, dk) sorted so that the flat column offsets are
+    ascending; coef_fn(offset_index, valid_mask, rows) -> values for those rows.
+    Out-of-grid neighbours are dropped (Dirichlet).
+    """
+    gx, gy, gz = dims
+    n = gx * gy * gz
+    r = np.arange(n, dtype=np.int64)
+    i = r % gx
+    j = (r // gx) % gy
+    k = r // (gx * gy)
+    flat = [dk * gx * gy + dj * gx + di for (di, dj, dk) in offsets]
+    order = np.argsort(flat, kind="stable")
+    masks, cols, vals = [], [], []
+    for o in order:
+        di, dj, dk = offsets[o]
+        ok = ((i + di >= 0) & (i + di < gx) & (j + dj >= 0) & (j + dj < gy) & (k + dk >= 0) & (k + dk < gz))
+        masks.append(ok)
+        cols.append((r + flat[o]).astype(np.int64))
+        vals.append(coef_fn(o, r))
+    mask = np.stack(masks, axis=1)
+    counts = mask.sum(axis=1)
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=row_ptr[1:])
+    col = np.stack(cols, axis=1)[mask].astype(np.int32)
+    val = np.stack(vals, axis=1)[mask].astype(np.float64)
+    return row_ptr.astype(np.int32), col, val
+
+
+def upwind_2d(g: int, beta=(10.0, 10.0)):
+    """Config 1: -Lap u + beta.grad u, 5-point first-order upwind, h = 1/(g+1)."""
+    h = 1.0 / (g + 1)
+    d = 4.0 / h ** 2 + (beta[0] + beta[1]) / h
+    offs = [(0, -1, 0), (-1, 0, 0), (0, 0, 0), (1, 0, 0), (0, 1, 0)]
+    upw = {0: -1.0 / h ** 2 - beta[1] / h, 1: -1.0 / h ** 2 - beta[0] / h, 2: d,
+           3: -1.0 / h ** 2, 4: -1.0 / h ** 2}
+    return _stencil_csr((g, g, 1), offs, lambda o, r: np.full(r.shape, upw[o]))
+
+
+def upwind_3d(g: int, beta: float = 20.0):
+    """Configs 2 / 5: 7-point upwind convection-diffusion, h = 1/(g+1)."""
+    h = 1.0 / (g + 1)
+    d = 6.0 / h ** 2 + 3 * beta / h
+    offs = [(0, 0, -1), (0, -1, 0), (-1, 0, 0), (0, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 1)]
+    coef = {0: -1.0 / h ** 2 - beta / h, 1: -1.0 / h ** 2 - beta / h, 2: -1.0 / h ** 2 - beta / h,
+            3: d, 4: -1.0 / h ** 2, 5: -1.0 / h ** 2, 6: -1.0 / h ** 2}
+    return _stencil_csr((g, g, g), offs, lambda o, r: np.full(r.shape, coef[o]))
+
+
+def stencil27(g: int, seed: int):
+    """Config 4: 27-point, off-diagonals -u*(1+0.1*sigma(d)), u~U[0,1), a_rr = 1.05*sum|a_rd|."""
+    offs = [(di, dj, dk) for dk in (-1, 0, 1) for dj in (-1, 0, 1) for di in (-1, 0, 1)]
+    n = g ** 3
+
+    def coef(o, r):
+        di, dj, dk = offs[o]
+        if (di, dj, dk) == (0, 0, 0):
+            return np.zeros(r.shape)
+        s = di + dj + dk
+        sig = 1.0 if s < 0 else (-1.0 if s > 0 else 0.0)
+        u = uniform(seed, n, 0.0, 1.0, offset=o * n)
+        return -u * (1.0 + 0.1 * sig)
+
+    rp, ci, v = _stencil_csr((g, g, g), offs, coef)
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    diag = ci == rows
+    rs = np.bincount(rows, weights=np.abs(v), minlength=n)
+    v[diag] = 1.05 * rs
+    return rp, ci, v
+
+
+def random_band(n: int, seed: int, band: int = 2, extra: int = 10):
+    """Config 3: band i-2..i+2 plus `extra` distinct random columns outside the band."""
+    cols = []
+    base = np.arange(n, dtype=np.int64)[:, None] + np.arange(-band, band + 1)[None, :]
+    rnd = uniform_int(seed, n * extra * 2, 0, n - 1).reshape(n, extra * 2)
+    rows = []
+    for i in range(n):  # only used at small sizes in tests; bench builds it vectorised later
+        c = set(int(x) for x in base[i] if 0 <= x < n)
+        band_set = set(c)
+        for x in rnd[i]:
+            if len(c) >= len(band_set) + extra:
+                break
+            if int(x) not in c:
+                c.add(int(x))
+        rows.append(sorted(c))
+    rp = np.zeros(n + 1, dtype=np.int32)
+    rp[1:] = np.cumsum([len(r) for r in rows])
+    ci = np.concatenate([np.array(r, dtype=np.int32) for r in rows])
+    offd = normal(seed ^ 0xABCDEF, len(ci))
+    rr = np.repeat(np.arange(n), np.diff(rp))
+    diag = ci == rr
+    offd[diag] = 0.0
+    rs = np.bincount(rr, weights=np.abs(offd), minlength=n)
+    offd[diag] = 1.2 * rs
+    return rp, ci, offd
+
+
+def spmv_np(rp, ci, v, x):
+    """y = A x in numpy (generator helper: builds b = A x*)."""
+    rows = np.repeat(np.arange(len(rp) - 1), np.diff(rp))
+    return np.bincount(rows, weights=v * x[ci], minlength=len(rp) - 1)
+
+
+# ---------------------------------------------------------------- small test matrices
+def laplacian2d(g: int):
+    """5-point Laplacian (4 on the diagonal, -1 off), natural order."""
+    offs = [(0, -1, 0), (-1, 0, 0), (0, 0, 0), (1, 0, 0), (0, 1, 0)]
+    return _stencil_csr((g, g, 1), offs, lambda o, r: np.full(r.shape, 4.0 if o == 2 else -1.0))
+
+
+def random_dominant(n: int, density: float, dominance: float, seed: int):
+    """Random sparse matrix, diagonal = dominance * (row abs sum + 0.25)."""
+    coin = uniform(seed, n * n, 0.0, 1.0).reshape(n, n)
+    val = uniform(seed ^ 0x55, n * n, -1.0, 1.0).reshape(n, n)
+    mask = coin < density
+    np.fill_diagonal(mask, False)
+    dense = np.where(mask, val, 0.0)
+    rs = np.abs(dense).sum(axis=1)
+    dense[np.arange(n), np.arange(n)] = dominance * (rs + 0.25)
+    mask[np.arange(n), np.arange(n)] = True
+    rp = np.zeros(n + 1, dtype=np.int32)
+    rp[1:] = np.cumsum(mask.sum(axis=1))
+    rr, cc = np.nonzero(mask)
+    return rp, cc.astype(np.int32), dense[rr, cc].astype(np.float64)
