@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""bench.py -- int-GMRES on one B200 (BASELINE.json metric, config 2 by default).
+
+Workload (BASELINE.json configs[1]): 3D 7-point upwind convection-diffusion on
+a 128^3 grid (n = 2,097,152, nnz = 14,581,760), beta = (20,20,20), b = A x*
+with x* ~ U[-1,1) (seeded SplitMix64), alpha_a = 32, integer ILU(0), Q33.30,
+preconditioned shift preset, GMRES(30), FP64 iterative refinement to 1e-10,
+checked mode (the reference's default).  One step = one full solve from x = 0.
+
+  value     = inner int-GMRES iterations / s over K timed solves, b and x
+              resident in HBM (CUDA events on the library's stream)
+  e2e       = the same through the public API with pinned HOST b / x: the
+              H2D of b and the D2H of x are inside the timed region
+  roofline  = the dominant kernel class of an instrumented solve, algorithmic
+              bytes / its summed launch time vs measured HBM
+  cpu_baseline = the reference library (oracle/_ref, built from
+              /root/reference) on this host, one refinement cycle, 1 thread
+
+``--impl reference`` times the reference's own CPU solver on the same config
+(one refinement cycle = 30 iterations per step).  For N > 1 (torchrun) every
+rank solves its own replica of the system (the refinement loop does not shard
+at this size: see DESIGN.md), scaling = weak, value = sum over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import gen  # noqa: E402
+
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+HBM_FALLBACK_GBS = 6650.0
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ----------------------------------------------------------------- workload
+def config2(g: int = 128):
+    rp, ci, v = gen.upwind_3d(g, 20.0)
+    n = len(rp) - 1
+    xs = gen.uniform(gen.SEED_BASE ^ 2, n)
+    bh = gen.spmv_np(rp, ci, v, xs)
+    return rp, ci, v, bh
+
+
+def setup_b200(rp, ci, v, bh, alpha=32):
+    import paper_2009_07495_b200 as igm
+    t0 = time.time()
+    vals, scale = igm.row_scale(rp, ci, v, alpha)
+    b = bh / scale
+    comp, al, _ = igm.build_split(vals, alpha, 1)
+    lower, upper = igm.factorize_split_cast(rp, ci, vals)
+    setup_s = time.time() - t0
+    S = igm.SplitMatrix(rp, ci, comp, al)
+    A = igm.CsrMatrixF(rp, ci, vals)
+    F = igm.IluFactors(lower, upper)
+    return S, A, F, b, lower, upper, setup_s
+
+
+def solve_cfg(igm, tol=1e-10, m=30, max_ref=1000):
+    return igm.RefineConfig(tol=tol, max_refinements=max_ref, m=m, frac_bits=30,
+                            shifts=igm.ShiftPlan.default_preconditioned(30), s=0, checked=True)
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------- helpers
+def peaks():
+    try:
+        with open(MEASURED) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback"
+
+
+def dist_init(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    return ws, rank, local
+
+
+def max_over_ranks(x: float, ws: int) -> float:
+    if ws <= 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def algorithmic_bytes(n, nnz, nnz_l, nnz_u, m_steps_dims, W=8):
+    """SURVEY.md 8(d) per-class algorithmic bytes for one solve."""
+    spmv = (W + 4) * nnz + 4 * (n + 1) + 2 * W * n
+    ilu = (W + 4) * (nnz_l + nnz_u) + 8 * (n + 1) + 4 * W * n
+    # MGS passes at step j: pass 0 (read w, v0), j fused passes (w, v_{i-1},
+    # v_i read, w write), tail (w, v_j read, w write): (4j+5) W n
+    mgs = sum((4 * j + 5) * W * n for dims in m_steps_dims for j in range(dims))
+    steps = sum(m_steps_dims)
+    return {"spmv_int": spmv * steps, "ilu_int": ilu * steps, "mgs": mgs,
+            "vec_div": 2 * W * n * steps}
+
+
+# ----------------------------------------------------------------- reference arm
+def reference_solver():
+    from oracle import ffi
+    if ffi.ref_available():
+        return ffi.Reference(), "reference"
+    return ffi.Oracle(), "port"
+
+
+def ref_setup(B, rp, ci, v, bh, alpha=32):
+    A = B.csrf(rp, ci, v)
+    vals, scale = B.row_scale(A, alpha)
+    As = B.csrf(rp, ci, vals)
+    b = bh / scale
+    if isinstance(B, __import__("oracle.ffi", fromlist=["Reference"]).Reference):
+        comp, al, _ = B.build_split(As, alpha, 1)
+    else:
+        comp, al, _ = B.build_split(vals, alpha, 1)
+    sp = B.split(rp, ci, comp, al)
+    lo, up = B.factorize_split_cast(As)
+    il = B.ilu(lo, up)
+    return sp, As, b, il
+
+
+def ref_cycle(B, sp, As, b, il, max_ref=1):
+    from oracle.ffi import Shifts
+    x, rep = B.solve(sp, As, b, 1e-10, max_ref, 30, 30, 0, Shifts(0, 0, 0, 0, 30, 0, 0, 0), checked=True,
+                     precond=il)
+    return rep
+
+
+def cpu_sample(rp, ci, v, bh):
+    B, kind = reference_solver()
+    sp, As, b, il = ref_setup(B, rp, ci, v, bh)
+    rep = ref_cycle(B, sp, As, b, il, 1)
+    its = rep["total_inner_iterations"]
+    return {"value": its / rep["wall_time_sec"], "unit": "iters/s", "cores": 1, "kind": kind,
+            "sample": f"1 refinement cycle ({its} int-GMRES iterations) of the config-2 solve, "
+                      f"checked mode, single thread (the reference has no threading); "
+                      f"{rep['wall_time_sec']:.2f} s"}
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return 0
+    rp, ci, v, bh = config2(args.grid)
+    B, kind = reference_solver()
+    sp, As, b, il = ref_setup(B, rp, ci, v, bh)
+    for _ in range(args.warmup):
+        ref_cycle(B, sp, As, b, il, 1)
+    t = 0.0
+    its = 0
+    for _ in range(args.steps):
+        rep = ref_cycle(B, sp, As, b, il, 1)
+        t += rep["wall_time_sec"]
+        its += rep["total_inner_iterations"]
+    val = its / t
+    line = {"impl": "reference", "metric": "int-GMRES iters/s", "value": val, "unit": "iters/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic (seeded SplitMix64)",
+            "config": {"workload": f"cfg2: 3D 7-pt upwind CD {args.grid}^3, ILU(0), GMRES(30), tol 1e-10",
+                       "step": "one refinement cycle (30 iterations) of the reference solver"},
+            "cpu_baseline": {"value": val, "unit": "iters/s", "cores": 1, "kind": kind,
+                             "sample": "each step = 1 refinement cycle of the config-2 solve"},
+            "e2e": {"value": val, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------- B200 arm
+def run_b200(args, ws, rank, local):
+    import torch
+    import paper_2009_07495_b200 as igm
+    from paper_2009_07495_b200._capi import KCLASS_NAMES
+
+    dev = igm.Device(local)
+    igm.Device._default = dev
+    rp, ci, v, bh = config2(args.grid)
+    n, nnz = len(rp) - 1, int(rp[-1])
+    S, A, F, b, lower, upper, setup_s = setup_b200(rp, ci, v, bh)
+    log(f"[bench] setup {setup_s:.2f}s n={n} nnz={nnz} levels fwd/bwd {F.levels(False)}/{F.levels(True)}")
+    cfg = solve_cfg(igm)
+    stream = torch.cuda.ExternalStream(dev.stream, device=f"cuda:{local}")
+    d_b = torch.from_numpy(b).to(f"cuda:{local}")
+    d_x = torch.empty(n, dtype=torch.float64, device=f"cuda:{local}")
+    torch.cuda.synchronize()
+
+    # warm-up
+    rep = None
+    for _ in range(args.warmup):
+        _, rep = igm.solve(S, A, d_b, cfg, precond=F, x_out=d_x)
+    log(f"[bench] warm-up solve: {rep.refinements} refinements, {rep.total_inner_iterations} iterations, "
+        f"relres {rep.relres_history[-1]:.3e}, overflows {rep.overflow_total}")
+
+    # timed region (device-resident)
+    l0 = dev.launches
+    barrier(ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    its = 0
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            _, rep = igm.solve(S, A, d_b, cfg, precond=F, x_out=d_x)
+            its += rep.total_inner_iterations
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = dev.launches - l0
+    ms = e0.elapsed_time(e1)
+    barrier(ws)
+    ms = max_over_ranks(ms, ws)
+    its_all = its * ws
+    value = its_all / (ms / 1e3)
+
+    # e2e through the public API: pinned host b in, host x out, per step
+    hb = torch.from_numpy(b).pin_memory()
+    hx = torch.empty(n, dtype=torch.float64).pin_memory()
+    barrier(ws)
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_its = 0
+    f0.record(stream)
+    for _ in range(args.steps):
+        _, r2 = igm.solve(S, A, hb.numpy(), cfg, precond=F, x_out=hx.numpy())
+        e2e_its += r2.total_inner_iterations
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(f0.elapsed_time(f1), ws)
+    e2e_val = e2e_its * ws / (e2e_ms / 1e3)
+
+    # instrumented solve: per-kernel-class device time -> roofline
+    igm.lib().igm_profile_enable(1)
+    _, rp_ = igm.solve(S, A, d_b, cfg, precond=F, x_out=d_x)
+    igm.lib().igm_profile_enable(0)
+    kms = np.zeros(11)
+    kcnt = np.zeros(11, dtype=np.uint64)
+    igm.lib().igm_profile_collect(kms.ctypes.data_as(igm._capi.f64p), kcnt.ctypes.data_as(igm._capi.u64p))
+    ab = algorithmic_bytes(n, nnz, len(lower[1]), len(upper[1]), rp_.inner_dims)
+    hbm, src = peaks()
+    breakdown = {}
+    for i, name in enumerate(KCLASS_NAMES):
+        if kcnt[i]:
+            e = {"ms": round(float(kms[i]), 4), "launches": int(kcnt[i])}
+            if name in ab:
+                e["GB/s"] = round(ab[name] / (kms[i] / 1e3) / 1e9, 1)
+            breakdown[name] = e
+    bw_classes = [k for k in ("mgs", "spmv_int", "vec_div") if k in breakdown]
+    dom = max(bw_classes, key=lambda k: breakdown[k]["ms"])
+    dom_ms = breakdown[dom]["ms"] / breakdown[dom]["launches"]
+    dom_bytes = ab[dom] / breakdown[dom]["launches"]
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    top = max(breakdown, key=lambda k: breakdown[k]["ms"])
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_sample(rp, ci, v, bh)
+        except Exception as exc:  # the baseline is reported, never required
+            cpu = {"value": None, "error": str(exc)}
+
+    if rank == 0:
+        line = {
+            "metric": "int-GMRES iters/s", "value": value, "unit": "iters/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "time_to_solution_s": ms / args.steps / 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic (seeded SplitMix64 x*, b = A x*)",
+            "config": {"workload": f"cfg2: 3D 7-pt upwind CD {args.grid}^3 (n={n}, nnz={nnz}), integer ILU(0), "
+                                   f"GMRES(30), FP64 refinement to 1e-10, Q33.30, checked",
+                       "refinements": rep.refinements, "iterations_per_solve": rep.total_inner_iterations,
+                       "final_relres": rep.relres_history[-1], "overflows": rep.overflow_total,
+                       "l2": "inputs larger than L2 (matrix + ILU + basis ~ 0.9 GB)",
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
+            "gpu_launches": int(launches),
+            "e2e": {"value": e2e_val, "unit": "iters/s", "h2d_bytes_per_step": int(8 * n),
+                    "d2h_bytes_per_step": int(8 * n)},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm,
+                         "peak_source": src, "unit": "GB/s", "frac": round(achieved / hbm, 4),
+                         "traffic": None,
+                         "note": f"algorithmic bytes per launch {dom_bytes:.3e}; top device-time class: {top}"},
+            "breakdown": breakdown,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--grid", type=int, default=128)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+    ws, rank, local = dist_init(args)
+    if args.impl == "reference":
+        return run_reference(args, ws, rank)
+    return run_b200(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

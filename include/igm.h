@@ -77,6 +77,12 @@ void* igm_ctx_stream(igm_ctx* ctx);
 uint64_t igm_ctx_launch_count(igm_ctx* ctx);
 const char* igm_last_error(void);
 const char* igm_version(void);
+/* Opt-in per-kernel-class device timing (CUDA events around each launch).
+ * Classes: 0 spmv_int, 1 ilu_int, 2 ilu_fp, 3 mgs, 4 vec_div, 5 step_scalar,
+ * 6 norm2_serial, 7 residual_fp, 8 x_update, 9 encode, 10 other.
+ * collect() fills ms[11] and count[11], resets, returns the class count. */
+void igm_profile_enable(int on);
+int igm_profile_collect(double* ms, uint64_t* count);
 
 /* ---- uploads (the hot path's inputs) ----------------------------------- */
 /* SplitMatrix (split.hpp:28-37): ncomp components sharing one CSR pattern;

@@ -32,6 +32,8 @@ STATUS_NAMES = {
 KERNEL_NAMES = ["", "spmv", "precond", "dot", "axpy", "norm", "vec_div", "givens",
                 "givens_norm", "givens_div", "rot"]
 OP_NAMES = ["", "add", "sub", "mul", "shl", "div"]
+KCLASS_NAMES = ["spmv_int", "ilu_int", "ilu_fp", "mgs", "vec_div", "step_scalar", "norm2_serial",
+                "residual_fp", "x_update", "encode", "other"]
 
 
 class Shifts(C.Structure):
@@ -95,6 +97,8 @@ SIGNATURES = [
     ("igm_ctx_launch_count", C.c_uint64, [C.c_void_p]),
     ("igm_last_error", C.c_char_p, []),
     ("igm_version", C.c_char_p, []),
+    ("igm_profile_enable", None, [C.c_int]),
+    ("igm_profile_collect", C.c_int, [f64p, u64p]),
     ("igm_upload_split", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
                                    C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
     ("igm_split_free", None, [C.c_void_p]),

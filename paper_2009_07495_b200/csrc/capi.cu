@@ -636,6 +636,14 @@ void* igm_ctx_stream(igm_ctx* c) { return c ? static_cast<void*>(c->stream) : nu
 
 uint64_t igm_ctx_launch_count(igm_ctx*) { return g_launches; }
 
+void igm_profile_enable(int on) { prof_enable(on != 0); }
+
+int igm_profile_collect(double* ms, uint64_t* count) {
+  static_assert(sizeof(uint64_t) == sizeof(unsigned long long), "u64");
+  prof_collect(ms, reinterpret_cast<unsigned long long*>(count));
+  return KC_COUNT;
+}
+
 // ---- uploads
 igm_status igm_upload_split(igm_ctx* c, int n, int nnz, const int* row_ptr, const int* col_idx,
                             int ncomp, const int64_t* comp_vals, const int* alphas,

@@ -164,4 +164,19 @@ void launch_basis_norms(cudaStream_t st, long long n, int nb, int f,
 int num_sms(int device);
 extern unsigned long long g_launches;  // kernels launched by this library
 
+// Opt-in per-kernel-class timing (CUDA events around each launch on the
+// launching stream); used by bench.py for the roofline figures.
+enum KClass {
+  KC_SPMV = 0, KC_TRI_INT, KC_TRI_FP, KC_MGS, KC_VEC_DIV, KC_SCALAR, KC_NORM2, KC_RESIDUAL,
+  KC_XUPDATE, KC_ENCODE, KC_OTHER, KC_COUNT
+};
+void prof_enable(bool on);
+void prof_collect(double* ms, unsigned long long* count);  // KC_COUNT each; resets
+struct ProfScope {
+  cudaStream_t st;
+  int cls;
+  ProfScope(cudaStream_t s, int c);
+  ~ProfScope();
+};
+
 }  // namespace igm

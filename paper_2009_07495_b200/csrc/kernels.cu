@@ -12,10 +12,62 @@
 #include <climits>
 #include <type_traits>
 #include <cstdio>
+#include <vector>
 
 namespace igm {
 
 unsigned long long g_launches = 0;
+
+namespace {
+struct ProfRec {
+  int cls;
+  cudaEvent_t a, b;
+};
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_pool;
+cudaEvent_t prof_event() {
+  if (!g_pool.empty()) {
+    cudaEvent_t e = g_pool.back();
+    g_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+void prof_enable(bool on) { g_prof_on = on; }
+
+ProfScope::ProfScope(cudaStream_t s, int c) : st(s), cls(c) {
+  if (!g_prof_on) return;
+  ProfRec r{c, prof_event(), prof_event()};
+  cudaEventRecord(r.a, s);
+  g_prof.push_back(r);
+}
+
+ProfScope::~ProfScope() {
+  if (!g_prof_on || g_prof.empty()) return;
+  cudaEventRecord(g_prof.back().b, st);
+}
+
+void prof_collect(double* ms, unsigned long long* count) {
+  for (int i = 0; i < KC_COUNT; ++i) {
+    ms[i] = 0.0;
+    count[i] = 0;
+  }
+  for (auto& r : g_prof) {
+    cudaEventSynchronize(r.b);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    ms[r.cls] += t;
+    count[r.cls] += 1;
+    g_pool.push_back(r.a);
+    g_pool.push_back(r.b);
+  }
+  g_prof.clear();
+}
 
 int num_sms(int device) {
   static int cached[64] = {0};
@@ -875,6 +927,7 @@ TriArgs tri_args(const DevTri& t) {
 
 void launch_spmv_int(cudaStream_t st, const DevSplit& m, int s, const i64* v, i64* out, u64* cnt,
                      const Ctl* ctl, bool checked) {
+  ProfScope prof_(st, KC_SPMV);
   const int nt = 256;
   const int g = static_cast<int>((m.n + nt - 1) / nt > 0 ? (m.n + nt - 1) / nt : 1);
   if (checked)
@@ -886,6 +939,7 @@ void launch_spmv_int(cudaStream_t st, const DevSplit& m, int s, const i64* v, i6
 
 void launch_spmv_fp_split(cudaStream_t st, const DevSplit& m, int s, const double* x,
                           const double* b, double* y, const Ctl* ctl) {
+  ProfScope prof_(st, KC_OTHER);
   const int nt = 256;
   const int g = (m.n + nt - 1) / nt > 0 ? (m.n + nt - 1) / nt : 1;
   k_spmv_fp_split<<<g, nt, 0, st>>>(m.n, m.row_ptr, m.col_idx, m.vals, m.nnz, m.alphas, s, x, b, y, ctl);
@@ -894,6 +948,7 @@ void launch_spmv_fp_split(cudaStream_t st, const DevSplit& m, int s, const doubl
 
 void launch_residual(cudaStream_t st, const DevCsrf& a, const double* x, const double* b,
                      double* r, Ctl* ctl, bool track_max) {
+  ProfScope prof_(st, KC_RESIDUAL);
   const int nt = 256;
   const int g = (a.n + nt - 1) / nt > 0 ? (a.n + nt - 1) / nt : 1;
   k_residual<<<g, nt, 0, st>>>(a.n, a.row_ptr, a.col_idx, a.vals, x, b, r, ctl, track_max ? 1 : 0);
@@ -901,23 +956,27 @@ void launch_residual(cudaStream_t st, const DevCsrf& a, const double* x, const d
 }
 
 void launch_gamma(cudaStream_t st, long long n, const double* r, Ctl* ctl) {
+  ProfScope prof_(st, KC_OTHER);
   k_gamma<<<grid_for(n, 256), 256, 0, st>>>(n, r, ctl);
   LAUNCH_CHECK();
 }
 
 void launch_scale_div(cudaStream_t st, long long n, const double* r, double* out, const Ctl* ctl) {
+  ProfScope prof_(st, KC_OTHER);
   k_scale_div<<<grid_for(n, 256), 256, 0, st>>>(n, r, out, ctl);
   LAUNCH_CHECK();
 }
 
 void launch_norm2_serial(cudaStream_t st, long long n, const double* v, double* out, Ctl* ctl,
                          int mode) {
+  ProfScope prof_(st, KC_NORM2);
   k_norm2_serial<<<1, 256, 0, st>>>(n, v, nullptr, 1.0, out, ctl, mode, 0);
   LAUNCH_CHECK();
 }
 
 void launch_basis_norms(cudaStream_t st, long long n, int nb, int f, const i64* basis, double* tmp,
                         double* out, Ctl* ctl) {
+  ProfScope prof_(st, KC_NORM2);
   (void)tmp;
   for (int k = 0; k < nb; ++k) {
     k_norm2_serial<<<1, 256, 0, st>>>(n, nullptr, basis + static_cast<long long>(k) * n,
@@ -927,6 +986,7 @@ void launch_basis_norms(cudaStream_t st, long long n, int nb, int f, const i64* 
 }
 
 void launch_encode(cudaStream_t st, long long n, const double* r0, i64* v0, int f, Ctl* ctl) {
+  ProfScope prof_(st, KC_ENCODE);
   k_encode<<<grid_for(n, 256), 256, 0, st>>>(n, r0, v0, f, ctl);
   LAUNCH_CHECK();
 }
@@ -934,6 +994,7 @@ void launch_encode(cudaStream_t st, long long n, const double* r0, i64* v0, int 
 void launch_mgs_pass(cudaStream_t st, long long n, int mode, i64* w, const i64* vprev,
                      const i64* vcur, const u64* hacc, u64* acc_out, u64* abs_out, int f,
                      ShiftsD sh, u64* cnt_axpy, u64* cnt_red, const Ctl* ctl, bool checked) {
+  ProfScope prof_(st, KC_MGS);
   const int nt = 512;
   const int g = grid_for(n, nt) > 2 * num_sms(0) ? 2 * num_sms(0) : grid_for(n, nt);
 #define MGS_CASE(MD)                                                                               \
@@ -955,6 +1016,7 @@ void launch_mgs_pass(cudaStream_t st, long long n, int mode, i64* w, const i64* 
 
 void launch_fx_red(cudaStream_t st, long long n, int mode, const i64* v, const i64* w, int b1,
                    int b2, u64* acc, u64* abs_out, u64* cnt, bool checked) {
+  ProfScope prof_(st, KC_MGS);
   const int nt = 512;
   const int g = grid_for(n, nt) > 2 * num_sms(0) ? 2 * num_sms(0) : grid_for(n, nt);
   if (checked)
@@ -966,6 +1028,7 @@ void launch_fx_red(cudaStream_t st, long long n, int mode, const i64* v, const i
 
 void launch_axpy_only(cudaStream_t st, long long n, i64* w, i64 h, const i64* v, int f, int b1,
                       u64* cnt, bool checked) {
+  ProfScope prof_(st, KC_MGS);
   const int nt = 512;
   const int g = grid_for(n, nt);
   if (checked)
@@ -977,6 +1040,7 @@ void launch_axpy_only(cudaStream_t st, long long n, i64* w, i64 h, const i64* v,
 
 void launch_vec_div(cudaStream_t st, long long n, const i64* w, i64* out, int f, ShiftsD sh,
                     u64* cnt, const Ctl* ctl, bool checked) {
+  ProfScope prof_(st, KC_VEC_DIV);
   const int nt = 512;
   const int g = grid_for(n, nt);
   if (checked)
@@ -990,24 +1054,28 @@ void launch_step_scalar(cudaStream_t st, int j, int f, ShiftsD sh, const u64* ac
                         const u64* abs_col, const u64* nacc, const u64* nabs, i64* hess, int ld,
                         i64* g, i64* cs, i64* sn, i64* gabs, const i64* w, u64* cnt_step, Ctl* ctl,
                         bool checked) {
+  ProfScope prof_(st, KC_SCALAR);
   k_step_scalar<<<1, 1, 0, st>>>(j, f, sh, acc_col, abs_col, nacc, nabs, hess, ld, g, cs, sn, gabs,
                                  w, cnt_step, ctl, checked ? 1 : 0);
   LAUNCH_CHECK();
 }
 
 void launch_cycle_init(cudaStream_t st, Ctl* ctl, i64* g, int f) {
+  ProfScope prof_(st, KC_OTHER);
   k_cycle_init<<<1, 1, 0, st>>>(ctl, g, f);
   LAUNCH_CHECK();
 }
 
 void launch_cycle_finish(cudaStream_t st, int m, int f, const i64* hess, const i64* g, double* y,
                          double* wts, Ctl* ctl) {
+  ProfScope prof_(st, KC_OTHER);
   k_cycle_finish<<<1, 1, 0, st>>>(m, f, hess, g, y, wts, ctl);
   LAUNCH_CHECK();
 }
 
 void launch_xupdate(cudaStream_t st, long long n, int m, int f, const i64* basis,
                     const double* wts, const double* x0, double* x, const Ctl* ctl, int mode) {
+  ProfScope prof_(st, KC_XUPDATE);
   (void)m;
   k_xupdate<<<grid_for(n, 256), 256, 0, st>>>(n, f, basis, wts, x0, x, ctl, mode);
   LAUNCH_CHECK();
@@ -1034,6 +1102,7 @@ void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* 
   cudaMemsetAsync(t.ticket, 0, sizeof(int), st);
   cudaMemsetAsync(t.prog, 0xff, sizeof(int) * t.ntiles, st);
   const TriArgs a = tri_args(t);
+  ProfScope prof_(st, KC_TRI_INT);
   if (backward) {
     if (checked) k_tri<i64, true, true><<<t.ntiles, 256, sm, st>>>(a, y, out, cnt, ctl, nullptr);
     else k_tri<i64, true, false><<<t.ntiles, 256, sm, st>>>(a, y, out, cnt, ctl, nullptr);
@@ -1052,6 +1121,7 @@ void launch_tri_fp(cudaStream_t st, const DevTri& t, bool backward, const double
   cudaMemsetAsync(t.ticket, 0, sizeof(int), st);
   cudaMemsetAsync(t.prog, 0xff, sizeof(int) * t.ntiles, st);
   const TriArgs a = tri_args(t);
+  ProfScope prof_(st, KC_TRI_FP);
   if (backward)
     k_tri<double, true, false><<<t.ntiles, 256, sm, st>>>(a, y, out, nullptr, ctl, prescale);
   else
