@@ -16,11 +16,11 @@ $(BUILD)/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(BUILD)/shim.o: $(PKG)/csrc/shim.cpp $(HDRS)
+$(BUILD)/%.o: $(PKG)/csrc/%.cpp $(HDRS) $(PKG)/csrc/schedule.hpp
 	@mkdir -p $(BUILD)
 	g++ $(CXXFLAGS) -I/usr/local/cuda/include -c $< -o $@
 
-$(LIB): $(BUILD)/kernels.o $(BUILD)/capi.o $(BUILD)/shim.o
+$(LIB): $(BUILD)/kernels.o $(BUILD)/capi.o $(BUILD)/shim.o $(BUILD)/schedule.o
 	$(NVCC) $(ARCH) -shared -o $@ $^
 
 oracle:

@@ -107,6 +107,11 @@ igm_status igm_upload_ilu(igm_ctx* ctx, int n, const int* l_row_ptr,
 void igm_ilu_free(igm_ilu* f);
 /* levels of the forward / backward substitution DAGs (diagnostics) */
 int igm_ilu_levels(const igm_ilu* f, int backward);
+/* schedule diagnostics: ntiles, nseg, nlevels, maxdeps, grid x/y/z,
+ * brick (x*1e6 + y*1e3 + z) */
+void igm_ilu_schedule_info(const igm_ilu* f, int backward, int* out8);
+/* debug: per-segment phase timestamps of one ILU tile (4 u64 per segment) */
+void igm_debug_tri_trace(int tile, unsigned long long* device_buf);
 
 /* ---- primitives (parity entry points) ---------------------------------- */
 /* replaces intgmres::spmv (split.hpp:48-49, split.cpp:137-157) */

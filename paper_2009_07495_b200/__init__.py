@@ -201,6 +201,13 @@ class IluFactors:
     def levels(self, backward: bool = False) -> int:
         return int(lib().igm_ilu_levels(self.h, 1 if backward else 0))
 
+    def schedule_info(self, backward: bool = False) -> dict:
+        out = (C.c_int32 * 8)()
+        lib().igm_ilu_schedule_info(self.h, 1 if backward else 0, out)
+        b = out[7]
+        return {"tiles": out[0], "segments": out[1], "levels": out[2], "max_deps": out[3],
+                "grid": (out[4], out[5], out[6]), "brick": (b // 1000000, (b // 1000) % 1000, b % 1000)}
+
     def __del__(self):
         try:
             lib().igm_ilu_free(self.h)

@@ -108,6 +108,8 @@ SIGNATURES = [
     ("igm_upload_ilu", C.c_int, [C.c_void_p, C.c_int] + [C.c_void_p] * 8 + [C.POINTER(C.c_void_p)]),
     ("igm_ilu_free", None, [C.c_void_p]),
     ("igm_ilu_levels", C.c_int, [C.c_void_p, C.c_int]),
+    ("igm_ilu_schedule_info", None, [C.c_void_p, C.c_int, i32p]),
+    ("igm_debug_tri_trace", None, [C.c_int, C.c_void_p]),
     ("igm_spmv", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.POINTER(Trace)]),
     ("igm_apply_inverse", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(Trace)]),
     ("igm_apply_inverse_fp", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),

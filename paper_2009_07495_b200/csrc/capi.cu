@@ -7,6 +7,7 @@
 // (run_cycle) or once per refinement (solve), exactly where the reference's
 // outer loop needs a scalar decision (refine.cpp:52-55, 85).
 #include "igm_internal.cuh"
+#include "schedule.hpp"
 
 #include <algorithm>
 #include <chrono>
@@ -81,8 +82,8 @@ bool is_device_ptr(const void* p) {
 template <class T>
 T* dalloc(size_t count) {
   void* p = nullptr;
-  if (count == 0) count = 1;
-  ck(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+  // +64 bytes: bulk L2 prefetches round ranges up to 16-byte granules
+  ck(cudaMalloc(&p, count * sizeof(T) + 64), "cudaMalloc");
   return static_cast<T*>(p);
 }
 
@@ -325,106 +326,58 @@ int env_int(const char* name, int dflt) {
 
 void build_tri(igm_ctx* c, DevTri& t, int n, const int* rp, const int* ci, const i64* vals,
                const int* dpos, bool upper) {
-  // strip the diagonal and the structurally-void entries (a "lower" entry
-  // with j > i multiplies a zero-initialised slot in ilu.cpp:126-135, an
-  // "upper" one with j < i likewise), keep CSR order
-  std::vector<int> orp(n + 1, 0), oci;
-  std::vector<i64> ov, dg(n);
-  std::vector<u64> mg(n);
-  std::vector<int> info(n);
-  oci.reserve(rp[n]);
-  ov.reserve(rp[n]);
-  for (int i = 0; i < n; ++i) {
-    for (int k = rp[i]; k < rp[i + 1]; ++k) {
-      const int j = ci[k];
-      if (j == i) continue;
-      if (j < 0 || j >= n) fail(IGM_INVALID_ARGUMENT, "upload_ilu: column index out of range");
-      if (upper ? (j < i) : (j > i)) continue;
-      oci.push_back(j);
-      ov.push_back(vals[k]);
-    }
-    orp[i + 1] = static_cast<int>(oci.size());
-    const int dp = dpos[i];
-    if (dp < 0 || dp >= rp[n]) fail(IGM_INVALID_ARGUMENT, "upload_ilu: diagonal position out of range");
-    const i64 d = vals[dp];
-    if (d == 0) fail(IGM_INVALID_ARGUMENT, "upload_ilu: zero diagonal entry");
-    dg[i] = d;
-    const SDivMagic gm = make_sdiv(d);
-    mg[i] = gm.u.m;
-    info[i] = gm.u.sh1 | (gm.u.sh2 << 1) | (gm.den_neg << 8) | (gm.den_is_m1 << 9);
+  TriSchedule S;
+  try {
+    S = build_tri_schedule(n, rp, ci, vals, dpos, upper, num_sms(c->device), env_int("IGM_TRI_TILE", 0));
+  } catch (const std::invalid_argument& e) {
+    fail(IGM_INVALID_ARGUMENT, e.what());
+  } catch (const std::logic_error& e) {
+    fail(IGM_LOGIC_ERROR, e.what());
   }
-  // DAG levels
-  std::vector<int> lev(n, 0);
-  int maxlev = 0;
-  if (!upper) {
-    for (int i = 0; i < n; ++i) {
-      int l = 0;
-      for (int k = orp[i]; k < orp[i + 1]; ++k) l = std::max(l, lev[oci[k]] + 1);
-      lev[i] = l;
-      maxlev = std::max(maxlev, l);
-    }
-  } else {
-    for (int i = n - 1; i >= 0; --i) {
-      int l = 0;
-      for (int k = orp[i]; k < orp[i + 1]; ++k) l = std::max(l, lev[oci[k]] + 1);
-      lev[i] = l;
-      maxlev = std::max(maxlev, l);
-    }
-  }
-  // tiles: contiguous row blocks sized to fill the GPU, <= 16384 rows so a
-  // tile's values fit in shared memory (128 KB as int64)
-  const int nsm = num_sms(c->device);
-  int T = env_int("IGM_TRI_TILE", 0);
-  if (T <= 0) T = std::min(16384, std::max(32, (n + nsm - 1) / std::max(1, nsm)));
-  T = std::min(T, 16384);
-  if (n == 0) T = 1;
-  const int ntiles = n > 0 ? (n + T - 1) / T : 1;
-  // per tile: rows bucketed by level (stable), one segment per level
-  std::vector<int> tile_seg(ntiles + 1, 0), seg_level, sr{0}, perm(std::max(n, 1));
-  std::vector<std::pair<int, int>> buf;
-  for (int tl = 0; tl < ntiles && n > 0; ++tl) {
-    const int r0 = tl * T, r1 = std::min(n, r0 + T);
-    buf.clear();
-    for (int i = r0; i < r1; ++i) buf.emplace_back(lev[i], i);
-    std::sort(buf.begin(), buf.end());
-    for (size_t q = 0; q < buf.size(); ++q) {
-      if (q == 0 || buf[q].first != buf[q - 1].first) {
-        if (q) sr.push_back(static_cast<int>(r0 + q));
-        seg_level.push_back(buf[q].first);
-      }
-      perm[r0 + q] = buf[q].second;
-    }
-    sr.push_back(r1);
-    tile_seg[tl + 1] = static_cast<int>(seg_level.size());
-  }
-  if (seg_level.empty()) seg_level.push_back(0);
-
   cudaStream_t st = c->stream;
   t.n = n;
-  t.nnz_off = static_cast<int>(oci.size());
-  t.rp = dupload(orp.data(), orp.size(), st);
-  t.ci = dupload(oci.data(), oci.size(), st);
-  t.vals = dupload(ov.data(), ov.size(), st);
-  t.diag = dupload(dg.data(), dg.size(), st);
-  t.dmag = dupload(mg.data(), mg.size(), st);
-  t.dinfo = dupload(info.data(), info.size(), st);
-  t.tile_rows = T;
-  t.ntiles = ntiles;
-  t.nseg = static_cast<int>(seg_level.size());
-  t.nlevels = n > 0 ? maxlev + 1 : 0;
-  t.tile_seg = dupload(tile_seg.data(), tile_seg.size(), st);
-  t.seg_level = dupload(seg_level.data(), seg_level.size(), st);
-  t.seg_rows = dupload(sr.data(), sr.size(), st);
-  t.perm = dupload(perm.data(), perm.size(), st);
-  t.prog = dalloc<int>(ntiles);
+  t.maxd = S.maxd;
+  t.stride = S.stride;
+  t.ntiles = S.ntiles;
+  t.nseg = static_cast<int>(S.seg_level.size());
+  t.nlevels = S.nlevels;
+  t.tile_cap = S.tile_cap;
+  for (int q = 0; q < S.ntiles; ++q)
+    t.max_tile_segs = std::max(t.max_tile_segs, S.tile_seg[q + 1] - S.tile_seg[q]);
+  for (int d = 0; d < 3; ++d) {
+    t.grid[d] = S.grid[d];
+    t.brick[d] = S.brick[d];
+  }
+  t.tile_pbase = dupload(S.tile_pbase.data(), S.tile_pbase.size(), st);
+  t.tile_seg = dupload(S.tile_seg.data(), S.tile_seg.size(), st);
+  t.seg_level = dupload(S.seg_level.data(), S.seg_level.size(), st);
+  t.seg_rows = dupload(S.seg_rows.data(), S.seg_rows.size(), st);
+  t.seg_wptr = dupload(S.seg_wptr.data(), S.seg_wptr.size(), st);
+  t.seg_wt = dupload(S.seg_wt.data(), S.seg_wt.size(), st);
+  t.p_row = dupload(S.p_row.data(), S.p_row.size(), st);
+  t.p_nd = dupload(S.p_nd.data(), S.p_nd.size(), st);
+  t.p_dep = dupload(S.p_dep.data(), S.p_dep.size(), st);
+  t.p_val = dupload(S.p_val.data(), S.p_val.size(), st);
+  t.p_xrp = dupload(S.p_xrp.data(), S.p_xrp.size(), st);
+  t.p_xdep = dupload(S.p_xdep.data(), S.p_xdep.size(), st);
+  t.p_xval = dupload(S.p_xval.data(), S.p_xval.size(), st);
+  t.p_mag = dupload(S.p_mag.data(), S.p_mag.size(), st);
+  t.p_info = dupload(S.p_info.data(), S.p_info.size(), st);
+  t.p_diag = dupload(S.p_diag.data(), S.p_diag.size(), st);
+  t.prog = dalloc<int>(S.ntiles);
   t.ticket = dalloc<int>(1);
   ck(cudaStreamSynchronize(st), "upload_ilu sync");
 }
 
 void free_tri(DevTri& t) {
-  dfree(t.rp); dfree(t.ci); dfree(t.vals); dfree(t.diag); dfree(t.dmag); dfree(t.dinfo);
-  dfree(t.tile_seg); dfree(t.seg_level); dfree(t.seg_rows); dfree(t.perm); dfree(t.prog);
-  dfree(t.ticket);
+  for (void* p : {static_cast<void*>(t.tile_pbase), static_cast<void*>(t.tile_seg),
+                  static_cast<void*>(t.seg_level), static_cast<void*>(t.seg_rows),
+                  static_cast<void*>(t.seg_wptr), static_cast<void*>(t.seg_wt),
+                  static_cast<void*>(t.p_row), static_cast<void*>(t.p_nd), static_cast<void*>(t.p_dep),
+                  static_cast<void*>(t.p_val), static_cast<void*>(t.p_xrp), static_cast<void*>(t.p_xdep),
+                  static_cast<void*>(t.p_xval), static_cast<void*>(t.p_mag), static_cast<void*>(t.p_info),
+                  static_cast<void*>(t.p_diag), static_cast<void*>(t.prog), static_cast<void*>(t.ticket)})
+    dfree(p);
   t = DevTri{};
 }
 
@@ -638,6 +591,11 @@ uint64_t igm_ctx_launch_count(igm_ctx*) { return g_launches; }
 
 void igm_profile_enable(int on) { prof_enable(on != 0); }
 
+// debug hook: per-segment phase timestamps of one ILU tile (4 u64 per segment)
+void igm_debug_tri_trace(int tile, unsigned long long* device_buf) {
+  igm::tri_trace_setup(tile, device_buf);
+}
+
 int igm_profile_collect(double* ms, uint64_t* count) {
   static_assert(sizeof(uint64_t) == sizeof(unsigned long long), "u64");
   prof_collect(ms, reinterpret_cast<unsigned long long*>(count));
@@ -735,6 +693,13 @@ void igm_ilu_free(igm_ilu* f) {
 
 int igm_ilu_levels(const igm_ilu* f, int backward) {
   return f ? (backward ? f->upper.nlevels : f->lower.nlevels) : 0;
+}
+
+void igm_ilu_schedule_info(const igm_ilu* f, int backward, int* out8) {
+  const DevTri& t = backward ? f->upper : f->lower;
+  const int v[8] = {t.ntiles, t.nseg, t.nlevels, t.maxd, t.grid[0], t.grid[1], t.grid[2],
+                    t.brick[0] * 1000000 + t.brick[1] * 1000 + t.brick[2]};
+  for (int i = 0; i < 8; ++i) out8[i] = v[i];
 }
 
 // ---- primitives

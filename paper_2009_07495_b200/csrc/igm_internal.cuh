@@ -74,23 +74,19 @@ struct DevCsrf {
   int device = 0;
 };
 
-// One triangular factor prepared for the wavefront kernels.
+// One triangular factor prepared for the wavefront kernels (see
+// schedule.hpp): records in schedule order (tile-major, level, row).
 struct DevTri {
-  int n = 0, nnz_off = 0;
-  int* rp = nullptr;       // n+1, off-diagonal entries only
-  int* ci = nullptr;
-  i64* vals = nullptr;
-  i64* diag = nullptr;     // n raw diagonal
-  u64* dmag = nullptr;     // n round-up reciprocals of |diag|
-  int* dinfo = nullptr;    // n: sh1 | sh2 << 1 | neg << 8 | (diag == -1) << 9
-  // schedule
-  int tile_rows = 0, ntiles = 0, nseg = 0, nlevels = 0;
-  int* tile_seg = nullptr; // ntiles+1
-  int* seg_level = nullptr;// nseg
-  int* seg_rows = nullptr; // nseg+1 into perm
-  int* perm = nullptr;     // n
-  int* prog = nullptr;     // ntiles progress words
-  int* ticket = nullptr;   // 1
+  int n = 0, maxd = 0, stride = 4, ntiles = 0, nseg = 0, nlevels = 0, tile_cap = 0, max_tile_segs = 0;
+  int grid[3] = {0, 0, 0}, brick[3] = {0, 0, 0};
+  int *tile_pbase = nullptr, *tile_seg = nullptr, *seg_level = nullptr, *seg_rows = nullptr;
+  int *seg_wptr = nullptr, *seg_wt = nullptr;
+  int *p_row = nullptr, *p_nd = nullptr, *p_dep = nullptr, *p_xrp = nullptr, *p_xdep = nullptr;
+  i64 *p_val = nullptr, *p_xval = nullptr, *p_diag = nullptr;
+  u64* p_mag = nullptr;
+  int* p_info = nullptr;
+  int* prog = nullptr;    // ntiles progress words
+  int* ticket = nullptr;  // 1
 };
 
 struct DevIlu {
@@ -162,6 +158,7 @@ void launch_basis_norms(cudaStream_t st, long long n, int nb, int f,
                         const i64* basis, double* tmp, double* out, Ctl* ctl);
 
 int num_sms(int device);
+void tri_trace_setup(int tile, unsigned long long* buf);
 extern unsigned long long g_launches;  // kernels launched by this library
 
 // Opt-in per-kernel-class timing (CUDA events around each launch on the

@@ -92,6 +92,16 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   return v;
 }
 
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void red_release_max(int* p, int v) {
+  asm volatile("red.release.gpu.global.max.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -791,128 +801,317 @@ __global__ void __launch_bounds__(256) k_xupdate(long long n, int f, const i64* 
 // its tile's rows level by level keeping the tile's results in shared
 // memory, and publishes per-tile progress ("all rows with level <= p are
 // final") with release/acquire.  Cross-tile dependencies wait on that
-// progress word and read the value through L2.  Per row the arithmetic is
-// the reference's: CSR order, wrapping mul/sub, truncating division by the
-// raw diagonal (exact reciprocal), or the same in FP64 on the integer
-// factors with no contraction.
+// progress word and read the value through L2.
+//
+// Row records are stored in schedule order (upload-time permutation), so a
+// segment's records are contiguous and coalesced; the whole tile's records
+// are bulk-prefetched into L2 when the CTA starts, and each thread keeps the
+// NEXT segment's record in registers while it works on the current one, so
+// the per-level critical path is only: wait -> dependency values -> multiply,
+// subtract -> exact reciprocal division -> store.
+//
+// Per row the arithmetic is the reference's: CSR order, wrapping mul/sub,
+// truncating division by the raw diagonal (exact reciprocal), or the same in
+// FP64 on the integer factors with no contraction.
 struct TriArgs {
-  int n, tile_rows, ntiles;
-  const int* rp;
-  const int* ci;
-  const i64* vals;
-  const i64* diag;
-  const u64* dmag;
-  const int* dinfo;
+  int n, ntiles;
+  const int* tile_pbase;  // first schedule slot of each tile
   const int* tile_seg;
   const int* seg_level;
   const int* seg_rows;
-  const int* perm;
+  const int* seg_wptr;    // external producer tiles per segment
+  const int* seg_wt;
+  const int* p_row;       // row id per slot
+  const int* p_nd;        // dependency count per slot
+  const int* p_dep;       // slot*stride: >= 0 tile-local slot, < 0 ~global row
+  const i64* p_val;
+  const int* p_xrp;       // dependencies beyond stride (CSR)
+  const int* p_xdep;
+  const i64* p_xval;
+  const u64* p_mag;       // exact reciprocal of |diag| per slot
+  const int* p_info;      // sh1 | sh2 << 1 | neg << 8 | (diag == -1) << 9
+  const i64* p_diag;
   int* prog;
   int* ticket;
 };
 
-template <typename T, bool BACKWARD, bool CHECKED>
-__global__ void __launch_bounds__(256) k_tri(TriArgs a, const T* __restrict__ y, T* out,
-                                             u64* cnt, const Ctl* ctl,
-                                             const double* prescale) {
+template <int MAXD>
+struct RowRec {
+  int row, nd, slot, xb;
+  u64 mag;
+  int info;
+  i64 diag;
+  int ci[MAXD];
+  i64 v[MAXD];
+};
+
+// every address is a function of p alone: the loads issue back to back and
+// only the consumer (next segment) waits for them
+template <int MAXD, bool FP>
+__device__ __forceinline__ void load_rec(const TriArgs& a, int p, int pb, RowRec<MAXD>& r) {
+  r.row = __ldg(a.p_row + p);
+  r.nd = __ldg(a.p_nd + p);
+  r.slot = p - pb;
+  r.xb = __ldg(a.p_xrp + p);
+  if (FP) {
+    r.diag = __ldg(a.p_diag + p);
+  } else {
+    r.mag = __ldg(a.p_mag + p);
+    r.info = __ldg(a.p_info + p);
+  }
+#pragma unroll
+  for (int d = 0; d < MAXD; ++d) {
+    r.ci[d] = __ldg(a.p_dep + static_cast<size_t>(p) * MAXD + d);
+    r.v[d] = __ldg(a.p_val + static_cast<size_t>(p) * MAXD + d);
+  }
+}
+
+__device__ __forceinline__ void l2_prefetch(const void* p, size_t bytes) {
+  // bulk L2 prefetch of [p, p+bytes), 16-byte granular (allocations are padded)
+  const size_t a = reinterpret_cast<size_t>(p) & ~size_t(15);
+  size_t e = (reinterpret_cast<size_t>(p) + bytes + 15) & ~size_t(15);
+  for (size_t q = a; q < e; q += (1u << 20)) {
+    const unsigned len = static_cast<unsigned>(min(e - q, static_cast<size_t>(1u << 20)));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(q), "r"(len) : "memory");
+  }
+}
+
+template <typename T, bool CHECKED>
+struct TriAcc {
+  u64 nmul = 0, nsub = 0, ndiv = 0;
+};
+
+// one dependency term: acc -= l_ij * z_j (value from smem or, cross-tile,
+// from L2 after the segment's poller acquired the producer's progress)
+template <typename T, bool CHECKED>
+__device__ __forceinline__ void tri_term(int c, i64 lv, const T* out, const T* zt, T& acc,
+                                         TriAcc<T, CHECKED>& st) {
+  const T zj = c >= 0 ? zt[c] : __ldcg(out + ~c);
+  if constexpr (std::is_same<T, double>::value) {
+    acc = __dsub_rn(acc, __dmul_rn(__ll2double_rn(lv), zj));
+  } else {
+    const i64 pr = wmul(lv, zj);
+    if (CHECKED) {
+      st.nmul += mul_ovf(lv, zj);
+      st.nsub += sub_ovf(acc, pr);
+    }
+    acc = wsub(acc, pr);
+  }
+}
+
+template <typename T, bool CHECKED, int MAXD>
+__device__ __forceinline__ void tri_row(const TriArgs& a, const RowRec<MAXD>& r, T acc, T* out,
+                                        T* zt, TriAcc<T, CHECKED>& st) {
+#pragma unroll
+  for (int d = 0; d < MAXD; ++d)
+    if (d < r.nd) tri_term<T, CHECKED>(r.ci[d], r.v[d], out, zt, acc, st);
+  for (int d = MAXD; d < r.nd; ++d)
+    tri_term<T, CHECKED>(__ldg(a.p_xdep + r.xb + d - MAXD), __ldg(a.p_xval + r.xb + d - MAXD), out, zt,
+                         acc, st);
+  T z;
+  if constexpr (std::is_same<T, double>::value) {
+    z = __ddiv_rn(acc, __ll2double_rn(r.diag));
+  } else {
+    SDivMagic gm;
+    gm.u.m = r.mag;
+    gm.u.sh1 = r.info & 1;
+    gm.u.sh2 = (r.info >> 1) & 127;
+    gm.den_neg = (r.info >> 8) & 1;
+    gm.den_is_m1 = (r.info >> 9) & 1;
+    if (CHECKED) st.ndiv += sdiv_ovf(acc, gm);
+    z = sdiv(acc, gm);
+  }
+  zt[r.slot] = z;
+  out[r.row] = z;
+}
+
+template <typename T>
+__device__ __forceinline__ T tri_load_y(const T* __restrict__ y, int row, bool scaled, double gamma) {
+  if constexpr (std::is_same<T, double>::value) return scaled ? __ddiv_rn(y[row], gamma) : y[row];
+  else return y[row];
+}
+
+// debug: per-segment phase timestamps of one tile (igm_debug_tri_trace)
+__device__ unsigned long long* g_tri_ts = nullptr;
+__device__ int g_tri_ts_tile = -1;
+__device__ __forceinline__ unsigned long long gtime() {
+  // SM cycle counter (the global timer ticks at ~1 us on this part); only
+  // differences within one CTA are meaningful
+  return clock64();
+}
+
+__device__ __forceinline__ void bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// Warp-specialised wavefront CTA: 8 compute warps (one row per thread per
+// level; wider levels loop), warp 8 = poller (acquires producer progress for
+// the NEXT level while the compute warps work), warps 9..12 = publishers,
+// round-robin over levels (a gpu-scope release costs ~1.5 us; with four of
+// them in flight it no longer paces the level loop).
+//   barrier 1       "level q may start": compute sync + poller sync + the
+//                   publisher of level q-1 arrives
+//   barrier 2+(q%4) "level q done":      compute arrive + publisher q%4 sync
+// Progress words only grow (red.release.max), so releases that complete out
+// of order cannot regress them.
+constexpr int kTriCompute = 256;
+constexpr int kTriPub = 4;
+constexpr int kTriThreads = kTriCompute + 32 + 32 * kTriPub;
+constexpr int kTriBar1 = kTriCompute + 64;  // compute + poller + one publisher warp
+
+template <typename T, bool BACKWARD, bool CHECKED, int MAXD>
+__global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restrict__ y, T* out,
+                                                     u64* cnt, const Ctl* ctl,
+                                                     const double* prescale, int seg_cap) {
+  constexpr bool FP = std::is_same<T, double>::value;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* zt = reinterpret_cast<T*>(smem_raw);
   __shared__ int s_tile;
+  __shared__ int s_seen_tile[16], s_seen_prog[16];
   if (cycle_over(ctl)) return;
   if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1);
-  __syncthreads();
-  const int k = s_tile;
-  const int tile = BACKWARD ? a.ntiles - 1 - k : k;
-  const int r0 = tile * a.tile_rows;
-  const int r1 = min(a.n, r0 + a.tile_rows);
-  const int sb = a.tile_seg[tile], se = a.tile_seg[tile + 1];
-  if (threadIdx.x == 0) st_release(a.prog + tile, a.seg_level[sb] - 1);
-  double inv_scale = 0.0;
-  if (prescale) inv_scale = __longlong_as_double(*reinterpret_cast<const long long*>(prescale));
-  u64 nmul = 0, nsub = 0, ndiv = 0;
-  for (int sgi = sb; sgi < se; ++sgi) {
-    const int lev = a.seg_level[sgi];
-    const int pe = a.seg_rows[sgi + 1];
-    for (int p = a.seg_rows[sgi] + threadIdx.x; p < pe; p += blockDim.x) {
-      const int i = a.perm[p];
-      T acc;
-      if constexpr (sizeof(T) == 8 && std::is_same<T, double>::value) {
-        acc = prescale ? __ddiv_rn(y[i], inv_scale) : y[i];
-      } else {
-        acc = y[i];
-      }
-      int waited = -1;
-      const int ke = a.rp[i + 1];
-      for (int kk = a.rp[i]; kk < ke; ++kk) {
-        const int jc = a.ci[kk];
-        const i64 lv = a.vals[kk];
-        T zj;
-        if (jc >= r0 && jc < r1) {
-          zj = zt[jc - r0];
-        } else {
-          const int tj = jc / a.tile_rows;
-          if (tj != waited) {
-            while (ld_acquire(a.prog + tj) < lev - 1) {
-            }
-            waited = tj;
-          }
-          zj = __ldcg(out + jc);
-        }
-        if constexpr (std::is_same<T, double>::value) {
-          acc = __dsub_rn(acc, __dmul_rn(__ll2double_rn(lv), zj));
-        } else {
-          const i64 pr = wmul(lv, zj);
-          if (CHECKED) {
-            nmul += mul_ovf(lv, zj);
-            nsub += sub_ovf(acc, pr);
-          }
-          acc = wsub(acc, pr);
-        }
-      }
-      T z;
-      if constexpr (std::is_same<T, double>::value) {
-        z = __ddiv_rn(acc, __ll2double_rn(a.diag[i]));
-      } else {
-        const int info = a.dinfo[i];
-        SDivMagic gm;
-        gm.u.m = a.dmag[i];
-        gm.u.sh1 = info & 1;
-        gm.u.sh2 = (info >> 1) & 127;
-        gm.den_neg = (info >> 8) & 1;
-        gm.den_is_m1 = (info >> 9) & 1;
-        if (CHECKED) ndiv += sdiv_ovf(acc, gm);
-        z = sdiv(acc, gm);
-      }
-      zt[i - r0] = z;
-      out[i] = z;
-    }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0)
-      st_release(a.prog + tile, sgi + 1 < se ? a.seg_level[sgi + 1] - 1 : INT_MAX);
+  if (threadIdx.x < 16) {
+    s_seen_tile[threadIdx.x] = -1;
+    s_seen_prog[threadIdx.x] = INT_MIN;
   }
-  if (CHECKED && !std::is_same<T, double>::value) {
-    bump(cnt, OP_MUL, nmul);
-    bump(cnt, OP_SUB, nsub);
-    bump(cnt, OP_DIV, ndiv);
+  __syncthreads();
+  const int tile = BACKWARD ? a.ntiles - 1 - s_tile : s_tile;
+  const int pb = __ldg(a.tile_pbase + tile), pe = __ldg(a.tile_pbase + tile + 1);
+  const int sb = __ldg(a.tile_seg + tile), se = __ldg(a.tile_seg + tile + 1);
+  const int nsg = se - sb;
+  // shared: tile values | segment first-slot table | segment levels
+  T* zt = reinterpret_cast<T*>(smem_raw);
+  int* s_rows = reinterpret_cast<int*>(smem_raw + sizeof(T) * static_cast<size_t>(pe - pb + 1));
+  int* s_lev = s_rows + (nsg + 2);
+  const bool seg_in_smem = nsg + 2 <= seg_cap;
+  if (seg_in_smem) {
+    for (int q = threadIdx.x; q <= nsg; q += blockDim.x) {
+      s_rows[q] = __ldg(a.seg_rows + sb + q);
+      if (q < nsg) s_lev[q] = __ldg(a.seg_level + sb + q);
+    }
+  }
+  if (threadIdx.x == 0) red_release_max(a.prog + tile, nsg > 0 ? __ldg(a.seg_level + sb) - 1 : INT_MAX);
+  __syncthreads();
+  auto seg_row = [&](int q) { return seg_in_smem ? s_rows[q] : __ldg(a.seg_rows + sb + q); };
+  auto seg_lev = [&](int q) { return seg_in_smem ? s_lev[q] : __ldg(a.seg_level + sb + q); };
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  unsigned long long* tsb = (!BACKWARD && g_tri_ts != nullptr && tile == g_tri_ts_tile) ? g_tri_ts : nullptr;
+
+  if (warp == 8) {  // ---------------- poller
+    for (int q = 0; q < nsg; ++q) {
+      if (lane == 0) {
+        const int lev = seg_lev(q);
+        if (tsb && q < 2048) tsb[q * 8 + 0] = gtime();
+        const int we = __ldg(a.seg_wptr + sb + q + 1);
+        for (int w = __ldg(a.seg_wptr + sb + q); w < we; ++w) {
+          const int pt = __ldg(a.seg_wt + w);
+          const int h = pt & 15;
+          // progress already observed (and acquired) for this producer?
+          if (s_seen_tile[h] == pt && s_seen_prog[h] >= lev - 1) continue;
+          const int* pw = a.prog + pt;
+          int v;
+          while ((v = ld_acquire(pw)) < lev - 1) {
+          }
+          s_seen_tile[h] = pt;
+          s_seen_prog[h] = v;
+        }
+        if (tsb && q < 2048) tsb[q * 8 + 1] = gtime();
+        // rolling L2 prefetch of the record streams 8..16 levels ahead
+        if ((q & 7) == 0 && q + 8 < nsg) {
+          const int p0 = seg_row(q + 8), p1 = seg_row(min(nsg, q + 16));
+          l2_prefetch(a.p_dep + static_cast<size_t>(p0) * MAXD, sizeof(int) * MAXD * (p1 - p0));
+          l2_prefetch(a.p_val + static_cast<size_t>(p0) * MAXD, sizeof(i64) * MAXD * (p1 - p0));
+          l2_prefetch(a.p_row + p0, sizeof(int) * (p1 - p0));
+          l2_prefetch(a.p_nd + p0, sizeof(int) * (p1 - p0));
+          if (FP) l2_prefetch(a.p_diag + p0, sizeof(i64) * (p1 - p0));
+          else l2_prefetch(a.p_mag + p0, sizeof(u64) * (p1 - p0));
+        }
+      }
+      __syncwarp();
+      bar_sync(1, kTriBar1);
+    }
+    return;
+  }
+  if (warp >= 9) {  // ---------------- publishers
+    const int r = warp - 9;
+    if (r == kTriPub - 1 && nsg > 0) bar_arrive(1, kTriBar1);  // "level -1" done
+    for (int q = r; q < nsg; q += kTriPub) {
+      bar_sync(2 + r, kTriCompute + 32);
+      if (tsb && lane == 0 && q < 2048) tsb[q * 8 + 5] = gtime();
+      if (q + 1 < nsg) bar_arrive(1, kTriBar1);
+      if (lane == 0) {
+        // bar.sync made the compute warps' stores of level q happen-before
+        // this point; the gpu-scope release is cumulative
+        red_release_max(a.prog + tile, q + 1 < nsg ? seg_lev(q + 1) - 1 : INT_MAX);
+        if (tsb && q < 2048) tsb[q * 8 + 6] = gtime();
+      }
+    }
+    return;
+  }
+  // ---------------- compute warps
+  const bool scaled = prescale != nullptr;
+  const double gamma = scaled ? __longlong_as_double(*reinterpret_cast<const long long*>(prescale)) : 1.0;
+  TriAcc<T, CHECKED> stt;
+  const int tid = threadIdx.x;
+  // 3-deep record pipeline, 2-deep right-hand-side pipeline
+  RowRec<MAXD> r0, r1, r2;
+  bool h0 = false, h1 = false, h2 = false;
+  T y0{}, y1{};
+  if (nsg > 0) { int p = seg_row(0) + tid; h0 = p < seg_row(1); if (h0) load_rec<MAXD, FP>(a, p, pb, r0); }
+  if (nsg > 1) { int p = seg_row(1) + tid; h1 = p < seg_row(2); if (h1) load_rec<MAXD, FP>(a, p, pb, r1); }
+  if (h0) y0 = tri_load_y<T>(y, r0.row, scaled, gamma);
+  for (int q = 0; q < nsg; ++q) {
+    const RowRec<MAXD> cur = r0;
+    const bool hc = h0;
+    const T ycur = y0;
+    r0 = r1; h0 = h1;
+    if (h0) y0 = tri_load_y<T>(y, r0.row, scaled, gamma);
+    h2 = false;
+    if (q + 2 < nsg) { int p = seg_row(q + 2) + tid; h2 = p < seg_row(q + 3); if (h2) load_rec<MAXD, FP>(a, p, pb, r2); }
+    r1 = r2; h1 = h2;
+    if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 2] = gtime();
+    bar_sync(1, kTriBar1);  // deps of level q ready, level q-1 complete
+    if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 3] = gtime();
+    if (hc) tri_row<T, CHECKED, MAXD>(a, cur, ycur, out, zt, stt);
+    const int s1 = seg_row(q + 1);
+    for (int p = seg_row(q) + tid + kTriCompute; p < s1; p += kTriCompute) {  // wide levels
+      RowRec<MAXD> r;
+      load_rec<MAXD, FP>(a, p, pb, r);
+      tri_row<T, CHECKED, MAXD>(a, r, tri_load_y<T>(y, r.row, scaled, gamma), out, zt, stt);
+    }
+    if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 4] = gtime();
+    bar_arrive(2 + (q & (kTriPub - 1)), kTriCompute + 32);
+  }
+  if (CHECKED && !FP) {
+    bump(cnt, OP_MUL, stt.nmul);
+    bump(cnt, OP_SUB, stt.nsub);
+    bump(cnt, OP_DIV, stt.ndiv);
   }
 }
 
 TriArgs tri_args(const DevTri& t) {
   TriArgs a;
   a.n = t.n;
-  a.tile_rows = t.tile_rows;
   a.ntiles = t.ntiles;
-  a.rp = t.rp;
-  a.ci = t.ci;
-  a.vals = t.vals;
-  a.diag = t.diag;
-  a.dmag = t.dmag;
-  a.dinfo = t.dinfo;
+  a.tile_pbase = t.tile_pbase;
   a.tile_seg = t.tile_seg;
   a.seg_level = t.seg_level;
   a.seg_rows = t.seg_rows;
-  a.perm = t.perm;
+  a.seg_wptr = t.seg_wptr;
+  a.seg_wt = t.seg_wt;
+  a.p_row = t.p_row;
+  a.p_nd = t.p_nd;
+  a.p_dep = t.p_dep;
+  a.p_val = t.p_val;
+  a.p_xrp = t.p_xrp;
+  a.p_xdep = t.p_xdep;
+  a.p_xval = t.p_xval;
+  a.p_mag = t.p_mag;
+  a.p_info = t.p_info;
+  a.p_diag = t.p_diag;
   a.prog = t.prog;
   a.ticket = t.ticket;
   return a;
@@ -1081,34 +1280,53 @@ void launch_xupdate(cudaStream_t st, long long n, int m, int f, const i64* basis
   LAUNCH_CHECK();
 }
 
-static void tri_smem_setup(size_t bytes) {
-  static size_t done = 0;
-  if (bytes > done) {
-    cudaFuncSetAttribute(k_tri<i64, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    cudaFuncSetAttribute(k_tri<i64, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    cudaFuncSetAttribute(k_tri<i64, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    cudaFuncSetAttribute(k_tri<i64, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    cudaFuncSetAttribute(k_tri<double, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    cudaFuncSetAttribute(k_tri<double, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    done = bytes;
+template <typename T, bool B, bool CK, int D>
+static void tri_launch_one(cudaStream_t st, const DevTri& t, const T* y, T* out, u64* cnt,
+                           const Ctl* ctl, const double* prescale) {
+  // tile values + segment tables (staged when they fit)
+  int seg_cap = t.max_tile_segs + 2;
+  size_t sm = static_cast<size_t>(t.tile_cap + 1) * sizeof(T) + 2 * sizeof(int) * seg_cap + 16;
+  if (sm > 220 * 1024) {
+    seg_cap = 0;
+    sm = static_cast<size_t>(t.tile_cap + 1) * sizeof(T) + 16;
   }
+  static size_t done = 0;
+  if (sm > done) {
+    cudaFuncSetAttribute(k_tri<T, B, CK, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    done = sm;
+  }
+  if (sm > 48 * 1024) {
+    // keep the L1 share for the record streams small, smem for the tile
+    cudaFuncSetAttribute(k_tri<T, B, CK, D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  }
+  k_tri<T, B, CK, D><<<t.ntiles, kTriThreads, sm, st>>>(tri_args(t), y, out, cnt, ctl, prescale, seg_cap);
+}
+
+template <typename T, bool B, bool CK>
+static void tri_dispatch(cudaStream_t st, const DevTri& t, const T* y, T* out, u64* cnt,
+                         const Ctl* ctl, const double* prescale) {
+  if (t.stride == 4) tri_launch_one<T, B, CK, 4>(st, t, y, out, cnt, ctl, prescale);
+  else if (t.stride == 8) tri_launch_one<T, B, CK, 8>(st, t, y, out, cnt, ctl, prescale);
+  else tri_launch_one<T, B, CK, 16>(st, t, y, out, cnt, ctl, prescale);
+}
+
+void tri_trace_setup(int tile, unsigned long long* buf) {
+  cudaMemcpyToSymbol(g_tri_ts, &buf, sizeof(buf));
+  cudaMemcpyToSymbol(g_tri_ts_tile, &tile, sizeof(int));
 }
 
 void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out,
                     u64* cnt, const Ctl* ctl, bool checked) {
   if (t.n == 0) return;
-  const size_t sm = static_cast<size_t>(t.tile_rows) * sizeof(i64);
-  tri_smem_setup(sm);
   cudaMemsetAsync(t.ticket, 0, sizeof(int), st);
   cudaMemsetAsync(t.prog, 0xff, sizeof(int) * t.ntiles, st);
-  const TriArgs a = tri_args(t);
   ProfScope prof_(st, KC_TRI_INT);
   if (backward) {
-    if (checked) k_tri<i64, true, true><<<t.ntiles, 256, sm, st>>>(a, y, out, cnt, ctl, nullptr);
-    else k_tri<i64, true, false><<<t.ntiles, 256, sm, st>>>(a, y, out, cnt, ctl, nullptr);
+    if (checked) tri_dispatch<i64, true, true>(st, t, y, out, cnt, ctl, nullptr);
+    else tri_dispatch<i64, true, false>(st, t, y, out, cnt, ctl, nullptr);
   } else {
-    if (checked) k_tri<i64, false, true><<<t.ntiles, 256, sm, st>>>(a, y, out, cnt, ctl, nullptr);
-    else k_tri<i64, false, false><<<t.ntiles, 256, sm, st>>>(a, y, out, cnt, ctl, nullptr);
+    if (checked) tri_dispatch<i64, false, true>(st, t, y, out, cnt, ctl, nullptr);
+    else tri_dispatch<i64, false, false>(st, t, y, out, cnt, ctl, nullptr);
   }
   LAUNCH_CHECK();
 }
@@ -1116,16 +1334,11 @@ void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* 
 void launch_tri_fp(cudaStream_t st, const DevTri& t, bool backward, const double* y, double* out,
                    const Ctl* ctl, const double* prescale) {
   if (t.n == 0) return;
-  const size_t sm = static_cast<size_t>(t.tile_rows) * sizeof(double);
-  tri_smem_setup(sm);
   cudaMemsetAsync(t.ticket, 0, sizeof(int), st);
   cudaMemsetAsync(t.prog, 0xff, sizeof(int) * t.ntiles, st);
-  const TriArgs a = tri_args(t);
   ProfScope prof_(st, KC_TRI_FP);
-  if (backward)
-    k_tri<double, true, false><<<t.ntiles, 256, sm, st>>>(a, y, out, nullptr, ctl, prescale);
-  else
-    k_tri<double, false, false><<<t.ntiles, 256, sm, st>>>(a, y, out, nullptr, ctl, prescale);
+  if (backward) tri_dispatch<double, true, false>(st, t, y, out, nullptr, ctl, prescale);
+  else tri_dispatch<double, false, false>(st, t, y, out, nullptr, ctl, prescale);
   LAUNCH_CHECK();
 }
 

@@ -1,0 +1,246 @@
+// schedule.cpp -- see schedule.hpp.
+#include "schedule.hpp"
+
+#include "fx_core.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <stdexcept>
+#include <utility>
+
+namespace igm {
+namespace {
+
+struct Grid {
+  long long gx = 0, gy = 0, gz = 0;
+};
+
+// Fraction of (sampled) dependencies that are +-1 neighbours on the grid.
+double neighbour_score(int n, const std::vector<int>& orp, const std::vector<int>& oci, long long gx,
+                       long long gxy) {
+  long long hit = 0, tot = 0;
+  const int step = std::max(1, n / 200000);
+  for (int i = 0; i < n; i += step) {
+    const long long xi = i % gx, yi = (i / gx) % (gxy / gx), zi = i / gxy;
+    for (int k = orp[i]; k < orp[i + 1]; ++k) {
+      const long long j = oci[k];
+      const long long xj = j % gx, yj = (j / gx) % (gxy / gx), zj = j / gxy;
+      ++tot;
+      if (std::llabs(xi - xj) <= 1 && std::llabs(yi - yj) <= 1 && std::llabs(zi - zj) <= 1) ++hit;
+    }
+  }
+  return tot ? static_cast<double>(hit) / tot : 0.0;
+}
+
+// Infer a gx*gy*gz natural-order grid from the distinct dependency offsets.
+Grid detect_grid(int n, const std::vector<int>& orp, const std::vector<int>& oci) {
+  std::vector<long long> offs;
+  for (int i = 0; i < n && offs.size() <= 64; i += std::max(1, n / 4096)) {
+    for (int k = orp[i]; k < orp[i + 1]; ++k) {
+      const long long d = std::llabs(static_cast<long long>(i) - oci[k]);
+      if (std::find(offs.begin(), offs.end(), d) == offs.end()) offs.push_back(d);
+    }
+  }
+  Grid best;
+  if (offs.empty() || offs.size() > 64) return best;
+  std::sort(offs.begin(), offs.end());
+  long long dmin2 = 0;
+  for (long long d : offs)
+    if (d >= 2) {
+      dmin2 = d;
+      break;
+    }
+  if (dmin2 == 0) return best;
+  double best_score = 0.0;
+  const long long dmax = offs.back();
+  for (long long gx = dmin2 - 1; gx <= dmin2 + 1; ++gx) {
+    if (gx < 2 || n % gx) continue;
+    std::vector<long long> cand{static_cast<long long>(n)};
+    for (int a = -1; a <= 1; ++a)
+      for (int b = -1; b <= 1; ++b) cand.push_back(dmax - a * gx - b);
+    for (long long gxy : cand) {
+      if (gxy < gx || gxy % gx || n % gxy) continue;
+      const double sc = neighbour_score(n, orp, oci, gx, gxy);
+      if (sc > best_score + 1e-12) {
+        best_score = sc;
+        best = Grid{gx, gxy / gx, n / gxy};
+      }
+    }
+  }
+  if (best_score < 0.99) return Grid{};
+  return best;
+}
+
+long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
+
+}  // namespace
+
+TriSchedule build_tri_schedule(int n, const int* rp, const int* ci, const std::int64_t* vals,
+                               const int* dpos, bool upper, int num_sms, int tile_cap_override) {
+  TriSchedule S;
+  S.n = n;
+  // ---- strip: off-diagonal, structurally meaningful entries in CSR order (a
+  // "lower" entry with j > i multiplies a zero-initialised slot in
+  // ilu.cpp:126-135, an "upper" one with j < i likewise) and the diagonal
+  std::vector<int> orp(static_cast<size_t>(n) + 1, 0), oci;
+  std::vector<std::int64_t> ov, dg(static_cast<size_t>(n));
+  oci.reserve(rp[n]);
+  ov.reserve(rp[n]);
+  for (int i = 0; i < n; ++i) {
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+      const int j = ci[k];
+      if (j < 0 || j >= n) throw std::invalid_argument("upload_ilu: column index out of range");
+      if (j == i || (upper ? (j < i) : (j > i))) continue;
+      oci.push_back(j);
+      ov.push_back(vals[k]);
+    }
+    orp[i + 1] = static_cast<int>(oci.size());
+    const int dp = dpos[i];
+    if (dp < 0 || dp >= rp[n]) throw std::invalid_argument("upload_ilu: diagonal position out of range");
+    dg[i] = vals[dp];
+    if (dg[i] == 0) throw std::invalid_argument("upload_ilu: zero diagonal entry");
+  }
+  // ---- DAG levels
+  std::vector<int> lev(static_cast<size_t>(n), 0);
+  for (int q = 0; q < n; ++q) {
+    const int i = upper ? n - 1 - q : q;
+    int l = 0;
+    for (int k = orp[i]; k < orp[i + 1]; ++k) l = std::max(l, lev[oci[k]] + 1);
+    lev[i] = l;
+    S.nlevels = std::max(S.nlevels, l + 1);
+    S.maxd = std::max(S.maxd, orp[i + 1] - orp[i]);
+  }
+  S.stride = S.maxd <= 4 ? 4 : (S.maxd <= 8 ? 8 : 16);
+  // ---- tiles
+  const int cap = tile_cap_override > 0 ? std::min(tile_cap_override, 16384) : 16384;
+  S.tile_cap = cap;
+  const int nsm = std::max(1, num_sms);
+  std::vector<int> tile_of(static_cast<size_t>(n));
+  const Grid g = n > 0 ? detect_grid(n, orp, oci) : Grid{};
+  if (g.gx > 0 && tile_cap_override <= 0) {
+    long long B[3] = {g.gx, g.gy, g.gz};
+    const long long G[3] = {g.gx, g.gy, g.gz};
+    // x-y cross-section <= 256 rows (one row per compute thread per level),
+    // then as deep in z as the shared-memory tile allows
+    while (B[0] * B[1] > 256 && (B[0] > 1 || B[1] > 1)) {
+      if (B[0] >= B[1]) B[0] = cdiv(B[0], 2);
+      else B[1] = cdiv(B[1], 2);
+    }
+    while (B[0] * B[1] * B[2] > cap) B[2] = cdiv(B[2], 2);
+    // bricks of one z-layer must be co-resident (cyclic deps within a layer)
+    while (cdiv(G[0], B[0]) * cdiv(G[1], B[1]) > nsm && B[2] > 1) {
+      B[2] = cdiv(B[2], 2);
+      if (B[0] <= B[1]) B[0] = std::min(G[0], 2 * B[0]);
+      else B[1] = std::min(G[1], 2 * B[1]);
+      while (B[0] * B[1] * B[2] > cap && B[2] > 1) B[2] = cdiv(B[2], 2);
+    }
+    const long long nb0 = cdiv(G[0], B[0]), nb1 = cdiv(G[1], B[1]), nb2 = cdiv(G[2], B[2]);
+    if (B[0] * B[1] * B[2] <= cap && nb0 * nb1 <= nsm) {
+      for (int d = 0; d < 3; ++d) {
+        S.grid[d] = static_cast<int>(G[d]);
+        S.brick[d] = static_cast<int>(B[d]);
+      }
+      S.ntiles = static_cast<int>(nb0 * nb1 * nb2);
+      for (int i = 0; i < n; ++i) {
+        const long long x = i % G[0], y = (i / G[0]) % G[1], z = i / (G[0] * G[1]);
+        tile_of[i] = static_cast<int>(((z / B[2]) * nb1 + y / B[1]) * nb0 + x / B[0]);
+      }
+    }
+  }
+  if (S.ntiles == 0) {  // contiguous row blocks (dependencies only to earlier blocks)
+    int T = std::min(cap, std::max(32, static_cast<int>(cdiv(std::max(n, 1), nsm))));
+    if (tile_cap_override > 0) T = cap;
+    S.ntiles = n > 0 ? static_cast<int>(cdiv(n, T)) : 1;
+    for (int i = 0; i < n; ++i) tile_of[i] = i / T;
+  }
+  // ---- slots: tile-major, then level, then row
+  std::vector<int> order(static_cast<size_t>(n));
+  std::iota(order.begin(), order.end(), 0);
+  std::sort(order.begin(), order.end(), [&](int a, int b) {
+    if (tile_of[a] != tile_of[b]) return tile_of[a] < tile_of[b];
+    if (lev[a] != lev[b]) return lev[a] < lev[b];
+    return a < b;
+  });
+  std::vector<int> slot(static_cast<size_t>(n));
+  for (int p = 0; p < n; ++p) slot[order[p]] = p;
+  S.tile_pbase.assign(static_cast<size_t>(S.ntiles) + 1, 0);
+  for (int i = 0; i < n; ++i) S.tile_pbase[tile_of[i] + 1]++;
+  for (int t = 0; t < S.ntiles; ++t) S.tile_pbase[t + 1] += S.tile_pbase[t];
+  for (int t = 0; t < S.ntiles; ++t)
+    if (S.tile_pbase[t + 1] - S.tile_pbase[t] > cap)
+      throw std::logic_error("upload_ilu: tile exceeds shared-memory capacity");
+  // segments
+  S.tile_seg.assign(static_cast<size_t>(S.ntiles) + 1, 0);
+  S.seg_rows.push_back(0);
+  for (int t = 0; t < S.ntiles; ++t) {
+    for (int p = S.tile_pbase[t]; p < S.tile_pbase[t + 1]; ++p) {
+      if (p == S.tile_pbase[t] || lev[order[p]] != lev[order[p - 1]]) {
+        if (p != S.tile_pbase[t]) S.seg_rows.push_back(p);
+        S.seg_level.push_back(lev[order[p]]);
+      }
+    }
+    if (S.tile_pbase[t + 1] > S.tile_pbase[t]) S.seg_rows.push_back(S.tile_pbase[t + 1]);
+    S.tile_seg[t + 1] = static_cast<int>(S.seg_level.size());
+  }
+  if (S.seg_level.empty()) {  // n == 0: one empty segment keeps the arrays valid
+    S.seg_level.push_back(0);
+    S.seg_rows.push_back(0);
+  }
+  // ---- per-slot records
+  const int W = S.stride;
+  S.p_row.resize(static_cast<size_t>(std::max(n, 1)));
+  S.p_nd.resize(static_cast<size_t>(std::max(n, 1)));
+  S.p_dep.assign(static_cast<size_t>(std::max(n, 1)) * W, 0);
+  S.p_val.assign(static_cast<size_t>(std::max(n, 1)) * W, 0);
+  S.p_xrp.assign(static_cast<size_t>(n) + 1, 0);
+  S.p_mag.resize(static_cast<size_t>(std::max(n, 1)));
+  S.p_info.resize(static_cast<size_t>(std::max(n, 1)));
+  S.p_diag.resize(static_cast<size_t>(std::max(n, 1)));
+  for (int p = 0; p < n; ++p) {
+    const int i = order[p];
+    const int t = tile_of[i];
+    S.p_row[p] = i;
+    S.p_nd[p] = orp[i + 1] - orp[i];
+    for (int k = orp[i], d = 0; k < orp[i + 1]; ++k, ++d) {
+      const int j = oci[k];
+      const int enc = tile_of[j] == t ? slot[j] - S.tile_pbase[t] : ~j;
+      if (d < W) {
+        S.p_dep[static_cast<size_t>(p) * W + d] = enc;
+        S.p_val[static_cast<size_t>(p) * W + d] = ov[k];
+      } else {
+        S.p_xdep.push_back(enc);
+        S.p_xval.push_back(ov[k]);
+      }
+    }
+    S.p_xrp[p + 1] = static_cast<int>(S.p_xdep.size());
+    const SDivMagic gm = make_sdiv(dg[i]);
+    S.p_mag[p] = gm.u.m;
+    S.p_info[p] = gm.u.sh1 | (gm.u.sh2 << 1) | (gm.den_neg << 8) | (gm.den_is_m1 << 9);
+    S.p_diag[p] = dg[i];
+  }
+  if (S.p_xdep.empty()) {
+    S.p_xdep.push_back(0);
+    S.p_xval.push_back(0);
+  }
+  // ---- per segment: producer tiles of its cross-tile dependencies
+  S.seg_wptr.push_back(0);
+  const int nseg = static_cast<int>(S.seg_level.size());
+  for (int sg = 0; sg < nseg; ++sg) {
+    const size_t w0 = S.seg_wt.size();
+    for (int p = S.seg_rows[sg]; p < S.seg_rows[sg + 1]; ++p) {
+      const int i = order[p];
+      for (int k = orp[i]; k < orp[i + 1]; ++k) {
+        const int tj = tile_of[oci[k]];
+        if (tj != tile_of[i] &&
+            std::find(S.seg_wt.begin() + static_cast<std::ptrdiff_t>(w0), S.seg_wt.end(), tj) == S.seg_wt.end())
+          S.seg_wt.push_back(tj);
+      }
+    }
+    S.seg_wptr.push_back(static_cast<int>(S.seg_wt.size()));
+  }
+  if (S.seg_wt.empty()) S.seg_wt.push_back(0);
+  return S;
+}
+
+}  // namespace igm

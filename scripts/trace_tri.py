@@ -1,0 +1,34 @@
+import os, sys, ctypes as C
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2009_07495_b200 as igm
+from workloads import gen
+rp, ci, v = gen.upwind_3d(128, 20.0)
+vals, scale = igm.row_scale(rp, ci, v, 32)
+lo, up = igm.factorize_split_cast(rp, ci, vals)
+F = igm.IluFactors(lo, up)
+n = len(rp) - 1
+print("fwd", F.schedule_info(False))
+y = torch.from_numpy(gen.uniform_int(7, n, -(1 << 45), 1 << 45)).cuda()
+z = igm.apply_inverse(F, y)
+buf = torch.zeros(2048 * 8, dtype=torch.int64, device="cuda")
+lib = igm.lib()
+names = ["poll0", "poll1", "c_presync", "c_postsync", "c_done", "pub_sync", "pub_done"]
+for tile in (0, 1, 9, 63, 127):
+    buf.zero_()
+    lib.igm_debug_tri_trace(tile, C.c_void_p(buf.data_ptr()))
+    z = igm.apply_inverse(F, y)
+    torch.cuda.synchronize()
+    ts = buf.cpu().numpy().reshape(-1, 8)[:, :7].astype(np.float64)
+    ts = ts[ts[:, 3] > 0]
+    t0 = ts[:, :].min()
+    ts -= t0
+    ts /= 1.9  # cycles -> ns at ~1.9 GHz
+    print(f"tile {tile}: segs {len(ts)} start {ts[0,3]/1e3:.1f}us end {ts[-1,4]/1e3:.1f}us")
+    per = np.diff(ts[:, 3])
+    print("  level period med %.0f mean %.0f ns | poll med %.0f | compute(post->done) med %.0f | presync wait(pre->post) med %.0f | pub (sync->done) med %.0f | done->pubsync %.0f" % (
+        np.median(per), per.mean(), np.median(ts[:, 1] - ts[:, 0]), np.median(ts[:, 4] - ts[:, 3]),
+        np.median(ts[:, 3] - ts[:, 2]), np.median(ts[:, 6] - ts[:, 5]), np.median(ts[:, 5] - ts[:, 4])))
+    for r in ts[5:8]:
+        print("   ", " ".join(f"{x/1e3:8.2f}" for x in r))
+lib.igm_debug_tri_trace(-1, None)
