@@ -110,7 +110,12 @@ int igm_ilu_levels(const igm_ilu* f, int backward);
 /* schedule diagnostics: ntiles, nseg, nlevels, maxdeps, grid x/y/z,
  * brick (x*1e6 + y*1e3 + z) */
 void igm_ilu_schedule_info(const igm_ilu* f, int backward, int* out8);
-/* debug: per-segment phase timestamps of one ILU tile (4 u64 per segment) */
+/* CPU-only: build + structurally validate the wavefront schedule of one
+ * factor (host arrays); returns 0 if valid (info as igm_ilu_schedule_info) */
+int igm_debug_tri_schedule(int n, const int* row_ptr, const int* col_idx,
+                           const int64_t* vals, const int* diag_pos, int upper,
+                           int num_sms, int* out8);
+/* debug: per-segment phase timestamps of one ILU tile (8 u64 per segment) */
 void igm_debug_tri_trace(int tile, unsigned long long* device_buf);
 
 /* ---- primitives (parity entry points) ---------------------------------- */

@@ -110,6 +110,8 @@ SIGNATURES = [
     ("igm_ilu_levels", C.c_int, [C.c_void_p, C.c_int]),
     ("igm_ilu_schedule_info", None, [C.c_void_p, C.c_int, i32p]),
     ("igm_debug_tri_trace", None, [C.c_int, C.c_void_p]),
+    ("igm_debug_tri_schedule", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                         C.c_int, i32p]),
     ("igm_spmv", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.POINTER(Trace)]),
     ("igm_apply_inverse", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(Trace)]),
     ("igm_apply_inverse_fp", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),

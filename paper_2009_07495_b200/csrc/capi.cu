@@ -695,6 +695,20 @@ int igm_ilu_levels(const igm_ilu* f, int backward) {
   return f ? (backward ? f->upper.nlevels : f->lower.nlevels) : 0;
 }
 
+int igm_debug_tri_schedule(int n, const int* rp, const int* ci, const int64_t* vals, const int* dpos,
+                           int upper, int num_sms_, int* out8) {
+  try {
+    const TriSchedule S = build_tri_schedule(n, rp, ci, vals, dpos, upper != 0, num_sms_, 0);
+    const int v[8] = {S.ntiles, static_cast<int>(S.seg_level.size()), S.nlevels, S.maxd, S.grid[0], S.grid[1],
+                      S.grid[2], S.brick[0] * 1000000 + S.brick[1] * 1000 + S.brick[2]};
+    for (int i = 0; i < 8; ++i) out8[i] = v[i];
+    return validate_tri_schedule(S, rp, ci, upper != 0);
+  } catch (const std::exception& e) {
+    t_err = e.what();
+    return -1;
+  }
+}
+
 void igm_ilu_schedule_info(const igm_ilu* f, int backward, int* out8) {
   const DevTri& t = backward ? f->upper : f->lower;
   const int v[8] = {t.ntiles, t.nseg, t.nlevels, t.maxd, t.grid[0], t.grid[1], t.grid[2],

@@ -119,33 +119,51 @@ TriSchedule build_tri_schedule(int n, const int* rp, const int* ci, const std::i
   std::vector<int> tile_of(static_cast<size_t>(n));
   const Grid g = n > 0 ? detect_grid(n, orp, oci) : Grid{};
   if (g.gx > 0 && tile_cap_override <= 0) {
-    long long B[3] = {g.gx, g.gy, g.gz};
     const long long G[3] = {g.gx, g.gy, g.gz};
     // x-y cross-section <= 256 rows (one row per compute thread per level),
     // then as deep in z as the shared-memory tile allows
+    long long B[3] = {g.gx, g.gy, g.gz};
     while (B[0] * B[1] > 256 && (B[0] > 1 || B[1] > 1)) {
       if (B[0] >= B[1]) B[0] = cdiv(B[0], 2);
       else B[1] = cdiv(B[1], 2);
     }
     while (B[0] * B[1] * B[2] > cap) B[2] = cdiv(B[2], 2);
-    // bricks of one z-layer must be co-resident (cyclic deps within a layer)
-    while (cdiv(G[0], B[0]) * cdiv(G[1], B[1]) > nsm && B[2] > 1) {
-      B[2] = cdiv(B[2], 2);
-      if (B[0] <= B[1]) B[0] = std::min(G[0], 2 * B[0]);
-      else B[1] = std::min(G[1], 2 * B[1]);
-      while (B[0] * B[1] * B[2] > cap && B[2] > 1) B[2] = cdiv(B[2], 2);
+    auto assign = [&](const long long* b) {
+      const long long nb0 = cdiv(G[0], b[0]), nb1 = cdiv(G[1], b[1]);
+      for (int i = 0; i < n; ++i) {
+        const long long x = i % G[0], y = (i / G[0]) % G[1], z = i / (G[0] * G[1]);
+        tile_of[i] = static_cast<int>(((z / b[2]) * nb1 + y / b[1]) * nb0 + x / b[0]);
+      }
+    };
+    // every dependency in an earlier-or-same tile (ticket order)?  Then the
+    // tile graph is acyclic and any residency works; otherwise the tiles of
+    // one z-layer (where back edges can occur) must fit on the GPU at once.
+    auto acyclic = [&]() {
+      for (int i = 0; i < n; ++i)
+        for (int k = orp[i]; k < orp[i + 1]; ++k) {
+          const int tj = tile_of[oci[k]];
+          if (upper ? (tj < tile_of[i]) : (tj > tile_of[i])) return false;
+        }
+      return true;
+    };
+    assign(B);
+    bool ok = acyclic();
+    if (!ok) {
+      while (cdiv(G[0], B[0]) * cdiv(G[1], B[1]) > nsm && B[2] > 1) {
+        B[2] = cdiv(B[2], 2);
+        if (B[0] <= B[1]) B[0] = std::min(G[0], 2 * B[0]);
+        else B[1] = std::min(G[1], 2 * B[1]);
+        while (B[0] * B[1] * B[2] > cap && B[2] > 1) B[2] = cdiv(B[2], 2);
+      }
+      ok = B[0] * B[1] * B[2] <= cap && cdiv(G[0], B[0]) * cdiv(G[1], B[1]) <= nsm;
+      if (ok) assign(B);
     }
-    const long long nb0 = cdiv(G[0], B[0]), nb1 = cdiv(G[1], B[1]), nb2 = cdiv(G[2], B[2]);
-    if (B[0] * B[1] * B[2] <= cap && nb0 * nb1 <= nsm) {
+    if (ok) {
       for (int d = 0; d < 3; ++d) {
         S.grid[d] = static_cast<int>(G[d]);
         S.brick[d] = static_cast<int>(B[d]);
       }
-      S.ntiles = static_cast<int>(nb0 * nb1 * nb2);
-      for (int i = 0; i < n; ++i) {
-        const long long x = i % G[0], y = (i / G[0]) % G[1], z = i / (G[0] * G[1]);
-        tile_of[i] = static_cast<int>(((z / B[2]) * nb1 + y / B[1]) * nb0 + x / B[0]);
-      }
+      S.ntiles = static_cast<int>(cdiv(G[0], B[0]) * cdiv(G[1], B[1]) * cdiv(G[2], B[2]));
     }
   }
   if (S.ntiles == 0) {  // contiguous row blocks (dependencies only to earlier blocks)
@@ -241,6 +259,59 @@ TriSchedule build_tri_schedule(int n, const int* rp, const int* ci, const std::i
   }
   if (S.seg_wt.empty()) S.seg_wt.push_back(0);
   return S;
+}
+
+int validate_tri_schedule(const TriSchedule& S, const int* rp, const int* ci, bool upper) {
+  const int n = S.n;
+  std::vector<int> slot_of(static_cast<size_t>(n), -1), tile_of(static_cast<size_t>(n), -1),
+      lev_of(static_cast<size_t>(n), -1);
+  for (int t = 0; t < S.ntiles; ++t)
+    for (int sg = S.tile_seg[t]; sg < S.tile_seg[t + 1]; ++sg)
+      for (int p = S.seg_rows[sg]; p < S.seg_rows[sg + 1]; ++p) {
+        const int i = S.p_row[p];
+        if (i < 0 || i >= n || slot_of[i] >= 0) return 1;  // each row exactly once
+        slot_of[i] = p;
+        tile_of[i] = t;
+        lev_of[i] = S.seg_level[sg];
+        if (p < S.tile_pbase[t] || p >= S.tile_pbase[t + 1]) return 2;
+      }
+  for (int i = 0; i < n; ++i)
+    if (slot_of[i] < 0) return 1;
+  for (int t = 0; t < S.ntiles; ++t)
+    for (int sg = S.tile_seg[t] + 1; sg < S.tile_seg[t + 1]; ++sg)
+      if (S.seg_level[sg] <= S.seg_level[sg - 1]) return 3;  // levels ascend in a tile
+  const int W = S.stride;
+  for (int i = 0; i < n; ++i) {
+    const int p = slot_of[i];
+    int d = 0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+      const int j = ci[k];
+      if (j == i || (upper ? (j < i) : (j > i))) continue;
+      const int enc = d < W ? S.p_dep[static_cast<size_t>(p) * W + d] : S.p_xdep[S.p_xrp[p] + d - W];
+      ++d;
+      if (lev_of[j] >= lev_of[i]) return 4;  // dependencies sit on lower levels
+      if (tile_of[j] == tile_of[i]) {
+        if (enc != slot_of[j] - S.tile_pbase[tile_of[i]]) return 5;
+      } else {
+        if (enc != ~j) return 5;
+        // ticket order: producer tile handed out no later than the layer of i
+        const int tk_i = upper ? S.ntiles - 1 - tile_of[i] : tile_of[i];
+        const int tk_j = upper ? S.ntiles - 1 - tile_of[j] : tile_of[j];
+        const int layer = S.brick[0] ? (S.grid[0] + S.brick[0] - 1) / S.brick[0] *
+                                           ((S.grid[1] + S.brick[1] - 1) / S.brick[1])
+                                     : 1;
+        if (tk_j / layer > tk_i / layer) return 6;
+        int sg = -1;
+        for (int q = S.tile_seg[tile_of[i]]; q < S.tile_seg[tile_of[i] + 1]; ++q)
+          if (S.seg_level[q] == lev_of[i]) sg = q;
+        bool listed = false;
+        for (int w = S.seg_wptr[sg]; w < S.seg_wptr[sg + 1]; ++w) listed = listed || S.seg_wt[w] == tile_of[j];
+        if (!listed) return 7;
+      }
+    }
+    if (d != S.p_nd[p]) return 8;
+  }
+  return 0;
 }
 
 }  // namespace igm

@@ -50,4 +50,11 @@ struct TriSchedule {
 TriSchedule build_tri_schedule(int n, const int* rp, const int* ci, const std::int64_t* vals,
                                const int* dpos, bool upper, int num_sms, int tile_cap_override);
 
+// Structural check of a schedule (CPU tests): every row scheduled once,
+// levels ascending inside a tile, tile-local dependencies resolved at a lower
+// level of the same tile, cross-tile dependencies covered by the segment's
+// wait list and pointing at the same or an earlier ticket layer.  Returns 0
+// when valid, otherwise the number of the first failed property.
+int validate_tri_schedule(const TriSchedule& S, const int* rp, const int* ci, bool upper);
+
 }  // namespace igm

@@ -1,0 +1,119 @@
+"""C-ABI library checks that need no GPU: it loads, exports every entry point
+include/igm.h declares, and its host-side setup (row scaling, splitting,
+ILU(0) + integer cast, wavefront schedule) matches the oracle / KATs."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+from tests.cases import CASES, build_case
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    txt = open(os.path.join(ROOT, "include", "igm.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(igm_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol(product_lib):
+    syms = declared_symbols()
+    assert len(syms) > 30
+    missing = [s for s in syms if not hasattr(product_lib, s)]
+    assert not missing, missing
+    from paper_2009_07495_b200 import _capi
+    bound = {s[0] for s in _capi.SIGNATURES}
+    assert set(syms) <= bound | {"igm_debug_tri_schedule"}
+
+
+def test_version_and_error(product_lib):
+    assert b"sm_100a" in product_lib.igm_version()
+
+
+def test_no_gpu_fails_loudly(igm):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(igm.CudaError):
+        igm.Device(0)
+
+
+def test_host_setup_kats(igm, kats):
+    k = kats["row_scale"]
+    vals, scale = igm.row_scale(k["row_ptr"], k["col_idx"], k["vals"], k["alpha"])
+    assert list(scale) == k["scale"] and list(vals) == k["scaled"]
+    k = kats["build_split"]
+    comp, al, ex = igm.build_split(k["vals"], k["alpha"], k["max"])
+    assert comp.tolist() == k["comps"] and al == k["alphas"] and ex
+    k = kats["split_cast"]
+    lo, up = igm.factorize_split_cast(k["row_ptr"], k["col_idx"], k["vals"])
+    assert lo[2].tolist() == k["lower"] and up[2].tolist() == k["upper"]
+    assert lo[3].tolist() == k["diag_pos_lower"] and up[3].tolist() == k["diag_pos_upper"]
+
+
+def test_host_setup_errors(igm):
+    with pytest.raises(RuntimeError, match="no nonzero entry"):
+        igm.row_scale([0, 1, 1], [0], [1.0], 16)          # test_split.cpp:69-70
+    with pytest.raises(ValueError):
+        igm.build_split([1.0], 16, 0)                       # test_split.cpp:187
+    with pytest.raises(RuntimeError, match="no diagonal"):
+        igm.factorize_split_cast([0, 1, 3], [1, 0, 1], [1.0, 1.0, 1.0])  # test_ilu.cpp:74-76
+    with pytest.raises(RuntimeError, match="zero pivot"):
+        igm.factorize_split_cast([0, 2, 4], [0, 1, 0, 1], [0.0, 1.0, 1.0, 1.0])
+    with pytest.raises(RuntimeError, match="truncates to zero"):
+        igm.factorize_split_cast([0, 1], [0], [0.25])     # test_ilu.cpp:97-101
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_host_setup_matches_oracle(igm, oracle, name):
+    c = build_case(name, oracle)
+    vals, scale = igm.row_scale(c["rp"], c["ci"], c["v"], c["alpha"])
+    assert np.array_equal(vals, c["vals"]) and np.array_equal(scale, c["scale"])
+    comp, al, _ = igm.build_split(vals, c["alpha"], CASES[name]["ncomp"])
+    assert np.array_equal(comp, c["comp"]) and al == c["alphas"]
+    if c.get("ilu"):
+        lo, up = igm.factorize_split_cast(c["rp"], c["ci"], vals)
+        for a, b in zip(list(lo) + list(up), c["ilu_arrays"]):
+            assert np.array_equal(a, b)
+
+
+def _schedule(igm, lo_or_up, upper, nsm=148):
+    rp, ci, v, dp = (np.ascontiguousarray(a) for a in lo_or_up)
+    rp = rp.astype(np.int32); ci = ci.astype(np.int32); v = v.astype(np.int64); dp = dp.astype(np.int32)
+    out = (C.c_int32 * 8)()
+    p = lambda a: C.c_void_p(a.ctypes.data)
+    rc = igm.lib().igm_debug_tri_schedule(len(rp) - 1, p(rp), p(ci), p(v), p(dp), 1 if upper else 0, nsm, out)
+    return rc, list(out)
+
+
+@pytest.mark.parametrize("g,kind", [(16, "7pt"), (24, "7pt"), (10, "27pt"), (40, "2d")])
+def test_wavefront_schedule_structured(igm, g, kind):
+    from workloads import gen
+    if kind == "7pt":
+        rp, ci, v = gen.upwind_3d(g)
+    elif kind == "27pt":
+        rp, ci, v = gen.stencil27(g, 5)
+    else:
+        rp, ci, v = gen.upwind_2d(g)
+    vals, _ = igm.row_scale(rp, ci, v, 32)
+    lo, up = igm.factorize_split_cast(rp, ci, vals)
+    for fac, upper in ((lo, False), (up, True)):
+        for nsm in (148, 4):
+            rc, info = _schedule(igm, fac, upper, nsm)
+            assert rc == 0, (rc, info)
+            expect_grid = (g, g, g) if kind != "2d" else (g, g, 1)
+            if nsm == 148 or kind != "27pt":  # 27-pt bricks need co-resident layers
+                assert tuple(info[4:7]) == expect_grid  # structured grid detected
+
+
+def test_wavefront_schedule_unstructured(igm):
+    from workloads import gen
+    rp, ci, v = gen.random_dominant(300, 0.05, 1.3, 9)
+    vals, _ = igm.row_scale(rp, ci, v, 32)
+    lo, up = igm.factorize_split_cast(rp, ci, vals)
+    for fac, upper in ((lo, False), (up, True)):
+        rc, info = _schedule(igm, fac, upper)
+        assert rc == 0 and info[4] == 0  # contiguous tiles

@@ -1,0 +1,271 @@
+"""Parity of the B200 path (C ABI -> sm_100a kernels) with the CPU oracle and
+with golden outputs of the reference library.  Bit-exact on every integer
+word (basis, Hessenberg, g, rotations, SpMV / ILU outputs) and on the FP64
+bookends (x, residual history) -- the FP kernels reproduce the reference's
+operation order with no contraction."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle.ffi import PyTrace, Shifts
+from tests.cases import CASES, build_case
+
+pytestmark = pytest.mark.gpu
+I64_MIN, I64_MAX = np.iinfo(np.int64).min, np.iinfo(np.int64).max
+
+
+def h(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def gpu(igm):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    return igm
+
+
+def product_case(igm, oracle, name):
+    c = build_case(name, oracle)
+    c["S"] = igm.SplitMatrix(c["rp"], c["ci"], c["comp"], c["alphas"])
+    c["A"] = igm.CsrMatrixF(c["rp"], c["ci"], c["vals"])
+    if c.get("ilu"):
+        c["F"] = igm.IluFactors(c["lower"], c["upper"])
+    c["plan"] = igm.ShiftPlan(*c["shifts"])
+    return c
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_spmv_bit_exact(gpu, oracle, goldens, name):
+    c = product_case(gpu, oracle, name)
+    rng = np.random.default_rng(1)
+    for s in range(c["ncomp"]):
+        for v in (c["v_full"], rng.integers(-(1 << 31), 1 << 31, c["n"], dtype=np.int64)):
+            t1, t2 = gpu.FxTrace(), PyTrace()
+            out = gpu.spmv(c["S"], s, v, t1)
+            assert np.array_equal(out, oracle.spmv(c["sp"], s, v, t2))
+            assert t1.total_overflows() == t2.total  # per-row sequential: exact
+        if "spmv" in goldens["cases"][name]:
+            assert h(gpu.spmv(c["S"], s, c["v_full"])) == goldens["cases"][name]["spmv"][str(s)]
+
+
+@pytest.mark.parametrize("name", ["cfg2_16", "cfg4_12", "ilu_random"])
+def test_ilu_apply_bit_exact(gpu, oracle, goldens, name):
+    c = product_case(gpu, oracle, name)
+    g = goldens["cases"][name]
+    assert h(gpu.apply_inverse(c["F"], c["y_int"])) == g["apply_inverse"]
+    assert h(gpu.apply_inverse_fp(c["F"], c["y_fp"])) == g["apply_inverse_fp"]
+    for y in (c["v_full"], c["y_int"]):
+        t1, t2 = gpu.FxTrace(), PyTrace()
+        assert np.array_equal(gpu.apply_inverse(c["F"], y, t1), oracle.apply_inverse(c["il"], y, t2))
+        assert t1.total_overflows() == t2.total
+    for _ in range(3):  # repeated launches: the spin-wait protocol is re-armed every call
+        assert h(gpu.apply_inverse(c["F"], c["y_int"])) == g["apply_inverse"]
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_run_cycle_state_bit_exact(gpu, oracle, goldens, name):
+    c = product_case(gpu, oracle, name)
+    cfg = gpu.CycleConfig(m=c["m"], frac_bits=30, shifts=c["plan"], s=c["s"], precond=c.get("F"))
+    r = gpu.run_cycle(c["S"], cfg, c["b"], np.zeros(c["n"]))
+    g = goldens["cases"][name]["cycle"]
+    assert r.dim == g["dim"] and r.r0_norm == g["r0_norm"] and len(r.basis) == g["n_basis"]
+    assert h(r.basis) == g["basis"]
+    assert h(r.hess) == g["hess"] and h(r.g) == g["g"]
+    assert h(r.cos_raw) == g["cos_raw"] and h(r.sin_raw) == g["sin_raw"]
+    assert h(r.x) == g["x"]
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_solve_bit_exact(gpu, oracle, goldens, name):
+    c = product_case(gpu, oracle, name)
+    cfg = gpu.RefineConfig(tol=c["tol"], max_refinements=c["max_ref"], m=c["m"], frac_bits=30,
+                           shifts=c["plan"], s=c["s"], checked=True)
+    x, rep = gpu.solve(c["S"], c["A"], c["b"], cfg, precond=c.get("F"))
+    g = goldens["cases"][name]["solve"]
+    assert h(x) == g["x"]
+    want = g["report"]
+    assert rep.converged == want["converged"] and rep.refinements == want["refinements"]
+    assert rep.total_inner_iterations == want["total_inner_iterations"]
+    assert rep.inner_dims == want["inner_dims"]
+    assert rep.relres_history == want["relres_history"]
+    assert rep.gamma_history == want["gamma_history"]
+    assert rep.overflow_per_restart == want["overflow_per_restart"]
+    assert rep.overflow_total == want["overflow_total"] and rep.overflow_exact
+
+
+def test_vector_kernels_random(gpu, oracle):
+    rng = np.random.default_rng(99)
+    for n in (1, 2, 31, 64, 1000, 4097, 100003):
+        v = rng.integers(I64_MIN, I64_MAX, n, dtype=np.int64)
+        w = rng.integers(I64_MIN, I64_MAX, n, dtype=np.int64)
+        b1, b2 = int(rng.integers(0, 30)), int(rng.integers(0, 30))
+        assert gpu.fx_dot(v, w, 30, b1, b2) == oracle.fx_dot(v, w, 30, b1, b2)
+        hh = int(rng.integers(I64_MIN, I64_MAX))
+        t1, t2 = gpu.FxTrace(), PyTrace()
+        ww = w.copy()
+        gpu.fx_axpy_sub(ww, hh, v, 30, b1, t1)
+        assert np.array_equal(ww, oracle.fx_axpy_sub(w, hh, v, 30, b1, t2))
+        assert t1.total_overflows() == t2.total
+        lim = (1 << 40) if n < 10000 else (1 << 33)  # keep sum of squares < 2^63
+        u = rng.integers(-lim, lim, n, dtype=np.int64)
+        t1, t2 = gpu.FxTrace(), PyTrace()
+        assert gpu.fx_norm(u, 30, 16, t1) == oracle.fx_norm(u, 30, 16, t2)
+        assert t1.total_overflows() == t2.total  # square wraps are exact
+        x = rng.uniform(-1, 1, n)
+        assert gpu.norm2(x) == oracle.norm2(x)
+
+
+def test_norm_wrap_raises(gpu):
+    with pytest.raises(ArithmeticError, match="wrapped negative"):
+        gpu.fx_norm(np.array([3 << 30], dtype=np.int64), 30, 0)  # test_fxp.cpp:144-149
+
+
+def test_fp_bookends_bit_exact(gpu, oracle):
+    c = product_case(gpu, oracle, "cfg1")
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-1, 1, c["n"])
+    r1, rel1 = gpu.residual_fp(c["A"], x, c["b"])
+    r2, rel2 = oracle.residual_fp(c["af"], x, c["b"])
+    assert np.array_equal(r1, r2) and rel1 == rel2
+    assert np.array_equal(gpu.spmv_fp_split(c["S"], 0, x), oracle.spmv_fp_split(c["sp"], 0, x))
+    g, bk = gpu.gamma_scale(r1)
+    assert g == np.abs(r2).max() and np.array_equal(bk, r2 / g)
+    with pytest.raises(ValueError, match="zero residual"):
+        gpu.gamma_scale(np.zeros(4))
+
+
+def test_run_cycle_nonzero_x0(gpu, oracle):
+    c = product_case(gpu, oracle, "split_s3")
+    x0 = np.random.default_rng(5).uniform(-1, 1, c["n"])
+    cfg = gpu.CycleConfig(m=c["m"], frac_bits=30, shifts=c["plan"], s=c["s"])
+    r = gpu.run_cycle(c["S"], cfg, c["b"], x0)
+    o = oracle.run_cycle(c["sp"], c["m"], 30, c["s"], Shifts(*c["shifts"]), c["b"], x0)
+    assert r.dim == o["dim"] and np.array_equal(r.x, o["x"]) and np.array_equal(r.basis, o["basis"])
+
+
+def test_cycle_edge_cases(gpu, oracle):
+    from workloads import gen
+    # zero right-hand side: x unchanged, dim 0 (test_gmres_cycle.cpp:192-204)
+    rp, ci, v = gen.laplacian2d(3)
+    comp, al, _ = gpu.build_split(v, 16, 4)
+    S = gpu.SplitMatrix(rp, ci, comp, al)
+    cfg = gpu.CycleConfig(m=5, frac_bits=30, shifts=gpu.ShiftPlan.default_unpreconditioned(30))
+    r = gpu.run_cycle(S, cfg, np.zeros(9), np.zeros(9))
+    assert r.dim == 0 and r.r0_norm == 0.0 and not r.x.any()
+    # cyclic permutation: exact happy breakdown at step n (test_gmres_cycle.cpp:167-190)
+    n = 8
+    rp = np.arange(n + 1, dtype=np.int32)
+    ci = np.array([(i - 1) % n for i in range(n)], dtype=np.int32)
+    comp, al, _ = gpu.build_split(np.ones(n), 16, 2)
+    S = gpu.SplitMatrix(rp, ci, comp, al)
+    b = np.zeros(n)
+    b[0] = 1.0
+    r = gpu.run_cycle(S, gpu.CycleConfig(m=n + 4, frac_bits=30, shifts=gpu.ShiftPlan.default_unpreconditioned(30)),
+                      b, np.zeros(n))
+    assert r.dim == n and len(r.basis) == n
+    # argument validation (test_gmres_cycle.cpp:206-221)
+    with pytest.raises(ValueError, match="m must be"):
+        gpu.run_cycle(S, gpu.CycleConfig(m=0, shifts=gpu.ShiftPlan.default_unpreconditioned(30)), b, np.zeros(n))
+    with pytest.raises(ValueError, match="splitting depth"):
+        gpu.run_cycle(S, gpu.CycleConfig(m=5, s=5, shifts=gpu.ShiftPlan.default_unpreconditioned(30)), b,
+                      np.zeros(n))
+
+
+def test_solve_edge_cases(gpu, oracle):
+    c = product_case(gpu, oracle, "cfg1")
+    plan = c["plan"]
+    # zero rhs converges with no refinement (test_refine.cpp:372-380)
+    x, rep = gpu.solve(c["S"], c["A"], np.zeros(c["n"]), gpu.RefineConfig(m=5, shifts=plan))
+    assert rep.converged and rep.refinements == 0 and rep.relres_history == [0.0] and not x.any()
+    # max_refinements = 0 reports the initial state (test_refine.cpp:382-390)
+    x, rep = gpu.solve(c["S"], c["A"], c["b"], gpu.RefineConfig(m=5, shifts=plan, max_refinements=0))
+    assert not rep.converged and rep.refinements == 0 and rep.relres_history == [1.0]
+    with pytest.raises(ValueError, match="max_refinements"):
+        gpu.solve(c["S"], c["A"], c["b"], gpu.RefineConfig(m=5, shifts=plan, max_refinements=-1))
+
+
+def test_s_schedule_consulted_once_per_refinement(gpu, oracle):
+    c = product_case(gpu, oracle, "split_s3")
+    asked = []
+    full = c["ncomp"] - 1
+
+    def sched(k):
+        asked.append(k)
+        return min(k, full)
+    cfg = gpu.RefineConfig(tol=1e-10, max_refinements=100, m=c["m"], shifts=c["plan"], s_schedule=sched)
+    x, rep = gpu.solve(c["S"], c["A"], c["b"], cfg)
+    assert asked == list(range(rep.refinements))
+    xo, ro = oracle.solve(c["sp"], c["af"], c["b"], 1e-10, 100, c["m"], 30, 0, Shifts(*c["shifts"]),
+                          s_schedule=[min(k, full) for k in range(100)])
+    assert np.array_equal(x, xo) and rep.relres_history == ro["relres_history"]
+
+
+def test_overflow_counts_and_traces(gpu, oracle):
+    """Removing the dot guard shift wraps products (test_refine.cpp:392-426):
+    the device counts events exactly and surfaces the same failure."""
+    from workloads import gen
+    rp, ci, v = gen.laplacian2d(8)
+    vals, scale = gpu.row_scale(rp, ci, v, 16)
+    comp, al, _ = gpu.build_split(vals, 16, 10)
+    S = gpu.SplitMatrix(rp, ci, comp, al)
+    A = gpu.CsrMatrixF(rp, ci, vals)
+    b = np.ones(len(rp) - 1) / scale
+    plan = gpu.ShiftPlan(0, 0, 16, 16, 16, 14, 16, 0)
+    t = gpu.FxTrace(checked=True)
+    try:
+        gpu.solve(S, A, b, gpu.RefineConfig(tol=1e-8, max_refinements=3, m=6, shifts=plan, s=len(al) - 1), trace=t)
+        threw = None
+    except (ArithmeticError, ValueError, OverflowError, RuntimeError) as e:
+        threw = type(e)
+    sp = oracle.split(rp, ci, comp, al)
+    to = PyTrace()
+    from oracle.ffi import CheckerError
+    try:
+        oracle.solve(sp, oracle.csrf(rp, ci, vals), b, 1e-8, 3, 6, 30, len(al) - 1, Shifts(0, 0, 16, 16, 16, 14, 16, 0),
+                     trace=to)
+        othrew = None
+    except CheckerError as e:
+        othrew = e.code
+    assert t.total_overflows() > 0 and to.total > 0
+    assert (threw is None) == (othrew is None)
+    assert t.events[0][2] == 0  # first events belong to restart 0
+    if t.exact:
+        assert t.total_overflows() == to.total
+
+
+def test_spmv_mgs_microbench_parity(gpu, oracle):
+    """Config-5 call (SpMV + MGS against k basis vectors, unchecked) at small n."""
+    import torch
+    from workloads import gen
+    rp, ci, v = gen.upwind_3d(20, 20.0)
+    vals, _ = gpu.row_scale(rp, ci, v, 16)
+    comp, al, _ = gpu.build_split(vals, 16, 1)
+    S = gpu.SplitMatrix(rp, ci, comp, al)
+    n, k = len(rp) - 1, 7
+    basis = gen.uniform_int(5, k * n, -(1 << 40), 1 << 40).reshape(k, n)
+    vin = gen.uniform_int(6, n, -(1 << 40), 1 << 40)
+    w = torch.empty(n, dtype=torch.int64, device="cuda")
+    hs = gpu.spmv_mgs(S, 0, torch.from_numpy(vin).cuda(), torch.from_numpy(basis).cuda(), k, 30, 16, 0, 16, w)
+    sp = oracle.split(rp, ci, comp, al)
+    wo = oracle.spmv(sp, 0, vin)
+    for i in range(k):
+        hi = oracle.fx_dot(wo, basis[i], 30, 16, 0)
+        assert hi == hs[i]
+        wo = oracle.fx_axpy_sub(wo, hi, basis[i], 30, 16)
+    assert np.array_equal(w.cpu().numpy(), wo)
+
+
+def test_device_resident_inputs(gpu, oracle):
+    """torch CUDA tensors are used in place (no staging) and give the same bits."""
+    import torch
+    c = product_case(gpu, oracle, "cfg2_16")
+    cfg = gpu.RefineConfig(tol=c["tol"], max_refinements=c["max_ref"], m=c["m"], shifts=c["plan"])
+    xh, _ = gpu.solve(c["S"], c["A"], c["b"], cfg, precond=c["F"])
+    xd = torch.empty(c["n"], dtype=torch.float64, device="cuda")
+    gpu.solve(c["S"], c["A"], torch.from_numpy(c["b"]).cuda(), cfg, precond=c["F"], x_out=xd)
+    assert np.array_equal(xh, xd.cpu().numpy())
+    yd = gpu.apply_inverse(c["F"], torch.from_numpy(c["y_int"]).cuda())
+    assert np.array_equal(yd.cpu().numpy(), gpu.apply_inverse(c["F"], c["y_int"]))
