@@ -10,6 +10,7 @@
 #include "igm_internal.cuh"
 
 #include <climits>
+#include <cstdlib>
 #include <type_traits>
 #include <cstdio>
 #include <vector>
@@ -302,6 +303,226 @@ __global__ void __launch_bounds__(256) k_norm2_serial(long long n, const double*
     }
   }
   if (threadIdx.x == 0) {
+    const double r = __dsqrt_rn(acc);
+    switch (mode) {
+      case 0: *out = r; break;
+      case 1: ctl->nb = r; break;
+      case 2:
+        ctl->nr = r;
+        ctl->relnorm = ctl->nb == 0.0 ? r : __ddiv_rn(r, ctl->nb);
+        break;
+      case 3:
+        ctl->r0n = r;
+        if (r == 0.0) ctl->stop = 1;
+        break;
+      case 4: out[basis_idx] = r; break;
+    }
+  }
+}
+
+// K8' norm2, exact parallel form of the same sequential chain.
+//
+// Inside one binade [2^E, 2^{E+1}) of the running sum the ulp u = 2^{E-52} is
+// fixed, the sum is M*u with M < 2^53, and fl(M*u + q) = u * rne(M + q/u)
+// (round to nearest, ties to even) as long as M + q/u < 2^53 - 1/2.  Each
+// term therefore adds an integer d = floor(q/u) (+1 above half, and at an
+// exact half +1 iff M + floor(q/u) is odd).  Only ties depend on the running
+// value, and only through its parity: every term is a function of one bit,
+// and a chunk composes as a 2-state automaton (total increment for an even
+// / odd start), so a block-wide scan gives every prefix.  The first term
+// whose exact sum would leave the binade (or a non-finite term) is replayed
+// with the real FP64 add, the binade is re-read from the result, and the scan
+// resumes after it.  The result is bit-identical to the serial chain
+// (split.cpp:45-49) by construction; the serial kernel above stays as the
+// fallback for non-finite data.
+constexpr int kN2Threads = 1024;
+constexpr int kN2Per = 8;
+constexpr int kN2Chunk = kN2Threads * kN2Per;
+constexpr u64 kTwo53 = 1ull << 53;
+
+struct Aut {  // increments for an even / odd incoming parity
+  u64 d0, d1;
+};
+
+__device__ __forceinline__ Aut aut_then(const Aut& f, const Aut& g) {
+  Aut h;
+  h.d0 = f.d0 + ((f.d0 & 1) ? g.d1 : g.d0);
+  h.d1 = f.d1 + (((f.d1 + 1) & 1) ? g.d1 : g.d0);
+  return h;
+}
+
+enum { N2_DOWN = 0, N2_UP = 1, N2_TIE = 2, N2_EXIT = 3 };
+
+// q = mq * 2^fq; u = 2^(E-52): floor(q/u) and the class of the remainder
+__device__ __forceinline__ int n2_classify(double q, int E, u64& a) {
+  const u64 bits = static_cast<u64>(__double_as_longlong(q));
+  const int ex = static_cast<int>((bits >> 52) & 0x7ff);
+  u64 mq = bits & ((1ull << 52) - 1);
+  a = 0;
+  if (ex == 0x7ff) return N2_EXIT;
+  int fq;
+  if (ex == 0) {
+    fq = -1074;
+  } else {
+    mq |= 1ull << 52;
+    fq = ex - 1075;
+  }
+  if (mq == 0) return N2_DOWN;
+  const int sh = (E - 52) - fq;
+  if (sh < 0) return N2_EXIT;  // q >= 2u * 2^52: leaves the binade
+  if (sh == 0) {
+    a = mq;
+    return N2_DOWN;
+  }
+  if (sh >= 64) return N2_DOWN;
+  a = mq >> sh;
+  const u64 rem = mq & ((1ull << sh) - 1), half = 1ull << (sh - 1);
+  return rem < half ? N2_DOWN : (rem == half ? N2_TIE : N2_UP);
+}
+
+__device__ __forceinline__ u64 n2_inc(u64 a, int cls, u64 parity) {
+  return cls == N2_DOWN ? a : (cls == N2_UP ? a + 1 : a + ((parity + a) & 1));
+}
+
+__global__ void __launch_bounds__(kN2Threads) k_norm2_exact(long long n, const double* __restrict__ v,
+                                                            const i64* __restrict__ raw, double scale,
+                                                            double* out, Ctl* ctl, int mode,
+                                                            int basis_idx) {
+  __shared__ Aut s_warp[32];
+  __shared__ int s_exit;
+  __shared__ u64 s_mprev;
+  __shared__ int s_E;
+  __shared__ u64 s_M;
+  __shared__ long long s_pos;
+  __shared__ int s_tail;
+  __shared__ double s_tailv;
+  if (mode == 3 && cycle_over(ctl)) return;
+  if (mode == 4 && (ctl->err || basis_idx >= ctl->nbasis)) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) {
+    s_E = -1022;  // s = 0: subnormal binade, u = 2^-1074
+    s_M = 0;
+    s_pos = 0;
+    s_tail = 0;
+  }
+  __syncthreads();
+  while (true) {
+    const long long pos = s_pos;
+    const int E = s_E;
+    const u64 M0 = s_M;
+    if (pos >= n || s_tail) break;
+    const long long base = pos + static_cast<long long>(tid) * kN2Per;
+    u64 a[kN2Per];
+    int cls[kN2Per];
+    Aut mine{0, 0};
+#pragma unroll
+    for (int g = 0; g < kN2Per; ++g) {
+      const long long idx = base + g;
+      if (idx < n && idx < pos + kN2Chunk) {
+        const double x = raw ? dec(raw[idx], scale) : v[idx];
+        cls[g] = n2_classify(__dmul_rn(x, x), E, a[g]);
+      } else {
+        cls[g] = N2_DOWN;
+        a[g] = 0;
+      }
+      Aut e;
+      e.d0 = n2_inc(a[g], cls[g] == N2_EXIT ? N2_DOWN : cls[g], 0);
+      e.d1 = n2_inc(a[g], cls[g] == N2_EXIT ? N2_DOWN : cls[g], 1);
+      mine = aut_then(mine, e);
+    }
+    // exclusive block scan of the automata (sequence order = thread order)
+    Aut inc = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      Aut up;
+      up.d0 = __shfl_up_sync(0xffffffffu, inc.d0, o);
+      up.d1 = __shfl_up_sync(0xffffffffu, inc.d1, o);
+      if (lane >= o) inc = aut_then(up, inc);
+    }
+    if (lane == 31) s_warp[wid] = inc;
+    if (tid == 0) s_exit = INT_MAX;
+    __syncthreads();
+    if (wid == 0) {
+      Aut w = s_warp[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        Aut up;
+        up.d0 = __shfl_up_sync(0xffffffffu, w.d0, o);
+        up.d1 = __shfl_up_sync(0xffffffffu, w.d1, o);
+        if (lane >= o) w = aut_then(up, w);
+      }
+      s_warp[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    Aut ex{0, 0};
+    if (wid > 0) ex = s_warp[wid - 1];
+    {
+      Aut lx;
+      lx.d0 = __shfl_up_sync(0xffffffffu, inc.d0, 1);
+      lx.d1 = __shfl_up_sync(0xffffffffu, inc.d1, 1);
+      if (lane > 0) ex = aut_then(ex, lx);
+    }
+    const Aut total = s_warp[31];
+    // walk this thread's terms from the true incoming value; first exit
+    u64 Mp = M0 + ((M0 & 1) ? ex.d1 : ex.d0);
+    int my_exit = INT_MAX;
+    u64 my_mprev = 0;
+#pragma unroll
+    for (int g = 0; g < kN2Per; ++g) {
+      if (my_exit != INT_MAX) break;
+      const long long idx = base + g;
+      if (idx >= n || idx >= pos + kN2Chunk) break;
+      const bool leave = cls[g] == N2_EXIT || a[g] >= kTwo53 ||
+                         Mp + a[g] + (cls[g] != N2_DOWN ? 1 : 0) >= kTwo53;
+      if (leave) {
+        my_exit = tid * kN2Per + g;
+        my_mprev = Mp;
+      } else {
+        Mp += n2_inc(a[g], cls[g], Mp & 1);
+      }
+    }
+    if (my_exit != INT_MAX) atomicMin(&s_exit, my_exit);
+    __syncthreads();
+    const int xe = s_exit;
+    if (xe != INT_MAX && my_exit == xe) s_mprev = my_mprev;
+    __syncthreads();
+    if (tid == 0) {
+      if (xe == INT_MAX) {
+        s_M = M0 + ((M0 & 1) ? total.d1 : total.d0);
+        s_pos = min(n, pos + kN2Chunk);
+      } else {
+        // replay the term that leaves the binade with the real FP64 add
+        const long long idx = pos + xe;
+        const double x = raw ? dec(raw[idx], scale) : v[idx];
+        const double sp = ldexp(static_cast<double>(s_mprev), E - 52);
+        const double sn = __dadd_rn(sp, __dmul_rn(x, x));
+        if (!isfinite(sn)) {
+          s_tail = 1;
+          s_tailv = sn;
+          s_pos = idx + 1;
+        } else {
+          const u64 b = static_cast<u64>(__double_as_longlong(sn));
+          const int ebits = static_cast<int>((b >> 52) & 0x7ff);
+          const int En = ebits == 0 ? -1022 : max(ebits - 1023, -1022);
+          s_E = En;
+          s_M = static_cast<u64>(ldexp(sn, 52 - En));
+          s_pos = idx + 1;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    double acc;
+    if (s_tail) {  // non-finite partial sum: finish the chain serially
+      acc = s_tailv;
+      for (long long i = s_pos; i < n; ++i) {
+        const double x = raw ? dec(raw[i], scale) : v[i];
+        acc = __dadd_rn(acc, __dmul_rn(x, x));
+      }
+    } else {
+      acc = ldexp(static_cast<double>(s_M), s_E - 52);
+    }
     const double r = __dsqrt_rn(acc);
     switch (mode) {
       case 0: *out = r; break;
@@ -1166,10 +1387,21 @@ void launch_scale_div(cudaStream_t st, long long n, const double* r, double* out
   LAUNCH_CHECK();
 }
 
+static bool norm2_serial_forced() {
+  static const int v = [] {
+    const char* e = std::getenv("IGM_NORM2_SERIAL");
+    return e && e[0] == '1' ? 1 : 0;
+  }();
+  return v != 0;
+}
+
 void launch_norm2_serial(cudaStream_t st, long long n, const double* v, double* out, Ctl* ctl,
                          int mode) {
   ProfScope prof_(st, KC_NORM2);
-  k_norm2_serial<<<1, 256, 0, st>>>(n, v, nullptr, 1.0, out, ctl, mode, 0);
+  if (norm2_serial_forced())
+    k_norm2_serial<<<1, 256, 0, st>>>(n, v, nullptr, 1.0, out, ctl, mode, 0);
+  else
+    k_norm2_exact<<<1, kN2Threads, 0, st>>>(n, v, nullptr, 1.0, out, ctl, mode, 0);
   LAUNCH_CHECK();
 }
 
@@ -1178,8 +1410,8 @@ void launch_basis_norms(cudaStream_t st, long long n, int nb, int f, const i64* 
   ProfScope prof_(st, KC_NORM2);
   (void)tmp;
   for (int k = 0; k < nb; ++k) {
-    k_norm2_serial<<<1, 256, 0, st>>>(n, nullptr, basis + static_cast<long long>(k) * n,
-                                      ldexp(1.0, -f), out, ctl, 4, k);
+    k_norm2_exact<<<1, kN2Threads, 0, st>>>(n, nullptr, basis + static_cast<long long>(k) * n,
+                                            ldexp(1.0, -f), out, ctl, 4, k);
     LAUNCH_CHECK();
   }
 }

@@ -269,3 +269,36 @@ def test_device_resident_inputs(gpu, oracle):
     assert np.array_equal(xh, xd.cpu().numpy())
     yd = gpu.apply_inverse(c["F"], torch.from_numpy(c["y_int"]).cuda())
     assert np.array_equal(yd.cpu().numpy(), gpu.apply_inverse(c["F"], c["y_int"]))
+
+
+def _norm2_cases():
+    rng = np.random.default_rng(2024)
+    cases = [np.zeros(0), np.zeros(5), np.array([3.0, 4.0]), rng.uniform(-1, 1, 1),
+             rng.uniform(-1, 1, 8191), rng.uniform(-1, 1, 8192), rng.uniform(-1, 1, 8193),
+             rng.uniform(-1, 1, 300000)]
+    # exact powers of two: every term exact, many binade crossings
+    cases.append(np.ldexp(1.0, rng.integers(-40, 40, 50000)))
+    # ties: running sum in [2,4) has ulp 2^-51; (2^-26)^2 = 2^-52 is exactly half an ulp
+    t = np.full(40000, 2.0 ** -26)
+    t[0] = 1.5
+    t[1000::997] = 2.0 ** -25.5 if False else 1.0
+    cases.append(t)
+    t2 = np.full(30000, 2.0 ** -26)
+    t2[0] = np.sqrt(2.5)
+    cases.append(t2)
+    # subnormal squares and huge dynamic range
+    cases.append(np.concatenate([np.full(5000, 1e-160), rng.uniform(-1, 1, 5000) * 1e-155]))
+    cases.append(rng.uniform(-1, 1, 60000) * np.ldexp(1.0, rng.integers(-500, 500, 60000)))
+    # overflow to inf, then nan
+    cases.append(np.array([1e200, 1e200, 1.0]))
+    cases.append(np.array([1.0, np.nan, 2.0]))
+    return cases
+
+
+def test_norm2_exact_parallel_chain(gpu, oracle):
+    """The parallel norm2 (binade automaton scan) is bit-identical to the
+    sequential FP64 chain of split.cpp:45-49 on adversarial data."""
+    for x in _norm2_cases():
+        a = gpu.norm2(x)
+        b = oracle.norm2(x)
+        assert np.float64(a).tobytes() == np.float64(b).tobytes(), (len(x), a, b)
