@@ -261,8 +261,9 @@ def run_b200(args, ws, rank, local):
     rep = None
     for _ in range(args.warmup):
         _, rep = igm.solve(S, A, d_b, cfg, precond=F, x_out=d_x)
-    log(f"[bench] warm-up solve: {rep.refinements} refinements, {rep.total_inner_iterations} iterations, "
-        f"relres {rep.relres_history[-1]:.3e}, overflows {rep.overflow_total}")
+    if rep is not None:
+        log(f"[bench] warm-up solve: {rep.refinements} refinements, {rep.total_inner_iterations} iterations, "
+            f"relres {rep.relres_history[-1]:.3e}, overflows {rep.overflow_total}")
 
     # timed region (device-resident)
     l0 = dev.launches

@@ -9,6 +9,7 @@
 // without host round trips.
 #include "igm_internal.cuh"
 
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 #include <type_traits>
@@ -576,7 +577,52 @@ __global__ void k_encode(long long n, const double* __restrict__ r0, i64* __rest
 // wrapping u64 sums (exact, order-free).  In checked mode per-element mul /
 // sub events are counted exactly and sum|term| is accumulated so the
 // running-sum ("add") events can be certified zero.
-template <int MODE, bool CHECKED>
+// 256-bit global accesses (LDG.E.ENL2.256 / STG.E.ENL2.256 on sm_100a)
+__device__ __forceinline__ void ld_v4(const i64* p, i64 (&v)[4]) {
+  asm volatile("ld.global.v4.b64 {%0, %1, %2, %3}, [%4];"
+               : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3])
+               : "l"(p));
+}
+__device__ __forceinline__ void ld_v4_nc(const i64* p, i64 (&v)[4]) {
+  asm volatile("ld.global.nc.v4.b64 {%0, %1, %2, %3}, [%4];"
+               : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3])
+               : "l"(p));
+}
+__device__ __forceinline__ void st_v4(i64* p, const i64 (&v)[4]) {
+  asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(v[0]), "l"(v[1]), "l"(v[2]),
+               "l"(v[3])
+               : "memory");
+}
+
+template <int VEC>
+__device__ __forceinline__ void ldv(const i64* p, i64 (&v)[VEC]) {
+  if constexpr (VEC == 4) {
+    ld_v4(p, v);
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) v[e] = p[e];
+  }
+}
+template <int VEC>
+__device__ __forceinline__ void ldv_nc(const i64* p, i64 (&v)[VEC]) {
+  if constexpr (VEC == 4) {
+    ld_v4_nc(p, v);
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) v[e] = __ldg(p + e);
+  }
+}
+template <int VEC>
+__device__ __forceinline__ void stv(i64* p, const i64 (&v)[VEC]) {
+  if constexpr (VEC == 4) {
+    st_v4(p, v);
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) p[e] = v[e];
+  }
+}
+
+template <int MODE, bool CHECKED, int VEC>
 __global__ void __launch_bounds__(512) k_mgs(long long n, i64* __restrict__ w,
                                              const i64* __restrict__ vprev,
                                              const i64* __restrict__ vcur,
@@ -594,42 +640,48 @@ __global__ void __launch_bounds__(512) k_mgs(long long n, i64* __restrict__ w,
     hs = asr(h, sh.axpy_b1);
   }
   u64 sum = 0, ahi = 0, alo = 0, nmul = 0, nsub = 0, nmul2 = 0;
+  const long long ng = n / VEC;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
-  for (long long l = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; l < n; l += stride) {
-    i64 wl = w[l];
-    if (MODE != 0) {
-      const i64 vp = __ldg(vprev + l);
-      const i64 p = wmul(hs, vp);
-      const i64 d = asr(p, post);
-      if (CHECKED) {
-        nmul += mul_ovf(hs, vp);
-        nsub += sub_ovf(wl, d);
+  for (long long gi = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; gi < ng; gi += stride) {
+    const long long l = gi * VEC;
+    i64 wv[VEC], pv[VEC], cv[VEC];
+    ldv<VEC>(w + l, wv);
+    if (MODE != 0) ldv_nc<VEC>(vprev + l, pv);
+    if (MODE == 0 || MODE == 1) ldv_nc<VEC>(vcur + l, cv);
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      i64 wl = wv[e];
+      if (MODE != 0) {
+        const i64 vp = pv[e];
+        const i64 d = asr(wmul(hs, vp), post);
+        if (CHECKED) {
+          nmul += mul_ovf(hs, vp);
+          nsub += sub_ovf(wl, d);
+        }
+        wl = wsub(wl, d);
+        wv[e] = wl;
       }
-      wl = wsub(wl, d);
-      w[l] = wl;
+      i64 t = 0;
+      if (MODE == 0 || MODE == 1) {
+        const i64 a = asr(wl, sh.dot_b1);
+        const i64 b = asr(cv[e], sh.dot_b2);
+        t = wmul(a, b);
+        if (CHECKED) nmul2 += mul_ovf(a, b);
+      } else if (MODE == 2) {
+        const i64 sq = asr(wl, sh.norm_b1);
+        t = wmul(sq, sq);
+        if (CHECKED) nmul2 += mul_ovf(sq, sq);
+      }
+      if (MODE != 3) {
+        sum += static_cast<u64>(t);
+        if (CHECKED) {
+          const u64 at = t < 0 ? 0ull - static_cast<u64>(t) : static_cast<u64>(t);
+          ahi += at >> 32;
+          alo += at & 0xffffffffull;
+        }
+      }
     }
-    if (MODE == 0 || MODE == 1) {
-      const i64 a = asr(wl, sh.dot_b1);
-      const i64 b = asr(__ldg(vcur + l), sh.dot_b2);
-      const i64 t = wmul(a, b);
-      sum += static_cast<u64>(t);
-      if (CHECKED) {
-        nmul2 += mul_ovf(a, b);
-        const u64 at = t < 0 ? 0ull - static_cast<u64>(t) : static_cast<u64>(t);
-        ahi += at >> 32;
-        alo += at & 0xffffffffull;
-      }
-    } else if (MODE == 2) {
-      const i64 s = asr(wl, sh.norm_b1);
-      const i64 t = wmul(s, s);
-      sum += static_cast<u64>(t);
-      if (CHECKED) {
-        nmul2 += mul_ovf(s, s);
-        const u64 at = t < 0 ? 0ull - static_cast<u64>(t) : static_cast<u64>(t);
-        ahi += at >> 32;
-        alo += at & 0xffffffffull;
-      }
-    }
+    if (MODE != 0) stv<VEC>(w + l, wv);
   }
   if (CHECKED) {
     if (MODE != 0) {
@@ -1427,14 +1479,27 @@ void launch_mgs_pass(cudaStream_t st, long long n, int mode, i64* w, const i64* 
                      ShiftsD sh, u64* cnt_axpy, u64* cnt_red, const Ctl* ctl, bool checked) {
   ProfScope prof_(st, KC_MGS);
   const int nt = 512;
-  const int g = grid_for(n, nt) > 2 * num_sms(0) ? 2 * num_sms(0) : grid_for(n, nt);
-#define MGS_CASE(MD)                                                                               \
-  if (checked)                                                                                     \
-    k_mgs<MD, true><<<g, nt, 0, st>>>(n, w, vprev, vcur, hacc, acc_out, abs_out, f, sh, cnt_axpy,  \
-                                      cnt_red, ctl);                                               \
-  else                                                                                             \
-    k_mgs<MD, false><<<g, nt, 0, st>>>(n, w, vprev, vcur, hacc, acc_out, abs_out, f, sh, cnt_axpy, \
-                                       cnt_red, ctl);
+  const int g = static_cast<int>(std::max<long long>(1, std::min<long long>(2LL * num_sms(0), (n / 4 + nt - 1) / nt)));
+  // 256-bit accesses when every stream is 32-byte aligned (n % 4 == 0 and
+  // aligned bases); scalar otherwise
+  auto al32 = [](const void* p) { return (reinterpret_cast<size_t>(p) & 31) == 0; };
+  const bool v4 = (n % 4 == 0) && al32(w) && (!vprev || al32(vprev)) && (!vcur || al32(vcur));
+#define MGS_CASE(MD)                                                                                 \
+  if (v4) {                                                                                          \
+    if (checked)                                                                                     \
+      k_mgs<MD, true, 4><<<g, nt, 0, st>>>(n, w, vprev, vcur, hacc, acc_out, abs_out, f, sh,          \
+                                           cnt_axpy, cnt_red, ctl);                                  \
+    else                                                                                             \
+      k_mgs<MD, false, 4><<<g, nt, 0, st>>>(n, w, vprev, vcur, hacc, acc_out, abs_out, f, sh,         \
+                                            cnt_axpy, cnt_red, ctl);                                 \
+  } else {                                                                                           \
+    if (checked)                                                                                     \
+      k_mgs<MD, true, 1><<<g, nt, 0, st>>>(n, w, vprev, vcur, hacc, acc_out, abs_out, f, sh,          \
+                                           cnt_axpy, cnt_red, ctl);                                  \
+    else                                                                                             \
+      k_mgs<MD, false, 1><<<g, nt, 0, st>>>(n, w, vprev, vcur, hacc, acc_out, abs_out, f, sh,         \
+                                            cnt_axpy, cnt_red, ctl);                                 \
+  }
   switch (mode) {
     case 0: MGS_CASE(0) break;
     case 1: MGS_CASE(1) break;
