@@ -364,6 +364,10 @@ void build_tri(igm_ctx* c, DevTri& t, int n, const int* rp, const int* ci, const
   t.p_mag = dupload(S.p_mag.data(), S.p_mag.size(), st);
   t.p_info = dupload(S.p_info.data(), S.p_info.size(), st);
   t.p_diag = dupload(S.p_diag.data(), S.p_diag.size(), st);
+  t.p_rec = dupload(S.p_rec.data(), S.p_rec.size(), st);
+  t.rec_bytes = S.rec_bytes;
+  t.xz = dalloc<ulonglong2>(static_cast<size_t>(std::max(n, 1)));
+  ck(cudaMemsetAsync(t.xz, 0, sizeof(ulonglong2) * std::max(n, 1), st), "xz");
   t.prog = dalloc<int>(S.ntiles);
   t.ticket = dalloc<int>(1);
   ck(cudaStreamSynchronize(st), "upload_ilu sync");
@@ -376,7 +380,9 @@ void free_tri(DevTri& t) {
                   static_cast<void*>(t.p_row), static_cast<void*>(t.p_nd), static_cast<void*>(t.p_dep),
                   static_cast<void*>(t.p_val), static_cast<void*>(t.p_xrp), static_cast<void*>(t.p_xdep),
                   static_cast<void*>(t.p_xval), static_cast<void*>(t.p_mag), static_cast<void*>(t.p_info),
-                  static_cast<void*>(t.p_diag), static_cast<void*>(t.prog), static_cast<void*>(t.ticket)})
+                  static_cast<void*>(t.p_diag), static_cast<void*>(t.p_rec), static_cast<void*>(t.xz),
+                  static_cast<void*>(t.prog),
+                  static_cast<void*>(t.ticket)})
     dfree(p);
   t = DevTri{};
 }

@@ -13,6 +13,7 @@
 #pragma once
 
 #include "fx_core.cuh"
+#include "schedule.hpp"
 #include "../../include/igm.h"
 
 #include <cuda_runtime.h>
@@ -85,6 +86,10 @@ struct DevTri {
   i64 *p_val = nullptr, *p_xval = nullptr, *p_diag = nullptr;
   u64* p_mag = nullptr;
   int* p_info = nullptr;
+  unsigned char* p_rec = nullptr;  // packed records, rec_bytes each
+  int rec_bytes = 0;
+  ulonglong2* xz = nullptr;        // n tagged exported values (128-bit each)
+  unsigned long long epoch = 0;    // launches so far (tag of the next one)
   int* prog = nullptr;    // ntiles progress words
   int* ticket = nullptr;  // 1
 };
@@ -159,6 +164,7 @@ void launch_basis_norms(cudaStream_t st, long long n, int nb, int f,
 
 int num_sms(int device);
 void tri_trace_setup(int tile, unsigned long long* buf);
+void tri_loader_mode(int sync_loader);
 extern unsigned long long g_launches;  // kernels launched by this library
 
 // Opt-in per-kernel-class timing (CUDA events around each launch on the

@@ -1104,6 +1104,10 @@ struct TriArgs {
   const u64* p_mag;       // exact reciprocal of |diag| per slot
   const int* p_info;      // sh1 | sh2 << 1 | neg << 8 | (diag == -1) << 9
   const i64* p_diag;
+  const unsigned char* p_rec;  // packed per-slot records (schedule.hpp)
+  int tile_cap;
+  ulonglong2* xz;              // exported values: (value, epoch ^ mix(value)) per row
+  unsigned long long epoch;    // unique per launch
   int* prog;
   int* ticket;
 };
@@ -1156,10 +1160,43 @@ struct TriAcc {
 
 // one dependency term: acc -= l_ij * z_j (value from smem or, cross-tile,
 // from L2 after the segment's poller acquired the producer's progress)
+__device__ __forceinline__ u64 xz_mix(u64 v) { return v * 0x9E3779B97F4A7C15ull; }
+
+// cross-tile value: spin on its 128-bit (value, tag) word -- one single-copy
+// atomic strong access, so no fence/flag protocol is needed; the tag binds
+// the value to this launch (and guards against a torn read)
+__device__ __forceinline__ u64 xz_wait(const ulonglong2* p, u64 epoch) {
+  u64 v, tg;
+  do {
+    asm volatile("{ .reg .b128 t; ld.global.relaxed.gpu.b128 t, [%2]; mov.b128 {%0, %1}, t; }"
+                 : "=l"(v), "=l"(tg)
+                 : "l"(p)
+                 : "memory");
+  } while (tg != (epoch ^ xz_mix(v)));
+  return v;
+}
+
+__device__ __forceinline__ void xz_put(ulonglong2* p, u64 v, u64 epoch) {
+  asm volatile("{ .reg .b128 t; mov.b128 t, {%0, %1}; st.global.relaxed.gpu.b128 [%2], t; }" ::"l"(v),
+               "l"(epoch ^ xz_mix(v)), "l"(p)
+               : "memory");
+}
+
+template <typename T>
+__device__ __forceinline__ T bits_to(u64 b) {
+  if constexpr (std::is_same<T, double>::value) return __longlong_as_double(static_cast<long long>(b));
+  else return static_cast<T>(b);
+}
+template <typename T>
+__device__ __forceinline__ u64 to_bits(T v) {
+  if constexpr (std::is_same<T, double>::value) return static_cast<u64>(__double_as_longlong(v));
+  else return static_cast<u64>(v);
+}
+
 template <typename T, bool CHECKED>
-__device__ __forceinline__ void tri_term(int c, i64 lv, const T* out, const T* zt, T& acc,
-                                         TriAcc<T, CHECKED>& st) {
-  const T zj = c >= 0 ? zt[c] : __ldcg(out + ~c);
+__device__ __forceinline__ void tri_term(int c, i64 lv, const ulonglong2* xz, u64 epoch, const T* zt,
+                                         T& acc, TriAcc<T, CHECKED>& st) {
+  const T zj = c >= 0 ? zt[c] : bits_to<T>(xz_wait(xz + ~c, epoch));
   if constexpr (std::is_same<T, double>::value) {
     acc = __dsub_rn(acc, __dmul_rn(__ll2double_rn(lv), zj));
   } else {
@@ -1177,10 +1214,10 @@ __device__ __forceinline__ void tri_row(const TriArgs& a, const RowRec<MAXD>& r,
                                         T* zt, TriAcc<T, CHECKED>& st) {
 #pragma unroll
   for (int d = 0; d < MAXD; ++d)
-    if (d < r.nd) tri_term<T, CHECKED>(r.ci[d], r.v[d], out, zt, acc, st);
+    if (d < r.nd) tri_term<T, CHECKED>(r.ci[d], r.v[d], a.xz, a.epoch, zt, acc, st);
   for (int d = MAXD; d < r.nd; ++d)
-    tri_term<T, CHECKED>(__ldg(a.p_xdep + r.xb + d - MAXD), __ldg(a.p_xval + r.xb + d - MAXD), out, zt,
-                         acc, st);
+    tri_term<T, CHECKED>(__ldg(a.p_xdep + r.xb + d - MAXD), __ldg(a.p_xval + r.xb + d - MAXD), a.xz,
+                         a.epoch, zt, acc, st);
   T z;
   if constexpr (std::is_same<T, double>::value) {
     z = __ddiv_rn(acc, __ll2double_rn(r.diag));
@@ -1196,6 +1233,7 @@ __device__ __forceinline__ void tri_row(const TriArgs& a, const RowRec<MAXD>& r,
   }
   zt[r.slot] = z;
   out[r.row] = z;
+  if (r.info & (1 << 10)) xz_put(a.xz + r.row, to_bits<T>(z), a.epoch);  // read by another tile
 }
 
 template <typename T>
@@ -1203,6 +1241,8 @@ __device__ __forceinline__ T tri_load_y(const T* __restrict__ y, int row, bool s
   if constexpr (std::is_same<T, double>::value) return scaled ? __ddiv_rn(y[row], gamma) : y[row];
   else return y[row];
 }
+
+__device__ int g_tri_sync_loader = 0;  // A/B switch (IGM_TRI_SYNC_LOADER)
 
 // debug: per-segment phase timestamps of one tile (igm_debug_tri_trace)
 __device__ unsigned long long* g_tri_ts = nullptr;
@@ -1220,107 +1260,165 @@ __device__ __forceinline__ void bar_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-// Warp-specialised wavefront CTA: 8 compute warps (one row per thread per
-// level; wider levels loop), warp 8 = poller (acquires producer progress for
-// the NEXT level while the compute warps work), warps 9..12 = publishers,
-// round-robin over levels (a gpu-scope release costs ~1.5 us; with four of
-// them in flight it no longer paces the level loop).
-//   barrier 1       "level q may start": compute sync + poller sync + the
-//                   publisher of level q-1 arrives
-//   barrier 2+(q%4) "level q done":      compute arrive + publisher q%4 sync
-// Progress words only grow (red.release.max), so releases that complete out
-// of order cannot regress them.
+// ---- mbarrier / bulk-copy helpers (sm_90+ PTX, valid on sm_100a)
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(void* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(void* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(void* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(void* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, void* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(void* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Wavefront CTA (one tile per CTA):
+//   warps 0-7  compute: one row per thread per level (segments <= 256 rows);
+//              a named barrier per level orders the tile's shared-memory values
+//   warp  8    loader: streams each level's packed row records (one TMA bulk
+//              copy) and right-hand-side values (cp.async gathers) into a
+//              shared-memory ring L levels ahead (mbarriers full/empty)
+// Values another tile needs are published as one aligned 128-bit
+// (value, tag) store and consumed by spinning on that word; there are no
+// progress flags and no gpu-scope fences (a fence's cost grows with the
+// SM's in-flight traffic: ~15 us here).  Tiles are handed out by a ticket
+// counter in a layer-major order, so every producer a thread waits on is
+// already running (schedule.hpp).
 constexpr int kTriCompute = 256;
-constexpr int kTriPub = 4;
-constexpr int kTriThreads = kTriCompute + 32 + 32 * kTriPub;
-constexpr int kTriBar1 = kTriCompute + 64;  // compute + poller + one publisher warp
+constexpr int kTriThreads = kTriCompute + 32;
+
+struct TriSmem {  // byte offsets of the dynamic shared-memory regions
+  size_t rows, lev, ring, bars, total;
+  int ring_slot;
+};
+
+template <typename T, int MAXD>
+__host__ __device__ inline TriSmem tri_smem_layout(int tile_cap, int seg_cap, int L) {
+  constexpr int REC = 32 + 12 * MAXD;
+  TriSmem m;
+  size_t o = (static_cast<size_t>(tile_cap) * sizeof(T) + 15) & ~size_t(15);
+  m.rows = o;
+  o += sizeof(int) * static_cast<size_t>(seg_cap);
+  m.lev = o;
+  o += sizeof(int) * static_cast<size_t>(seg_cap);
+  o = (o + 127) & ~size_t(127);
+  m.ring = o;
+  m.ring_slot = kTriSegRows * (REC + 8);
+  o += static_cast<size_t>(L) * m.ring_slot;
+  o = (o + 15) & ~size_t(15);
+  m.bars = o;
+  o += 16 * static_cast<size_t>(L);
+  m.total = o;
+  return m;
+}
 
 template <typename T, bool BACKWARD, bool CHECKED, int MAXD>
 __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restrict__ y, T* out,
                                                      u64* cnt, const Ctl* ctl,
-                                                     const double* prescale, int seg_cap) {
+                                                     const double* prescale, int seg_cap, int L) {
   constexpr bool FP = std::is_same<T, double>::value;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int REC = 32 + 12 * MAXD;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ int s_tile;
-  __shared__ int s_seen_tile[16], s_seen_prog[16];
   if (cycle_over(ctl)) return;
-  if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1);
-  if (threadIdx.x < 16) {
-    s_seen_tile[threadIdx.x] = -1;
-    s_seen_prog[threadIdx.x] = INT_MIN;
+  const TriSmem lay = tri_smem_layout<T, MAXD>(a.tile_cap, seg_cap, L);
+  T* zt = reinterpret_cast<T*>(smem_raw);
+  int* s_rows = reinterpret_cast<int*>(smem_raw + lay.rows);
+  unsigned char* ring = smem_raw + lay.ring;
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem_raw + lay.bars);
+  unsigned long long* empty = full + L;
+  if (threadIdx.x == 0) {
+    s_tile = atomicAdd(a.ticket, 1);
+    for (int k = 0; k < L; ++k) {
+      mbar_init(full + k, g_tri_sync_loader ? 32 : 33);  // lane-0 expect_tx + 32 cp.async arrivals
+      mbar_init(empty + k, kTriCompute / 32);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
   const int tile = BACKWARD ? a.ntiles - 1 - s_tile : s_tile;
-  const int pb = __ldg(a.tile_pbase + tile), pe = __ldg(a.tile_pbase + tile + 1);
+  const int pb = __ldg(a.tile_pbase + tile);
   const int sb = __ldg(a.tile_seg + tile), se = __ldg(a.tile_seg + tile + 1);
   const int nsg = se - sb;
-  // shared: tile values | segment first-slot table | segment levels
-  T* zt = reinterpret_cast<T*>(smem_raw);
-  int* s_rows = reinterpret_cast<int*>(smem_raw + sizeof(T) * static_cast<size_t>(pe - pb + 1));
-  int* s_lev = s_rows + (nsg + 2);
   const bool seg_in_smem = nsg + 2 <= seg_cap;
-  if (seg_in_smem) {
-    for (int q = threadIdx.x; q <= nsg; q += blockDim.x) {
-      s_rows[q] = __ldg(a.seg_rows + sb + q);
-      if (q < nsg) s_lev[q] = __ldg(a.seg_level + sb + q);
-    }
-  }
-  if (threadIdx.x == 0) red_release_max(a.prog + tile, nsg > 0 ? __ldg(a.seg_level + sb) - 1 : INT_MAX);
+  if (seg_in_smem)
+    for (int q = threadIdx.x; q <= nsg; q += blockDim.x) s_rows[q] = __ldg(a.seg_rows + sb + q);
   __syncthreads();
   auto seg_row = [&](int q) { return seg_in_smem ? s_rows[q] : __ldg(a.seg_rows + sb + q); };
-  auto seg_lev = [&](int q) { return seg_in_smem ? s_lev[q] : __ldg(a.seg_level + sb + q); };
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   unsigned long long* tsb = (!BACKWARD && g_tri_ts != nullptr && tile == g_tri_ts_tile) ? g_tri_ts : nullptr;
 
-  if (warp == 8) {  // ---------------- poller
+  if (warp == 8) {  // ---------------- loader
+    // row ids of the next level are loaded one iteration ahead (registers),
+    // so the right-hand-side gathers never wait on a dependent load
+    constexpr int RPL = kTriSegRows / 32;  // rows per lane per level
+    int rows_nx[RPL];
+    auto load_rows = [&](int q, int (&rr)[RPL]) {
+      const int s0 = seg_row(q), c = seg_row(q + 1) - s0;
+#pragma unroll
+      for (int t = 0; t < RPL; ++t) {
+        const int r = lane + 32 * t;
+        rr[t] = r < c ? __ldg(a.p_row + s0 + r) : 0;
+      }
+    };
+    if (nsg > 0) load_rows(0, rows_nx);
     for (int q = 0; q < nsg; ++q) {
-      if (lane == 0) {
-        const int lev = seg_lev(q);
-        if (tsb && q < 2048) tsb[q * 8 + 0] = gtime();
-        const int we = __ldg(a.seg_wptr + sb + q + 1);
-        for (int w = __ldg(a.seg_wptr + sb + q); w < we; ++w) {
-          const int pt = __ldg(a.seg_wt + w);
-          const int h = pt & 15;
-          // progress already observed (and acquired) for this producer?
-          if (s_seen_tile[h] == pt && s_seen_prog[h] >= lev - 1) continue;
-          const int* pw = a.prog + pt;
-          int v;
-          while ((v = ld_acquire(pw)) < lev - 1) {
-          }
-          s_seen_tile[h] = pt;
-          s_seen_prog[h] = v;
+      const int k = q % L;
+      int rows[RPL];
+#pragma unroll
+      for (int t = 0; t < RPL; ++t) rows[t] = rows_nx[t];
+      if (q >= L) mbar_wait(empty + k, static_cast<unsigned>((q / L - 1) & 1));
+      const int s0 = seg_row(q), c = seg_row(q + 1) - s0;
+      unsigned char* slot = ring + static_cast<size_t>(k) * lay.ring_slot;
+      T* yslot = reinterpret_cast<T*>(slot + kTriSegRows * REC);
+      if (g_tri_sync_loader) {  // A/B: synchronous copy through registers
+        const int4* src = reinterpret_cast<const int4*>(a.p_rec + static_cast<size_t>(s0) * REC);
+        int4* dst = reinterpret_cast<int4*>(slot);
+        for (int i = lane; i < c * REC / 16; i += 32) dst[i] = __ldg(src + i);
+#pragma unroll
+        for (int t = 0; t < RPL; ++t)
+          if (lane + 32 * t < c) yslot[lane + 32 * t] = y[rows[t]];
+        __syncwarp();
+        mbar_arrive(full + k);
+      } else {
+        if (lane == 0) {
+          mbar_arrive_expect_tx(full + k, static_cast<unsigned>(c * REC));
+          bulk_g2s(slot, a.p_rec + static_cast<size_t>(s0) * REC, static_cast<unsigned>(c * REC), full + k);
         }
-        if (tsb && q < 2048) tsb[q * 8 + 1] = gtime();
-        // rolling L2 prefetch of the record streams 8..16 levels ahead
-        if ((q & 7) == 0 && q + 8 < nsg) {
-          const int p0 = seg_row(q + 8), p1 = seg_row(min(nsg, q + 16));
-          l2_prefetch(a.p_dep + static_cast<size_t>(p0) * MAXD, sizeof(int) * MAXD * (p1 - p0));
-          l2_prefetch(a.p_val + static_cast<size_t>(p0) * MAXD, sizeof(i64) * MAXD * (p1 - p0));
-          l2_prefetch(a.p_row + p0, sizeof(int) * (p1 - p0));
-          l2_prefetch(a.p_nd + p0, sizeof(int) * (p1 - p0));
-          if (FP) l2_prefetch(a.p_diag + p0, sizeof(i64) * (p1 - p0));
-          else l2_prefetch(a.p_mag + p0, sizeof(u64) * (p1 - p0));
-        }
+#pragma unroll
+        for (int t = 0; t < RPL; ++t)
+          if (lane + 32 * t < c) cp_async8(yslot + lane + 32 * t, y + rows[t]);
+        cp_async_mbar_arrive(full + k);
       }
-      __syncwarp();
-      bar_sync(1, kTriBar1);
-    }
-    return;
-  }
-  if (warp >= 9) {  // ---------------- publishers
-    const int r = warp - 9;
-    if (r == kTriPub - 1 && nsg > 0) bar_arrive(1, kTriBar1);  // "level -1" done
-    for (int q = r; q < nsg; q += kTriPub) {
-      bar_sync(2 + r, kTriCompute + 32);
-      if (tsb && lane == 0 && q < 2048) tsb[q * 8 + 5] = gtime();
-      if (q + 1 < nsg) bar_arrive(1, kTriBar1);
-      if (lane == 0) {
-        // bar.sync made the compute warps' stores of level q happen-before
-        // this point; the gpu-scope release is cumulative
-        red_release_max(a.prog + tile, q + 1 < nsg ? seg_lev(q + 1) - 1 : INT_MAX);
-        if (tsb && q < 2048) tsb[q * 8 + 6] = gtime();
-      }
+      if (q + 1 < nsg) load_rows(q + 1, rows_nx);
     }
     return;
   }
@@ -1329,34 +1427,40 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
   const double gamma = scaled ? __longlong_as_double(*reinterpret_cast<const long long*>(prescale)) : 1.0;
   TriAcc<T, CHECKED> stt;
   const int tid = threadIdx.x;
-  // 3-deep record pipeline, 2-deep right-hand-side pipeline
-  RowRec<MAXD> r0, r1, r2;
-  bool h0 = false, h1 = false, h2 = false;
-  T y0{}, y1{};
-  if (nsg > 0) { int p = seg_row(0) + tid; h0 = p < seg_row(1); if (h0) load_rec<MAXD, FP>(a, p, pb, r0); }
-  if (nsg > 1) { int p = seg_row(1) + tid; h1 = p < seg_row(2); if (h1) load_rec<MAXD, FP>(a, p, pb, r1); }
-  if (h0) y0 = tri_load_y<T>(y, r0.row, scaled, gamma);
   for (int q = 0; q < nsg; ++q) {
-    const RowRec<MAXD> cur = r0;
-    const bool hc = h0;
-    const T ycur = y0;
-    r0 = r1; h0 = h1;
-    if (h0) y0 = tri_load_y<T>(y, r0.row, scaled, gamma);
-    h2 = false;
-    if (q + 2 < nsg) { int p = seg_row(q + 2) + tid; h2 = p < seg_row(q + 3); if (h2) load_rec<MAXD, FP>(a, p, pb, r2); }
-    r1 = r2; h1 = h2;
+    const int k = q % L;
+    const int s0 = seg_row(q);
+    const int c = seg_row(q + 1) - s0;
+    mbar_wait(full + k, static_cast<unsigned>((q / L) & 1));
     if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 2] = gtime();
-    bar_sync(1, kTriBar1);  // deps of level q ready, level q-1 complete
+    bar_sync(1, kTriCompute);  // level q-1 values of this tile are in shared memory
     if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 3] = gtime();
-    if (hc) tri_row<T, CHECKED, MAXD>(a, cur, ycur, out, zt, stt);
-    const int s1 = seg_row(q + 1);
-    for (int p = seg_row(q) + tid + kTriCompute; p < s1; p += kTriCompute) {  // wide levels
+    if (tid < c) {
+      const unsigned char* slot = ring + static_cast<size_t>(k) * lay.ring_slot;
+      const unsigned char* rp = slot + static_cast<size_t>(tid) * REC;
       RowRec<MAXD> r;
-      load_rec<MAXD, FP>(a, p, pb, r);
-      tri_row<T, CHECKED, MAXD>(a, r, tri_load_y<T>(y, r.row, scaled, gamma), out, zt, stt);
+      const int4 hdr = *reinterpret_cast<const int4*>(rp);
+      r.row = hdr.x;
+      r.nd = hdr.y;
+      r.info = hdr.z;
+      r.xb = hdr.w;
+      r.mag = *reinterpret_cast<const u64*>(rp + 16);
+      r.diag = *reinterpret_cast<const i64*>(rp + 24);
+      r.slot = s0 + tid - pb;
+#pragma unroll
+      for (int d = 0; d < MAXD; ++d) {
+        r.ci[d] = *reinterpret_cast<const int*>(rp + 32 + 4 * d);
+        r.v[d] = *reinterpret_cast<const i64*>(rp + 32 + 4 * MAXD + 8 * d);
+      }
+      T yv = reinterpret_cast<const T*>(slot + kTriSegRows * REC)[tid];
+      if constexpr (FP) {
+        if (scaled) yv = __ddiv_rn(yv, gamma);
+      }
+      tri_row<T, CHECKED, MAXD>(a, r, yv, out, zt, stt);
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + k);
     if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 4] = gtime();
-    bar_arrive(2 + (q & (kTriPub - 1)), kTriCompute + 32);
   }
   if (CHECKED && !FP) {
     bump(cnt, OP_MUL, stt.nmul);
@@ -1385,6 +1489,10 @@ TriArgs tri_args(const DevTri& t) {
   a.p_mag = t.p_mag;
   a.p_info = t.p_info;
   a.p_diag = t.p_diag;
+  a.p_rec = t.p_rec;
+  a.tile_cap = t.tile_cap;
+  a.xz = t.xz;
+  a.epoch = 0;
   a.prog = t.prog;
   a.ticket = t.ticket;
   return a;
@@ -1580,23 +1688,37 @@ void launch_xupdate(cudaStream_t st, long long n, int m, int f, const i64* basis
 template <typename T, bool B, bool CK, int D>
 static void tri_launch_one(cudaStream_t st, const DevTri& t, const T* y, T* out, u64* cnt,
                            const Ctl* ctl, const double* prescale) {
-  // tile values + segment tables (staged when they fit)
+  constexpr size_t kBudget = 227 * 1024 - 256;  // static smem (tile id, caches) excluded
   int seg_cap = t.max_tile_segs + 2;
-  size_t sm = static_cast<size_t>(t.tile_cap + 1) * sizeof(T) + 2 * sizeof(int) * seg_cap + 16;
-  if (sm > 220 * 1024) {
+  static const int env_L = [] {
+    const char* e = std::getenv("IGM_TRI_L");
+    return e ? std::atoi(e) : 0;
+  }();
+  int L = env_L > 0 ? env_L : 2;
+  TriSmem lay = tri_smem_layout<T, D>(t.tile_cap, seg_cap, L);
+  while (L > 1 && lay.total > kBudget) lay = tri_smem_layout<T, D>(t.tile_cap, seg_cap, --L);
+  if (lay.total > kBudget) {  // segment tables stay in global memory
     seg_cap = 0;
-    sm = static_cast<size_t>(t.tile_cap + 1) * sizeof(T) + 16;
+    L = env_L > 0 ? env_L : 2;
+    lay = tri_smem_layout<T, D>(t.tile_cap, seg_cap, L);
+    while (L > 1 && lay.total > kBudget) lay = tri_smem_layout<T, D>(t.tile_cap, seg_cap, --L);
   }
+  const size_t sm = lay.total;
+  static const int env_sync = [] {
+    const char* e = std::getenv("IGM_TRI_SYNC_LOADER");
+    const int v = e ? std::atoi(e) : 0;
+    tri_loader_mode(v);
+    return v;
+  }();
+  (void)env_sync;
   static size_t done = 0;
   if (sm > done) {
     cudaFuncSetAttribute(k_tri<T, B, CK, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     done = sm;
   }
-  if (sm > 48 * 1024) {
-    // keep the L1 share for the record streams small, smem for the tile
-    cudaFuncSetAttribute(k_tri<T, B, CK, D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  }
-  k_tri<T, B, CK, D><<<t.ntiles, kTriThreads, sm, st>>>(tri_args(t), y, out, cnt, ctl, prescale, seg_cap);
+  TriArgs args = tri_args(t);
+  args.epoch = ++const_cast<DevTri&>(t).epoch;  // unique tag per launch
+  k_tri<T, B, CK, D><<<t.ntiles, kTriThreads, sm, st>>>(args, y, out, cnt, ctl, prescale, seg_cap, L);
 }
 
 template <typename T, bool B, bool CK>
@@ -1605,6 +1727,10 @@ static void tri_dispatch(cudaStream_t st, const DevTri& t, const T* y, T* out, u
   if (t.stride == 4) tri_launch_one<T, B, CK, 4>(st, t, y, out, cnt, ctl, prescale);
   else if (t.stride == 8) tri_launch_one<T, B, CK, 8>(st, t, y, out, cnt, ctl, prescale);
   else tri_launch_one<T, B, CK, 16>(st, t, y, out, cnt, ctl, prescale);
+}
+
+void tri_loader_mode(int sync_loader) {
+  cudaMemcpyToSymbol(g_tri_sync_loader, &sync_loader, sizeof(int));
 }
 
 void tri_trace_setup(int tile, unsigned long long* buf) {
@@ -1616,7 +1742,6 @@ void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* 
                     u64* cnt, const Ctl* ctl, bool checked) {
   if (t.n == 0) return;
   cudaMemsetAsync(t.ticket, 0, sizeof(int), st);
-  cudaMemsetAsync(t.prog, 0xff, sizeof(int) * t.ntiles, st);
   ProfScope prof_(st, KC_TRI_INT);
   if (backward) {
     if (checked) tri_dispatch<i64, true, true>(st, t, y, out, cnt, ctl, nullptr);
@@ -1632,7 +1757,6 @@ void launch_tri_fp(cudaStream_t st, const DevTri& t, bool backward, const double
                    const Ctl* ctl, const double* prescale) {
   if (t.n == 0) return;
   cudaMemsetAsync(t.ticket, 0, sizeof(int), st);
-  cudaMemsetAsync(t.prog, 0xff, sizeof(int) * t.ntiles, st);
   ProfScope prof_(st, KC_TRI_FP);
   if (backward) tri_dispatch<double, true, false>(st, t, y, out, nullptr, ctl, prescale);
   else tri_dispatch<double, false, false>(st, t, y, out, nullptr, ctl, prescale);

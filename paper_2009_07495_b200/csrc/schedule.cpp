@@ -4,6 +4,7 @@
 #include "fx_core.cuh"
 
 #include <algorithm>
+#include <cstring>
 #include <cmath>
 #include <numeric>
 #include <stdexcept>
@@ -113,7 +114,8 @@ TriSchedule build_tri_schedule(int n, const int* rp, const int* ci, const std::i
   }
   S.stride = S.maxd <= 4 ? 4 : (S.maxd <= 8 ? 8 : 16);
   // ---- tiles
-  const int cap = tile_cap_override > 0 ? std::min(tile_cap_override, 16384) : 16384;
+  const int cap = tile_cap_override > 0 ? std::min(tile_cap_override, tri_tile_cap(S.stride))
+                                        : tri_tile_cap(S.stride);
   S.tile_cap = cap;
   const int nsm = std::max(1, num_sms);
   std::vector<int> tile_of(static_cast<size_t>(n));
@@ -192,10 +194,14 @@ TriSchedule build_tri_schedule(int n, const int* rp, const int* ci, const std::i
   S.tile_seg.assign(static_cast<size_t>(S.ntiles) + 1, 0);
   S.seg_rows.push_back(0);
   for (int t = 0; t < S.ntiles; ++t) {
+    int seg_start = S.tile_pbase[t];
     for (int p = S.tile_pbase[t]; p < S.tile_pbase[t + 1]; ++p) {
-      if (p == S.tile_pbase[t] || lev[order[p]] != lev[order[p - 1]]) {
+      // a new segment per level, and wide levels split into <= 256-row parts
+      // (rows of one level are independent of each other)
+      if (p == S.tile_pbase[t] || lev[order[p]] != lev[order[p - 1]] || p - seg_start >= kTriSegRows) {
         if (p != S.tile_pbase[t]) S.seg_rows.push_back(p);
         S.seg_level.push_back(lev[order[p]]);
+        seg_start = p;
       }
     }
     if (S.tile_pbase[t + 1] > S.tile_pbase[t]) S.seg_rows.push_back(S.tile_pbase[t + 1]);
@@ -241,6 +247,27 @@ TriSchedule build_tri_schedule(int n, const int* rp, const int* ci, const std::i
     S.p_xdep.push_back(0);
     S.p_xval.push_back(0);
   }
+  // rows read by another tile are published as tagged 128-bit words
+  {
+    std::vector<char> exported(static_cast<size_t>(std::max(n, 1)), 0);
+    for (int i = 0; i < n; ++i)
+      for (int k = orp[i]; k < orp[i + 1]; ++k)
+        if (tile_of[oci[k]] != tile_of[i]) exported[oci[k]] = 1;
+    for (int p = 0; p < n; ++p)
+      if (exported[order[p]]) S.p_info[p] |= 1 << 10;
+  }
+  // packed records
+  S.rec_bytes = 32 + 12 * W;
+  S.p_rec.assign(static_cast<size_t>(std::max(n, 1)) * S.rec_bytes, 0);
+  for (int p = 0; p < n; ++p) {
+    unsigned char* r = S.p_rec.data() + static_cast<size_t>(p) * S.rec_bytes;
+    const int hdr[4] = {S.p_row[p], S.p_nd[p], S.p_info[p], S.p_xrp[p]};
+    std::memcpy(r, hdr, 16);
+    std::memcpy(r + 16, &S.p_mag[p], 8);
+    std::memcpy(r + 24, &S.p_diag[p], 8);
+    std::memcpy(r + 32, &S.p_dep[static_cast<size_t>(p) * W], 4 * W);
+    std::memcpy(r + 32 + 4 * W, &S.p_val[static_cast<size_t>(p) * W], 8 * W);
+  }
   // ---- per segment: producer tiles of its cross-tile dependencies
   S.seg_wptr.push_back(0);
   const int nseg = static_cast<int>(S.seg_level.size());
@@ -279,7 +306,8 @@ int validate_tri_schedule(const TriSchedule& S, const int* rp, const int* ci, bo
     if (slot_of[i] < 0) return 1;
   for (int t = 0; t < S.ntiles; ++t)
     for (int sg = S.tile_seg[t] + 1; sg < S.tile_seg[t + 1]; ++sg)
-      if (S.seg_level[sg] <= S.seg_level[sg - 1]) return 3;  // levels ascend in a tile
+      if (S.seg_level[sg] < S.seg_level[sg - 1] || S.seg_rows[sg + 1] - S.seg_rows[sg] > kTriSegRows)
+        return 3;  // levels non-decreasing in a tile, segments <= 256 rows
   const int W = S.stride;
   for (int i = 0; i < n; ++i) {
     const int p = slot_of[i];
@@ -303,7 +331,7 @@ int validate_tri_schedule(const TriSchedule& S, const int* rp, const int* ci, bo
         if (tk_j / layer > tk_i / layer) return 6;
         int sg = -1;
         for (int q = S.tile_seg[tile_of[i]]; q < S.tile_seg[tile_of[i] + 1]; ++q)
-          if (S.seg_level[q] == lev_of[i]) sg = q;
+          if (p >= S.seg_rows[q] && p < S.seg_rows[q + 1]) sg = q;
         bool listed = false;
         for (int w = S.seg_wptr[sg]; w < S.seg_wptr[sg + 1]; ++w) listed = listed || S.seg_wt[w] == tile_of[j];
         if (!listed) return 7;

@@ -43,12 +43,21 @@ struct TriSchedule {
   std::vector<std::uint64_t> p_mag;  // exact reciprocal of |diag|
   std::vector<int> p_info;
   std::vector<std::int64_t> p_diag;
+  // the same per-slot data as one packed record (what the kernel streams):
+  //   int32 row, nd, info, xb | u64 mag | i64 diag | int32 dep[stride] | i64 val[stride]
+  int rec_bytes = 0;                 // 32 + 12*stride (multiple of 16)
+  std::vector<unsigned char> p_rec;  // n * rec_bytes
 };
+
+constexpr int kTriSegRows = 256;  // rows per segment (one per compute thread)
 
 // rp/ci/vals: the factor (diagonal included); dpos: diagonal slot per row.
 // upper = backward substitution.  Throws std::invalid_argument on bad input.
 TriSchedule build_tri_schedule(int n, const int* rp, const int* ci, const std::int64_t* vals,
                                const int* dpos, bool upper, int num_sms, int tile_cap_override);
+
+// shared-memory tile capacity (rows) for a dependency stride
+inline int tri_tile_cap(int stride) { return stride <= 8 ? 16384 : 8192; }
 
 // Structural check of a schedule (CPU tests): every row scheduled once,
 // levels ascending inside a tile, tile-local dependencies resolved at a lower
