@@ -239,7 +239,83 @@ def run_reference(args, ws, rank):
     return 0
 
 
+# ----------------------------------------------------------------- config 5
+def run_cfg5(args, igm, dev, local, g=400, k=30):
+    """BASELINE.json configs[4]: 400^3 7-pt operator (alpha_a = 16, A_0 only),
+    one call = w = spmv(A, 0, v_30) then MGS of w against 30 int64 vectors
+    uniform in [-2^40, 2^40) (dot b1=16, b2=0; axpy b1=16), unchecked."""
+    import torch
+    t0 = time.time()
+    rp, ci, v = gen.upwind_3d_lean(g, 20.0)
+    vals, _ = igm.row_scale(rp, ci, v, 16)
+    del v
+    comp, al, _ = igm.build_split(vals, 16, 1)
+    del vals
+    n, nnz = len(rp) - 1, int(rp[-1])
+    S = igm.SplitMatrix(rp, ci, comp, al, device=dev)
+    del comp, rp, ci
+    dvc = f"cuda:{local}"
+    seed = gen.SEED_BASE ^ 5
+    basis = torch.empty((k, n), dtype=torch.int64, device=dvc)
+    for i in range(k):
+        basis[i] = gen.device_uniform_int40(n, seed, (i + 1) * n, dvc)
+    vin = gen.device_uniform_int40(n, seed, 0, dvc)
+    w = torch.empty(n, dtype=torch.int64, device=dvc)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+    stream = torch.cuda.ExternalStream(dev.stream, device=dvc)
+    for _ in range(max(args.warmup, 1)):
+        igm.spmv_mgs(S, 0, vin, basis, k, 30, 16, 0, 16, w)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        igm.spmv_mgs(S, 0, vin, basis, k, 30, 16, 0, 16, w)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    igm.lib().igm_profile_enable(1)
+    igm.spmv_mgs(S, 0, vin, basis, k, 30, 16, 0, 16, w)
+    igm.lib().igm_profile_enable(0)
+    kms = np.zeros(11)
+    kcnt = np.zeros(11, dtype=np.uint64)
+    igm.lib().igm_profile_collect(kms.ctypes.data_as(igm._capi.f64p), kcnt.ctypes.data_as(igm._capi.u64p))
+    b_spmv = 12 * nnz + 4 * (n + 1) + 16 * n
+    b_mgs = (4 * k + 1) * 8 * n
+    hbm, src = peaks()
+    mgs_gbs = b_mgs / (kms[3] / 1e3) / 1e9
+    spmv_gbs = b_spmv / (kms[0] / 1e3) / 1e9
+    call_gbs = (b_spmv + b_mgs) / (ms / 1e3) / 1e9
+    del S, basis, vin, w
+    torch.cuda.empty_cache()
+    return {
+        "workload": f"cfg5: SpMV (400^3 7-pt, alpha 16, s=0; n={n}, nnz={nnz}) + MGS against {k} int64 "
+                    "vectors uniform in [-2^40,2^40), unchecked",
+        "ms_per_call": ms, "bytes_per_call": b_spmv + b_mgs, "GB/s": round(call_gbs, 1),
+        "frac": round(call_gbs / hbm, 4), "peak": hbm, "peak_source": src,
+        "spmv": {"ms": round(float(kms[0]), 4), "GB/s": round(spmv_gbs, 1), "frac": round(spmv_gbs / hbm, 4)},
+        "mgs": {"ms": round(float(kms[3]), 4), "launches": int(kcnt[3]), "GB/s": round(mgs_gbs, 1),
+                "frac": round(mgs_gbs / hbm, 4), "bytes": b_mgs},
+        "setup_s": round(setup_s, 1), "l2": "vectors 512 MB each, far larger than L2",
+    }
+
+
 # ----------------------------------------------------------------- B200 arm
+def roofline_line(micro, dom, achieved, dom_bytes, hbm, src, top, breakdown):
+    """Dominant HBM-streaming kernel: the MGS pass in the config-5 call (all
+    operands from HBM); the config-2 view (L2-resident vectors) is attached."""
+    cfg2 = {"kernel": dom, "achieved": round(achieved, 1), "frac": round(achieved / hbm, 4),
+            "bytes_per_launch": dom_bytes, "top_device_time_class": top,
+            "top_class_note": "ilu_int is latency-bound (382-level wavefront), not bandwidth-bound"}
+    if micro and "mgs" in micro:
+        m = micro["mgs"]
+        return {"bound": "hbm", "kernel": "k_mgs (fused axpy_{i-1}+dot_i pass), config 5",
+                "achieved": m["GB/s"], "peak": hbm, "peak_source": src, "unit": "GB/s", "frac": m["frac"],
+                "traffic": None, "bytes_per_launch": m["bytes"] / max(1, m["launches"]), "cfg2": cfg2}
+    return {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm, "peak_source": src,
+            "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None, "cfg2": cfg2}
+
+
 def run_b200(args, ws, rank, local):
     import torch
     import paper_2009_07495_b200 as igm
@@ -324,6 +400,16 @@ def run_b200(args, ws, rank, local):
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
     top = max(breakdown, key=lambda k: breakdown[k]["ms"])
 
+    del S, A, F, d_b, d_x, hb, hx
+    torch.cuda.empty_cache()
+    micro = None
+    if not args.no_cfg5:
+        try:
+            micro = run_cfg5(args, igm, dev, local)
+        except Exception as exc:
+            micro = {"error": repr(exc)}
+        log(f"[bench] cfg5 microbench: {micro}")
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
@@ -347,10 +433,8 @@ def run_b200(args, ws, rank, local):
             "gpu_launches": int(launches),
             "e2e": {"value": e2e_val, "unit": "iters/s", "h2d_bytes_per_step": int(8 * n),
                     "d2h_bytes_per_step": int(8 * n)},
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm,
-                         "peak_source": src, "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                         "traffic": None,
-                         "note": f"algorithmic bytes per launch {dom_bytes:.3e}; top device-time class: {top}"},
+            "roofline": roofline_line(micro, dom, achieved, dom_bytes, hbm, src, top, breakdown),
+            "kernel_microbench": micro,
             "breakdown": breakdown,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
@@ -367,6 +451,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--grid", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cfg5", action="store_true", help="skip the config-5 kernel microbench")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     ws, rank, local = dist_init(args)

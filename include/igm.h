@@ -9,7 +9,10 @@
  * Memory: every vector/array argument may be HOST memory or DEVICE memory of
  * the context's GPU; the library detects which (cudaPointerGetAttributes) and
  * stages host buffers through its own device workspace.  Results are written
- * back into the same space the output pointer lives in.
+ * back into the same space the output pointer lives in.  Device buffers are
+ * accessed on the context's stream (igm_ctx_stream): the caller orders any
+ * producer stream before the call; every call returns with the stream
+ * synchronised unless documented otherwise (igm_spmv_mgs with h_out == NULL).
  *
  * Errors: every call returns igm_status; igm_last_error() returns the message
  * of the last failure on the calling thread.  Status codes map 1:1 onto the

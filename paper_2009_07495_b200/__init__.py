@@ -67,12 +67,19 @@ def _is_torch(a) -> bool:
 
 
 def _ptr(a, dtype):
-    """(void*, keepalive) for a numpy array or a torch tensor."""
+    """(void*, keepalive) for a numpy array or a torch tensor.
+
+    Device tensors are read/written on the library's own stream
+    (igm_ctx_stream); work queued on torch's current stream is ordered before
+    the call here (the C ABI leaves stream ordering to the caller)."""
     if a is None:
         return None, None
     if _is_torch(a):
         if not a.is_contiguous():
             raise ValueError("tensor must be contiguous")
+        if a.is_cuda:
+            import torch
+            torch.cuda.current_stream(a.device).synchronize()
         return C.c_void_p(a.data_ptr()), a
     arr = np.ascontiguousarray(a, dtype=dtype)
     return C.c_void_p(arr.ctypes.data), arr
@@ -516,6 +523,8 @@ def spmv_mgs(m: SplitMatrix, s: int, v_in, basis, k: int, f: int, dot_b1: int, d
              axpy_b1: int, w):
     """Config-5 kernel call on device tensors: w = A v_in, then MGS against k basis vectors."""
     h = np.zeros(k, dtype=np.int64)
+    for t in (v_in, basis, w):
+        _ptr(t, np.int64)  # orders torch's stream before the call
     _check(lib().igm_spmv_mgs(m.dev.h, m.h, s, C.c_void_p(v_in.data_ptr()), C.c_void_p(basis.data_ptr()),
                               k, f, dot_b1, dot_b2, axpy_b1, C.c_void_p(w.data_ptr()),
                               h.ctypes.data_as(_capi.i64p)))

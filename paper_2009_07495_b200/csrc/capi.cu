@@ -341,7 +341,7 @@ void build_tri(igm_ctx* c, DevTri& t, int n, const int* rp, const int* ci, const
   t.ntiles = S.ntiles;
   t.nseg = static_cast<int>(S.seg_level.size());
   t.nlevels = S.nlevels;
-  t.tile_cap = S.tile_cap;
+  t.tile_cap = std::max(1, S.max_tile_rows);  // shared-memory slots the kernel reserves
   for (int q = 0; q < S.ntiles; ++q)
     t.max_tile_segs = std::max(t.max_tile_segs, S.tile_seg[q + 1] - S.tile_seg[q]);
   for (int d = 0; d < 3; ++d) {

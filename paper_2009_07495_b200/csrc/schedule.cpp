@@ -4,6 +4,7 @@
 #include "fx_core.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <cmath>
 #include <numeric>
@@ -125,11 +126,19 @@ TriSchedule build_tri_schedule(int n, const int* rp, const int* ci, const std::i
     // x-y cross-section <= 256 rows (one row per compute thread per level),
     // then as deep in z as the shared-memory tile allows
     long long B[3] = {g.gx, g.gy, g.gz};
-    while (B[0] * B[1] > 256 && (B[0] > 1 || B[1] > 1)) {
+    static const long long xsec = [] {
+      const char* e = std::getenv("IGM_TRI_XSEC");
+      return e ? std::max(1LL, std::atoll(e)) : 256LL;
+    }();
+    static const long long zcap = [] {
+      const char* e = std::getenv("IGM_TRI_ZCAP");
+      return e ? std::max(1LL, std::atoll(e)) : (1LL << 40);
+    }();
+    while (B[0] * B[1] > xsec && (B[0] > 1 || B[1] > 1)) {
       if (B[0] >= B[1]) B[0] = cdiv(B[0], 2);
       else B[1] = cdiv(B[1], 2);
     }
-    while (B[0] * B[1] * B[2] > cap) B[2] = cdiv(B[2], 2);
+    while (B[0] * B[1] * B[2] > cap || B[2] > zcap) B[2] = cdiv(B[2], 2);
     auto assign = [&](const long long* b) {
       const long long nb0 = cdiv(G[0], b[0]), nb1 = cdiv(G[1], b[1]);
       for (int i = 0; i < n; ++i) {
@@ -187,9 +196,11 @@ TriSchedule build_tri_schedule(int n, const int* rp, const int* ci, const std::i
   S.tile_pbase.assign(static_cast<size_t>(S.ntiles) + 1, 0);
   for (int i = 0; i < n; ++i) S.tile_pbase[tile_of[i] + 1]++;
   for (int t = 0; t < S.ntiles; ++t) S.tile_pbase[t + 1] += S.tile_pbase[t];
-  for (int t = 0; t < S.ntiles; ++t)
+  for (int t = 0; t < S.ntiles; ++t) {
     if (S.tile_pbase[t + 1] - S.tile_pbase[t] > cap)
       throw std::logic_error("upload_ilu: tile exceeds shared-memory capacity");
+    S.max_tile_rows = std::max(S.max_tile_rows, S.tile_pbase[t + 1] - S.tile_pbase[t]);
+  }
   // segments
   S.tile_seg.assign(static_cast<size_t>(S.ntiles) + 1, 0);
   S.seg_rows.push_back(0);

@@ -302,3 +302,31 @@ def test_norm2_exact_parallel_chain(gpu, oracle):
         a = gpu.norm2(x)
         b = oracle.norm2(x)
         assert np.float64(a).tobytes() == np.float64(b).tobytes(), (len(x), a, b)
+
+
+@pytest.mark.parametrize("g,k", [(96, 30), (256, 8)])
+def test_spmv_mgs_large_vs_torch(gpu, g, k):
+    """Config-5 call at scale (n = g^3, vectors far beyond L2) against an
+    independent torch int64 implementation: wrapping products, arithmetic
+    shifts (floor), wrapping sums -- the same mod-2^64 algebra."""
+    import torch
+    from workloads import gen
+    rp, ci, v = gen.upwind_3d_lean(g, 20.0)
+    vals, _ = gpu.row_scale(rp, ci, v, 16)
+    comp, al, _ = gpu.build_split(vals, 16, 1)
+    S = gpu.SplitMatrix(rp, ci, comp, al)
+    n = len(rp) - 1
+    basis = torch.stack([gen.device_uniform_int40(n, 99, (i + 1) * n) for i in range(k)])
+    vin = gen.device_uniform_int40(n, 99, 0)
+    w = torch.empty(n, dtype=torch.int64, device="cuda")
+    hs = gpu.spmv_mgs(S, 0, vin, basis, k, 30, 16, 0, 16, w)
+    # torch reference
+    rows = torch.repeat_interleave(torch.arange(n, device="cuda"), torch.from_numpy(np.diff(rp).astype(np.int64)).cuda())
+    prod = torch.from_numpy(comp[0]).cuda() * vin[torch.from_numpy(ci.astype(np.int64)).cuda()]
+    wr = torch.zeros(n, dtype=torch.int64, device="cuda").index_add_(0, rows, prod)
+    for i in range(k):
+        acc = int(((wr >> 16) * basis[i]).sum().item())
+        h = acc >> 14  # fx_dot finalisation: e = f - b1 - b2 = 14
+        assert h == hs[i]
+        wr = wr - (((h >> 16) * basis[i]) >> 14)
+    assert torch.equal(wr, w)

@@ -181,3 +181,55 @@ def random_dominant(n: int, density: float, dominance: float, seed: int):
     rp[1:] = np.cumsum(mask.sum(axis=1))
     rr, cc = np.nonzero(mask)
     return rp, cc.astype(np.int32), dense[rr, cc].astype(np.float64)
+
+
+def upwind_3d_lean(g: int, beta: float = 20.0):
+    """upwind_3d() for large grids (config 5: 400^3) without n x 7 temporaries.
+
+    Same matrix, row for row, as upwind_3d(); rows are filled offset by
+    offset in ascending column order."""
+    h = 1.0 / (g + 1)
+    n = g * g * g
+    d = 6.0 / h ** 2 + 3 * beta / h
+    lo, hi = -1.0 / h ** 2 - beta / h, -1.0 / h ** 2
+    r = np.arange(n, dtype=np.int64)
+    i = (r % g).astype(np.int32)
+    j = ((r // g) % g).astype(np.int32)
+    k = (r // (g * g)).astype(np.int32)
+    del r
+    offs = [(k > 0, -g * g, lo), (j > 0, -g, lo), (i > 0, -1, lo), (None, 0, d),
+            (i < g - 1, 1, hi), (j < g - 1, g, hi), (k < g - 1, g * g, hi)]
+    counts = np.full(n, 1, dtype=np.int32)
+    for m, _, _ in offs:
+        if m is not None:
+            counts += m
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=row_ptr[1:])
+    del counts
+    nnz = int(row_ptr[-1])
+    col = np.empty(nnz, dtype=np.int32)
+    val = np.empty(nnz, dtype=np.float64)
+    cur = row_ptr[:-1].copy()
+    for m, off, c in offs:
+        idx = np.arange(n, dtype=np.int64) if m is None else np.nonzero(m)[0]
+        pos = cur[idx]
+        col[pos] = (idx + off).astype(np.int32)
+        val[pos] = c
+        cur[idx] += 1
+        del idx, pos
+    return row_ptr.astype(np.int32), col, val
+
+
+def device_uniform_int40(n: int, seed: int, offset: int, device="cuda"):
+    """Seeded SplitMix64 on the device (torch int64, wrapping), mapped to
+    integers uniform in [-2^40, 2^40): config 5's vector distribution
+    (bench_kernels.cpp:14-21 uses +-2^40)."""
+    import torch
+    to_i64 = lambda u: int(np.uint64(u).view(np.int64))
+    gold, m1, m2 = to_i64(0x9E3779B97F4A7C15), to_i64(0xBF58476D1CE4E5B9), to_i64(0x94D049BB133111EB)
+    z = torch.arange(offset + 1, offset + n + 1, dtype=torch.int64, device=device)
+    z = z * gold + to_i64(seed & 0xFFFFFFFFFFFFFFFF)
+    z = (z ^ ((z >> 30) & ((1 << 34) - 1))) * m1
+    z = (z ^ ((z >> 27) & ((1 << 37) - 1))) * m2
+    z = z ^ ((z >> 31) & ((1 << 33) - 1))
+    return ((z >> 23) & ((1 << 41) - 1)) - (1 << 40)
