@@ -366,6 +366,13 @@ void build_tri(igm_ctx* c, DevTri& t, int n, const int* rp, const int* ci, const
   t.p_diag = dupload(S.p_diag.data(), S.p_diag.size(), st);
   t.p_rec = dupload(S.p_rec.data(), S.p_rec.size(), st);
   t.rec_bytes = S.rec_bytes;
+  t.seg_xptr = dupload(S.seg_xptr.data(), S.seg_xptr.size(), st);
+  t.seg_xrow = dupload(S.seg_xrow.data(), S.seg_xrow.size(), st);
+  t.max_seg_ext = S.max_seg_ext;
+  t.c_rp = dupload(S.c_rp.data(), S.c_rp.size(), st);
+  t.c_ci = dupload(S.c_ci.data(), S.c_ci.size(), st);
+  t.c_val = dupload(S.c_val.data(), S.c_val.size(), st);
+  t.c_diag = dupload(S.c_diag.data(), std::max<size_t>(S.c_diag.size(), 1), st);
   t.xz = dalloc<ulonglong2>(static_cast<size_t>(std::max(n, 1)));
   ck(cudaMemsetAsync(t.xz, 0, sizeof(ulonglong2) * std::max(n, 1), st), "xz");
   t.prog = dalloc<int>(S.ntiles);
@@ -381,6 +388,8 @@ void free_tri(DevTri& t) {
                   static_cast<void*>(t.p_val), static_cast<void*>(t.p_xrp), static_cast<void*>(t.p_xdep),
                   static_cast<void*>(t.p_xval), static_cast<void*>(t.p_mag), static_cast<void*>(t.p_info),
                   static_cast<void*>(t.p_diag), static_cast<void*>(t.p_rec), static_cast<void*>(t.xz),
+                  static_cast<void*>(t.seg_xptr), static_cast<void*>(t.seg_xrow), static_cast<void*>(t.c_rp),
+                  static_cast<void*>(t.c_ci), static_cast<void*>(t.c_val), static_cast<void*>(t.c_diag),
                   static_cast<void*>(t.prog),
                   static_cast<void*>(t.ticket)})
     dfree(p);

@@ -89,6 +89,10 @@ struct DevTri {
   unsigned char* p_rec = nullptr;  // packed records, rec_bytes each
   int rec_bytes = 0;
   ulonglong2* xz = nullptr;        // n tagged exported values (128-bit each)
+  int *seg_xptr = nullptr, *seg_xrow = nullptr;
+  int max_seg_ext = 0;
+  int *c_rp = nullptr, *c_ci = nullptr;
+  i64 *c_val = nullptr, *c_diag = nullptr;
   unsigned long long epoch = 0;    // launches so far (tag of the next one)
   int* prog = nullptr;    // ntiles progress words
   int* ticket = nullptr;  // 1

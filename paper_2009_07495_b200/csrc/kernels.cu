@@ -1108,6 +1108,13 @@ struct TriArgs {
   int tile_cap;
   ulonglong2* xz;              // exported values: (value, epoch ^ mix(value)) per row
   unsigned long long epoch;    // unique per launch
+  const int* seg_xptr;         // per segment: cross-tile producer rows
+  const int* seg_xrow;
+  int max_seg_ext;
+  const int* c_rp;             // stripped factor, natural order (counting pass)
+  const int* c_ci;
+  const i64* c_val;
+  const i64* c_diag;
   int* prog;
   int* ticket;
 };
@@ -1193,10 +1200,23 @@ __device__ __forceinline__ u64 to_bits(T v) {
   else return static_cast<u64>(v);
 }
 
+// one cross-tile word (value, tag) loaded ahead of use
+__device__ __forceinline__ void xz_load(const ulonglong2* p, u64& v, u64& tg) {
+  asm volatile("{ .reg .b128 t; ld.global.relaxed.gpu.b128 t, [%2]; mov.b128 {%0, %1}, t; }"
+               : "=l"(v), "=l"(tg)
+               : "l"(p)
+               : "memory");
+}
+
 template <typename T, bool CHECKED>
-__device__ __forceinline__ void tri_term(int c, i64 lv, const ulonglong2* xz, u64 epoch, const T* zt,
+__device__ __forceinline__ void tri_term(int c, i64 lv, u64 xv, u64 xt, const TriArgs& a, const T* zt,
                                          T& acc, TriAcc<T, CHECKED>& st) {
-  const T zj = c >= 0 ? zt[c] : bits_to<T>(xz_wait(xz + ~c, epoch));
+  T zj;
+  if (c >= 0) {
+    zj = zt[c];  // tile-local value
+  } else {       // cross-tile: the word was loaded one level early; spin only if not yet valid
+    zj = bits_to<T>(xt == (a.epoch ^ xz_mix(xv)) ? xv : xz_wait(a.xz + ~c, a.epoch));
+  }
   if constexpr (std::is_same<T, double>::value) {
     acc = __dsub_rn(acc, __dmul_rn(__ll2double_rn(lv), zj));
   } else {
@@ -1211,13 +1231,14 @@ __device__ __forceinline__ void tri_term(int c, i64 lv, const ulonglong2* xz, u6
 
 template <typename T, bool CHECKED, int MAXD>
 __device__ __forceinline__ void tri_row(const TriArgs& a, const RowRec<MAXD>& r, T acc, T* out,
-                                        T* zt, TriAcc<T, CHECKED>& st) {
+                                        T* zt, const u64 (&xv)[MAXD], const u64 (&xt)[MAXD],
+                                        TriAcc<T, CHECKED>& st) {
 #pragma unroll
   for (int d = 0; d < MAXD; ++d)
-    if (d < r.nd) tri_term<T, CHECKED>(r.ci[d], r.v[d], a.xz, a.epoch, zt, acc, st);
+    if (d < r.nd) tri_term<T, CHECKED>(r.ci[d], r.v[d], xv[d], xt[d], a, zt, acc, st);
   for (int d = MAXD; d < r.nd; ++d)
-    tri_term<T, CHECKED>(__ldg(a.p_xdep + r.xb + d - MAXD), __ldg(a.p_xval + r.xb + d - MAXD), a.xz,
-                         a.epoch, zt, acc, st);
+    tri_term<T, CHECKED>(__ldg(a.p_xdep + r.xb + d - MAXD), __ldg(a.p_xval + r.xb + d - MAXD), 0,
+                         ~a.epoch /* never a valid tag for value 0: forces the spin path */, a, zt, acc, st);
   T z;
   if constexpr (std::is_same<T, double>::value) {
     z = __ddiv_rn(acc, __ll2double_rn(r.diag));
@@ -1312,7 +1333,7 @@ __device__ __forceinline__ void cp_async_mbar_arrive(void* bar) {
 // counter in a layer-major order, so every producer a thread waits on is
 // already running (schedule.hpp).
 constexpr int kTriCompute = 256;
-constexpr int kTriThreads = kTriCompute + 32;
+constexpr int kTriThreads = kTriCompute + 32;  // + loader warp
 
 struct TriSmem {  // byte offsets of the dynamic shared-memory regions
   size_t rows, lev, ring, bars, total;
@@ -1320,7 +1341,7 @@ struct TriSmem {  // byte offsets of the dynamic shared-memory regions
 };
 
 template <typename T, int MAXD>
-__host__ __device__ inline TriSmem tri_smem_layout(int tile_cap, int seg_cap, int L) {
+__host__ __device__ inline TriSmem tri_smem_layout(int tile_cap, int seg_cap, int L, int max_ext) {
   constexpr int REC = 32 + 12 * MAXD;
   TriSmem m;
   size_t o = (static_cast<size_t>(tile_cap) * sizeof(T) + 15) & ~size_t(15);
@@ -1330,11 +1351,11 @@ __host__ __device__ inline TriSmem tri_smem_layout(int tile_cap, int seg_cap, in
   o += sizeof(int) * static_cast<size_t>(seg_cap);
   o = (o + 127) & ~size_t(127);
   m.ring = o;
-  m.ring_slot = kTriSegRows * (REC + 8);
+  m.ring_slot = kTriSegRows * (REC + 8) + ((8 * max_ext + 15) & ~15);
   o += static_cast<size_t>(L) * m.ring_slot;
   o = (o + 15) & ~size_t(15);
   m.bars = o;
-  o += 16 * static_cast<size_t>(L);
+  o += 24 * static_cast<size_t>(L);  // full, empty, xfull
   m.total = o;
   return m;
 }
@@ -1348,7 +1369,7 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ int s_tile;
   if (cycle_over(ctl)) return;
-  const TriSmem lay = tri_smem_layout<T, MAXD>(a.tile_cap, seg_cap, L);
+  const TriSmem lay = tri_smem_layout<T, MAXD>(a.tile_cap, seg_cap, L, a.max_seg_ext);
   T* zt = reinterpret_cast<T*>(smem_raw);
   int* s_rows = reinterpret_cast<int*>(smem_raw + lay.rows);
   unsigned char* ring = smem_raw + lay.ring;
@@ -1427,39 +1448,65 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
   const double gamma = scaled ? __longlong_as_double(*reinterpret_cast<const long long*>(prescale)) : 1.0;
   TriAcc<T, CHECKED> stt;
   const int tid = threadIdx.x;
+  auto read_rec = [&](int q, RowRec<MAXD>& r) {
+    const unsigned char* rp = ring + static_cast<size_t>(q % L) * lay.ring_slot + static_cast<size_t>(tid) * REC;
+    const int4 hdr = *reinterpret_cast<const int4*>(rp);
+    r.row = hdr.x;
+    r.nd = hdr.y;
+    r.info = hdr.z;
+    r.xb = hdr.w;
+    r.mag = *reinterpret_cast<const u64*>(rp + 16);
+    r.diag = *reinterpret_cast<const i64*>(rp + 24);
+    r.slot = seg_row(q) + tid - pb;
+#pragma unroll
+    for (int d = 0; d < MAXD; ++d) {
+      r.ci[d] = *reinterpret_cast<const int*>(rp + 32 + 4 * d);
+      r.v[d] = *reinterpret_cast<const i64*>(rp + 32 + 4 * MAXD + 8 * d);
+    }
+  };
+  // cross-tile words of the NEXT level, issued before this level's barrier
+  RowRec<MAXD> nrec;
+  u64 nxv[MAXD], nxt[MAXD];
+  bool nhave = false;
+  auto prefetch = [&](int q) {
+    nhave = false;
+    if (q >= nsg) return;
+    mbar_wait(full + q % L, static_cast<unsigned>((q / L) & 1));
+    if (tid >= seg_row(q + 1) - seg_row(q)) return;
+    read_rec(q, nrec);
+    nhave = true;
+#pragma unroll
+    for (int d = 0; d < MAXD; ++d) {
+      nxv[d] = 0;
+      nxt[d] = 0;  // only read for cross-tile dependencies, which are always loaded
+      if (d < nrec.nd && nrec.ci[d] < 0) xz_load(a.xz + ~nrec.ci[d], nxv[d], nxt[d]);
+    }
+  };
+  prefetch(0);
   for (int q = 0; q < nsg; ++q) {
     const int k = q % L;
-    const int s0 = seg_row(q);
-    const int c = seg_row(q + 1) - s0;
-    mbar_wait(full + k, static_cast<unsigned>((q / L) & 1));
+    const RowRec<MAXD> cur = nrec;
+    u64 xv[MAXD], xt[MAXD];
+#pragma unroll
+    for (int d = 0; d < MAXD; ++d) {
+      xv[d] = nxv[d];
+      xt[d] = nxt[d];
+    }
+    const bool hc = nhave;
     if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 2] = gtime();
     bar_sync(1, kTriCompute);  // level q-1 values of this tile are in shared memory
     if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 3] = gtime();
-    if (tid < c) {
+    if (hc) {
       const unsigned char* slot = ring + static_cast<size_t>(k) * lay.ring_slot;
-      const unsigned char* rp = slot + static_cast<size_t>(tid) * REC;
-      RowRec<MAXD> r;
-      const int4 hdr = *reinterpret_cast<const int4*>(rp);
-      r.row = hdr.x;
-      r.nd = hdr.y;
-      r.info = hdr.z;
-      r.xb = hdr.w;
-      r.mag = *reinterpret_cast<const u64*>(rp + 16);
-      r.diag = *reinterpret_cast<const i64*>(rp + 24);
-      r.slot = s0 + tid - pb;
-#pragma unroll
-      for (int d = 0; d < MAXD; ++d) {
-        r.ci[d] = *reinterpret_cast<const int*>(rp + 32 + 4 * d);
-        r.v[d] = *reinterpret_cast<const i64*>(rp + 32 + 4 * MAXD + 8 * d);
-      }
       T yv = reinterpret_cast<const T*>(slot + kTriSegRows * REC)[tid];
       if constexpr (FP) {
         if (scaled) yv = __ddiv_rn(yv, gamma);
       }
-      tri_row<T, CHECKED, MAXD>(a, r, yv, out, zt, stt);
+      tri_row<T, CHECKED, MAXD>(a, cur, yv, out, zt, xv, xt, stt);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + k);
+    prefetch(q + 1);
     if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 4] = gtime();
   }
   if (CHECKED && !FP) {
@@ -1467,6 +1514,35 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
     bump(cnt, OP_SUB, stt.nsub);
     bump(cnt, OP_DIV, stt.ndiv);
   }
+}
+
+// Checked-mode overflow events of one integer substitution (ilu.cpp:126-153),
+// counted AFTER the wavefront from its inputs and outputs: every row's
+// products and subtractions are known once z is, so this is a fully parallel
+// pass and the 3g-level critical path stays free of overflow tests.
+__global__ void __launch_bounds__(256) k_tri_count(int n, const int* __restrict__ rp,
+                                                   const int* __restrict__ ci,
+                                                   const i64* __restrict__ val,
+                                                   const i64* __restrict__ diag,
+                                                   const i64* __restrict__ y,
+                                                   const i64* __restrict__ z, u64* cnt,
+                                                   const Ctl* ctl) {
+  if (cycle_over(ctl)) return;
+  u64 nmul = 0, nsub = 0, ndiv = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    i64 acc = y[i];
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+      const i64 l = val[k], zj = z[ci[k]];
+      const i64 p = wmul(l, zj);
+      nmul += mul_ovf(l, zj);
+      nsub += sub_ovf(acc, p);
+      acc = wsub(acc, p);
+    }
+    ndiv += (acc == INT64_MIN && diag[i] == -1);
+  }
+  bump(cnt, OP_MUL, nmul);
+  bump(cnt, OP_SUB, nsub);
+  bump(cnt, OP_DIV, ndiv);
 }
 
 TriArgs tri_args(const DevTri& t) {
@@ -1493,6 +1569,13 @@ TriArgs tri_args(const DevTri& t) {
   a.tile_cap = t.tile_cap;
   a.xz = t.xz;
   a.epoch = 0;
+  a.seg_xptr = t.seg_xptr;
+  a.seg_xrow = t.seg_xrow;
+  a.max_seg_ext = t.max_seg_ext;
+  a.c_rp = t.c_rp;
+  a.c_ci = t.c_ci;
+  a.c_val = t.c_val;
+  a.c_diag = t.c_diag;
   a.prog = t.prog;
   a.ticket = t.ticket;
   return a;
@@ -1694,14 +1777,14 @@ static void tri_launch_one(cudaStream_t st, const DevTri& t, const T* y, T* out,
     const char* e = std::getenv("IGM_TRI_L");
     return e ? std::atoi(e) : 0;
   }();
-  int L = env_L > 0 ? env_L : 2;
-  TriSmem lay = tri_smem_layout<T, D>(t.tile_cap, seg_cap, L);
-  while (L > 1 && lay.total > kBudget) lay = tri_smem_layout<T, D>(t.tile_cap, seg_cap, --L);
+  int L = env_L > 0 ? env_L : 8;
+  TriSmem lay = tri_smem_layout<T, D>(t.tile_cap, seg_cap, L, t.max_seg_ext);
+  while (L > 1 && lay.total > kBudget) lay = tri_smem_layout<T, D>(t.tile_cap, seg_cap, --L, t.max_seg_ext);
   if (lay.total > kBudget) {  // segment tables stay in global memory
     seg_cap = 0;
-    L = env_L > 0 ? env_L : 2;
-    lay = tri_smem_layout<T, D>(t.tile_cap, seg_cap, L);
-    while (L > 1 && lay.total > kBudget) lay = tri_smem_layout<T, D>(t.tile_cap, seg_cap, --L);
+    L = env_L > 0 ? env_L : 8;
+    lay = tri_smem_layout<T, D>(t.tile_cap, seg_cap, L, t.max_seg_ext);
+    while (L > 1 && lay.total > kBudget) lay = tri_smem_layout<T, D>(t.tile_cap, seg_cap, --L, t.max_seg_ext);
   }
   const size_t sm = lay.total;
   static const int env_sync = [] {
@@ -1742,15 +1825,17 @@ void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* 
                     u64* cnt, const Ctl* ctl, bool checked) {
   if (t.n == 0) return;
   cudaMemsetAsync(t.ticket, 0, sizeof(int), st);
-  ProfScope prof_(st, KC_TRI_INT);
-  if (backward) {
-    if (checked) tri_dispatch<i64, true, true>(st, t, y, out, cnt, ctl, nullptr);
-    else tri_dispatch<i64, true, false>(st, t, y, out, cnt, ctl, nullptr);
-  } else {
-    if (checked) tri_dispatch<i64, false, true>(st, t, y, out, cnt, ctl, nullptr);
+  {
+    ProfScope prof_(st, KC_TRI_INT);
+    if (backward) tri_dispatch<i64, true, false>(st, t, y, out, cnt, ctl, nullptr);
     else tri_dispatch<i64, false, false>(st, t, y, out, cnt, ctl, nullptr);
   }
   LAUNCH_CHECK();
+  if (checked) {
+    ProfScope prof_(st, KC_OTHER);
+    k_tri_count<<<grid_for(t.n, 256), 256, 0, st>>>(t.n, t.c_rp, t.c_ci, t.c_val, t.c_diag, y, out, cnt, ctl);
+    LAUNCH_CHECK();
+  }
 }
 
 void launch_tri_fp(cudaStream_t st, const DevTri& t, bool backward, const double* y, double* out,

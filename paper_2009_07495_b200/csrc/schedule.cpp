@@ -222,6 +222,39 @@ TriSchedule build_tri_schedule(int n, const int* rp, const int* ci, const std::i
     S.seg_level.push_back(0);
     S.seg_rows.push_back(0);
   }
+  // ---- per segment: distinct cross-tile producer rows (staged by the
+  // kernel's prefetch warp); position of each in its segment's list
+  const int nseg_all = static_cast<int>(S.seg_level.size());
+  S.seg_xptr.assign(static_cast<size_t>(nseg_all) + 1, 0);
+  std::vector<int> seg_of_slot(static_cast<size_t>(std::max(n, 1)), 0);
+  for (int sg = 0; sg < nseg_all; ++sg)
+    for (int p = S.seg_rows[sg]; p < S.seg_rows[sg + 1] && p < n; ++p) seg_of_slot[p] = sg;
+  std::vector<int> xpos_of;  // per (slot, dep) position, filled below in record order
+  for (int sg = 0; sg < nseg_all; ++sg) {
+    const size_t x0 = S.seg_xrow.size();
+    for (int p = S.seg_rows[sg]; p < S.seg_rows[sg + 1] && p < n; ++p) {
+      const int i = order[p];
+      for (int k = orp[i]; k < orp[i + 1]; ++k) {
+        const int j = oci[k];
+        if (tile_of[j] == tile_of[i]) continue;
+        if (std::find(S.seg_xrow.begin() + static_cast<std::ptrdiff_t>(x0), S.seg_xrow.end(), j) == S.seg_xrow.end())
+          S.seg_xrow.push_back(j);
+      }
+    }
+    S.seg_xptr[sg + 1] = static_cast<int>(S.seg_xrow.size());
+    S.max_seg_ext = std::max(S.max_seg_ext, S.seg_xptr[sg + 1] - S.seg_xptr[sg]);
+  }
+  if (S.seg_xrow.empty()) S.seg_xrow.push_back(0);
+  // ---- stripped factor in natural order (counting pass)
+  S.c_rp = orp;
+  S.c_ci = oci;
+  S.c_val = ov;
+  S.c_diag = dg;
+  if (S.c_ci.empty()) {
+    S.c_ci.push_back(0);
+    S.c_val.push_back(0);
+  }
+  if (S.c_diag.empty()) S.c_diag.push_back(1);
   // ---- per-slot records
   const int W = S.stride;
   S.p_row.resize(static_cast<size_t>(std::max(n, 1)));

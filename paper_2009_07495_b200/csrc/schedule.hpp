@@ -48,6 +48,14 @@ struct TriSchedule {
   //   int32 row, nd, info, xb | u64 mag | i64 diag | int32 dep[stride] | i64 val[stride]
   int rec_bytes = 0;                 // 32 + 12*stride (multiple of 16)
   std::vector<unsigned char> p_rec;  // n * rec_bytes
+  // cross-tile dependencies of each segment: distinct producer rows; a
+  // record's external dependency is encoded as ~(index into this list)
+  std::vector<int> seg_xptr;  // nseg+1
+  std::vector<int> seg_xrow;
+  int max_seg_ext = 0;
+  // the stripped factor in natural row order (checked-mode counting pass)
+  std::vector<int> c_rp, c_ci;
+  std::vector<std::int64_t> c_val, c_diag;
 };
 
 constexpr int kTriSegRows = 256;  // rows per segment (one per compute thread)
