@@ -1253,8 +1253,54 @@ __device__ __forceinline__ void tri_row(const TriArgs& a, const RowRec<MAXD>& r,
     z = sdiv(acc, gm);
   }
   zt[r.slot] = z;
+#ifndef IGM_TRI_NOSTORE
   out[r.row] = z;
   if (r.info & (1 << 10)) xz_put(a.xz + r.row, to_bits<T>(z), a.epoch);  // read by another tile
+#endif
+}
+
+// Integer row, straight-line: every one of the MAXD dependency slots is used
+// (unused slots are padded with factor 0 and local slot 0 at upload, which
+// adds exact zeros mod 2^64), the products are independent and summed as a
+// tree (integer wrapping sums are order-free), cross-tile words were loaded
+// one level early and are only re-polled if their tag is not yet valid.
+template <int MAXD>
+__device__ __forceinline__ i64 tri_row_int_fast(const TriArgs& a, const RowRec<MAXD>& r, i64 y,
+                                                const i64* zt, const u64 (&xv)[MAXD],
+                                                const u64 (&xt)[MAXD]) {
+  i64 z[MAXD];
+#pragma unroll
+  for (int d = 0; d < MAXD; ++d) z[d] = zt[r.ci[d] < 0 ? 0 : r.ci[d]];
+  bool stale = false;
+#pragma unroll
+  for (int d = 0; d < MAXD; ++d) {
+    if (r.ci[d] < 0) {
+      z[d] = static_cast<i64>(xv[d]);
+      stale |= xt[d] != (a.epoch ^ xz_mix(xv[d]));
+    }
+  }
+  if (stale) {  // a producer tile had not published yet when the word was loaded
+#pragma unroll
+    for (int d = 0; d < MAXD; ++d)
+      if (r.ci[d] < 0 && xt[d] != (a.epoch ^ xz_mix(xv[d])))
+        z[d] = static_cast<i64>(xz_wait(a.xz + ~r.ci[d], a.epoch));
+  }
+  u64 s = 0;
+#pragma unroll
+  for (int d = 0; d < MAXD; ++d) s += static_cast<u64>(r.v[d]) * static_cast<u64>(z[d]);
+  for (int d = MAXD; d < r.nd; ++d) {  // rows wider than the record stride (rare)
+    const int c = __ldg(a.p_xdep + r.xb + d - MAXD);
+    const i64 zj = c >= 0 ? zt[c] : static_cast<i64>(xz_wait(a.xz + ~c, a.epoch));
+    s += static_cast<u64>(__ldg(a.p_xval + r.xb + d - MAXD)) * static_cast<u64>(zj);
+  }
+  const i64 acc = static_cast<i64>(static_cast<u64>(y) - s);
+  SDivMagic gm;
+  gm.u.m = r.mag;
+  gm.u.sh1 = r.info & 1;
+  gm.u.sh2 = (r.info >> 1) & 127;
+  gm.den_neg = (r.info >> 8) & 1;
+  gm.den_is_m1 = (r.info >> 9) & 1;
+  return sdiv(acc, gm);
 }
 
 template <typename T>
@@ -1395,14 +1441,20 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
   auto seg_row = [&](int q) { return seg_in_smem ? s_rows[q] : __ldg(a.seg_rows + sb + q); };
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+#ifdef IGM_TRI_TRACE
   unsigned long long* tsb = (!BACKWARD && g_tri_ts != nullptr && tile == g_tri_ts_tile) ? g_tri_ts : nullptr;
+#else
+  constexpr unsigned long long* tsb = nullptr;  // phase timestamps compiled out
+#endif
 
   if (warp == 8) {  // ---------------- loader
-    // row ids of the next level are loaded one iteration ahead (registers),
-    // so the right-hand-side gathers never wait on a dependent load
+    // row ids are loaded D levels ahead (register pipeline), so the
+    // right-hand-side gathers never wait on a dependent load
     constexpr int RPL = kTriSegRows / 32;  // rows per lane per level
-    int rows_nx[RPL];
+    constexpr int D = 4;
+    int rows[D][RPL];
     auto load_rows = [&](int q, int (&rr)[RPL]) {
+      if (q >= nsg) return;
       const int s0 = seg_row(q), c = seg_row(q + 1) - s0;
 #pragma unroll
       for (int t = 0; t < RPL; ++t) {
@@ -1410,36 +1462,45 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
         rr[t] = r < c ? __ldg(a.p_row + s0 + r) : 0;
       }
     };
-    if (nsg > 0) load_rows(0, rows_nx);
-    for (int q = 0; q < nsg; ++q) {
-      const int k = q % L;
-      int rows[RPL];
 #pragma unroll
-      for (int t = 0; t < RPL; ++t) rows[t] = rows_nx[t];
-      if (q >= L) mbar_wait(empty + k, static_cast<unsigned>((q / L - 1) & 1));
-      const int s0 = seg_row(q), c = seg_row(q + 1) - s0;
-      unsigned char* slot = ring + static_cast<size_t>(k) * lay.ring_slot;
-      T* yslot = reinterpret_cast<T*>(slot + kTriSegRows * REC);
-      if (g_tri_sync_loader) {  // A/B: synchronous copy through registers
-        const int4* src = reinterpret_cast<const int4*>(a.p_rec + static_cast<size_t>(s0) * REC);
-        int4* dst = reinterpret_cast<int4*>(slot);
-        for (int i = lane; i < c * REC / 16; i += 32) dst[i] = __ldg(src + i);
+    for (int d = 0; d < D; ++d) load_rows(d, rows[d]);
+    int k = 0;
+    unsigned ph = 1;  // parity of the previous use of slot k (first L levels: none)
+    for (int q0 = 0; q0 < nsg; q0 += D) {
 #pragma unroll
-        for (int t = 0; t < RPL; ++t)
-          if (lane + 32 * t < c) yslot[lane + 32 * t] = y[rows[t]];
-        __syncwarp();
-        mbar_arrive(full + k);
-      } else {
-        if (lane == 0) {
-          mbar_arrive_expect_tx(full + k, static_cast<unsigned>(c * REC));
-          bulk_g2s(slot, a.p_rec + static_cast<size_t>(s0) * REC, static_cast<unsigned>(c * REC), full + k);
+      for (int d = 0; d < D; ++d) {  // unrolled so rows[d] stays in registers
+        const int q = q0 + d;
+        if (q >= nsg) break;
+        if (q >= L) mbar_wait(empty + k, ph);
+        const int s0 = seg_row(q), c = seg_row(q + 1) - s0;
+        unsigned char* slot = ring + static_cast<size_t>(k) * lay.ring_slot;
+        T* yslot = reinterpret_cast<T*>(slot + kTriSegRows * REC);
+        if (g_tri_sync_loader) {  // A/B: synchronous copy through registers
+          const int4* src = reinterpret_cast<const int4*>(a.p_rec + static_cast<size_t>(s0) * REC);
+          int4* dst = reinterpret_cast<int4*>(slot);
+          for (int i = lane; i < c * REC / 16; i += 32) dst[i] = __ldg(src + i);
+#pragma unroll
+          for (int t = 0; t < RPL; ++t)
+            if (lane + 32 * t < c) yslot[lane + 32 * t] = y[rows[d][t]];
+          __syncwarp();
+          mbar_arrive(full + k);
+        } else {
+          if (lane == 0) {
+            mbar_arrive_expect_tx(full + k, static_cast<unsigned>(c * REC));
+            bulk_g2s(slot, a.p_rec + static_cast<size_t>(s0) * REC, static_cast<unsigned>(c * REC), full + k);
+          }
+#pragma unroll
+          for (int t = 0; t < RPL; ++t)
+            if (lane + 32 * t < c) cp_async8(yslot + lane + 32 * t, y + rows[d][t]);
+          cp_async_mbar_arrive(full + k);
         }
-#pragma unroll
-        for (int t = 0; t < RPL; ++t)
-          if (lane + 32 * t < c) cp_async8(yslot + lane + 32 * t, y + rows[t]);
-        cp_async_mbar_arrive(full + k);
+        if (tsb && lane == 0 && q < 2048) tsb[q * 8 + 7] = gtime();
+        load_rows(q + D, rows[d]);
+        if (++k == L) {
+          k = 0;
+          ph ^= 1u;
+        }
       }
-      if (q + 1 < nsg) load_rows(q + 1, rows_nx);
     }
     return;
   }
@@ -1448,43 +1509,53 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
   const double gamma = scaled ? __longlong_as_double(*reinterpret_cast<const long long*>(prescale)) : 1.0;
   TriAcc<T, CHECKED> stt;
   const int tid = threadIdx.x;
-  auto read_rec = [&](int q, RowRec<MAXD>& r) {
-    const unsigned char* rp = ring + static_cast<size_t>(q % L) * lay.ring_slot + static_cast<size_t>(tid) * REC;
+  // one row per thread per level: the per-level critical path is this warp's
+  // in-order instruction stream, so everything loop-invariant or derivable
+  // incrementally stays out of it
+  auto read_rec = [&](const unsigned char* slotp, int s0, RowRec<MAXD>& r) {
+    const unsigned char* rp = slotp + static_cast<size_t>(tid) * REC;
     const int4 hdr = *reinterpret_cast<const int4*>(rp);
     r.row = hdr.x;
     r.nd = hdr.y;
     r.info = hdr.z;
     r.xb = hdr.w;
-    r.mag = *reinterpret_cast<const u64*>(rp + 16);
-    r.diag = *reinterpret_cast<const i64*>(rp + 24);
-    r.slot = seg_row(q) + tid - pb;
+    if (FP) r.diag = *reinterpret_cast<const i64*>(rp + 24);
+    else r.mag = *reinterpret_cast<const u64*>(rp + 16);
+    r.slot = s0 + tid - pb;
 #pragma unroll
     for (int d = 0; d < MAXD; ++d) {
       r.ci[d] = *reinterpret_cast<const int*>(rp + 32 + 4 * d);
       r.v[d] = *reinterpret_cast<const i64*>(rp + 32 + 4 * MAXD + 8 * d);
     }
   };
-  // cross-tile words of the NEXT level, issued before this level's barrier
+  // record + cross-tile words of the NEXT level, issued before this level's barrier
   RowRec<MAXD> nrec;
   u64 nxv[MAXD], nxt[MAXD];
   bool nhave = false;
+  int kn = 0;          // ring slot of the next level
+  unsigned phn = 0;    // its mbarrier phase parity
+  int s_next = seg_row(0);
   auto prefetch = [&](int q) {
     nhave = false;
     if (q >= nsg) return;
-    mbar_wait(full + q % L, static_cast<unsigned>((q / L) & 1));
-    if (tid >= seg_row(q + 1) - seg_row(q)) return;
-    read_rec(q, nrec);
+    mbar_wait(full + kn, phn);
+    const int s1 = seg_row(q + 1);
+    const int s0 = s_next;
+    s_next = s1;
+    if (tid >= s1 - s0) return;
+    read_rec(ring + static_cast<size_t>(kn) * lay.ring_slot, s0, nrec);
     nhave = true;
 #pragma unroll
-    for (int d = 0; d < MAXD; ++d) {
-      nxv[d] = 0;
-      nxt[d] = 0;  // only read for cross-tile dependencies, which are always loaded
+    for (int d = 0; d < MAXD; ++d)
       if (d < nrec.nd && nrec.ci[d] < 0) xz_load(a.xz + ~nrec.ci[d], nxv[d], nxt[d]);
-    }
   };
   prefetch(0);
   for (int q = 0; q < nsg; ++q) {
-    const int k = q % L;
+    const int k = kn;
+    if (++kn == L) {
+      kn = 0;
+      phn ^= 1u;
+    }
     const RowRec<MAXD> cur = nrec;
     u64 xv[MAXD], xt[MAXD];
 #pragma unroll
@@ -1496,16 +1567,31 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
     if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 2] = gtime();
     bar_sync(1, kTriCompute);  // level q-1 values of this tile are in shared memory
     if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 3] = gtime();
+#ifdef IGM_TRI_SKELETON
+    if (false) {
+#else
     if (hc) {
+#endif
       const unsigned char* slot = ring + static_cast<size_t>(k) * lay.ring_slot;
       T yv = reinterpret_cast<const T*>(slot + kTriSegRows * REC)[tid];
       if constexpr (FP) {
         if (scaled) yv = __ddiv_rn(yv, gamma);
       }
-      tri_row<T, CHECKED, MAXD>(a, cur, yv, out, zt, xv, xt, stt);
+      if constexpr (FP) {
+        tri_row<T, CHECKED, MAXD>(a, cur, yv, out, zt, xv, xt, stt);
+      } else {
+        const i64 z = tri_row_int_fast<MAXD>(a, cur, yv, zt, xv, xt);
+        zt[cur.slot] = z;
+#ifndef IGM_TRI_NOSTORE
+        out[cur.row] = z;
+        if (cur.info & (1 << 10)) xz_put(a.xz + cur.row, static_cast<u64>(z), a.epoch);
+#endif
+      }
     }
+    if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 5] = gtime();
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + k);
+    if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 6] = gtime();
     prefetch(q + 1);
     if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 4] = gtime();
   }

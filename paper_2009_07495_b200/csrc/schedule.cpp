@@ -259,6 +259,7 @@ TriSchedule build_tri_schedule(int n, const int* rp, const int* ci, const std::i
   const int W = S.stride;
   S.p_row.resize(static_cast<size_t>(std::max(n, 1)));
   S.p_nd.resize(static_cast<size_t>(std::max(n, 1)));
+  // unused dependency slots: local slot 0 with factor 0 (an exact zero term)
   S.p_dep.assign(static_cast<size_t>(std::max(n, 1)) * W, 0);
   S.p_val.assign(static_cast<size_t>(std::max(n, 1)) * W, 0);
   S.p_xrp.assign(static_cast<size_t>(n) + 1, 0);

@@ -19,16 +19,19 @@ for tile in (0, 1, 9, 63, 127):
     lib.igm_debug_tri_trace(tile, C.c_void_p(buf.data_ptr()))
     z = igm.apply_inverse(F, y)
     torch.cuda.synchronize()
-    ts = buf.cpu().numpy().reshape(-1, 8)[:, :7].astype(np.float64)
+    ts = buf.cpu().numpy().reshape(-1, 8)[:, :8].astype(np.float64)
     ts = ts[ts[:, 3] > 0]
-    t0 = ts[:, :].min()
+    t0 = ts[:, 2:8].min()
     ts -= t0
     ts /= 1.9  # cycles -> ns at ~1.9 GHz
     print(f"tile {tile}: segs {len(ts)} start {ts[0,3]/1e3:.1f}us end {ts[-1,4]/1e3:.1f}us")
     per = np.diff(ts[:, 3])
-    print("  level period med %.0f mean %.0f ns | poll med %.0f | compute(post->done) med %.0f | presync wait(pre->post) med %.0f | pub (sync->done) med %.0f | done->pubsync %.0f" % (
-        np.median(per), per.mean(), np.median(ts[:, 1] - ts[:, 0]), np.median(ts[:, 4] - ts[:, 3]),
-        np.median(ts[:, 3] - ts[:, 2]), np.median(ts[:, 6] - ts[:, 5]), np.median(ts[:, 5] - ts[:, 4])))
+    print("  level period med %.0f mean %.0f ns | barrier wait %.0f | row %.0f | syncwarp+arrive %.0f | prefetch next %.0f" % (
+        np.median(per), per.mean(), np.median(ts[:, 3] - ts[:, 2]), np.median(ts[:, 5] - ts[:, 3]),
+        np.median(ts[:, 6] - ts[:, 5]), np.median(ts[:, 4] - ts[:, 6])))
+    lead = ts[1:, 2] - ts[1:, 7]   # compute reaches level q  minus  loader issued level q
+    print("  loader lead over compute: med %.0f ns, min %.0f; loader period med %.0f ns" % (
+        np.median(lead), lead.min(), np.median(np.diff(ts[:, 7]))))
     for r in ts[5:8]:
         print("   ", " ".join(f"{x/1e3:8.2f}" for x in r))
 lib.igm_debug_tri_trace(-1, None)
