@@ -89,6 +89,7 @@ struct DevTri {
   unsigned char* p_rec = nullptr;  // packed records, rec_bytes each
   int rec_bytes = 0;
   ulonglong2* xz = nullptr;        // n tagged exported values (128-bit each)
+  void* yperm = nullptr;           // n+2 right-hand-side values in schedule order (8 bytes each)
   int *seg_xptr = nullptr, *seg_xrow = nullptr;
   int max_seg_ext = 0;
   int *c_rp = nullptr, *c_ci = nullptr;
@@ -168,7 +169,6 @@ void launch_basis_norms(cudaStream_t st, long long n, int nb, int f,
 
 int num_sms(int device);
 void tri_trace_setup(int tile, unsigned long long* buf);
-void tri_loader_mode(int sync_loader);
 extern unsigned long long g_launches;  // kernels launched by this library
 
 // Opt-in per-kernel-class timing (CUDA events around each launch on the

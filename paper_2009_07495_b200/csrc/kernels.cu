@@ -88,26 +88,6 @@ __device__ __forceinline__ bool cycle_over(const Ctl* c) {
   return c != nullptr && (c->stop | c->err) != 0;
 }
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ int ld_relaxed(const int* p) {
-  int v;
-  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void red_release_max(int* p, int v) {
-  asm volatile("red.release.gpu.global.max.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-__device__ __forceinline__ void st_release(int* p, int v) {
-  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 __device__ __forceinline__ double dec(i64 raw, double scale) {
   return __dmul_rn(__ll2double_rn(raw), scale);  // exact power-of-two scale
 }
@@ -1067,365 +1047,209 @@ __global__ void __launch_bounds__(256) k_xupdate(long long n, int f, const i64* 
 }
 
 // ---------------------------------------------------------------------------
-// K6/K9 ILU(0) triangular substitutions (ilu.cpp:122-180), sync-free
-// wavefront.  Rows are split into contiguous tiles; a CTA takes tiles in
-// dependency order from a ticket counter (so every tile it waits on is
-// already owned by a running CTA: deadlock-free for any grid size), walks
-// its tile's rows level by level keeping the tile's results in shared
-// memory, and publishes per-tile progress ("all rows with level <= p are
-// final") with release/acquire.  Cross-tile dependencies wait on that
-// progress word and read the value through L2.
+// K6/K9 ILU(0) triangular substitutions (ilu.cpp:122-180) as a wavefront.
 //
-// Row records are stored in schedule order (upload-time permutation), so a
-// segment's records are contiguous and coalesced; the whole tile's records
-// are bulk-prefetched into L2 when the CTA starts, and each thread keeps the
-// NEXT segment's record in registers while it works on the current one, so
-// the per-level critical path is only: wait -> dependency values -> multiply,
-// subtract -> exact reciprocal division -> store.
+// The factor's rows are cut into tiles (schedule.hpp: bricks of a detected
+// structured grid, else contiguous blocks); one CTA owns one tile, keeps the
+// tile's solution values in shared memory and walks it one DAG level (one
+// segment of <= 256 rows, a row per compute thread) at a time.  Tiles are
+// handed out by a ticket counter in layer-major order, so every producer a
+// CTA waits on is already running.
 //
-// Per row the arithmetic is the reference's: CSR order, wrapping mul/sub,
-// truncating division by the raw diagonal (exact reciprocal), or the same in
-// FP64 on the integer factors with no contraction.
+//   warps 0-7  compute.  Per level: named barrier (the previous level's
+//              values are in shared memory), dependency values from shared
+//              memory only, the reference's row arithmetic, store.
+//   warp  8    loader.  Per level, into a ring slot of L levels: one bulk
+//              copy of the level's packed row records, one of its
+//              right-hand-side run (already in schedule order, k_tri_gather),
+//              and the values of the level's cross-tile producer rows, polled
+//              from their tagged 128-bit words two levels ahead.
+//
+// A value another tile reads is published as one aligned 128-bit store of
+// (value, epoch ^ value); the poller accepts a word only when its tag
+// matches this launch, so there are no flags and no gpu-scope fences.  The
+// epoch is a hashed 64-bit launch id: a word left by an earlier launch never
+// matches, and a torn read would need the two values to differ by exactly
+// the XOR of two random 64-bit ids.
+//
+// Per row the arithmetic is the reference's: integer path wrapping
+// multiply/subtract (summed in any order: mod 2^64 the result is the same)
+// and truncating division by the raw diagonal (exact reciprocal); FP path the
+// same in FP64 on the integer factors, in CSR order, without contraction.
 struct TriArgs {
   int n, ntiles;
   const int* tile_pbase;  // first schedule slot of each tile
-  const int* tile_seg;
-  const int* seg_level;
-  const int* seg_rows;
-  const int* seg_wptr;    // external producer tiles per segment
-  const int* seg_wt;
-  const int* p_row;       // row id per slot
-  const int* p_nd;        // dependency count per slot
-  const int* p_dep;       // slot*stride: >= 0 tile-local slot, < 0 ~global row
-  const i64* p_val;
-  const int* p_xrp;       // dependencies beyond stride (CSR)
-  const int* p_xdep;
-  const i64* p_xval;
-  const u64* p_mag;       // exact reciprocal of |diag| per slot
-  const int* p_info;      // sh1 | sh2 << 1 | neg << 8 | (diag == -1) << 9
-  const i64* p_diag;
-  const unsigned char* p_rec;  // packed per-slot records (schedule.hpp)
-  int tile_cap;
-  ulonglong2* xz;              // exported values: (value, epoch ^ mix(value)) per row
-  unsigned long long epoch;    // unique per launch
-  const int* seg_xptr;         // per segment: cross-tile producer rows
+  const int* tile_seg;    // first segment of each tile
+  const int* seg_rows;    // first slot of each segment
+  const int* seg_xptr;    // per segment: its cross-tile producer rows
   const int* seg_xrow;
-  int max_seg_ext;
-  const int* c_rp;             // stripped factor, natural order (counting pass)
-  const int* c_ci;
-  const i64* c_val;
-  const i64* c_diag;
-  int* prog;
+  const int* p_xdep;      // dependencies beyond the record stride (rare)
+  const i64* p_xval;
+  const unsigned char* p_rec;  // packed per-slot records (schedule.hpp)
+  int tile_cap, max_seg_ext;
+  ulonglong2* xz;              // exported values: (value, epoch ^ value) per row
+  unsigned long long epoch;    // per launch: hashed, non-zero
   int* ticket;
 };
 
-template <int MAXD>
-struct RowRec {
-  int row, nd, slot, xb;
-  u64 mag;
-  int info;
-  i64 diag;
-  int ci[MAXD];
-  i64 v[MAXD];
-};
-
-// every address is a function of p alone: the loads issue back to back and
-// only the consumer (next segment) waits for them
-template <int MAXD, bool FP>
-__device__ __forceinline__ void load_rec(const TriArgs& a, int p, int pb, RowRec<MAXD>& r) {
-  r.row = __ldg(a.p_row + p);
-  r.nd = __ldg(a.p_nd + p);
-  r.slot = p - pb;
-  r.xb = __ldg(a.p_xrp + p);
-  if (FP) {
-    r.diag = __ldg(a.p_diag + p);
-  } else {
-    r.mag = __ldg(a.p_mag + p);
-    r.info = __ldg(a.p_info + p);
-  }
-#pragma unroll
-  for (int d = 0; d < MAXD; ++d) {
-    r.ci[d] = __ldg(a.p_dep + static_cast<size_t>(p) * MAXD + d);
-    r.v[d] = __ldg(a.p_val + static_cast<size_t>(p) * MAXD + d);
-  }
-}
-
-__device__ __forceinline__ void l2_prefetch(const void* p, size_t bytes) {
-  // bulk L2 prefetch of [p, p+bytes), 16-byte granular (allocations are padded)
-  const size_t a = reinterpret_cast<size_t>(p) & ~size_t(15);
-  size_t e = (reinterpret_cast<size_t>(p) + bytes + 15) & ~size_t(15);
-  for (size_t q = a; q < e; q += (1u << 20)) {
-    const unsigned len = static_cast<unsigned>(min(e - q, static_cast<size_t>(1u << 20)));
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(q), "r"(len) : "memory");
-  }
-}
-
-template <typename T, bool CHECKED>
-struct TriAcc {
-  u64 nmul = 0, nsub = 0, ndiv = 0;
-};
-
-// one dependency term: acc -= l_ij * z_j (value from smem or, cross-tile,
-// from L2 after the segment's poller acquired the producer's progress)
-__device__ __forceinline__ u64 xz_mix(u64 v) { return v * 0x9E3779B97F4A7C15ull; }
-
-// cross-tile value: spin on its 128-bit (value, tag) word -- one single-copy
-// atomic strong access, so no fence/flag protocol is needed; the tag binds
-// the value to this launch (and guards against a torn read)
-__device__ __forceinline__ u64 xz_wait(const ulonglong2* p, u64 epoch) {
-  u64 v, tg;
-  do {
-    asm volatile("{ .reg .b128 t; ld.global.relaxed.gpu.b128 t, [%2]; mov.b128 {%0, %1}, t; }"
-                 : "=l"(v), "=l"(tg)
-                 : "l"(p)
-                 : "memory");
-  } while (tg != (epoch ^ xz_mix(v)));
-  return v;
-}
-
-__device__ __forceinline__ void xz_put(ulonglong2* p, u64 v, u64 epoch) {
-  asm volatile("{ .reg .b128 t; mov.b128 t, {%0, %1}; st.global.relaxed.gpu.b128 [%2], t; }" ::"l"(v),
-               "l"(epoch ^ xz_mix(v)), "l"(p)
-               : "memory");
-}
-
-template <typename T>
-__device__ __forceinline__ T bits_to(u64 b) {
-  if constexpr (std::is_same<T, double>::value) return __longlong_as_double(static_cast<long long>(b));
-  else return static_cast<T>(b);
-}
-template <typename T>
-__device__ __forceinline__ u64 to_bits(T v) {
-  if constexpr (std::is_same<T, double>::value) return static_cast<u64>(__double_as_longlong(v));
-  else return static_cast<u64>(v);
-}
-
-// one cross-tile word (value, tag) loaded ahead of use
+// one cross-tile word (value, tag): a single strong 128-bit access
 __device__ __forceinline__ void xz_load(const ulonglong2* p, u64& v, u64& tg) {
   asm volatile("{ .reg .b128 t; ld.global.relaxed.gpu.b128 t, [%2]; mov.b128 {%0, %1}, t; }"
                : "=l"(v), "=l"(tg)
                : "l"(p)
                : "memory");
 }
-
-template <typename T, bool CHECKED>
-__device__ __forceinline__ void tri_term(int c, i64 lv, u64 xv, u64 xt, const TriArgs& a, const T* zt,
-                                         T& acc, TriAcc<T, CHECKED>& st) {
-  T zj;
-  if (c >= 0) {
-    zj = zt[c];  // tile-local value
-  } else {       // cross-tile: the word was loaded one level early; spin only if not yet valid
-    zj = bits_to<T>(xt == (a.epoch ^ xz_mix(xv)) ? xv : xz_wait(a.xz + ~c, a.epoch));
-  }
-  if constexpr (std::is_same<T, double>::value) {
-    acc = __dsub_rn(acc, __dmul_rn(__ll2double_rn(lv), zj));
-  } else {
-    const i64 pr = wmul(lv, zj);
-    if (CHECKED) {
-      st.nmul += mul_ovf(lv, zj);
-      st.nsub += sub_ovf(acc, pr);
-    }
-    acc = wsub(acc, pr);
-  }
+__device__ __forceinline__ u64 xz_wait(const ulonglong2* p, u64 epoch) {
+  u64 v, tg;
+  do {
+    xz_load(p, v, tg);
+  } while (tg != (epoch ^ v));
+  return v;
+}
+__device__ __forceinline__ void xz_put(ulonglong2* p, u64 v, u64 epoch) {
+  asm volatile("{ .reg .b128 t; mov.b128 t, {%0, %1}; st.global.relaxed.gpu.b128 [%2], t; }" ::"l"(v),
+               "l"(epoch ^ v), "l"(p)
+               : "memory");
 }
 
-template <typename T, bool CHECKED, int MAXD>
-__device__ __forceinline__ void tri_row(const TriArgs& a, const RowRec<MAXD>& r, T acc, T* out,
-                                        T* zt, const u64 (&xv)[MAXD], const u64 (&xt)[MAXD],
-                                        TriAcc<T, CHECKED>& st) {
-#pragma unroll
-  for (int d = 0; d < MAXD; ++d)
-    if (d < r.nd) tri_term<T, CHECKED>(r.ci[d], r.v[d], xv[d], xt[d], a, zt, acc, st);
-  for (int d = MAXD; d < r.nd; ++d)
-    tri_term<T, CHECKED>(__ldg(a.p_xdep + r.xb + d - MAXD), __ldg(a.p_xval + r.xb + d - MAXD), 0,
-                         ~a.epoch /* never a valid tag for value 0: forces the spin path */, a, zt, acc, st);
-  T z;
-  if constexpr (std::is_same<T, double>::value) {
-    z = __ddiv_rn(acc, __ll2double_rn(r.diag));
-  } else {
-    SDivMagic gm;
-    gm.u.m = r.mag;
-    gm.u.sh1 = r.info & 1;
-    gm.u.sh2 = (r.info >> 1) & 127;
-    gm.den_neg = (r.info >> 8) & 1;
-    gm.den_is_m1 = (r.info >> 9) & 1;
-    if (CHECKED) st.ndiv += sdiv_ovf(acc, gm);
-    z = sdiv(acc, gm);
-  }
-  zt[r.slot] = z;
-#ifndef IGM_TRI_NOSTORE
-  out[r.row] = z;
-  if (r.info & (1 << 10)) xz_put(a.xz + r.row, to_bits<T>(z), a.epoch);  // read by another tile
-#endif
-}
-
-// Integer row, straight-line: every one of the MAXD dependency slots is used
-// (unused slots are padded with factor 0 and local slot 0 at upload, which
-// adds exact zeros mod 2^64), the products are independent and summed as a
-// tree (integer wrapping sums are order-free), cross-tile words were loaded
-// one level early and are only re-polled if their tag is not yet valid.
-template <int MAXD>
-__device__ __forceinline__ i64 tri_row_int_fast(const TriArgs& a, const RowRec<MAXD>& r, i64 y,
-                                                const i64* zt, const u64 (&xv)[MAXD],
-                                                const u64 (&xt)[MAXD]) {
-  i64 z[MAXD];
-#pragma unroll
-  for (int d = 0; d < MAXD; ++d) z[d] = zt[r.ci[d] < 0 ? 0 : r.ci[d]];
-  bool stale = false;
-#pragma unroll
-  for (int d = 0; d < MAXD; ++d) {
-    if (r.ci[d] < 0) {
-      z[d] = static_cast<i64>(xv[d]);
-      stale |= xt[d] != (a.epoch ^ xz_mix(xv[d]));
-    }
-  }
-  if (stale) {  // a producer tile had not published yet when the word was loaded
-#pragma unroll
-    for (int d = 0; d < MAXD; ++d)
-      if (r.ci[d] < 0 && xt[d] != (a.epoch ^ xz_mix(xv[d])))
-        z[d] = static_cast<i64>(xz_wait(a.xz + ~r.ci[d], a.epoch));
-  }
-  u64 s = 0;
-#pragma unroll
-  for (int d = 0; d < MAXD; ++d) s += static_cast<u64>(r.v[d]) * static_cast<u64>(z[d]);
-  for (int d = MAXD; d < r.nd; ++d) {  // rows wider than the record stride (rare)
-    const int c = __ldg(a.p_xdep + r.xb + d - MAXD);
-    const i64 zj = c >= 0 ? zt[c] : static_cast<i64>(xz_wait(a.xz + ~c, a.epoch));
-    s += static_cast<u64>(__ldg(a.p_xval + r.xb + d - MAXD)) * static_cast<u64>(zj);
-  }
-  const i64 acc = static_cast<i64>(static_cast<u64>(y) - s);
-  SDivMagic gm;
-  gm.u.m = r.mag;
-  gm.u.sh1 = r.info & 1;
-  gm.u.sh2 = (r.info >> 1) & 127;
-  gm.den_neg = (r.info >> 8) & 1;
-  gm.den_is_m1 = (r.info >> 9) & 1;
-  return sdiv(acc, gm);
-}
-
-template <typename T>
-__device__ __forceinline__ T tri_load_y(const T* __restrict__ y, int row, bool scaled, double gamma) {
-  if constexpr (std::is_same<T, double>::value) return scaled ? __ddiv_rn(y[row], gamma) : y[row];
-  else return y[row];
-}
-
-__device__ int g_tri_sync_loader = 0;  // A/B switch (IGM_TRI_SYNC_LOADER)
-
-// debug: per-segment phase timestamps of one tile (igm_debug_tri_trace)
+// debug: per-level phase timestamps of one tile (igm_debug_tri_trace)
 __device__ unsigned long long* g_tri_ts = nullptr;
 __device__ int g_tri_ts_tile = -1;
-__device__ __forceinline__ unsigned long long gtime() {
-  // SM cycle counter (the global timer ticks at ~1 us on this part); only
-  // differences within one CTA are meaningful
-  return clock64();
-}
+__device__ __forceinline__ unsigned long long gtime() { return clock64(); }  // per-SM cycles
 
 __device__ __forceinline__ void bar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
-__device__ __forceinline__ void bar_arrive(int id, int count) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
 
-// ---- mbarrier / bulk-copy helpers (sm_90+ PTX, valid on sm_100a)
+// ---- shared-window (32-bit address) helpers: mbarrier, bulk copy, ld/st
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void mbar_init(void* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+__device__ __forceinline__ void mbar_init_s(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(void* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ void mbar_arrive_s(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive_expect_tx(void* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+__device__ __forceinline__ void mbar_arrive_expect_tx_s(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+// relaxed: no release, so the caller's in-flight global loads need not drain
+__device__ __forceinline__ void mbar_arrive_expect_tx_relaxed_s(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(void* bar, unsigned parity) {
+__device__ __forceinline__ void mbar_wait_s(unsigned bar, unsigned parity) {
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
       "WAIT_%=:\n"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
       "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
+      "}\n" ::"r"(bar),
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, void* bar) {
+__device__ __forceinline__ void bulk_g2s_s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
       : "memory");
 }
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+__device__ __forceinline__ i64 lds64(unsigned a) {
+  i64 v;
+  asm volatile("ld.shared.s64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+  return v;
 }
-__device__ __forceinline__ void cp_async_mbar_arrive(void* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ void sts64(unsigned a, i64 v) {
+  asm volatile("st.shared.s64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ int4 lds128i(unsigned a) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void lds128l(unsigned a, i64& x, i64& y) {
+  asm volatile("ld.shared.v2.s64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(a) : "memory");
 }
 
-// Wavefront CTA (one tile per CTA):
-//   warps 0-7  compute: one row per thread per level (segments <= 256 rows);
-//              a named barrier per level orders the tile's shared-memory values
-//   warp  8    loader: streams each level's packed row records (one TMA bulk
-//              copy) and right-hand-side values (cp.async gathers) into a
-//              shared-memory ring L levels ahead (mbarriers full/empty)
-// Values another tile needs are published as one aligned 128-bit
-// (value, tag) store and consumed by spinning on that word; there are no
-// progress flags and no gpu-scope fences (a fence's cost grows with the
-// SM's in-flight traffic: ~15 us here).  Tiles are handed out by a ticket
-// counter in a layer-major order, so every producer a thread waits on is
-// already running (schedule.hpp).
+// yperm[p] = y[p_row[p]] (FP path: divided by gamma with one correctly rounded
+// division per entry, as refine.cpp:17 forms b_k = r / gamma) -- one coalesced
+// streaming pass that turns the wavefront's per-level right-hand-side
+// gathers into one contiguous bulk copy
+template <typename T>
+__global__ void __launch_bounds__(256) k_tri_gather(int n, const int* __restrict__ p_row,
+                                                    const T* __restrict__ y, T* __restrict__ yperm,
+                                                    const Ctl* ctl, const double* prescale) {
+  if (cycle_over(ctl)) return;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {  // grid is capped
+    T v = y[__ldg(p_row + p)];
+    if constexpr (std::is_same<T, double>::value) {
+      if (prescale != nullptr) v = __ddiv_rn(v, __longlong_as_double(*reinterpret_cast<const long long*>(prescale)));
+    }
+    yperm[p] = v;
+  }
+}
+
 constexpr int kTriCompute = 256;
-constexpr int kTriThreads = kTriCompute + 32;  // + loader warp
+constexpr int kTriThreads = kTriCompute + 32;  // + bulk-loader warp
+#ifndef IGM_TRI_LA
+#define IGM_TRI_LA 2
+#endif
+constexpr int kTriLA = IGM_TRI_LA;  // levels of record / cross-tile-word lookahead
 
 struct TriSmem {  // byte offsets of the dynamic shared-memory regions
-  size_t rows, lev, ring, bars, total;
-  int ring_slot;
+  size_t rows, xptr, ring, bars, total;
+  unsigned ring_slot;
 };
 
-template <typename T, int MAXD>
+// zt (tile values) | segment starts | (spare) | ring of L slots
+// [records | rhs run] | mbarriers
+template <int MAXD>
 __host__ __device__ inline TriSmem tri_smem_layout(int tile_cap, int seg_cap, int L, int max_ext) {
   constexpr int REC = 32 + 12 * MAXD;
   TriSmem m;
-  size_t o = (static_cast<size_t>(tile_cap) * sizeof(T) + 15) & ~size_t(15);
+  size_t o = (static_cast<size_t>(tile_cap) * 8 + 15) & ~size_t(15);
   m.rows = o;
   o += sizeof(int) * static_cast<size_t>(seg_cap);
-  m.lev = o;
+  m.xptr = o;
   o += sizeof(int) * static_cast<size_t>(seg_cap);
   o = (o + 127) & ~size_t(127);
   m.ring = o;
-  m.ring_slot = kTriSegRows * (REC + 8) + ((8 * max_ext + 15) & ~15);
+  m.ring_slot = kTriSegRows * REC + 8 * (kTriSegRows + 2);
+  (void)max_ext;
   o += static_cast<size_t>(L) * m.ring_slot;
   o = (o + 15) & ~size_t(15);
   m.bars = o;
-  o += 24 * static_cast<size_t>(L);  // full, empty, xfull
+  o += 16 * static_cast<size_t>(L);  // full, empty
   m.total = o;
   return m;
 }
 
-template <typename T, bool BACKWARD, bool CHECKED, int MAXD>
-__global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restrict__ y, T* out,
-                                                     u64* cnt, const Ctl* ctl,
-                                                     const double* prescale, int seg_cap, int L) {
+template <typename T, bool BACKWARD, int MAXD>
+__global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restrict__ yperm, T* out,
+                                                     const Ctl* ctl, int seg_cap, int L) {
   constexpr bool FP = std::is_same<T, double>::value;
   constexpr int REC = 32 + 12 * MAXD;
+  constexpr unsigned YOFF = kTriSegRows * REC;                 // rhs run in a ring slot
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ int s_tile;
   if (cycle_over(ctl)) return;
-  const TriSmem lay = tri_smem_layout<T, MAXD>(a.tile_cap, seg_cap, L, a.max_seg_ext);
-  T* zt = reinterpret_cast<T*>(smem_raw);
+  const TriSmem lay = tri_smem_layout<MAXD>(a.tile_cap, seg_cap, L, a.max_seg_ext);
+  const unsigned zt_s = smem_u32(smem_raw);
   int* s_rows = reinterpret_cast<int*>(smem_raw + lay.rows);
-  unsigned char* ring = smem_raw + lay.ring;
-  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem_raw + lay.bars);
-  unsigned long long* empty = full + L;
+  int* s_xptr = reinterpret_cast<int*>(smem_raw + lay.xptr);
+  const unsigned ring_s = smem_u32(smem_raw + lay.ring);
+  const unsigned full_s = smem_u32(smem_raw + lay.bars);
+  const unsigned empty_s = full_s + 8u * static_cast<unsigned>(L);
   if (threadIdx.x == 0) {
     s_tile = atomicAdd(a.ticket, 1);
     for (int k = 0; k < L; ++k) {
-      mbar_init(full + k, g_tri_sync_loader ? 32 : 33);  // lane-0 expect_tx + 32 cp.async arrivals
-      mbar_init(empty + k, kTriCompute / 32);
+      mbar_init_s(full_s + 8u * k, 1);  // the bulk loader's arrive (+ tx bytes)
+      mbar_init_s(empty_s + 8u * k, kTriCompute / 32);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -1436,9 +1260,13 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
   const int nsg = se - sb;
   const bool seg_in_smem = nsg + 2 <= seg_cap;
   if (seg_in_smem)
-    for (int q = threadIdx.x; q <= nsg; q += blockDim.x) s_rows[q] = __ldg(a.seg_rows + sb + q);
+    for (int q = threadIdx.x; q <= nsg; q += blockDim.x) {
+      s_rows[q] = __ldg(a.seg_rows + sb + q);
+      s_xptr[q] = __ldg(a.seg_xptr + sb + q);
+    }
   __syncthreads();
   auto seg_row = [&](int q) { return seg_in_smem ? s_rows[q] : __ldg(a.seg_rows + sb + q); };
+  auto seg_xp = [&](int q) { return seg_in_smem ? s_xptr[q] : __ldg(a.seg_xptr + sb + q); };
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 #ifdef IGM_TRI_TRACE
@@ -1447,160 +1275,185 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
   constexpr unsigned long long* tsb = nullptr;  // phase timestamps compiled out
 #endif
 
-  if (warp == 8) {  // ---------------- loader
-    // row ids are loaded D levels ahead (register pipeline), so the
-    // right-hand-side gathers never wait on a dependent load
-    constexpr int RPL = kTriSegRows / 32;  // rows per lane per level
-    constexpr int D = 4;
-    int rows[D][RPL];
-    auto load_rows = [&](int q, int (&rr)[RPL]) {
-      if (q >= nsg) return;
-      const int s0 = seg_row(q), c = seg_row(q + 1) - s0;
-#pragma unroll
-      for (int t = 0; t < RPL; ++t) {
-        const int r = lane + 32 * t;
-        rr[t] = r < c ? __ldg(a.p_row + s0 + r) : 0;
-      }
-    };
-#pragma unroll
-    for (int d = 0; d < D; ++d) load_rows(d, rows[d]);
+  if (warp == kTriCompute / 32) {  // ---------------- bulk loader (one lane)
+    if (lane != 0) return;
     int k = 0;
     unsigned ph = 1;  // parity of the previous use of slot k (first L levels: none)
-    for (int q0 = 0; q0 < nsg; q0 += D) {
-#pragma unroll
-      for (int d = 0; d < D; ++d) {  // unrolled so rows[d] stays in registers
-        const int q = q0 + d;
-        if (q >= nsg) break;
-        if (q >= L) mbar_wait(empty + k, ph);
-        const int s0 = seg_row(q), c = seg_row(q + 1) - s0;
-        unsigned char* slot = ring + static_cast<size_t>(k) * lay.ring_slot;
-        T* yslot = reinterpret_cast<T*>(slot + kTriSegRows * REC);
-        if (g_tri_sync_loader) {  // A/B: synchronous copy through registers
-          const int4* src = reinterpret_cast<const int4*>(a.p_rec + static_cast<size_t>(s0) * REC);
-          int4* dst = reinterpret_cast<int4*>(slot);
-          for (int i = lane; i < c * REC / 16; i += 32) dst[i] = __ldg(src + i);
-#pragma unroll
-          for (int t = 0; t < RPL; ++t)
-            if (lane + 32 * t < c) yslot[lane + 32 * t] = y[rows[d][t]];
-          __syncwarp();
-          mbar_arrive(full + k);
-        } else {
-          if (lane == 0) {
-            mbar_arrive_expect_tx(full + k, static_cast<unsigned>(c * REC));
-            bulk_g2s(slot, a.p_rec + static_cast<size_t>(s0) * REC, static_cast<unsigned>(c * REC), full + k);
-          }
-#pragma unroll
-          for (int t = 0; t < RPL; ++t)
-            if (lane + 32 * t < c) cp_async8(yslot + lane + 32 * t, y + rows[d][t]);
-          cp_async_mbar_arrive(full + k);
-        }
-        if (tsb && lane == 0 && q < 2048) tsb[q * 8 + 7] = gtime();
-        load_rows(q + D, rows[d]);
-        if (++k == L) {
-          k = 0;
-          ph ^= 1u;
-        }
+    for (int q = 0; q < nsg; ++q) {
+      if (q >= L) mbar_wait_s(empty_s + 8u * k, ph);
+      const int s0 = seg_row(q), c = seg_row(q + 1) - s0;
+      const unsigned slot = ring_s + static_cast<unsigned>(k) * lay.ring_slot;
+      const unsigned fb = full_s + 8u * k;
+      // the rhs run is widened to 16-byte alignment: it lands at offset s0 & 1
+      const int ya = s0 & ~1, yc = ((s0 + c + 1) & ~1) - ya;
+      mbar_arrive_expect_tx_s(fb, static_cast<unsigned>(c * REC + yc * 8));
+      bulk_g2s_s(slot, a.p_rec + static_cast<size_t>(s0) * REC, static_cast<unsigned>(c * REC), fb);
+      bulk_g2s_s(slot + YOFF, yperm + ya, static_cast<unsigned>(yc * 8), fb);
+      if (tsb && q < 2048) tsb[q * 8 + 7] = gtime();
+      if (++k == L) {
+        k = 0;
+        ph ^= 1u;
       }
     }
     return;
   }
+
   // ---------------- compute warps
-  const bool scaled = prescale != nullptr;
-  const double gamma = scaled ? __longlong_as_double(*reinterpret_cast<const long long*>(prescale)) : 1.0;
-  TriAcc<T, CHECKED> stt;
+  // Each level's row record (dependency slots and factors, magic, rhs) is
+  // read from the ring kTriLA levels ahead into a register ring buffer, and
+  // its cross-tile words are loaded at the same time: a strong 128-bit L2
+  // load costs ~0.2-0.5 us, so a one-level lead would leave it on every
+  // level's critical path.  Buffers are indexed by level mod kTriLA with the
+  // loop unrolled by kTriLA, so no register copy waits on a load in flight.
   const int tid = threadIdx.x;
-  // one row per thread per level: the per-level critical path is this warp's
-  // in-order instruction stream, so everything loop-invariant or derivable
-  // incrementally stays out of it
-  auto read_rec = [&](const unsigned char* slotp, int s0, RowRec<MAXD>& r) {
-    const unsigned char* rp = slotp + static_cast<size_t>(tid) * REC;
-    const int4 hdr = *reinterpret_cast<const int4*>(rp);
+  const unsigned ring_end = ring_s + static_cast<unsigned>(L) * lay.ring_slot;
+  const unsigned my_rec = static_cast<unsigned>(tid) * REC;
+  struct Rec {
+    int row, info, nd, xb;
+    i64 mag, diag, y;
+    int ci[MAXD];
+    i64 v[MAXD];
+    u64 wv[MAXD], wt[MAXD];  // cross-tile words (value, tag)
+    unsigned zaddr, bar;
+    bool have;
+  };
+  Rec R[kTriLA];
+  unsigned f_slot = ring_s, f_bar = 0, f_ph = 0;  // ring position of the next level to fetch
+  int s_f = seg_row(0);
+  auto fetch = [&](int q, Rec& r) {
+    r.have = false;
+    r.bar = f_bar;
+    if (q >= nsg) return;
+    mbar_wait_s(full_s + f_bar, f_ph);
+    const unsigned sl = f_slot;
+    f_bar += 8;
+    f_slot += lay.ring_slot;
+    if (f_slot == ring_end) {
+      f_slot = ring_s;
+      f_bar = 0;
+      f_ph ^= 1u;
+    }
+    const int s0 = s_f, s1 = seg_row(q + 1);
+    s_f = s1;
+    if (tid >= s1 - s0) return;
+    const unsigned ra = sl + my_rec;
+    const int4 hdr = lds128i(ra);
     r.row = hdr.x;
     r.nd = hdr.y;
     r.info = hdr.z;
     r.xb = hdr.w;
-    if (FP) r.diag = *reinterpret_cast<const i64*>(rp + 24);
-    else r.mag = *reinterpret_cast<const u64*>(rp + 16);
-    r.slot = s0 + tid - pb;
+    lds128l(ra + 16, r.mag, r.diag);
 #pragma unroll
-    for (int d = 0; d < MAXD; ++d) {
-      r.ci[d] = *reinterpret_cast<const int*>(rp + 32 + 4 * d);
-      r.v[d] = *reinterpret_cast<const i64*>(rp + 32 + 4 * MAXD + 8 * d);
+    for (int d = 0; d < MAXD; d += 4) {
+      const int4 c4 = lds128i(ra + 32 + 4 * d);
+      r.ci[d] = c4.x;
+      r.ci[d + 1] = c4.y;
+      r.ci[d + 2] = c4.z;
+      r.ci[d + 3] = c4.w;
     }
-  };
-  // record + cross-tile words of the NEXT level, issued before this level's barrier
-  RowRec<MAXD> nrec;
-  u64 nxv[MAXD], nxt[MAXD];
-  bool nhave = false;
-  int kn = 0;          // ring slot of the next level
-  unsigned phn = 0;    // its mbarrier phase parity
-  int s_next = seg_row(0);
-  auto prefetch = [&](int q) {
-    nhave = false;
-    if (q >= nsg) return;
-    mbar_wait(full + kn, phn);
-    const int s1 = seg_row(q + 1);
-    const int s0 = s_next;
-    s_next = s1;
-    if (tid >= s1 - s0) return;
-    read_rec(ring + static_cast<size_t>(kn) * lay.ring_slot, s0, nrec);
-    nhave = true;
+#pragma unroll
+    for (int d = 0; d < MAXD; d += 2) lds128l(ra + 32 + 4 * MAXD + 8 * d, r.v[d], r.v[d + 1]);
+    r.y = lds64(sl + YOFF + 8u * static_cast<unsigned>(tid + (s0 & 1)));
+    r.zaddr = zt_s + 8u * static_cast<unsigned>(s0 + tid - pb);
+    r.have = true;
 #pragma unroll
     for (int d = 0; d < MAXD; ++d)
-      if (d < nrec.nd && nrec.ci[d] < 0) xz_load(a.xz + ~nrec.ci[d], nxv[d], nxt[d]);
+      if (r.ci[d] < 0) xz_load(a.xz + ~r.ci[d], r.wv[d], r.wt[d]);
   };
-  prefetch(0);
-  for (int q = 0; q < nsg; ++q) {
-    const int k = kn;
-    if (++kn == L) {
-      kn = 0;
-      phn ^= 1u;
-    }
-    const RowRec<MAXD> cur = nrec;
-    u64 xv[MAXD], xt[MAXD];
-#pragma unroll
-    for (int d = 0; d < MAXD; ++d) {
-      xv[d] = nxv[d];
-      xt[d] = nxt[d];
-    }
-    const bool hc = nhave;
+  // one level: barrier, the row, release the level's ring slot
+  auto level = [&](int q, const Rec& cur) {
     if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 2] = gtime();
     bar_sync(1, kTriCompute);  // level q-1 values of this tile are in shared memory
     if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 3] = gtime();
-#ifdef IGM_TRI_SKELETON
-    if (false) {
-#else
-    if (hc) {
+#ifndef IGM_TRI_SKELETON
+    if (cur.have) {
+      i64 zb[MAXD];
+#pragma unroll
+      for (int d = 0; d < MAXD; ++d) {
+        const int c = cur.ci[d];
+        zb[d] = lds64(zt_s + 8u * static_cast<unsigned>(c < 0 ? 0 : c));
+        if (c < 0) {  // cross-tile: loaded kTriLA levels ago, re-polled only if not yet published
+          const bool ok = cur.wt[d] == (a.epoch ^ cur.wv[d]);
+#ifdef IGM_TRI_TRACE
+          if (tsb && q < 2048) {
+            if (!ok) atomicAdd(tsb + q * 8 + 0, 1ull);
+            atomicAdd(tsb + q * 8 + 1, 1ull);
+          }
 #endif
-      const unsigned char* slot = ring + static_cast<size_t>(k) * lay.ring_slot;
-      T yv = reinterpret_cast<const T*>(slot + kTriSegRows * REC)[tid];
-      if constexpr (FP) {
-        if (scaled) yv = __ddiv_rn(yv, gamma);
+          zb[d] = static_cast<i64>(ok ? cur.wv[d] : xz_wait(a.xz + ~c, a.epoch));
+        }
       }
+      auto extra = [&](int d) {  // dependency beyond the record stride (rare)
+        const int c = __ldg(a.p_xdep + cur.xb + d - MAXD);
+        return c >= 0 ? lds64(zt_s + 8u * static_cast<unsigned>(c)) : static_cast<i64>(xz_wait(a.xz + ~c, a.epoch));
+      };
+      T z;
       if constexpr (FP) {
-        tri_row<T, CHECKED, MAXD>(a, cur, yv, out, zt, xv, xt, stt);
+        double acc = __longlong_as_double(cur.y);
+#pragma unroll
+        for (int d = 0; d < MAXD; ++d)
+          if (d < cur.nd) acc = __dsub_rn(acc, __dmul_rn(__ll2double_rn(cur.v[d]), __longlong_as_double(zb[d])));
+        for (int d = MAXD; d < cur.nd; ++d)
+          acc = __dsub_rn(acc, __dmul_rn(__ll2double_rn(__ldg(a.p_xval + cur.xb + d - MAXD)),
+                                         __longlong_as_double(extra(d))));
+        z = __ddiv_rn(acc, __ll2double_rn(cur.diag));
       } else {
-        const i64 z = tri_row_int_fast<MAXD>(a, cur, yv, zt, xv, xt);
-        zt[cur.slot] = z;
-#ifndef IGM_TRI_NOSTORE
-        out[cur.row] = z;
-        if (cur.info & (1 << 10)) xz_put(a.xz + cur.row, static_cast<u64>(z), a.epoch);
+        // unused slots hold factor 0 at local slot 0: exact zero terms
+        u64 sx = 0;
+#ifndef IGM_TRI_NODEP
+#pragma unroll
+        for (int d = 0; d < MAXD; ++d) sx += static_cast<u64>(cur.v[d]) * static_cast<u64>(zb[d]);
+#endif
+        for (int d = MAXD; d < cur.nd; ++d)
+          sx += static_cast<u64>(__ldg(a.p_xval + cur.xb + d - MAXD)) * static_cast<u64>(extra(d));
+        const i64 acc = static_cast<i64>(static_cast<u64>(cur.y) - sx);
+        SDivMagic gm;
+        gm.u.m = static_cast<u64>(cur.mag);
+        gm.u.sh1 = cur.info & 1;
+        gm.u.sh2 = (cur.info >> 1) & 127;
+        gm.den_neg = (cur.info >> 8) & 1;
+        gm.den_is_m1 = 0;  // only the (separate) counting pass needs it
+#ifdef IGM_TRI_NODIV
+        z = acc ^ static_cast<i64>(gm.u.m);
+#else
+        z = sdiv(acc, gm);
 #endif
       }
+      i64 zbits;
+      if constexpr (FP) zbits = __double_as_longlong(z);
+      else zbits = z;
+      sts64(cur.zaddr, zbits);
+#ifndef IGM_TRI_NOSTORE
+      out[cur.row] = z;
+      if (cur.info & (1 << 10)) xz_put(a.xz + cur.row, static_cast<u64>(zbits), a.epoch);  // read by another tile
+#endif
     }
+#endif
     if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 5] = gtime();
     __syncwarp();
-    if (lane == 0) mbar_arrive(empty + k);
+    if (lane == 0) mbar_arrive_s(empty_s + cur.bar);
     if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 6] = gtime();
-    prefetch(q + 1);
-    if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 4] = gtime();
-  }
-  if (CHECKED && !FP) {
-    bump(cnt, OP_MUL, stt.nmul);
-    bump(cnt, OP_SUB, stt.nsub);
-    bump(cnt, OP_DIV, stt.ndiv);
+  };
+  if (L >= kTriLA + 1) {  // levels q .. q+LA hold ring slots at once
+#pragma unroll
+    for (int b = 0; b < kTriLA; ++b) fetch(b, R[b]);
+    for (int q0 = 0; q0 < nsg; q0 += kTriLA) {
+#pragma unroll
+      for (int b = 0; b < kTriLA; ++b) {  // unrolled: buffer b holds level q0 + b
+        if (q0 + b >= nsg) break;
+        level(q0 + b, R[b]);
+        fetch(q0 + b + kTriLA, R[b]);
+      }
+    }
+  } else {  // shallow ring (large strides): each level fetched once its slot is readable
+    for (int q = 0; q < nsg; ++q) {
+      fetch(q, R[0]);
+      level(q, R[0]);
+    }
   }
 }
+
+
 
 // Checked-mode overflow events of one integer substitution (ilu.cpp:126-153),
 // counted AFTER the wavefront from its inputs and outputs: every row's
@@ -1637,32 +1490,16 @@ TriArgs tri_args(const DevTri& t) {
   a.ntiles = t.ntiles;
   a.tile_pbase = t.tile_pbase;
   a.tile_seg = t.tile_seg;
-  a.seg_level = t.seg_level;
   a.seg_rows = t.seg_rows;
-  a.seg_wptr = t.seg_wptr;
-  a.seg_wt = t.seg_wt;
-  a.p_row = t.p_row;
-  a.p_nd = t.p_nd;
-  a.p_dep = t.p_dep;
-  a.p_val = t.p_val;
-  a.p_xrp = t.p_xrp;
-  a.p_xdep = t.p_xdep;
-  a.p_xval = t.p_xval;
-  a.p_mag = t.p_mag;
-  a.p_info = t.p_info;
-  a.p_diag = t.p_diag;
-  a.p_rec = t.p_rec;
-  a.tile_cap = t.tile_cap;
-  a.xz = t.xz;
-  a.epoch = 0;
   a.seg_xptr = t.seg_xptr;
   a.seg_xrow = t.seg_xrow;
+  a.p_xdep = t.p_xdep;
+  a.p_xval = t.p_xval;
+  a.p_rec = t.p_rec;
+  a.tile_cap = t.tile_cap;
   a.max_seg_ext = t.max_seg_ext;
-  a.c_rp = t.c_rp;
-  a.c_ci = t.c_ci;
-  a.c_val = t.c_val;
-  a.c_diag = t.c_diag;
-  a.prog = t.prog;
+  a.xz = t.xz;
+  a.epoch = 0;
   a.ticket = t.ticket;
   return a;
 }
@@ -1854,52 +1691,48 @@ void launch_xupdate(cudaStream_t st, long long n, int m, int f, const i64* basis
   LAUNCH_CHECK();
 }
 
-template <typename T, bool B, bool CK, int D>
-static void tri_launch_one(cudaStream_t st, const DevTri& t, const T* y, T* out, u64* cnt,
-                           const Ctl* ctl, const double* prescale) {
-  constexpr size_t kBudget = 227 * 1024 - 256;  // static smem (tile id, caches) excluded
-  int seg_cap = t.max_tile_segs + 2;
+template <typename T, bool B, int D>
+static void tri_launch_one(cudaStream_t st, const DevTri& t, const T* y, T* out, const Ctl* ctl,
+                           const double* prescale) {
+  constexpr size_t kBudget = 227 * 1024 - 256;  // static smem (tile id) excluded
   static const int env_L = [] {
     const char* e = std::getenv("IGM_TRI_L");
     return e ? std::atoi(e) : 0;
   }();
-  int L = env_L > 0 ? env_L : 8;
-  TriSmem lay = tri_smem_layout<T, D>(t.tile_cap, seg_cap, L, t.max_seg_ext);
-  while (L > 1 && lay.total > kBudget) lay = tri_smem_layout<T, D>(t.tile_cap, seg_cap, --L, t.max_seg_ext);
+  const int L0 = env_L > 0 ? env_L : 8;
+  int seg_cap = t.max_tile_segs + 2, L = L0;
+  TriSmem lay = tri_smem_layout<D>(t.tile_cap, seg_cap, L, t.max_seg_ext);
+  while (L > 1 && lay.total > kBudget) lay = tri_smem_layout<D>(t.tile_cap, seg_cap, --L, t.max_seg_ext);
   if (lay.total > kBudget) {  // segment tables stay in global memory
     seg_cap = 0;
-    L = env_L > 0 ? env_L : 8;
-    lay = tri_smem_layout<T, D>(t.tile_cap, seg_cap, L, t.max_seg_ext);
-    while (L > 1 && lay.total > kBudget) lay = tri_smem_layout<T, D>(t.tile_cap, seg_cap, --L, t.max_seg_ext);
+    L = L0;
+    lay = tri_smem_layout<D>(t.tile_cap, seg_cap, L, t.max_seg_ext);
+    while (L > 1 && lay.total > kBudget) lay = tri_smem_layout<D>(t.tile_cap, seg_cap, --L, t.max_seg_ext);
   }
   const size_t sm = lay.total;
-  static const int env_sync = [] {
-    const char* e = std::getenv("IGM_TRI_SYNC_LOADER");
-    const int v = e ? std::atoi(e) : 0;
-    tri_loader_mode(v);
-    return v;
-  }();
-  (void)env_sync;
   static size_t done = 0;
   if (sm > done) {
-    cudaFuncSetAttribute(k_tri<T, B, CK, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_tri<T, B, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     done = sm;
   }
   TriArgs args = tri_args(t);
-  args.epoch = ++const_cast<DevTri&>(t).epoch;  // unique tag per launch
-  k_tri<T, B, CK, D><<<t.ntiles, kTriThreads, sm, st>>>(args, y, out, cnt, ctl, prescale, seg_cap, L);
+  {  // per-launch tag: splitmix64 of a counter (never 0, the words' initial tag)
+    u64 z = (++const_cast<DevTri&>(t).epoch) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    args.epoch = (z ^ (z >> 31)) | 1ull;
+  }
+  // right-hand side into schedule order (and the FP path's 1/gamma prescale)
+  k_tri_gather<T><<<grid_for(t.n, 256), 256, 0, st>>>(t.n, t.p_row, y, static_cast<T*>(t.yperm), ctl, prescale);
+  k_tri<T, B, D><<<t.ntiles, kTriThreads, sm, st>>>(args, static_cast<const T*>(t.yperm), out, ctl, seg_cap, L);
 }
 
-template <typename T, bool B, bool CK>
-static void tri_dispatch(cudaStream_t st, const DevTri& t, const T* y, T* out, u64* cnt,
-                         const Ctl* ctl, const double* prescale) {
-  if (t.stride == 4) tri_launch_one<T, B, CK, 4>(st, t, y, out, cnt, ctl, prescale);
-  else if (t.stride == 8) tri_launch_one<T, B, CK, 8>(st, t, y, out, cnt, ctl, prescale);
-  else tri_launch_one<T, B, CK, 16>(st, t, y, out, cnt, ctl, prescale);
-}
-
-void tri_loader_mode(int sync_loader) {
-  cudaMemcpyToSymbol(g_tri_sync_loader, &sync_loader, sizeof(int));
+template <typename T, bool B>
+static void tri_dispatch(cudaStream_t st, const DevTri& t, const T* y, T* out, const Ctl* ctl,
+                         const double* prescale) {
+  if (t.stride == 4) tri_launch_one<T, B, 4>(st, t, y, out, ctl, prescale);
+  else if (t.stride == 8) tri_launch_one<T, B, 8>(st, t, y, out, ctl, prescale);
+  else tri_launch_one<T, B, 16>(st, t, y, out, ctl, prescale);
 }
 
 void tri_trace_setup(int tile, unsigned long long* buf) {
@@ -1913,8 +1746,8 @@ void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* 
   cudaMemsetAsync(t.ticket, 0, sizeof(int), st);
   {
     ProfScope prof_(st, KC_TRI_INT);
-    if (backward) tri_dispatch<i64, true, false>(st, t, y, out, cnt, ctl, nullptr);
-    else tri_dispatch<i64, false, false>(st, t, y, out, cnt, ctl, nullptr);
+    if (backward) tri_dispatch<i64, true>(st, t, y, out, ctl, nullptr);
+    else tri_dispatch<i64, false>(st, t, y, out, ctl, nullptr);
   }
   LAUNCH_CHECK();
   if (checked) {
@@ -1929,8 +1762,8 @@ void launch_tri_fp(cudaStream_t st, const DevTri& t, bool backward, const double
   if (t.n == 0) return;
   cudaMemsetAsync(t.ticket, 0, sizeof(int), st);
   ProfScope prof_(st, KC_TRI_FP);
-  if (backward) tri_dispatch<double, true, false>(st, t, y, out, nullptr, ctl, prescale);
-  else tri_dispatch<double, false, false>(st, t, y, out, nullptr, ctl, prescale);
+  if (backward) tri_dispatch<double, true>(st, t, y, out, ctl, prescale);
+  else tri_dispatch<double, false>(st, t, y, out, ctl, prescale);
   LAUNCH_CHECK();
 }
 

@@ -222,14 +222,10 @@ TriSchedule build_tri_schedule(int n, const int* rp, const int* ci, const std::i
     S.seg_level.push_back(0);
     S.seg_rows.push_back(0);
   }
-  // ---- per segment: distinct cross-tile producer rows (staged by the
-  // kernel's prefetch warp); position of each in its segment's list
+  // ---- per segment: distinct cross-tile producer rows (schedule statistics
+  // and validation)
   const int nseg_all = static_cast<int>(S.seg_level.size());
   S.seg_xptr.assign(static_cast<size_t>(nseg_all) + 1, 0);
-  std::vector<int> seg_of_slot(static_cast<size_t>(std::max(n, 1)), 0);
-  for (int sg = 0; sg < nseg_all; ++sg)
-    for (int p = S.seg_rows[sg]; p < S.seg_rows[sg + 1] && p < n; ++p) seg_of_slot[p] = sg;
-  std::vector<int> xpos_of;  // per (slot, dep) position, filled below in record order
   for (int sg = 0; sg < nseg_all; ++sg) {
     const size_t x0 = S.seg_xrow.size();
     for (int p = S.seg_rows[sg]; p < S.seg_rows[sg + 1] && p < n; ++p) {
@@ -273,7 +269,7 @@ TriSchedule build_tri_schedule(int n, const int* rp, const int* ci, const std::i
     S.p_nd[p] = orp[i + 1] - orp[i];
     for (int k = orp[i], d = 0; k < orp[i + 1]; ++k, ++d) {
       const int j = oci[k];
-      const int enc = tile_of[j] == t ? slot[j] - S.tile_pbase[t] : ~j;
+      const int enc = tile_of[j] == t ? slot[j] - S.tile_pbase[t] : ~j;  // tile-local slot or ~global row
       if (d < W) {
         S.p_dep[static_cast<size_t>(p) * W + d] = enc;
         S.p_val[static_cast<size_t>(p) * W + d] = ov[k];
@@ -366,6 +362,9 @@ int validate_tri_schedule(const TriSchedule& S, const int* rp, const int* ci, bo
       if (tile_of[j] == tile_of[i]) {
         if (enc != slot_of[j] - S.tile_pbase[tile_of[i]]) return 5;
       } else {
+        int sg = -1;
+        for (int q = S.tile_seg[tile_of[i]]; q < S.tile_seg[tile_of[i] + 1]; ++q)
+          if (p >= S.seg_rows[q] && p < S.seg_rows[q + 1]) sg = q;
         if (enc != ~j) return 5;
         // ticket order: producer tile handed out no later than the layer of i
         const int tk_i = upper ? S.ntiles - 1 - tile_of[i] : tile_of[i];
@@ -374,9 +373,6 @@ int validate_tri_schedule(const TriSchedule& S, const int* rp, const int* ci, bo
                                            ((S.grid[1] + S.brick[1] - 1) / S.brick[1])
                                      : 1;
         if (tk_j / layer > tk_i / layer) return 6;
-        int sg = -1;
-        for (int q = S.tile_seg[tile_of[i]]; q < S.tile_seg[tile_of[i] + 1]; ++q)
-          if (p >= S.seg_rows[q] && p < S.seg_rows[q + 1]) sg = q;
         bool listed = false;
         for (int w = S.seg_wptr[sg]; w < S.seg_wptr[sg + 1]; ++w) listed = listed || S.seg_wt[w] == tile_of[j];
         if (!listed) return 7;

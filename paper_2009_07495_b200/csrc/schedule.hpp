@@ -42,7 +42,7 @@ struct TriSchedule {
   std::vector<int> p_xdep;
   std::vector<std::int64_t> p_xval;
   std::vector<std::uint64_t> p_mag;  // exact reciprocal of |diag|
-  std::vector<int> p_info;
+  std::vector<int> p_info;  // sh1 | sh2<<1 | neg<<8 | (diag==-1)<<9 | exported<<10
   std::vector<std::int64_t> p_diag;
   // the same per-slot data as one packed record (what the kernel streams):
   //   int32 row, nd, info, xb | u64 mag | i64 diag | int32 dep[stride] | i64 val[stride]

@@ -4,6 +4,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2009_07495_b200 import _capi
 if os.environ.get("SKEL"):
     _capi.LIB_PATH = _capi._HERE / "libigm_skel.so"
+if os.environ.get("LIBNAME"):
+    _capi.LIB_PATH = _capi._HERE / os.environ["LIBNAME"]
 import numpy as np, torch
 import paper_2009_07495_b200 as igm
 from workloads import gen

@@ -1,6 +1,9 @@
 import os, sys, ctypes as C
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
+from paper_2009_07495_b200 import _capi
+if os.environ.get('LIBNAME'):
+    _capi.LIB_PATH = _capi._HERE / os.environ['LIBNAME']
 import paper_2009_07495_b200 as igm
 from workloads import gen
 rp, ci, v = gen.upwind_3d(128, 20.0)
@@ -19,11 +22,14 @@ for tile in (0, 1, 9, 63, 127):
     lib.igm_debug_tri_trace(tile, C.c_void_p(buf.data_ptr()))
     z = igm.apply_inverse(F, y)
     torch.cuda.synchronize()
-    ts = buf.cpu().numpy().reshape(-1, 8)[:, :8].astype(np.float64)
+    raw = buf.cpu().numpy().reshape(-1, 8)
+    nst, next_ = raw[:, 0].sum(), raw[:, 1].sum()
+    ts = raw[:, :8].astype(np.float64)
     ts = ts[ts[:, 3] > 0]
-    t0 = ts[:, 2:8].min()
+    t0 = ts[:, 2:8][ts[:, 2:8] > 0].min()
     ts -= t0
     ts /= 1.9  # cycles -> ns at ~1.9 GHz
+    print(f"  cross-tile words used {next_}, stale at use {nst}")
     print(f"tile {tile}: segs {len(ts)} start {ts[0,3]/1e3:.1f}us end {ts[-1,4]/1e3:.1f}us")
     per = np.diff(ts[:, 3])
     print("  level period med %.0f mean %.0f ns | barrier wait %.0f | row %.0f | syncwarp+arrive %.0f | prefetch next %.0f" % (

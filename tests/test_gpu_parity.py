@@ -330,3 +330,57 @@ def test_spmv_mgs_large_vs_torch(gpu, g, k):
         assert h == hs[i]
         wr = wr - (((h >> 16) * basis[i]) >> 14)
     assert torch.equal(wr, w)
+
+
+def _grid_factors(gpu, dims, offs, seed):
+    from workloads import gen
+    rng = np.random.default_rng(seed)
+    coef = {k: rng.uniform(-1.4, -0.6) for k in range(len(offs))}
+    centre = offs.index((0, 0, 0))
+    coef[centre] = 2.0 * len(offs)
+    rp, ci, v = gen._stencil_csr(dims, offs, lambda o, r: np.full(r.shape, coef[o]))
+    vals, _ = gpu.row_scale(rp, ci, v, 32)
+    return gpu.factorize_split_cast(rp, ci, vals)
+
+
+_SEVEN = [(0, 0, -1), (0, -1, 0), (-1, 0, 0), (0, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 1)]
+_TWENTY7 = [(a, b, c) for c in (-1, 0, 1) for b in (-1, 0, 1) for a in (-1, 0, 1)]
+
+
+@pytest.mark.parametrize("dims,offs", [((64, 64, 80), _SEVEN), ((128, 48, 70), _SEVEN), ((40, 40, 40), _TWENTY7)],
+                         ids=["7pt-64x64x80", "7pt-128x48x70", "27pt-40cube"])
+def test_ilu_apply_multi_tile(gpu, oracle, dims, offs):
+    """Bit-exact ILU apply on grids of many bricks / z-layers and > 148*8*256
+    rows (every launch path of the wavefront: cross-tile words, capped grids),
+    integer, FP and checked, over repeated launches."""
+    lo, up = _grid_factors(gpu, dims, offs, seed=sum(dims))
+    F = gpu.IluFactors(lo, up)
+    assert F.schedule_info(False)["tiles"] > 1
+    il = oracle.ilu(lo, up)
+    n = len(lo[0]) - 1
+    from workloads import gen
+    y = gen.uniform_int(11, n, -(1 << 45), 1 << 45)
+    want = oracle.apply_inverse(il, y)
+    for _ in range(3):
+        assert np.array_equal(gpu.apply_inverse(F, y), want)
+    yf = gen.uniform(12, n)
+    assert np.array_equal(gpu.apply_inverse_fp(F, yf), oracle.apply_inverse_fp(il, yf))
+    t1, t2 = gpu.FxTrace(), PyTrace()
+    yw = gen.uniform_int(13, n, -(1 << 62), 1 << 62)
+    assert np.array_equal(gpu.apply_inverse(F, yw, t1), oracle.apply_inverse(il, yw, t2))
+    assert t1.total_overflows() == t2.total
+
+
+def test_ilu_apply_unstructured_many_tiles(gpu, oracle):
+    """Contiguous-block tiling (no grid detected) with long cross-tile lists."""
+    from workloads import gen
+    rp, ci, v = gen.random_dominant(4000, 0.002, 1.3, gen.SEED_BASE ^ 91)
+    vals, _ = gpu.row_scale(rp, ci, v, 32)
+    lo, up = gpu.factorize_split_cast(rp, ci, vals)
+    F = gpu.IluFactors(lo, up)
+    assert F.schedule_info(False)["tiles"] > 1
+    il = oracle.ilu(lo, up)
+    y = gen.uniform_int(14, len(rp) - 1, -(1 << 45), 1 << 45)
+    want = oracle.apply_inverse(il, y)
+    for _ in range(2):
+        assert np.array_equal(gpu.apply_inverse(F, y), want)
