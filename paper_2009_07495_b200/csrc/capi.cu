@@ -144,7 +144,21 @@ struct igm_ctx {
   // primitive scratch
   u64* red = nullptr;  // acc, abs hi, abs lo, cnt[OP_COUNT]
   u64* h_red = nullptr;
+  void* n2s = nullptr;  // norm2 per-block scratch (norm2_scratch_bytes)
+  size_t n2s_bytes = 0;
 };
+
+// norm2 scratch for vectors of length n (grown on demand; stream-ordered use)
+void* n2_scratch(igm_ctx* c, long long n) {
+  const size_t need = norm2_scratch_bytes(n);
+  if (need > c->n2s_bytes) {
+    ck(cudaStreamSynchronize(c->stream), "norm2 scratch");
+    dfree(c->n2s);
+    c->n2s = dalloc<unsigned char>(need);
+    c->n2s_bytes = need;
+  }
+  return c->n2s;
+}
 
 namespace {
 
@@ -447,7 +461,7 @@ void enqueue_cycle(igm_ctx* c, const CycleParams& p, CycleMode mode, const doubl
       r0 = src;
     }
   }
-  launch_norm2_serial(st, n, r0, nullptr, ctl, 3);
+  launch_norm2_serial(st, n, r0, nullptr, ctl, 3, n2_scratch(c, n));
   launch_encode(st, n, r0, w.basis, f, ctl);
   // ---- Arnoldi steps (gmres_int.cpp:90-160)
   const size_t cstride = static_cast<size_t>(K_COUNT) * OP_COUNT;
@@ -483,7 +497,7 @@ void enqueue_cycle(igm_ctx* c, const CycleParams& p, CycleMode mode, const doubl
     launch_xupdate(st, n, M, f, w.basis, w.wts, nullptr, w.x, ctl, 1);
   else
     launch_xupdate(st, n, M, f, w.basis, w.wts, d_x0, d_xout, ctl, 0);
-  if (p.collect_norms) launch_basis_norms(st, n, M + 1, f, w.basis, nullptr, w.bnorms, ctl);
+  if (p.collect_norms) launch_basis_norms(st, n, M + 1, f, w.basis, n2_scratch(c, n), w.bnorms, ctl);
 }
 
 // copy Ctl + small arrays back (async on the stream; caller syncs)
@@ -591,6 +605,7 @@ void igm_ctx_destroy(igm_ctx* c) {
   ws_free(c->ws);
   dfree(c->ctl);
   dfree(c->red);
+  dfree(c->n2s);
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
   if (c->h_red) cudaFreeHost(c->h_red);
   cudaStreamDestroy(c->stream);
@@ -913,8 +928,8 @@ igm_status igm_residual_fp(igm_ctx* c, const igm_csrf* a, const double* x, const
     Out<double> dr(r, a->n);
     reset_ctl(c);
     launch_residual(c->stream, *a, dx.d, db.d, dr.d, c->ctl, false);
-    launch_norm2_serial(c->stream, a->n, db.d, nullptr, c->ctl, 1);
-    launch_norm2_serial(c->stream, a->n, dr.d, nullptr, c->ctl, 2);
+    launch_norm2_serial(c->stream, a->n, db.d, nullptr, c->ctl, 1, n2_scratch(c, a->n));
+    launch_norm2_serial(c->stream, a->n, dr.d, nullptr, c->ctl, 2, n2_scratch(c, a->n));
     dr.fetch(c->stream);
     ck(cudaMemcpyAsync(c->h_ctl, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream), "D2H");
     ck(cudaStreamSynchronize(c->stream), "sync");
@@ -940,7 +955,7 @@ igm_status igm_norm2(igm_ctx* c, int64_t n, const double* v, double* out) {
     need_ctx(c);
     In<double> dv(v, n, c->stream);
     double* d = dalloc<double>(1);
-    launch_norm2_serial(c->stream, n, dv.d, d, c->ctl, 0);
+    launch_norm2_serial(c->stream, n, dv.d, d, c->ctl, 0, n2_scratch(c, n));
     ck(cudaMemcpyAsync(c->h_red, d, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
     ck(cudaStreamSynchronize(c->stream), "sync");
     std::memcpy(out, c->h_red, sizeof(double));
@@ -1076,9 +1091,9 @@ igm_status igm_solve(igm_ctx* c, const igm_split* m, const igm_csrf* a_fp, const
     In<double> db(b, n, st, w.b);
     ck(cudaMemsetAsync(w.x, 0, sizeof(double) * n, st), "x=0");
     reset_ctl(c);
-    launch_norm2_serial(st, n, db.d, nullptr, c->ctl, 1);  // ||b||
+    launch_norm2_serial(st, n, db.d, nullptr, c->ctl, 1, n2_scratch(c, n));  // ||b||
     launch_residual(st, *a_fp, w.x, db.d, w.r, c->ctl, true);
-    launch_norm2_serial(st, n, w.r, nullptr, c->ctl, 2);
+    launch_norm2_serial(st, n, w.r, nullptr, c->ctl, 2, n2_scratch(c, n));
     ck(cudaMemcpyAsync(c->h_ctl, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st), "ctl");
     ck(cudaStreamSynchronize(st), "sync");
     double relnorm = c->h_ctl->relnorm;
@@ -1112,7 +1127,7 @@ igm_status igm_solve(igm_ctx* c, const igm_split* m, const igm_csrf* a_fp, const
       if (dim == 0) break;
       ck(cudaMemsetAsync(&c->ctl->rmax_bits, 0, sizeof(u64), st), "rmax reset");
       launch_residual(st, *a_fp, w.x, db.d, w.r, c->ctl, true);
-      launch_norm2_serial(st, n, w.r, nullptr, c->ctl, 2);
+      launch_norm2_serial(st, n, w.r, nullptr, c->ctl, 2, n2_scratch(c, n));
       ck(cudaMemcpyAsync(c->h_ctl, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st), "ctl");
       ck(cudaStreamSynchronize(st), "sync");
       rep->refinements = k + 1;

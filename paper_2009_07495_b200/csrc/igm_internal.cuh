@@ -133,8 +133,10 @@ void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward,
 void launch_tri_fp(cudaStream_t st, const DevTri& t, bool backward,
                    const double* y, double* out, const Ctl* ctl,
                    const double* prescale /* divide y by *prescale or null */);
+// exact sequential-order norm2 (split.cpp:45-49); scratch: norm2_scratch_bytes(n)
+size_t norm2_scratch_bytes(long long n);
 void launch_norm2_serial(cudaStream_t st, long long n, const double* v,
-                         double* out, Ctl* ctl, int mode);
+                         double* out, Ctl* ctl, int mode, void* scratch);
 void launch_mgs_pass(cudaStream_t st, long long n, int mode, i64* w,
                      const i64* vprev, const i64* vcur, const u64* hacc,
                      u64* acc_out, u64* abs_out, int f, ShiftsD sh,
@@ -165,7 +167,7 @@ void launch_axpy_only(cudaStream_t st, long long n, i64* w, i64 h,
                       const i64* v, int f, int b1, u64* cnt, bool checked);
 void launch_gamma(cudaStream_t st, long long n, const double* r, Ctl* ctl);
 void launch_basis_norms(cudaStream_t st, long long n, int nb, int f,
-                        const i64* basis, double* tmp, double* out, Ctl* ctl);
+                        const i64* basis, void* scratch, double* out, Ctl* ctl);
 
 int num_sms(int device);
 void tri_trace_setup(int tile, unsigned long long* buf);

@@ -365,33 +365,37 @@ __device__ __forceinline__ u64 n2_inc(u64 a, int cls, u64 parity) {
   return cls == N2_DOWN ? a : (cls == N2_UP ? a + 1 : a + ((parity + a) & 1));
 }
 
-__global__ void __launch_bounds__(kN2Threads) k_norm2_exact(long long n, const double* __restrict__ v,
-                                                            const i64* __restrict__ raw, double scale,
-                                                            double* out, Ctl* ctl, int mode,
-                                                            int basis_idx) {
-  __shared__ Aut s_warp[32];
-  __shared__ int s_exit;
-  __shared__ u64 s_mprev;
-  __shared__ int s_E;
-  __shared__ u64 s_M;
-  __shared__ long long s_pos;
-  __shared__ int s_tail;
-  __shared__ double s_tailv;
-  if (mode == 3 && cycle_over(ctl)) return;
-  if (mode == 4 && (ctl->err || basis_idx >= ctl->nbasis)) return;
+// shared state of the exact chain inside one CTA
+struct N2State {
+  Aut warp[32];
+  int exit_at;
+  u64 mprev;
+  int E;          // binade of the running sum: s = M * 2^(E-52)
+  u64 M;
+  long long pos;  // next term
+  int tail;       // the sum became non-finite at pos-1: finish serially
+  double tailv;
+};
+
+__device__ __forceinline__ double n2_term(long long i, const double* __restrict__ v, const i64* __restrict__ raw,
+                                          double scale) {
+  const double x = raw ? dec(raw[i], scale) : v[i];
+  return __dmul_rn(x, x);
+}
+
+// Advance the exact chain from S.pos to hi (one CTA of kN2Threads threads):
+// chunks of kN2Chunk terms are classified against the current binade, scanned
+// as 2-state automata, and the first term that would leave the binade is
+// replayed with the real FP64 add.
+__device__ void n2_advance(long long hi, const double* __restrict__ v, const i64* __restrict__ raw, double scale,
+                           N2State& S) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (tid == 0) {
-    s_E = -1022;  // s = 0: subnormal binade, u = 2^-1074
-    s_M = 0;
-    s_pos = 0;
-    s_tail = 0;
-  }
-  __syncthreads();
   while (true) {
-    const long long pos = s_pos;
-    const int E = s_E;
-    const u64 M0 = s_M;
-    if (pos >= n || s_tail) break;
+    const long long pos = S.pos;
+    const int E = S.E;
+    const u64 M0 = S.M;
+    if (pos >= hi || S.tail) break;
+    const long long lim = min(hi, pos + kN2Chunk);
     const long long base = pos + static_cast<long long>(tid) * kN2Per;
     u64 a[kN2Per];
     int cls[kN2Per];
@@ -399,9 +403,8 @@ __global__ void __launch_bounds__(kN2Threads) k_norm2_exact(long long n, const d
 #pragma unroll
     for (int g = 0; g < kN2Per; ++g) {
       const long long idx = base + g;
-      if (idx < n && idx < pos + kN2Chunk) {
-        const double x = raw ? dec(raw[idx], scale) : v[idx];
-        cls[g] = n2_classify(__dmul_rn(x, x), E, a[g]);
+      if (idx < lim) {
+        cls[g] = n2_classify(n2_term(idx, v, raw, scale), E, a[g]);
       } else {
         cls[g] = N2_DOWN;
         a[g] = 0;
@@ -420,11 +423,11 @@ __global__ void __launch_bounds__(kN2Threads) k_norm2_exact(long long n, const d
       up.d1 = __shfl_up_sync(0xffffffffu, inc.d1, o);
       if (lane >= o) inc = aut_then(up, inc);
     }
-    if (lane == 31) s_warp[wid] = inc;
-    if (tid == 0) s_exit = INT_MAX;
+    if (lane == 31) S.warp[wid] = inc;
+    if (tid == 0) S.exit_at = INT_MAX;
     __syncthreads();
     if (wid == 0) {
-      Aut w = s_warp[lane];
+      Aut w = S.warp[lane];
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         Aut up;
@@ -432,18 +435,18 @@ __global__ void __launch_bounds__(kN2Threads) k_norm2_exact(long long n, const d
         up.d1 = __shfl_up_sync(0xffffffffu, w.d1, o);
         if (lane >= o) w = aut_then(up, w);
       }
-      s_warp[lane] = w;  // inclusive over warps
+      S.warp[lane] = w;  // inclusive over warps
     }
     __syncthreads();
     Aut ex{0, 0};
-    if (wid > 0) ex = s_warp[wid - 1];
+    if (wid > 0) ex = S.warp[wid - 1];
     {
       Aut lx;
       lx.d0 = __shfl_up_sync(0xffffffffu, inc.d0, 1);
       lx.d1 = __shfl_up_sync(0xffffffffu, inc.d1, 1);
       if (lane > 0) ex = aut_then(ex, lx);
     }
-    const Aut total = s_warp[31];
+    const Aut total = S.warp[31];
     // walk this thread's terms from the true incoming value; first exit
     u64 Mp = M0 + ((M0 & 1) ? ex.d1 : ex.d0);
     int my_exit = INT_MAX;
@@ -452,7 +455,7 @@ __global__ void __launch_bounds__(kN2Threads) k_norm2_exact(long long n, const d
     for (int g = 0; g < kN2Per; ++g) {
       if (my_exit != INT_MAX) break;
       const long long idx = base + g;
-      if (idx >= n || idx >= pos + kN2Chunk) break;
+      if (idx >= lim) break;
       const bool leave = cls[g] == N2_EXIT || a[g] >= kTwo53 ||
                          Mp + a[g] + (cls[g] != N2_DOWN ? 1 : 0) >= kTwo53;
       if (leave) {
@@ -462,63 +465,234 @@ __global__ void __launch_bounds__(kN2Threads) k_norm2_exact(long long n, const d
         Mp += n2_inc(a[g], cls[g], Mp & 1);
       }
     }
-    if (my_exit != INT_MAX) atomicMin(&s_exit, my_exit);
+    if (my_exit != INT_MAX) atomicMin(&S.exit_at, my_exit);
     __syncthreads();
-    const int xe = s_exit;
-    if (xe != INT_MAX && my_exit == xe) s_mprev = my_mprev;
+    const int xe = S.exit_at;
+    if (xe != INT_MAX && my_exit == xe) S.mprev = my_mprev;
     __syncthreads();
     if (tid == 0) {
       if (xe == INT_MAX) {
-        s_M = M0 + ((M0 & 1) ? total.d1 : total.d0);
-        s_pos = min(n, pos + kN2Chunk);
+        S.M = M0 + ((M0 & 1) ? total.d1 : total.d0);
+        S.pos = lim;
       } else {
         // replay the term that leaves the binade with the real FP64 add
         const long long idx = pos + xe;
-        const double x = raw ? dec(raw[idx], scale) : v[idx];
-        const double sp = ldexp(static_cast<double>(s_mprev), E - 52);
-        const double sn = __dadd_rn(sp, __dmul_rn(x, x));
+        const double sp = ldexp(static_cast<double>(S.mprev), E - 52);
+        const double sn = __dadd_rn(sp, n2_term(idx, v, raw, scale));
         if (!isfinite(sn)) {
-          s_tail = 1;
-          s_tailv = sn;
-          s_pos = idx + 1;
+          S.tail = 1;
+          S.tailv = sn;
+          S.pos = idx + 1;
         } else {
           const u64 b = static_cast<u64>(__double_as_longlong(sn));
           const int ebits = static_cast<int>((b >> 52) & 0x7ff);
           const int En = ebits == 0 ? -1022 : max(ebits - 1023, -1022);
-          s_E = En;
-          s_M = static_cast<u64>(ldexp(sn, 52 - En));
-          s_pos = idx + 1;
+          S.E = En;
+          S.M = static_cast<u64>(ldexp(sn, 52 - En));
+          S.pos = idx + 1;
         }
       }
     }
     __syncthreads();
   }
-  if (tid == 0) {
-    double acc;
-    if (s_tail) {  // non-finite partial sum: finish the chain serially
-      acc = s_tailv;
-      for (long long i = s_pos; i < n; ++i) {
-        const double x = raw ? dec(raw[i], scale) : v[i];
-        acc = __dadd_rn(acc, __dmul_rn(x, x));
-      }
-    } else {
-      acc = ldexp(static_cast<double>(s_M), s_E - 52);
-    }
-    const double r = __dsqrt_rn(acc);
-    switch (mode) {
-      case 0: *out = r; break;
-      case 1: ctl->nb = r; break;
-      case 2:
-        ctl->nr = r;
-        ctl->relnorm = ctl->nb == 0.0 ? r : __ddiv_rn(r, ctl->nb);
-        break;
-      case 3:
-        ctl->r0n = r;
-        if (r == 0.0) ctl->stop = 1;
-        break;
-      case 4: out[basis_idx] = r; break;
-    }
+}
+
+__device__ __forceinline__ bool n2_skip(const Ctl* ctl, int mode, int basis_idx) {
+  return (mode == 3 && cycle_over(ctl)) || (mode == 4 && (ctl->err || basis_idx >= ctl->nbasis));
+}
+
+// final value of the chain and its destination (see k_norm2_serial's modes)
+__device__ void n2_finish(long long n, const double* __restrict__ v, const i64* __restrict__ raw, double scale,
+                          const N2State& S, double* out, Ctl* ctl, int mode, int basis_idx) {
+  double acc;
+  if (S.tail) {  // non-finite partial sum: finish the chain serially
+    acc = S.tailv;
+    for (long long i = S.pos; i < n; ++i) acc = __dadd_rn(acc, n2_term(i, v, raw, scale));
+  } else {
+    acc = ldexp(static_cast<double>(S.M), S.E - 52);
   }
+  const double r = __dsqrt_rn(acc);
+  switch (mode) {
+    case 0: *out = r; break;
+    case 1: ctl->nb = r; break;
+    case 2:
+      ctl->nr = r;
+      ctl->relnorm = ctl->nb == 0.0 ? r : __ddiv_rn(r, ctl->nb);
+      break;
+    case 3:
+      ctl->r0n = r;
+      if (r == 0.0) ctl->stop = 1;
+      break;
+    case 4: out[basis_idx] = r; break;
+  }
+}
+
+__device__ __forceinline__ void n2_init(N2State& S) {
+  S.E = -1022;  // s = 0: subnormal binade, u = 2^-1074
+  S.M = 0;
+  S.pos = 0;
+  S.tail = 0;
+}
+
+// single-CTA exact chain (short vectors)
+__global__ void __launch_bounds__(kN2Threads) k_norm2_exact(long long n, const double* __restrict__ v,
+                                                            const i64* __restrict__ raw, double scale,
+                                                            double* out, Ctl* ctl, int mode,
+                                                            int basis_idx) {
+  __shared__ N2State S;
+  if (n2_skip(ctl, mode, basis_idx)) return;
+  if (threadIdx.x == 0) n2_init(S);
+  __syncthreads();
+  n2_advance(n, v, raw, scale, S);
+  if (threadIdx.x == 0) n2_finish(n, v, raw, scale, S, out, ctl, mode, basis_idx);
+}
+
+// Multi-CTA form for long vectors.  A block of kN2Chunk terms can be applied
+// in O(1) -- M += d(parity of M) -- when (i) the running sum's binade at the
+// block start is the one the block was classified against and (ii) no term
+// can leave it: M + max(d0, d1) + 1 < 2^53, no term >= 2^53 ulps, no
+// non-finite term.  Pass 1 sums each block's squares (any order: only a
+// guess), pass 2 guesses each block's starting binade from the approximate
+// prefix and reduces the block's automaton against it, pass 3 (one CTA) walks
+// the blocks in order: O(1) per block when (i)-(ii) hold, otherwise the
+// block is replayed exactly (n2_advance) from the true state.  Replays happen
+// only around binade crossings (~log2 n of them, mostly in the first block).
+struct N2Blk {
+  double s;   // approximate sum of the block's squares
+  int E;      // binade the automaton was built against
+  int bad;    // a term >= 2^53 ulps or non-finite: always replay
+  u64 d0, d1;
+};
+
+constexpr int kN2BThreads = 512;
+constexpr int kN2BPer = kN2Chunk / kN2BThreads;
+
+__global__ void __launch_bounds__(kN2BThreads) k_n2_bsum(long long n, const double* __restrict__ v,
+                                                         const i64* __restrict__ raw, double scale, N2Blk* blk,
+                                                         const Ctl* ctl, int mode, int basis_idx) {
+  __shared__ double sh[kN2BThreads / 32];
+  if (n2_skip(ctl, mode, basis_idx)) return;
+  const long long lo = static_cast<long long>(blockIdx.x) * kN2Chunk;
+  const long long hi = min(n, lo + kN2Chunk);
+  double acc = 0.0;
+  for (long long i = lo + threadIdx.x; i < hi; i += kN2BThreads) acc += n2_term(i, v, raw, scale);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kN2BThreads / 32; ++w) t += sh[w];
+    blk[blockIdx.x].s = t;
+  }
+}
+
+__global__ void __launch_bounds__(kN2BThreads) k_n2_baut(long long n, const double* __restrict__ v,
+                                                         const i64* __restrict__ raw, double scale, N2Blk* blk,
+                                                         const Ctl* ctl, int mode, int basis_idx) {
+  __shared__ double shs[kN2BThreads / 32];
+  __shared__ Aut sha[kN2BThreads / 32];
+  __shared__ int sbad;
+  __shared__ int sE;
+  if (n2_skip(ctl, mode, basis_idx)) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // approximate prefix of the earlier blocks -> guessed starting binade
+  double p = 0.0;
+  for (int b = tid; b < static_cast<int>(blockIdx.x); b += kN2BThreads) p += blk[b].s;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) p += __shfl_down_sync(0xffffffffu, p, o);
+  if (lane == 0) shs[wid] = p;
+  if (tid == 0) sbad = 0;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kN2BThreads / 32; ++w) t += shs[w];
+    int E = -1022;
+    if (t > 0.0 && isfinite(t)) {
+      const int eb = static_cast<int>((static_cast<u64>(__double_as_longlong(t)) >> 52) & 0x7ff);
+      E = eb == 0 ? -1022 : max(eb - 1023, -1022);
+    }
+    sE = E;
+  }
+  __syncthreads();
+  const int E = sE;
+  // this thread's consecutive run, composed in order
+  const long long lo = static_cast<long long>(blockIdx.x) * kN2Chunk + static_cast<long long>(tid) * kN2BPer;
+  Aut mine{0, 0};
+  int bad = 0;
+#pragma unroll 4
+  for (int g = 0; g < kN2BPer; ++g) {
+    const long long idx = lo + g;
+    if (idx >= n) break;
+    u64 aa;
+    const int c = n2_classify(n2_term(idx, v, raw, scale), E, aa);
+    if (c == N2_EXIT || aa >= kTwo53) bad = 1;
+    Aut e;
+    e.d0 = n2_inc(aa, c == N2_EXIT ? N2_DOWN : c, 0);
+    e.d1 = n2_inc(aa, c == N2_EXIT ? N2_DOWN : c, 1);
+    mine = aut_then(mine, e);
+  }
+  // ordered reduction: warp (lane order), then warps (warp order)
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    Aut up;
+    up.d0 = __shfl_down_sync(0xffffffffu, mine.d0, o);
+    up.d1 = __shfl_down_sync(0xffffffffu, mine.d1, o);
+    if ((lane & (2 * o - 1)) == 0 && lane + o < 32) mine = aut_then(mine, up);
+  }
+  if (lane == 0) sha[wid] = mine;
+  if (bad) sbad = 1;
+  __syncthreads();
+  if (tid == 0) {
+    Aut t = sha[0];
+    for (int w = 1; w < kN2BThreads / 32; ++w) t = aut_then(t, sha[w]);
+    N2Blk& B = blk[blockIdx.x];
+    B.E = E;
+    B.bad = sbad;
+    B.d0 = t.d0;
+    B.d1 = t.d1;
+  }
+}
+
+__global__ void __launch_bounds__(kN2Threads) k_n2_walk(long long n, int nblk, const double* __restrict__ v,
+                                                        const i64* __restrict__ raw, double scale,
+                                                        const N2Blk* blk, double* out, Ctl* ctl, int mode,
+                                                        int basis_idx) {
+  constexpr int kPage = 512;
+  __shared__ N2State S;
+  __shared__ N2Blk page[kPage];
+  __shared__ int s_fast;
+  if (n2_skip(ctl, mode, basis_idx)) return;
+  if (threadIdx.x == 0) n2_init(S);
+  for (int p0 = 0; p0 < nblk; p0 += kPage) {
+    const int np = min(kPage, nblk - p0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < np; i += blockDim.x) page[i] = blk[p0 + i];
+    __syncthreads();
+    int b = 0;
+    while (b < np) {
+      if (threadIdx.x == 0) {
+        // O(1) blocks, sequentially, until one needs an exact replay
+        while (b < np && !S.tail) {
+          const N2Blk& B = page[b];
+          const u64 dm = B.d0 > B.d1 ? B.d0 : B.d1;
+          if (B.bad || B.E != S.E || S.M + dm + 1 >= kTwo53) break;
+          S.M += (S.M & 1) ? B.d1 : B.d0;
+          ++b;
+        }
+        S.pos = min(n, static_cast<long long>(p0 + b) * kN2Chunk);
+        s_fast = b;
+      }
+      __syncthreads();
+      b = s_fast;
+      if (b >= np || S.tail) break;
+      n2_advance(min(n, static_cast<long long>(p0 + b + 1) * kN2Chunk), v, raw, scale, S);  // replay block b
+      ++b;
+    }
+    if (S.tail) break;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) n2_finish(n, v, raw, scale, S, out, ctl, mode, basis_idx);
 }
 
 // K10 encode v1 = trunc(ldexp(r0_i / ||r0||, f)) (gmres_int.cpp:77-81,
@@ -1561,25 +1735,38 @@ static bool norm2_serial_forced() {
   return v != 0;
 }
 
-void launch_norm2_serial(cudaStream_t st, long long n, const double* v, double* out, Ctl* ctl,
-                         int mode) {
-  ProfScope prof_(st, KC_NORM2);
-  if (norm2_serial_forced())
-    k_norm2_serial<<<1, 256, 0, st>>>(n, v, nullptr, 1.0, out, ctl, mode, 0);
-  else
-    k_norm2_exact<<<1, kN2Threads, 0, st>>>(n, v, nullptr, 1.0, out, ctl, mode, 0);
+size_t norm2_scratch_bytes(long long n) {
+  return sizeof(N2Blk) * static_cast<size_t>(std::max<long long>(1, (n + kN2Chunk - 1) / kN2Chunk));
+}
+
+// exact norm2 chain of v (or of the decoded raw words when raw != null)
+static void norm2_enqueue(cudaStream_t st, long long n, const double* v, const i64* raw, double scale,
+                          double* out, Ctl* ctl, int mode, int basis_idx, void* scratch) {
+  if (norm2_serial_forced()) {
+    k_norm2_serial<<<1, 256, 0, st>>>(n, v, raw, scale, out, ctl, mode, basis_idx);
+  } else if (n <= 2 * kN2Chunk || scratch == nullptr) {
+    k_norm2_exact<<<1, kN2Threads, 0, st>>>(n, v, raw, scale, out, ctl, mode, basis_idx);
+  } else {
+    const int nblk = static_cast<int>((n + kN2Chunk - 1) / kN2Chunk);
+    N2Blk* blk = static_cast<N2Blk*>(scratch);
+    k_n2_bsum<<<nblk, kN2BThreads, 0, st>>>(n, v, raw, scale, blk, ctl, mode, basis_idx);
+    k_n2_baut<<<nblk, kN2BThreads, 0, st>>>(n, v, raw, scale, blk, ctl, mode, basis_idx);
+    k_n2_walk<<<1, kN2Threads, 0, st>>>(n, nblk, v, raw, scale, blk, out, ctl, mode, basis_idx);
+  }
   LAUNCH_CHECK();
 }
 
-void launch_basis_norms(cudaStream_t st, long long n, int nb, int f, const i64* basis, double* tmp,
+void launch_norm2_serial(cudaStream_t st, long long n, const double* v, double* out, Ctl* ctl, int mode,
+                         void* scratch) {
+  ProfScope prof_(st, KC_NORM2);
+  norm2_enqueue(st, n, v, nullptr, 1.0, out, ctl, mode, 0, scratch);
+}
+
+void launch_basis_norms(cudaStream_t st, long long n, int nb, int f, const i64* basis, void* scratch,
                         double* out, Ctl* ctl) {
   ProfScope prof_(st, KC_NORM2);
-  (void)tmp;
-  for (int k = 0; k < nb; ++k) {
-    k_norm2_exact<<<1, kN2Threads, 0, st>>>(n, nullptr, basis + static_cast<long long>(k) * n,
-                                            ldexp(1.0, -f), out, ctl, 4, k);
-    LAUNCH_CHECK();
-  }
+  for (int k = 0; k < nb; ++k)
+    norm2_enqueue(st, n, nullptr, basis + static_cast<long long>(k) * n, ldexp(1.0, -f), out, ctl, 4, k, scratch);
 }
 
 void launch_encode(cudaStream_t st, long long n, const double* r0, i64* v0, int f, Ctl* ctl) {
