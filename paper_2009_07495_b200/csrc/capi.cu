@@ -465,6 +465,8 @@ void enqueue_cycle(igm_ctx* c, const CycleParams& p, CycleMode mode, const doubl
   launch_encode(st, n, r0, w.basis, f, ctl);
   // ---- Arnoldi steps (gmres_int.cpp:90-160)
   const size_t cstride = static_cast<size_t>(K_COUNT) * OP_COUNT;
+  const long long arn_S = arnoldi_slice(n, c->device);
+  unsigned gbase = 0;  // grid-barrier arrivals so far in this cycle (Ctl::gbar reset by cycle_init)
   for (int j = 0; j < M; ++j) {
     u64* cstep = w.cnt + static_cast<size_t>(j) * cstride;
     i64* vj = w.basis + static_cast<long long>(j) * n;
@@ -477,6 +479,12 @@ void enqueue_cycle(igm_ctx* c, const CycleParams& p, CycleMode mode, const doubl
     }
     u64* accj = w.acc + static_cast<size_t>(j) * (M + 1);
     u64* absj = w.absacc + static_cast<size_t>(j) * (M + 1) * 2;
+    if (arn_S > 0) {  // one persistent launch: passes, scalar work and vec_div
+      launch_arnoldi(st, n, j, arn_S, w.w, w.basis, accj, absj, w.nacc + j, w.nabs + 2 * j, f, sh, cstep, w.hess, ld,
+                     w.g, w.cs, w.sn, w.gabs, ctl, gbase, p.checked);
+      gbase += static_cast<unsigned>(arnoldi_barriers(j));
+      continue;
+    }
     for (int i = 0; i <= j; ++i) {
       const i64* vi = w.basis + static_cast<long long>(i) * n;
       const i64* vp = i > 0 ? w.basis + static_cast<long long>(i - 1) * n : nullptr;

@@ -54,6 +54,7 @@ struct Ctl {
   u64 rmax_bits;  // max |r_i| as IEEE bits (non-negative doubles order as u64)
   double nb, nr, relnorm;
   double scalar;  // scratch result of norm2 kernels
+  unsigned gbar;  // grid-barrier arrivals of the persistent Arnoldi kernel (reset per cycle)
 };
 
 struct DevSplit {
@@ -166,6 +167,12 @@ void launch_fx_red(cudaStream_t st, long long n, int mode, const i64* v,
 void launch_axpy_only(cudaStream_t st, long long n, i64* w, i64 h,
                       const i64* v, int f, int b1, u64* cnt, bool checked);
 void launch_gamma(cudaStream_t st, long long n, const double* r, Ctl* ctl);
+// persistent Arnoldi step (passes + scalar + vec_div in one cooperative launch)
+long long arnoldi_slice(long long n, int device);
+int arnoldi_barriers(int j);
+void launch_arnoldi(cudaStream_t st, long long n, int j, long long S, const i64* w, i64* basis, u64* accj,
+                    u64* absj, u64* nacc, u64* nabs, int f, ShiftsD sh, u64* cstep, i64* hess, int ld, i64* g,
+                    i64* cs, i64* sn, i64* gabs, Ctl* ctl, unsigned gbase, bool checked);
 void launch_basis_norms(cudaStream_t st, long long n, int nb, int f,
                         const i64* basis, void* scratch, double* out, Ctl* ctl);
 

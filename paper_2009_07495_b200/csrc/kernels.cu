@@ -1044,10 +1044,10 @@ __device__ bool abs_small(const u64* ab) {
   return s < (static_cast<unsigned __int128>(1) << 63);
 }
 
-__global__ void k_step_scalar(int j, int f, ShiftsD sh, const u64* acc_col, const u64* abs_col,
-                              const u64* nacc, const u64* nabs, i64* hess, int ld, i64* g,
-                              i64* cs, i64* sn, i64* gabs, const i64* w, u64* cnt_step, Ctl* ctl,
-                              int checked) {
+__device__ void step_scalar_dev(int j, int f, ShiftsD sh, const u64* acc_col, const u64* abs_col,
+                                const u64* nacc, const u64* nabs, i64* hess, int ld, i64* g,
+                                i64* cs, i64* sn, i64* gabs, const i64* w, u64* cnt_step, Ctl* ctl,
+                                int checked) {
   ctl->do_vecdiv = 0;
   if (cycle_over(ctl)) return;
   Ev ev{cnt_step, checked != 0};
@@ -1163,7 +1163,304 @@ __global__ void k_step_scalar(int j, int f, ShiftsD sh, const u64* acc_col, cons
   if (happy) ctl->stop = 1;
 }
 
+__global__ void k_step_scalar(int j, int f, ShiftsD sh, const u64* acc_col, const u64* abs_col,
+                              const u64* nacc, const u64* nabs, i64* hess, int ld, i64* g,
+                              i64* cs, i64* sn, i64* gabs, const i64* w, u64* cnt_step, Ctl* ctl,
+                              int checked) {
+  step_scalar_dev(j, f, sh, acc_col, abs_col, nacc, nabs, hess, ld, g, cs, sn, gabs, w, cnt_step, ctl, checked);
+}
+
+// ---------------------------------------------------------------------------
+// K2-K5 as ONE persistent kernel per Arnoldi step (gmres_int.cpp:90-126):
+// the same passes, reductions and scalar work as k_mgs / k_step_scalar /
+// k_vec_div, but each CTA keeps its slice of w -- and of the previous basis
+// vector -- in shared memory across the j+3 passes of the step, so a pass
+// reads one basis vector from HBM instead of streaming w in and out, and the
+// step costs one launch.  Passes are separated by a grid barrier (all CTAs
+// are co-resident: cooperative launch, one CTA per SM).  Every arithmetic
+// step is the per-element one of the pass kernels, and reductions are the
+// same wrapping (order-free) u64 sums, so results are bit-identical.
+constexpr int kArnThreads = 1024;
+constexpr size_t kArnSmemMax = 227 * 1024 - 1024;  // dynamic; the static reduction scratch is 768 B
+
+// grid barrier: arrival count since the cycle started (Ctl::gbar); barrier
+// number k completes when all G CTAs have arrived k times.  The acquire spin
+// also orders this SM's later loads after every CTA's pre-barrier atomics.
+__device__ __forceinline__ u64 ld_cg_u64(const u64* p) {
+  u64 v;
+  asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// ...and thread 0 fetches the one word the next pass needs (a reduced
+// accumulator) and broadcasts it through shared memory: one L2 request per
+// CTA instead of one per warp on a single hot line
+__device__ __forceinline__ u64 grid_barrier(Ctl* ctl, unsigned target, const u64* fetch, u64* s_word) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned* p = &ctl->gbar;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    } while (v < target);
+    if (fetch) *s_word = ld_cg_u64(fetch);
+  }
+  __syncthreads();
+  return fetch ? *s_word : 0;
+}
+
+// CTA-wide wrapping sums of (s0, s1, s2) -> one atomic each (s1, s2 when CHECKED)
+template <bool CHECKED>
+__device__ __forceinline__ void cta_reduce_add(u64 s0, u64 s1, u64 s2, u64* out0, u64* out12, u64 (*red)[32]) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_down_sync(0xffffffffu, s0, o);
+    if (CHECKED) {
+      s1 += __shfl_down_sync(0xffffffffu, s1, o);
+      s2 += __shfl_down_sync(0xffffffffu, s2, o);
+    }
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][wid] = s0;
+    red[1][wid] = s1;
+    red[2][wid] = s2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u64 a = 0, b = 0, c = 0;
+    for (int i = 0; i < kArnThreads / 32; ++i) {
+      a += red[0][i];
+      b += red[1][i];
+      c += red[2][i];
+    }
+    atomicAdd(reinterpret_cast<unsigned long long*>(out0), static_cast<unsigned long long>(a));
+    if (CHECKED) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(out12), static_cast<unsigned long long>(b));
+      atomicAdd(reinterpret_cast<unsigned long long*>(out12 + 1), static_cast<unsigned long long>(c));
+    }
+  }
+  __syncthreads();
+}
+
+// per-element pieces of the passes (identical to k_mgs / k_vec_div)
+struct ArnAcc {
+  u64 sum = 0, ahi = 0, alo = 0, n1 = 0, n2 = 0, n3 = 0;
+  __device__ __forceinline__ void abs_add(i64 t) {
+    const u64 at = t < 0 ? 0ull - static_cast<u64>(t) : static_cast<u64>(t);
+    ahi += at >> 32;
+    alo += at & 0xffffffffull;
+  }
+};
+
+__device__ __forceinline__ void lds_q(const i64* p, i64 (&v)[4]) {
+  const longlong2 a = *reinterpret_cast<const longlong2*>(p), b = *reinterpret_cast<const longlong2*>(p + 2);
+  v[0] = a.x;
+  v[1] = a.y;
+  v[2] = b.x;
+  v[3] = b.y;
+}
+__device__ __forceinline__ void sts_q(i64* p, const i64 (&v)[4]) {
+  *reinterpret_cast<longlong2*>(p) = make_longlong2(v[0], v[1]);
+  *reinterpret_cast<longlong2*>(p + 2) = make_longlong2(v[2], v[3]);
+}
+
+// Walk this CTA's rows four at a time (256-bit global, 128-bit shared
+// accesses), then the < 4 tail rows; fn(r, k, ...) handles row r.
+template <typename F>
+__device__ __forceinline__ void arn_rows(long long cnt, F&& fn) {
+  const long long nq = cnt >> 2;
+#pragma unroll 2
+  for (long long q = threadIdx.x; q < nq; q += kArnThreads) fn(q * 4, 4);
+  for (long long r = nq * 4 + threadIdx.x; r < cnt; r += kArnThreads) fn(r, 1);
+}
+
+template <bool CHECKED>
+__global__ void __launch_bounds__(kArnThreads, 1)
+    k_arnoldi(long long n, int j, long long S, const i64* __restrict__ win, i64* basis, u64* accj, u64* absj,
+              u64* nacc, u64* nabs, int f, ShiftsD sh, u64* cstep, i64* hess, int ld, i64* g, i64* cs, i64* sn,
+              i64* gabs, Ctl* ctl, unsigned gbase) {
+  extern __shared__ __align__(16) i64 arn_sm[];
+  __shared__ u64 red[3][32];
+  __shared__ u64 s_word;
+  __shared__ int s_vd[6];
+  if (cycle_over(ctl)) return;  // uniform: ctl is not written before the first barrier
+  const unsigned G = gridDim.x;
+  unsigned nbar = gbase;
+  i64* sw = arn_sm;      // this CTA's rows of w
+  i64* sv = arn_sm + S;  // this CTA's rows of the previous pass's basis vector
+  const long long lo = static_cast<long long>(blockIdx.x) * S;
+  const long long cnt = max(0LL, min(n, lo + S) - lo);
+  u64 *cA = cstep + K_AXPY * OP_COUNT, *cD = cstep + K_DOT * OP_COUNT, *cN = cstep + K_NORM * OP_COUNT;
+  const int post = f - sh.axpy_b1;
+  // a quad (k == 4) or a single row (k == 1) of global / shared data
+  auto gload = [](const i64* p, int k, i64 (&v)[4]) {
+    if (k == 4) ld_v4_nc(p, v);
+    else v[0] = __ldg(p);
+  };
+  auto sload = [](const i64* p, int k, i64 (&v)[4]) {
+    if (k == 4) lds_q(p, v);
+    else v[0] = *p;
+  };
+  auto sstore = [](i64* p, int k, const i64 (&v)[4]) {
+    if (k == 4) sts_q(p, v);
+    else *p = v[0];
+  };
+  auto dot_term = [&](i64 wl, i64 c, ArnAcc& A) {
+    const i64 a = asr(wl, sh.dot_b1), b = asr(c, sh.dot_b2);
+    const i64 t = wmul(a, b);
+    A.sum += static_cast<u64>(t);
+    if (CHECKED) {
+      A.n3 += mul_ovf(a, b);
+      A.abs_add(t);
+    }
+  };
+  auto axpy_term = [&](i64 hs, i64 vp, i64& wl, ArnAcc& A) {
+    const i64 d = asr(wmul(hs, vp), post);
+    if (CHECKED) {
+      A.n1 += mul_ovf(hs, vp);
+      A.n2 += sub_ovf(wl, d);
+    }
+    wl = wsub(wl, d);
+  };
+  // ---- pass 0: w -> shared memory, dot_0 = <w, v_0>
+  {
+    const i64* v0 = basis + lo;
+    ArnAcc A;
+    arn_rows(cnt, [&](long long r, int k) {
+      i64 wq[4], cq[4];
+      gload(win + lo + r, k, wq);
+      gload(v0 + r, k, cq);
+      sstore(sw + r, k, wq);
+      sstore(sv + r, k, cq);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (e < k) dot_term(wq[e], cq[e], A);
+    });
+    if (CHECKED) bump(cD, OP_MUL, A.n3);
+    cta_reduce_add<CHECKED>(A.sum, A.ahi, A.alo, accj + 0, absj + 0, red);
+  }
+  // ---- passes 1..j: axpy_{i-1} (v_{i-1} from shared memory), dot_i
+  const int e0 = f - sh.dot_b1 - sh.dot_b2;
+  auto h_of = [&](u64 acc) {  // h_{i-1} re-derived from the reduced accumulator
+    const i64 a = static_cast<i64>(acc);
+    const i64 h = e0 >= 0 ? asr(a, e0) : wrap_shl(a, -e0);
+    return asr(h, sh.axpy_b1);
+  };
+  for (int i = 1; i <= j; ++i) {
+    const i64 hs = h_of(grid_barrier(ctl, (++nbar) * G, accj + i - 1, &s_word));
+    const i64* vi = basis + static_cast<long long>(i) * n + lo;
+    ArnAcc A;
+    arn_rows(cnt, [&](long long r, int k) {
+      i64 wq[4], pq[4], cq[4];
+      gload(vi + r, k, cq);
+      sload(sw + r, k, wq);
+      sload(sv + r, k, pq);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (e < k) {
+          axpy_term(hs, pq[e], wq[e], A);
+          dot_term(wq[e], cq[e], A);
+        }
+      sstore(sw + r, k, wq);
+      sstore(sv + r, k, cq);
+    });
+    if (CHECKED) {
+      bump(cA, OP_MUL, A.n1);
+      bump(cA, OP_SUB, A.n2);
+      bump(cD, OP_MUL, A.n3);
+    }
+    cta_reduce_add<CHECKED>(A.sum, A.ahi, A.alo, accj + i, absj + 2 * i, red);
+  }
+  // ---- axpy_j, then the norm sum of the orthogonalised w
+  {
+    const i64 hs = h_of(grid_barrier(ctl, (++nbar) * G, accj + j, &s_word));
+    ArnAcc A;
+    arn_rows(cnt, [&](long long r, int k) {
+      i64 wq[4], pq[4];
+      sload(sw + r, k, wq);
+      sload(sv + r, k, pq);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (e < k) {
+          axpy_term(hs, pq[e], wq[e], A);
+          const i64 sq = asr(wq[e], sh.norm_b1);
+          const i64 t = wmul(sq, sq);
+          A.sum += static_cast<u64>(t);
+          if (CHECKED) {
+            A.n3 += mul_ovf(sq, sq);
+            A.abs_add(t);
+          }
+        }
+      sstore(sw + r, k, wq);
+    });
+    if (CHECKED) {
+      bump(cA, OP_MUL, A.n1);
+      bump(cA, OP_SUB, A.n2);
+      bump(cN, OP_MUL, A.n3);
+    }
+    cta_reduce_add<CHECKED>(A.sum, A.ahi, A.alo, nacc, nabs, red);
+  }
+  // ---- per-step scalar work (one thread), then v_{j+1} = w / h_{j+1,j}
+  grid_barrier(ctl, (++nbar) * G, nullptr, nullptr);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    __threadfence();  // this SM's L1 holds no stale copy of the reduced words
+    step_scalar_dev(j, f, sh, accj, absj, nacc, nabs, hess, ld, g, cs, sn, gabs, sw, cstep, ctl, CHECKED ? 1 : 0);
+  }
+  const u64 dm = grid_barrier(ctl, (++nbar) * G, &ctl->div_m, &s_word);
+  if (threadIdx.x == 0) {  // the divisor's magic, once per CTA
+    volatile const int* c = &ctl->do_vecdiv;
+    s_vd[0] = c[0];
+    s_vd[1] = *static_cast<volatile int*>(&ctl->div_sh1);
+    s_vd[2] = *static_cast<volatile int*>(&ctl->div_sh2);
+    s_vd[3] = *static_cast<volatile int*>(&ctl->div_neg);
+    s_vd[4] = *static_cast<volatile int*>(&ctl->div_m1);
+  }
+  __syncthreads();
+  if (!s_vd[0]) return;
+  {
+    SDivMagic gm;
+    gm.u.m = dm;
+    gm.u.sh1 = s_vd[1];
+    gm.u.sh2 = s_vd[2];
+    gm.den_neg = s_vd[3];
+    gm.den_is_m1 = s_vd[4];
+    const int b1 = sh.div_b1, ee = f - sh.div_b1 - sh.div_b2;
+    i64* out = basis + static_cast<long long>(j + 1) * n + lo;
+    u64 nshl = 0, ndiv = 0;
+    arn_rows(cnt, [&](long long r, int k) {
+      i64 wq[4], vq[4];
+      sload(sw + r, k, wq);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (e < k) {
+          const i64 a = wq[e];
+          const i64 num = wrap_shl(a, b1);
+          const i64 q = sdiv(num, gm);
+          if (ee >= 0) {
+            vq[e] = wrap_shl(q, ee);
+            if (CHECKED) nshl += shl_ovf(q, ee);
+          } else {
+            vq[e] = asr(q, -ee);
+          }
+          if (CHECKED) {
+            nshl += shl_ovf(a, b1);
+            ndiv += sdiv_ovf(num, gm);
+          }
+        }
+      if (k == 4) st_v4(out + r, vq);
+      else out[r] = vq[0];
+    });
+    if (CHECKED) {
+      bump(cstep + K_VEC_DIV * OP_COUNT, OP_SHL, nshl);
+      bump(cstep + K_VEC_DIV * OP_COUNT, OP_DIV, ndiv);
+    }
+  }
+}
+
 __global__ void k_cycle_init(Ctl* ctl, i64* g, int f) {
+  ctl->gbar = 0;
   ctl->stop = 0;
   ctl->dim = 0;
   ctl->nbasis = 1;
@@ -1854,6 +2151,42 @@ void launch_step_scalar(cudaStream_t st, int j, int f, ShiftsD sh, const u64* ac
   ProfScope prof_(st, KC_SCALAR);
   k_step_scalar<<<1, 1, 0, st>>>(j, f, sh, acc_col, abs_col, nacc, nabs, hess, ld, g, cs, sn, gabs,
                                  w, cnt_step, ctl, checked ? 1 : 0);
+  LAUNCH_CHECK();
+}
+
+// rows per CTA and dynamic shared memory of the persistent step kernel; 0
+// when w and one basis slice do not fit on chip (the pass kernels are used)
+long long arnoldi_slice(long long n, int device) {
+  static const int off = [] {
+    const char* e = std::getenv("IGM_ARNOLDI");
+    return e && e[0] == '0' ? 1 : 0;
+  }();
+  if (off || n < 4096 || n % 4 != 0) return 0;  // 32-byte aligned basis vectors
+  const int G = num_sms(device);
+  const long long S = ((n + G - 1) / G + 3) / 4 * 4;
+  const size_t bytes = static_cast<size_t>(S) * 16;
+  if (bytes > kArnSmemMax) return 0;
+  return S;
+}
+
+int arnoldi_barriers(int j) { return j + 3; }
+
+void launch_arnoldi(cudaStream_t st, long long n, int j, long long S, const i64* w, i64* basis, u64* accj,
+                    u64* absj, u64* nacc, u64* nabs, int f, ShiftsD sh, u64* cstep, i64* hess, int ld, i64* g,
+                    i64* cs, i64* sn, i64* gabs, Ctl* ctl, unsigned gbase, bool checked) {
+  ProfScope prof_(st, KC_MGS);
+  const int G = num_sms(0);
+  const size_t smem = static_cast<size_t>(S) * 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_arnoldi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kArnSmemMax));
+    cudaFuncSetAttribute(k_arnoldi<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kArnSmemMax));
+    attr = true;
+  }
+  void* args[] = {&n, &j, &S, &w, &basis, &accj, &absj, &nacc, &nabs, &f, &sh, &cstep,
+                  &hess, &ld, &g, &cs, &sn, &gabs, &ctl, &gbase};
+  const void* fn = checked ? reinterpret_cast<const void*>(k_arnoldi<true>) : reinterpret_cast<const void*>(k_arnoldi<false>);
+  cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kArnThreads), args, smem, st);
   LAUNCH_CHECK();
 }
 

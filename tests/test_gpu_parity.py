@@ -4,6 +4,7 @@ word (basis, Hessenberg, g, rotations, SpMV / ILU outputs) and on the FP64
 bookends (x, residual history) -- the FP kernels reproduce the reference's
 operation order with no contraction."""
 import hashlib
+import re
 
 import numpy as np
 import pytest
@@ -384,3 +385,45 @@ def test_ilu_apply_unstructured_many_tiles(gpu, oracle):
     want = oracle.apply_inverse(il, y)
     for _ in range(2):
         assert np.array_equal(gpu.apply_inverse(F, y), want)
+
+
+@pytest.mark.parametrize("precond,g", [(False, 18), (True, 40)], ids=["plain", "ilu"])
+def test_run_cycle_large_vs_oracle(gpu, oracle, precond, g):
+    """A full cycle on grids whose rows do not divide evenly over the SMs
+    (18^3 unpreconditioned, 40^3 with ILU; n % 4 == 0 selects the persistent
+    path): the persistent Arnoldi-step
+    kernel against the oracle, checked (trace totals) and unchecked, every
+    basis word and Hessenberg entry; error behaviour must match too."""
+    from workloads import gen
+    from oracle.ffi import CheckerError
+    from tests.cases import PRE, UNPRE
+    rp, ci, v = gen.upwind_3d(g, 20.0)
+    n = len(rp) - 1
+    A = oracle.csrf(rp, ci, v)
+    vals, scale = oracle.row_scale(A, 32)
+    comp, alphas, _ = oracle.build_split(vals, 32, 1)
+    sp = oracle.split(rp, ci, comp, alphas)
+    S = gpu.SplitMatrix(rp, ci, comp, alphas)
+    b = gen.uniform(78, n)
+    plan = PRE if precond else UNPRE
+    F = il = None
+    if precond:
+        lo, up = oracle.factorize_split_cast(oracle.csrf(rp, ci, vals))
+        il = oracle.ilu(lo, up)
+        F = gpu.IluFactors(lo, up)
+    for checked in (False, True):
+        t1, t2 = (gpu.FxTrace(), PyTrace()) if checked else (None, None)
+        cfg = gpu.CycleConfig(m=12, frac_bits=30, shifts=gpu.ShiftPlan(*plan), s=0, precond=F)
+        try:
+            o = oracle.run_cycle(sp, 12, 30, 0, Shifts(*plan), b, np.zeros(n), precond=il, trace=t2)
+        except CheckerError as e:
+            with pytest.raises(ArithmeticError, match=re.escape(e.msg.split(":")[0])):
+                gpu.run_cycle(S, cfg, b, np.zeros(n), t1)
+            continue
+        r = gpu.run_cycle(S, cfg, b, np.zeros(n), t1)
+        assert r.dim == o["dim"] and r.dim > 3
+        assert np.array_equal(r.basis, o["basis"])
+        assert np.array_equal(r.hess, o["hess"]) and np.array_equal(r.g, o["g"])
+        assert np.array_equal(r.x, o["x"])
+        if checked:
+            assert t1.total_overflows() == t2.total
