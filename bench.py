@@ -300,6 +300,78 @@ def run_cfg5(args, igm, dev, local, g=400, k=30):
     }
 
 
+def run_cfg5_sharded(args, igm, dev, local, rank, ws, g=400, k=30):
+    """Config 5 row-block partitioned over the ws GPUs: each
+    rank owns 400/ws z-planes (its slab of the operator, built locally), the
+    SpMV input's boundary planes move to the neighbours (NCCL P2P), and each
+    of the k MGS passes all-reduces one int64 accumulator (exact).  Strong
+    scaling: the global problem is the 1-GPU config-5 call, word for word
+    (vectors are drawn by global row index)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2009_07495_b200 import dist as D
+    t0 = time.time()
+    sl = D.make_slab(g, g * g, rank, ws)
+    rp, ci, v, h0, own0, own1 = gen.upwind_3d_slab(g, 20.0, sl.z0, sl.z1)
+    assert (h0, own0, own1) == (sl.h0, sl.own0, sl.own1)
+    vals, _ = igm.row_scale(rp, ci, v, 16)
+    del v
+    comp, al, _ = igm.build_split(vals, 16, 1)
+    del vals
+    nnz_local = int(rp[-1])
+    be = D.CudaSlabBackend(igm, dev)
+    S = be.upload(rp, ci, comp, al)
+    del comp, rp, ci
+    dvc = f"cuda:{local}"
+    n = g ** 3
+    seed = gen.SEED_BASE ^ 5
+    g0, g1 = sl.global_rows
+    basis = torch.empty((k, sl.n_own), dtype=torch.int64, device=dvc)
+    for i in range(k):
+        basis[i] = gen.device_uniform_int40(sl.n_own, seed, (i + 1) * n + g0, dvc)
+    vown = gen.device_uniform_int40(sl.n_own, seed, g0, dvc)
+    work = dict(vext=torch.zeros(sl.next_, dtype=torch.int64, device=dvc),
+                wext=torch.zeros(sl.next_, dtype=torch.int64, device=dvc),
+                acc=torch.zeros(k, dtype=torch.int64, device=dvc))
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+    call = lambda: D.spmv_mgs_sharded(be, sl, S, 0, vown, basis, k, 30, 16, 0, 16, dist, work)
+    for _ in range(max(args.warmup, 1)):
+        call()
+    torch.cuda.synchronize()
+    barrier(ws)
+    stream = torch.cuda.ExternalStream(dev.stream, device=dvc)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        call()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, ws)
+    # global checksum of w and the h's: identical at every world size
+    w, acc = call()
+    torch.cuda.synchronize()
+    wsum = torch.tensor([int(w.sum().item()) & ((1 << 63) - 1)], dtype=torch.int64, device=dvc)
+    if ws > 1:
+        dist.all_reduce(wsum)
+    nnz = 7 * n - 6 * g * g
+    b_spmv = 12 * nnz + 4 * (n + 1) + 16 * n
+    b_mgs = (4 * k + 1) * 8 * n
+    hbm, src = peaks()
+    gbs = (b_spmv + b_mgs) / (ms / 1e3) / 1e9
+    del S, basis, vown, work
+    torch.cuda.empty_cache()
+    return {
+        "workload": f"cfg5 sharded: z-slabs of {g}^3 over {ws} GPU(s) ({sl.z1 - sl.z0} planes on rank {rank}), "
+                    f"halo exchange (NCCL P2P) + per-pass int64 allreduce; SpMV + MGS against {k} vectors",
+        "parallelism": f"z-slab x{ws}", "scaling": "strong", "ms_per_call": round(ms, 4),
+        "bytes_per_call": b_spmv + b_mgs, "GB/s": round(gbs, 1), "GB/s_per_gpu": round(gbs / ws, 1),
+        "frac_per_gpu": round(gbs / ws / hbm, 4), "peak": hbm, "peak_source": src,
+        "h_acc_checksum": [int(x) for x in acc.cpu().tolist()][:3], "w_checksum_low63": int(wsum.item()),
+        "rank0_local_nnz": nnz_local, "setup_s": round(setup_s, 1),
+    }
+
+
 # ----------------------------------------------------------------- B200 arm
 def roofline_line(micro, dom, achieved, dom_bytes, hbm, src, top, breakdown):
     """Dominant HBM-streaming kernel: the MGS pass in the config-5 call (all
@@ -405,10 +477,16 @@ def run_b200(args, ws, rank, local):
     micro = None
     if not args.no_cfg5:
         try:
-            micro = run_cfg5(args, igm, dev, local)
+            micro = run_cfg5(args, igm, dev, local) if ws == 1 else \
+                run_cfg5_sharded(args, igm, dev, local, rank, ws)
         except Exception as exc:
             micro = {"error": repr(exc)}
         log(f"[bench] cfg5 microbench: {micro}")
+    if args.cfg5_sharded and ws == 1 and not args.no_cfg5:
+        try:
+            micro["sharded_driver_1gpu"] = run_cfg5_sharded(args, igm, dev, local, rank, ws)
+        except Exception as exc:
+            micro["sharded_driver_1gpu"] = {"error": repr(exc)}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -452,6 +530,8 @@ def main():
     ap.add_argument("--grid", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cfg5", action="store_true", help="skip the config-5 kernel microbench")
+    ap.add_argument("--cfg5-sharded", action="store_true",
+                    help="at 1 GPU, also run the row-block partitioned config-5 driver")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     ws, rank, local = dist_init(args)

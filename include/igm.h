@@ -12,7 +12,8 @@
  * back into the same space the output pointer lives in.  Device buffers are
  * accessed on the context's stream (igm_ctx_stream): the caller orders any
  * producer stream before the call; every call returns with the stream
- * synchronised unless documented otherwise (igm_spmv_mgs with h_out == NULL).
+ * synchronised unless documented otherwise (igm_spmv_mgs with h_out == NULL,
+ * igm_mgs_pass).
  *
  * Errors: every call returns igm_status; igm_last_error() returns the message
  * of the last failure on the calling thread.  Status codes map 1:1 onto the
@@ -230,6 +231,19 @@ igm_status igm_spmv_mgs(igm_ctx* ctx, const igm_split* m, int s,
                         const int64_t* v_in, const int64_t* basis, int k,
                         int frac_bits, int dot_b1, int dot_b2, int axpy_b1,
                         int64_t* w, int64_t* h_out);
+
+/* One fused MGS pass of the config-5 / multi-GPU path on DEVICE pointers,
+ * enqueued on the context stream and NOT synchronised (the distributed
+ * driver all-reduces *acc_out between passes):
+ *   mode 0: *acc_out += sum_l wrap(asr(w_l, dot_b1) * asr(vcur_l, dot_b2))
+ *   mode 1: w -= asr(wrap(h * vprev), f - axpy_b1) elementwise with
+ *           h = asr(fx_dot finalisation of *hacc, axpy_b1), then mode 0
+ *   mode 3: the axpy of mode 1 only
+ * (fxp.cpp:49-67, 88-104).  acc_out must be zeroed by the caller; the sum is
+ * the wrapping u64 accumulator, so partial sums of row blocks add exactly. */
+igm_status igm_mgs_pass(igm_ctx* ctx, int64_t n, int mode, int64_t* w, const int64_t* vprev,
+                        const int64_t* vcur, const uint64_t* hacc, uint64_t* acc_out, int f,
+                        int dot_b1, int dot_b2, int axpy_b1);
 
 /* ---- host setup (not on the GPU hot path; inputs of the calls above) ---- */
 /* replaces intgmres::row_scale (split.cpp:61-79) */

@@ -531,6 +531,15 @@ def spmv_mgs(m: SplitMatrix, s: int, v_in, basis, k: int, f: int, dot_b1: int, d
     return h
 
 
+def mgs_pass(dev: "Device", mode: int, w, vprev, vcur, hacc, acc_out, f: int, dot_b1: int, dot_b2: int,
+             axpy_b1: int) -> None:
+    """One fused MGS pass on device tensors, enqueued on dev's stream (no sync):
+    mode 0 dot, 1 axpy(vprev, h from hacc) + dot, 3 axpy only (igm_mgs_pass)."""
+    p = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None
+    _check(lib().igm_mgs_pass(dev.h, int(w.numel()), mode, p(w), p(vprev), p(vcur), p(hacc), p(acc_out), f,
+                              dot_b1, dot_b2, axpy_b1))
+
+
 # ---------------------------------------------------------------- host setup
 def row_scale(row_ptr, col_idx, vals, alpha_a: int):
     row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int32)

@@ -1197,4 +1197,21 @@ igm_status igm_spmv_mgs(igm_ctx* c, const igm_split* m, int s, const int64_t* v_
   });
 }
 
+igm_status igm_mgs_pass(igm_ctx* c, int64_t n, int mode, int64_t* w, const int64_t* vprev,
+                        const int64_t* vcur, const uint64_t* hacc, uint64_t* acc_out, int f, int dot_b1,
+                        int dot_b2, int axpy_b1) {
+  return guarded([&] {
+    need_ctx(c);
+    if (mode != 0 && mode != 1 && mode != 3) fail(IGM_INVALID_ARGUMENT, "mgs_pass: mode must be 0, 1 or 3");
+    if (n < 0) fail(IGM_INVALID_ARGUMENT, "mgs_pass: negative length");
+    if (n == 0) return;
+    if (!is_device_ptr(w) || (mode != 3 && (!is_device_ptr(vcur) || !is_device_ptr(acc_out))) ||
+        (mode != 0 && (!is_device_ptr(vprev) || !is_device_ptr(hacc))))
+      fail(IGM_INVALID_ARGUMENT, "mgs_pass: vectors and accumulators must be device memory");
+    ShiftsD sh{dot_b1, dot_b2, axpy_b1, 0, 0, 0, 0, 0};
+    launch_mgs_pass(c->stream, n, mode, w, vprev, vcur, hacc, acc_out, nullptr, f, sh, nullptr, nullptr, nullptr,
+                    false);  // no Ctl: a free-standing pass never ends early
+  });
+}
+
 }  // extern "C"

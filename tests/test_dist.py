@@ -1,0 +1,114 @@
+"""Row-block (z-slab) sharding of the config-5 kernel:
+partition / halo exchange / exact u64 allreduce over gloo with world_size 2
+(CPU), against the single-process oracle.  The GPU parity of the same driver
+at world_size 1 through the CUDA backend is in test_gpu_parity."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2009_07495_b200 import dist as D
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_plane_split_and_slab_csr():
+    assert D.plane_split(10, 4) == [(0, 3), (3, 6), (6, 8), (8, 10)]
+    with pytest.raises(ValueError):
+        D.plane_split(2, 3)
+    from workloads import gen
+    g = 6
+    rp, ci, v = gen.upwind_3d(g, 20.0)
+    for world in (1, 2, 3):
+        rows = []
+        for r in range(world):
+            sl = D.make_slab(g, g * g, r, world)
+            lrp, lci, (lv,) = D.slab_csr(rp, ci, [v], sl)
+            assert len(lrp) == sl.next_ + 1 and lrp[sl.own0] == 0
+            for i in range(sl.own0, sl.own1):  # every own row maps back to the global row
+                gi = sl.h0 + i
+                a, b = rp[gi], rp[gi + 1]
+                assert np.array_equal(lci[lrp[i]:lrp[i + 1]] + sl.h0, ci[a:b])
+                assert np.array_equal(lv[lrp[i]:lrp[i + 1]], v[a:b])
+            rows.append(sl.global_rows)
+        assert rows[0][0] == 0 and rows[-1][1] == g ** 3
+        assert all(rows[i][1] == rows[i + 1][0] for i in range(world - 1))
+    # the generator's slab form is the same local matrix
+    for world in (2, 3):
+        for r in range(world):
+            sl = D.make_slab(g, g * g, r, world)
+            a = D.slab_csr(rp, ci, [v], sl)
+            b = gen.upwind_3d_slab(g, 20.0, sl.z0, sl.z1)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[2][0], b[2])
+            assert (b[3], b[4], b[5]) == (sl.h0, sl.own0, sl.own1)
+
+
+def _worker(rank, world, port, g, k, seed, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from tests.dist_np import NumpySlabBackend
+        from workloads import gen
+        import paper_2009_07495_b200 as igm
+        rp, ci, v = gen.upwind_3d(g, 20.0)
+        vals, _ = igm.row_scale(rp, ci, v, 16)
+        comp, al, _ = igm.build_split(vals, 16, 2)
+        n = len(rp) - 1
+        sl = D.make_slab(g, g * g, rank, world)
+        lrp, lci, lcomp = D.slab_csr(rp, ci, comp, sl)
+        be = NumpySlabBackend()
+        m = be.upload(lrp, lci, lcomp, al)
+        rng = np.random.default_rng(seed)
+        vfull = rng.integers(-(1 << 40), 1 << 40, n, dtype=np.int64)
+        bfull = rng.integers(-(1 << 40), 1 << 40, (k, n), dtype=np.int64)
+        g0, g1 = sl.global_rows
+        v_own = torch.from_numpy(vfull[g0:g1].copy())
+        b_own = torch.from_numpy(bfull[:, g0:g1].copy())
+        work = dict(vext=torch.zeros(sl.next_, dtype=torch.int64), wext=torch.zeros(sl.next_, dtype=torch.int64),
+                    acc=torch.zeros(k, dtype=torch.int64))
+        w, acc = D.spmv_mgs_sharded(be, sl, m, 1, v_own, b_own, k, 30, 16, 0, 16, dist, work)
+        parts = [None] * world
+        dist.all_gather_object(parts, (g0, w.numpy().copy()))
+        if rank == 0:
+            wg = np.concatenate([p[1] for p in sorted(parts, key=lambda t: t[0])])
+            q.put((wg, acc.numpy().copy(), vfull, bfull))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_spmv_mgs_matches_oracle(oracle, world):
+    """World-size 2/3 gloo run of dist.spmv_mgs_sharded == the single-process
+    reference sequence (spmv with a depth-1 split, then k x (fx_dot,
+    fx_axpy_sub)) on every word of w and every h_i."""
+    g, k, seed = 8, 5, 1234
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, g, k, seed, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    wg, acc, vfull, bfull = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from workloads import gen
+    import paper_2009_07495_b200 as igm
+    rp, ci, v = gen.upwind_3d(g, 20.0)
+    vals, _ = igm.row_scale(rp, ci, v, 16)
+    comp, al, _ = oracle.build_split(vals, 16, 2)
+    sp = oracle.split(rp, ci, comp, al)
+    w = oracle.spmv(sp, 1, vfull)
+    for i in range(k):
+        h = oracle.fx_dot(w, bfull[i], 30, 16, 0)
+        assert h == D.fx_dot_finalize(int(acc[i]), 30, 16, 0)
+        w = oracle.fx_axpy_sub(w, h, bfull[i], 30, 16)
+    assert np.array_equal(wg, w)

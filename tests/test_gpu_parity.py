@@ -427,3 +427,42 @@ def test_run_cycle_large_vs_oracle(gpu, oracle, precond, g):
         assert np.array_equal(r.x, o["x"])
         if checked:
             assert t1.total_overflows() == t2.total
+
+
+def test_sharded_driver_cuda_backend(gpu, oracle):
+    """dist.spmv_mgs_sharded through the CUDA slab backend (igm_spmv on the
+    extended local CSR + igm_mgs_pass) == the oracle's reference sequence.
+    Multi-rank partition / halo / allreduce logic: tests/test_dist.py (gloo)."""
+    import torch
+    import torch.distributed as tdist
+    from paper_2009_07495_b200 import dist as D
+    from workloads import gen
+    g, k = 20, 6
+    sl = D.make_slab(g, g * g, 0, 1)
+    rp, ci, v, h0, own0, own1 = gen.upwind_3d_slab(g, 20.0, sl.z0, sl.z1)
+    vals, _ = gpu.row_scale(rp, ci, v, 16)
+    comp, al, _ = gpu.build_split(vals, 16, 2)
+    dev = gpu.Device.default()
+    be = D.CudaSlabBackend(gpu, dev)
+    S = be.upload(rp, ci, comp, al)
+    n = g ** 3
+    rng = np.random.default_rng(9)
+    vfull = rng.integers(-(1 << 40), 1 << 40, n, dtype=np.int64)
+    bfull = rng.integers(-(1 << 40), 1 << 40, (k, n), dtype=np.int64)
+    work = dict(vext=torch.zeros(sl.next_, dtype=torch.int64, device="cuda"),
+                wext=torch.zeros(sl.next_, dtype=torch.int64, device="cuda"),
+                acc=torch.zeros(k, dtype=torch.int64, device="cuda"))
+    w, acc = D.spmv_mgs_sharded(be, sl, S, 1, torch.from_numpy(vfull).cuda(), torch.from_numpy(bfull).cuda(), k,
+                                30, 16, 0, 16, tdist, work)
+    torch.cuda.synchronize()
+    rpg, cig, vg = gen.upwind_3d(g, 20.0)
+    valsg, _ = gpu.row_scale(rpg, cig, vg, 16)
+    compg, alg, _ = oracle.build_split(valsg, 16, 2)
+    sp = oracle.split(rpg, cig, compg, alg)
+    wo = oracle.spmv(sp, 1, vfull)
+    accs = acc.cpu().numpy()
+    for i in range(k):
+        h = oracle.fx_dot(wo, bfull[i], 30, 16, 0)
+        assert h == D.fx_dot_finalize(int(accs[i]), 30, 16, 0)
+        wo = oracle.fx_axpy_sub(wo, h, bfull[i], 30, 16)
+    assert np.array_equal(w.cpu().numpy(), wo)

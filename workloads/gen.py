@@ -233,3 +233,46 @@ def device_uniform_int40(n: int, seed: int, offset: int, device="cuda"):
     z = (z ^ ((z >> 27) & ((1 << 37) - 1))) * m2
     z = z ^ ((z >> 31) & ((1 << 33) - 1))
     return ((z >> 23) & ((1 << 41) - 1)) - (1 << 40)
+
+
+def upwind_3d_slab(g: int, beta: float, z0: int, z1: int):
+    """Planes [z0, z1) of upwind_3d(g) as an extended-square local CSR for
+    row-block partitioning: the local index space is the
+    halo range of planes [max(0, z0-1), min(g, z1+1)); rows of the halo
+    planes are empty, rows of the own planes are upwind_3d's rows with
+    columns shifted into the local space.  Returns (row_ptr, col, val,
+    h0, own0, own1) with h0 = first global row of the local space and
+    [own0, own1) the own rows in local indices."""
+    zh0, zh1 = max(0, z0 - 1), min(g, z1 + 1)
+    p = g * g
+    h0 = zh0 * p
+    nl = (zh1 - zh0) * p
+    own0, own1 = (z0 - zh0) * p, (z1 - zh0) * p
+    h = 1.0 / (g + 1)
+    d = 6.0 / h ** 2 + 3 * beta / h
+    lo, hi = -1.0 / h ** 2 - beta / h, -1.0 / h ** 2
+    r = np.arange(z0 * p, z1 * p, dtype=np.int64)  # own global rows
+    i = (r % g).astype(np.int32)
+    j = ((r // g) % g).astype(np.int32)
+    k = (r // p).astype(np.int32)
+    offs = [(k > 0, -p, lo), (j > 0, -g, lo), (i > 0, -1, lo), (None, 0, d),
+            (i < g - 1, 1, hi), (j < g - 1, g, hi), (k < g - 1, p, hi)]
+    no = len(r)
+    counts = np.full(no, 1, dtype=np.int32)
+    for m, _, _ in offs:
+        if m is not None:
+            counts += m
+    row_ptr = np.zeros(nl + 1, dtype=np.int64)
+    np.cumsum(counts, out=row_ptr[own0 + 1:own1 + 1])
+    row_ptr[own1 + 1:] = row_ptr[own1]
+    nnz = int(row_ptr[own1])
+    col = np.empty(nnz, dtype=np.int32)
+    val = np.empty(nnz, dtype=np.float64)
+    cur = row_ptr[own0:own1].copy()
+    for m, off, c in offs:
+        idx = np.arange(no, dtype=np.int64) if m is None else np.nonzero(m)[0]
+        pos = cur[idx]
+        col[pos] = (r[idx] + off - h0).astype(np.int32)
+        val[pos] = c
+        cur[idx] += 1
+    return row_ptr.astype(np.int32), col, val, h0, own0, own1
