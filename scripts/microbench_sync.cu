@@ -130,6 +130,27 @@ __global__ void overlap(const ulonglong2* w, int iters, u64* out) {
   }
 }
 
+// cost of a CTA barrier right after this warp issued a global store
+template <int MODE>
+__global__ void store_then_bar(ulonglong2* w, int iters, u64* out) {
+  u64 acc = 0;
+  u64 t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    ulonglong2* p = w + ((i * 97 + threadIdx.x * 131) & 65535) * 8;
+    if (MODE == 1) st128(p, acc, acc ^ 5);                                  // strong .gpu 128-bit
+    if (MODE == 2) *reinterpret_cast<u64*>(p) = acc;                         // weak 64-bit
+    if (MODE == 3) asm volatile("st.global.relaxed.gpu.b64 [%0], %1;" ::"l"(p), "l"(acc) : "memory");
+    if (MODE == 4) asm volatile("st.global.wt.b64 [%0], %1;" ::"l"(p), "l"(acc) : "memory");
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    acc = acc * 3 + i;
+  }
+  u64 t1 = clock64();
+  if (threadIdx.x == 0) {
+    out[0] = (t1 - t0) / iters;
+    out[1] = acc;
+  }
+}
+
 int main() {
   ulonglong2* w;
   u64* out;
@@ -166,6 +187,16 @@ int main() {
     if (m == 5) overlap<5><<<1, 32>>>(w, 2000, out);
     cudaDeviceSynchronize();
     printf("overlap: loads consumed next iteration, op=%-18s %llu cycles/iter\n", on[m], out[0]);
+  }
+  const char* sn[] = {"no store", "st.relaxed.gpu.b128", "weak st.b64", "st.relaxed.gpu.b64", "st.wt.b64"};
+  for (int m = 0; m < 5; ++m) {
+    if (m == 0) store_then_bar<0><<<1, 256>>>(w, 2000, out);
+    if (m == 1) store_then_bar<1><<<1, 256>>>(w, 2000, out);
+    if (m == 2) store_then_bar<2><<<1, 256>>>(w, 2000, out);
+    if (m == 3) store_then_bar<3><<<1, 256>>>(w, 2000, out);
+    if (m == 4) store_then_bar<4><<<1, 256>>>(w, 2000, out);
+    cudaDeviceSynchronize();
+    printf("store then bar.sync(256): %-22s %llu cycles/iter\n", sn[m], out[0]);
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
