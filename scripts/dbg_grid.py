@@ -35,3 +35,6 @@ for rep in range(3):
     got = igm.apply_inverse(F, y)
     bad = np.nonzero(got != want)[0]
     print("rep", rep, "mismatches", len(bad), "first", bad[:10], flush=True)
+    if len(bad) and os.environ.get("SHOW"):
+        for r in bad[:4]:
+            print("   row", r, "got", int(got[r]), "want", int(want[r]), "diff", int(got[r]) - int(want[r]))

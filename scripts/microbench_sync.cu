@@ -151,6 +151,35 @@ __global__ void store_then_bar(ulonglong2* w, int iters, u64* out) {
   }
 }
 
+// weak-load consumer: CTA 0 publishes (value_i, tag_i = e ^ value_i) for a
+// stream of rows, CTA 1 polls them with .cg loads and checks every accepted
+// value against the expected one
+__device__ __forceinline__ void ld128_cg(const ulonglong2* p, u64& v, u64& t) {
+  asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(v), "=l"(t) : "l"(p) : "memory");
+}
+__global__ void weak_consumer(ulonglong2* w, int rows, u64 e, u64* out) {
+  const int lane = threadIdx.x;
+  if (blockIdx.x == 0) {
+    for (int r = lane; r < rows; r += 32) {
+      const u64 v = 0x1234567ull * (r + 1) + e;
+      st128(w + r, v, e ^ v);
+      for (int z = 0; z < 50; ++z) asm volatile("nanosleep.u32 20;");
+    }
+  } else {
+    u64 bad = 0, polls = 0;
+    for (int r = lane; r < rows; r += 32) {
+      u64 v, t;
+      do {
+        ld128_cg(w + r, v, t);
+        ++polls;
+      } while (t != (e ^ v));
+      if (v != 0x1234567ull * (r + 1) + e) ++bad;
+    }
+    atomicAdd(out, bad);
+    atomicAdd(out + 1, polls);
+  }
+}
+
 int main() {
   ulonglong2* w;
   u64* out;
@@ -187,6 +216,13 @@ int main() {
     if (m == 5) overlap<5><<<1, 32>>>(w, 2000, out);
     cudaDeviceSynchronize();
     printf("overlap: loads consumed next iteration, op=%-18s %llu cycles/iter\n", on[m], out[0]);
+  }
+  for (int rep = 0; rep < 3; ++rep) {
+    out[0] = out[1] = 0;
+    weak_consumer<<<2, 32>>>(w, 4096, 0x9E3779B97F4A7C15ull * (rep + 1) | 1, out);
+    cudaDeviceSynchronize();
+    printf("weak .cg consumer rep %d: wrong accepted %llu, polls %llu (%s)\n", rep, out[0], out[1],
+           cudaGetErrorString(cudaGetLastError()));
   }
   const char* sn[] = {"no store", "st.relaxed.gpu.b128", "weak st.b64", "st.relaxed.gpu.b64", "st.wt.b64"};
   for (int m = 0; m < 5; ++m) {

@@ -6,7 +6,13 @@ if os.environ.get('LIBNAME'):
     _capi.LIB_PATH = _capi._HERE / os.environ['LIBNAME']
 import paper_2009_07495_b200 as igm
 from workloads import gen
-rp, ci, v = gen.upwind_3d(128, 20.0)
+dims = tuple(int(x) for x in os.environ.get("DIMS", "128,128,128").split(","))
+if len(set(dims)) == 1:
+    rp, ci, v = gen.upwind_3d(dims[0], 20.0)
+else:
+    offs = [(0, 0, -1), (0, -1, 0), (-1, 0, 0), (0, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 1)]
+    coef = {0: -1.3, 1: -1.2, 2: -1.1, 3: 8.0, 4: -0.9, 5: -0.8, 6: -0.7}
+    rp, ci, v = gen._stencil_csr(dims, offs, lambda o, r: np.full(r.shape, coef[o]))
 vals, scale = igm.row_scale(rp, ci, v, 32)
 lo, up = igm.factorize_split_cast(rp, ci, vals)
 F = igm.IluFactors(lo, up)
@@ -17,7 +23,8 @@ z = igm.apply_inverse(F, y)
 buf = torch.zeros(2048 * 8, dtype=torch.int64, device="cuda")
 lib = igm.lib()
 names = ["poll0", "poll1", "c_presync", "c_postsync", "c_done", "pub_sync", "pub_done"]
-for tile in (0, 1, 9, 63, 127):
+tiles = [int(x) for x in os.environ.get("TILES", "0,1,9,63,127").split(",")]
+for tile in tiles:
     buf.zero_()
     lib.igm_debug_tri_trace(tile, C.c_void_p(buf.data_ptr()))
     z = igm.apply_inverse(F, y)
