@@ -390,6 +390,12 @@ void build_tri(igm_ctx* c, DevTri& t, int n, const int* rp, const int* ci, const
   t.xz = dalloc<ulonglong2>(static_cast<size_t>(std::max(n, 1)));
   ck(cudaMemsetAsync(t.xz, 0, sizeof(ulonglong2) * std::max(n, 1), st), "xz");
   t.yperm = dalloc<i64>(static_cast<size_t>(n) + 2);
+  t.stats = dalloc<u64>(2);
+  t.maxabs_l = 0;
+  for (const i64 v : S.c_val) {
+    const u64 a = v < 0 ? 0ull - static_cast<u64>(v) : static_cast<u64>(v);
+    t.maxabs_l = std::max(t.maxabs_l, a);
+  }
   t.prog = dalloc<int>(S.ntiles);
   t.ticket = dalloc<int>(1);
   ck(cudaStreamSynchronize(st), "upload_ilu sync");
@@ -405,7 +411,7 @@ void free_tri(DevTri& t) {
                   static_cast<void*>(t.p_diag), static_cast<void*>(t.p_rec), static_cast<void*>(t.xz),
                   static_cast<void*>(t.seg_xptr), static_cast<void*>(t.seg_xrow), static_cast<void*>(t.c_rp),
                   static_cast<void*>(t.c_ci), static_cast<void*>(t.c_val), static_cast<void*>(t.c_diag),
-                  static_cast<void*>(t.prog), static_cast<void*>(t.yperm),
+                  static_cast<void*>(t.prog), static_cast<void*>(t.yperm), static_cast<void*>(t.stats),
                   static_cast<void*>(t.ticket)})
     dfree(p);
   t = DevTri{};

@@ -91,6 +91,8 @@ struct DevTri {
   int rec_bytes = 0;
   ulonglong2* xz = nullptr;        // n tagged exported values (128-bit each)
   void* yperm = nullptr;           // n+2 right-hand-side values in schedule order (8 bytes each)
+  u64* stats = nullptr;            // [max|y|, max|z|] of the current integer apply (device)
+  u64 maxabs_l = 0;                // max |factor value| of the stripped factor (host)
   int *seg_xptr = nullptr, *seg_xrow = nullptr;
   int max_seg_ext = 0;
   int *c_rp = nullptr, *c_ci = nullptr;

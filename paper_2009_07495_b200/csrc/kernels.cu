@@ -113,6 +113,13 @@ __device__ __forceinline__ void bump(u64* cnt, int op, u64 v) {
   if (v) atomicAdd(reinterpret_cast<unsigned long long*>(cnt + op), static_cast<unsigned long long>(v));
 }
 
+// one thread per element (latency-bound per-row kernels: every row's chain
+// of dependent loads in flight at once)
+inline int grid_full(long long n, int nt) {
+  const long long g = (n + nt - 1) / nt;
+  return static_cast<int>(g < 1 ? 1 : (g > 0x7fffffffLL ? 0x7fffffffLL : g));
+}
+
 inline int grid_for(long long n, int nt, int device = 0) {
   long long g = (n + nt - 1) / nt;
   const long long cap = static_cast<long long>(num_sms(device)) * 8;
@@ -1558,6 +1565,7 @@ struct TriArgs {
   const i64* p_xval;
   const unsigned char* p_rec;  // packed per-slot records (schedule.hpp)
   int tile_cap, max_seg_ext;
+  u64* zmax;                   // max |z| of the integer apply (checked mode's overflow bound)
   ulonglong2* xz;              // exported values: (value, epoch ^ value) per row
   unsigned long long epoch;    // per launch: hashed, non-zero
   int* ticket;
@@ -1651,17 +1659,39 @@ __device__ __forceinline__ void lds128l(unsigned a, i64& x, i64& y) {
 // division per entry, as refine.cpp:17 forms b_k = r / gamma) -- one coalesced
 // streaming pass that turns the wavefront's per-level right-hand-side
 // gathers into one contiguous bulk copy
+__device__ __forceinline__ u64 abs_u64(i64 v) { return v < 0 ? 0ull - static_cast<u64>(v) : static_cast<u64>(v); }
+
+__device__ __forceinline__ void warp_max_to(u64 m, u64* dst) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, static_cast<u64>(__shfl_down_sync(0xffffffffu, m, o)));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(reinterpret_cast<unsigned long long*>(dst), static_cast<unsigned long long>(m));
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_tri_gather(int n, const int* __restrict__ p_row,
                                                     const T* __restrict__ y, T* __restrict__ yperm,
-                                                    const Ctl* ctl, const double* prescale) {
+                                                    const Ctl* ctl, const double* prescale, u64* ymax) {
   if (cycle_over(ctl)) return;
+  u64 m = 0;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {  // grid is capped
     T v = y[__ldg(p_row + p)];
     if constexpr (std::is_same<T, double>::value) {
       if (prescale != nullptr) v = __ddiv_rn(v, __longlong_as_double(*reinterpret_cast<const long long*>(prescale)));
+    } else {
+      m = max(m, abs_u64(v));
     }
     yperm[p] = v;
+  }
+  if (ymax != nullptr) {  // block max, then one atomic per block (a single hot word)
+    __shared__ u64 sm[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, static_cast<u64>(__shfl_down_sync(0xffffffffu, m, o)));
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) m = max(m, sm[w]);
+      if (m) atomicMax(reinterpret_cast<unsigned long long*>(ymax), static_cast<unsigned long long>(m));
+    }
   }
 }
 
@@ -1831,6 +1861,8 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
     for (int d = 0; d < MAXD; ++d)
       if (r.ci[d] < 0) xz_load(a.xz + ~r.ci[d], r.wv[d], r.wt[d]);
   };
+  u64 zmx = 0;   // max |z| of this thread's rows (integer path)
+  i64 zlast = 0;
   // one level: barrier, the row, release the level's ring slot
   auto level = [&](int q, const Rec& cur) {
     if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 2] = gtime();
@@ -1838,6 +1870,7 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
     if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 3] = gtime();
 #ifndef IGM_TRI_SKELETON
     if (cur.have) {
+      if constexpr (!FP) zmx = max(zmx, abs_u64(zlast));
       i64 zb[MAXD];
 #pragma unroll
       for (int d = 0; d < MAXD; ++d) {
@@ -1891,8 +1924,12 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
 #endif
       }
       i64 zbits;
-      if constexpr (FP) zbits = __double_as_longlong(z);
-      else zbits = z;
+      if constexpr (FP) {
+        zbits = __double_as_longlong(z);
+      } else {
+        zbits = z;
+        zlast = z;  // folded into zmx off the critical path (next level)
+      }
       sts64(cur.zaddr, zbits);
 #ifndef IGM_TRI_NOSTORE
       out[cur.row] = z;
@@ -1922,6 +1959,7 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
       level(q, R[0]);
     }
   }
+  if constexpr (!FP) warp_max_to(max(zmx, abs_u64(zlast)), a.zmax);
 }
 
 
@@ -1936,8 +1974,19 @@ __global__ void __launch_bounds__(256) k_tri_count(int n, const int* __restrict_
                                                    const i64* __restrict__ diag,
                                                    const i64* __restrict__ y,
                                                    const i64* __restrict__ z, u64* cnt,
-                                                   const Ctl* ctl) {
+                                                   const Ctl* ctl, const u64* stats, double maxl, int maxd) {
+  __shared__ int s_skip;
   if (cycle_over(ctl)) return;
+  // every partial sum of every row is bounded by max|y| + maxd * max|l| * max|z|:
+  // below 2^63 no product, subtraction or INT64_MIN / -1 can overflow, so the
+  // exact count is zero (the bound is taken in FP64 with a factor-2 margin)
+  if (threadIdx.x == 0) {
+    const double b = __dadd_rn(static_cast<double>(stats[0]),
+                               static_cast<double>(maxd) * maxl * static_cast<double>(stats[1]));
+    s_skip = b < 4611686018427387904.0;  // 2^62
+  }
+  __syncthreads();
+  if (s_skip) return;
   u64 nmul = 0, nsub = 0, ndiv = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     i64 acc = y[i];
@@ -1970,6 +2019,7 @@ TriArgs tri_args(const DevTri& t) {
   a.tile_cap = t.tile_cap;
   a.max_seg_ext = t.max_seg_ext;
   a.xz = t.xz;
+  a.zmax = t.stats + 1;
   a.epoch = 0;
   a.ticket = t.ticket;
   return a;
@@ -2243,7 +2293,8 @@ static void tri_launch_one(cudaStream_t st, const DevTri& t, const T* y, T* out,
     args.epoch = (z ^ (z >> 31)) | 1ull;
   }
   // right-hand side into schedule order (and the FP path's 1/gamma prescale)
-  k_tri_gather<T><<<grid_for(t.n, 256), 256, 0, st>>>(t.n, t.p_row, y, static_cast<T*>(t.yperm), ctl, prescale);
+  k_tri_gather<T><<<grid_full(t.n, 256), 256, 0, st>>>(t.n, t.p_row, y, static_cast<T*>(t.yperm), ctl, prescale,
+                                                       std::is_same<T, double>::value ? nullptr : t.stats);
   k_tri<T, B, D><<<t.ntiles, kTriThreads, sm, st>>>(args, static_cast<const T*>(t.yperm), out, ctl, seg_cap, L);
 }
 
@@ -2264,6 +2315,7 @@ void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* 
                     u64* cnt, const Ctl* ctl, bool checked) {
   if (t.n == 0) return;
   cudaMemsetAsync(t.ticket, 0, sizeof(int), st);
+  if (checked) cudaMemsetAsync(t.stats, 0, 2 * sizeof(u64), st);
   {
     ProfScope prof_(st, KC_TRI_INT);
     if (backward) tri_dispatch<i64, true>(st, t, y, out, ctl, nullptr);
@@ -2272,7 +2324,8 @@ void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* 
   LAUNCH_CHECK();
   if (checked) {
     ProfScope prof_(st, KC_OTHER);
-    k_tri_count<<<grid_for(t.n, 256), 256, 0, st>>>(t.n, t.c_rp, t.c_ci, t.c_val, t.c_diag, y, out, cnt, ctl);
+    k_tri_count<<<grid_full(t.n, 256), 256, 0, st>>>(t.n, t.c_rp, t.c_ci, t.c_val, t.c_diag, y, out, cnt, ctl,
+                                                      t.stats, static_cast<double>(t.maxabs_l), t.maxd);
     LAUNCH_CHECK();
   }
 }
