@@ -117,3 +117,22 @@ def test_wavefront_schedule_unstructured(igm):
     for fac, upper in ((lo, False), (up, True)):
         rc, info = _schedule(igm, fac, upper)
         assert rc == 0 and info[4] == 0  # contiguous tiles
+
+
+def build_cpp_dropin(tmp_dir):
+    """Compile tests/cpp/dropin_solve.cpp against include/ and the product .so."""
+    import subprocess
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    lib = root / "paper_2009_07495_b200"
+    exe = Path(tmp_dir) / "dropin_solve"
+    cmd = ["g++", "-std=c++20", "-O1", f"-I{root / 'include'}", str(root / "tests/cpp/dropin_solve.cpp"),
+           f"-L{lib}", "-ligm_b200", f"-Wl,-rpath,{lib}", "-o", str(exe)]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return exe
+
+
+def test_cpp_dropin_builds(product_lib, tmp_path):
+    """The reference's C++ API (include/intgmres/*.hpp) compiles and links
+    against libigm_b200.so alone (running it needs a GPU: test_gpu_parity)."""
+    assert build_cpp_dropin(tmp_path).exists()

@@ -466,3 +466,39 @@ def test_sharded_driver_cuda_backend(gpu, oracle):
         assert h == D.fx_dot_finalize(int(accs[i]), 30, 16, 0)
         wo = oracle.fx_axpy_sub(wo, h, bfull[i], 30, 16)
     assert np.array_equal(w.cpu().numpy(), wo)
+
+
+def test_cpp_dropin_solve(gpu, oracle, tmp_path):
+    """A C++ program written against the reference's API (intgmres::solve,
+    row_scale, build_split, factorize_ilu0 / split_cast; tests/cpp) and linked
+    to libigm_b200.so: its x and report match the oracle bit for bit."""
+    import subprocess
+    from tests.test_capi import build_cpp_dropin
+    from workloads import gen
+    from tests.cases import PRE, UNPRE
+    exe = build_cpp_dropin(tmp_path)
+    out = subprocess.run([str(exe), "32"], check=True, capture_output=True, text=True, timeout=300).stdout
+    got = {}
+    for line in out.splitlines():
+        tag, key, *vals = line.split()
+        got.setdefault(tag, {})[key] = vals
+    rp, ci, v = gen.upwind_2d(32)
+    n = len(rp) - 1
+    xs = (np.arange(n) % 7) * 0.25 - 0.75
+    bh = gen.spmv_np(rp, ci, v, xs)
+    for tag, alpha, plan, pre in (("plain", 16, UNPRE, False), ("ilu", 32, PRE, True)):
+        A = oracle.csrf(rp, ci, v)
+        vals, scale = oracle.row_scale(A, alpha)
+        af = oracle.csrf(rp, ci, vals)
+        comp, al, _ = oracle.build_split(vals, alpha, 1)
+        sp = oracle.split(rp, ci, comp, al)
+        il = None
+        if pre:
+            lo, up = oracle.factorize_split_cast(af)
+            il = oracle.ilu(lo, up)
+        x, rep = oracle.solve(sp, af, bh / scale, 1e-10, 60, 30, 30, 0, Shifts(*plan), checked=True, precond=il)
+        g = got[tag]
+        assert int(g["refinements"][0]) == rep["refinements"] and int(g["refinements"][2]) == rep["total_inner_iterations"]
+        assert int(g["refinements"][4]) == rep["overflow_total"] and int(g["refinements"][6]) == int(rep["converged"])
+        assert [float.fromhex(t) for t in g["relres"]] == rep["relres_history"]
+        assert np.array_equal(np.array([float.fromhex(t) for t in g["x"]]), x)
