@@ -506,6 +506,7 @@ def run_b200(args, ws, rank, local):
                                    f"GMRES(30), FP64 refinement to 1e-10, Q33.30, checked",
                        "refinements": rep.refinements, "iterations_per_solve": rep.total_inner_iterations,
                        "final_relres": rep.relres_history[-1], "overflows": rep.overflow_total,
+                       "overflow_count_exact": rep.overflow_exact,
                        "l2": "inputs larger than L2 (matrix + ILU + basis ~ 0.9 GB)",
                        "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
             "gpu_launches": int(launches),

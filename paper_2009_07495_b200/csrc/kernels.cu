@@ -1202,11 +1202,16 @@ __device__ __forceinline__ u64 ld_cg_u64(const u64* p) {
 // ...and thread 0 fetches the one word the next pass needs (a reduced
 // accumulator) and broadcasts it through shared memory: one L2 request per
 // CTA instead of one per warp on a single hot line
-__device__ __forceinline__ u64 grid_barrier(Ctl* ctl, unsigned target, const u64* fetch, u64* s_word) {
+// pre: an optional [pre, pre + pre_bytes) range (this CTA's slice of the next
+// pass's basis vector) prefetched into L2 while the barrier is pending
+__device__ __forceinline__ u64 grid_barrier(Ctl* ctl, unsigned target, const u64* fetch, u64* s_word,
+                                            const void* pre = nullptr, unsigned pre_bytes = 0) {
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned* p = &ctl->gbar;
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+    if (pre_bytes)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pre), "r"(pre_bytes) : "memory");
     unsigned v;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -1356,8 +1361,9 @@ __global__ void __launch_bounds__(kArnThreads, 1)
     return asr(h, sh.axpy_b1);
   };
   for (int i = 1; i <= j; ++i) {
-    const i64 hs = h_of(grid_barrier(ctl, (++nbar) * G, accj + i - 1, &s_word));
     const i64* vi = basis + static_cast<long long>(i) * n + lo;
+    const i64 hs = h_of(grid_barrier(ctl, (++nbar) * G, accj + i - 1, &s_word, vi,
+                                     static_cast<unsigned>(cnt * 8) & ~15u));
     ArnAcc A;
     arn_rows(cnt, [&](long long r, int k) {
       i64 wq[4], pq[4], cq[4];

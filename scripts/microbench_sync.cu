@@ -180,7 +180,45 @@ __global__ void weak_consumer(ulonglong2* w, int rows, u64 e, u64* out) {
   }
 }
 
-int main() {
+// wavefront-like iteration: 3 loads issued per thread, consumed two
+// iterations later; some shared-memory work and a CTA barrier per iteration
+template <int STRONG>
+__global__ void pipelined_loads(const ulonglong2* w, int iters, u64* out) {
+  __shared__ u64 sh[256];
+  u64 V[2][3], T[2][3];
+  u64 acc = threadIdx.x;
+  auto issue = [&](int it, int b) {
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const ulonglong2* p = w + (((it * 3 + d) * 389 + threadIdx.x * 131 + blockIdx.x * 7919) & 65535) * 8;
+      if (STRONG) ld128(p, V[b][d], T[b][d]);
+      else asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(V[b][d]), "=l"(T[b][d]) : "l"(p) : "memory");
+    }
+  };
+  issue(0, 0);
+  issue(1, 1);
+  u64 t0 = clock64();
+  for (int it = 0; it < iters; it += 2) {
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      u64 s = 0;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) s += V[b][d] ^ T[b][d];
+      acc = acc * 3 + s;
+      sh[threadIdx.x] = acc;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      acc += sh[(threadIdx.x + 1) & 255];
+      issue(it + b + 2, b);
+    }
+  }
+  u64 t1 = clock64();
+  if (threadIdx.x == 0) {
+    out[0] = (t1 - t0) / iters;
+    out[1] = acc;
+  }
+}
+
+int main(int argc, char** argv) {
   ulonglong2* w;
   u64* out;
   cudaMalloc(&w, sizeof(ulonglong2) * 65536 * 8);
@@ -217,12 +255,21 @@ int main() {
     cudaDeviceSynchronize();
     printf("overlap: loads consumed next iteration, op=%-18s %llu cycles/iter\n", on[m], out[0]);
   }
-  for (int rep = 0; rep < 3; ++rep) {
+  for (int rep = 0; rep < (argc > 1 && argv[1][0] == 'w' ? 3 : 0); ++rep) {  // "w": hangs on B200
     out[0] = out[1] = 0;
     weak_consumer<<<2, 32>>>(w, 4096, 0x9E3779B97F4A7C15ull * (rep + 1) | 1, out);
     cudaDeviceSynchronize();
     printf("weak .cg consumer rep %d: wrong accepted %llu, polls %llu (%s)\n", rep, out[0], out[1],
            cudaGetErrorString(cudaGetLastError()));
+  }
+  for (int grid : {1, 148}) {
+    pipelined_loads<1><<<grid, 256>>>(w, 4000, out);
+    cudaDeviceSynchronize();
+    const u64 a = out[0];
+    pipelined_loads<0><<<grid, 256>>>(w, 4000, out);
+    cudaDeviceSynchronize();
+    printf("pipelined loads (3/thread, used 2 iterations later) grid %d: strong %llu, weak %llu cycles/iter\n", grid,
+           a, out[0]);
   }
   const char* sn[] = {"no store", "st.relaxed.gpu.b128", "weak st.b64", "st.relaxed.gpu.b64", "st.wt.b64"};
   for (int m = 0; m < 5; ++m) {
