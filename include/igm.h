@@ -200,6 +200,8 @@ typedef struct {
   const int* s_schedule;         /* NULL or max_refinements entries */
   igm_schedule_fn s_schedule_fn; /* NULL or callback, wins over the array */
   void* s_schedule_user;
+  int engine; /* 0 = Engine::fixed_point, 1 = Engine::floating_point (refine.hpp:22):
+                 FP64 GMRES(m) on reconstruct_fp(m, s) (refsolve.cpp:9-105) */
 } igm_refine_cfg;
 
 /* SolveReport (refine.hpp:36-47); arrays sized max_refinements (+1). */

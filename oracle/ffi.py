@@ -319,7 +319,7 @@ class _Backend:
                     g=bufs["g"], cos_raw=bufs["cos_raw"], sin_raw=bufs["sin_raw"], n_basis=out.n_basis)
 
     def solve(self, sp, a, b, tol, max_ref, m, f, s, shifts, checked=True, precond=None, s_schedule=None,
-              trace=None):
+              trace=None, engine=0):
         R = max(max_ref, 0)
         dims = np.zeros(R + 1, np.int32); rel = np.zeros(R + 2); gam = np.zeros(R + 1)
         ovf = np.zeros(R + 1, np.uint64)
@@ -329,9 +329,15 @@ class _Backend:
         rep = Report(0, 0, 0, _p(dims, i32p), _p(rel, f64p), 0, _p(gam, f64p), _p(ovf, u64p), 0, 0.0)
         x = np.zeros(sp.n)
         b = np.ascontiguousarray(b, np.float64)
-        self._rc(self.fn("solve")(C.byref(sp), C.byref(a), _p(b, f64p), C.byref(cfg),
-                                  C.pointer(precond) if precond is not None else None, _p(x, f64p), C.byref(rep),
-                                  C.byref(trace.c) if trace else None))
+        args = (C.byref(sp), C.byref(a), _p(b, f64p), C.byref(cfg),
+                C.pointer(precond) if precond is not None else None, _p(x, f64p), C.byref(rep),
+                C.byref(trace.c) if trace else None)
+        if engine:  # the FP64 comparator engine exists only in the reference library
+            fn = self.fn("solve_engine")
+            fn.argtypes = None
+            self._rc(fn(*args, C.c_int(engine)))
+        else:
+            self._rc(self.fn("solve")(*args))
         k = rep.refinements
         return x, dict(converged=bool(rep.converged), refinements=k,
                        total_inner_iterations=int(rep.total_inner_iterations),

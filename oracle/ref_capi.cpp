@@ -374,9 +374,20 @@ int ref_run_cycle(const ora_split* m, const ora_cycle_cfg* cfg, const double* b,
   return rc;
 }
 
+int ref_solve_engine(const ora_split* m, const ora_csrf* a_fp, const double* b,
+                     const ora_refine_cfg* cfg, const ora_ilu* precond, double* x_out,
+                     ora_report* rep, ora_trace* ext, int engine);
+
 int ref_solve(const ora_split* m, const ora_csrf* a_fp, const double* b,
               const ora_refine_cfg* cfg, const ora_ilu* precond, double* x_out,
               ora_report* rep, ora_trace* ext) {
+  return ref_solve_engine(m, a_fp, b, cfg, precond, x_out, rep, ext, 0);
+}
+
+// engine: 0 = Engine::fixed_point, 1 = Engine::floating_point (refine.hpp:22)
+int ref_solve_engine(const ora_split* m, const ora_csrf* a_fp, const double* b,
+                     const ora_refine_cfg* cfg, const ora_ilu* precond, double* x_out,
+                     ora_report* rep, ora_trace* ext, int engine) {
   TraceBridge tb(ext);
   IluFactors ilu;
   if (precond) ilu = to_ilu(precond);
@@ -391,6 +402,7 @@ int ref_solve(const ora_split* m, const ora_csrf* a_fp, const double* b,
     rc2.shifts = to_plan(cfg->shifts);
     rc2.s = cfg->s;
     rc2.checked = cfg->checked != 0;
+    rc2.engine = engine ? Engine::floating_point : Engine::fixed_point;
     if (cfg->s_schedule) {
       const int* sched = cfg->s_schedule;
       rc2.s_schedule = [sched](int k) { return sched[k]; };

@@ -469,6 +469,7 @@ class RefineConfig:
     s: int = 0
     checked: bool = True
     s_schedule: Optional[Callable[[int], int]] = None
+    engine: int = 0  # 0 fixed_point, 1 floating_point (refine.hpp:22; refsolve.cpp)
 
 
 @dataclass
@@ -498,7 +499,7 @@ def solve(m: SplitMatrix, a_fp: CsrMatrixF, b, cfg: RefineConfig, precond: Optio
     rep.gamma_history = gam.ctypes.data_as(_capi.f64p)
     rep.overflow_per_restart = ovf.ctypes.data_as(_capi.u64p)
     rc = _capi.RefineCfg(cfg.tol, cfg.max_refinements, cfg.m, cfg.frac_bits, cfg.s,
-                         1 if cfg.checked else 0, cfg.shifts.c(), None, _capi.SCHED_FN(), None)
+                         1 if cfg.checked else 0, cfg.shifts.c(), None, _capi.SCHED_FN(), None, cfg.engine)
     cb = None
     if cfg.s_schedule is not None:
         fn = cfg.s_schedule

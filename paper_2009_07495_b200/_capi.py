@@ -74,7 +74,7 @@ class RefineCfg(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_refinements", C.c_int), ("m", C.c_int),
                 ("frac_bits", C.c_int), ("s", C.c_int), ("checked", C.c_int),
                 ("shifts", Shifts), ("s_schedule", i32p), ("s_schedule_fn", SCHED_FN),
-                ("s_schedule_user", C.c_void_p)]
+                ("s_schedule_user", C.c_void_p), ("engine", C.c_int)]
 
 
 class Report(C.Structure):

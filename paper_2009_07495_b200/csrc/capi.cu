@@ -10,6 +10,7 @@
 #include "schedule.hpp"
 
 #include <algorithm>
+#include <cfloat>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -146,6 +147,11 @@ struct igm_ctx {
   u64* h_red = nullptr;
   void* n2s = nullptr;  // norm2 per-block scratch (norm2_scratch_bytes)
   size_t n2s_bytes = 0;
+  // FP64 engine: reconstructed operator values (reconstruct_fp) + scalars
+  double* fp_vals = nullptr;
+  size_t fp_vals_n = 0;
+  double* fp_sc = nullptr;  // [r0n, wnorm_pre, h_0..h_m, hnext] + fdot partials + weights
+  size_t fp_sc_n = 0;
 };
 
 // norm2 scratch for vectors of length n (grown on demand; stream-ordered use)
@@ -620,6 +626,8 @@ void igm_ctx_destroy(igm_ctx* c) {
   dfree(c->ctl);
   dfree(c->red);
   dfree(c->n2s);
+  dfree(c->fp_vals);
+  dfree(c->fp_sc);
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
   if (c->h_red) cudaFreeHost(c->h_red);
   cudaStreamDestroy(c->stream);
@@ -1076,6 +1084,100 @@ igm_status igm_run_cycle(igm_ctx* c, const igm_split* m, const igm_cycle_cfg* cf
 }
 
 // ---- solve
+// Engine::floating_point cycle (refsolve.cpp:9-105) on the reconstructed
+// operator, from x0 = 0 with b = r / gamma (refine.cpp:79-81); adds
+// gamma * correction to ws.x (refine.cpp:87).  SpMV, preconditioner,
+// norms, scaling and the x update are the reference's operation order
+// (bit-exact); the MGS dots are deterministic tree reductions.  Givens
+// rotations and the back substitution run on the host exactly as in
+// refsolve.cpp.  Returns the Krylov dimension.
+static int fp_cycle_solve(igm_ctx* c, const DevCsrf& A, int M, double gamma, const igm_ilu* pre) {
+  Work& w = c->ws;
+  cudaStream_t st = c->stream;
+  const long long n = A.n;
+  const size_t need = static_cast<size_t>(M) + 8 + fdot_blocks() + static_cast<size_t>(M) + 2;
+  if (c->fp_sc_n < need) {
+    ck(cudaStreamSynchronize(st), "fp scratch");
+    dfree(c->fp_sc);
+    c->fp_sc = dalloc<double>(need);
+    c->fp_sc_n = need;
+  }
+  double* sc = c->fp_sc;                   // [0] r0n, [1] wnorm_pre, [2..] h_0..h_j, hnext
+  double* part = sc + M + 6;               // fdot partials
+  double* wts = part + fdot_blocks();      // x-update weights
+  double* V = reinterpret_cast<double*>(w.basis);  // (m+1) x n doubles (same bytes as the int basis)
+  Ctl* ctl = c->ctl;
+  // b = r / gamma, then the preconditioner (fp_precond = apply_inverse_fp, refine.cpp:47-50)
+  if (pre) {
+    const double* gbits = reinterpret_cast<const double*>(&ctl->rmax_bits);
+    launch_tri_fp(st, pre->lower, false, w.r, w.t1, ctl, gbits);
+    launch_tri_fp(st, pre->upper, true, w.t1, w.r0, ctl, nullptr);
+  } else {
+    launch_scale_div(st, n, w.r, w.r0, ctl);
+  }
+  launch_norm2_serial(st, n, w.r0, sc, ctl, 0, n2_scratch(c, n));
+  double r0n = 0.0;
+  ck(cudaMemcpyAsync(&r0n, sc, sizeof(double), cudaMemcpyDeviceToHost, st), "r0n");
+  ck(cudaStreamSynchronize(st), "sync");
+  if (r0n == 0.0) return 0;
+  launch_fscale(st, n, w.r0, V, sc);
+  const int ld = M + 1;
+  std::vector<double> hess(static_cast<size_t>(ld) * M, 0.0), g(ld, 0.0), cs(M, 0.0), sn(M, 0.0);
+  std::vector<double> hbuf(M + 4);
+  g[0] = 1.0;
+  int dim = 0;
+  for (int j = 0; j < M; ++j) {
+    double* col = &hess[static_cast<size_t>(j) * ld];
+    const double* vj = V + static_cast<long long>(j) * n;
+    launch_residual(st, A, vj, nullptr, w.t1, ctl, false);  // w = A v_j
+    if (pre) {
+      launch_tri_fp(st, pre->lower, false, w.t1, w.r, ctl, nullptr);
+      launch_tri_fp(st, pre->upper, true, w.r, w.t1, ctl, nullptr);
+    }
+    launch_norm2_serial(st, n, w.t1, sc + 1, ctl, 0, n2_scratch(c, n));  // wnorm_pre
+    for (int i = 0; i <= j; ++i)
+      launch_fdot_axpy(st, n, w.t1, V + static_cast<long long>(i) * n, part, sc + 2 + i);
+    launch_norm2_serial(st, n, w.t1, sc + 3 + j, ctl, 0, n2_scratch(c, n));  // hnext
+    ck(cudaMemcpyAsync(hbuf.data(), sc + 1, sizeof(double) * (j + 3), cudaMemcpyDeviceToHost, st), "h");
+    ck(cudaStreamSynchronize(st), "sync");
+    const double wnorm_pre = hbuf[0];
+    for (int i = 0; i <= j; ++i) col[i] = hbuf[1 + i];
+    const double hnext = hbuf[2 + j];
+    col[j + 1] = hnext;
+    const bool happy = hnext <= wnorm_pre * (8.0 * DBL_EPSILON);
+    if (!happy) launch_fscale(st, n, w.t1, V + static_cast<long long>(j + 1) * n, sc + 3 + j);
+    for (int i = 0; i < j; ++i) {
+      const double hi = col[i], hn = col[i + 1];
+      col[i] = cs[i] * hi + sn[i] * hn;
+      col[i + 1] = cs[i] * hn - sn[i] * hi;
+    }
+    const double t = std::hypot(col[j], col[j + 1]);
+    if (t == 0.0) break;
+    cs[j] = col[j] / t;
+    sn[j] = col[j + 1] / t;
+    col[j] = t;
+    col[j + 1] = 0.0;
+    const double g_old = g[j];
+    g[j + 1] = -sn[j] * g_old;
+    g[j] = cs[j] * g_old;
+    dim = j + 1;
+    if (happy) break;
+  }
+  if (dim > 0) {
+    std::vector<double> y(dim), wt(dim);
+    for (int i = dim - 1; i >= 0; --i) {
+      double acc = g[i];
+      for (int jj = i + 1; jj < dim; ++jj) acc -= hess[static_cast<size_t>(jj) * ld + i] * y[jj];
+      y[i] = acc / hess[static_cast<size_t>(i) * ld + i];
+    }
+    for (int jj = 0; jj < dim; ++jj) wt[jj] = r0n * y[jj];
+    ck(cudaMemcpyAsync(wts, wt.data(), sizeof(double) * dim, cudaMemcpyHostToDevice, st), "wts");
+    launch_fxupdate(st, n, dim, V, wts, gamma, w.x);
+    ck(cudaStreamSynchronize(st), "sync");  // wt (host) is read by the copy above
+  }
+  return dim;
+}
+
 igm_status igm_solve(igm_ctx* c, const igm_split* m, const igm_csrf* a_fp, const double* b,
                      const igm_refine_cfg* cfg, const igm_ilu* precond, double* x_out,
                      igm_report* rep, igm_trace* ext) {
@@ -1112,6 +1214,7 @@ igm_status igm_solve(igm_ctx* c, const igm_split* m, const igm_csrf* a_fp, const
     ck(cudaStreamSynchronize(st), "sync");
     double relnorm = c->h_ctl->relnorm;
     rep->relres_history[rep->n_relres++] = relnorm;
+    int fp_depth = -1;  // FP engine: depth the reconstructed operator was built for
 
     for (int k = 0; k < cfg->max_refinements && relnorm >= cfg->tol; ++k) {
       const u64 rbits = c->h_ctl->rmax_bits;
@@ -1123,6 +1226,44 @@ igm_status igm_solve(igm_ctx* c, const igm_split* m, const igm_csrf* a_fp, const
       const int depth = cfg->s_schedule_fn ? cfg->s_schedule_fn(cfg->s_schedule_user, k)
                         : cfg->s_schedule  ? cfg->s_schedule[k]
                                            : cfg->s;
+      if (cfg->engine == 1) {  // Engine::floating_point (refine.cpp:74-82)
+        if (depth < 0 || depth > m->ncomp - 1)
+          fail(IGM_INVALID_ARGUMENT, "reconstruct_fp: component index out of range");
+        if (cfg->m < 1) fail(IGM_INVALID_ARGUMENT, "fp_cycle: m must be >= 1");
+        if (depth != fp_depth) {  // operator rebuilt lazily when the depth changes
+          if (c->fp_vals_n < static_cast<size_t>(std::max(m->nnz, 1))) {
+            ck(cudaStreamSynchronize(st), "fp vals");
+            dfree(c->fp_vals);
+            c->fp_vals = dalloc<double>(std::max(m->nnz, 1));
+            c->fp_vals_n = static_cast<size_t>(std::max(m->nnz, 1));
+          }
+          launch_recon_vals(st, *m, depth, c->fp_vals);
+          fp_depth = depth;
+        }
+        DevCsrf Ar;
+        Ar.n = m->n;
+        Ar.nnz = m->nnz;
+        Ar.row_ptr = m->row_ptr;
+        Ar.col_idx = m->col_idx;
+        Ar.vals = c->fp_vals;
+        Ar.device = m->device;
+        const int dim = fp_cycle_solve(c, Ar, cfg->m, rmax, precond);
+        raise_device_error(c);
+        if (dim == 0) break;
+        ck(cudaMemsetAsync(&c->ctl->rmax_bits, 0, sizeof(u64), st), "rmax reset");
+        launch_residual(st, *a_fp, w.x, db.d, w.r, c->ctl, true);
+        launch_norm2_serial(st, n, w.r, nullptr, c->ctl, 2, n2_scratch(c, n));
+        ck(cudaMemcpyAsync(c->h_ctl, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st), "ctl");
+        ck(cudaStreamSynchronize(st), "sync");
+        rep->refinements = k + 1;
+        rep->total_inner_iterations += dim;
+        rep->inner_dims[k] = dim;
+        rep->gamma_history[k] = rmax;
+        rep->overflow_per_restart[k] = t->total - before;
+        relnorm = c->h_ctl->relnorm;
+        rep->relres_history[rep->n_relres++] = relnorm;
+        continue;
+      }
       // run_cycle validation (gmres_int.cpp:47-52)
       if (cfg->m < 1) fail(IGM_INVALID_ARGUMENT, "run_cycle: m must be >= 1");
       if (depth < 0 || depth > m->ncomp - 1) fail(IGM_INVALID_ARGUMENT, "run_cycle: splitting depth out of range");

@@ -169,6 +169,13 @@ void launch_fx_red(cudaStream_t st, long long n, int mode, const i64* v,
 void launch_axpy_only(cudaStream_t st, long long n, i64* w, i64 h,
                       const i64* v, int f, int b1, u64* cnt, bool checked);
 void launch_gamma(cudaStream_t st, long long n, const double* r, Ctl* ctl);
+// FP64 engine pieces (refsolve.cpp)
+void launch_recon_vals(cudaStream_t st, const DevSplit& m, int s, double* out);
+void launch_fdot_axpy(cudaStream_t st, long long n, double* w, const double* v, double* part, double* h);
+void launch_fscale(cudaStream_t st, long long n, const double* w, double* out, const double* d);
+void launch_fxupdate(cudaStream_t st, long long n, int dim, const double* basis, const double* wts, double gamma,
+                     double* x);
+int fdot_blocks();
 // persistent Arnoldi step (passes + scalar + vec_div in one cooperative launch)
 long long arnoldi_slice(long long n, int device);
 int arnoldi_barriers(int j);

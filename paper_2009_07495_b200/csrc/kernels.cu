@@ -2034,6 +2034,78 @@ TriArgs tri_args(const DevTri& t) {
 }  // namespace
 
 // ---------------------------------------------------------------------------
+// FP64 engine (Engine::floating_point: refine.cpp:47-86, refsolve.cpp:9-105)
+// reconstruct_fp (split.cpp:177-191): vals[k] = sum_l ldexp(double(c_l[k]), -alpha_l), from 0.0
+__global__ void k_recon_vals(long long nnz, int s, const i64* __restrict__ vals, const int* __restrict__ alphas,
+                             double* __restrict__ out) {
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < nnz;
+       k += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double acc = 0.0;
+    for (int l = 0; l <= s; ++l) acc = __dadd_rn(acc, ldexp(__ll2double_rn(vals[l * nnz + k]), -alphas[l]));
+    out[k] = acc;
+  }
+}
+
+// MGS dot h = sum_l w_l v_l in a fixed tree order (deterministic; the
+// reference's sequential sum has no cheap exact parallel form for mixed
+// signs -- SURVEY.md §8(f) row 2 compares this engine by iteration counts)
+constexpr int kFdotBlocks = 592;
+__global__ void __launch_bounds__(256) k_fdot_partial(long long n, const double* __restrict__ w,
+                                                      const double* __restrict__ v, double* part) {
+  __shared__ double sh[8];
+  double acc = 0.0;
+  for (long long l = blockIdx.x * 256LL + threadIdx.x; l < n; l += static_cast<long long>(gridDim.x) * 256)
+    acc = __dadd_rn(acc, __dmul_rn(w[l], v[l]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < 8; ++i) t = __dadd_rn(t, sh[i]);
+    part[blockIdx.x] = t;
+  }
+}
+__global__ void __launch_bounds__(256) k_fdot_final(int nb, const double* __restrict__ part, double* h) {
+  __shared__ double sh[8];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < nb; i += 256) acc = __dadd_rn(acc, part[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < 8; ++i) t = __dadd_rn(t, sh[i]);
+    *h = t;
+  }
+}
+// w -= h v (refsolve.cpp:58, no contraction)
+__global__ void k_faxpy(long long n, double* __restrict__ w, const double* __restrict__ v, const double* h) {
+  const double hv = *h;
+  for (long long l = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; l < n;
+       l += static_cast<long long>(gridDim.x) * blockDim.x)
+    w[l] = __dsub_rn(w[l], __dmul_rn(hv, v[l]));
+}
+// out = w / *d (refsolve.cpp:37, 69)
+__global__ void k_fscale(long long n, const double* __restrict__ w, double* __restrict__ out, const double* d) {
+  const double dv = *d;
+  for (long long l = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; l < n;
+       l += static_cast<long long>(gridDim.x) * blockDim.x)
+    out[l] = __ddiv_rn(w[l], dv);
+}
+// x += gamma * (0.0 + sum_j wts_j v_j), j in order (refsolve.cpp:95-100, refine.cpp:87)
+__global__ void k_fxupdate(long long n, int dim, const double* __restrict__ basis, const double* __restrict__ wts,
+                           double gamma, double* __restrict__ x) {
+  for (long long l = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; l < n;
+       l += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < dim; ++j) acc = __dadd_rn(acc, __dmul_rn(wts[j], basis[static_cast<long long>(j) * n + l]));
+    x[l] = __dadd_rn(x[l], __dmul_rn(gamma, acc));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // launchers
 
 #define LAUNCH_CHECK() ++g_launches
@@ -2245,6 +2317,33 @@ void launch_arnoldi(cudaStream_t st, long long n, int j, long long S, const i64*
   cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kArnThreads), args, smem, st);
   LAUNCH_CHECK();
 }
+
+void launch_recon_vals(cudaStream_t st, const DevSplit& m, int s, double* out) {
+  ProfScope prof_(st, KC_OTHER);
+  k_recon_vals<<<grid_for(m.nnz, 256), 256, 0, st>>>(m.nnz, s, m.vals, m.alphas, out);
+  LAUNCH_CHECK();
+}
+void launch_fdot_axpy(cudaStream_t st, long long n, double* w, const double* v, double* part, double* h) {
+  ProfScope prof_(st, KC_MGS);
+  k_fdot_partial<<<kFdotBlocks, 256, 0, st>>>(n, w, v, part);
+  k_fdot_final<<<1, 256, 0, st>>>(kFdotBlocks, part, h);
+  k_faxpy<<<grid_for(n, 256), 256, 0, st>>>(n, w, v, h);
+  LAUNCH_CHECK();
+  LAUNCH_CHECK();
+  LAUNCH_CHECK();
+}
+void launch_fscale(cudaStream_t st, long long n, const double* w, double* out, const double* d) {
+  ProfScope prof_(st, KC_VEC_DIV);
+  k_fscale<<<grid_for(n, 256), 256, 0, st>>>(n, w, out, d);
+  LAUNCH_CHECK();
+}
+void launch_fxupdate(cudaStream_t st, long long n, int dim, const double* basis, const double* wts, double gamma,
+                     double* x) {
+  ProfScope prof_(st, KC_XUPDATE);
+  k_fxupdate<<<grid_for(n, 256), 256, 0, st>>>(n, dim, basis, wts, gamma, x);
+  LAUNCH_CHECK();
+}
+int fdot_blocks() { return kFdotBlocks; }
 
 void launch_cycle_init(cudaStream_t st, Ctl* ctl, i64* g, int f) {
   ProfScope prof_(st, KC_OTHER);

@@ -688,8 +688,6 @@ SolveResult solve(const SplitMatrix& m, const CsrMatrixF& a_fp, const std::vecto
   const int n = m.n;
   if (a_fp.n != n || static_cast<int>(b.size()) != n) throw std::invalid_argument("solve: dimension mismatch");
   if (cfg.max_refinements < 0) throw std::invalid_argument("solve: max_refinements must be >= 0");
-  if (cfg.engine != Engine::fixed_point)
-    throw std::logic_error("solve: the floating_point engine is not part of the B200 build");
   const auto t0 = std::chrono::steady_clock::now();
   FxTrace own(cfg.checked, false);
   FxTrace* trace = external_trace ? external_trace : &own;
@@ -706,6 +704,7 @@ SolveResult solve(const SplitMatrix& m, const CsrMatrixF& a_fp, const std::vecto
   rc.s = cfg.s;
   rc.checked = cfg.checked ? 1 : 0;
   rc.shifts = to_c(cfg.shifts);
+  rc.engine = cfg.engine == Engine::floating_point ? 1 : 0;
   if (cfg.s_schedule) {
     rc.s_schedule_fn = &call_schedule;
     rc.s_schedule_user = const_cast<std::function<int(int)>*>(&cfg.s_schedule);
