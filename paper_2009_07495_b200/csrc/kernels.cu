@@ -1619,11 +1619,6 @@ __device__ __forceinline__ void mbar_arrive_s(unsigned bar) {
 __device__ __forceinline__ void mbar_arrive_expect_tx_s(unsigned bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
-// relaxed: no release, so the caller's in-flight global loads need not drain
-__device__ __forceinline__ void mbar_arrive_expect_tx_relaxed_s(unsigned bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-               : "memory");
-}
 __device__ __forceinline__ void mbar_wait_s(unsigned bar, unsigned parity) {
   asm volatile(
       "{\n"

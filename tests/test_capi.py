@@ -136,3 +136,18 @@ def test_cpp_dropin_builds(product_lib, tmp_path):
     """The reference's C++ API (include/intgmres/*.hpp) compiles and links
     against libigm_b200.so alone (running it needs a GPU: test_gpu_parity)."""
     assert build_cpp_dropin(tmp_path).exists()
+
+
+def test_cpp_matrix_market_io(product_lib, tmp_path):
+    """Matrix Market ingestion of the drop-in API (tests/cpp/mm_io_test.cpp):
+    the reference's accepted inputs and diagnostics, bit-exact round trip."""
+    import subprocess
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    lib = root / "paper_2009_07495_b200"
+    exe = tmp_path / "mm_io_test"
+    subprocess.run(["g++", "-std=c++20", "-O1", f"-I{root / 'include'}", str(root / "tests/cpp/mm_io_test.cpp"),
+                    f"-L{lib}", "-ligm_b200", f"-Wl,-rpath,{lib}", "-o", str(exe)], check=True,
+                   capture_output=True, text=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert out.stdout.strip() == "ok", out.stdout + out.stderr
