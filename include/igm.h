@@ -224,6 +224,17 @@ igm_status igm_solve(igm_ctx* ctx, const igm_split* m, const igm_csrf* a_fp,
                      const igm_ilu* precond, double* x_out, igm_report* rep,
                      igm_trace* external_trace);
 
+/* replaces intgmres::fp_cycle (refsolve.hpp:26-29, refsolve.cpp:9-105): one
+ * FP64 GMRES(m) cycle from x0 on a, with an optional LEFT preconditioner
+ * given as a host callback (in/out host buffers of n doubles; returns 0 on
+ * success).  Outputs: x_out (n), dim, r0_norm (preconditioned), g_abs (m,
+ * may be NULL).  SpMV, norms, scalings and updates follow the reference's
+ * order; the MGS dots are deterministic tree reductions. */
+typedef int (*igm_fp_precond_fn)(void* user, int64_t n, const double* in, double* out);
+igm_status igm_fp_cycle(igm_ctx* ctx, const igm_csrf* a, int m, const double* b,
+                        const double* x0, igm_fp_precond_fn precond, void* user,
+                        double* x_out, int* dim, double* r0_norm, double* g_abs);
+
 /* ---- kernel microbench (BASELINE config 5) ------------------------------ */
 /* One call = w = spmv(m, s, v_in); then for i in 0..k-1:
  * h_i = fx_dot(w, basis_i, dot_b1, dot_b2); fx_axpy_sub(w, h_i, basis_i,

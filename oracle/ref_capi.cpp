@@ -428,3 +428,48 @@ int ref_solve_engine(const ora_split* m, const ora_csrf* a_fp, const double* b,
 }
 
 }  // extern "C"
+
+// ---- the reference's FP64 comparator (refsolve.cpp), for the device
+// implementation's tests: fp_cycle / solve_fp on a CsrMatrixF, optionally
+// preconditioned with apply_fp(factorize_ilu0(a)).
+#include "intgmres/refsolve.hpp"
+
+extern "C" {
+
+int ref_fp_cycle(const ora_csrf* a, int m, const double* b, const double* x0, int use_ilu, double* x_out,
+                 int* dim, double* r0_norm, double* g_abs) {
+  return guard([&] {
+    const CsrMatrixF af = to_csrf(a);
+    PrecondFn pf;
+    FpIluFactors f;
+    if (use_ilu) {
+      f = factorize_ilu0(af);
+      pf = [&f](const std::vector<double>& y) { return apply_fp(f, y); };
+    }
+    const FpCycleResult r = fp_cycle(af, m, std::vector<double>(b, b + a->n), std::vector<double>(x0, x0 + a->n), pf);
+    std::memcpy(x_out, r.x.data(), sizeof(double) * static_cast<std::size_t>(a->n));
+    *dim = r.dim;
+    *r0_norm = r.r0_norm;
+    for (std::size_t i = 0; i < r.g_abs.size(); ++i) g_abs[i] = r.g_abs[i];
+  });
+}
+
+int ref_solve_fp(const ora_csrf* a, const double* b, int m, double tol, int max_restarts, int use_ilu,
+                 double* x_out, int* restarts, long* iterations, int* converged) {
+  return guard([&] {
+    const CsrMatrixF af = to_csrf(a);
+    FpGmresConfig cfg;
+    cfg.m = m;
+    cfg.tol = tol;
+    cfg.max_restarts = max_restarts;
+    FpIluFactors f;
+    if (use_ilu) f = factorize_ilu0(af);
+    const FpSolveResult r = solve_fp(af, std::vector<double>(b, b + a->n), cfg, use_ilu ? &f : nullptr);
+    std::memcpy(x_out, r.x.data(), sizeof(double) * static_cast<std::size_t>(a->n));
+    *restarts = r.restarts;
+    *iterations = r.iterations;
+    *converged = r.converged;
+  });
+}
+
+}  // extern "C"

@@ -132,6 +132,8 @@ SIGNATURES = [
                             C.c_void_p, C.c_void_p, C.POINTER(Report), C.POINTER(Trace)]),
     ("igm_spmv_mgs", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
                                C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, i64p]),
+    ("igm_fp_cycle", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                               C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_double), C.c_void_p]),
     ("igm_mgs_pass", C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]),
     ("igm_row_scale", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,

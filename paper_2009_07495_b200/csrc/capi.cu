@@ -1084,14 +1084,40 @@ igm_status igm_run_cycle(igm_ctx* c, const igm_split* m, const igm_cycle_cfg* cf
 }
 
 // ---- solve
-// Engine::floating_point cycle (refsolve.cpp:9-105) on the reconstructed
-// operator, from x0 = 0 with b = r / gamma (refine.cpp:79-81); adds
-// gamma * correction to ws.x (refine.cpp:87).  SpMV, preconditioner,
-// norms, scaling and the x update are the reference's operation order
-// (bit-exact); the MGS dots are deterministic tree reductions.  Givens
-// rotations and the back substitution run on the host exactly as in
-// refsolve.cpp.  Returns the Krylov dimension.
-static int fp_cycle_solve(igm_ctx* c, const DevCsrf& A, int M, double gamma, const igm_ilu* pre) {
+// FP64 GMRES(m) cycle (refsolve.cpp:9-105).  On entry ws.r0 holds
+// b - A x0 (pre_r0: the preconditioner is still to be applied to it) or the
+// preconditioned r0.  SpMV, preconditioner (integer factors in FP64, or a
+// host callback), norms, scalings and the x update follow the reference's
+// operation order bit for bit; the MGS dots are deterministic tree
+// reductions.  Givens rotations and the back substitution run on the host
+// exactly as in refsolve.cpp.  x: mode 1 adds gamma * correction (the
+// refinement, refine.cpp:87), mode 0 accumulates onto x0 (fp_cycle).
+// Returns the Krylov dimension.
+struct FpPre {
+  const igm_ilu* ilu = nullptr;
+  igm_fp_precond_fn fn = nullptr;
+  void* user = nullptr;
+};
+
+static void fp_apply_pre(igm_ctx* c, const FpPre& P, long long n, const double* in, double* scratch, double* out) {
+  cudaStream_t st = c->stream;
+  if (P.ilu) {
+    launch_tri_fp(st, P.ilu->lower, false, in, scratch, c->ctl, nullptr);
+    launch_tri_fp(st, P.ilu->upper, true, scratch, out, c->ctl, nullptr);
+  } else if (P.fn) {
+    std::vector<double> hin(static_cast<size_t>(n)), hout(static_cast<size_t>(n));
+    ck(cudaMemcpyAsync(hin.data(), in, sizeof(double) * n, cudaMemcpyDeviceToHost, st), "precond D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+    if (P.fn(P.user, n, hin.data(), hout.data()) != 0) fail(IGM_RUNTIME_ERROR, "fp_cycle: preconditioner failed");
+    ck(cudaMemcpyAsync(out, hout.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st), "precond H2D");
+    ck(cudaStreamSynchronize(st), "sync");  // hout is read by the copy
+  } else if (out != in) {
+    ck(cudaMemcpyAsync(out, in, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "copy");
+  }
+}
+
+static int fp_cycle_core(igm_ctx* c, const DevCsrf& A, int M, const FpPre& P, bool pre_r0, double gamma,
+                         double* x, int xmode, double* r0n_out, std::vector<double>* gabs) {
   Work& w = c->ws;
   cudaStream_t st = c->stream;
   const long long n = A.n;
@@ -1107,18 +1133,12 @@ static int fp_cycle_solve(igm_ctx* c, const DevCsrf& A, int M, double gamma, con
   double* wts = part + fdot_blocks();      // x-update weights
   double* V = reinterpret_cast<double*>(w.basis);  // (m+1) x n doubles (same bytes as the int basis)
   Ctl* ctl = c->ctl;
-  // b = r / gamma, then the preconditioner (fp_precond = apply_inverse_fp, refine.cpp:47-50)
-  if (pre) {
-    const double* gbits = reinterpret_cast<const double*>(&ctl->rmax_bits);
-    launch_tri_fp(st, pre->lower, false, w.r, w.t1, ctl, gbits);
-    launch_tri_fp(st, pre->upper, true, w.t1, w.r0, ctl, nullptr);
-  } else {
-    launch_scale_div(st, n, w.r, w.r0, ctl);
-  }
+  if (pre_r0) fp_apply_pre(c, P, n, w.r0, w.t1, w.r0);
   launch_norm2_serial(st, n, w.r0, sc, ctl, 0, n2_scratch(c, n));
   double r0n = 0.0;
   ck(cudaMemcpyAsync(&r0n, sc, sizeof(double), cudaMemcpyDeviceToHost, st), "r0n");
   ck(cudaStreamSynchronize(st), "sync");
+  if (r0n_out) *r0n_out = r0n;
   if (r0n == 0.0) return 0;
   launch_fscale(st, n, w.r0, V, sc);
   const int ld = M + 1;
@@ -1130,10 +1150,7 @@ static int fp_cycle_solve(igm_ctx* c, const DevCsrf& A, int M, double gamma, con
     double* col = &hess[static_cast<size_t>(j) * ld];
     const double* vj = V + static_cast<long long>(j) * n;
     launch_residual(st, A, vj, nullptr, w.t1, ctl, false);  // w = A v_j
-    if (pre) {
-      launch_tri_fp(st, pre->lower, false, w.t1, w.r, ctl, nullptr);
-      launch_tri_fp(st, pre->upper, true, w.r, w.t1, ctl, nullptr);
-    }
+    fp_apply_pre(c, P, n, w.t1, w.r, w.t1);
     launch_norm2_serial(st, n, w.t1, sc + 1, ctl, 0, n2_scratch(c, n));  // wnorm_pre
     for (int i = 0; i <= j; ++i)
       launch_fdot_axpy(st, n, w.t1, V + static_cast<long long>(i) * n, part, sc + 2 + i);
@@ -1161,6 +1178,7 @@ static int fp_cycle_solve(igm_ctx* c, const DevCsrf& A, int M, double gamma, con
     g[j + 1] = -sn[j] * g_old;
     g[j] = cs[j] * g_old;
     dim = j + 1;
+    if (gabs) gabs->push_back(std::fabs(g[j + 1]));
     if (happy) break;
   }
   if (dim > 0) {
@@ -1172,10 +1190,25 @@ static int fp_cycle_solve(igm_ctx* c, const DevCsrf& A, int M, double gamma, con
     }
     for (int jj = 0; jj < dim; ++jj) wt[jj] = r0n * y[jj];
     ck(cudaMemcpyAsync(wts, wt.data(), sizeof(double) * dim, cudaMemcpyHostToDevice, st), "wts");
-    launch_fxupdate(st, n, dim, V, wts, gamma, w.x);
+    launch_fxupdate(st, n, dim, V, wts, gamma, x, xmode);
     ck(cudaStreamSynchronize(st), "sync");  // wt (host) is read by the copy above
   }
   return dim;
+}
+
+// the refinement's FP engine cycle: b = r / gamma, x0 = 0, x += gamma * correction
+static int fp_cycle_solve(igm_ctx* c, const DevCsrf& A, int M, double gamma, const igm_ilu* pre) {
+  Work& w = c->ws;
+  if (pre) {  // b / gamma fused into the preconditioner's gather
+    const double* gbits = reinterpret_cast<const double*>(&c->ctl->rmax_bits);
+    launch_tri_fp(c->stream, pre->lower, false, w.r, w.t1, c->ctl, gbits);
+    launch_tri_fp(c->stream, pre->upper, true, w.t1, w.r0, c->ctl, nullptr);
+  } else {
+    launch_scale_div(c->stream, A.n, w.r, w.r0, c->ctl);
+  }
+  FpPre P;
+  P.ilu = pre;
+  return fp_cycle_core(c, A, M, P, false, gamma, w.x, 1, nullptr, nullptr);
 }
 
 igm_status igm_solve(igm_ctx* c, const igm_split* m, const igm_csrf* a_fp, const double* b,
@@ -1341,6 +1374,39 @@ igm_status igm_spmv_mgs(igm_ctx* c, const igm_split* m, int s, const int64_t* v_
         h_out[i] = e >= 0 ? asr(a, e) : wrap_shl(a, -e);
       }
     }
+  });
+}
+
+igm_status igm_fp_cycle(igm_ctx* c, const igm_csrf* a, int m, const double* b, const double* x0,
+                        igm_fp_precond_fn precond, void* user, double* x_out, int* dim, double* r0_norm,
+                        double* g_abs) {
+  return guarded([&] {
+    need_ctx(c);
+    if (m < 1) fail(IGM_INVALID_ARGUMENT, "fp_cycle: m must be >= 1");
+    if (!a || !b || !x0 || !x_out) fail(IGM_INVALID_ARGUMENT, "fp_cycle: dimension mismatch");
+    const long long n = a->n;
+    ws_ensure(c, n, m);
+    Work& w = c->ws;
+    cudaStream_t st = c->stream;
+    reset_ctl(c);
+    In<double> db(b, n, st);
+    In<double> dx0(x0, n, st);
+    launch_residual(st, *a, dx0.d, db.d, w.r0, c->ctl, false);  // r0 = b - A x0
+    ck(cudaMemcpyAsync(w.x, dx0.d, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "x0");
+    FpPre P;
+    P.fn = precond;
+    P.user = user;
+    std::vector<double> gabs;
+    double r0n = 0.0;
+    const int d = fp_cycle_core(c, *a, m, P, true, 1.0, w.x, 0, &r0n, &gabs);
+    if (dim) *dim = d;
+    if (r0_norm) *r0_norm = r0n;
+    if (g_abs)
+      for (size_t i = 0; i < gabs.size(); ++i) g_abs[i] = gabs[i];
+    ck(cudaMemcpyAsync(x_out, w.x, sizeof(double) * n,
+                       is_device_ptr(x_out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st),
+       "x");
+    ck(cudaStreamSynchronize(st), "sync");
   });
 }
 

@@ -174,7 +174,7 @@ void launch_recon_vals(cudaStream_t st, const DevSplit& m, int s, double* out);
 void launch_fdot_axpy(cudaStream_t st, long long n, double* w, const double* v, double* part, double* h);
 void launch_fscale(cudaStream_t st, long long n, const double* w, double* out, const double* d);
 void launch_fxupdate(cudaStream_t st, long long n, int dim, const double* basis, const double* wts, double gamma,
-                     double* x);
+                     double* x, int mode);
 int fdot_blocks();
 // persistent Arnoldi step (passes + scalar + vec_div in one cooperative launch)
 long long arnoldi_slice(long long n, int device);

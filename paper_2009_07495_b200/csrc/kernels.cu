@@ -2090,13 +2090,15 @@ __global__ void k_fscale(long long n, const double* __restrict__ w, double* __re
     out[l] = __ddiv_rn(w[l], dv);
 }
 // x += gamma * (0.0 + sum_j wts_j v_j), j in order (refsolve.cpp:95-100, refine.cpp:87)
+// mode 1: x += gamma * (0.0 + sum_j wts_j v_j) (the refinement's correction);
+// mode 0: x = x0 + w_0 v_0 + w_1 v_1 + ... accumulated onto x0 (fp_cycle)
 __global__ void k_fxupdate(long long n, int dim, const double* __restrict__ basis, const double* __restrict__ wts,
-                           double gamma, double* __restrict__ x) {
+                           double gamma, double* __restrict__ x, int mode) {
   for (long long l = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; l < n;
        l += static_cast<long long>(gridDim.x) * blockDim.x) {
-    double acc = 0.0;
+    double acc = mode == 0 ? x[l] : 0.0;
     for (int j = 0; j < dim; ++j) acc = __dadd_rn(acc, __dmul_rn(wts[j], basis[static_cast<long long>(j) * n + l]));
-    x[l] = __dadd_rn(x[l], __dmul_rn(gamma, acc));
+    x[l] = mode == 0 ? acc : __dadd_rn(x[l], __dmul_rn(gamma, acc));
   }
 }
 
@@ -2333,9 +2335,9 @@ void launch_fscale(cudaStream_t st, long long n, const double* w, double* out, c
   LAUNCH_CHECK();
 }
 void launch_fxupdate(cudaStream_t st, long long n, int dim, const double* basis, const double* wts, double gamma,
-                     double* x) {
+                     double* x, int mode) {
   ProfScope prof_(st, KC_XUPDATE);
-  k_fxupdate<<<grid_for(n, 256), 256, 0, st>>>(n, dim, basis, wts, gamma, x);
+  k_fxupdate<<<grid_for(n, 256), 256, 0, st>>>(n, dim, basis, wts, gamma, x, mode);
   LAUNCH_CHECK();
 }
 int fdot_blocks() { return kFdotBlocks; }

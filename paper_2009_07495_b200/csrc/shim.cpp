@@ -851,3 +851,69 @@ extern "C" igm_status igm_build_split(int /*n*/, int nnz, const double* vals, in
   *ncomp_out = layers;
   return IGM_OK;
 }
+
+// ===========================================================================
+// refsolve (refsolve.hpp): the FP64 GMRES comparator on the device
+
+#include "intgmres/refsolve.hpp"
+
+namespace intgmres {
+namespace {
+int call_precond(void* user, int64_t n, const double* in, double* out) {
+  const PrecondFn& f = *static_cast<const PrecondFn*>(user);
+  const std::vector<double> r = f(std::vector<double>(in, in + n));
+  if (static_cast<int64_t>(r.size()) != n) return 1;
+  std::copy(r.begin(), r.end(), out);
+  return 0;
+}
+
+FpCycleResult fp_cycle_up(const CsrfUp& up, int n, int m, const std::vector<double>& b,
+                          const std::vector<double>& x0, const PrecondFn& precond) {
+  FpCycleResult res;
+  res.x.resize(static_cast<size_t>(n));
+  std::vector<double> gabs(static_cast<size_t>(std::max(m, 1)));
+  int dim = 0;
+  ok(igm_fp_cycle(ctx(), up.h, m, b.data(), x0.data(), precond ? &call_precond : nullptr,
+                  precond ? const_cast<PrecondFn*>(&precond) : nullptr, res.x.data(), &dim, &res.r0_norm,
+                  gabs.data()));
+  res.dim = dim;
+  res.g_abs.assign(gabs.begin(), gabs.begin() + dim);
+  return res;
+}
+}  // namespace
+
+FpCycleResult fp_cycle(const CsrMatrixF& a, int m, const std::vector<double>& b, const std::vector<double>& x0,
+                       const PrecondFn& precond) {
+  if (m < 1) throw std::invalid_argument("fp_cycle: m must be >= 1");
+  if (static_cast<int>(b.size()) != a.n || static_cast<int>(x0.size()) != a.n)
+    throw std::invalid_argument("fp_cycle: dimension mismatch");
+  CsrfUp up(a);
+  return fp_cycle_up(up, a.n, m, b, x0, precond);
+}
+
+FpSolveResult solve_fp(const CsrMatrixF& a, const std::vector<double>& b, const FpGmresConfig& cfg,
+                       const FpIluFactors* precond) {
+  PrecondFn pf;
+  if (precond) pf = [precond](const std::vector<double>& y) { return apply_fp(*precond, y); };
+  if (cfg.m < 1) throw std::invalid_argument("fp_cycle: m must be >= 1");
+  if (static_cast<int>(b.size()) != a.n) throw std::invalid_argument("fp_cycle: dimension mismatch");
+  CsrfUp up(a);
+  FpSolveResult res;
+  res.x.assign(static_cast<size_t>(a.n), 0.0);
+  double relres = residual_fp(a, res.x, b).relnorm;
+  res.relres_history.push_back(relres);
+  while (relres >= cfg.tol && res.restarts < cfg.max_restarts) {
+    const FpCycleResult cyc = fp_cycle_up(up, a.n, cfg.m, b, res.x, pf);
+    if (cyc.dim == 0) break;  // no progress possible
+    res.x = cyc.x;
+    res.restarts += 1;
+    res.iterations += cyc.dim;
+    res.cycle_dims.push_back(cyc.dim);
+    relres = residual_fp(a, res.x, b).relnorm;
+    res.relres_history.push_back(relres);
+  }
+  res.converged = relres < cfg.tol;
+  return res;
+}
+
+}  // namespace intgmres

@@ -524,3 +524,55 @@ def test_fp64_engine_vs_reference(gpu, oracle, reference, name):
     assert rep.relres_history[0] == rr["relres_history"][0]  # same residual kernel, same x = 0
     assert np.linalg.norm(x - xr) <= 1e-6 * np.linalg.norm(xr)
     assert rep.overflow_total == 0
+
+
+def test_cpp_refsolve(gpu, reference, tmp_path):
+    """fp_cycle / solve_fp of the drop-in API (device FP64 GMRES) against the
+    reference library's own: Krylov dimensions, r0 norm (bit-exact: same
+    residual, preconditioner and norm order), restarts within one and x to
+    solver accuracy (the MGS dots are tree reductions)."""
+    import ctypes as C
+    import subprocess
+    from pathlib import Path
+    from workloads import gen
+    root = Path(__file__).resolve().parents[1]
+    lib = root / "paper_2009_07495_b200"
+    exe = tmp_path / "refsolve_run"
+    subprocess.run(["g++", "-std=c++20", "-O1", f"-I{root / 'include'}", str(root / "tests/cpp/refsolve_run.cpp"),
+                    f"-L{lib}", "-ligm_b200", f"-Wl,-rpath,{lib}", "-o", str(exe)], check=True,
+                   capture_output=True, text=True)
+    out = subprocess.run([str(exe), "24"], check=True, capture_output=True, text=True, timeout=300).stdout
+    got = {}
+    for line in out.splitlines():
+        tok = line.split()
+        d = {}
+        k = 1
+        while k < len(tok):
+            if tok[k] == "x":
+                d["x"] = np.array([float.fromhex(v) for v in tok[k + 1:]])
+                break
+            d[tok[k]] = tok[k + 1]
+            k += 2
+        got[tok[0]] = d
+    rp, ci, v = gen.upwind_2d(24)
+    n = len(rp) - 1
+    A = reference.csrf(rp, ci, v)
+    xs = (np.arange(n) % 7) * 0.25 - 0.75
+    b = gen.spmv_np(rp, ci, v, xs)
+    x0 = (np.arange(n) % 5) * 0.125
+    lib_r = reference.lib
+    p = lambda a_: a_.ctypes.data_as(C.c_void_p)
+    for pre in (0, 1):
+        xr = np.zeros(n); dim = C.c_int(); r0 = C.c_double(); gab = np.zeros(20)
+        assert lib_r.ref_fp_cycle(C.byref(A), 20, p(b), p(x0), pre, p(xr), C.byref(dim), C.byref(r0), p(gab)) == 0
+        gc = got[f"cycle{pre}"]
+        assert int(gc["dim"]) == dim.value
+        assert float.fromhex(gc["r0"]) == r0.value
+        assert np.linalg.norm(gc["x"] - xr) <= 1e-9 * np.linalg.norm(xr)
+        xs_ = np.zeros(n); rs = C.c_int(); it = C.c_long(); cv = C.c_int()
+        assert lib_r.ref_solve_fp(C.byref(A), p(b), 20, C.c_double(1e-10), 100000, pre, p(xs_), C.byref(rs),
+                                  C.byref(it), C.byref(cv)) == 0
+        gs = got[f"solve{pre}"]
+        assert int(gs["conv"]) == 1 and cv.value == 1
+        assert abs(int(gs["restarts"]) - rs.value) <= 1
+        assert np.linalg.norm(gs["x"] - xs_) <= 1e-7 * np.linalg.norm(xs_)
