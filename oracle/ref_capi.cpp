@@ -473,3 +473,26 @@ int ref_solve_fp(const ora_csrf* a, const double* b, int m, double tol, int max_
 }
 
 }  // extern "C"
+
+// ---- the reference's experiment path (experiment.cpp), for the drop-in's test
+#include "intgmres/experiment.hpp"
+
+extern "C" {
+
+int ref_run_experiment(const char* path, int solver, int precond, int m, double tol, int max_ref, char* csv,
+                       int csv_cap, char* summary, int summary_cap) {
+  return guard([&] {
+    ExperimentSpec spec;
+    spec.matrix_path = path;
+    spec.solver = solver ? SolverKind::fp64 : SolverKind::integer;
+    spec.precond = precond ? PrecondKind::ilu0 : PrecondKind::none;
+    spec.m = m;
+    spec.tol = tol;
+    spec.max_refinements = max_ref;
+    const ExperimentResult r = run_experiment(spec);
+    std::snprintf(csv, static_cast<std::size_t>(csv_cap), "%s", r.csv.c_str());
+    std::snprintf(summary, static_cast<std::size_t>(summary_cap), "%s", r.summary.c_str());
+  });
+}
+
+}  // extern "C"

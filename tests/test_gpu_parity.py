@@ -576,3 +576,38 @@ def test_cpp_refsolve(gpu, reference, tmp_path):
         assert int(gs["conv"]) == 1 and cv.value == 1
         assert abs(int(gs["restarts"]) - rs.value) <= 1
         assert np.linalg.norm(gs["x"] - xs_) <= 1e-7 * np.linalg.norm(xs_)
+
+
+def test_cpp_experiment(gpu, reference, tmp_path):
+    """run_experiment of the drop-in API (Matrix Market in, CSV history and
+    summary out) vs the reference library's run_experiment on the same file:
+    byte-identical CSV and summary for the integer solver (bit-exact solve),
+    the same restarts (within one) for the FP64 comparator."""
+    import ctypes as C
+    import subprocess
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    lib = root / "paper_2009_07495_b200"
+    exe = tmp_path / "experiment_run"
+    subprocess.run(["g++", "-std=c++20", "-O1", f"-I{root / 'include'}", str(root / "tests/cpp/experiment_run.cpp"),
+                    f"-L{lib}", "-ligm_b200", f"-Wl,-rpath,{lib}", "-o", str(exe)], check=True,
+                   capture_output=True, text=True)
+    mtx = tmp_path / "upwind24.mtx"
+    out = subprocess.run([str(exe), str(mtx), "24"], check=True, capture_output=True, text=True, timeout=300).stdout
+    blocks = {}
+    for part in out.split("### ")[1:]:
+        head, body = part.split("\n", 1)
+        blocks[tuple(int(t) for t in head.split())] = body.rstrip("\n")
+    for (solver, pre), body in blocks.items():
+        csv = C.create_string_buffer(1 << 16)
+        summ = C.create_string_buffer(1024)
+        assert reference.lib.ref_run_experiment(str(mtx).encode(), solver, pre, 20, C.c_double(1e-10), 60, csv,
+                                                len(csv), summ, len(summ)) == 0
+        ref_text = csv.value.decode() + summ.value.decode()
+        if solver == 0:
+            assert body == ref_text
+        else:
+            ours = body.splitlines()
+            refl = ref_text.splitlines()
+            assert abs(len(ours) - len(refl)) <= 1 and ours[-1].split()[:4] == refl[-1].split()[:4]
+            assert ours[-1].endswith("converged=yes") and refl[-1].endswith("converged=yes")
