@@ -1698,10 +1698,6 @@ __global__ void __launch_bounds__(256) k_tri_gather(int n, const int* __restrict
 
 constexpr int kTriCompute = 256;
 constexpr int kTriThreads = kTriCompute + 32;  // + bulk-loader warp
-#ifndef IGM_TRI_LA
-#define IGM_TRI_LA 2
-#endif
-constexpr int kTriLA = IGM_TRI_LA;  // levels of record / cross-tile-word lookahead
 
 struct TriSmem {  // byte offsets of the dynamic shared-memory regions
   size_t rows, xptr, ring, bars, total;
@@ -1802,11 +1798,8 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
 
   // ---------------- compute warps
   // Each level's row record (dependency slots and factors, magic, rhs) is
-  // read from the ring kTriLA levels ahead into a register ring buffer, and
-  // its cross-tile words are loaded at the same time: a strong 128-bit L2
-  // load costs ~0.2-0.5 us, so a one-level lead would leave it on every
-  // level's critical path.  Buffers are indexed by level mod kTriLA with the
-  // loop unrolled by kTriLA, so no register copy waits on a load in flight.
+  // read from the ring into registers and its cross-tile words are loaded
+  // together with it.
   const int tid = threadIdx.x;
   const unsigned ring_end = ring_s + static_cast<unsigned>(L) * lay.ring_slot;
   const unsigned my_rec = static_cast<unsigned>(tid) * REC;
@@ -1819,7 +1812,7 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
     unsigned zaddr, bar;
     bool have;
   };
-  Rec R[kTriLA];
+  Rec R;
   unsigned f_slot = ring_s, f_bar = 0, f_ph = 0;  // ring position of the next level to fetch
   int s_f = seg_row(0);
   auto fetch = [&](int q, Rec& r) {
@@ -1877,7 +1870,7 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
       for (int d = 0; d < MAXD; ++d) {
         const int c = cur.ci[d];
         zb[d] = lds64(zt_s + 8u * static_cast<unsigned>(c < 0 ? 0 : c));
-        if (c < 0) {  // cross-tile: loaded kTriLA levels ago, re-polled only if not yet published
+        if (c < 0) {  // cross-tile word loaded with the record, re-polled only if not yet published
           const bool ok = cur.wt[d] == (a.epoch ^ cur.wv[d]);
 #ifdef IGM_TRI_TRACE
           if (tsb && q < 2048) {
@@ -1943,22 +1936,14 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
     if (lane == 0) mbar_arrive_s(empty_s + cur.bar);
     if (tsb && tid == 0 && q < 2048) tsb[q * 8 + 6] = gtime();
   };
-  if (L >= kTriLA + 1) {  // levels q .. q+LA hold ring slots at once
-#pragma unroll
-    for (int b = 0; b < kTriLA; ++b) fetch(b, R[b]);
-    for (int q0 = 0; q0 < nsg; q0 += kTriLA) {
-#pragma unroll
-      for (int b = 0; b < kTriLA; ++b) {  // unrolled: buffer b holds level q0 + b
-        if (q0 + b >= nsg) break;
-        level(q0 + b, R[b]);
-        fetch(q0 + b + kTriLA, R[b]);
-      }
-    }
-  } else {  // shallow ring (large strides): each level fetched once its slot is readable
-    for (int q = 0; q < nsg; ++q) {
-      fetch(q, R[0]);
-      level(q, R[0]);
-    }
+  // Each level's record is read (and its cross-tile loads issued) right
+  // before the level's barrier, so their latency overlaps the barrier wait.
+  // Measured faster than reading records one to four levels ahead into a
+  // register ring (fewer registers, half the code): 1.07 vs 1.16 us/level at
+  // 128^3, 0.67 vs 0.75 for a single brick.
+  for (int q = 0; q < nsg; ++q) {
+    fetch(q, R);
+    level(q, R);
   }
   if constexpr (!FP) warp_max_to(max(zmx, abs_u64(zlast)), a.zmax);
 }
