@@ -258,6 +258,80 @@ igm_status igm_mgs_pass(igm_ctx* ctx, int64_t n, int mode, int64_t* w, const int
                         const int64_t* vcur, const uint64_t* hacc, uint64_t* acc_out, int f,
                         int dot_b1, int dot_b2, int axpy_b1);
 
+/* ---- row-block (z-slab) partition: rank-local building blocks ----------
+ * SURVEY.md 8(e).  The distributed driver (paper_2009_07495_b200/dist.py:
+ * solve_sharded) owns the rank's vectors (device pointers) and the
+ * collectives (halo planes, exact u64 sums, the relayed norm2 chain, the
+ * ILU pipeline hand-offs); each entry below enqueues the same kernels as
+ * igm_solve / igm_run_cycle on the context stream and returns WITHOUT
+ * synchronising, so a whole cycle is enqueued with no host round trip.
+ * igm_dstate holds the replicated per-cycle scalars (Ctl, H, g, cos, sin)
+ * and the per-step reduction slots:
+ *   RED  step j: (m+2) slots x 3 u64 {wrapped accumulator, sum|t| hi, lo};
+ *        slot i <= j: MGS pass i (fx_dot, fxp.cpp:49-67), slot j+1: fx_norm
+ *        (fxp.cpp:69-86).  A pass's 3 words are summed over ranks (SUM of
+ *        u64 mod 2^64: exact in any order) before the next pass reads them.
+ *   LCNT step j: overflow counters of the rank-local kernels [K][OP]; summed
+ *        over ranks after the norm pass, before igm_dc_step reads it.
+ *   VCNT all steps: vec_div counters, summed once per cycle.
+ *   RMAX ctl's max|r| as IEEE bits (int64 MAX over ranks = gamma_scale's max).
+ *   CHAIN 4 doubles of scratch for the norm2 relay. */
+typedef struct igm_dstate igm_dstate;
+enum { IGM_DS_RED = 0, IGM_DS_LCNT = 1, IGM_DS_VCNT = 2, IGM_DS_RMAX = 3, IGM_DS_CHAIN = 4 };
+typedef struct {
+  int dim, stop, nbasis, add_inexact;
+  double r0_norm, relnorm, nb, nr, gamma;
+  uint64_t overflows; /* this cycle's events (all-reduced counters + scalar events) */
+} igm_dc_info;
+igm_status igm_dstate_create(igm_ctx* ctx, int m, igm_dstate** out);
+void igm_dstate_free(igm_dstate* d);
+igm_status igm_dstate_buffer(igm_dstate* d, int which, int j, void** ptr, int64_t* bytes);
+/* ctl := 0 (start of a solve) */
+igm_status igm_dc_reset(igm_ctx* ctx, igm_dstate* d);
+/* r = b - A x over the rank's rows (A: own rows x extended columns), max|r|
+ * into RMAX (residual_fp, split.cpp:51-59; gamma_scale, refine.cpp:11-19) */
+igm_status igm_dc_residual(igm_ctx* ctx, igm_dstate* d, const igm_csrf* a, const double* x_ext,
+                           const double* b, double* r);
+/* norm2 (split.cpp:45-49) continued from *start (device, NULL = 0.0) over n
+ * terms; mode 5: *out = running sum; 1: ||b|| (ctl.nb); 2: ||r|| and the
+ * relative norm; 3: ||r0|| (stops the cycle when 0) */
+igm_status igm_dc_norm2(igm_ctx* ctx, igm_dstate* d, int64_t n, const double* v, const double* start,
+                        double* out, int mode);
+/* zero the per-cycle state, g_0 = 2^f (gmres_int.cpp:83-89) */
+igm_status igm_dc_begin(igm_ctx* ctx, igm_dstate* d, int frac_bits);
+/* out = r / gamma (refine.cpp:17-18) */
+igm_status igm_dc_scale(igm_ctx* ctx, igm_dstate* d, int64_t n, const double* r, double* out);
+/* one FP64 / integer substitution of the (extended-local) factors
+ * (ilu.cpp:157-180 / 122-155) */
+igm_status igm_dc_tri_fp(igm_ctx* ctx, igm_dstate* d, const igm_ilu* f, int backward, const double* in,
+                         double* out);
+igm_status igm_dc_tri(igm_ctx* ctx, igm_dstate* d, const igm_ilu* f, int backward, const int64_t* in,
+                      int64_t* out, int j, int checked);
+/* v0 = encode(r0 / ||r0||) (gmres_int.cpp:71-81) */
+igm_status igm_dc_encode(igm_ctx* ctx, igm_dstate* d, int64_t n, const double* r0, int64_t* v0,
+                         int frac_bits);
+/* out = spmv(A, s, v) over the rank's rows (split.cpp:137-157) */
+igm_status igm_dc_spmv(igm_ctx* ctx, igm_dstate* d, const igm_split* m, int s, const int64_t* v_ext,
+                       int64_t* out, int j, int checked);
+/* MGS pass i of step j: i == 0 dot_0; 0 < i <= j axpy_{i-1} then dot_i;
+ * i == j+1 axpy_j then the norm sum (gmres_int.cpp:101-116) */
+igm_status igm_dc_mgs_pass(igm_ctx* ctx, igm_dstate* d, int64_t n, int j, int i, int64_t* w,
+                           const int64_t* vprev, const int64_t* vcur, int frac_bits,
+                           const igm_shifts* shifts, int checked);
+/* the step's scalar work, replicated on every rank (gmres_int.cpp:101-159) */
+igm_status igm_dc_step(igm_ctx* ctx, igm_dstate* d, int j, int frac_bits, const igm_shifts* shifts,
+                       const int64_t* w, int checked);
+/* v_{j+1} = w / h_{j+1,j} (gmres_int.cpp:117-125) */
+igm_status igm_dc_vec_div(igm_ctx* ctx, igm_dstate* d, int64_t n, int j, const int64_t* w, int64_t* vout,
+                          int frac_bits, const igm_shifts* shifts, int checked);
+/* least squares + x += gamma * (0 + sum_j w_j v_j) (gmres_int.cpp:163-180,
+ * refine.cpp:87) over the rank's rows */
+igm_status igm_dc_finish(igm_ctx* ctx, igm_dstate* d, int frac_bits, int64_t n, const int64_t* basis,
+                         double* x);
+/* synchronise and read the cycle/refinement scalars; returns the device
+ * error of the cycle (domain_error, ...) with the reference's message */
+igm_status igm_dc_fetch(igm_ctx* ctx, igm_dstate* d, igm_dc_info* info);
+
 /* ---- host setup (not on the GPU hot path; inputs of the calls above) ---- */
 /* replaces intgmres::row_scale (split.cpp:61-79) */
 igm_status igm_row_scale(int n, const int* row_ptr, const int* col_idx,

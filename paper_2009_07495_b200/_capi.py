@@ -67,6 +67,15 @@ class CycleOut(C.Structure):
     ]
 
 
+class DcInfo(C.Structure):
+    _fields_ = [("dim", C.c_int), ("stop", C.c_int), ("nbasis", C.c_int), ("add_inexact", C.c_int),
+                ("r0_norm", C.c_double), ("relnorm", C.c_double), ("nb", C.c_double), ("nr", C.c_double),
+                ("gamma", C.c_double), ("overflows", C.c_uint64)]
+
+
+IGM_DS_RED, IGM_DS_LCNT, IGM_DS_VCNT, IGM_DS_RMAX, IGM_DS_CHAIN = range(5)
+K_COUNT, OP_COUNT = 11, 6
+
 SCHED_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int)
 
 
@@ -136,6 +145,29 @@ SIGNATURES = [
                                C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_double), C.c_void_p]),
     ("igm_mgs_pass", C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]),
+    # row-block partition building blocks (dist.solve_sharded); device pointers, asynchronous
+    ("igm_dstate_create", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+    ("igm_dstate_free", None, [C.c_void_p]),
+    ("igm_dstate_buffer", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
+    ("igm_dc_reset", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("igm_dc_residual", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("igm_dc_norm2", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
+    ("igm_dc_begin", C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
+    ("igm_dc_scale", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    ("igm_dc_tri_fp", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
+    ("igm_dc_tri", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                             C.c_int]),
+    ("igm_dc_encode", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int]),
+    ("igm_dc_spmv", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                              C.c_int]),
+    ("igm_dc_mgs_pass", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                  C.c_void_p, C.c_int, C.POINTER(Shifts), C.c_int]),
+    ("igm_dc_step", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(Shifts), C.c_void_p,
+                              C.c_int]),
+    ("igm_dc_vec_div", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                                 C.POINTER(Shifts), C.c_int]),
+    ("igm_dc_finish", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_void_p]),
+    ("igm_dc_fetch", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     ("igm_row_scale", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
                                 C.c_void_p]),
     ("igm_build_split", C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p,

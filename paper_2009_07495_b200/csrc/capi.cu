@@ -1410,6 +1410,296 @@ igm_status igm_fp_cycle(igm_ctx* c, const igm_csrf* a, int m, const double* b, c
   });
 }
 
+}  // extern "C"
+
+// ---- row-block (z-slab) partition: rank-local building blocks -------------
+// The distributed driver (paper_2009_07495_b200/dist.py) owns the vectors and
+// the collectives; these entries enqueue the same kernels as enqueue_cycle on
+// the context stream, over device pointers, without synchronising.
+namespace {
+constexpr size_t kCntStride = static_cast<size_t>(K_COUNT) * OP_COUNT;
+}  // namespace
+
+struct igm_dstate {
+  int device = 0, m = 0;
+  Ctl* ctl = nullptr;
+  Ctl* h_ctl = nullptr;
+  unsigned char* small = nullptr;
+  size_t small_bytes = 0;
+  unsigned char* h_small = nullptr;
+  u64 *red = nullptr, *lcnt = nullptr, *vcnt = nullptr, *cnt = nullptr;
+  i64 *hess = nullptr, *g = nullptr, *cs = nullptr, *sn = nullptr, *gabs = nullptr;
+  double *y = nullptr, *wts = nullptr, *chain = nullptr;
+  void* n2s = nullptr;
+  size_t n2s_bytes = 0;
+  u64* slot(int j, int i) const { return red + (static_cast<size_t>(j) * (m + 2) + i) * 3; }
+};
+
+namespace {
+igm_dstate* need_ds(igm_ctx* c, igm_dstate* d) {
+  need_ctx(c);
+  if (!d) fail(IGM_INVALID_ARGUMENT, "null igm_dstate");
+  if (d->device != c->device) fail(IGM_INVALID_ARGUMENT, "igm_dstate belongs to another device");
+  return d;
+}
+void* ds_n2(igm_ctx* c, igm_dstate* d, long long n) {
+  const size_t need = norm2_scratch_bytes(n);
+  if (need > d->n2s_bytes) {
+    ck(cudaStreamSynchronize(c->stream), "norm2 scratch");
+    dfree(d->n2s);
+    d->n2s = dalloc<unsigned char>(need);
+    d->n2s_bytes = need;
+  }
+  return d->n2s;
+}
+void need_dev(const void* p, const char* who) {
+  if (p && !is_device_ptr(p)) fail(IGM_INVALID_ARGUMENT, std::string(who) + ": vectors must be device memory");
+}
+}  // namespace
+
+extern "C" {
+
+igm_status igm_dstate_create(igm_ctx* c, int m, igm_dstate** out) {
+  return guarded([&] {
+    need_ctx(c);
+    if (!out) fail(IGM_INVALID_ARGUMENT, "dstate_create: null out");
+    if (m < 1) fail(IGM_INVALID_ARGUMENT, "run_cycle: m must be >= 1");
+    auto d = std::make_unique<igm_dstate>();
+    d->device = c->device;
+    d->m = m;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes); return o; };
+    const size_t o_red = take(sizeof(u64) * 3 * m * (m + 2));
+    const size_t o_l = take(sizeof(u64) * m * kCntStride);
+    const size_t o_v = take(sizeof(u64) * m * kCntStride);
+    const size_t o_c = take(sizeof(u64) * m * kCntStride);
+    const size_t o_h = take(sizeof(i64) * (m + 1) * m);
+    const size_t o_g = take(sizeof(i64) * (m + 1));
+    const size_t o_cs = take(sizeof(i64) * m);
+    const size_t o_sn = take(sizeof(i64) * m);
+    const size_t o_ga = take(sizeof(i64) * m);
+    const size_t o_y = take(sizeof(double) * m);
+    const size_t o_w = take(sizeof(double) * m);
+    const size_t o_ch = take(sizeof(double) * 4);
+    d->small_bytes = off;
+    d->small = dalloc<unsigned char>(off);
+    ck(cudaMallocHost(reinterpret_cast<void**>(&d->h_small), off), "cudaMallocHost");
+    d->ctl = dalloc<Ctl>(1);
+    ck(cudaMallocHost(reinterpret_cast<void**>(&d->h_ctl), sizeof(Ctl)), "cudaMallocHost");
+    d->red = reinterpret_cast<u64*>(d->small + o_red);
+    d->lcnt = reinterpret_cast<u64*>(d->small + o_l);
+    d->vcnt = reinterpret_cast<u64*>(d->small + o_v);
+    d->cnt = reinterpret_cast<u64*>(d->small + o_c);
+    d->hess = reinterpret_cast<i64*>(d->small + o_h);
+    d->g = reinterpret_cast<i64*>(d->small + o_g);
+    d->cs = reinterpret_cast<i64*>(d->small + o_cs);
+    d->sn = reinterpret_cast<i64*>(d->small + o_sn);
+    d->gabs = reinterpret_cast<i64*>(d->small + o_ga);
+    d->y = reinterpret_cast<double*>(d->small + o_y);
+    d->wts = reinterpret_cast<double*>(d->small + o_w);
+    d->chain = reinterpret_cast<double*>(d->small + o_ch);
+    ck(cudaMemsetAsync(d->small, 0, d->small_bytes, c->stream), "memset");
+    ck(cudaMemsetAsync(d->ctl, 0, sizeof(Ctl), c->stream), "memset");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    *out = d.release();
+  });
+}
+
+void igm_dstate_free(igm_dstate* d) {
+  if (!d) return;
+  cudaSetDevice(d->device);
+  dfree(d->small); dfree(d->ctl); dfree(d->n2s);
+  if (d->h_small) cudaFreeHost(d->h_small);
+  if (d->h_ctl) cudaFreeHost(d->h_ctl);
+  delete d;
+}
+
+igm_status igm_dstate_buffer(igm_dstate* d, int which, int j, void** ptr, int64_t* bytes) {
+  return guarded([&] {
+    if (!d || !ptr || !bytes) fail(IGM_INVALID_ARGUMENT, "dstate_buffer: null argument");
+    if (which != IGM_DS_VCNT && which != IGM_DS_RMAX && which != IGM_DS_CHAIN && (j < 0 || j >= d->m))
+      fail(IGM_INVALID_ARGUMENT, "dstate_buffer: step out of range");
+    switch (which) {
+      case IGM_DS_RED: *ptr = d->slot(j, 0); *bytes = sizeof(u64) * 3 * (d->m + 2); break;
+      case IGM_DS_LCNT: *ptr = d->lcnt + j * kCntStride; *bytes = sizeof(u64) * kCntStride; break;
+      case IGM_DS_VCNT: *ptr = d->vcnt; *bytes = sizeof(u64) * kCntStride * d->m; break;
+      case IGM_DS_RMAX: *ptr = &d->ctl->rmax_bits; *bytes = sizeof(u64); break;
+      case IGM_DS_CHAIN: *ptr = d->chain; *bytes = sizeof(double) * 4; break;
+      default: fail(IGM_INVALID_ARGUMENT, "dstate_buffer: unknown buffer");
+    }
+  });
+}
+
+igm_status igm_dc_reset(igm_ctx* c, igm_dstate* d) {
+  return guarded([&] {
+    need_ds(c, d);
+    ck(cudaMemsetAsync(d->ctl, 0, sizeof(Ctl), c->stream), "ctl reset");
+  });
+}
+
+igm_status igm_dc_residual(igm_ctx* c, igm_dstate* d, const igm_csrf* a, const double* x_ext, const double* b,
+                           double* r) {
+  return guarded([&] {
+    need_ds(c, d);
+    if (!a) fail(IGM_INVALID_ARGUMENT, "dc_residual: null matrix");
+    need_dev(x_ext, "dc_residual"); need_dev(b, "dc_residual"); need_dev(r, "dc_residual");
+    ck(cudaMemsetAsync(&d->ctl->rmax_bits, 0, sizeof(u64), c->stream), "rmax reset");
+    launch_residual(c->stream, *a, x_ext, b, r, d->ctl, true);
+  });
+}
+
+igm_status igm_dc_norm2(igm_ctx* c, igm_dstate* d, int64_t n, const double* v, const double* start, double* out,
+                        int mode) {
+  return guarded([&] {
+    need_ds(c, d);
+    if (mode != 1 && mode != 2 && mode != 3 && mode != 5) fail(IGM_INVALID_ARGUMENT, "dc_norm2: bad mode");
+    if (mode == 5 && !out) fail(IGM_INVALID_ARGUMENT, "dc_norm2: null out");
+    need_dev(v, "dc_norm2"); need_dev(start, "dc_norm2"); need_dev(out, "dc_norm2");
+    launch_norm2_serial(c->stream, n, v, out, d->ctl, mode, ds_n2(c, d, n), start);
+  });
+}
+
+igm_status igm_dc_begin(igm_ctx* c, igm_dstate* d, int f) {
+  return guarded([&] {
+    need_ds(c, d);
+    check_qformat(f);
+    ck(cudaMemsetAsync(d->small, 0, d->small_bytes, c->stream), "memset small");
+    launch_cycle_init(c->stream, d->ctl, d->g, f);
+  });
+}
+
+igm_status igm_dc_scale(igm_ctx* c, igm_dstate* d, int64_t n, const double* r, double* out) {
+  return guarded([&] {
+    need_ds(c, d);
+    need_dev(r, "dc_scale"); need_dev(out, "dc_scale");
+    launch_scale_div(c->stream, n, r, out, d->ctl);
+  });
+}
+
+igm_status igm_dc_tri_fp(igm_ctx* c, igm_dstate* d, const igm_ilu* f, int backward, const double* in,
+                         double* out) {
+  return guarded([&] {
+    need_ds(c, d);
+    if (!f) fail(IGM_INVALID_ARGUMENT, "dc_tri_fp: null factors");
+    need_dev(in, "dc_tri_fp"); need_dev(out, "dc_tri_fp");
+    launch_tri_fp(c->stream, backward ? f->upper : f->lower, backward != 0, in, out, d->ctl, nullptr);
+  });
+}
+
+igm_status igm_dc_encode(igm_ctx* c, igm_dstate* d, int64_t n, const double* r0, int64_t* v0, int f) {
+  return guarded([&] {
+    need_ds(c, d);
+    need_dev(r0, "dc_encode"); need_dev(v0, "dc_encode");
+    launch_encode(c->stream, n, r0, v0, f, d->ctl);
+  });
+}
+
+igm_status igm_dc_spmv(igm_ctx* c, igm_dstate* d, const igm_split* m, int s, const int64_t* v_ext, int64_t* out,
+                       int j, int checked) {
+  return guarded([&] {
+    need_ds(c, d);
+    if (!m) fail(IGM_INVALID_ARGUMENT, "dc_spmv: null matrix");
+    if (s < 0 || s > m->ncomp - 1) fail(IGM_INVALID_ARGUMENT, "run_cycle: splitting depth out of range");
+    if (j < 0 || j >= d->m) fail(IGM_INVALID_ARGUMENT, "dc_spmv: step out of range");
+    need_dev(v_ext, "dc_spmv"); need_dev(out, "dc_spmv");
+    launch_spmv_int(c->stream, *m, s, v_ext, out, d->lcnt + j * kCntStride + K_SPMV * OP_COUNT, d->ctl,
+                    checked != 0);
+  });
+}
+
+igm_status igm_dc_tri(igm_ctx* c, igm_dstate* d, const igm_ilu* f, int backward, const int64_t* in,
+                      int64_t* out, int j, int checked) {
+  return guarded([&] {
+    need_ds(c, d);
+    if (!f) fail(IGM_INVALID_ARGUMENT, "dc_tri: null factors");
+    if (j < 0 || j >= d->m) fail(IGM_INVALID_ARGUMENT, "dc_tri: step out of range");
+    need_dev(in, "dc_tri"); need_dev(out, "dc_tri");
+    launch_tri_int(c->stream, backward ? f->upper : f->lower, backward != 0, in, out,
+                   d->lcnt + j * kCntStride + K_PRECOND * OP_COUNT, d->ctl, checked != 0);
+  });
+}
+
+igm_status igm_dc_mgs_pass(igm_ctx* c, igm_dstate* d, int64_t n, int j, int i, int64_t* w, const int64_t* vprev,
+                           const int64_t* vcur, int f, const igm_shifts* sh, int checked) {
+  return guarded([&] {
+    need_ds(c, d);
+    if (!sh) fail(IGM_INVALID_ARGUMENT, "dc_mgs_pass: null shifts");
+    if (j < 0 || j >= d->m || i < 0 || i > j + 1) fail(IGM_INVALID_ARGUMENT, "dc_mgs_pass: step out of range");
+    const int mode = i == 0 ? 0 : (i <= j ? 1 : 2);
+    need_dev(w, "dc_mgs_pass"); need_dev(vprev, "dc_mgs_pass"); need_dev(vcur, "dc_mgs_pass");
+    if ((mode != 2 && !vcur) || (mode != 0 && !vprev)) fail(IGM_INVALID_ARGUMENT, "dc_mgs_pass: missing vector");
+    u64* lc = d->lcnt + j * kCntStride;
+    u64* sl = d->slot(j, i);
+    launch_mgs_pass(c->stream, n, mode, w, vprev, mode == 2 ? nullptr : vcur, i > 0 ? d->slot(j, i - 1) : nullptr,
+                    sl, sl + 1, f, to_sd(*sh), lc + K_AXPY * OP_COUNT, lc + (mode == 2 ? K_NORM : K_DOT) * OP_COUNT,
+                    d->ctl, checked != 0);
+  });
+}
+
+igm_status igm_dc_step(igm_ctx* c, igm_dstate* d, int j, int f, const igm_shifts* sh, const int64_t* w,
+                       int checked) {
+  return guarded([&] {
+    need_ds(c, d);
+    if (!sh) fail(IGM_INVALID_ARGUMENT, "dc_step: null shifts");
+    if (j < 0 || j >= d->m) fail(IGM_INVALID_ARGUMENT, "dc_step: step out of range");
+    need_dev(w, "dc_step");
+    u64* s0 = d->slot(j, 0);
+    u64* sn = d->slot(j, j + 1);
+    launch_step_scalar(c->stream, j, f, to_sd(*sh), s0, s0 + 1, sn, sn + 1, d->hess, d->m + 1, d->g, d->cs, d->sn,
+                       d->gabs, w, d->cnt + j * kCntStride, d->ctl, checked != 0, 3, 3,
+                       d->lcnt + j * kCntStride + K_NORM * OP_COUNT + OP_MUL);
+  });
+}
+
+igm_status igm_dc_vec_div(igm_ctx* c, igm_dstate* d, int64_t n, int j, const int64_t* w, int64_t* vout, int f,
+                          const igm_shifts* sh, int checked) {
+  return guarded([&] {
+    need_ds(c, d);
+    if (!sh) fail(IGM_INVALID_ARGUMENT, "dc_vec_div: null shifts");
+    if (j < 0 || j >= d->m) fail(IGM_INVALID_ARGUMENT, "dc_vec_div: step out of range");
+    need_dev(w, "dc_vec_div"); need_dev(vout, "dc_vec_div");
+    launch_vec_div(c->stream, n, w, vout, f, to_sd(*sh), d->vcnt + j * kCntStride + K_VEC_DIV * OP_COUNT, d->ctl,
+                   checked != 0);
+  });
+}
+
+igm_status igm_dc_finish(igm_ctx* c, igm_dstate* d, int f, int64_t n, const int64_t* basis, double* x) {
+  return guarded([&] {
+    need_ds(c, d);
+    need_dev(basis, "dc_finish"); need_dev(x, "dc_finish");
+    launch_cycle_finish(c->stream, d->m, f, d->hess, d->g, d->y, d->wts, d->ctl);
+    launch_xupdate(c->stream, n, d->m, f, basis, d->wts, nullptr, x, d->ctl, 1);
+  });
+}
+
+igm_status igm_dc_fetch(igm_ctx* c, igm_dstate* d, igm_dc_info* info) {
+  return guarded([&] {
+    need_ds(c, d);
+    if (!info) fail(IGM_INVALID_ARGUMENT, "dc_fetch: null info");
+    ck(cudaMemcpyAsync(d->h_ctl, d->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream), "ctl D2H");
+    ck(cudaMemcpyAsync(d->h_small, d->small, d->small_bytes, cudaMemcpyDeviceToHost, c->stream), "small D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    const Ctl& h = *d->h_ctl;
+    info->dim = h.dim;
+    info->stop = h.stop;
+    info->nbasis = h.nbasis;
+    info->add_inexact = h.add_inexact;
+    info->r0_norm = h.r0n;
+    info->relnorm = h.relnorm;
+    info->nb = h.nb;
+    info->nr = h.nr;
+    std::memcpy(&info->gamma, &h.rmax_bits, sizeof(double));
+    u64 tot = 0;
+    auto sum = [&](const u64* dev) {
+      const u64* hp = reinterpret_cast<const u64*>(d->h_small + (reinterpret_cast<const unsigned char*>(dev) - d->small));
+      for (size_t k = 0; k < kCntStride * d->m; ++k) tot += hp[k];
+    };
+    sum(d->lcnt); sum(d->vcnt); sum(d->cnt);
+    info->overflows = tot;
+    if (h.err) fail(static_cast<igm_status>(h.err), em_text(h.err_msg));
+  });
+}
+
 igm_status igm_mgs_pass(igm_ctx* c, int64_t n, int mode, int64_t* w, const int64_t* vprev,
                         const int64_t* vcur, const uint64_t* hacc, uint64_t* acc_out, int f, int dot_b1,
                         int dot_b2, int axpy_b1) {

@@ -138,8 +138,11 @@ void launch_tri_fp(cudaStream_t st, const DevTri& t, bool backward,
                    const double* prescale /* divide y by *prescale or null */);
 // exact sequential-order norm2 (split.cpp:45-49); scratch: norm2_scratch_bytes(n)
 size_t norm2_scratch_bytes(long long n);
+// start: device pointer to the chain's starting value (null = 0.0); mode 5
+// writes the running sum itself to *out (one rank's leg of a relayed chain)
 void launch_norm2_serial(cudaStream_t st, long long n, const double* v,
-                         double* out, Ctl* ctl, int mode, void* scratch);
+                         double* out, Ctl* ctl, int mode, void* scratch,
+                         const double* start = nullptr);
 void launch_mgs_pass(cudaStream_t st, long long n, int mode, i64* w,
                      const i64* vprev, const i64* vcur, const u64* hacc,
                      u64* acc_out, u64* abs_out, int f, ShiftsD sh,
@@ -152,7 +155,8 @@ void launch_step_scalar(cudaStream_t st, int j, int f, ShiftsD sh,
                         const u64* acc_col, const u64* abs_col, const u64* nacc,
                         const u64* nabs, i64* hess, int ld, i64* g, i64* cs,
                         i64* sn, i64* gabs, const i64* w, u64* cnt_step,
-                        Ctl* ctl, bool checked);
+                        Ctl* ctl, bool checked, int acc_st = 1, int abs_st = 2,
+                        const u64* norm_mul = nullptr /* cnt_step's slot */);
 void launch_cycle_init(cudaStream_t st, Ctl* ctl, i64* g, int f);
 void launch_encode(cudaStream_t st, long long n, const double* r0, i64* v0,
                    int f, Ctl* ctl);

@@ -254,17 +254,19 @@ __global__ void k_scale_div(long long n, const double* __restrict__ r, double* _
 // warp 0 runs the dependent FP64 add chain over the current tile.
 // mode: 0 -> *out = sqrt; 1 -> ctl->nb; 2 -> ctl->nr and ctl->relnorm;
 //       3 -> ctl->r0n (stop the cycle when zero); 4 -> out[0] (decode raw
-//       basis words first: collect_basis_norms).
+//       basis words first: collect_basis_norms); 5 -> *out = the running sum
+//       (no sqrt: one rank's leg of a chain relayed across a row partition).
+// start (device, may be null): the chain's starting value.
 constexpr int kNormTile = 2048;
 
 __global__ void __launch_bounds__(256) k_norm2_serial(long long n, const double* __restrict__ v,
                                                       const i64* __restrict__ raw, double scale,
                                                       double* out, Ctl* ctl, int mode,
-                                                      int basis_idx) {
+                                                      int basis_idx, const double* start) {
   __shared__ double buf[2][kNormTile];
   if (mode == 3 && cycle_over(ctl)) return;
   if (mode == 4 && (ctl->err || basis_idx >= ctl->nbasis)) return;
-  double acc = 0.0;
+  double acc = start ? *start : 0.0;
   const long long ntiles = (n + kNormTile - 1) / kNormTile;
   for (long long t = 0; t < ntiles; ++t) {
     double* b = buf[t & 1];
@@ -293,6 +295,7 @@ __global__ void __launch_bounds__(256) k_norm2_serial(long long n, const double*
   if (threadIdx.x == 0) {
     const double r = __dsqrt_rn(acc);
     switch (mode) {
+      case 5: *out = acc; break;
       case 0: *out = r; break;
       case 1: ctl->nb = r; break;
       case 2:
@@ -520,6 +523,7 @@ __device__ void n2_finish(long long n, const double* __restrict__ v, const i64* 
   }
   const double r = __dsqrt_rn(acc);
   switch (mode) {
+    case 5: *out = acc; break;  // the running sum itself (a rank's leg of a distributed chain)
     case 0: *out = r; break;
     case 1: ctl->nb = r; break;
     case 2:
@@ -534,21 +538,37 @@ __device__ void n2_finish(long long n, const double* __restrict__ v, const i64* 
   }
 }
 
-__device__ __forceinline__ void n2_init(N2State& S) {
+// s0: the chain's starting value (0, or the running sum handed over by the
+// previous rank of a row-block partition); any non-negative double
+__device__ __forceinline__ void n2_init(N2State& S, const double* start) {
   S.E = -1022;  // s = 0: subnormal binade, u = 2^-1074
   S.M = 0;
   S.pos = 0;
   S.tail = 0;
+  const double s0 = start ? *start : 0.0;
+  if (s0 != 0.0) {
+    const u64 bits = static_cast<u64>(__double_as_longlong(s0));
+    const int ex = static_cast<int>((bits >> 52) & 0x7ff);
+    if (ex == 0x7ff || s0 < 0.0) {  // non-finite (or not a sum of squares): serial tail
+      S.tail = 1;
+      S.tailv = s0;
+    } else if (ex == 0) {
+      S.M = bits & ((1ull << 52) - 1);
+    } else {
+      S.E = ex - 1023;
+      S.M = (bits & ((1ull << 52) - 1)) | (1ull << 52);
+    }
+  }
 }
 
 // single-CTA exact chain (short vectors)
 __global__ void __launch_bounds__(kN2Threads) k_norm2_exact(long long n, const double* __restrict__ v,
                                                             const i64* __restrict__ raw, double scale,
                                                             double* out, Ctl* ctl, int mode,
-                                                            int basis_idx) {
+                                                            int basis_idx, const double* start) {
   __shared__ N2State S;
   if (n2_skip(ctl, mode, basis_idx)) return;
-  if (threadIdx.x == 0) n2_init(S);
+  if (threadIdx.x == 0) n2_init(S, start);
   __syncthreads();
   n2_advance(n, v, raw, scale, S);
   if (threadIdx.x == 0) n2_finish(n, v, raw, scale, S, out, ctl, mode, basis_idx);
@@ -596,7 +616,8 @@ __global__ void __launch_bounds__(kN2BThreads) k_n2_bsum(long long n, const doub
 
 __global__ void __launch_bounds__(kN2BThreads) k_n2_baut(long long n, const double* __restrict__ v,
                                                          const i64* __restrict__ raw, double scale, N2Blk* blk,
-                                                         const Ctl* ctl, int mode, int basis_idx) {
+                                                         const Ctl* ctl, int mode, int basis_idx,
+                                                         const double* start) {
   __shared__ double shs[kN2BThreads / 32];
   __shared__ Aut sha[kN2BThreads / 32];
   __shared__ int sbad;
@@ -612,7 +633,7 @@ __global__ void __launch_bounds__(kN2BThreads) k_n2_baut(long long n, const doub
   if (tid == 0) sbad = 0;
   __syncthreads();
   if (tid == 0) {
-    double t = 0.0;
+    double t = start ? *start : 0.0;
     for (int w = 0; w < kN2BThreads / 32; ++w) t += shs[w];
     int E = -1022;
     if (t > 0.0 && isfinite(t)) {
@@ -664,13 +685,13 @@ __global__ void __launch_bounds__(kN2BThreads) k_n2_baut(long long n, const doub
 __global__ void __launch_bounds__(kN2Threads) k_n2_walk(long long n, int nblk, const double* __restrict__ v,
                                                         const i64* __restrict__ raw, double scale,
                                                         const N2Blk* blk, double* out, Ctl* ctl, int mode,
-                                                        int basis_idx) {
+                                                        int basis_idx, const double* start) {
   constexpr int kPage = 512;
   __shared__ N2State S;
   __shared__ N2Blk page[kPage];
   __shared__ int s_fast;
   if (n2_skip(ctl, mode, basis_idx)) return;
-  if (threadIdx.x == 0) n2_init(S);
+  if (threadIdx.x == 0) n2_init(S, start);
   for (int p0 = 0; p0 < nblk; p0 += kPage) {
     const int np = min(kPage, nblk - p0);
     __syncthreads();
@@ -1051,10 +1072,13 @@ __device__ bool abs_small(const u64* ab) {
   return s < (static_cast<unsigned __int128>(1) << 63);
 }
 
-__device__ void step_scalar_dev(int j, int f, ShiftsD sh, const u64* acc_col, const u64* abs_col,
-                                const u64* nacc, const u64* nabs, i64* hess, int ld, i64* g,
-                                i64* cs, i64* sn, i64* gabs, const i64* w, u64* cnt_step, Ctl* ctl,
-                                int checked) {
+// acc_col[i * acc_st] / abs_col[i * abs_st .. +1]: pass i's wrapped
+// accumulator and sum|term| (hi, lo); norm_mul: the norm pass's square-overflow
+// count (cnt_step's own slot on one GPU, the all-reduced one on a partition).
+__device__ void step_scalar_dev(int j, int f, ShiftsD sh, const u64* acc_col, int acc_st, const u64* abs_col,
+                                int abs_st, const u64* nacc, const u64* nabs, const u64* norm_mul, i64* hess,
+                                int ld, i64* g, i64* cs, i64* sn, i64* gabs, const i64* w, u64* cnt_step,
+                                Ctl* ctl, int checked) {
   ctl->do_vecdiv = 0;
   if (cycle_over(ctl)) return;
   Ev ev{cnt_step, checked != 0};
@@ -1062,21 +1086,21 @@ __device__ void step_scalar_dev(int j, int f, ShiftsD sh, const u64* acc_col, co
   // h_ij = fx_dot finalisation (fxp.cpp:63-65)
   const int e = f - sh.dot_b1 - sh.dot_b2;
   for (int i = 0; i <= j; ++i) {
-    const i64 acc = static_cast<i64>(acc_col[i]);
+    const i64 acc = static_cast<i64>(acc_col[i * acc_st]);
     if (e >= 0) {
       col[i] = asr(acc, e);
     } else {
       if (shl_ovf(acc, -e)) ev.hit(K_DOT, OP_SHL);
       col[i] = wrap_shl(acc, -e);
     }
-    if (checked && !abs_small(abs_col + 2 * i)) ctl->add_inexact = 1;
+    if (checked && !abs_small(abs_col + i * abs_st)) ctl->add_inexact = 1;
   }
   // h_{j+1,j} = fx_norm(w) (fxp.cpp:69-86)
   const i64 nsum = static_cast<i64>(*nacc);
   if (checked) {
     // all terms s*s are >= 0 unless a square itself wrapped: then the
     // running sum is monotone and its wrap count is exact.
-    if (cnt_step[K_NORM * OP_COUNT + OP_MUL] == 0) {
+    if (*norm_mul == 0) {
       const unsigned __int128 s = (static_cast<unsigned __int128>(nabs[0]) << 32) + nabs[1];
       const unsigned __int128 wraps = (s + (static_cast<unsigned __int128>(1) << 63)) >> 64;
       cnt_step[K_NORM * OP_COUNT + OP_ADD] += static_cast<u64>(wraps);
@@ -1170,11 +1194,12 @@ __device__ void step_scalar_dev(int j, int f, ShiftsD sh, const u64* acc_col, co
   if (happy) ctl->stop = 1;
 }
 
-__global__ void k_step_scalar(int j, int f, ShiftsD sh, const u64* acc_col, const u64* abs_col,
-                              const u64* nacc, const u64* nabs, i64* hess, int ld, i64* g,
-                              i64* cs, i64* sn, i64* gabs, const i64* w, u64* cnt_step, Ctl* ctl,
-                              int checked) {
-  step_scalar_dev(j, f, sh, acc_col, abs_col, nacc, nabs, hess, ld, g, cs, sn, gabs, w, cnt_step, ctl, checked);
+__global__ void k_step_scalar(int j, int f, ShiftsD sh, const u64* acc_col, int acc_st, const u64* abs_col,
+                              int abs_st, const u64* nacc, const u64* nabs, const u64* norm_mul, i64* hess,
+                              int ld, i64* g, i64* cs, i64* sn, i64* gabs, const i64* w, u64* cnt_step,
+                              Ctl* ctl, int checked) {
+  step_scalar_dev(j, f, sh, acc_col, acc_st, abs_col, abs_st, nacc, nabs, norm_mul, hess, ld, g, cs, sn, gabs, w,
+                  cnt_step, ctl, checked);
 }
 
 // ---------------------------------------------------------------------------
@@ -1419,7 +1444,8 @@ __global__ void __launch_bounds__(kArnThreads, 1)
   grid_barrier(ctl, (++nbar) * G, nullptr, nullptr);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     __threadfence();  // this SM's L1 holds no stale copy of the reduced words
-    step_scalar_dev(j, f, sh, accj, absj, nacc, nabs, hess, ld, g, cs, sn, gabs, sw, cstep, ctl, CHECKED ? 1 : 0);
+    step_scalar_dev(j, f, sh, accj, 1, absj, 2, nacc, nabs, cstep + K_NORM * OP_COUNT + OP_MUL, hess, ld, g, cs,
+                    sn, gabs, sw, cstep, ctl, CHECKED ? 1 : 0);
   }
   const u64 dm = grid_barrier(ctl, (++nbar) * G, &ctl->div_m, &s_word);
   if (threadIdx.x == 0) {  // the divisor's magic, once per CTA
@@ -2148,25 +2174,26 @@ size_t norm2_scratch_bytes(long long n) {
 
 // exact norm2 chain of v (or of the decoded raw words when raw != null)
 static void norm2_enqueue(cudaStream_t st, long long n, const double* v, const i64* raw, double scale,
-                          double* out, Ctl* ctl, int mode, int basis_idx, void* scratch) {
+                          double* out, Ctl* ctl, int mode, int basis_idx, void* scratch,
+                          const double* start = nullptr) {
   if (norm2_serial_forced()) {
-    k_norm2_serial<<<1, 256, 0, st>>>(n, v, raw, scale, out, ctl, mode, basis_idx);
+    k_norm2_serial<<<1, 256, 0, st>>>(n, v, raw, scale, out, ctl, mode, basis_idx, start);
   } else if (n <= 2 * kN2Chunk || scratch == nullptr) {
-    k_norm2_exact<<<1, kN2Threads, 0, st>>>(n, v, raw, scale, out, ctl, mode, basis_idx);
+    k_norm2_exact<<<1, kN2Threads, 0, st>>>(n, v, raw, scale, out, ctl, mode, basis_idx, start);
   } else {
     const int nblk = static_cast<int>((n + kN2Chunk - 1) / kN2Chunk);
     N2Blk* blk = static_cast<N2Blk*>(scratch);
     k_n2_bsum<<<nblk, kN2BThreads, 0, st>>>(n, v, raw, scale, blk, ctl, mode, basis_idx);
-    k_n2_baut<<<nblk, kN2BThreads, 0, st>>>(n, v, raw, scale, blk, ctl, mode, basis_idx);
-    k_n2_walk<<<1, kN2Threads, 0, st>>>(n, nblk, v, raw, scale, blk, out, ctl, mode, basis_idx);
+    k_n2_baut<<<nblk, kN2BThreads, 0, st>>>(n, v, raw, scale, blk, ctl, mode, basis_idx, start);
+    k_n2_walk<<<1, kN2Threads, 0, st>>>(n, nblk, v, raw, scale, blk, out, ctl, mode, basis_idx, start);
   }
   LAUNCH_CHECK();
 }
 
 void launch_norm2_serial(cudaStream_t st, long long n, const double* v, double* out, Ctl* ctl, int mode,
-                         void* scratch) {
+                         void* scratch, const double* start) {
   ProfScope prof_(st, KC_NORM2);
-  norm2_enqueue(st, n, v, nullptr, 1.0, out, ctl, mode, 0, scratch);
+  norm2_enqueue(st, n, v, nullptr, 1.0, out, ctl, mode, 0, scratch, start);
 }
 
 void launch_basis_norms(cudaStream_t st, long long n, int nb, int f, const i64* basis, void* scratch,
@@ -2257,10 +2284,11 @@ void launch_vec_div(cudaStream_t st, long long n, const i64* w, i64* out, int f,
 void launch_step_scalar(cudaStream_t st, int j, int f, ShiftsD sh, const u64* acc_col,
                         const u64* abs_col, const u64* nacc, const u64* nabs, i64* hess, int ld,
                         i64* g, i64* cs, i64* sn, i64* gabs, const i64* w, u64* cnt_step, Ctl* ctl,
-                        bool checked) {
+                        bool checked, int acc_st, int abs_st, const u64* norm_mul) {
   ProfScope prof_(st, KC_SCALAR);
-  k_step_scalar<<<1, 1, 0, st>>>(j, f, sh, acc_col, abs_col, nacc, nabs, hess, ld, g, cs, sn, gabs,
-                                 w, cnt_step, ctl, checked ? 1 : 0);
+  if (!norm_mul) norm_mul = cnt_step + K_NORM * OP_COUNT + OP_MUL;
+  k_step_scalar<<<1, 1, 0, st>>>(j, f, sh, acc_col, acc_st, abs_col, abs_st, nacc, nabs, norm_mul, hess, ld, g,
+                                 cs, sn, gabs, w, cnt_step, ctl, checked ? 1 : 0);
   LAUNCH_CHECK();
 }
 

@@ -111,7 +111,9 @@ def halo_ops(slab: Slab, own, ext, dist, group=None):
 
 def halo_exchange(slab: Slab, own, ext, dist, group=None) -> None:
     """Fill ext (extended local vector) from own rows + the neighbours' planes."""
-    ext[slab.own0:slab.own1].copy_(own)
+    dst = ext[slab.own0:slab.own1]
+    if dst.data_ptr() != own.data_ptr():
+        dst.copy_(own)
     ops = halo_ops(slab, own, ext, dist, group)
     if ops:
         for r in dist.batch_isend_irecv(ops):
@@ -149,15 +151,141 @@ class CudaSlabBackend:
     def upload(self, rp, ci, comp, alphas):
         return self.igm.SplitMatrix(rp, ci, comp, alphas, device=self.dev)
 
-    def spmv(self, m, s, v_ext, out_ext):
+    def spmv_c5(self, m, s, v_ext, out_ext):
         import ctypes as C
         # device pointers: enqueued on the library stream (== torch's current
         # stream inside stream()), returns synchronised
         self.igm._check(self.igm.lib().igm_spmv(self.dev.h, m.h, s, C.c_void_p(v_ext.data_ptr()),
                                                 C.c_void_p(out_ext.data_ptr()), None))
 
-    def mgs_pass(self, mode, w, vprev, vcur, hacc, acc_out, f, b1, b2, a1):
+    def mgs_pass_c5(self, mode, w, vprev, vcur, hacc, acc_out, f, b1, b2, a1):
         self.igm.mgs_pass(self.dev, mode, w, vprev, vcur, hacc, acc_out, f, b1, b2, a1)
+
+    # ---- the partitioned solve (solve_sharded): igm_dstate + igm_dc_* entries
+    def sync(self):
+        self._torch.cuda.synchronize(self.dev.index)
+
+    def zeros(self, shape, kind):
+        dt = {"i64": self._torch.int64, "f64": self._torch.float64}[kind]
+        with self.stream():
+            return self._torch.zeros(shape, dtype=dt, device=f"cuda:{self.dev.index}")
+
+    def host_i64(self, vals):
+        return self._torch.tensor(vals, dtype=self._torch.int64, device=f"cuda:{self.dev.index}")
+
+    def upload_rows(self, rp, ci, comp, alphas, fp_vals):
+        """own rows x extended columns: SplitMatrix + CsrMatrixF (shared pattern)"""
+        return (self.igm.SplitMatrix(rp, ci, comp, alphas, device=self.dev),
+                self.igm.CsrMatrixF(rp, ci, fp_vals, device=self.dev))
+
+    def upload_factors(self, lower, upper):
+        return self.igm.IluFactors(lower, upper, device=self.dev)
+
+    def state(self, m):
+        return _DState(self, m)
+
+    def view(self, st, which, j=0):
+        return st.view(which, j)
+
+    def _c(self, name, *args):
+        self.igm._check(getattr(self.igm.lib(), name)(self.dev.h, *args))
+
+    @staticmethod
+    def _p(t):
+        import ctypes as C
+        return None if t is None else C.c_void_p(t.data_ptr())
+
+    def reset(self, st):
+        self._c("igm_dc_reset", st.h)
+
+    def residual(self, st, a, x_ext, b, r):
+        self._c("igm_dc_residual", st.h, a.h, self._p(x_ext), self._p(b), self._p(r))
+
+    def norm2(self, st, v, start, out, mode):
+        self._c("igm_dc_norm2", st.h, int(v.numel()), self._p(v), self._p(start), self._p(out), mode)
+
+    def begin(self, st, f):
+        self._c("igm_dc_begin", st.h, f)
+
+    def scale(self, st, r, out):
+        self._c("igm_dc_scale", st.h, int(r.numel()), self._p(r), self._p(out))
+
+    def tri(self, st, fac, backward, src, dst, fp, j, checked):
+        if fp:
+            self._c("igm_dc_tri_fp", st.h, fac.h, 1 if backward else 0, self._p(src), self._p(dst))
+        else:
+            self._c("igm_dc_tri", st.h, fac.h, 1 if backward else 0, self._p(src), self._p(dst), j,
+                    1 if checked else 0)
+
+    def encode(self, st, r0, v0, f):
+        self._c("igm_dc_encode", st.h, int(r0.numel()), self._p(r0), self._p(v0), f)
+
+    def spmv(self, st, m, s, v_ext, out, j, checked):
+        self._c("igm_dc_spmv", st.h, m.h, s, self._p(v_ext), self._p(out), j, 1 if checked else 0)
+
+    def mgs_pass(self, st, j, i, w, vprev, vcur, f, sh, checked):
+        import ctypes as C
+        self._c("igm_dc_mgs_pass", st.h, int(w.numel()), j, i, self._p(w), self._p(vprev), self._p(vcur), f,
+                C.byref(sh.c()), 1 if checked else 0)
+
+    def step(self, st, j, f, sh, w, checked):
+        import ctypes as C
+        self._c("igm_dc_step", st.h, j, f, C.byref(sh.c()), self._p(w), 1 if checked else 0)
+
+    def vec_div(self, st, j, w, vout, f, sh, checked):
+        import ctypes as C
+        self._c("igm_dc_vec_div", st.h, int(w.numel()), j, self._p(w), self._p(vout), f, C.byref(sh.c()),
+                1 if checked else 0)
+
+    def finish(self, st, f, basis, x):
+        self._c("igm_dc_finish", st.h, f, int(x.numel()), self._p(basis), self._p(x))
+
+    def fetch(self, st):
+        import ctypes as C
+        from . import _capi
+        info = _capi.DcInfo()
+        self._c("igm_dc_fetch", st.h, C.byref(info))
+        return info
+
+
+class _DevView:
+    """__cuda_array_interface__ over a device buffer of the C library (no copy)."""
+
+    def __init__(self, ptr, count, typestr):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class _DState:
+    """igm_dstate: the rank's replicated per-cycle scalars + reduction slots."""
+
+    def __init__(self, be, m):
+        import ctypes as C
+        self.be, self.m = be, m
+        h = C.c_void_p()
+        be.igm._check(be.igm.lib().igm_dstate_create(be.dev.h, m, C.byref(h)))
+        self.h = h
+        self._views = {}
+
+    def view(self, which, j=0):
+        import ctypes as C
+        from . import _capi
+        key = (which, j)
+        if key not in self._views:
+            code = {"red": _capi.IGM_DS_RED, "lcnt": _capi.IGM_DS_LCNT, "vcnt": _capi.IGM_DS_VCNT,
+                    "rmax": _capi.IGM_DS_RMAX, "chain": _capi.IGM_DS_CHAIN}[which]
+            ptr, nb = C.c_void_p(), C.c_int64()
+            self.be.igm._check(self.be.igm.lib().igm_dstate_buffer(self.h, code, j, C.byref(ptr), C.byref(nb)))
+            ts = "<f8" if which == "chain" else "<i8"
+            self._views[key] = self.be._torch.as_tensor(_DevView(ptr.value, nb.value // 8, ts),
+                                                        device=f"cuda:{self.be.dev.index}")
+        return self._views[key]
+
+    def __del__(self):
+        try:
+            self.be.igm.lib().igm_dstate_free(self.h)
+        except Exception:
+            pass
 
 
 def spmv_mgs_sharded(backend, slab: Slab, m, s: int, v_own, basis_own, k: int, f: int, b1: int, b2: int,
@@ -170,13 +298,340 @@ def spmv_mgs_sharded(backend, slab: Slab, m, s: int, v_own, basis_own, k: int, f
     vext, wext, acc = work["vext"], work["wext"], work["acc"]
     with backend.stream():
         halo_exchange(slab, v_own, vext, dist, group)
-        backend.spmv(m, s, vext, wext)
+        backend.spmv_c5(m, s, vext, wext)
         w = wext[slab.own0:slab.own1]
         acc.zero_()
         for i in range(k):
-            backend.mgs_pass(0 if i == 0 else 1, w, basis_own[i - 1] if i > 0 else None, basis_own[i],
+            backend.mgs_pass_c5(0 if i == 0 else 1, w, basis_own[i - 1] if i > 0 else None, basis_own[i],
                              acc[i - 1:i] if i > 0 else None, acc[i:i + 1], f, b1, b2, a1)
             if slab.world > 1:
                 dist.all_reduce(acc[i:i + 1], op=dist.ReduceOp.SUM, group=group)
-        backend.mgs_pass(3, w, basis_own[k - 1], None, acc[k - 1:k], None, f, b1, b2, a1)
+        backend.mgs_pass_c5(3, w, basis_own[k - 1], None, acc[k - 1:k], None, f, b1, b2, a1)
     return w, acc
+
+
+# ===========================================================================
+# The whole refinement solve on a row-block partition (SURVEY.md §8(e),
+# BASELINE config 4: "rows block-partitioned along z at 1/2/4/8 GPUs with halo
+# exchange and NCCL int64 dot allreduce").
+#
+# Every rank runs the reference's solve (refine.cpp:21-106) and cycle
+# (gmres_int.cpp:42-196) over its own rows; the exchanges are exactly the
+# data the sequential algorithm moves across a plane boundary:
+#   * SpMV / FP residual: one halo plane per side (7- and 27-point stencils);
+#   * MGS / norm passes: the wrapping u64 accumulators (+ the sum|t| words of
+#     checked mode) summed over ranks -- Z/2^64 addition, exact in any order;
+#     the per-step scalar work (h_ij, fx_norm, Givens, g) is then replicated;
+#   * norm2 (split.cpp:45-49) is one sequential FP64 chain: rank p continues
+#     it from rank p-1's running sum (a rank-ordered relay), the last rank
+#     hands the total to all -- bit-identical to the single-chain order;
+#   * gamma = max|r_i|: int64 MAX of the IEEE bits (non-negative doubles
+#     order as integers);
+#   * ILU(0) substitutions (ilu.cpp:122-180) stay the GLOBAL factors (a
+#     block-Jacobi split would change the bits): forward solves run rank 0 ->
+#     P-1, each rank starting once its lower neighbour's last plane of z has
+#     arrived (placed in a unit halo row of its extended local factor: z = y /
+#     1 exactly), backward solves run P-1 -> 0 the same way.  The DAG's
+#     critical path is unchanged by P (§8(e)).
+# Everything else (encode, vec_div, x update) is row-local.
+# ===========================================================================
+from dataclasses import field
+
+
+def slab_rows(row_ptr, col_idx, vals: Sequence[np.ndarray], slab: Slab):
+    """The rank's rows of a global CSR as a RECTANGULAR local CSR: own rows x
+    extended columns (own planes + one halo plane per side).  Row order and
+    each row's entry order are the global ones, so per-row CSR-order sums are
+    the reference's."""
+    row_ptr = np.asarray(row_ptr, dtype=np.int64)
+    g0, g1 = slab.global_rows
+    a, b = int(row_ptr[g0]), int(row_ptr[g1])
+    cols = np.asarray(col_idx[a:b], dtype=np.int64) - slab.h0
+    if cols.size and (cols.min() < 0 or cols.max() >= slab.next_):
+        raise ValueError("slab_rows: a row reaches beyond the one-plane halo")
+    rp = (row_ptr[g0:g1 + 1] - a).astype(np.int32)
+    return rp, cols.astype(np.int32), [np.asarray(v[a:b]) for v in vals]
+
+
+def slab_factor(factor, slab: Slab):
+    """Extended-square local copy of one global ILU factor (row_ptr, col_idx,
+    vals, diag_pos): own rows keep their entries (columns shifted into the
+    local space), halo rows become unit rows (diagonal 1, no off-diagonals),
+    so a substitution copies the neighbour's values placed in their rhs
+    slots exactly (integer: trunc(y / 1) = y; FP64: y / 1.0 = y)."""
+    rp, ci, v, dp = (np.asarray(a) for a in factor)
+    rp = rp.astype(np.int64)
+    g0, g1 = slab.global_rows
+    a, b = int(rp[g0]), int(rp[g1])
+    own_cols = ci[a:b].astype(np.int64) - slab.h0
+    if own_cols.size and (own_cols.min() < 0 or own_cols.max() >= slab.next_):
+        raise ValueError("slab_factor: a factor row reaches beyond the one-plane halo")
+    nl, o0, o1 = slab.next_, slab.own0, slab.own1
+    counts = np.ones(nl, dtype=np.int64)
+    counts[o0:o1] = np.diff(rp[g0:g1 + 1])
+    lrp = np.zeros(nl + 1, dtype=np.int64)
+    np.cumsum(counts, out=lrp[1:])
+    nnz = int(lrp[-1])
+    lci = np.empty(nnz, dtype=np.int32)
+    lv = np.empty(nnz, dtype=np.int64)
+    ldp = np.empty(nl, dtype=np.int32)
+    halo = np.r_[np.arange(0, o0), np.arange(o1, nl)].astype(np.int64)
+    lci[lrp[halo]] = halo
+    lv[lrp[halo]] = 1
+    ldp[halo] = lrp[halo]
+    s0 = int(lrp[o0])
+    lci[s0:s0 + (b - a)] = own_cols
+    lv[s0:s0 + (b - a)] = np.asarray(v[a:b], dtype=np.int64)
+    ldp[o0:o1] = (np.asarray(dp[g0:g1], dtype=np.int64) - rp[g0:g1]) + lrp[o0:o1]
+    return lrp.astype(np.int32), lci, lv, ldp
+
+
+def shard_problem(be, slab: Slab, row_ptr, col_idx, comp, alphas, a_fp_vals, factors=None) -> dict:
+    """The rank's inputs of solve_sharded from the global SplitMatrix (comp,
+    alphas over row_ptr/col_idx), the FP64 matrix values on the same pattern,
+    and optionally the global integer ILU factors (lower, upper)."""
+    comp = [np.asarray(c) for c in np.atleast_2d(comp)]
+    rp, ci, vals = slab_rows(row_ptr, col_idx, comp + [np.asarray(a_fp_vals)], slab)
+    sp, af = be.upload_rows(rp, ci, np.stack(vals[:-1]), alphas, vals[-1])
+    ilu = None
+    if factors is not None:
+        ilu = be.upload_factors(slab_factor(factors[0], slab), slab_factor(factors[1], slab))
+    return dict(split=sp, csrf=af, ilu=ilu, ncomp=len(comp))
+
+
+@dataclass
+class ShardedReport:
+    """SolveReport (refine.hpp:36-47) of a partitioned solve (identical on every rank)."""
+    converged: bool = False
+    refinements: int = 0
+    total_inner_iterations: int = 0
+    inner_dims: List[int] = field(default_factory=list)
+    relres_history: List[float] = field(default_factory=list)
+    gamma_history: List[float] = field(default_factory=list)
+    overflow_per_restart: List[int] = field(default_factory=list)
+    overflow_total: int = 0
+    overflow_exact: bool = True
+
+
+class _Comm:
+    """The rank's exchanges (torch.distributed: NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, slab: Slab, dist, group=None):
+        self.s, self.d, self.g = slab, dist, group
+        self.rank, self.world = slab.rank, slab.world
+
+    def sum_(self, t):
+        if self.world > 1:
+            self.d.all_reduce(t, op=self.d.ReduceOp.SUM, group=self.g)
+
+    def max_(self, t):
+        if self.world > 1:
+            self.d.all_reduce(t, op=self.d.ReduceOp.MAX, group=self.g)
+
+    def send(self, t, dst):
+        self.d.send(t.contiguous(), dst, group=self.g)
+
+    def recv(self, t, src):
+        self.d.recv(t, src, group=self.g)
+
+    def bcast(self, t, src):
+        if self.world > 1:
+            self.d.broadcast(t, src, group=self.g)
+
+    def halo(self, own, ext):
+        halo_exchange(self.s, own, ext, self.d, self.g)
+
+
+def _validate_cycle(m: int, f: int, depth: int, ncomp: int, sh) -> None:
+    """run_cycle's argument checks, same order and texts (gmres_int.cpp:47-52,
+    fxp.hpp:24-27, fxp.cpp:106-127)."""
+    if m < 1:
+        raise ValueError("run_cycle: m must be >= 1")
+    if depth < 0 or depth > ncomp - 1:
+        raise ValueError("run_cycle: splitting depth out of range")
+    if f < 0 or f > 62:
+        raise ValueError("QFormat: frac_bits must be in [0, 62]")
+    for name, b in (("dot_b1", sh.dot_b1), ("dot_b2", sh.dot_b2), ("axpy_b1", sh.axpy_b1),
+                    ("norm_b1", sh.norm_b1), ("div_b1", sh.div_b1), ("div_b2", sh.div_b2),
+                    ("givens_b2", sh.givens_b2), ("rot_b", sh.rot_b)):
+        if b < 0 or b > 62:
+            raise ValueError(f"ShiftPlan: {name} out of range")
+    if sh.dot_b1 + sh.dot_b2 > f:
+        raise ValueError("ShiftPlan: dot shifts exceed frac_bits")
+    if sh.axpy_b1 > f:
+        raise ValueError("ShiftPlan: axpy shift exceeds frac_bits")
+    if 2 * (f - sh.norm_b1) > 62:
+        raise ValueError("ShiftPlan: norm accumulator exceeds 62 fractional bits")
+    if sh.div_b1 + sh.div_b2 > f + 62:
+        raise ValueError("ShiftPlan: division shifts out of range")
+
+
+def solve_sharded(be, slab: Slab, mats: dict, b_own, cfg, dist, group=None, s_schedule=None):
+    """solve() (refine.cpp:21-106, fixed-point engine) on this rank's rows.
+
+    be:   rank-local backend (CudaSlabBackend: the product's kernels through
+          the C ABI; tests drive the same code with a CPU restatement)
+    mats: {'split': own rows x ext cols SplitMatrix, 'csrf': the same for
+          A_fp, 'ilu': extended-square local factors or None, 'ncomp': int}
+    b_own: the rank's rows of b; cfg: RefineConfig-like (tol,
+          max_refinements, m, frac_bits, s, checked, shifts).
+    Returns (x_own, ShardedReport); every rank returns the same report."""
+    comm = _Comm(slab, dist, group)
+    be.sync()  # inputs produced on other streams are complete
+    n, nx, P = slab.n_own, slab.next_, slab.plane
+    o0, o1 = slab.own0, slab.own1
+    rank, world = slab.rank, slab.world
+    M = max(cfg.m, 1)
+    f, sh, checked = cfg.frac_bits, cfg.shifts, bool(cfg.checked)
+    pre = mats.get("ilu")
+    st = be.state(M)
+    x_ext = be.zeros(nx, "f64")
+    x_own = x_ext[o0:o1]
+    r = be.zeros(n, "f64")
+    t_ext = be.zeros(nx, "f64")
+    u_ext = be.zeros(nx, "f64")
+    r0 = be.zeros(n, "f64")
+    basis = be.zeros((M + 1, n), "i64")
+    v_ext = be.zeros(nx, "i64")
+    y_ext = be.zeros(nx, "i64")
+    z_ext = be.zeros(nx, "i64")
+    q_ext = be.zeros(nx, "i64")
+    w_plain = be.zeros(n, "i64")
+    chain = be.view(st, "chain")
+
+    def norm2_relay(v, mode):
+        """norm2 (split.cpp:45-49) over the global vector: one sequential chain
+        through the ranks in order, then finished (sqrt) on every rank."""
+        with be.stream():
+            if rank > 0:
+                comm.recv(chain[1:2], rank - 1)
+            be.norm2(st, v, chain[1:2] if rank > 0 else None, chain[0:1], 5)
+            if rank < world - 1:
+                comm.send(chain[0:1], rank + 1)
+            chain[2:3].copy_(chain[0:1])
+            comm.bcast(chain[2:3], world - 1)
+            be.norm2(st, v[:0], chain[2:3], None, mode)
+
+    def tri_pipeline(fac_fp, src_ext, mid_ext, dst_ext, j=0):
+        """forward (ranks in order) then backward (reverse order) substitution
+        of the global factors; src_ext's own rows hold the rhs."""
+        with be.stream():
+            if rank > 0:
+                comm.recv(src_ext[:o0], rank - 1)
+            be.tri(st, pre, False, src_ext, mid_ext, fac_fp, j, checked)
+            if rank < world - 1:
+                comm.send(mid_ext[o1 - P:o1], rank + 1)
+                comm.recv(mid_ext[o1:], rank + 1)
+            be.tri(st, pre, True, mid_ext, dst_ext, fac_fp, j, checked)
+            if rank > 0:
+                comm.send(dst_ext[o0:o0 + P], rank - 1)
+
+    def fetch():
+        """synchronise, read the scalars; a device error on any rank is raised on all"""
+        err = None
+        try:
+            info = be.fetch(st)
+        except (ArithmeticError, ValueError, RuntimeError, OverflowError) as e:
+            err, info = e, None
+        code = be.host_i64([0 if err is None else _err_code(err)])
+        comm.max_(code)
+        c = int(code[0])
+        if c:
+            if err is not None:
+                raise err
+            raise _ERR_TYPES.get(c, RuntimeError)("error raised on another rank")
+        return info
+
+    rep = ShardedReport()
+    with be.stream():
+        be.reset(st)
+    norm2_relay(b_own, 1)  # ||b|| (residual_fp's denominator)
+
+    def residual():
+        with be.stream():
+            comm.halo(x_own, x_ext)
+            be.residual(st, mats["csrf"], x_ext, b_own, r)
+            comm.max_(be.view(st, "rmax"))
+        norm2_relay(r, 2)
+        return fetch()
+
+    info = residual()
+    relnorm = info.relnorm
+    rep.relres_history.append(relnorm)
+    ncomp = mats["ncomp"]
+    k = 0
+    while k < cfg.max_refinements and relnorm >= cfg.tol:
+        gamma = info.gamma
+        if gamma == 0.0:
+            break
+        depth = s_schedule(k) if s_schedule is not None else cfg.s
+        _validate_cycle(cfg.m, f, depth, ncomp, sh)
+        # ---- one int-GMRES(m) cycle on b_k = r / gamma, x0 = 0
+        with be.stream():
+            be.begin(st, f)
+            if pre is not None:
+                be.scale(st, r, t_ext[o0:o1])
+        if pre is not None:
+            tri_pipeline(True, t_ext, u_ext, t_ext)
+            r0_own = t_ext[o0:o1]
+        else:
+            with be.stream():
+                be.scale(st, r, r0)
+            r0_own = r0
+        norm2_relay(r0_own, 3)
+        with be.stream():
+            be.encode(st, r0_own, basis[0], f)
+        for j in range(M):
+            with be.stream():
+                comm.halo(basis[j], v_ext)
+                if pre is not None:
+                    be.spmv(st, mats["split"], depth, v_ext, y_ext[o0:o1], j, checked)
+            if pre is not None:
+                tri_pipeline(False, y_ext, z_ext, q_ext, j)
+                w = q_ext[o0:o1]
+            else:
+                with be.stream():
+                    be.spmv(st, mats["split"], depth, v_ext, w_plain, j, checked)
+                w = w_plain
+            with be.stream():
+                red = be.view(st, "red", j)
+                for i in range(j + 2):
+                    be.mgs_pass(st, j, i, w, basis[i - 1] if i > 0 else None, basis[i] if i <= j else None,
+                                f, sh, checked)
+                    comm.sum_(red[3 * i:3 * i + 3])
+                if checked:
+                    comm.sum_(be.view(st, "lcnt", j))
+                be.step(st, j, f, sh, w, checked)
+                be.vec_div(st, j, w, basis[j + 1], f, sh, checked)
+        with be.stream():
+            if checked:
+                comm.sum_(be.view(st, "vcnt"))
+            be.finish(st, f, basis, x_own)
+        info = fetch()
+        dim = info.dim
+        if info.add_inexact:
+            rep.overflow_exact = False
+        if dim == 0:
+            break
+        rep.refinements = k + 1
+        rep.total_inner_iterations += dim
+        rep.inner_dims.append(dim)
+        rep.gamma_history.append(gamma)
+        rep.overflow_per_restart.append(int(info.overflows))
+        rep.overflow_total += int(info.overflows)
+        info = residual()
+        relnorm = info.relnorm
+        rep.relres_history.append(relnorm)
+        k += 1
+    rep.converged = relnorm < cfg.tol
+    return x_own, rep
+
+
+_ERR_TYPES = {1: ValueError, 2: ArithmeticError, 3: OverflowError, 4: RuntimeError}
+
+
+def _err_code(e) -> int:
+    for code, t in ((3, OverflowError), (2, ArithmeticError), (1, ValueError), (4, RuntimeError)):
+        if isinstance(e, t):
+            return code
+    return 4

@@ -112,3 +112,127 @@ def test_sharded_spmv_mgs_matches_oracle(oracle, world):
         assert h == D.fx_dot_finalize(int(acc[i]), 30, 16, 0)
         w = oracle.fx_axpy_sub(w, h, bfull[i], 30, 16)
     assert np.array_equal(wg, w)
+
+
+# ---------------------------------------------------------------------------
+# the whole partitioned solve (dist.solve_sharded) vs the single-process oracle
+def _problem(kind, g, oracle):
+    from workloads import gen
+    if kind == "27pt_ilu":
+        rp, ci, v = gen.stencil27(g, 5)
+    else:
+        rp, ci, v = gen.upwind_3d(g, 20.0)
+    n = len(rp) - 1
+    A = oracle.csrf(rp, ci, v)
+    alpha = 32 if kind == "27pt_ilu" else 16
+    vals, scale = oracle.row_scale(A, alpha)
+    comp, al, _ = oracle.build_split(vals, alpha, 1 if kind == "27pt_ilu" else 2)
+    fac = oracle.factorize_split_cast(oracle.csrf(rp, ci, vals)) if kind == "27pt_ilu" else None
+    b = gen.spmv_np(rp, ci, v, gen.uniform(17, n)) / scale
+    return rp, ci, vals, comp, al, fac, b
+
+
+def _solve_worker(rank, world, port, kind, g, m, s, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.ffi import Oracle
+        from tests.dist_np import OracleSlabBackend
+        import paper_2009_07495_b200 as igm
+        O = Oracle()
+        rp, ci, vals, comp, al, fac, b = _problem(kind, g, O)
+        sl = D.make_slab(g, g * g, rank, world)
+        be = OracleSlabBackend(O)
+        mats = D.shard_problem(be, sl, rp, ci, comp, al, vals, fac)
+        g0, g1 = sl.global_rows
+        plan = igm.ShiftPlan.default_preconditioned(30) if fac is not None else igm.ShiftPlan.default_unpreconditioned(30)
+        cfg = igm.RefineConfig(tol=1e-10, max_refinements=30, m=m, frac_bits=30, s=s, checked=True, shifts=plan)
+        x, rep = D.solve_sharded(be, sl, mats, torch.from_numpy(b[g0:g1].copy()), cfg, dist)
+        parts = [None] * world
+        dist.all_gather_object(parts, (g0, x.numpy().copy(), rep))
+        if rank == 0:
+            q.put(sorted(parts, key=lambda t: t[0]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind,world", [("27pt_ilu", 2), ("27pt_ilu", 3), ("7pt_plain", 2)])
+def test_sharded_solve_matches_oracle(oracle, kind, world):
+    """World 2/3 gloo run of dist.solve_sharded (halo planes, exact u64 pass
+    sums, relayed norm2 chain, rank-pipelined global ILU) against the
+    single-process oracle solve: every x word, the relative-residual history,
+    the inner dimensions and the gammas bit-identical."""
+    g, m = 6, 8
+    s = 0 if kind == "27pt_ilu" else 1
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_solve_worker, args=(r, world, port, kind, g, m, s, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    x = np.concatenate([p[1] for p in parts])
+    rep = parts[0][2]
+    assert all(p[2] == rep for p in parts)  # replicated report
+    from oracle.ffi import Shifts
+    from tests.cases import PRE, UNPRE
+    rp, ci, vals, comp, al, fac, b = _problem(kind, g, oracle)
+    sp, af = oracle.split(rp, ci, comp, al), oracle.csrf(rp, ci, vals)
+    il = oracle.ilu(*fac) if fac is not None else None
+    xo, ro = oracle.solve(sp, af, b, 1e-10, 30, m, 30, s, Shifts(*(PRE if fac is not None else UNPRE)),
+                          precond=il)
+    assert rep.converged and ro["converged"]
+    assert rep.relres_history == ro["relres_history"]
+    assert rep.inner_dims == ro["inner_dims"] and rep.gamma_history == ro["gamma_history"]
+    assert rep.overflow_total == ro["overflow_total"] == 0
+    assert np.array_equal(x, xo)
+
+
+def run_sharded_threads(oracle, make_backend, kind, g, m, s, world, to_dev=lambda t: t):
+    """dist.solve_sharded on `world` in-process ranks (tests/thread_comm.py);
+    returns (x, reports, problem)."""
+    from tests.thread_comm import run_ranks
+    import paper_2009_07495_b200 as igm
+    prob = _problem(kind, g, oracle)
+    rp, ci, vals, comp, al, fac, b = prob
+    plan = igm.ShiftPlan.default_preconditioned(30) if fac is not None else igm.ShiftPlan.default_unpreconditioned(30)
+    cfg = igm.RefineConfig(tol=1e-10, max_refinements=30, m=m, frac_bits=30, s=s, checked=True, shifts=plan)
+
+    def rank_fn(rank, comm):
+        be = make_backend(rank)
+        sl = D.make_slab(g, g * g, rank, world)
+        mats = D.shard_problem(be, sl, rp, ci, comp, al, vals, fac)
+        g0, g1 = sl.global_rows
+        x, rep = D.solve_sharded(be, sl, mats, to_dev(torch.from_numpy(b[g0:g1].copy())), cfg, comm)
+        return g0, x.cpu().numpy().copy(), rep
+
+    parts = sorted(run_ranks(world, rank_fn), key=lambda t: t[0])
+    return np.concatenate([p[1] for p in parts]), [p[2] for p in parts], prob
+
+
+def check_sharded_vs_oracle(oracle, x, reps, prob, m, s):
+    from oracle.ffi import Shifts
+    from tests.cases import PRE, UNPRE
+    rp, ci, vals, comp, al, fac, b = prob
+    rep = reps[0]
+    assert all(r == rep for r in reps)
+    sp, af = oracle.split(rp, ci, comp, al), oracle.csrf(rp, ci, vals)
+    il = oracle.ilu(*fac) if fac is not None else None
+    xo, ro = oracle.solve(sp, af, b, 1e-10, 30, m, 30, s, Shifts(*(PRE if fac is not None else UNPRE)),
+                          precond=il)
+    assert rep.converged and ro["converged"] and rep.refinements >= 2
+    assert rep.relres_history == ro["relres_history"]
+    assert rep.inner_dims == ro["inner_dims"] and rep.gamma_history == ro["gamma_history"]
+    assert rep.overflow_total == ro["overflow_total"]
+    assert np.array_equal(x, xo)
+
+
+def test_sharded_solve_thread_ranks_oracle_backend(oracle):
+    """The in-process rank harness the GPU test uses (threads + host queues)
+    gives the same bit-exact solve as the gloo processes."""
+    from tests.dist_np import OracleSlabBackend
+    x, reps, prob = run_sharded_threads(oracle, lambda r: OracleSlabBackend(oracle), "27pt_ilu", 6, 8, 0, 3)
+    check_sharded_vs_oracle(oracle, x, reps, prob, 8, 0)

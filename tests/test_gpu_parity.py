@@ -611,3 +611,25 @@ def test_cpp_experiment(gpu, reference, tmp_path):
             refl = ref_text.splitlines()
             assert abs(len(ours) - len(refl)) <= 1 and ours[-1].split()[:4] == refl[-1].split()[:4]
             assert ours[-1].endswith("converged=yes") and refl[-1].endswith("converged=yes")
+
+
+@pytest.mark.parametrize("kind,g,world", [("27pt_ilu", 12, 1), ("27pt_ilu", 12, 3), ("7pt_plain", 10, 2)])
+def test_sharded_solve_cuda_backend(gpu, oracle, kind, g, world):
+    """dist.solve_sharded through the product kernels (igm_dc_* entries: rank
+    local SpMV / MGS passes / replicated scalar step / vec_div / pipelined
+    global ILU / relayed norm2 / residual) on `world` ranks sharing this GPU
+    as threads with their own contexts and streams (exchanges are host copies:
+    no kernel waits on another rank) == the single-process oracle solve, bit
+    for bit.  Multi-process gloo runs of the same driver: tests/test_dist.py."""
+    import torch
+    from tests.test_dist import run_sharded_threads, check_sharded_vs_oracle
+    from paper_2009_07495_b200 import dist as D
+    devs = {}
+
+    def make_backend(rank):
+        devs[rank] = gpu.Device(0)
+        return D.CudaSlabBackend(gpu, devs[rank])
+
+    m, s = 10, (0 if kind == "27pt_ilu" else 1)
+    x, reps, prob = run_sharded_threads(oracle, make_backend, kind, g, m, s, world, to_dev=lambda t: t.cuda())
+    check_sharded_vs_oracle(oracle, x, reps, prob, m, s)
