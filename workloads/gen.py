@@ -276,3 +276,92 @@ def upwind_3d_slab(g: int, beta: float, z0: int, z1: int):
         val[pos] = c
         cur[idx] += 1
     return row_ptr.astype(np.int32), col, val, h0, own0, own1
+
+
+def stencil27_lean(g: int, seed: int):
+    """stencil27() for large grids (config 4: 256^3) without n x 27
+    temporaries: the same arrays, entry for entry (rows filled offset by
+    offset in ascending column order; the diagonal's row sum accumulated in
+    the same left-to-right order as stencil27's bincount)."""
+    n = g ** 3
+    p = g * g
+    r = np.arange(n, dtype=np.int64)
+    i = (r % g).astype(np.int16)
+    j = ((r // g) % g).astype(np.int16)
+    k = (r // p).astype(np.int16)
+    del r
+    offs = [(di, dj, dk) for dk in (-1, 0, 1) for dj in (-1, 0, 1) for di in (-1, 0, 1)]
+
+    def ok(di, dj, dk):
+        m = np.ones(n, dtype=bool)
+        for c, d in ((i, di), (j, dj), (k, dk)):
+            if d < 0:
+                m &= c > 0
+            elif d > 0:
+                m &= c < g - 1
+        return m
+
+    counts = np.zeros(n, dtype=np.int32)
+    for (di, dj, dk) in offs:
+        counts += ok(di, dj, dk)
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=row_ptr[1:])
+    del counts
+    nnz = int(row_ptr[-1])
+    col = np.empty(nnz, dtype=np.int32)
+    val = np.empty(nnz, dtype=np.float64)
+    cur = row_ptr[:-1].copy()
+    rs = np.zeros(n)
+    dpos = None
+    for o, (di, dj, dk) in enumerate(offs):
+        m = ok(di, dj, dk)
+        idx = np.nonzero(m)[0]
+        pos = cur[idx]
+        col[pos] = (idx + (dk * p + dj * g + di)).astype(np.int32)
+        if (di, dj, dk) == (0, 0, 0):
+            val[pos] = 0.0
+            dpos = pos
+        else:
+            s = di + dj + dk
+            sig = 1.0 if s < 0 else (-1.0 if s > 0 else 0.0)
+            u = uniform(seed, n, 0.0, 1.0, offset=o * n)
+            v = -u[idx] * (1.0 + 0.1 * sig)
+            val[pos] = v
+            a = np.zeros(n)
+            a[idx] = np.abs(v)
+            rs += a
+            del u, v, a
+        cur[idx] += 1
+        del m, idx, pos
+    val[dpos] = 1.05 * rs
+    return row_ptr.astype(np.int32), col, val
+
+
+def random_band_fast(n: int, seed: int, band: int = 2, extra: int = 10):
+    """random_band() vectorised (config 3 at n = 1M): the same matrix.  Per
+    row the candidates rnd[i, :] are taken in order, skipping band members
+    and repeats, until `extra` were added."""
+    cand = uniform_int(seed, n * extra * 2, 0, n - 1).reshape(n, extra * 2)
+    rows = np.arange(n, dtype=np.int64)[:, None]
+    new = np.abs(cand - rows) > band
+    for t in range(1, cand.shape[1]):
+        new[:, t] &= ~np.any(cand[:, :t] == cand[:, t:t + 1], axis=1)
+    new &= np.cumsum(new, axis=1) <= extra
+    bandc = rows + np.arange(-band, band + 1)[None, :]
+    inb = (bandc >= 0) & (bandc < n)
+    big = np.iinfo(np.int64).max
+    allc = np.concatenate([np.where(inb, bandc, big), np.where(new, cand, big)], axis=1)
+    allc.sort(axis=1)
+    keep = allc != big
+    counts = keep.sum(axis=1)
+    rp = np.zeros(n + 1, dtype=np.int32)
+    rp[1:] = np.cumsum(counts)
+    ci = allc[keep].astype(np.int32)
+    del allc, keep, cand, new
+    offd = normal(seed ^ 0xABCDEF, len(ci))
+    rr = np.repeat(np.arange(n), np.diff(rp))
+    diag = ci == rr
+    offd[diag] = 0.0
+    rs = np.bincount(rr, weights=np.abs(offd), minlength=n)
+    offd[diag] = 1.2 * rs
+    return rp, ci, offd
