@@ -351,6 +351,26 @@ igm_status igm_factorize_split_cast(int n, const int* row_ptr,
                                     int* u_row_ptr, int* u_col_idx,
                                     int64_t* u_vals, int* u_diag_pos);
 
+/* ---- device-side setup -------------------------- *
+ * The same three functions on the GPU, bit-identical to the host versions
+ * above (per-row / per-entry IEEE sequences in the reference's order; the
+ * ILU(0) factorisation runs one DAG level per launch, a thread per row).
+ * Array arguments may be host or device pointers; outputs are written where
+ * they point.  Errors (types and texts) are the reference's; the reported row
+ * is the first one the sequential code would meet. */
+/* replaces intgmres::row_scale (split.cpp:61-79) */
+igm_status igm_row_scale_dev(igm_ctx* ctx, int n, const int* row_ptr, const double* vals, int alpha_a,
+                             double* vals_out, double* scale_out);
+/* replaces intgmres::build_split (split.cpp:90-135); alphas_out (host) holds
+ * max_components ints, comp_vals_out max_components*nnz */
+igm_status igm_build_split_dev(igm_ctx* ctx, int nnz, const double* vals, int alpha_a, int max_components,
+                               int64_t* comp_vals_out, int* alphas_out, int* ncomp_out, int* exact_out);
+/* replaces intgmres::split_cast(factorize_ilu0(a)) (ilu.cpp:25-120) */
+igm_status igm_factorize_split_cast_dev(igm_ctx* ctx, int n, const int* row_ptr, const int* col_idx,
+                                        const double* vals, int* l_row_ptr, int* l_col_idx, int64_t* l_vals,
+                                        int* l_diag_pos, int* u_row_ptr, int* u_col_idx, int64_t* u_vals,
+                                        int* u_diag_pos);
+
 #ifdef __cplusplus
 }
 #endif

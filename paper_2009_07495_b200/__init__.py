@@ -582,3 +582,67 @@ def factorize_split_cast(row_ptr, col_idx, vals):
                                           p(urp), p(uci), p(uv), p(udp)))
     nl, nu = int(lrp[-1]), int(urp[-1])
     return (lrp, lci[:nl].copy(), lv[:nl].copy(), ldp), (urp, uci[:nu].copy(), uv[:nu].copy(), udp)
+
+
+# ---------------------------------------------------------------- device setup
+# row_scale / build_split / split_cast(factorize_ilu0)
+# on the GPU (igm_*_dev), bit-identical to the host versions above.  numpy
+# inputs give numpy outputs; torch CUDA tensors stay on the device.
+def _alloc_like(t, n, dtype):
+    if _is_torch(t) and t.is_cuda:
+        import torch
+        tdt = {np.int64: torch.int64, np.float64: torch.float64, np.int32: torch.int32}[dtype]
+        return torch.empty(n, dtype=tdt, device=t.device)
+    return np.empty(n, dtype=dtype)
+
+
+def _vp(a, dtype):
+    return _ptr(a, dtype)
+
+
+def row_scale_device(row_ptr, col_idx, vals, alpha_a: int, device: Optional[Device] = None):
+    dev = _dev(device)
+    n = (row_ptr.numel() if _is_torch(row_ptr) else len(row_ptr)) - 1
+    nnz = vals.numel() if _is_torch(vals) else len(vals)
+    rp, k1 = _vp(row_ptr, np.int32)
+    v, k2 = _vp(vals, np.float64)
+    out, scale = _alloc_like(vals, nnz, np.float64), _alloc_like(vals, n, np.float64)
+    po, k3 = _vp(out, np.float64)
+    ps, k4 = _vp(scale, np.float64)
+    _check(lib().igm_row_scale_dev(dev.h, n, rp, v, alpha_a, po, ps))
+    return out, scale
+
+
+def build_split_device(vals, alpha_a: int, max_components: int, device: Optional[Device] = None):
+    dev = _dev(device)
+    nnz = vals.numel() if _is_torch(vals) else len(vals)
+    mc = max(max_components, 1)
+    comp = _alloc_like(vals, mc * nnz, np.int64)
+    v, k1 = _vp(vals, np.float64)
+    pc, k2 = _vp(comp, np.int64)
+    alphas = np.zeros(mc, dtype=np.int32)
+    nc, ex = C.c_int(), C.c_int()
+    _check(lib().igm_build_split_dev(dev.h, nnz, v, alpha_a, max_components, pc,
+                                     C.c_void_p(alphas.ctypes.data), C.byref(nc), C.byref(ex)))
+    k = nc.value
+    return comp[:k * nnz].reshape(k, nnz), [int(a) for a in alphas[:k]], bool(ex.value)
+
+
+def factorize_split_cast_device(row_ptr, col_idx, vals, device: Optional[Device] = None):
+    """split_cast(factorize_ilu0(A)) on the device -> (lower, upper) tuples of
+    (row_ptr, col_idx, vals, diag_pos), trimmed to the factors' sizes."""
+    dev = _dev(device)
+    n = (row_ptr.numel() if _is_torch(row_ptr) else len(row_ptr)) - 1
+    nnz = col_idx.numel() if _is_torch(col_idx) else len(col_idx)
+    bufs = [_alloc_like(vals, n + 1, np.int32), _alloc_like(vals, nnz, np.int32), _alloc_like(vals, nnz, np.int64),
+            _alloc_like(vals, n, np.int32), _alloc_like(vals, n + 1, np.int32), _alloc_like(vals, nnz, np.int32),
+            _alloc_like(vals, nnz, np.int64), _alloc_like(vals, n, np.int32)]
+    ptrs = [_vp(b, b.dtype.type if isinstance(b, np.ndarray) else None)[0] if isinstance(b, np.ndarray)
+            else C.c_void_p(b.data_ptr()) for b in bufs]
+    rp, k1 = _vp(row_ptr, np.int32)
+    ci, k2 = _vp(col_idx, np.int32)
+    v, k3 = _vp(vals, np.float64)
+    _check(lib().igm_factorize_split_cast_dev(dev.h, n, rp, ci, v, *ptrs))
+    lrp, lci, lv, ldp, urp, uci, uv, udp = bufs
+    nl, nu = int(lrp[-1]), int(urp[-1])
+    return (lrp, lci[:nl], lv[:nl], ldp), (urp, uci[:nu], uv[:nu], udp)

@@ -168,6 +168,11 @@ SIGNATURES = [
                                  C.POINTER(Shifts), C.c_int]),
     ("igm_dc_finish", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_void_p]),
     ("igm_dc_fetch", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("igm_row_scale_dev", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
+                                    C.c_void_p]),
+    ("igm_build_split_dev", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
+                                      C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("igm_factorize_split_cast_dev", C.c_int, [C.c_void_p, C.c_int] + [C.c_void_p] * 11),
     ("igm_row_scale", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
                                 C.c_void_p]),
     ("igm_build_split", C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p,

@@ -10,6 +10,8 @@
 #include "schedule.hpp"
 
 #include <algorithm>
+#include <climits>
+#include <cub/cub.cuh>
 #include <cfloat>
 #include <chrono>
 #include <cmath>
@@ -1406,6 +1408,194 @@ igm_status igm_fp_cycle(igm_ctx* c, const igm_csrf* a, int m, const double* b, c
     ck(cudaMemcpyAsync(x_out, w.x, sizeof(double) * n,
                        is_device_ptr(x_out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st),
        "x");
+    ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+}  // extern "C"
+
+
+// ---- device-side setup (setup.cu) --------------------
+namespace {
+struct ErrRow {  // smallest offending row, reported by atomicMin
+  int* d = nullptr;
+  explicit ErrRow(cudaStream_t st) {
+    d = dalloc<int>(1);
+    const int big = INT_MAX;
+    ck(cudaMemcpyAsync(d, &big, sizeof(int), cudaMemcpyHostToDevice, st), "err init");
+  }
+  int get(cudaStream_t st) const {
+    int h = INT_MAX;
+    ck(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, st), "err D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+    return h;
+  }
+  ~ErrRow() { dfree(d); }
+};
+
+template <class T>
+std::vector<T> host_copy(const T* p, size_t count) {
+  return is_device_ptr(p) ? to_host(p, count) : std::vector<T>(p, p + count);
+}
+
+// exclusive sum of cnt[0..n) into out[0..n] (out[n] = total)
+void exclusive_sum(cudaStream_t st, int* cnt, int* out, int n) {
+  ck(cudaMemsetAsync(cnt + n, 0, sizeof(int), st), "memset");
+  size_t bytes = 0;
+  ck(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt, out, n + 1, st), "scan size");
+  void* tmp = dalloc<unsigned char>(std::max<size_t>(bytes, 1));
+  ck(cub::DeviceScan::ExclusiveSum(tmp, bytes, cnt, out, n + 1, st), "scan");
+  ck(cudaStreamSynchronize(st), "sync");
+  dfree(tmp);
+}
+}  // namespace
+
+extern "C" {
+
+igm_status igm_row_scale_dev(igm_ctx* c, int n, const int* row_ptr, const double* vals, int alpha_a,
+                             double* vals_out, double* scale_out) {
+  return guarded([&] {
+    need_ctx(c);
+    if (n < 0 || !row_ptr) fail(IGM_INVALID_ARGUMENT, "row_scale: bad arguments");
+    cudaStream_t st = c->stream;
+    int nnz = 0;
+    ck(cudaMemcpy(&nnz, row_ptr + n, sizeof(int), cudaMemcpyDefault), "nnz");
+    In<int> rp(row_ptr, n + 1, st);
+    In<double> v(vals, nnz, st);
+    Out<double> out(vals_out, nnz), sc(scale_out, n);
+    ErrRow err(st);
+    launch_row_scale(st, n, rp.d, v.d, alpha_a, out.d, sc.d, err.d);
+    const int bad = err.get(st);
+    if (bad != INT_MAX) fail(IGM_RUNTIME_ERROR, "row_scale: row " + std::to_string(bad) + " has no nonzero entry");
+    out.fetch(st);
+    sc.fetch(st);
+    ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+igm_status igm_build_split_dev(igm_ctx* c, int nnz, const double* vals, int alpha_a, int max_components,
+                               int64_t* comp_vals_out, int* alphas_out, int* ncomp_out, int* exact_out) {
+  return guarded([&] {
+    need_ctx(c);
+    if (max_components < 1) fail(IGM_INVALID_ARGUMENT, "build_split: need at least one component");
+    if (nnz < 0 || !alphas_out || !ncomp_out || !exact_out) fail(IGM_INVALID_ARGUMENT, "build_split: bad arguments");
+    cudaStream_t st = c->stream;
+    In<double> v(vals, nnz, st);
+    Out<i64> comp(comp_vals_out, static_cast<size_t>(max_components) * nnz);
+    double* rem = dalloc<double>(std::max(nnz, 1));
+    u64* mx = dalloc<u64>(1);
+    auto max_rem = [&](bool first, int alpha, i64* layer) {
+      ck(cudaMemsetAsync(mx, 0, sizeof(u64), st), "memset");
+      launch_split_layer(st, nnz, v.d, rem, alpha, layer, mx, first);
+      u64 h = 0;
+      ck(cudaMemcpyAsync(&h, mx, sizeof(u64), cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaStreamSynchronize(st), "sync");
+      double d;
+      std::memcpy(&d, &h, sizeof d);
+      return d;
+    };
+    std::vector<int> alphas{0};
+    double m = max_rem(true, 0, comp.d);
+    igm_status st_err = IGM_OK;
+    while (static_cast<int>(alphas.size()) < max_components) {
+      if (m == 0.0) break;
+      const int alpha = alpha_a - std::ilogb(m);
+      if (alpha <= alphas.back()) {
+        st_err = IGM_LOGIC_ERROR;
+        break;
+      }
+      m = max_rem(false, alpha, comp.d + alphas.size() * static_cast<size_t>(nnz));
+      alphas.push_back(alpha);
+    }
+    dfree(rem);
+    dfree(mx);
+    if (st_err != IGM_OK) fail(st_err, "build_split: exponents must increase");
+    comp.count = alphas.size() * static_cast<size_t>(nnz);
+    comp.fetch(st);
+    ck(cudaStreamSynchronize(st), "sync");
+    for (size_t l = 0; l < alphas.size(); ++l) alphas_out[l] = alphas[l];
+    *ncomp_out = static_cast<int>(alphas.size());
+    *exact_out = m == 0.0 ? 1 : 0;
+  });
+}
+
+igm_status igm_factorize_split_cast_dev(igm_ctx* c, int n, const int* rp_, const int* ci_, const double* vals,
+                                        int* lrp_o, int* lci_o, int64_t* lv_o, int* ldp_o, int* urp_o, int* uci_o,
+                                        int64_t* uv_o, int* udp_o) {
+  return guarded([&] {
+    need_ctx(c);
+    if (n < 0 || !rp_) fail(IGM_INVALID_ARGUMENT, "factorize_ilu0: bad arguments");
+    cudaStream_t st = c->stream;
+    // DAG levels of the lower pattern (index work on the host, O(nnz)):
+    // level(i) = 1 + max level(j) over j < i in row i
+    const std::vector<int> hrp = host_copy(rp_, static_cast<size_t>(n) + 1);
+    const int nnz = hrp[n];
+    const std::vector<int> hci = host_copy(ci_, static_cast<size_t>(nnz));
+    std::vector<int> lev(static_cast<size_t>(n), 0);
+    int nlev = n > 0 ? 1 : 0;
+    for (int i = 0; i < n; ++i) {
+      int l = 0;
+      for (int k = hrp[i]; k < hrp[i + 1]; ++k) {
+        const int j = hci[k];
+        if (j >= i) break;
+        l = std::max(l, lev[j] + 1);
+      }
+      lev[i] = l;
+      nlev = std::max(nlev, l + 1);
+    }
+    std::vector<int> off(static_cast<size_t>(nlev) + 1, 0), order(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) ++off[lev[i] + 1];
+    for (int l = 0; l < nlev; ++l) off[l + 1] += off[l];
+    {
+      std::vector<int> cur(off.begin(), off.end() - 1);
+      for (int i = 0; i < n; ++i) order[cur[lev[i]]++] = i;
+    }
+    In<int> rp(rp_, n + 1, st), ci(ci_, nnz, st);
+    In<double> v(vals, nnz, st);
+    int* rows = dupload(order.data(), order.size(), st);
+    double* lu = dalloc<double>(std::max(nnz, 1));
+    if (nnz) ck(cudaMemcpyAsync(lu, v.d, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, st), "lu");
+    int* diag = dalloc<int>(std::max(n, 1));
+    int* lcnt = dalloc<int>(n + 1);
+    int* ucnt = dalloc<int>(n + 1);
+    Out<int> lrp(lrp_o, n + 1), urp(urp_o, n + 1), ldp(ldp_o, n), udp(udp_o, n);
+    auto cleanup = [&] { dfree(rows); dfree(lu); dfree(diag); dfree(lcnt); dfree(ucnt); };
+    {
+      ErrRow e(st);
+      launch_ilu_pattern(st, n, rp.d, ci.d, diag, lcnt, ucnt, e.d);
+      const int bad = e.get(st);
+      if (bad != INT_MAX) {
+        cleanup();
+        fail(IGM_RUNTIME_ERROR,
+             "factorize_ilu0: row " + std::to_string(bad) + " has no diagonal entry in the pattern");
+      }
+    }
+    {
+      ErrRow e(st);
+      for (int l = 0; l < nlev; ++l) launch_ilu_level(st, off[l + 1] - off[l], rows + off[l], rp.d, ci.d, diag, lu, e.d);
+      const int bad = e.get(st);
+      if (bad != INT_MAX) {
+        cleanup();
+        fail(IGM_RUNTIME_ERROR, "factorize_ilu0: zero pivot in row " + std::to_string(bad));
+      }
+    }
+    exclusive_sum(st, lcnt, lrp.d, n);
+    exclusive_sum(st, ucnt, urp.d, n);
+    int nl = 0, nu = 0;
+    ck(cudaMemcpy(&nl, lrp.d + n, sizeof(int), cudaMemcpyDeviceToHost), "nl");
+    ck(cudaMemcpy(&nu, urp.d + n, sizeof(int), cudaMemcpyDeviceToHost), "nu");
+    Out<int> lci(lci_o, nl), uci(uci_o, nu);
+    Out<i64> lv(lv_o, nl), uv(uv_o, nu);
+    ErrRow e(st);
+    launch_split_cast(st, n, rp.d, ci.d, diag, lu, lrp.d, urp.d, lci.d, lv.d, ldp.d, uci.d, uv.d, udp.d, e.d);
+    const int bad = e.get(st);
+    cleanup();
+    if (bad != INT_MAX)
+      fail(IGM_RUNTIME_ERROR, "split_cast: diagonal entry of row " + std::to_string(bad) +
+                                  " truncates to zero; scale the matrix up before factorizing");
+    for (auto* o : {&lrp, &urp, &ldp, &udp, &lci, &uci}) o->fetch(st);
+    lv.fetch(st);
+    uv.fetch(st);
     ck(cudaStreamSynchronize(st), "sync");
   });
 }

@@ -189,6 +189,19 @@ void launch_arnoldi(cudaStream_t st, long long n, int j, long long S, const i64*
 void launch_basis_norms(cudaStream_t st, long long n, int nb, int f,
                         const i64* basis, void* scratch, double* out, Ctl* ctl);
 
+// device-side setup (setup.cu)
+void launch_row_scale(cudaStream_t st, int n, const int* rp, const double* v, int alpha, double* out,
+                      double* scale, int* err_row);
+void launch_split_layer(cudaStream_t st, long long nnz, const double* v, double* rem, int alpha, i64* comp,
+                        u64* mx_out, bool first);
+void launch_ilu_pattern(cudaStream_t st, int n, const int* rp, const int* ci, int* diag, int* lcnt, int* ucnt,
+                        int* err_row);
+void launch_ilu_level(cudaStream_t st, int cnt, const int* rows, const int* rp, const int* ci, const int* diag,
+                      double* lu, int* err_row);
+void launch_split_cast(cudaStream_t st, int n, const int* rp, const int* ci, const int* diag, const double* lu,
+                       const int* lrp, const int* urp, int* lci, i64* lv, int* ldp, int* uci, i64* uv, int* udp,
+                       int* err_row);
+
 int num_sms(int device);
 void tri_trace_setup(int tile, unsigned long long* buf);
 extern unsigned long long g_launches;  // kernels launched by this library

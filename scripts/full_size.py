@@ -43,6 +43,27 @@ def setup(rp, ci, v, bh, alpha, ncomp, ilu):
     return dict(vals=vals, scale=scale, comp=comp, al=al, fac=fac, b=bh / scale, setup_s=time.time() - t)
 
 
+def dev_setup(rp, ci, v, P, alpha, ncomp, ilu):
+    """device-side setup (8(f) row 1) from device-resident inputs: timing and
+    array-for-array equality with the host setup P"""
+    import torch
+    td = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    rpd, cid, vd = td(rp), td(ci), td(v)
+    torch.cuda.synchronize()
+    t = time.time()
+    vals, scale = igm.row_scale_device(rpd, cid, vd, alpha)
+    comp, al, _ = igm.build_split_device(vals, alpha, ncomp)
+    fac = igm.factorize_split_cast_device(rpd, cid, vals) if ilu else None
+    torch.cuda.synchronize()
+    dt = time.time() - t
+    same = (np.array_equal(vals.cpu().numpy(), P["vals"]) and np.array_equal(scale.cpu().numpy(), P["scale"])
+            and al == list(P["al"]) and np.array_equal(comp.cpu().numpy(), np.atleast_2d(P["comp"])))
+    if ilu:
+        for a, b in zip(fac[0] + fac[1], list(P["fac"][0]) + list(P["fac"][1])):
+            same = same and np.array_equal(a.cpu().numpy(), np.asarray(b))
+    return dict(device_setup_s=dt, device_setup_bit_exact=bool(same))
+
+
 def gpu_solve(rp, ci, P, m, shifts, tol=1e-10, reps=2):
     S = igm.SplitMatrix(rp, ci, P["comp"], P["al"])
     A = igm.CsrMatrixF(rp, ci, P["vals"])
@@ -60,6 +81,22 @@ def gpu_solve(rp, ci, P, m, shifts, tol=1e-10, reps=2):
         dt = time.time() - t
         best = dt if best is None else min(best, dt)
     return S, A, F, x.cpu().numpy() if hasattr(x, "cpu") else x, rep, best
+
+
+def class_times(S, A, F, P, m, shifts):
+    """per-kernel-class device time of one more solve (CUDA events, igm_profile_*)"""
+    import torch
+    from paper_2009_07495_b200._capi import KCLASS_NAMES
+    cfg = igm.RefineConfig(tol=1e-10, max_refinements=100, m=m, frac_bits=30, shifts=igm.ShiftPlan(*shifts),
+                           checked=True)
+    bd = torch.from_numpy(P["b"]).cuda()
+    igm.lib().igm_profile_enable(1)
+    igm.solve(S, A, bd, cfg, precond=F)
+    igm.lib().igm_profile_enable(0)
+    kms = np.zeros(len(KCLASS_NAMES))
+    kcnt = np.zeros(len(KCLASS_NAMES), np.uint64)
+    igm.lib().igm_profile_collect(kms.ctypes.data_as(igm._capi.f64p), kcnt.ctypes.data_as(igm._capi.u64p))
+    return {nm: [round(float(kms[i]), 3), int(kcnt[i])] for i, nm in enumerate(KCLASS_NAMES) if kcnt[i]}
 
 
 def report(rep):
@@ -94,6 +131,7 @@ def cfg2(O):
     bh = gen.spmv_np(rp, ci, v, gen.uniform(gen.SEED_BASE ^ 2, n))
     P = setup(rp, ci, v, bh, 32, 1, True)
     out = dict(config="cfg2", n=n, nnz=int(rp[-1]), setup_s=P["setup_s"])
+    out.update(dev_setup(rp, ci, v, P, 32, 1, True))
     full_parity(out, "cfg2", rp, ci, P, 30, PRE, O)
     return out
 
@@ -119,9 +157,13 @@ def cfg4(O, g=256):
     P = setup(rp, ci, v, bh, 32, 1, True)
     out = dict(config=f"cfg4 ({g}^3 27-pt)", n=n, nnz=int(rp[-1]), nnz_l=int(P["fac"][0][0][-1]),
                gen_s=gen_s, setup_s=P["setup_s"])
+    out.update(dev_setup(rp, ci, v, P, 32, 1, True))
+    t = time.time()
     S, A, F, x, rep, dt = gpu_solve(rp, ci, P, 30, PRE, reps=1)
+    out["upload_and_solve_s"] = time.time() - t
     out.update(gpu=report(rep), gpu_solve_s=dt, gpu_iters_per_s=rep.total_inner_iterations / dt,
-               levels=[F.levels(False), F.levels(True)])
+               levels=[F.levels(False), F.levels(True)], schedule=[F.schedule_info(False), F.schedule_info(True)])
+    out["breakdown_ms"] = class_times(S, A, F, P, 30, PRE)
     # property: independent FP64 residual of the GPU's x on the scaled system
     r = P["b"] - gen.spmv_np(rp, ci, P["vals"], x)
     out["indep_relres"] = float(np.linalg.norm(r) / np.linalg.norm(P["b"]))

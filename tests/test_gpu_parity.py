@@ -633,3 +633,53 @@ def test_sharded_solve_cuda_backend(gpu, oracle, kind, g, world):
     m, s = 10, (0 if kind == "27pt_ilu" else 1)
     x, reps, prob = run_sharded_threads(oracle, make_backend, kind, g, m, s, world, to_dev=lambda t: t.cuda())
     check_sharded_vs_oracle(oracle, x, reps, prob, m, s)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2_16", "cfg4_12", "cfg3_small", "split_s3", "ilu_random"])
+def test_device_setup_bit_exact(gpu, oracle, name):
+    """Device-side setup (igm_row_scale_dev / igm_build_split_dev /
+    igm_factorize_split_cast_dev) == the oracle's
+    restatement of row_scale, build_split and split_cast(factorize_ilu0),
+    array for array (host numpy and device tensor arguments)."""
+    import torch
+    from tests.cases import CASES, build_case
+    c = build_case(name, oracle)
+    rp, ci, v = c["rp"], c["ci"], c["v"]
+    vals, scale = gpu.row_scale_device(rp, ci, v, c["alpha"])
+    assert np.array_equal(vals, c["vals"]) and np.array_equal(scale, c["scale"])
+    comp, al, ex = gpu.build_split_device(vals, c["alpha"], CASES[name]["ncomp"])
+    assert al == list(c["alphas"]) and np.array_equal(comp, np.atleast_2d(c["comp"]))
+    co, alo, exo = oracle.build_split(vals, c["alpha"], CASES[name]["ncomp"])
+    assert ex == exo
+    # device-resident arguments (torch CUDA tensors in, out)
+    td = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    vd, sd = gpu.row_scale_device(td(rp.astype(np.int32)), td(ci.astype(np.int32)), td(v), c["alpha"])
+    assert np.array_equal(vd.cpu().numpy(), c["vals"]) and np.array_equal(sd.cpu().numpy(), c["scale"])
+    if c.get("ilu"):
+        lo, up = gpu.factorize_split_cast_device(rp, ci, vals)
+        for a, b in zip(lo + up, list(c["lower"]) + list(c["upper"])):
+            assert np.array_equal(np.asarray(a), np.asarray(b))
+        lod, upd = gpu.factorize_split_cast_device(td(rp.astype(np.int32)), td(ci.astype(np.int32)), td(vals))
+        for a, b in zip(lod + upd, list(c["lower"]) + list(c["upper"])):
+            assert np.array_equal(a.cpu().numpy(), np.asarray(b))
+
+
+def test_device_setup_errors(gpu):
+    """The reference's setup exceptions (type and text, first offending row)."""
+    rp = np.array([0, 1, 1, 2], np.int32)  # row 1 empty
+    with pytest.raises(RuntimeError, match=r"row_scale: row 1 has no nonzero entry"):
+        gpu.row_scale_device(rp, np.array([0, 2], np.int32), np.array([1.0, 2.0]), 16)
+    with pytest.raises(ValueError, match="build_split: need at least one component"):
+        gpu.build_split_device(np.array([1.0]), 16, 0)
+    # row 2 has no diagonal in its pattern
+    rp = np.array([0, 1, 2, 3], np.int32)
+    with pytest.raises(RuntimeError, match=r"factorize_ilu0: row 2 has no diagonal entry in the pattern"):
+        gpu.factorize_split_cast_device(rp, np.array([0, 1, 0], np.int32), np.array([2.0, 2.0, 1.0]))
+    # zero pivot in row 1 (a_11 - a_10 a_01 / a_00 = 1 - 1 = 0)
+    rp = np.array([0, 2, 4], np.int32)
+    with pytest.raises(RuntimeError, match=r"factorize_ilu0: zero pivot in row 1"):
+        gpu.factorize_split_cast_device(rp, np.array([0, 1, 0, 1], np.int32), np.array([1.0, 1.0, 1.0, 1.0]))
+    # sqrt|d| truncates to zero
+    rp = np.array([0, 1, 2], np.int32)
+    with pytest.raises(RuntimeError, match=r"split_cast: diagonal entry of row 0 truncates to zero"):
+        gpu.factorize_split_cast_device(rp, np.array([0, 1], np.int32), np.array([0.5, 4.0]))
