@@ -1662,6 +1662,10 @@ __device__ __forceinline__ void bulk_g2s_s(unsigned dst, const void* src, unsign
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
 }
+// L2 prefetch of a global range (16-byte aligned, size a multiple of 16)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ i64 lds64(unsigned a) {
   i64 v;
   asm volatile("ld.shared.s64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
@@ -1755,7 +1759,7 @@ __host__ __device__ inline TriSmem tri_smem_layout(int tile_cap, int seg_cap, in
 
 template <typename T, bool BACKWARD, int MAXD>
 __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restrict__ yperm, T* out,
-                                                     const Ctl* ctl, int seg_cap, int L) {
+                                                     const Ctl* ctl, int seg_cap, int L, int pf) {
   constexpr bool FP = std::is_same<T, double>::value;
   constexpr int REC = 32 + 12 * MAXD;
   constexpr unsigned YOFF = kTriSegRows * REC;                 // rhs run in a ring slot
@@ -1803,7 +1807,19 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
     if (lane != 0) return;
     int k = 0;
     unsigned ph = 1;  // parity of the previous use of slot k (first L levels: none)
+    // records and rhs runs of levels q+L .. q+pf-1 are pulled into L2 ahead of
+    // their shared-memory copy: the ring (L slots, bounded by the tile's
+    // values in shared memory) then waits on an L2 hit, not on HBM latency
+    auto prefetch = [&](int qq) {
+      if (qq >= nsg) return;
+      const int p0 = seg_row(qq), pc = seg_row(qq + 1) - p0;
+      const int pa = p0 & ~1, pyc = ((p0 + pc + 1) & ~1) - pa;
+      bulk_prefetch_l2(a.p_rec + static_cast<size_t>(p0) * REC, static_cast<unsigned>(pc * REC));
+      bulk_prefetch_l2(yperm + pa, static_cast<unsigned>(pyc * 8));
+    };
+    for (int q = L; q < pf; ++q) prefetch(q);
     for (int q = 0; q < nsg; ++q) {
+      if (pf > L) prefetch(q + pf);
       if (q >= L) mbar_wait_s(empty_s + 8u * k, ph);
       const int s0 = seg_row(q), c = seg_row(q + 1) - s0;
       const unsigned slot = ring_s + static_cast<unsigned>(k) * lay.ring_slot;
@@ -1952,7 +1968,9 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
       }
       sts64(cur.zaddr, zbits);
 #ifndef IGM_TRI_NOSTORE
+#ifndef IGM_TRI_NOOUT
       out[cur.row] = z;
+#endif
       if (cur.info & (1 << 10)) xz_put(a.xz + cur.row, static_cast<u64>(zbits), a.epoch);  // read by another tile
 #endif
     }
@@ -2410,7 +2428,12 @@ static void tri_launch_one(cudaStream_t st, const DevTri& t, const T* y, T* out,
   // right-hand side into schedule order (and the FP path's 1/gamma prescale)
   k_tri_gather<T><<<grid_full(t.n, 256), 256, 0, st>>>(t.n, t.p_row, y, static_cast<T*>(t.yperm), ctl, prescale,
                                                        std::is_same<T, double>::value ? nullptr : t.stats);
-  k_tri<T, B, D><<<t.ntiles, kTriThreads, sm, st>>>(args, static_cast<const T*>(t.yperm), out, ctl, seg_cap, L);
+  static const int env_pf = [] {
+    const char* e = std::getenv("IGM_TRI_PF");
+    return e ? std::atoi(e) : 12;
+  }();
+  k_tri<T, B, D><<<t.ntiles, kTriThreads, sm, st>>>(args, static_cast<const T*>(t.yperm), out, ctl, seg_cap, L,
+                                                    env_pf);
 }
 
 template <typename T, bool B>

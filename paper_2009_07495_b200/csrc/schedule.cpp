@@ -1,6 +1,9 @@
 // schedule.cpp -- see schedule.hpp.
 #include "schedule.hpp"
 
+#include <array>
+#include <cstdint>
+
 #include "fx_core.cuh"
 
 #include <algorithm>
@@ -159,6 +162,101 @@ TriSchedule build_tri_schedule(int n, const int* rp, const int* ci, const std::i
     };
     assign(B);
     bool ok = acyclic();
+    // Wavefront ticket order (stencils whose z-layer tile graph has cycles,
+    // e.g. 27-point): tiles sorted by the DAG level of their first row in
+    // ticket direction, tickets of equal level forming one layer.  Valid when
+    // every cross-tile dependency points to a strictly earlier layer, or to
+    // the same layer with each layer small enough to be co-resident; then
+    // the wavefront flows through consecutive layers instead of serialising
+    // the z-layers (which must each be fully resident).  Among candidate
+    // bricks the one with the smallest max(critical path, tile-levels / SMs)
+    // is taken.
+    if (!ok) {
+      struct Cand {
+        long long b[3];
+        double cost;
+        std::vector<int> perm;   // old tile id -> new (ticket-ordered) id
+        std::vector<int> layer;  // per new tile id
+      };
+      auto try_wave = [&](const long long* b, Cand& c) {
+        assign(b);
+        const long long nb0 = cdiv(G[0], b[0]), nb1 = cdiv(G[1], b[1]), nb2 = cdiv(G[2], b[2]);
+        const long long nt = nb0 * nb1 * nb2;
+        if (b[0] * b[1] * b[2] > cap) return false;
+        std::vector<int> lo(static_cast<size_t>(nt), INT32_MAX), hi(static_cast<size_t>(nt), -1);
+        for (int i = 0; i < n; ++i) {
+          lo[tile_of[i]] = std::min(lo[tile_of[i]], lev[i]);
+          hi[tile_of[i]] = std::max(hi[tile_of[i]], lev[i]);
+        }
+        std::vector<int> ord(static_cast<size_t>(nt));
+        std::iota(ord.begin(), ord.end(), 0);
+        // ticket order = ascending first level; the backward factor's tickets
+        // run from the last tile id down, so its ids are assigned reversed
+        std::stable_sort(ord.begin(), ord.end(), [&](int a, int bb) { return lo[a] < lo[bb]; });
+        if (upper) std::reverse(ord.begin(), ord.end());
+        c.perm.assign(static_cast<size_t>(nt), 0);
+        for (long long q = 0; q < nt; ++q) c.perm[ord[q]] = static_cast<int>(q);
+        c.layer.assign(static_cast<size_t>(nt), 0);
+        std::vector<int> key(static_cast<size_t>(nt));
+        for (long long t = 0; t < nt; ++t) key[c.perm[t]] = lo[t];
+        // layers in ticket order
+        long long max_layer = 0, run = 0;
+        int lay = -1;
+        for (long long q = 0; q < nt; ++q) {
+          const int id = upper ? static_cast<int>(nt - 1 - q) : static_cast<int>(q);
+          const int prev = upper ? static_cast<int>(nt - q) : static_cast<int>(q - 1);
+          if (q == 0 || key[id] != key[prev]) {
+            ++lay;
+            run = 0;
+          }
+          c.layer[id] = lay;
+          max_layer = std::max(max_layer, ++run);
+        }
+        bool same_layer_dep = false;
+        for (int i = 0; i < n; ++i)
+          for (int k = orp[i]; k < orp[i + 1]; ++k) {
+            const int ti = c.perm[tile_of[i]], tj = c.perm[tile_of[oci[k]]];
+            if (ti == tj) continue;
+            if (c.layer[tj] > c.layer[ti]) return false;
+            if (c.layer[tj] == c.layer[ti]) same_layer_dep = true;
+          }
+        if (same_layer_dep && max_layer > nsm) return false;
+        long long tl = 0;
+        for (long long t = 0; t < nt; ++t)
+          if (hi[t] >= 0) tl += hi[t] - lo[t] + 1;
+        c.cost = std::max(static_cast<double>(S.nlevels), static_cast<double>(tl) / nsm) *
+                 (same_layer_dep ? 1.1 : 1.0);
+        for (int d = 0; d < 3; ++d) c.b[d] = b[d];
+        return true;
+      };
+      std::vector<std::array<long long, 3>> cands;
+      cands.push_back({B[0], B[1], B[2]});
+      {  // the co-resident z-layer brick (below) as a candidate too
+        long long b[3] = {B[0], B[1], B[2]};
+        while (cdiv(G[0], b[0]) * cdiv(G[1], b[1]) > nsm && b[2] > 1) {
+          b[2] = cdiv(b[2], 2);
+          if (b[0] <= b[1]) b[0] = std::min(G[0], 2 * b[0]);
+          else b[1] = std::min(G[1], 2 * b[1]);
+          while (b[0] * b[1] * b[2] > cap && b[2] > 1) b[2] = cdiv(b[2], 2);
+        }
+        cands.push_back({b[0], b[1], b[2]});
+      }
+      Cand best;
+      best.cost = -1;
+      for (auto& cb : cands) {
+        Cand c;
+        if (try_wave(cb.data(), c) && (best.cost < 0 || c.cost < best.cost)) best = std::move(c);
+      }
+      if (best.cost >= 0 && !std::getenv("IGM_TRI_NO_WAVE")) {
+        assign(best.b);
+        for (int i = 0; i < n; ++i) tile_of[i] = best.perm[tile_of[i]];
+        for (int d = 0; d < 3; ++d) B[d] = best.b[d];
+        S.tile_layer = best.layer;
+        ok = true;
+      } else {
+        assign(B);
+      }
+    }
     if (!ok) {
       while (cdiv(G[0], B[0]) * cdiv(G[1], B[1]) > nsm && B[2] > 1) {
         B[2] = cdiv(B[2], 2);
@@ -369,10 +467,14 @@ int validate_tri_schedule(const TriSchedule& S, const int* rp, const int* ci, bo
         // ticket order: producer tile handed out no later than the layer of i
         const int tk_i = upper ? S.ntiles - 1 - tile_of[i] : tile_of[i];
         const int tk_j = upper ? S.ntiles - 1 - tile_of[j] : tile_of[j];
-        const int layer = S.brick[0] ? (S.grid[0] + S.brick[0] - 1) / S.brick[0] *
-                                           ((S.grid[1] + S.brick[1] - 1) / S.brick[1])
-                                     : 1;
-        if (tk_j / layer > tk_i / layer) return 6;
+        if (!S.tile_layer.empty()) {  // wavefront order: explicit layers
+          if (S.tile_layer[tile_of[j]] > S.tile_layer[tile_of[i]]) return 6;
+        } else {
+          const int layer = S.brick[0] ? (S.grid[0] + S.brick[0] - 1) / S.brick[0] *
+                                             ((S.grid[1] + S.brick[1] - 1) / S.brick[1])
+                                       : 1;
+          if (tk_j / layer > tk_i / layer) return 6;
+        }
         bool listed = false;
         for (int w = S.seg_wptr[sg]; w < S.seg_wptr[sg + 1]; ++w) listed = listed || S.seg_wt[w] == tile_of[j];
         if (!listed) return 7;

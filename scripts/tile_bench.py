@@ -14,7 +14,11 @@ h = 1.0 / 129
 offs = [(0, 0, -1), (0, -1, 0), (-1, 0, 0), (0, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 1)]
 coef = {0: -1 / h**2 - 20 / h, 1: -1 / h**2 - 20 / h, 2: -1 / h**2 - 20 / h, 3: 6 / h**2 + 60 / h,
         4: -1 / h**2, 5: -1 / h**2, 6: -1 / h**2}
-rp, ci, v = gen._stencil_csr(dims, offs, lambda o, r: np.full(r.shape, coef[o]))
+if os.environ.get("KIND") == "27":
+    assert dims[0] == dims[1] == dims[2]
+    rp, ci, v = gen.stencil27_lean(dims[0], 5)
+else:
+    rp, ci, v = gen._stencil_csr(dims, offs, lambda o, r: np.full(r.shape, coef[o]))
 vals, _ = igm.row_scale(rp, ci, v, 32)
 lo, up = igm.factorize_split_cast(rp, ci, vals)
 F = igm.IluFactors(lo, up)
@@ -35,4 +39,4 @@ torch.cuda.synchronize()
 dt = (time.time() - t0) / R
 info = F.schedule_info(False)
 L = info["levels"]
-print(f"dims {dims} tiles {info['tiles']} levels {L}: apply {dt*1e6:.1f} us -> {dt*1e6/(2*L):.3f} us/level (fwd+bwd, incl. launch)")
+print(f"kind {os.environ.get('KIND','7')} brick {info['brick']} dims {dims} tiles {info['tiles']} levels {L}: apply {dt*1e6:.1f} us -> {dt*1e6/(2*L):.3f} us/level (fwd+bwd, incl. launch)")
