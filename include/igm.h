@@ -79,6 +79,14 @@ igm_status igm_ctx_synchronize(igm_ctx* ctx);
 void* igm_ctx_stream(igm_ctx* ctx);
 /* number of kernels this context has launched so far */
 uint64_t igm_ctx_launch_count(igm_ctx* ctx);
+/* Exact running-sum ("add") overflow events for the fx_dot / fx_norm
+ * reductions in checked mode: after every reduction
+ * whose sum|term| certificate fails, an exact int128 prefix scan counts the
+ * sequential order's wrap crossings, so igm_trace.total / igm_report
+ * overflow counts are the reference's in every case (overflow_exact = 1).
+ * Off by default (the certificate already proves zero events in configured
+ * runs); on, the cycle runs the separate pass kernels. */
+igm_status igm_set_exact_overflow_counts(igm_ctx* ctx, int on);
 const char* igm_last_error(void);
 const char* igm_version(void);
 /* Opt-in per-kernel-class device timing (CUDA events around each launch).

@@ -118,6 +118,10 @@ class Device:
     def stream(self) -> int:
         return lib().igm_ctx_stream(self.h) or 0
 
+    def set_exact_overflow_counts(self, on: bool = True) -> None:
+        """Exact running-sum overflow events in checked mode (8(f) row 4)."""
+        _check(lib().igm_set_exact_overflow_counts(self.h, 1 if on else 0))
+
     @property
     def launches(self) -> int:
         return int(lib().igm_ctx_launch_count(self.h))

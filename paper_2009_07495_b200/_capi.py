@@ -104,6 +104,7 @@ SIGNATURES = [
     ("igm_ctx_synchronize", C.c_int, [C.c_void_p]),
     ("igm_ctx_stream", C.c_void_p, [C.c_void_p]),
     ("igm_ctx_launch_count", C.c_uint64, [C.c_void_p]),
+    ("igm_set_exact_overflow_counts", C.c_int, [C.c_void_p, C.c_int]),
     ("igm_last_error", C.c_char_p, []),
     ("igm_version", C.c_char_p, []),
     ("igm_profile_enable", None, [C.c_int]),

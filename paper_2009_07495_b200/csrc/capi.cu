@@ -154,7 +154,23 @@ struct igm_ctx {
   size_t fp_vals_n = 0;
   double* fp_sc = nullptr;  // [r0n, wnorm_pre, h_0..h_m, hnext] + fdot partials + weights
   size_t fp_sc_n = 0;
+  // exact running-sum overflow counting (igm_set_exact_overflow_counts)
+  bool exact_adds = false;
+  void* adds_s = nullptr;
+  size_t adds_bytes = 0;
 };
+
+// scratch of the exact add-event count (grown on demand; stream-ordered use)
+void* adds_scratch(igm_ctx* c, long long n) {
+  const size_t need = exact_adds_scratch_bytes(n);
+  if (need > c->adds_bytes) {
+    ck(cudaStreamSynchronize(c->stream), "adds scratch");
+    dfree(c->adds_s);
+    c->adds_s = dalloc<unsigned char>(need);
+    c->adds_bytes = need;
+  }
+  return c->adds_s;
+}
 
 // norm2 scratch for vectors of length n (grown on demand; stream-ordered use)
 void* n2_scratch(igm_ctx* c, long long n) {
@@ -479,7 +495,11 @@ void enqueue_cycle(igm_ctx* c, const CycleParams& p, CycleMode mode, const doubl
   launch_encode(st, n, r0, w.basis, f, ctl);
   // ---- Arnoldi steps (gmres_int.cpp:90-160)
   const size_t cstride = static_cast<size_t>(K_COUNT) * OP_COUNT;
-  const long long arn_S = arnoldi_slice(n, c->device);
+  // exact add-event counting (8(f) row 4) runs the separate pass kernels
+  // with a counting pass after each reduction
+  const bool exact = p.checked && c->exact_adds;
+  void* adds = exact ? adds_scratch(c, n) : nullptr;
+  const long long arn_S = exact ? 0 : arnoldi_slice(n, c->device);
   unsigned gbase = 0;  // grid-barrier arrivals so far in this cycle (Ctl::gbar reset by cycle_init)
   for (int j = 0; j < M; ++j) {
     u64* cstep = w.cnt + static_cast<size_t>(j) * cstride;
@@ -505,11 +525,17 @@ void enqueue_cycle(igm_ctx* c, const CycleParams& p, CycleMode mode, const doubl
       launch_mgs_pass(st, n, i == 0 ? 0 : 1, w.w, vp, vi, i > 0 ? accj + (i - 1) : nullptr,
                       accj + i, absj + 2 * i, f, sh, cstep + K_AXPY * OP_COUNT,
                       cstep + K_DOT * OP_COUNT, ctl, p.checked);
+      if (exact)
+        launch_exact_adds(st, n, 0, w.w, vi, sh.dot_b1, sh.dot_b2, absj + 2 * i, ctl,
+                          cstep + K_DOT * OP_COUNT + OP_ADD, adds);
     }
     launch_mgs_pass(st, n, 2, w.w, vj, nullptr, accj + j, w.nacc + j, w.nabs + 2 * j, f, sh,
                     cstep + K_AXPY * OP_COUNT, cstep + K_NORM * OP_COUNT, ctl, p.checked);
+    if (exact)
+      launch_exact_adds(st, n, 1, w.w, nullptr, sh.norm_b1, sh.norm_b1, w.nabs + 2 * j, ctl,
+                        cstep + K_NORM * OP_COUNT + OP_ADD, adds);
     launch_step_scalar(st, j, f, sh, accj, absj, w.nacc + j, w.nabs + 2 * j, w.hess, ld, w.g, w.cs,
-                       w.sn, w.gabs, w.w, cstep, ctl, p.checked);
+                       w.sn, w.gabs, w.w, cstep, ctl, exact ? 2 : (p.checked ? 1 : 0));
     launch_vec_div(st, n, w.w, w.basis + static_cast<long long>(j + 1) * n, f, sh,
                    cstep + K_VEC_DIV * OP_COUNT, ctl, p.checked);
   }
@@ -633,6 +659,7 @@ void igm_ctx_destroy(igm_ctx* c) {
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
   if (c->h_red) cudaFreeHost(c->h_red);
   cudaStreamDestroy(c->stream);
+  dfree(c->adds_s);
   delete c;
 }
 
@@ -643,6 +670,13 @@ igm_status igm_ctx_synchronize(igm_ctx* c) {
 void* igm_ctx_stream(igm_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
 
 uint64_t igm_ctx_launch_count(igm_ctx*) { return g_launches; }
+
+igm_status igm_set_exact_overflow_counts(igm_ctx* c, int on) {
+  return guarded([&] {
+    need_ctx(c);
+    c->exact_adds = on != 0;
+  });
+}
 
 void igm_profile_enable(int on) { prof_enable(on != 0); }
 
@@ -833,6 +867,9 @@ static void fx_red_common(igm_ctx* c, long long n, int mode, const int64_t* v, c
   In<i64> dw(mode == 0 ? w : nullptr, n, c->stream);
   ck(cudaMemsetAsync(c->red, 0, sizeof(u64) * (3 + OP_COUNT), c->stream), "memset");
   if (n > 0) launch_fx_red(c->stream, n, mode, dv.d, dw.d, b1, b2, c->red, c->red + 1, c->red + 3, chk);
+  if (n > 0 && chk && c->exact_adds)  // exact running-sum events (no-op under the certificate)
+    launch_exact_adds(c->stream, n, mode, dv.d, dw.d, b1, b2, c->red + 1, nullptr, c->red + 3 + OP_ADD,
+                      adds_scratch(c, n));
   ck(cudaMemcpyAsync(c->h_red, c->red, sizeof(u64) * (3 + OP_COUNT), cudaMemcpyDeviceToHost, c->stream), "D2H");
   ck(cudaStreamSynchronize(c->stream), "sync");
 }
@@ -854,7 +891,8 @@ igm_status igm_fx_dot(igm_ctx* c, int64_t n, const int64_t* v, const int64_t* w,
     const i64 acc = static_cast<i64>(c->h_red[0]);
     if (chk) {
       trace_add(t, t->kernel, OP_MUL, c->h_red[3 + OP_MUL], t->restart, t->step);
-      if (!abs_small_h(c->h_red + 1)) t->exact = 0;
+      if (c->exact_adds) trace_add(t, t->kernel, OP_ADD, c->h_red[3 + OP_ADD], t->restart, t->step);
+      else if (!abs_small_h(c->h_red + 1)) t->exact = 0;
     }
     const int e = f - b1 - b2;
     if (e >= 0) {
@@ -882,7 +920,9 @@ igm_status igm_fx_norm(igm_ctx* c, int64_t n, const int64_t* v, int f, int b1, i
     if (chk) {
       const u64 nmul = c->h_red[3 + OP_MUL];
       trace_add(t, t->kernel, OP_MUL, nmul, t->restart, t->step);
-      if (nmul == 0) {
+      if (c->exact_adds) {
+        trace_add(t, t->kernel, OP_ADD, c->h_red[3 + OP_ADD], t->restart, t->step);
+      } else if (nmul == 0) {
         const unsigned __int128 s = (static_cast<unsigned __int128>(c->h_red[1]) << 32) + c->h_red[2];
         const u64 wraps = static_cast<u64>((s + (static_cast<unsigned __int128>(1) << 63)) >> 64);
         trace_add(t, t->kernel, OP_ADD, wraps, t->restart, t->step);

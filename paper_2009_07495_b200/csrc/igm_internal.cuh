@@ -155,8 +155,14 @@ void launch_step_scalar(cudaStream_t st, int j, int f, ShiftsD sh,
                         const u64* acc_col, const u64* abs_col, const u64* nacc,
                         const u64* nabs, i64* hess, int ld, i64* g, i64* cs,
                         i64* sn, i64* gabs, const i64* w, u64* cnt_step,
-                        Ctl* ctl, bool checked, int acc_st = 1, int abs_st = 2,
-                        const u64* norm_mul = nullptr /* cnt_step's slot */);
+                        Ctl* ctl, int checked /* 2: add events counted exactly */, int acc_st = 1,
+                        int abs_st = 2, const u64* norm_mul = nullptr /* cnt_step's slot */);
+// exact add-event count of one fx_dot (mode 0, terms asr(w,b1)*asr(v,b2)) or
+// fx_norm (mode 1, asr(w,b1)^2) reduction into *cnt_add; a no-op when the
+// certificate cert = {sum|t| hi, lo} is below 2^63
+size_t exact_adds_scratch_bytes(long long n);
+void launch_exact_adds(cudaStream_t st, long long n, int mode, const i64* w, const i64* v, int b1, int b2,
+                       const u64* cert, const Ctl* ctl, u64* cnt_add, void* scratch);
 void launch_cycle_init(cudaStream_t st, Ctl* ctl, i64* g, int f);
 void launch_encode(cudaStream_t st, long long n, const double* r0, i64* v0,
                    int f, Ctl* ctl);

@@ -1015,6 +1015,105 @@ __global__ void __launch_bounds__(512) k_vec_div(long long n, const i64* __restr
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Exact running-sum ("add") overflow events of one fx_dot / fx_norm
+// reduction.  The reference adds the
+// wrapped int64 terms t_l sequentially, acc <- acc + t_l, and records an
+// event whenever the exact sum leaves int64.  With P_l the exact (int128)
+// prefix sum, acc_l = wrap(P_l) and the event at l happens iff
+// floor((P_{l+1} + 2^63) / 2^64) != floor((P_l + 2^63) / 2^64).  Pass 1 sums
+// each chunk exactly, pass 2 scans the chunk sums in order, pass 3 walks
+// every chunk from its exact start and counts the crossings.  All three
+// passes return at once when the pass kernel's certificate (sum |t| < 2^63,
+// cert = {hi, lo} 32-bit halves) already proves zero events.
+constexpr int kAddChunk = 8192;
+constexpr int kAddThreads = 512;
+constexpr int kAddPer = kAddChunk / kAddThreads;
+
+__device__ __forceinline__ i64 add_term(int mode, const i64* __restrict__ w, const i64* __restrict__ v,
+                                        long long l, int b1, int b2) {
+  const i64 a = asr(w[l], b1);
+  return wmul(a, mode == 0 ? asr(v[l], b2) : a);
+}
+__device__ __forceinline__ bool adds_certified(const u64* cert, const Ctl* ctl) {
+  if (ctl && cycle_over(ctl)) return true;
+  const unsigned __int128 s = (static_cast<unsigned __int128>(cert[0]) << 32) + cert[1];
+  return s < (static_cast<unsigned __int128>(1) << 63);
+}
+__device__ __forceinline__ long long wrap_index(__int128 p) {
+  return static_cast<long long>((p + (static_cast<__int128>(1) << 63)) >> 64);
+}
+
+__global__ void __launch_bounds__(kAddThreads) k_adds_blk(long long n, int mode, const i64* __restrict__ w,
+                                                          const i64* __restrict__ v, int b1, int b2,
+                                                          const u64* cert, const Ctl* ctl, __int128* blk) {
+  __shared__ __int128 sh[kAddThreads / 32];
+  if (adds_certified(cert, ctl)) return;
+  const long long lo = static_cast<long long>(blockIdx.x) * kAddChunk;
+  const long long hi = min(n, lo + kAddChunk);
+  __int128 acc = 0;
+  for (long long l = lo + threadIdx.x; l < hi; l += kAddThreads) acc += add_term(mode, w, v, l, b1, b2);
+  // exact: any order
+  for (int o = 16; o > 0; o >>= 1) {
+    const u64 a = __shfl_down_sync(0xffffffffu, static_cast<u64>(acc), o);
+    const u64 b = __shfl_down_sync(0xffffffffu, static_cast<u64>(static_cast<unsigned __int128>(acc) >> 64), o);
+    acc += static_cast<__int128>((static_cast<unsigned __int128>(b) << 64) | a);
+  }
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __int128 t = 0;
+    for (int i = 0; i < kAddThreads / 32; ++i) t += sh[i];
+    blk[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_adds_scan(int nblk, const u64* cert, const Ctl* ctl, __int128* blk) {
+  if (adds_certified(cert, ctl)) return;
+  if (threadIdx.x != 0) return;
+  __int128 p = 0;
+  for (int b = 0; b < nblk; ++b) {
+    const __int128 t = blk[b];
+    blk[b] = p;
+    p += t;
+  }
+}
+
+__global__ void __launch_bounds__(kAddThreads) k_adds_count(long long n, int mode, const i64* __restrict__ w,
+                                                            const i64* __restrict__ v, int b1, int b2,
+                                                            const u64* cert, const Ctl* ctl,
+                                                            const __int128* pre, u64* cnt_add) {
+  __shared__ __int128 sh[kAddThreads];
+  if (adds_certified(cert, ctl)) return;
+  const long long lo = static_cast<long long>(blockIdx.x) * kAddChunk + static_cast<long long>(threadIdx.x) * kAddPer;
+  const long long hi = min(n, lo + kAddPer);
+  __int128 s = 0;
+  for (long long l = lo; l < hi; ++l) s += add_term(mode, w, v, l, b1, b2);
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive scan in element order
+    __int128 p = pre[blockIdx.x];
+    for (int i = 0; i < kAddThreads; ++i) {
+      const __int128 t = sh[i];
+      sh[i] = p;
+      p += t;
+    }
+  }
+  __syncthreads();
+  __int128 p = sh[threadIdx.x];
+  long long wi = wrap_index(p);
+  unsigned long long ev = 0;
+  for (long long l = lo; l < hi; ++l) {
+    p += add_term(mode, w, v, l, b1, b2);
+    const long long wn = wrap_index(p);
+    ev += wn != wi;
+    wi = wn;
+  }
+  for (int o = 16; o > 0; o >>= 1) ev += __shfl_down_sync(0xffffffffu, ev, o);
+  if ((threadIdx.x & 31) == 0 && ev) atomicAdd(reinterpret_cast<unsigned long long*>(cnt_add), ev);
+}
+
 // ---------------------------------------------------------------------------
 // K5 per-step scalar work (gmres_int.cpp:101-159): finalise the h_ij from
 // the wrapped accumulators, fx_norm -> h_{j+1,j}, vec_div reciprocal, the
@@ -1093,11 +1192,11 @@ __device__ void step_scalar_dev(int j, int f, ShiftsD sh, const u64* acc_col, in
       if (shl_ovf(acc, -e)) ev.hit(K_DOT, OP_SHL);
       col[i] = wrap_shl(acc, -e);
     }
-    if (checked && !abs_small(abs_col + i * abs_st)) ctl->add_inexact = 1;
+    if (checked == 1 && !abs_small(abs_col + i * abs_st)) ctl->add_inexact = 1;
   }
   // h_{j+1,j} = fx_norm(w) (fxp.cpp:69-86)
   const i64 nsum = static_cast<i64>(*nacc);
-  if (checked) {
+  if (checked == 1) {  // (checked == 2: the norm's add events were counted exactly by k_adds_*)
     // all terms s*s are >= 0 unless a square itself wrapped: then the
     // running sum is monotone and its wrap count is exact.
     if (*norm_mul == 0) {
@@ -2275,6 +2374,22 @@ void launch_fx_red(cudaStream_t st, long long n, int mode, const i64* v, const i
   LAUNCH_CHECK();
 }
 
+size_t exact_adds_scratch_bytes(long long n) {
+  return sizeof(__int128) * static_cast<size_t>(std::max<long long>(1, (n + kAddChunk - 1) / kAddChunk));
+}
+
+void launch_exact_adds(cudaStream_t st, long long n, int mode, const i64* w, const i64* v, int b1, int b2,
+                       const u64* cert, const Ctl* ctl, u64* cnt_add, void* scratch) {
+  if (n <= 0) return;
+  ProfScope prof_(st, KC_OTHER);
+  const int nblk = static_cast<int>((n + kAddChunk - 1) / kAddChunk);
+  __int128* blk = static_cast<__int128*>(scratch);
+  k_adds_blk<<<nblk, kAddThreads, 0, st>>>(n, mode, w, v, b1, b2, cert, ctl, blk);
+  k_adds_scan<<<1, 32, 0, st>>>(nblk, cert, ctl, blk);
+  k_adds_count<<<nblk, kAddThreads, 0, st>>>(n, mode, w, v, b1, b2, cert, ctl, blk, cnt_add);
+  g_launches += 3;
+}
+
 void launch_axpy_only(cudaStream_t st, long long n, i64* w, i64 h, const i64* v, int f, int b1,
                       u64* cnt, bool checked) {
   ProfScope prof_(st, KC_MGS);
@@ -2302,11 +2417,11 @@ void launch_vec_div(cudaStream_t st, long long n, const i64* w, i64* out, int f,
 void launch_step_scalar(cudaStream_t st, int j, int f, ShiftsD sh, const u64* acc_col,
                         const u64* abs_col, const u64* nacc, const u64* nabs, i64* hess, int ld,
                         i64* g, i64* cs, i64* sn, i64* gabs, const i64* w, u64* cnt_step, Ctl* ctl,
-                        bool checked, int acc_st, int abs_st, const u64* norm_mul) {
+                        int checked, int acc_st, int abs_st, const u64* norm_mul) {
   ProfScope prof_(st, KC_SCALAR);
   if (!norm_mul) norm_mul = cnt_step + K_NORM * OP_COUNT + OP_MUL;
   k_step_scalar<<<1, 1, 0, st>>>(j, f, sh, acc_col, acc_st, abs_col, abs_st, nacc, nabs, norm_mul, hess, ld, g,
-                                 cs, sn, gabs, w, cnt_step, ctl, checked ? 1 : 0);
+                                 cs, sn, gabs, w, cnt_step, ctl, checked);
   LAUNCH_CHECK();
 }
 

@@ -58,6 +58,10 @@ igm_ctx* ctx() {
   if (!h.c) {
     const char* dev = std::getenv("IGM_DEVICE");
     ok(igm_ctx_create(dev ? std::atoi(dev) : 0, &h.c));
+    // exact running-sum overflow events: opt-in, the
+    // reference API has no switch for it
+    const char* ex = std::getenv("IGM_EXACT_OVERFLOW");
+    if (ex && std::atoi(ex) != 0) ok(igm_set_exact_overflow_counts(h.c, 1));
   }
   return h.c;
 }

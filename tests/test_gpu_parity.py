@@ -683,3 +683,61 @@ def test_device_setup_errors(gpu):
     rp = np.array([0, 1, 2], np.int32)
     with pytest.raises(RuntimeError, match=r"split_cast: diagonal entry of row 0 truncates to zero"):
         gpu.factorize_split_cast_device(rp, np.array([0, 1], np.int32), np.array([0.5, 4.0]))
+
+
+def test_exact_overflow_counts(gpu, oracle):
+    """Exact running-sum overflow events: with
+    igm_set_exact_overflow_counts on, fx_dot / fx_norm reductions whose sums
+    wrap up and down many times (and whose products wrap too) report the
+    reference's sequential event count, and the trace stays exact."""
+    from oracle.ffi import CheckerError
+    dev = gpu.Device.default()
+    dev.set_exact_overflow_counts(True)
+    try:
+        rng = np.random.default_rng(3)
+        n = 50_000
+        mag = rng.integers(1 << 61, 1 << 62, n, dtype=np.int64)
+        v = np.where(rng.random(n) < 0.55, mag, -mag).astype(np.int64)
+        for w in (np.ones(n, np.int64), rng.integers(-5, 6, n, dtype=np.int64)):
+            t, to = gpu.FxTrace(checked=True), PyTrace()
+            assert gpu.fx_dot(v, w, 30, 0, 0, t) == oracle.fx_dot(v, w, 30, 0, 0, to)
+            assert t.exact and t.total_overflows() == to.total > 100
+        for seed in range(4):
+            r2 = np.random.default_rng(10 + seed)
+            vn = r2.integers(-(1 << 33), 1 << 33, 20_000 + seed, dtype=np.int64)
+            t, to = gpu.FxTrace(checked=True), PyTrace()
+            try:
+                ro = oracle.fx_norm(vn, 31, 0, to)
+            except CheckerError:
+                ro = None
+            if ro is None:
+                with pytest.raises(ArithmeticError):
+                    gpu.fx_norm(vn, 31, 0, t)
+            else:
+                assert gpu.fx_norm(vn, 31, 0, t) == ro
+            assert t.exact and t.total_overflows() == to.total > 100
+        # a whole solve whose dot products wrap (test_refine.cpp:392-426 setup)
+        from workloads import gen
+        rp, ci, vv = gen.laplacian2d(8)
+        vals, scale = gpu.row_scale(rp, ci, vv, 16)
+        comp, al, _ = gpu.build_split(vals, 16, 10)
+        S, A = gpu.SplitMatrix(rp, ci, comp, al), gpu.CsrMatrixF(rp, ci, vals)
+        b = np.ones(len(rp) - 1) / scale
+        plan = gpu.ShiftPlan(0, 0, 16, 16, 16, 14, 16, 0)
+        t, to = gpu.FxTrace(checked=True), PyTrace()
+        try:
+            gpu.solve(S, A, b, gpu.RefineConfig(tol=1e-8, max_refinements=3, m=6, shifts=plan, s=len(al) - 1),
+                      trace=t)
+            threw = False
+        except (ArithmeticError, ValueError, OverflowError, RuntimeError):
+            threw = True
+        try:
+            oracle.solve(oracle.split(rp, ci, comp, al), oracle.csrf(rp, ci, vals), b, 1e-8, 3, 6, 30, len(al) - 1,
+                         Shifts(0, 0, 16, 16, 16, 14, 16, 0), trace=to)
+            othrew = False
+        except CheckerError:
+            othrew = True
+        assert threw == othrew
+        assert t.exact and t.total_overflows() == to.total > 0
+    finally:
+        dev.set_exact_overflow_counts(False)
