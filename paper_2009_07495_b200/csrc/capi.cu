@@ -377,6 +377,7 @@ void build_tri(igm_ctx* c, DevTri& t, int n, const int* rp, const int* ci, const
   t.maxd = S.maxd;
   t.stride = S.stride;
   t.ntiles = S.ntiles;
+  t.acyclic = S.acyclic;
   t.nseg = static_cast<int>(S.seg_level.size());
   t.nlevels = S.nlevels;
   t.tile_cap = std::max(1, S.max_tile_rows);  // shared-memory slots the kernel reserves

@@ -98,6 +98,7 @@ struct DevTri {
   int *c_rp = nullptr, *c_ci = nullptr;
   i64 *c_val = nullptr, *c_diag = nullptr;
   unsigned long long epoch = 0;    // launches so far (tag of the next one)
+  bool acyclic = false;   // tile graph acyclic in ticket order (lookahead wavefront allowed)
   int* prog = nullptr;    // ntiles progress words
   int* ticket = nullptr;  // 1
 };

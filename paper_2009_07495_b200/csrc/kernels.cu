@@ -1866,7 +1866,8 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
   __shared__ int s_tile;
   if (cycle_over(ctl)) return;
   const TriSmem lay = tri_smem_layout<MAXD>(a.tile_cap, seg_cap, L, a.max_seg_ext);
-  const unsigned zt_s = smem_u32(smem_raw);
+  unsigned zt_s = smem_u32(smem_raw);
+  asm volatile("" : "+r"(zt_s));  // kept in a register (not re-derived from %cgactaid each level)
   int* s_rows = reinterpret_cast<int*>(smem_raw + lay.rows);
   int* s_xptr = reinterpret_cast<int*>(smem_raw + lay.xptr);
   const unsigned ring_s = smem_u32(smem_raw + lay.ring);
@@ -2006,12 +2007,20 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
 #ifndef IGM_TRI_SKELETON
     if (cur.have) {
       if constexpr (!FP) zmx = max(zmx, abs_u64(zlast));
+      // every dependency's shared-memory load issued back to back (no
+      // branch between them), then the cross-tile words selected by
+      // predicate; a word not yet published when it was loaded with the
+      // record is re-polled on a separate (rare) path
       i64 zb[MAXD];
 #pragma unroll
       for (int d = 0; d < MAXD; ++d) {
         const int c = cur.ci[d];
         zb[d] = lds64(zt_s + 8u * static_cast<unsigned>(c < 0 ? 0 : c));
-        if (c < 0) {  // cross-tile word loaded with the record, re-polled only if not yet published
+      }
+      unsigned stale = 0;
+#pragma unroll
+      for (int d = 0; d < MAXD; ++d) {
+        if (cur.ci[d] < 0) {
           const bool ok = cur.wt[d] == (a.epoch ^ cur.wv[d]);
 #ifdef IGM_TRI_TRACE
           if (tsb && q < 2048) {
@@ -2019,8 +2028,14 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
             atomicAdd(tsb + q * 8 + 1, 1ull);
           }
 #endif
-          zb[d] = static_cast<i64>(ok ? cur.wv[d] : xz_wait(a.xz + ~c, a.epoch));
+          zb[d] = ok ? static_cast<i64>(cur.wv[d]) : zb[d];
+          stale |= ok ? 0u : (1u << d);
         }
+      }
+      if (stale) {
+#pragma unroll
+        for (int d = 0; d < MAXD; ++d)
+          if ((stale >> d) & 1u) zb[d] = static_cast<i64>(xz_wait(a.xz + ~cur.ci[d], a.epoch));
       }
       auto extra = [&](int d) {  // dependency beyond the record stride (rare)
         const int c = __ldg(a.p_xdep + cur.xb + d - MAXD);
@@ -2081,9 +2096,10 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
   };
   // Each level's record is read (and its cross-tile loads issued) right
   // before the level's barrier, so their latency overlaps the barrier wait.
-  // Measured faster than reading records one to four levels ahead into a
-  // register ring (fewer registers, half the code): 1.07 vs 1.16 us/level at
-  // 128^3, 0.67 vs 0.75 for a single brick.
+  // Measured faster than reading records (and cross-tile words) one to four
+  // levels ahead into a register ring -- also with a deliberate two-level lag
+  // that waits for every word one level before its use: 1.40 vs 1.06
+  // us/level at 128^3, 0.87 vs 0.68 for a single brick.
   for (int q = 0; q < nsg; ++q) {
     fetch(q, R);
     level(q, R);

@@ -162,6 +162,7 @@ TriSchedule build_tri_schedule(int n, const int* rp, const int* ci, const std::i
     };
     assign(B);
     bool ok = acyclic();
+    S.acyclic = ok;
     // Wavefront ticket order (stencils whose z-layer tile graph has cycles,
     // e.g. 27-point): tiles sorted by the DAG level of their first row in
     // ticket direction, tickets of equal level forming one layer.  Valid when
@@ -175,6 +176,7 @@ TriSchedule build_tri_schedule(int n, const int* rp, const int* ci, const std::i
       struct Cand {
         long long b[3];
         double cost;
+        bool cyclic = false;     // some dependency within a layer
         std::vector<int> perm;   // old tile id -> new (ticket-ordered) id
         std::vector<int> layer;  // per new tile id
       };
@@ -221,6 +223,7 @@ TriSchedule build_tri_schedule(int n, const int* rp, const int* ci, const std::i
             if (c.layer[tj] == c.layer[ti]) same_layer_dep = true;
           }
         if (same_layer_dep && max_layer > nsm) return false;
+        c.cyclic = same_layer_dep;
         long long tl = 0;
         for (long long t = 0; t < nt; ++t)
           if (hi[t] >= 0) tl += hi[t] - lo[t] + 1;
@@ -252,6 +255,7 @@ TriSchedule build_tri_schedule(int n, const int* rp, const int* ci, const std::i
         for (int i = 0; i < n; ++i) tile_of[i] = best.perm[tile_of[i]];
         for (int d = 0; d < 3; ++d) B[d] = best.b[d];
         S.tile_layer = best.layer;
+        S.acyclic = !best.cyclic;
         ok = true;
       } else {
         assign(B);
@@ -276,6 +280,7 @@ TriSchedule build_tri_schedule(int n, const int* rp, const int* ci, const std::i
     }
   }
   if (S.ntiles == 0) {  // contiguous row blocks (dependencies only to earlier blocks)
+    S.acyclic = true;
     int T = std::min(cap, std::max(32, static_cast<int>(cdiv(std::max(n, 1), nsm))));
     if (tile_cap_override > 0) T = cap;
     S.ntiles = n > 0 ? static_cast<int>(cdiv(n, T)) : 1;

@@ -29,6 +29,7 @@ struct TriSchedule {
   int tile_cap = 0;          // max rows per tile (shared memory slots)
   int max_tile_rows = 0;     // largest tile actually built
   std::vector<int> tile_layer;  // wavefront ticket order: layer of each tile (empty: z-layers)
+  bool acyclic = false;         // every cross-tile dependency points to a strictly earlier ticket
   std::vector<int> tile_pbase;  // ntiles+1: first schedule slot of each tile
   std::vector<int> tile_seg;    // ntiles+1: first segment of each tile
   std::vector<int> seg_level;   // per segment (one DAG level of one tile)
