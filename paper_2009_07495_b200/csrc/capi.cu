@@ -405,6 +405,7 @@ void build_tri(igm_ctx* c, DevTri& t, int n, const int* rp, const int* ci, const
   t.p_diag = dupload(S.p_diag.data(), S.p_diag.size(), st);
   t.p_rec = dupload(S.p_rec.data(), S.p_rec.size(), st);
   t.rec_bytes = S.rec_bytes;
+  t.compact = S.compact;
   t.seg_xptr = dupload(S.seg_xptr.data(), S.seg_xptr.size(), st);
   t.seg_xrow = dupload(S.seg_xrow.data(), S.seg_xrow.size(), st);
   t.max_seg_ext = S.max_seg_ext;

@@ -89,6 +89,7 @@ struct DevTri {
   int* p_info = nullptr;
   unsigned char* p_rec = nullptr;  // packed records, rec_bytes each
   int rec_bytes = 0;
+  bool compact = false;            // compact records (schedule.hpp)
   ulonglong2* xz = nullptr;        // n tagged exported values (128-bit each)
   void* yperm = nullptr;           // n+2 right-hand-side values in schedule order (8 bytes each)
   u64* stats = nullptr;            // [max|y|, max|z|] of the current integer apply (device)

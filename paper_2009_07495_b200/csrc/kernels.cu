@@ -1695,6 +1695,8 @@ struct TriArgs {
   const int* p_xdep;      // dependencies beyond the record stride (rare)
   const i64* p_xval;
   const unsigned char* p_rec;  // packed per-slot records (schedule.hpp)
+  const int* p_xrp;            // compact records: extra-dependency index per slot
+  const i64* p_diag;           // compact records: diagonal per slot (FP path)
   int tile_cap, max_seg_ext;
   u64* zmax;                   // max |z| of the integer apply (checked mode's overflow bound)
   ulonglong2* xz;              // exported values: (value, epoch ^ value) per row
@@ -1835,9 +1837,14 @@ struct TriSmem {  // byte offsets of the dynamic shared-memory regions
 
 // zt (tile values) | segment starts | (spare) | ring of L slots
 // [records | rhs run] | mbarriers
-template <int MAXD>
+template <int MAXD, bool COMPACT>
+__host__ __device__ constexpr int tri_rec_bytes() {
+  return COMPACT ? 16 + 8 * MAXD : 32 + 12 * MAXD;
+}
+
+template <int MAXD, bool COMPACT>
 __host__ __device__ inline TriSmem tri_smem_layout(int tile_cap, int seg_cap, int L, int max_ext) {
-  constexpr int REC = 32 + 12 * MAXD;
+  constexpr int REC = tri_rec_bytes<MAXD, COMPACT>();
   TriSmem m;
   size_t o = (static_cast<size_t>(tile_cap) * 8 + 15) & ~size_t(15);
   m.rows = o;
@@ -1856,16 +1863,16 @@ __host__ __device__ inline TriSmem tri_smem_layout(int tile_cap, int seg_cap, in
   return m;
 }
 
-template <typename T, bool BACKWARD, int MAXD>
+template <typename T, bool BACKWARD, int MAXD, bool COMPACT>
 __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restrict__ yperm, T* out,
                                                      const Ctl* ctl, int seg_cap, int L, int pf) {
   constexpr bool FP = std::is_same<T, double>::value;
-  constexpr int REC = 32 + 12 * MAXD;
+  constexpr int REC = tri_rec_bytes<MAXD, COMPACT>();
   constexpr unsigned YOFF = kTriSegRows * REC;                 // rhs run in a ring slot
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ int s_tile;
   if (cycle_over(ctl)) return;
-  const TriSmem lay = tri_smem_layout<MAXD>(a.tile_cap, seg_cap, L, a.max_seg_ext);
+  const TriSmem lay = tri_smem_layout<MAXD, COMPACT>(a.tile_cap, seg_cap, L, a.max_seg_ext);
   unsigned zt_s = smem_u32(smem_raw);
   asm volatile("" : "+r"(zt_s));  // kept in a register (not re-derived from %cgactaid each level)
   int* s_rows = reinterpret_cast<int*>(smem_raw + lay.rows);
@@ -1975,21 +1982,45 @@ __global__ void __launch_bounds__(kTriThreads) k_tri(TriArgs a, const T* __restr
     if (tid >= s1 - s0) return;
     const unsigned ra = sl + my_rec;
     const int4 hdr = lds128i(ra);
-    r.row = hdr.x;
-    r.nd = hdr.y;
-    r.info = hdr.z;
-    r.xb = hdr.w;
-    lds128l(ra + 16, r.mag, r.diag);
+    if constexpr (COMPACT) {
+      r.row = hdr.x;
+      r.info = hdr.y & 0xffff;
+      r.nd = hdr.y >> 16;
+      r.mag = static_cast<i64>(static_cast<u64>(static_cast<unsigned>(hdr.z)) |
+                               (static_cast<u64>(static_cast<unsigned>(hdr.w)) << 32));
+      const int slot = s0 + tid;
+      r.xb = r.nd > MAXD ? __ldg(a.p_xrp + slot) : 0;
+      if constexpr (FP) r.diag = __ldg(a.p_diag + slot);  // used after the barrier
 #pragma unroll
-    for (int d = 0; d < MAXD; d += 4) {
-      const int4 c4 = lds128i(ra + 32 + 4 * d);
-      r.ci[d] = c4.x;
-      r.ci[d + 1] = c4.y;
-      r.ci[d + 2] = c4.z;
-      r.ci[d + 3] = c4.w;
+      for (int d = 0; d < MAXD; d += 4) {
+        const int4 c4 = lds128i(ra + 16 + 4 * d);
+        r.ci[d] = c4.x;
+        r.ci[d + 1] = c4.y;
+        r.ci[d + 2] = c4.z;
+        r.ci[d + 3] = c4.w;
+        const int4 v4 = lds128i(ra + 16 + 4 * MAXD + 4 * d);
+        r.v[d] = v4.x;
+        r.v[d + 1] = v4.y;
+        r.v[d + 2] = v4.z;
+        r.v[d + 3] = v4.w;
+      }
+    } else {
+      r.row = hdr.x;
+      r.nd = hdr.y;
+      r.info = hdr.z;
+      r.xb = hdr.w;
+      lds128l(ra + 16, r.mag, r.diag);
+#pragma unroll
+      for (int d = 0; d < MAXD; d += 4) {
+        const int4 c4 = lds128i(ra + 32 + 4 * d);
+        r.ci[d] = c4.x;
+        r.ci[d + 1] = c4.y;
+        r.ci[d + 2] = c4.z;
+        r.ci[d + 3] = c4.w;
+      }
+#pragma unroll
+      for (int d = 0; d < MAXD; d += 2) lds128l(ra + 32 + 4 * MAXD + 8 * d, r.v[d], r.v[d + 1]);
     }
-#pragma unroll
-    for (int d = 0; d < MAXD; d += 2) lds128l(ra + 32 + 4 * MAXD + 8 * d, r.v[d], r.v[d + 1]);
     r.y = lds64(sl + YOFF + 8u * static_cast<unsigned>(tid + (s0 & 1)));
     r.zaddr = zt_s + 8u * static_cast<unsigned>(s0 + tid - pb);
     r.have = true;
@@ -2161,6 +2192,8 @@ TriArgs tri_args(const DevTri& t) {
   a.p_xdep = t.p_xdep;
   a.p_xval = t.p_xval;
   a.p_rec = t.p_rec;
+  a.p_xrp = t.p_xrp;
+  a.p_diag = t.p_diag;
   a.tile_cap = t.tile_cap;
   a.max_seg_ext = t.max_seg_ext;
   a.xz = t.xz;
@@ -2525,7 +2558,7 @@ void launch_xupdate(cudaStream_t st, long long n, int m, int f, const i64* basis
   LAUNCH_CHECK();
 }
 
-template <typename T, bool B, int D>
+template <typename T, bool B, int D, bool CP>
 static void tri_launch_one(cudaStream_t st, const DevTri& t, const T* y, T* out, const Ctl* ctl,
                            const double* prescale) {
   constexpr size_t kBudget = 227 * 1024 - 256;  // static smem (tile id) excluded
@@ -2535,18 +2568,18 @@ static void tri_launch_one(cudaStream_t st, const DevTri& t, const T* y, T* out,
   }();
   const int L0 = env_L > 0 ? env_L : 8;
   int seg_cap = t.max_tile_segs + 2, L = L0;
-  TriSmem lay = tri_smem_layout<D>(t.tile_cap, seg_cap, L, t.max_seg_ext);
-  while (L > 1 && lay.total > kBudget) lay = tri_smem_layout<D>(t.tile_cap, seg_cap, --L, t.max_seg_ext);
+  TriSmem lay = tri_smem_layout<D, CP>(t.tile_cap, seg_cap, L, t.max_seg_ext);
+  while (L > 1 && lay.total > kBudget) lay = tri_smem_layout<D, CP>(t.tile_cap, seg_cap, --L, t.max_seg_ext);
   if (lay.total > kBudget) {  // segment tables stay in global memory
     seg_cap = 0;
     L = L0;
-    lay = tri_smem_layout<D>(t.tile_cap, seg_cap, L, t.max_seg_ext);
-    while (L > 1 && lay.total > kBudget) lay = tri_smem_layout<D>(t.tile_cap, seg_cap, --L, t.max_seg_ext);
+    lay = tri_smem_layout<D, CP>(t.tile_cap, seg_cap, L, t.max_seg_ext);
+    while (L > 1 && lay.total > kBudget) lay = tri_smem_layout<D, CP>(t.tile_cap, seg_cap, --L, t.max_seg_ext);
   }
   const size_t sm = lay.total;
   static size_t done = 0;
   if (sm > done) {
-    cudaFuncSetAttribute(k_tri<T, B, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_tri<T, B, D, CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     done = sm;
   }
   TriArgs args = tri_args(t);
@@ -2563,16 +2596,22 @@ static void tri_launch_one(cudaStream_t st, const DevTri& t, const T* y, T* out,
     const char* e = std::getenv("IGM_TRI_PF");
     return e ? std::atoi(e) : 12;
   }();
-  k_tri<T, B, D><<<t.ntiles, kTriThreads, sm, st>>>(args, static_cast<const T*>(t.yperm), out, ctl, seg_cap, L,
-                                                    env_pf);
+  k_tri<T, B, D, CP><<<t.ntiles, kTriThreads, sm, st>>>(args, static_cast<const T*>(t.yperm), out, ctl, seg_cap,
+                                                        L, env_pf);
 }
 
 template <typename T, bool B>
 static void tri_dispatch(cudaStream_t st, const DevTri& t, const T* y, T* out, const Ctl* ctl,
                          const double* prescale) {
-  if (t.stride == 4) tri_launch_one<T, B, 4>(st, t, y, out, ctl, prescale);
-  else if (t.stride == 8) tri_launch_one<T, B, 8>(st, t, y, out, ctl, prescale);
-  else tri_launch_one<T, B, 16>(st, t, y, out, ctl, prescale);
+  if (t.compact) {
+    if (t.stride == 4) tri_launch_one<T, B, 4, true>(st, t, y, out, ctl, prescale);
+    else if (t.stride == 8) tri_launch_one<T, B, 8, true>(st, t, y, out, ctl, prescale);
+    else tri_launch_one<T, B, 16, true>(st, t, y, out, ctl, prescale);
+  } else {
+    if (t.stride == 4) tri_launch_one<T, B, 4, false>(st, t, y, out, ctl, prescale);
+    else if (t.stride == 8) tri_launch_one<T, B, 8, false>(st, t, y, out, ctl, prescale);
+    else tri_launch_one<T, B, 16, false>(st, t, y, out, ctl, prescale);
+  }
 }
 
 void tri_trace_setup(int tile, unsigned long long* buf) {

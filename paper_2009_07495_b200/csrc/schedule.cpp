@@ -2,6 +2,7 @@
 #include "schedule.hpp"
 
 #include <array>
+#include <climits>
 #include <cstdint>
 
 #include "fx_core.cuh"
@@ -400,17 +401,32 @@ TriSchedule build_tri_schedule(int n, const int* rp, const int* ci, const std::i
     for (int p = 0; p < n; ++p)
       if (exported[order[p]]) S.p_info[p] |= 1 << 10;
   }
-  // packed records
-  S.rec_bytes = 32 + 12 * W;
+  // packed records (compact when every factor value fits in int32)
+  S.compact = !std::getenv("IGM_TRI_WIDE_REC");
+  for (size_t q = 0; q < S.p_val.size() && S.compact; ++q)
+    S.compact = S.p_val[q] >= INT32_MIN && S.p_val[q] <= INT32_MAX;
+  for (int p = 0; p < n && S.compact; ++p) S.compact = S.p_nd[p] <= 255;
+  S.rec_bytes = S.compact ? 16 + 8 * W : 32 + 12 * W;
   S.p_rec.assign(static_cast<size_t>(std::max(n, 1)) * S.rec_bytes, 0);
   for (int p = 0; p < n; ++p) {
     unsigned char* r = S.p_rec.data() + static_cast<size_t>(p) * S.rec_bytes;
-    const int hdr[4] = {S.p_row[p], S.p_nd[p], S.p_info[p], S.p_xrp[p]};
-    std::memcpy(r, hdr, 16);
-    std::memcpy(r + 16, &S.p_mag[p], 8);
-    std::memcpy(r + 24, &S.p_diag[p], 8);
-    std::memcpy(r + 32, &S.p_dep[static_cast<size_t>(p) * W], 4 * W);
-    std::memcpy(r + 32 + 4 * W, &S.p_val[static_cast<size_t>(p) * W], 8 * W);
+    if (S.compact) {
+      const int hdr[2] = {S.p_row[p], S.p_info[p] | (S.p_nd[p] << 16)};
+      std::memcpy(r, hdr, 8);
+      std::memcpy(r + 8, &S.p_mag[p], 8);
+      std::memcpy(r + 16, &S.p_dep[static_cast<size_t>(p) * W], 4 * W);
+      for (int d = 0; d < W; ++d) {
+        const int32_t v = static_cast<int32_t>(S.p_val[static_cast<size_t>(p) * W + d]);
+        std::memcpy(r + 16 + 4 * W + 4 * d, &v, 4);
+      }
+    } else {
+      const int hdr[4] = {S.p_row[p], S.p_nd[p], S.p_info[p], S.p_xrp[p]};
+      std::memcpy(r, hdr, 16);
+      std::memcpy(r + 16, &S.p_mag[p], 8);
+      std::memcpy(r + 24, &S.p_diag[p], 8);
+      std::memcpy(r + 32, &S.p_dep[static_cast<size_t>(p) * W], 4 * W);
+      std::memcpy(r + 32 + 4 * W, &S.p_val[static_cast<size_t>(p) * W], 8 * W);
+    }
   }
   // ---- per segment: producer tiles of its cross-tile dependencies
   S.seg_wptr.push_back(0);

@@ -49,6 +49,11 @@ struct TriSchedule {
   // the same per-slot data as one packed record (what the kernel streams):
   //   int32 row, nd, info, xb | u64 mag | i64 diag | int32 dep[stride] | i64 val[stride]
   int rec_bytes = 0;                 // 32 + 12*stride (multiple of 16)
+  // compact records (every factor value fits in int32, nd <= 255):
+  //   int32 row | int32 info | (nd << 16) | u64 mag | int32 dep[stride] | int32 val[stride]
+  // = 16 + 8*stride bytes; the rare extra-dependency index is read from p_xrp
+  // and the FP path's diagonal from p_diag
+  bool compact = false;
   std::vector<unsigned char> p_rec;  // n * rec_bytes
   // cross-tile dependencies of each segment: distinct producer rows; a
   // record's external dependency is encoded as ~(index into this list)
