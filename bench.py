@@ -59,10 +59,11 @@ def config2(g: int = 128):
 def setup_b200(rp, ci, v, bh, alpha=32):
     import paper_2009_07495_b200 as igm
     t0 = time.time()
-    vals, scale = igm.row_scale(rp, ci, v, alpha)
+    # device-side setup (bit-identical to the host code)
+    vals, scale = igm.row_scale_device(rp, ci, v, alpha)
     b = bh / scale
-    comp, al, _ = igm.build_split(vals, alpha, 1)
-    lower, upper = igm.factorize_split_cast(rp, ci, vals)
+    comp, al, _ = igm.build_split_device(vals, alpha, 1)
+    lower, upper = igm.factorize_split_cast_device(rp, ci, vals)
     setup_s = time.time() - t0
     S = igm.SplitMatrix(rp, ci, comp, al)
     A = igm.CsrMatrixF(rp, ci, vals)
@@ -373,6 +374,16 @@ def run_cfg5_sharded(args, igm, dev, local, rank, ws, g=400, k=30):
 
 
 # ----------------------------------------------------------------- B200 arm
+def measured_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full
+    capture summary (profiles/traffic.json), or None"""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(kernel, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
 def roofline_line(micro, dom, achieved, dom_bytes, hbm, src, top, breakdown):
     """Dominant HBM-streaming kernel: the MGS pass in the config-5 call (all
     operands from HBM); the config-2 view (L2-resident vectors) is attached."""
@@ -383,7 +394,8 @@ def roofline_line(micro, dom, achieved, dom_bytes, hbm, src, top, breakdown):
         m = micro["mgs"]
         return {"bound": "hbm", "kernel": "k_mgs (fused axpy_{i-1}+dot_i pass), config 5",
                 "achieved": m["GB/s"], "peak": hbm, "peak_source": src, "unit": "GB/s", "frac": m["frac"],
-                "traffic": None, "bytes_per_launch": m["bytes"] / max(1, m["launches"]), "cfg2": cfg2}
+                "traffic": measured_traffic("k_mgs_cfg5"), "bytes_per_launch": m["bytes"] / max(1, m["launches"]),
+                "cfg2": cfg2}
     return {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm, "peak_source": src,
             "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None, "cfg2": cfg2}
 
@@ -531,6 +543,7 @@ def main():
     ap.add_argument("--grid", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cfg5", action="store_true", help="skip the config-5 kernel microbench")
+    ap.add_argument("--only-cfg5", action="store_true", help="run only the config-5 microbench (profiling)")
     ap.add_argument("--cfg5-sharded", action="store_true",
                     help="at 1 GPU, also run the row-block partitioned config-5 driver")
     args = ap.parse_args()
@@ -538,6 +551,12 @@ def main():
     ws, rank, local = dist_init(args)
     if args.impl == "reference":
         return run_reference(args, ws, rank)
+    if args.only_cfg5:
+        import paper_2009_07495_b200 as igm
+        dev = igm.Device(local)
+        igm.Device._default = dev
+        print(json.dumps(run_cfg5(args, igm, dev, local)), flush=True)
+        return 0
     return run_b200(args, ws, rank, local)
 
 
