@@ -1,3 +1,4 @@
+mkdir -p gpurun_out/prof
 set -x
 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_rc=$?
 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-cfg5 > gpurun_out/prof/plain.json 2>/dev/null && \
