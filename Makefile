@@ -8,7 +8,7 @@ BUILD   := build
 LIB     := $(PKG)/libigm_b200.so
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -fmad=false -Iinclude
 CXXFLAGS:= -O2 -std=c++20 -fPIC -ffp-contract=off -fno-fast-math -Wall -Iinclude
-HDRS    := $(wildcard $(PKG)/csrc/*.cuh) $(PKG)/csrc/schedule.hpp include/igm.h $(wildcard include/intgmres/*.hpp)
+HDRS    := $(wildcard $(PKG)/csrc/*.cuh) $(PKG)/csrc/schedule.hpp $(PKG)/csrc/pencil.hpp include/igm.h $(wildcard include/intgmres/*.hpp)
 
 all: $(LIB) oracle
 

@@ -8,6 +8,7 @@
 // outer loop needs a scalar decision (refine.cpp:52-55, 85).
 #include "igm_internal.cuh"
 #include "schedule.hpp"
+#include "pencil.hpp"
 
 #include <algorithm>
 #include <climits>
@@ -424,6 +425,22 @@ void build_tri(igm_ctx* c, DevTri& t, int n, const int* rp, const int* ci, const
   }
   t.prog = dalloc<int>(S.ntiles);
   t.ticket = dalloc<int>(1);
+  if (S.grid[0] > 0 && env_int("IGM_PENCIL", 1) != 0) {  // structured 7-point: the pencil wavefront
+    const PencilStream P = build_pencil_stream(n, rp, ci, vals, dpos, upper, S.grid[0], S.grid[1], S.grid[2]);
+    if (P.ok) {
+      t.pen = true;
+      t.pen_gx = P.gx;
+      t.pen_gy = P.gy;
+      t.pen_gz = P.gz;
+      t.pen_nbx = P.nbx;
+      t.pen_nby = P.nby;
+      t.pen_nbricks = P.nbricks;
+      t.pen_S = P.S;
+      t.pen_pad = P.pad;
+      t.pen_blk = dupload(P.blk.data(), P.blk.size(), st);
+      t.pen_bot = dupload(P.brick_of_ticket.data(), P.brick_of_ticket.size(), st);
+    }
+  }
   ck(cudaStreamSynchronize(st), "upload_ilu sync");
 }
 
@@ -438,7 +455,7 @@ void free_tri(DevTri& t) {
                   static_cast<void*>(t.seg_xptr), static_cast<void*>(t.seg_xrow), static_cast<void*>(t.c_rp),
                   static_cast<void*>(t.c_ci), static_cast<void*>(t.c_val), static_cast<void*>(t.c_diag),
                   static_cast<void*>(t.prog), static_cast<void*>(t.yperm), static_cast<void*>(t.stats),
-                  static_cast<void*>(t.ticket)})
+                  static_cast<void*>(t.ticket), t.pen_blk, static_cast<void*>(t.pen_bot)})
     dfree(p);
   t = DevTri{};
 }

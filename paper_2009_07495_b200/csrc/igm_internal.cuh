@@ -101,6 +101,11 @@ struct DevTri {
   unsigned long long epoch = 0;    // launches so far (tag of the next one)
   bool acyclic = false;   // tile graph acyclic in ticket order (lookahead wavefront allowed)
   int* prog = nullptr;    // ntiles progress words
+  // structured 7-point factors: the pencil wavefront's stream (pencil.hpp)
+  bool pen = false;
+  int pen_gx = 0, pen_gy = 0, pen_gz = 0, pen_nbx = 0, pen_nby = 0, pen_nbricks = 0, pen_S = 0, pen_pad = 0;
+  void* pen_blk = nullptr;
+  int* pen_bot = nullptr;
   int* ticket = nullptr;  // 1
 };
 

@@ -8,8 +8,12 @@
 // cycle has already ended (break / error), so a whole cycle is enqueued
 // without host round trips.
 #include "igm_internal.cuh"
+#include "tri_pencil.cuh"
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <random>
 #include <climits>
 #include <cstdlib>
 #include <type_traits>
@@ -2619,6 +2623,57 @@ void tri_trace_setup(int tile, unsigned long long* buf) {
   cudaMemcpyToSymbol(g_tri_ts_tile, &tile, sizeof(int));
 }
 
+// Per-launch tag of the pencil wavefront: unique in the process and seeded
+// per process, because its in-CTA shared-memory words may meet words left on
+// the SM by an earlier kernel (of this or another factor, or process).
+static u64 pen_epoch() {
+  static std::atomic<u64> ctr{[] {
+    std::random_device rd;
+    return (static_cast<u64>(rd()) << 32) ^ rd() ^
+           static_cast<u64>(std::chrono::steady_clock::now().time_since_epoch().count());
+  }()};
+  u64 z = ctr.fetch_add(1) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return (z ^ (z >> 31)) | 1ull;
+}
+
+// pencil wavefront (tri_pencil.cuh) of a structured 7-point factor
+static void pen_launch(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out, const Ctl* ctl,
+                       bool checked) {
+  constexpr int D = 4, R = 16;
+  const size_t sm = pencil_smem_bytes(R, D);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_tri_pencil<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    cudaFuncSetAttribute(k_tri_pencil<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    attr = true;
+  }
+  PenArgs a;
+  a.gx = t.pen_gx;
+  a.gy = t.pen_gy;
+  a.gz = t.pen_gz;
+  a.nbx = t.pen_nbx;
+  a.nby = t.pen_nby;
+  a.S = t.pen_S;
+  a.R = R;
+  a.pad = t.pen_pad;
+  a.n = t.n;
+  a.mirror = backward ? 1 : 0;
+  a.rec = t.pen_blk;
+  a.brick_of_ticket = t.pen_bot;
+  a.xz = t.xz;
+  a.epoch = pen_epoch();
+  a.ticket = t.ticket;
+  a.stats = reinterpret_cast<unsigned long long*>(t.stats);
+  const int* stop = ctl ? &ctl->stop : nullptr;
+  const int* err = ctl ? &ctl->err : nullptr;
+  if (checked)
+    k_tri_pencil<D, true><<<t.pen_nbricks, kPenThreads, sm, st>>>(a, y, out, stop, err);
+  else
+    k_tri_pencil<D, false><<<t.pen_nbricks, kPenThreads, sm, st>>>(a, y, out, stop, err);
+}
+
 void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out,
                     u64* cnt, const Ctl* ctl, bool checked) {
   if (t.n == 0) return;
@@ -2626,7 +2681,8 @@ void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* 
   if (checked) cudaMemsetAsync(t.stats, 0, 2 * sizeof(u64), st);
   {
     ProfScope prof_(st, KC_TRI_INT);
-    if (backward) tri_dispatch<i64, true>(st, t, y, out, ctl, nullptr);
+    if (t.pen) pen_launch(st, t, backward, y, out, ctl, checked);
+    else if (backward) tri_dispatch<i64, true>(st, t, y, out, ctl, nullptr);
     else tri_dispatch<i64, false>(st, t, y, out, ctl, nullptr);
   }
   LAUNCH_CHECK();
