@@ -127,6 +127,14 @@ void igm_ilu_schedule_info(const igm_ilu* f, int backward, int* out8);
 int igm_debug_tri_schedule(int n, const int* row_ptr, const int* col_idx,
                            const int64_t* vals, const int* diag_pos, int upper,
                            int num_sms, int* out8);
+/* bricks of the pencil wavefront (structured 7-point factor, csrc/pencil.hpp)
+ * that apply_inverse uses for this substitution; 0 = the generic wavefront */
+int igm_ilu_pencil(const igm_ilu* f, int backward);
+/* CPU-only: build the pencil record stream of one factor on a gx*gy*gz grid
+ * (host arrays); returns 1 if the factor has the 7-point structure, then
+ * out4 = {bricks, steps per warp, bricks in x, bricks in y} */
+int igm_debug_pencil_stream(int n, const int* row_ptr, const int* col_idx, const int64_t* vals,
+                            const int* diag_pos, int upper, int gx, int gy, int gz, int* out4);
 /* debug: per-segment phase timestamps of one ILU tile (8 u64 per segment) */
 void igm_debug_tri_trace(int tile, unsigned long long* device_buf);
 

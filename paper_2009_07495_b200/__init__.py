@@ -212,6 +212,10 @@ class IluFactors:
     def levels(self, backward: bool = False) -> int:
         return int(lib().igm_ilu_levels(self.h, 1 if backward else 0))
 
+    def pencil_bricks(self, backward: bool = False) -> int:
+        """Bricks of the pencil wavefront used for this substitution (0: generic wavefront)."""
+        return int(lib().igm_ilu_pencil(self.h, 1 if backward else 0))
+
     def schedule_info(self, backward: bool = False) -> dict:
         out = (C.c_int32 * 8)()
         lib().igm_ilu_schedule_info(self.h, 1 if backward else 0, out)

@@ -119,6 +119,9 @@ SIGNATURES = [
     ("igm_ilu_free", None, [C.c_void_p]),
     ("igm_ilu_levels", C.c_int, [C.c_void_p, C.c_int]),
     ("igm_ilu_schedule_info", None, [C.c_void_p, C.c_int, i32p]),
+    ("igm_ilu_pencil", C.c_int, [C.c_void_p, C.c_int]),
+    ("igm_debug_pencil_stream", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                          C.c_int, C.c_int, C.c_int, i32p]),
     ("igm_debug_tri_trace", None, [C.c_int, C.c_void_p]),
     ("igm_debug_tri_schedule", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                          C.c_int, i32p]),

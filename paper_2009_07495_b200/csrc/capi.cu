@@ -799,6 +799,23 @@ void igm_ilu_free(igm_ilu* f) {
   delete f;
 }
 
+int igm_ilu_pencil(const igm_ilu* f, int backward) {
+  if (!f) return 0;
+  const DevTri& t = backward ? f->upper : f->lower;
+  return t.pen ? t.pen_nbricks : 0;
+}
+
+int igm_debug_pencil_stream(int n, const int* rp, const int* ci, const int64_t* vals, const int* dpos, int upper,
+                            int gx, int gy, int gz, int* out4) {
+  const PencilStream P = build_pencil_stream(n, rp, ci, vals, dpos, upper != 0, gx, gy, gz);
+  if (!P.ok) return 0;
+  out4[0] = P.nbricks;
+  out4[1] = P.S;
+  out4[2] = P.nbx;
+  out4[3] = P.nby;
+  return 1;
+}
+
 int igm_ilu_levels(const igm_ilu* f, int backward) {
   return f ? (backward ? f->upper.nlevels : f->lower.nlevels) : 0;
 }

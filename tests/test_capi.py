@@ -151,3 +151,39 @@ def test_cpp_matrix_market_io(product_lib, tmp_path):
                    capture_output=True, text=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
     assert out.stdout.strip() == "ok", out.stdout + out.stderr
+
+
+def _pencil_info(product_lib, lo, upper, dims):
+    rp, ci, v, dp = [np.ascontiguousarray(a, dt) for a, dt in zip(lo, (np.int32, np.int32, np.int64, np.int32))]
+    out = (C.c_int * 4)()
+    ok = product_lib.igm_debug_pencil_stream(len(rp) - 1, rp.ctypes.data_as(C.c_void_p), ci.ctypes.data_as(C.c_void_p),
+                                             v.ctypes.data_as(C.c_void_p), dp.ctypes.data_as(C.c_void_p), int(upper),
+                                             *dims, out)
+    return ok, list(out)
+
+
+def test_pencil_stream_structure(product_lib, igm):
+    """The pencil wavefront applies exactly to 7-point factors on the grid
+    (csrc/pencil.hpp): bricks of 16 x 8 pencils, gz + 16 steps per warp;
+    27-point factors, wrong grids and factor values beyond int32 fall back to
+    the generic wavefront."""
+    from workloads import gen
+    for dims in ((12, 12, 12), (17, 35, 9), (40, 3, 5)):
+        offs = [(0, 0, -1), (0, -1, 0), (-1, 0, 0), (0, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 1)]
+        rp, ci, v = gen._stencil_csr(dims, offs, lambda o, r: np.full(r.shape, 7.0 if o == 3 else -1.0))
+        vals, _ = igm.row_scale(rp, ci, v, 32)
+        lo, up = igm.factorize_split_cast(rp, ci, vals)
+        for f, upper in ((lo, False), (up, True)):
+            ok, info = _pencil_info(product_lib, f, upper, dims)
+            assert ok == 1
+            assert info == [-(-dims[0] // 16) * -(-dims[1] // 8), dims[2] + 16, -(-dims[0] // 16), -(-dims[1] // 8)]
+        assert _pencil_info(product_lib, lo, False, (dims[1], dims[0], dims[2]))[0] == (dims[0] == dims[1])
+        big = (lo[0], lo[1], lo[2].copy(), lo[3])
+        assert lo[3][5] == lo[0][5] + 1  # row 5 = (5, 0, 0): its -x entry, then the diagonal
+        big[2][lo[0][5]] = 1 << 40
+        assert _pencil_info(product_lib, big, False, dims)[0] == 0
+    rp, ci, v = gen.stencil27(8, 3)
+    vals, _ = igm.row_scale(rp, ci, v, 32)
+    lo, up = igm.factorize_split_cast(rp, ci, vals)
+    assert _pencil_info(product_lib, lo, False, (8, 8, 8))[0] == 0
+    assert _pencil_info(product_lib, up, True, (8, 8, 8))[0] == 0

@@ -4,6 +4,7 @@ word (basis, Hessenberg, g, rotations, SpMV / ILU outputs) and on the FP64
 bookends (x, residual history) -- the FP kernels reproduce the reference's
 operation order with no contraction."""
 import hashlib
+import os
 import re
 
 import numpy as np
@@ -741,3 +742,38 @@ def test_exact_overflow_counts(gpu, oracle):
         assert t.exact and t.total_overflows() == to.total > 0
     finally:
         dev.set_exact_overflow_counts(False)
+
+
+_PENCIL_SHAPES = [(12, 12, 12), (17, 35, 9), (16, 16, 40), (33, 9, 20), (5, 70, 3), (2, 2, 50), (64, 64, 1)]
+
+
+@pytest.mark.parametrize("dims", _PENCIL_SHAPES, ids=["x".join(map(str, d)) for d in _PENCIL_SHAPES])
+def test_ilu_pencil_wavefront(gpu, oracle, dims):
+    """The structured 7-point pencil wavefront (csrc/tri_pencil.cuh) on ragged
+    grids (partial bricks in x and y, short and single-plane z): bit-exact vs
+    the oracle's sequential substitution (ilu.cpp:122-155), integer with and
+    without wrapping, checked-mode event totals, repeated launches, and equal
+    to the generic wavefront on the same factors."""
+    offs = _SEVEN if dims[2] > 1 else [o for o in _SEVEN if o[2] == 0]
+    lo, up = _grid_factors(gpu, dims, offs, seed=7 + sum(dims))
+    F = gpu.IluFactors(lo, up)
+    assert F.pencil_bricks(False) > 0 and F.pencil_bricks(True) > 0
+    il = oracle.ilu(lo, up)
+    n = len(lo[0]) - 1
+    from workloads import gen
+    for seed, mag in ((21, 45), (22, 62)):
+        y = gen.uniform_int(seed, n, -(1 << mag), 1 << mag)
+        t1, t2 = gpu.FxTrace(), PyTrace()
+        want = oracle.apply_inverse(il, y, t2)
+        for _ in range(2):
+            assert np.array_equal(gpu.apply_inverse(F, y), want)
+        assert np.array_equal(gpu.apply_inverse(F, y, t1), want)
+        assert t1.total_overflows() == t2.total
+    os.environ["IGM_PENCIL"] = "0"
+    try:
+        G = gpu.IluFactors(lo, up)
+    finally:
+        del os.environ["IGM_PENCIL"]
+    assert G.pencil_bricks(False) == 0
+    y = gen.uniform_int(23, n, -(1 << 50), 1 << 50)
+    assert np.array_equal(gpu.apply_inverse(G, y), gpu.apply_inverse(F, y))
