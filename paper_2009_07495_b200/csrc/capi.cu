@@ -438,6 +438,8 @@ void build_tri(igm_ctx* c, DevTri& t, int n, const int* rp, const int* ci, const
       t.pen_S = P.S;
       t.pen_pad = P.pad;
       t.pen_blk = dupload(P.blk.data(), P.blk.size(), st);
+      const PencilStream Q = build_pencil_stream(n, rp, ci, vals, dpos, upper, S.grid[0], S.grid[1], S.grid[2], 16, true);
+      if (Q.ok) t.pen_blk_fp = dupload(Q.blk.data(), Q.blk.size(), st);
       t.pen_bot = dupload(P.brick_of_ticket.data(), P.brick_of_ticket.size(), st);
     }
   }
@@ -455,7 +457,7 @@ void free_tri(DevTri& t) {
                   static_cast<void*>(t.seg_xptr), static_cast<void*>(t.seg_xrow), static_cast<void*>(t.c_rp),
                   static_cast<void*>(t.c_ci), static_cast<void*>(t.c_val), static_cast<void*>(t.c_diag),
                   static_cast<void*>(t.prog), static_cast<void*>(t.yperm), static_cast<void*>(t.stats),
-                  static_cast<void*>(t.ticket), t.pen_blk, static_cast<void*>(t.pen_bot)})
+                  static_cast<void*>(t.ticket), t.pen_blk, t.pen_blk_fp, static_cast<void*>(t.pen_bot)})
     dfree(p);
   t = DevTri{};
 }

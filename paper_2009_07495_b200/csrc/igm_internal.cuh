@@ -105,6 +105,7 @@ struct DevTri {
   bool pen = false;
   int pen_gx = 0, pen_gy = 0, pen_gz = 0, pen_nbx = 0, pen_nby = 0, pen_nbricks = 0, pen_S = 0, pen_pad = 0;
   void* pen_blk = nullptr;
+  void* pen_blk_fp = nullptr;  // the FP64 substitution's stream (diagonal as a double)
   int* pen_bot = nullptr;
   int* ticket = nullptr;  // 1
 };

@@ -2638,15 +2638,17 @@ static u64 pen_epoch() {
   return (z ^ (z >> 31)) | 1ull;
 }
 
-// pencil wavefront (tri_pencil.cuh) of a structured 7-point factor
-static void pen_launch(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out, const Ctl* ctl,
-                       bool checked) {
+// pencil wavefront (tri_pencil.cuh) of a structured 7-point factor: integer
+// (FP = false) or FP64 (apply_inverse_fp) substitution
+template <bool FP>
+static void pen_launch(cudaStream_t st, const DevTri& t, bool backward, const void* y, void* out, const Ctl* ctl,
+                       bool checked, const double* prescale) {
   constexpr int D = 4, R = 16;
   const size_t sm = pencil_smem_bytes(R, D);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_tri_pencil<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-    cudaFuncSetAttribute(k_tri_pencil<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    cudaFuncSetAttribute(k_tri_pencil<D, true, FP>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    cudaFuncSetAttribute(k_tri_pencil<D, false, FP>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
     attr = true;
   }
   PenArgs a;
@@ -2660,7 +2662,7 @@ static void pen_launch(cudaStream_t st, const DevTri& t, bool backward, const i6
   a.pad = t.pen_pad;
   a.n = t.n;
   a.mirror = backward ? 1 : 0;
-  a.rec = t.pen_blk;
+  a.rec = FP ? t.pen_blk_fp : t.pen_blk;
   a.brick_of_ticket = t.pen_bot;
   a.xz = t.xz;
   a.epoch = pen_epoch();
@@ -2668,10 +2670,12 @@ static void pen_launch(cudaStream_t st, const DevTri& t, bool backward, const i6
   a.stats = reinterpret_cast<unsigned long long*>(t.stats);
   const int* stop = ctl ? &ctl->stop : nullptr;
   const int* err = ctl ? &ctl->err : nullptr;
-  if (checked)
-    k_tri_pencil<D, true><<<t.pen_nbricks, kPenThreads, sm, st>>>(a, y, out, stop, err);
+  const i64* yi = static_cast<const i64*>(y);
+  i64* oi = static_cast<i64*>(out);
+  if (checked && !FP)
+    k_tri_pencil<D, true, FP><<<t.pen_nbricks, kPenThreads, sm, st>>>(a, yi, oi, stop, err, prescale);
   else
-    k_tri_pencil<D, false><<<t.pen_nbricks, kPenThreads, sm, st>>>(a, y, out, stop, err);
+    k_tri_pencil<D, false, FP><<<t.pen_nbricks, kPenThreads, sm, st>>>(a, yi, oi, stop, err, prescale);
 }
 
 void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out,
@@ -2681,7 +2685,7 @@ void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* 
   if (checked) cudaMemsetAsync(t.stats, 0, 2 * sizeof(u64), st);
   {
     ProfScope prof_(st, KC_TRI_INT);
-    if (t.pen) pen_launch(st, t, backward, y, out, ctl, checked);
+    if (t.pen) pen_launch<false>(st, t, backward, y, out, ctl, checked, nullptr);
     else if (backward) tri_dispatch<i64, true>(st, t, y, out, ctl, nullptr);
     else tri_dispatch<i64, false>(st, t, y, out, ctl, nullptr);
   }
@@ -2699,7 +2703,8 @@ void launch_tri_fp(cudaStream_t st, const DevTri& t, bool backward, const double
   if (t.n == 0) return;
   cudaMemsetAsync(t.ticket, 0, sizeof(int), st);
   ProfScope prof_(st, KC_TRI_FP);
-  if (backward) tri_dispatch<double, true>(st, t, y, out, ctl, prescale);
+  if (t.pen && t.pen_blk_fp) pen_launch<true>(st, t, backward, y, out, ctl, false, prescale);
+  else if (backward) tri_dispatch<double, true>(st, t, y, out, ctl, prescale);
   else tri_dispatch<double, false>(st, t, y, out, ctl, prescale);
   LAUNCH_CHECK();
 }

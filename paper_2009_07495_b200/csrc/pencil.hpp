@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstring>
 #include <vector>
 
 #include "fx_core.cuh"
@@ -40,9 +41,9 @@ struct PencilStream {
   std::vector<int> brick_of_ticket;  // (by << 16) | bx, wavefront order (bx+by, then bx)
 };
 
-// info bits: sh1 | sh2 << 1 | den_neg << 8 | active << 9
-inline std::int32_t pencil_info(const SDivMagic& g, bool active) {
-  return (g.u.sh1 & 1) | ((g.u.sh2 & 127) << 1) | (g.den_neg << 8) | (active ? 1 << 9 : 0);
+// info bits: sh1 | sh2 << 1 | den_neg << 8 | active << 9 | entry present toward -x, -y, -z << 10..12
+inline std::int32_t pencil_info(const SDivMagic& g, bool active, int present = 0) {
+  return (g.u.sh1 & 1) | ((g.u.sh2 & 127) << 1) | (g.den_neg << 8) | (active ? 1 << 9 : 0) | (present << 10);
 }
 
 // rp/ci/vals: the factor with its diagonal (dpos), natural row order; upper =
@@ -50,7 +51,8 @@ inline std::int32_t pencil_info(const SDivMagic& g, bool active) {
 // structure on the given grid, a factor value does not fit in int32, or a
 // row has a duplicate column: the generic wavefront handles those.
 inline PencilStream build_pencil_stream(int n, const int* rp, const int* ci, const std::int64_t* vals,
-                                        const int* dpos, bool upper, int gx, int gy, int gz, int pad = 16) {
+                                        const int* dpos, bool upper, int gx, int gy, int gz, int pad = 16,
+                                        bool fp = false) {
   PencilStream P;
   if (gx < 2 || gy < 2 || gz < 1 || static_cast<long long>(gx) * gy * gz != n || gx > 0xffff * kPenX ||
       gy > 0x7fff * kPenY)
@@ -59,6 +61,8 @@ inline PencilStream build_pencil_stream(int n, const int* rp, const int* ci, con
   // per solve-order row: factor values toward -x, -y, -z
   std::vector<std::int32_t> f(static_cast<size_t>(n) * 3, 0);
   std::vector<SDivMagic> dm(static_cast<size_t>(n));
+  std::vector<double> dd(fp ? static_cast<size_t>(n) : 0);
+  std::vector<unsigned char> pres(static_cast<size_t>(n), 0);
   for (int r = 0; r < n; ++r) {
     const long long rs = upper ? n - 1 - r : r;  // solve-order index of natural row r
     const long long i = rs % gx, j = (rs / gx) % gy, k = rs / plane;
@@ -77,12 +81,14 @@ inline PencilStream build_pencil_stream(int n, const int* rp, const int* ci, con
       else return P;
       if (seen[slot]) return P;
       seen[slot] = true;
+      pres[static_cast<size_t>(rs)] |= static_cast<unsigned char>(1 << slot);
       const std::int64_t v = vals[q];
       if (v < INT32_MIN || v > INT32_MAX) return P;
       f[static_cast<size_t>(rs) * 3 + slot] = static_cast<std::int32_t>(v);
     }
     if (dpos[r] < rp[r] || dpos[r] >= rp[r + 1] || ci[dpos[r]] != r || vals[dpos[r]] == 0) return P;
     dm[static_cast<size_t>(rs)] = make_sdiv(vals[dpos[r]]);
+    if (fp) dd[static_cast<size_t>(rs)] = static_cast<double>(vals[dpos[r]]);
   }
   P.gx = gx;
   P.gy = gy;
@@ -117,11 +123,17 @@ inline PencilStream build_pencil_stream(int n, const int* rp, const int* ci, con
             rr[0] = f[rs * 3];
             rr[1] = f[rs * 3 + 1];
             rr[2] = f[rs * 3 + 2];
-            rr[3] = pencil_info(dm[rs], true);
-            *mm = dm[rs].u.m;
+            rr[3] = pencil_info(dm[rs], true, pres[rs]);
+            if (fp) std::memcpy(mm, &dd[rs], 8);
+            else *mm = dm[rs].u.m;
           } else {  // idle lane-step: 0 / 1 = 0, nothing stored
             rr[3] = pencil_info(one, false);
-            *mm = one.u.m;
+            if (fp) {
+              const double d1 = 1.0;
+              std::memcpy(mm, &d1, 8);
+            } else {
+              *mm = one.u.m;
+            }
           }
         }
   }

@@ -94,9 +94,17 @@ __device__ unsigned long long g_pen_cnt[kPenWarps * 4];
 // prefetch ring: per step D slot of 16 KB = four 16-byte fields x 256 lanes
 constexpr unsigned kPenFRec = 0, kPenFMy = 4096, kPenFXi = 8192, kPenFYi = 12288, kPenStep = 16384;
 
-template <int D, bool CHECKED>
+// FP: the same substitutions in FP64 on the integer factors (apply_inverse_fp,
+// ilu.cpp:157-180): acc = y (optionally / gamma, refine.cpp:17), acc -= L_rd
+// * z_d over the row's entries in CSR order (-z, -y, -x for the lower factor;
+// +x, +y, +z for the upper), then acc / diag, every operation rounded on its
+// own (no contraction); absent entries are skipped, not subtracted as zero
+// (a -0 rhs must stay -0).  The stream's reciprocal field holds the diagonal
+// as a double.
+template <int D, bool CHECKED, bool FP>
 __global__ void __launch_bounds__(kPenThreads, 1)
-    k_tri_pencil(PenArgs a, const i64* __restrict__ y, i64* __restrict__ out, const int* stop, const int* err) {
+    k_tri_pencil(PenArgs a, const i64* __restrict__ y, i64* __restrict__ out, const int* stop, const int* err,
+                 const double* prescale) {
   extern __shared__ __align__(16) unsigned char pen_smem[];
   __shared__ int s_t;
   __shared__ volatile int s_prog[kPenWarps];
@@ -184,13 +192,13 @@ __global__ void __launch_bounds__(kPenThreads, 1)
   unsigned cslot = 0;
   i64 zc = 0;
   u64 ymx = 0, zmx = 0;
+  const double gam = prescale != nullptr ? *prescale : 1.0;
   int cons_seen = 0;  // last observed progress of warp w+1 (ring back-pressure)
 #pragma unroll 1
   for (int s = 0; s < S; ++s) {
 #ifdef PEN_TRACE
     if (t == 0 && lane == 0 && s < 4096) g_pen_ts[w * 4096 + s] = clock64();
 #endif
-    issue();
     const int k = s - kb;
     const bool act = static_cast<unsigned>(s - sa) < static_cast<unsigned>(gz);
     const unsigned rs = (static_cast<unsigned>(k) & Rm) * 256u;
@@ -198,7 +206,7 @@ __global__ void __launch_bounds__(kPenThreads, 1)
     __syncwarp();  // reconverge after a (rare) divergent stale path: the shuffles' fast path
     const i64 zxs = __shfl_up_sync(0xffffffffu, zc, 1);
     const i64 zys = __shfl_xor_sync(0xffffffffu, zc, 16);
-    asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(D - 2) : "memory");  // this step's group (the newest is s + D - 2)
     const unsigned d = pre0 + cslot;
     // the lane's -y source: warp w-1's ring slot or the prefetched import word
     const bool pys = (ycons || yin) && act, pxs = xin && act;
@@ -222,6 +230,7 @@ __global__ void __launch_bounds__(kPenThreads, 1)
         : "=l"(xv), "=l"(xt)
         : "r"(d + kPenFXi), "r"((int)pxs)
         : "memory");
+    issue();  // the prefetch of step s + D - 1: its slot was read last step
     if ((pys && vt != (want ^ vv)) || (pxs && xt != (want ^ xv))) {  // not there yet when fetched (rare)
       if (pxs)
         while (xt != (want ^ xv)) pen_xz_load(ep - 1, xv, xt);
@@ -234,17 +243,37 @@ __global__ void __launch_bounds__(kPenThreads, 1)
     }
     const i64 zx = xl == 0 ? static_cast<i64>(xv) : zxs;
     const i64 zy = jj == 0 ? static_cast<i64>(vv) : zys;
-    const u64 sx = static_cast<u64>(static_cast<i64>(rc.x)) * static_cast<u64>(zx) +
-                   static_cast<u64>(static_cast<i64>(rc.y)) * static_cast<u64>(zy) +
-                   static_cast<u64>(static_cast<i64>(rc.z)) * static_cast<u64>(zc);
-    const i64 acc = static_cast<i64>(yv - sx);
-    SDivMagic gm;
-    gm.u.m = mg;
-    gm.u.sh1 = rc.w & 1;
-    gm.u.sh2 = (rc.w >> 1) & 127;
-    gm.den_neg = (rc.w >> 8) & 1;
-    gm.den_is_m1 = 0;
-    const i64 z = sdiv(acc, gm);
+    i64 z;
+    if constexpr (FP) {
+      double acc = __longlong_as_double(static_cast<long long>(yv));
+      if (prescale != nullptr) acc = __ddiv_rn(acc, gam);
+      auto term = [&](double c, int f, i64 zb, int bit) {
+        const double t = __dsub_rn(c, __dmul_rn(static_cast<double>(f), __longlong_as_double(zb)));
+        return (rc.w >> bit) & 1 ? t : c;
+      };
+      if (a.mirror) {  // upper factor: +x, +y, +z columns ascending
+        acc = term(acc, rc.x, zx, 10);
+        acc = term(acc, rc.y, zy, 11);
+        acc = term(acc, rc.z, zc, 12);
+      } else {         // lower factor: -z, -y, -x columns ascending
+        acc = term(acc, rc.z, zc, 12);
+        acc = term(acc, rc.y, zy, 11);
+        acc = term(acc, rc.x, zx, 10);
+      }
+      z = __double_as_longlong(__ddiv_rn(acc, __longlong_as_double(static_cast<long long>(mg))));
+    } else {
+      const u64 sx = static_cast<u64>(static_cast<i64>(rc.x)) * static_cast<u64>(zx) +
+                     static_cast<u64>(static_cast<i64>(rc.y)) * static_cast<u64>(zy) +
+                     static_cast<u64>(static_cast<i64>(rc.z)) * static_cast<u64>(zc);
+      const i64 acc = static_cast<i64>(yv - sx);
+      SDivMagic gm;
+      gm.u.m = mg;
+      gm.u.sh1 = rc.w & 1;
+      gm.u.sh2 = (rc.w >> 1) & 127;
+      gm.den_neg = (rc.w >> 8) & 1;
+      gm.den_is_m1 = 0;
+      z = sdiv(acc, gm);
+    }
     if (yprod && s - a.R > cons_seen) {  // ring slot of row k - R must have been read by warp w+1
       do {
         cons_seen = s_prog[w + 1];
@@ -264,7 +293,7 @@ __global__ void __launch_bounds__(kPenThreads, 1)
         "@p st.volatile.shared.v2.u64 [%0], {%1, %2}; }" ::"r"(ring_prod + rs),
         "l"(z), "l"(tg), "r"((int)(act && pprod))
         : "memory");
-    if constexpr (CHECKED) {  // magnitude bounds: OR of v ^ (v >> 63) (idle lanes contribute 0)
+    if constexpr (CHECKED && !FP) {  // magnitude bounds: OR of v ^ (v >> 63) (idle lanes contribute 0)
       ymx |= yv ^ static_cast<u64>(static_cast<i64>(yv) >> 63);
       zmx |= static_cast<u64>(z ^ (z >> 63));
     }
@@ -278,7 +307,7 @@ __global__ void __launch_bounds__(kPenThreads, 1)
     cslot = cslot + kPenStep == D * kPenStep ? 0 : cslot + kPenStep;
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
-  if constexpr (CHECKED) {  // |v| <= (v ^ (v >> 63)) + 1
+  if constexpr (CHECKED && !FP) {  // |v| <= (v ^ (v >> 63)) + 1
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       ymx |= static_cast<u64>(__shfl_down_sync(0xffffffffu, ymx, o));

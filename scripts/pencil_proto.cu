@@ -48,7 +48,7 @@ static float run(const PencilStream& PS, int n, bool upper, const std::vector<i6
   CK(cudaMemcpy(d_y, y.data(), static_cast<size_t>(n) * 8, cudaMemcpyHostToDevice));
   CK(cudaMemset(d_xz, 0, static_cast<size_t>(n) * 16));
   const size_t sm = pencil_smem_bytes(R, P);
-  CK(cudaFuncSetAttribute(k_tri_pencil<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+  CK(cudaFuncSetAttribute(k_tri_pencil<P, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
   PenArgs a;
   a.gx = PS.gx;
   a.gy = PS.gy;
@@ -74,7 +74,7 @@ static float run(const PencilStream& PS, int n, bool upper, const std::vector<i6
     CK(cudaMemset(d_ticket, 0, 4));
     CK(cudaMemset(d_z, 0x5a, static_cast<size_t>(n) * 8));
     cudaEventRecord(e0);
-    k_tri_pencil<P, true><<<PS.nbricks, kPenThreads, sm>>>(a, d_y, d_z, nullptr, nullptr);
+    k_tri_pencil<P, true, false><<<PS.nbricks, kPenThreads, sm>>>(a, d_y, d_z, nullptr, nullptr, nullptr);
     cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1));
     CK(cudaGetLastError());

@@ -769,6 +769,12 @@ def test_ilu_pencil_wavefront(gpu, oracle, dims):
             assert np.array_equal(gpu.apply_inverse(F, y), want)
         assert np.array_equal(gpu.apply_inverse(F, y, t1), want)
         assert t1.total_overflows() == t2.total
+    # FP64 substitution on the integer factors (apply_inverse_fp), with -0.0
+    # and tiny right-hand sides: absent stencil entries must not be applied
+    yf = gen.uniform(24, n)
+    yf[::7] = -0.0
+    yf[3::11] = 5e-324
+    assert np.array_equal(gpu.apply_inverse_fp(F, yf).view(np.int64), oracle.apply_inverse_fp(il, yf).view(np.int64))
     os.environ["IGM_PENCIL"] = "0"
     try:
         G = gpu.IluFactors(lo, up)
