@@ -133,6 +133,7 @@ struct Work {
   unsigned char* small = nullptr;
   size_t small_bytes = 0;
   u64 *acc = nullptr, *absacc = nullptr, *nacc = nullptr, *nabs = nullptr, *cnt = nullptr;
+  u64* vmx = nullptr;  // per CTA and basis vector: max |v_i| over the CTA's rows (k_arnoldi certificates)
   i64 *hess = nullptr, *g = nullptr, *cs = nullptr, *sn = nullptr, *gabs = nullptr;
   int* steprec = nullptr;
   double *y = nullptr, *wts = nullptr, *bnorms = nullptr;
@@ -189,7 +190,7 @@ namespace {
 
 void ws_free(Work& w) {
   dfree(w.basis); dfree(w.w); dfree(w.z); dfree(w.vin); dfree(w.r); dfree(w.r0); dfree(w.t1);
-  dfree(w.x); dfree(w.b); dfree(w.x0); dfree(w.small);
+  dfree(w.x); dfree(w.b); dfree(w.x0); dfree(w.small); dfree(w.vmx);
   if (w.h_small) cudaFreeHost(w.h_small);
   w = Work{};
 }
@@ -214,6 +215,7 @@ void ws_ensure(igm_ctx* c, long long n, int m) {
   w.x = dalloc<double>(nn);
   w.b = dalloc<double>(nn);
   w.x0 = dalloc<double>(nn);
+  w.vmx = dalloc<u64>(static_cast<size_t>(1024) * (mm + 2));
   // small arrays
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes); return o; };
@@ -536,7 +538,7 @@ void enqueue_cycle(igm_ctx* c, const CycleParams& p, CycleMode mode, const doubl
     u64* absj = w.absacc + static_cast<size_t>(j) * (M + 1) * 2;
     if (arn_S > 0) {  // one persistent launch: passes, scalar work and vec_div
       launch_arnoldi(st, n, j, arn_S, w.w, w.basis, accj, absj, w.nacc + j, w.nabs + 2 * j, f, sh, cstep, w.hess, ld,
-                     w.g, w.cs, w.sn, w.gabs, ctl, gbase, p.checked);
+                     w.g, w.cs, w.sn, w.gabs, ctl, gbase, p.checked, w.vmx);
       gbase += static_cast<unsigned>(arnoldi_barriers(j));
       continue;
     }

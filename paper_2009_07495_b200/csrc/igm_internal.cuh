@@ -199,7 +199,7 @@ long long arnoldi_slice(long long n, int device);
 int arnoldi_barriers(int j);
 void launch_arnoldi(cudaStream_t st, long long n, int j, long long S, const i64* w, i64* basis, u64* accj,
                     u64* absj, u64* nacc, u64* nabs, int f, ShiftsD sh, u64* cstep, i64* hess, int ld, i64* g,
-                    i64* cs, i64* sn, i64* gabs, Ctl* ctl, unsigned gbase, bool checked);
+                    i64* cs, i64* sn, i64* gabs, Ctl* ctl, unsigned gbase, bool checked, u64* vmx);
 void launch_basis_norms(cudaStream_t st, long long n, int nb, int f,
                         const i64* basis, void* scratch, double* out, Ctl* ctl);
 

@@ -1420,7 +1420,7 @@ template <bool CHECKED>
 __global__ void __launch_bounds__(kArnThreads, 1)
     k_arnoldi(long long n, int j, long long S, const i64* __restrict__ win, i64* basis, u64* accj, u64* absj,
               u64* nacc, u64* nabs, int f, ShiftsD sh, u64* cstep, i64* hess, int ld, i64* g, i64* cs, i64* sn,
-              i64* gabs, Ctl* ctl, unsigned gbase) {
+              i64* gabs, Ctl* ctl, unsigned gbase, u64* vmx) {
   extern __shared__ __align__(16) i64 arn_sm[];
   __shared__ u64 red[3][32];
   __shared__ u64 s_word;
@@ -1447,22 +1447,67 @@ __global__ void __launch_bounds__(kArnThreads, 1)
     if (k == 4) sts_q(p, v);
     else *p = v[0];
   };
-  auto dot_term = [&](i64 wl, i64 c, ArnAcc& A) {
+  // OVF: per-element product / subtraction overflow tests.  In checked mode
+  // a pass runs without them when this CTA's magnitude bounds prove none of
+  // its rows can overflow (certify() below); the sum |t| certificate of the
+  // order-dependent add events is always accumulated.
+  auto dot_term = [&](i64 wl, i64 c, ArnAcc& A, auto ovf) {
     const i64 a = asr(wl, sh.dot_b1), b = asr(c, sh.dot_b2);
     const i64 t = wmul(a, b);
     A.sum += static_cast<u64>(t);
     if (CHECKED) {
-      A.n3 += mul_ovf(a, b);
+      if (decltype(ovf)::value) A.n3 += mul_ovf(a, b);
       A.abs_add(t);
     }
   };
-  auto axpy_term = [&](i64 hs, i64 vp, i64& wl, ArnAcc& A) {
+  auto axpy_term = [&](i64 hs, i64 vp, i64& wl, ArnAcc& A, auto ovf) {
     const i64 d = asr(wmul(hs, vp), post);
-    if (CHECKED) {
+    if (CHECKED && decltype(ovf)::value) {
       A.n1 += mul_ovf(hs, vp);
       A.n2 += sub_ovf(wl, d);
     }
     wl = wsub(wl, d);
+  };
+  // ---- magnitude bounds of this CTA's rows (checked mode): W >= max|w|,
+  // vmx[blk][i] = max|v_i| (written by this CTA when it produced v_i), V0 =
+  // max|v_0| (measured in pass 0)
+  constexpr u64 kLim = 1ull << 63;
+  auto absu = [](i64 v) -> u64 { return v < 0 ? u64{0} - static_cast<u64>(v) : static_cast<u64>(v); };
+  auto mul_lt = [&](u64 x, u64 y2) { return __umul64hi(x, y2) == 0 && x * y2 < kLim; };
+  auto shb = [](u64 v, int s2) { return (s2 >= 63 ? 0ull : (v >> (s2 < 0 ? 0 : s2))) + 1; };  // >= |asr(x, s)| for |x| <= v
+  const int vst = ld + 1;
+  u64* vmx_me = vmx + static_cast<size_t>(blockIdx.x) * vst;
+  u64 Wb = 0, V0 = 0;
+  __shared__ u64 s_mx[2];
+  auto cta_max2 = [&](u64 m0, u64 m1) {  // CTA-wide maxima -> (s_mx[0], s_mx[1])
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      m0 = max(m0, static_cast<u64>(__shfl_down_sync(0xffffffffu, m0, o)));
+      m1 = max(m1, static_cast<u64>(__shfl_down_sync(0xffffffffu, m1, o)));
+    }
+    if (threadIdx.x == 0) s_mx[0] = s_mx[1] = 0;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+      atomicMax(reinterpret_cast<unsigned long long*>(&s_mx[0]), static_cast<unsigned long long>(m0));
+      atomicMax(reinterpret_cast<unsigned long long*>(&s_mx[1]), static_cast<unsigned long long>(m1));
+    }
+    __syncthreads();
+  };
+  // a pass "axpy with (hs, Vp), then a product of asr(w, b1) with a value
+  // bounded by Q" is free of product / subtraction overflow when the bounds
+  // say so; advances Wb past the axpy
+  auto certify = [&](u64 ahs, u64 Vp, int qs1, u64 Q, bool has_axpy) {
+    bool ok = true;
+    u64 W2 = Wb;
+    if (has_axpy) {
+      ok = post >= 0 && mul_lt(ahs, Vp);
+      const u64 dmax = ok ? ((ahs * Vp) >> post) + 1 : kLim;
+      ok = ok && W2 < kLim && dmax < kLim - W2;
+      W2 = ok ? W2 + dmax : kLim;
+    }
+    ok = ok && mul_lt(shb(W2, qs1), Q);
+    Wb = W2;
+    return ok;
   };
   // ---- pass 0: w -> shared memory, dot_0 = <w, v_0>
   {
@@ -1476,10 +1521,21 @@ __global__ void __launch_bounds__(kArnThreads, 1)
       sstore(sv + r, k, cq);
 #pragma unroll
       for (int e = 0; e < 4; ++e)
-        if (e < k) dot_term(wq[e], cq[e], A);
+        if (e < k) {
+          dot_term(wq[e], cq[e], A, std::true_type{});
+          if (CHECKED) {
+            Wb = max(Wb, absu(wq[e]));
+            V0 = max(V0, absu(cq[e]));
+          }
+        }
     });
     if (CHECKED) bump(cD, OP_MUL, A.n3);
     cta_reduce_add<CHECKED>(A.sum, A.ahi, A.alo, accj + 0, absj + 0, red);
+    if (CHECKED) {
+      cta_max2(Wb, V0);
+      Wb = s_mx[0];
+      V0 = s_mx[1];
+    }
   }
   // ---- passes 1..j: axpy_{i-1} (v_{i-1} from shared memory), dot_i
   const int e0 = f - sh.dot_b1 - sh.dot_b2;
@@ -1493,20 +1549,26 @@ __global__ void __launch_bounds__(kArnThreads, 1)
     const i64 hs = h_of(grid_barrier(ctl, (++nbar) * G, accj + i - 1, &s_word, vi,
                                      static_cast<unsigned>(cnt * 8) & ~15u));
     ArnAcc A;
-    arn_rows(cnt, [&](long long r, int k) {
-      i64 wq[4], pq[4], cq[4];
-      gload(vi + r, k, cq);
-      sload(sw + r, k, wq);
-      sload(sv + r, k, pq);
+    auto pass = [&](auto ovf) {
+      arn_rows(cnt, [&](long long r, int k) {
+        i64 wq[4], pq[4], cq[4];
+        gload(vi + r, k, cq);
+        sload(sw + r, k, wq);
+        sload(sv + r, k, pq);
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (e < k) {
-          axpy_term(hs, pq[e], wq[e], A);
-          dot_term(wq[e], cq[e], A);
-        }
-      sstore(sw + r, k, wq);
-      sstore(sv + r, k, cq);
-    });
+        for (int e = 0; e < 4; ++e)
+          if (e < k) {
+            axpy_term(hs, pq[e], wq[e], A, ovf);
+            dot_term(wq[e], cq[e], A, ovf);
+          }
+        sstore(sw + r, k, wq);
+        sstore(sv + r, k, cq);
+      });
+    };
+    if (CHECKED && certify(absu(hs), i == 1 ? V0 : vmx_me[i - 1], sh.dot_b1, shb(vmx_me[i], sh.dot_b2), true))
+      pass(std::false_type{});
+    else
+      pass(std::true_type{});
     if (CHECKED) {
       bump(cA, OP_MUL, A.n1);
       bump(cA, OP_SUB, A.n2);
@@ -1518,24 +1580,36 @@ __global__ void __launch_bounds__(kArnThreads, 1)
   {
     const i64 hs = h_of(grid_barrier(ctl, (++nbar) * G, accj + j, &s_word));
     ArnAcc A;
-    arn_rows(cnt, [&](long long r, int k) {
-      i64 wq[4], pq[4];
-      sload(sw + r, k, wq);
-      sload(sv + r, k, pq);
+    auto pass = [&](auto ovf) {
+      arn_rows(cnt, [&](long long r, int k) {
+        i64 wq[4], pq[4];
+        sload(sw + r, k, wq);
+        sload(sv + r, k, pq);
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (e < k) {
-          axpy_term(hs, pq[e], wq[e], A);
-          const i64 sq = asr(wq[e], sh.norm_b1);
-          const i64 t = wmul(sq, sq);
-          A.sum += static_cast<u64>(t);
-          if (CHECKED) {
-            A.n3 += mul_ovf(sq, sq);
-            A.abs_add(t);
+        for (int e = 0; e < 4; ++e)
+          if (e < k) {
+            axpy_term(hs, pq[e], wq[e], A, ovf);
+            const i64 sq = asr(wq[e], sh.norm_b1);
+            const i64 t = wmul(sq, sq);
+            A.sum += static_cast<u64>(t);
+            if (CHECKED) {
+              if (decltype(ovf)::value) A.n3 += mul_ovf(sq, sq);
+              A.abs_add(t);
+            }
           }
-        }
-      sstore(sw + r, k, wq);
-    });
+        sstore(sw + r, k, wq);
+      });
+    };
+    bool fast = false;
+    if (CHECKED) {
+      const u64 Vp = j == 0 ? V0 : vmx_me[j];
+      fast = certify(absu(hs), Vp, 0, 1, true);  // the axpy (the product bound is checked next)
+      fast = fast && mul_lt(shb(Wb, sh.norm_b1), shb(Wb, sh.norm_b1));
+    }
+    if (fast)
+      pass(std::false_type{});
+    else
+      pass(std::true_type{});
     if (CHECKED) {
       bump(cA, OP_MUL, A.n1);
       bump(cA, OP_SUB, A.n2);
@@ -1570,7 +1644,7 @@ __global__ void __launch_bounds__(kArnThreads, 1)
     gm.den_is_m1 = s_vd[4];
     const int b1 = sh.div_b1, ee = f - sh.div_b1 - sh.div_b2;
     i64* out = basis + static_cast<long long>(j + 1) * n + lo;
-    u64 nshl = 0, ndiv = 0;
+    u64 nshl = 0, ndiv = 0, vmax = 0;
     arn_rows(cnt, [&](long long r, int k) {
       i64 wq[4], vq[4];
       sload(sw + r, k, wq);
@@ -1593,10 +1667,14 @@ __global__ void __launch_bounds__(kArnThreads, 1)
         }
       if (k == 4) st_v4(out + r, vq);
       else out[r] = vq[0];
+      if (CHECKED)
+        for (int e = 0; e < k; ++e) vmax = max(vmax, absu(vq[e]));
     });
     if (CHECKED) {
       bump(cstep + K_VEC_DIV * OP_COUNT, OP_SHL, nshl);
       bump(cstep + K_VEC_DIV * OP_COUNT, OP_DIV, ndiv);
+      cta_max2(vmax, 0);
+      if (threadIdx.x == 0) vmx_me[j + 1] = s_mx[0];  // read by this CTA in later steps of the cycle
     }
   }
 }
@@ -2497,7 +2575,7 @@ int arnoldi_barriers(int j) { return j + 3; }
 
 void launch_arnoldi(cudaStream_t st, long long n, int j, long long S, const i64* w, i64* basis, u64* accj,
                     u64* absj, u64* nacc, u64* nabs, int f, ShiftsD sh, u64* cstep, i64* hess, int ld, i64* g,
-                    i64* cs, i64* sn, i64* gabs, Ctl* ctl, unsigned gbase, bool checked) {
+                    i64* cs, i64* sn, i64* gabs, Ctl* ctl, unsigned gbase, bool checked, u64* vmx) {
   ProfScope prof_(st, KC_MGS);
   const int G = num_sms(0);
   const size_t smem = static_cast<size_t>(S) * 16;
@@ -2508,7 +2586,7 @@ void launch_arnoldi(cudaStream_t st, long long n, int j, long long S, const i64*
     attr = true;
   }
   void* args[] = {&n, &j, &S, &w, &basis, &accj, &absj, &nacc, &nabs, &f, &sh, &cstep,
-                  &hess, &ld, &g, &cs, &sn, &gabs, &ctl, &gbase};
+                  &hess, &ld, &g, &cs, &sn, &gabs, &ctl, &gbase, &vmx};
   const void* fn = checked ? reinterpret_cast<const void*>(k_arnoldi<true>) : reinterpret_cast<const void*>(k_arnoldi<false>);
   cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kArnThreads), args, smem, st);
   LAUNCH_CHECK();

@@ -783,3 +783,49 @@ def test_ilu_pencil_wavefront(gpu, oracle, dims):
     assert G.pencil_bricks(False) == 0
     y = gen.uniform_int(23, n, -(1 << 50), 1 << 50)
     assert np.array_equal(gpu.apply_inverse(G, y), gpu.apply_inverse(F, y))
+
+
+_CERT_SCRIPT = r"""
+import sys, json
+import numpy as np
+import paper_2009_07495_b200 as gpu
+from workloads import gen
+plan = tuple(json.loads(sys.argv[1]))
+rp, ci, v = gen.laplacian2d(64)
+n = len(rp) - 1
+vals, scale = gpu.row_scale(rp, ci, v, 16)
+comp, al, _ = gpu.build_split(vals, 16, 1)
+S = gpu.SplitMatrix(rp, ci, comp, al)
+b = gen.uniform(31, n) / scale
+t = gpu.FxTrace(checked=True)
+try:
+    r = gpu.run_cycle(S, gpu.CycleConfig(m=8, shifts=gpu.ShiftPlan(*plan)), b, np.zeros(n), trace=t)
+    st = [int(r.dim), int(np.bitwise_xor.reduce(r.basis.view(np.uint64))), int(np.bitwise_xor.reduce(r.hess.view(np.uint64)))]
+except Exception as e:
+    st = type(e).__name__
+print(json.dumps({"state": st, "total": t.total_overflows(), "exact": t.exact, "events": sorted(map(list, t.events))}))
+"""
+
+
+@pytest.mark.parametrize("plan", [(16, 0, 16, 16, 16, 14, 16, 0), (0, 0, 16, 16, 16, 14, 16, 0), (0, 0, 0, 0, 0, 30, 0, 0)],
+                         ids=["guarded", "dot-guard-removed", "no-shifts"])
+def test_arnoldi_overflow_certificate(gpu, plan):
+    """The persistent Arnoldi step skips per-element product / subtraction
+    overflow tests for a pass only when the CTA's magnitude bounds prove none
+    can occur (kernels.cu k_arnoldi certify).  On n = 4096 (the fused path),
+    with plans that do and do not wrap, its checked-mode trace (events,
+    total, exactness) and cycle state equal those of the separate pass
+    kernels, which test every element (IGM_ARNOLDI=0)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env in ({}, {"IGM_ARNOLDI": "0"}):
+        r = subprocess.run([sys.executable, "-c", _CERT_SCRIPT, json.dumps(plan)], cwd=root, capture_output=True,
+                           text=True, env={**os.environ, **env}, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0] == outs[1]
+    if plan[:2] == (0, 0) and plan[2] == 16:  # the wrapping plan: events on both paths
+        assert outs[0]["total"] > 0
