@@ -426,7 +426,8 @@ void build_tri(igm_ctx* c, DevTri& t, int n, const int* rp, const int* ci, const
     t.maxabs_l = std::max(t.maxabs_l, a);
   }
   t.prog = dalloc<int>(S.ntiles);
-  t.ticket = dalloc<int>(1);
+  t.ticket = dalloc<int>(2);  // [tickets taken, CTAs finished]
+  ck(cudaMemsetAsync(t.ticket, 0, 2 * sizeof(int), st), "ticket");
   if (S.grid[0] > 0 && env_int("IGM_PENCIL", 1) != 0) {  // structured 7-point: the pencil wavefront
     const PencilStream P = build_pencil_stream(n, rp, ci, vals, dpos, upper, S.grid[0], S.grid[1], S.grid[2]);
     if (P.ok) {

@@ -2759,7 +2759,7 @@ static void pen_launch(cudaStream_t st, const DevTri& t, bool backward, const vo
 void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out,
                     u64* cnt, const Ctl* ctl, bool checked) {
   if (t.n == 0) return;
-  cudaMemsetAsync(t.ticket, 0, sizeof(int), st);
+  if (!t.pen) cudaMemsetAsync(t.ticket, 0, sizeof(int), st);  // the pencil kernel's last CTA resets it
   if (checked) cudaMemsetAsync(t.stats, 0, 2 * sizeof(u64), st);
   {
     ProfScope prof_(st, KC_TRI_INT);
@@ -2770,7 +2770,7 @@ void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* 
   LAUNCH_CHECK();
   if (checked) {
     ProfScope prof_(st, KC_OTHER);
-    k_tri_count<<<grid_full(t.n, 256), 256, 0, st>>>(t.n, t.c_rp, t.c_ci, t.c_val, t.c_diag, y, out, cnt, ctl,
+    k_tri_count<<<grid_for(t.n, 256), 256, 0, st>>>(t.n, t.c_rp, t.c_ci, t.c_val, t.c_diag, y, out, cnt, ctl,
                                                       t.stats, static_cast<double>(t.maxabs_l), t.maxd);
     LAUNCH_CHECK();
   }
@@ -2779,7 +2779,7 @@ void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* 
 void launch_tri_fp(cudaStream_t st, const DevTri& t, bool backward, const double* y, double* out,
                    const Ctl* ctl, const double* prescale) {
   if (t.n == 0) return;
-  cudaMemsetAsync(t.ticket, 0, sizeof(int), st);
+  if (!(t.pen && t.pen_blk_fp)) cudaMemsetAsync(t.ticket, 0, sizeof(int), st);
   ProfScope prof_(st, KC_TRI_FP);
   if (t.pen && t.pen_blk_fp) pen_launch<true>(st, t, backward, y, out, ctl, false, prescale);
   else if (backward) tri_dispatch<double, true>(st, t, y, out, ctl, prescale);

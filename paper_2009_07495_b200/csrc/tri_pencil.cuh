@@ -318,6 +318,17 @@ __global__ void __launch_bounds__(kPenThreads, 1)
       atomicMax(a.stats + 1, static_cast<unsigned long long>(zmx + 1));
     }
   }
+  // the last CTA to finish resets the ticket counters for the next launch
+  // (ticket[1] counts finished CTAs), so no memset precedes a launch
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(a.ticket + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+      a.ticket[0] = 0;
+      a.ticket[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 }  // namespace igm

@@ -38,7 +38,8 @@ static float run(const PencilStream& PS, int n, bool upper, const std::vector<i6
   i64 *d_y, *d_z;
   CK(cudaMalloc(&d_rec, PS.blk.size() * 8));
   CK(cudaMalloc(&d_bot, PS.brick_of_ticket.size() * 4));
-  CK(cudaMalloc(&d_ticket, 4));
+  CK(cudaMalloc(&d_ticket, 8));
+  CK(cudaMemset(d_ticket, 0, 8));
   CK(cudaMalloc(&d_stats, 16));
   CK(cudaMalloc(&d_xz, static_cast<size_t>(n) * 16));
   CK(cudaMalloc(&d_y, static_cast<size_t>(n) * 8));
@@ -71,7 +72,7 @@ static float run(const PencilStream& PS, int n, bool upper, const std::vector<i6
   float best = 1e30f, tot = 0;
   for (int it = -50; it < iters + 2; ++it) {
     a.epoch = (0x1234567ull + it) * 0x9E3779B97F4A7C15ull | 1ull;
-    CK(cudaMemset(d_ticket, 0, 4));
+
     CK(cudaMemset(d_z, 0x5a, static_cast<size_t>(n) * 8));
     cudaEventRecord(e0);
     k_tri_pencil<P, true, false><<<PS.nbricks, kPenThreads, sm>>>(a, d_y, d_z, nullptr, nullptr, nullptr);
