@@ -21,8 +21,10 @@
  *
  * Threading: a context owns one CUDA stream; calls on one context must be
  * serialised by the caller (the reference is single-threaded, FxTrace is not
- * thread-safe).  Uploaded matrices are immutable and may be shared by
- * contexts on the same device.
+ * thread-safe).  Uploaded split and FP64 matrices are immutable and may be
+ * shared by contexts on the same device; an ILU handle also carries its
+ * substitutions' device scratch (wavefront tickets, tagged exported values,
+ * magnitude bounds) and must be used by one context at a time.
  */
 #ifndef IGM_H
 #define IGM_H
