@@ -9,6 +9,7 @@
 #include "igm_internal.cuh"
 #include "schedule.hpp"
 #include "pencil.hpp"
+#include "pencil27.cuh"
 
 #include <algorithm>
 #include <climits>
@@ -446,6 +447,18 @@ void build_tri(igm_ctx* c, DevTri& t, int n, const int* rp, const int* ci, const
       t.pen_bot = dupload(P.brick_of_ticket.data(), P.brick_of_ticket.size(), st);
     }
   }
+  if (!t.pen && S.grid[0] > 0 && env_int("IGM_PENCIL", 1) != 0) {  // structured 27-point: the 27-point pencil
+    Pencil27Stream Q = build_pencil27_stream(n, rp, ci, vals, dpos, upper, S.grid[0], S.grid[1], S.grid[2]);
+    if (Q.ok && Q.nbricks <= pencil27_max_resident(c->device)) {  // every brick resident at once
+      t.pen27 = true;
+      t.p27_gx = Q.gx;
+      t.p27_gy = Q.gy;
+      t.p27_gz = Q.gz;
+      t.p27_nbx = Q.nbx;
+      t.p27_nbricks = Q.nbricks;
+      t.p27_rec = dupload(Q.rec.data(), Q.rec.size(), st);
+    }
+  }
   ck(cudaStreamSynchronize(st), "upload_ilu sync");
 }
 
@@ -460,7 +473,7 @@ void free_tri(DevTri& t) {
                   static_cast<void*>(t.seg_xptr), static_cast<void*>(t.seg_xrow), static_cast<void*>(t.c_rp),
                   static_cast<void*>(t.c_ci), static_cast<void*>(t.c_val), static_cast<void*>(t.c_diag),
                   static_cast<void*>(t.prog), static_cast<void*>(t.yperm), static_cast<void*>(t.stats),
-                  static_cast<void*>(t.ticket), t.pen_blk, t.pen_blk_fp, static_cast<void*>(t.pen_bot)})
+                  static_cast<void*>(t.ticket), t.pen_blk, t.pen_blk_fp, static_cast<void*>(t.pen_bot), t.p27_rec})
     dfree(p);
   t = DevTri{};
 }
@@ -807,7 +820,7 @@ void igm_ilu_free(igm_ilu* f) {
 int igm_ilu_pencil(const igm_ilu* f, int backward) {
   if (!f) return 0;
   const DevTri& t = backward ? f->upper : f->lower;
-  return t.pen ? t.pen_nbricks : 0;
+  return t.pen ? t.pen_nbricks : (t.pen27 ? t.p27_nbricks : 0);
 }
 
 int igm_debug_pencil_stream(int n, const int* rp, const int* ci, const int64_t* vals, const int* dpos, int upper,

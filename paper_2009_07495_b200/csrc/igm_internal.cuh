@@ -105,6 +105,10 @@ struct DevTri {
   bool pen = false;
   int pen_gx = 0, pen_gy = 0, pen_gz = 0, pen_nbx = 0, pen_nby = 0, pen_nbricks = 0, pen_S = 0, pen_pad = 0;
   void* pen_blk = nullptr;
+  // structured 27-point factors: the 27-point pencil wavefront (pencil27.cuh)
+  bool pen27 = false;
+  int p27_gx = 0, p27_gy = 0, p27_gz = 0, p27_nbx = 0, p27_nbricks = 0;
+  void* p27_rec = nullptr;
   void* pen_blk_fp = nullptr;  // the FP64 substitution's stream (diagonal as a double)
   int* pen_bot = nullptr;
   int* ticket = nullptr;  // 1
@@ -138,6 +142,7 @@ void launch_spmv_fp_split(cudaStream_t st, const DevSplit& m, int s,
                           const Ctl* ctl);
 void launch_residual(cudaStream_t st, const DevCsrf& a, const double* x,
                      const double* b, double* r, Ctl* ctl, bool track_max);
+int pencil27_max_resident(int device);  // CTAs of k_tri27 that fit on the GPU at once
 void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward,
                     const i64* y, i64* out, u64* cnt, const Ctl* ctl,
                     bool checked);

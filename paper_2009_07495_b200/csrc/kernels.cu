@@ -9,6 +9,7 @@
 // without host round trips.
 #include "igm_internal.cuh"
 #include "tri_pencil.cuh"
+#include "pencil27.cuh"
 
 #include <algorithm>
 #include <atomic>
@@ -2756,6 +2757,41 @@ static void pen_launch(cudaStream_t st, const DevTri& t, bool backward, const vo
     k_tri_pencil<D, false, FP><<<t.pen_nbricks, kPenThreads, sm, st>>>(a, yi, oi, stop, err, prescale);
 }
 
+int pencil27_max_resident(int device) {
+  const size_t sm = pencil27_smem_bytes();
+  cudaFuncSetAttribute(k_tri27<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+  cudaFuncSetAttribute(k_tri27<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+  int a = 0, b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_tri27<true>, kP27Threads, sm) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_tri27<false>, kP27Threads, sm) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return std::min(a, b) * num_sms(device);
+}
+
+static void pen27_launch(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out, const Ctl* ctl,
+                         bool checked) {
+  P27Args a;
+  a.gx = t.p27_gx;
+  a.gy = t.p27_gy;
+  a.gz = t.p27_gz;
+  a.nbx = t.p27_nbx;
+  a.n = t.n;
+  a.mirror = backward ? 1 : 0;
+  a.rec = static_cast<const unsigned char*>(t.p27_rec);
+  a.xz = t.xz;
+  a.epoch = pen_epoch();
+  a.stats = reinterpret_cast<unsigned long long*>(t.stats);
+  const int* stop = ctl ? &ctl->stop : nullptr;
+  const int* err = ctl ? &ctl->err : nullptr;
+  const size_t sm = pencil27_smem_bytes();
+  if (checked)
+    k_tri27<true><<<t.p27_nbricks, kP27Threads, sm, st>>>(a, y, out, stop, err);
+  else
+    k_tri27<false><<<t.p27_nbricks, kP27Threads, sm, st>>>(a, y, out, stop, err);
+}
+
 void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out,
                     u64* cnt, const Ctl* ctl, bool checked) {
   if (t.n == 0) return;
@@ -2764,6 +2800,7 @@ void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* 
   {
     ProfScope prof_(st, KC_TRI_INT);
     if (t.pen) pen_launch<false>(st, t, backward, y, out, ctl, checked, nullptr);
+    else if (t.pen27) pen27_launch(st, t, backward, y, out, ctl, checked);
     else if (backward) tri_dispatch<i64, true>(st, t, y, out, ctl, nullptr);
     else tri_dispatch<i64, false>(st, t, y, out, ctl, nullptr);
   }
