@@ -829,3 +829,36 @@ def test_arnoldi_overflow_certificate(gpu, plan):
     assert outs[0] == outs[1]
     if plan[:2] == (0, 0) and plan[2] == 16:  # the wrapping plan: events on both paths
         assert outs[0]["total"] > 0
+
+
+_P27_SHAPES = [(12, 12, 12), (17, 35, 9), (33, 20, 7), (2, 2, 30), (40, 3, 5)]
+
+
+@pytest.mark.parametrize("dims", _P27_SHAPES, ids=["x".join(map(str, d)) for d in _P27_SHAPES])
+def test_ilu_pencil27_wavefront(gpu, oracle, dims):
+    """The 27-point pencil wavefront (csrc/pencil27.cuh) on ragged grids:
+    integer substitutions bit-exact vs the oracle's sequential ones
+    (ilu.cpp:122-155), with and without wrapping, checked-mode event totals,
+    repeated launches, and equal to the generic wavefront."""
+    lo, up = _grid_factors(gpu, dims, _TWENTY7, seed=11 + sum(dims))
+    F = gpu.IluFactors(lo, up)
+    assert F.pencil_bricks(False) > 0 and F.pencil_bricks(True) > 0
+    il = oracle.ilu(lo, up)
+    n = len(lo[0]) - 1
+    from workloads import gen
+    for seed, mag in ((31, 45), (32, 62)):
+        y = gen.uniform_int(seed, n, -(1 << mag), 1 << mag)
+        t1, t2 = gpu.FxTrace(), PyTrace()
+        want = oracle.apply_inverse(il, y, t2)
+        for _ in range(2):
+            assert np.array_equal(gpu.apply_inverse(F, y), want)
+        assert np.array_equal(gpu.apply_inverse(F, y, t1), want)
+        assert t1.total_overflows() == t2.total
+    os.environ["IGM_PENCIL"] = "0"
+    try:
+        G = gpu.IluFactors(lo, up)
+    finally:
+        del os.environ["IGM_PENCIL"]
+    assert G.pencil_bricks(False) == 0
+    y = gen.uniform_int(33, n, -(1 << 50), 1 << 50)
+    assert np.array_equal(gpu.apply_inverse(G, y), gpu.apply_inverse(F, y))
