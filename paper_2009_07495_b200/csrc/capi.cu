@@ -457,6 +457,10 @@ void build_tri(igm_ctx* c, DevTri& t, int n, const int* rp, const int* ci, const
       t.p27_nbx = Q.nbx;
       t.p27_nbricks = Q.nbricks;
       t.p27_rec = dupload(Q.rec.data(), Q.rec.size(), st);
+      Q = Pencil27Stream{};
+      const Pencil27Stream Qf =
+          build_pencil27_stream(n, rp, ci, vals, dpos, upper, S.grid[0], S.grid[1], S.grid[2], true);
+      if (Qf.ok) t.p27_rec_fp = dupload(Qf.rec.data(), Qf.rec.size(), st);
     }
   }
   ck(cudaStreamSynchronize(st), "upload_ilu sync");
@@ -473,7 +477,7 @@ void free_tri(DevTri& t) {
                   static_cast<void*>(t.seg_xptr), static_cast<void*>(t.seg_xrow), static_cast<void*>(t.c_rp),
                   static_cast<void*>(t.c_ci), static_cast<void*>(t.c_val), static_cast<void*>(t.c_diag),
                   static_cast<void*>(t.prog), static_cast<void*>(t.yperm), static_cast<void*>(t.stats),
-                  static_cast<void*>(t.ticket), t.pen_blk, t.pen_blk_fp, static_cast<void*>(t.pen_bot), t.p27_rec})
+                  static_cast<void*>(t.ticket), t.pen_blk, t.pen_blk_fp, static_cast<void*>(t.pen_bot), t.p27_rec, t.p27_rec_fp})
     dfree(p);
   t = DevTri{};
 }

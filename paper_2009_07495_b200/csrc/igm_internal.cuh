@@ -109,6 +109,7 @@ struct DevTri {
   bool pen27 = false;
   int p27_gx = 0, p27_gy = 0, p27_gz = 0, p27_nbx = 0, p27_nbricks = 0;
   void* p27_rec = nullptr;
+  void* p27_rec_fp = nullptr;  // the FP64 substitution's stream (diagonal as a double)
   void* pen_blk_fp = nullptr;  // the FP64 substitution's stream (diagonal as a double)
   int* pen_bot = nullptr;
   int* ticket = nullptr;  // 1

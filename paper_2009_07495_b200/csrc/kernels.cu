@@ -2761,17 +2761,19 @@ int pencil27_max_resident(int device) {
   const size_t sm = pencil27_smem_bytes();
   cudaFuncSetAttribute(k_tri27<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
   cudaFuncSetAttribute(k_tri27<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-  int a = 0, b = 0;
+  cudaFuncSetAttribute(k_tri27<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+  int a = 0, b = 0, c = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_tri27<true>, kP27Threads, sm) != cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_tri27<false>, kP27Threads, sm) != cudaSuccess) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_tri27<false>, kP27Threads, sm) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_tri27<false, true>, kP27Threads, sm) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
-  return std::min(a, b) * num_sms(device);
+  return std::min(std::min(a, b), c) * num_sms(device);
 }
 
 static void pen27_launch(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out, const Ctl* ctl,
-                         bool checked) {
+                         bool checked, bool fp = false, const double* prescale = nullptr) {
   P27Args a;
   a.gx = t.p27_gx;
   a.gy = t.p27_gy;
@@ -2779,17 +2781,19 @@ static void pen27_launch(cudaStream_t st, const DevTri& t, bool backward, const 
   a.nbx = t.p27_nbx;
   a.n = t.n;
   a.mirror = backward ? 1 : 0;
-  a.rec = static_cast<const unsigned char*>(t.p27_rec);
+  a.rec = static_cast<const unsigned char*>(fp ? t.p27_rec_fp : t.p27_rec);
   a.xz = t.xz;
   a.epoch = pen_epoch();
   a.stats = reinterpret_cast<unsigned long long*>(t.stats);
   const int* stop = ctl ? &ctl->stop : nullptr;
   const int* err = ctl ? &ctl->err : nullptr;
   const size_t sm = pencil27_smem_bytes();
-  if (checked)
-    k_tri27<true><<<t.p27_nbricks, kP27Threads, sm, st>>>(a, y, out, stop, err);
+  if (fp)
+    k_tri27<false, true><<<t.p27_nbricks, kP27Threads, sm, st>>>(a, y, out, stop, err, prescale);
+  else if (checked)
+    k_tri27<true><<<t.p27_nbricks, kP27Threads, sm, st>>>(a, y, out, stop, err, nullptr);
   else
-    k_tri27<false><<<t.p27_nbricks, kP27Threads, sm, st>>>(a, y, out, stop, err);
+    k_tri27<false><<<t.p27_nbricks, kP27Threads, sm, st>>>(a, y, out, stop, err, nullptr);
 }
 
 void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out,
@@ -2819,6 +2823,9 @@ void launch_tri_fp(cudaStream_t st, const DevTri& t, bool backward, const double
   if (!(t.pen && t.pen_blk_fp)) cudaMemsetAsync(t.ticket, 0, sizeof(int), st);
   ProfScope prof_(st, KC_TRI_FP);
   if (t.pen && t.pen_blk_fp) pen_launch<true>(st, t, backward, y, out, ctl, false, prescale);
+  else if (t.pen27 && t.p27_rec_fp)
+    pen27_launch(st, t, backward, reinterpret_cast<const i64*>(y), reinterpret_cast<i64*>(out), ctl, false, true,
+                 prescale);
   else if (backward) tri_dispatch<double, true>(st, t, y, out, ctl, prescale);
   else tri_dispatch<double, false>(st, t, y, out, ctl, prescale);
   LAUNCH_CHECK();

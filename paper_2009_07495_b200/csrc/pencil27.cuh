@@ -46,7 +46,7 @@ struct Pencil27Stream {
 
 // info: sh1 | sh2 << 1 | den_neg << 8 | presence of dependency q << (9 + q)
 inline Pencil27Stream build_pencil27_stream(int n, const int* rp, const int* ci, const std::int64_t* vals,
-                                            const int* dpos, bool upper, int gx, int gy, int gz) {
+                                            const int* dpos, bool upper, int gx, int gy, int gz, bool fp = false) {
   Pencil27Stream P;
   if (gx < 2 || gy < 2 || gz < 1 || static_cast<long long>(gx) * gy * gz != n) return P;
   const long long plane = static_cast<long long>(gx) * gy;
@@ -88,7 +88,12 @@ inline Pencil27Stream build_pencil27_stream(int n, const int* rp, const int* ci,
     unsigned char* e = &P.rec[((static_cast<size_t>(by * P.nbx + bx) * kP27Threads + t) * gz + k) * kP27Rec];
     std::memcpy(e, f, 52);
     std::memcpy(e + 52, &info, 4);
-    std::memcpy(e + 56, &g.u.m, 8);
+    if (fp) {
+      const double dd = static_cast<double>(vals[dpos[r]]);
+      std::memcpy(e + 56, &dd, 8);
+    } else {
+      std::memcpy(e + 56, &g.u.m, 8);
+    }
   }
   P.ok = true;
   return P;
@@ -114,9 +119,15 @@ __device__ __forceinline__ void p27_lds16(unsigned a, u64& v, u64& t) {
   asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v), "=l"(t) : "r"(a) : "memory");
 }
 
-template <bool CHECKED>
+// FP = true: the FP64 substitution on the integer factors (apply_inverse_fp,
+// ilu.cpp:157-180): acc = y (or y / gamma), acc -= L_rd * z_d over the row's
+// entries in CSR order -- dependencies 0..12 for the lower factor, 12..0 for
+// the mirrored upper one -- every operation rounded on its own, absent
+// entries skipped, then acc / diag (the stream holds the diagonal as a double)
+template <bool CHECKED, bool FP = false>
 __global__ void __launch_bounds__(kP27Threads, 2) k_tri27(P27Args a, const i64* __restrict__ y, i64* __restrict__ out,
-                                                          const int* stop, const int* err) {
+                                                          const int* stop, const int* err,
+                                                          const double* prescale = nullptr) {
   extern __shared__ __align__(16) unsigned char p27_smem[];
   if (stop != nullptr && (*stop | *err) != 0) return;
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31, xl = lane & 15, jl = 2 * w + (lane >> 4);
@@ -206,7 +217,6 @@ __global__ void __launch_bounds__(kP27Threads, 2) k_tri27(P27Args a, const i64* 
         else
           p27_ldg16(a.xz + (r + p27_di(q) + static_cast<long long>(p27_dj(q)) * a.gx + p27_dk(q) * plane), v[q], t[q]);
       }
-      u64 sx = 0;
 #pragma unroll
       for (int q = 0; q < 13; ++q) {
         const u64 want = p27_dk(q) ? w1 : w0;
@@ -224,15 +234,30 @@ __global__ void __launch_bounds__(kP27Threads, 2) k_tri27(P27Args a, const i64* 
             } while (t[q] != (want ^ v[q]));
           }
         }
-        sx += static_cast<u64>(static_cast<i64>(f[q])) * v[q];
       }
-      SDivMagic gm;
-      gm.u.m = mg;
-      gm.u.sh1 = info & 1;
-      gm.u.sh2 = (info >> 1) & 127;
-      gm.den_neg = (info >> 8) & 1;
-      gm.den_is_m1 = 0;
-      const i64 z = sdiv(static_cast<i64>(yv - sx), gm);
+      i64 z;
+      if constexpr (FP) {
+        double acc = __longlong_as_double(static_cast<long long>(yv));
+        if (prescale != nullptr) acc = __ddiv_rn(acc, *prescale);
+#pragma unroll
+        for (int u = 0; u < 13; ++u) {
+          const int q = a.mirror ? 12 - u : u;
+          if ((mask >> q) & 1)
+            acc = __dsub_rn(acc, __dmul_rn(static_cast<double>(f[q]), __longlong_as_double(static_cast<long long>(v[q]))));
+        }
+        z = __double_as_longlong(__ddiv_rn(acc, __longlong_as_double(static_cast<long long>(mg))));
+      } else {
+        u64 sx = 0;
+#pragma unroll
+        for (int q = 0; q < 13; ++q) sx += static_cast<u64>(static_cast<i64>(f[q])) * v[q];
+        SDivMagic gm;
+        gm.u.m = mg;
+        gm.u.sh1 = info & 1;
+        gm.u.sh2 = (info >> 1) & 127;
+        gm.den_neg = (info >> 8) & 1;
+        gm.den_is_m1 = 0;
+        z = sdiv(static_cast<i64>(yv - sx), gm);
+      }
       const u64 tg = w0 ^ static_cast<u64>(z);
       asm volatile("st.volatile.shared.v2.u64 [%0], {%1, %2};" ::"r"(my_ring + static_cast<unsigned>(k & (kP27R - 1)) * 16u),
                    "l"(z), "l"(tg)
@@ -242,13 +267,13 @@ __global__ void __launch_bounds__(kP27Threads, 2) k_tri27(P27Args a, const i64* 
                      "l"(a.xz + r)
                      : "memory");
       out[a.mirror ? a.n - 1 - r : r] = z;
-      if (CHECKED) {
+      if (CHECKED && !FP) {
         ymx |= yv ^ static_cast<u64>(static_cast<i64>(yv) >> 63);
         zmx |= static_cast<u64>(z ^ (z >> 63));
       }
     }
   }
-  if (CHECKED && a.stats != nullptr) {
+  if (CHECKED && !FP && a.stats != nullptr) {
     if (ymx) atomicMax(a.stats, static_cast<unsigned long long>(ymx + 1));
     if (zmx) atomicMax(a.stats + 1, static_cast<unsigned long long>(zmx + 1));
   }

@@ -854,6 +854,9 @@ def test_ilu_pencil27_wavefront(gpu, oracle, dims):
             assert np.array_equal(gpu.apply_inverse(F, y), want)
         assert np.array_equal(gpu.apply_inverse(F, y, t1), want)
         assert t1.total_overflows() == t2.total
+    yf = gen.uniform(34, n)
+    yf[::5] = -0.0
+    assert np.array_equal(gpu.apply_inverse_fp(F, yf).view(np.int64), oracle.apply_inverse_fp(il, yf).view(np.int64))
     os.environ["IGM_PENCIL"] = "0"
     try:
         G = gpu.IluFactors(lo, up)
