@@ -137,6 +137,11 @@ int igm_ilu_pencil(const igm_ilu* f, int backward);
  * out4 = {bricks, steps per warp, bricks in x, bricks in y} */
 int igm_debug_pencil_stream(int n, const int* row_ptr, const int* col_idx, const int64_t* vals,
                             const int* diag_pos, int upper, int gx, int gy, int gz, int* out4);
+/* CPU-only: the 27-point pencil stream (csrc/pencil27.cuh) of one factor on
+ * a gx*gy*gz grid; returns 1 if every entry is one of the 13 lower 27-point
+ * neighbours, then out2 = {bricks, stream bytes / 64} */
+int igm_debug_pencil27_stream(int n, const int* row_ptr, const int* col_idx, const int64_t* vals,
+                              const int* diag_pos, int upper, int gx, int gy, int gz, long long* out2);
 /* debug: per-segment phase timestamps of one ILU tile (8 u64 per segment) */
 void igm_debug_tri_trace(int tile, unsigned long long* device_buf);
 

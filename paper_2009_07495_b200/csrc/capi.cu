@@ -838,6 +838,15 @@ int igm_debug_pencil_stream(int n, const int* rp, const int* ci, const int64_t* 
   return 1;
 }
 
+int igm_debug_pencil27_stream(int n, const int* rp, const int* ci, const int64_t* vals, const int* dpos, int upper,
+                              int gx, int gy, int gz, long long* out2) {
+  const Pencil27Stream P = build_pencil27_stream(n, rp, ci, vals, dpos, upper != 0, gx, gy, gz);
+  if (!P.ok) return 0;
+  out2[0] = P.nbricks;
+  out2[1] = static_cast<long long>(P.rec.size() / kP27Rec);
+  return 1;
+}
+
 int igm_ilu_levels(const igm_ilu* f, int backward) {
   return f ? (backward ? f->upper.nlevels : f->lower.nlevels) : 0;
 }

@@ -187,3 +187,45 @@ def test_pencil_stream_structure(product_lib, igm):
     lo, up = igm.factorize_split_cast(rp, ci, vals)
     assert _pencil_info(product_lib, lo, False, (8, 8, 8))[0] == 0
     assert _pencil_info(product_lib, up, True, (8, 8, 8))[0] == 0
+
+
+def test_pencil27_stream_structure(product_lib, igm):
+    """The 27-point pencil stream (csrc/pencil27.cuh) accepts exactly factors
+    whose entries are among the 13 lower 27-point neighbours: 27-point L and U
+    on ragged grids (16 x 16 bricks, 64 B per pencil row), 7-point factors
+    too (a subset), not a wrong grid or an entry two planes away."""
+    from workloads import gen
+    offs27 = [(a, b, c) for c in (-1, 0, 1) for b in (-1, 0, 1) for a in (-1, 0, 1)]
+    for dims in ((12, 12, 12), (17, 35, 9)):
+        rp, ci, v = gen._stencil_csr(dims, offs27, lambda o, r: np.full(r.shape, 30.0 if o == 13 else -1.0))
+        vals, _ = igm.row_scale(rp, ci, v, 32)
+        lo, up = igm.factorize_split_cast(rp, ci, vals)
+        for f, upper in ((lo, False), (up, True)):
+            a = [np.ascontiguousarray(x, dt) for x, dt in zip(f, (np.int32, np.int32, np.int64, np.int32))]
+            out = (C.c_longlong * 2)()
+            ok = product_lib.igm_debug_pencil27_stream(len(a[0]) - 1, *[x.ctypes.data_as(C.c_void_p) for x in a],
+                                                      int(upper), *dims, out)
+            nb = -(-dims[0] // 16) * -(-dims[1] // 16)
+            assert ok == 1 and list(out) == [nb, nb * 256 * dims[2]]
+            bad = 1 if dims[0] != dims[1] else 0
+            if bad:
+                assert product_lib.igm_debug_pencil27_stream(len(a[0]) - 1, *[x.ctypes.data_as(C.c_void_p) for x in a],
+                                                            int(upper), dims[1], dims[0], dims[2], out) == 0
+    # an entry two planes away is not a 27-point neighbour
+    n = 4 * 4 * 4
+    rp, cols, vl, dp = [0], [], [], []
+    for r in range(n):
+        if r >= 32:
+            cols.append(r - 32)
+            vl.append(1)
+        dp.append(len(cols))
+        cols.append(r)
+        vl.append(5)
+        rp.append(len(cols))
+    a = [np.ascontiguousarray(x, dt) for x, dt in zip((rp, cols, vl, dp), (np.int32, np.int32, np.int64, np.int32))]
+    out = (C.c_longlong * 2)()
+    assert product_lib.igm_debug_pencil27_stream(n, *[x.ctypes.data_as(C.c_void_p) for x in a], 0, 4, 4, 4, out) == 0
+    # ... while the same pattern one plane away is
+    cols2 = [c + 16 if c < r and r >= 32 else c for c, r in zip(cols, [rr for rr in range(n) for _ in range(1 + (rr >= 32))])]
+    a2 = [np.ascontiguousarray(x, dt) for x, dt in zip((rp, cols2, vl, dp), (np.int32, np.int32, np.int64, np.int32))]
+    assert product_lib.igm_debug_pencil27_stream(n, *[x.ctypes.data_as(C.c_void_p) for x in a2], 0, 4, 4, 4, out) == 1
