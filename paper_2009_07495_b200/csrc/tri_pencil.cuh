@@ -280,6 +280,11 @@ __global__ void __launch_bounds__(kPenThreads, 1)
       } while (cons_seen < s - a.R);
     }
     const u64 tg = want ^ static_cast<u64>(z);
+    asm volatile(
+        "{ .reg .pred p; setp.ne.b32 p, %3, 0;\n"
+        "@p st.volatile.shared.v2.u64 [%0], {%1, %2}; }" ::"r"(ring_prod + rs),
+        "l"(z), "l"(tg), "r"((int)(act && pprod))
+        : "memory");
     asm volatile("{ .reg .pred p; setp.ne.b32 p, %2, 0;\n@p st.global.b64 [%0], %1; }" ::"l"(op), "l"(z),
                  "r"((int)act)
                  : "memory");
@@ -288,11 +293,7 @@ __global__ void __launch_bounds__(kPenThreads, 1)
         "@p st.global.relaxed.gpu.b128 [%0], t; }" ::"l"(ep),
         "l"(z), "l"(tg), "r"((int)(act && exp_))
         : "memory");
-    asm volatile(
-        "{ .reg .pred p; setp.ne.b32 p, %3, 0;\n"
-        "@p st.volatile.shared.v2.u64 [%0], {%1, %2}; }" ::"r"(ring_prod + rs),
-        "l"(z), "l"(tg), "r"((int)(act && pprod))
-        : "memory");
+
     if constexpr (CHECKED && !FP) {  // magnitude bounds: OR of v ^ (v >> 63) (idle lanes contribute 0)
       ymx |= yv ^ static_cast<u64>(static_cast<i64>(yv) >> 63);
       zmx |= static_cast<u64>(z ^ (z >> 63));
