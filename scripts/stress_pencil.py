@@ -9,12 +9,15 @@ from workloads import gen
 
 O = Oracle()
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 50
-offs = [(0, 0, -1), (0, -1, 0), (-1, 0, 0), (0, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 1)]
+offs7 = [(0, 0, -1), (0, -1, 0), (-1, 0, 0), (0, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 1)]
+offs27 = [(a, b, c) for c in (-1, 0, 1) for b in (-1, 0, 1) for a in (-1, 0, 1)]
 bad = 0
-for dims in [(128, 128, 128), (64, 96, 33), (17, 35, 9), (200, 24, 10)]:
+cases = [(d, offs7) for d in [(128, 128, 128), (64, 96, 33), (17, 35, 9), (200, 24, 10)]]
+cases += [(d, offs27) for d in [(96, 96, 48), (33, 47, 21), (12, 12, 12)]]
+for dims, offs in cases:
     rng = np.random.default_rng(sum(dims))
-    coef = {q: rng.uniform(-1.4, -0.6) for q in range(7)}
-    coef[3] = 14.0
+    coef = {q: rng.uniform(-1.4, -0.6) for q in range(len(offs))}
+    coef[offs.index((0, 0, 0))] = 2.0 * len(offs)
     rp, ci, v = gen._stencil_csr(dims, offs, lambda o, r: np.full(r.shape, coef[o]))
     vals, _ = igm.row_scale(rp, ci, v, 32)
     lo, up = igm.factorize_split_cast(rp, ci, vals)
@@ -35,5 +38,5 @@ for dims in [(128, 128, 128), (64, 96, 33), (17, 35, 9), (200, 24, 10)]:
         if not np.array_equal(igm.apply_inverse_fp(F, yf).view(np.int64), firstf.view(np.int64)):
             bad += 1
             print("fp mismatch", dims, r)
-    print(dims, "pencil bricks", F.pencil_bricks(False), "reps", reps, "bad so far", bad, flush=True)
+    print(dims, len(offs), "pt, pencil bricks", F.pencil_bricks(False), "reps", reps, "bad so far", bad, flush=True)
 print("TOTAL BAD", bad)
