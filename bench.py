@@ -166,8 +166,10 @@ def algorithmic_bytes(n, nnz, nnz_l, nnz_u, m_steps_dims, W=8):
     # MGS passes at step j: pass 0 (read w, v0), j fused passes (w, v_{i-1},
     # v_i read, w write), tail (w, v_j read, w write): (4j+5) W n
     mgs = sum((4 * j + 5) * W * n for dims in m_steps_dims for j in range(dims))
+    # what k_arnoldi moves: the j+1 basis vectors and w read once, v_{j+1} written
+    mgs_actual = sum((j + 3) * W * n for dims in m_steps_dims for j in range(dims))
     steps = sum(m_steps_dims)
-    return {"spmv_int": spmv * steps, "ilu_int": ilu * steps, "mgs": mgs,
+    return {"spmv_int": spmv * steps, "ilu_int": ilu * steps, "mgs": mgs, "mgs_actual": mgs_actual,
             "vec_div": 2 * W * n * steps}
 
 
@@ -201,15 +203,44 @@ def ref_cycle(B, sp, As, b, il, max_ref=1):
     return rep
 
 
+def host_cpu():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model, os.cpu_count()
+
+
+class pinned_core:
+    """Pin this process to one host core (taskset equivalent) for a CPU sample."""
+
+    def __enter__(self):
+        self.old = os.sched_getaffinity(0)
+        self.core = max(self.old)
+        os.sched_setaffinity(0, {self.core})
+        return self
+
+    def __exit__(self, *a):
+        os.sched_setaffinity(0, self.old)
+
+
 def cpu_sample(rp, ci, v, bh):
     B, kind = reference_solver()
     sp, As, b, il = ref_setup(B, rp, ci, v, bh)
-    rep = ref_cycle(B, sp, As, b, il, 1)
+    with pinned_core() as pc:
+        rep = ref_cycle(B, sp, As, b, il, 1)
     its = rep["total_inner_iterations"]
+    model, total = host_cpu()
     return {"value": its / rep["wall_time_sec"], "unit": "iters/s", "cores": 1, "kind": kind,
+            "host_cpu": model, "host_cores_total": total, "pinned_core": pc.core,
             "sample": f"1 refinement cycle ({its} int-GMRES iterations) of the config-2 solve, "
-                      f"checked mode, single thread (the reference has no threading); "
-                      f"{rep['wall_time_sec']:.2f} s"}
+                      f"checked mode, single thread pinned to core {pc.core} (the reference has no "
+                      f"threading); {rep['wall_time_sec']:.2f} s"}
 
 
 def run_reference(args, ws, rank):
@@ -234,7 +265,9 @@ def run_reference(args, ws, rank):
             "config": {"workload": f"cfg2: 3D 7-pt upwind CD {args.grid}^3, ILU(0), GMRES(30), tol 1e-10",
                        "step": "one refinement cycle (30 iterations) of the reference solver"},
             "cpu_baseline": {"value": val, "unit": "iters/s", "cores": 1, "kind": kind,
-                             "sample": "each step = 1 refinement cycle of the config-2 solve"},
+                             "host_cpu": host_cpu()[0], "host_cores_total": host_cpu()[1],
+                             "sample": "each step = 1 refinement cycle of the config-2 solve; the reference "
+                                       "is single-threaded (no threads / OpenMP in proj/core)"},
             "e2e": {"value": val, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -373,6 +406,29 @@ def run_cfg5_sharded(args, igm, dev, local, rank, ws, g=400, k=30):
     }
 
 
+# ----------------------------------------------------------------- parity
+def parity_check(d_x, rep, grid):
+    """The timed solve's x (every word) and report against the reference
+    library's whole solve of the same system (tests/golden/full_goldens.json,
+    made by tests/golden/make_full_goldens.py from oracle/_ref)."""
+    import hashlib
+    if grid != 128:
+        return {"parity": None, "why": "goldens exist for the 128^3 config only"}
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "full_goldens.json")) as f:
+            g = json.load(f)["cfg2"]["solve"]
+    except (OSError, KeyError, ValueError) as exc:
+        return {"parity": None, "why": f"no golden: {exc}"}
+    x = d_x.cpu().numpy()
+    xh = hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest()
+    r = g["report"]
+    same_rep = (rep.inner_dims == r["inner_dims"] and rep.relres_history == r["relres_history"]
+                and rep.gamma_history == r["gamma_history"] and rep.overflow_total == r["overflow_total"])
+    return {"parity": bool(xh == g["x"] and same_rep), "x_sha256": xh[:16], "golden_x_sha256": g["x"][:16],
+            "report_equal": bool(same_rep),
+            "against": "reference library whole solve (tests/golden/full_goldens.json cfg2)"}
+
+
 # ----------------------------------------------------------------- B200 arm
 def measured_traffic(kernel):
     """DRAM bytes per launch of `kernel` from the committed ncu --set full
@@ -384,20 +440,53 @@ def measured_traffic(kernel):
         return None
 
 
-def roofline_line(micro, dom, achieved, dom_bytes, hbm, src, top, breakdown):
-    """Dominant HBM-streaming kernel: the MGS pass in the config-5 call (all
-    operands from HBM); the config-2 view (L2-resident vectors) is attached."""
-    cfg2 = {"kernel": dom, "achieved": round(achieved, 1), "frac": round(achieved / hbm, 4),
-            "bytes_per_launch": dom_bytes, "top_device_time_class": top,
-            "top_class_note": "ilu_int is latency-bound (382-level wavefront), not bandwidth-bound"}
-    if micro and "mgs" in micro:
-        m = micro["mgs"]
-        return {"bound": "hbm", "kernel": "k_mgs (fused axpy_{i-1}+dot_i pass), config 5",
-                "achieved": m["GB/s"], "peak": hbm, "peak_source": src, "unit": "GB/s", "frac": m["frac"],
-                "traffic": measured_traffic("k_mgs_cfg5"), "bytes_per_launch": m["bytes"] / max(1, m["launches"]),
-                "cfg2": cfg2}
-    return {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm, "peak_source": src,
-            "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None, "cfg2": cfg2}
+def roofline_line(breakdown, ab, n, levels, ms_step, refinements, hbm, src, micro):
+    """The dominant kernel of the headline step: the integer ILU(0)
+    substitution (k_tri_pencil, 2 launches per iteration).  achieved = its
+    SURVEY.md 8(d) algorithmic bytes per launch / its average launch time
+    (CUDA events around each launch on the library's stream, instrumented
+    solve); traffic = ncu DRAM bytes per launch (profiles/traffic.json).
+    Every other class is listed under `classes` with its own fraction; MGS
+    (the persistent k_arnoldi step) is given against both the streaming
+    formula and the bytes it actually moves (w stays on chip), and the whole
+    cycle against BASELINE.md's 47.744 GB."""
+    ilu = breakdown["ilu_int"]
+    per_launch_ms = ilu["ms"] / ilu["launches"]
+    bytes_launch = ab["ilu_int"] / ilu["launches"]
+    achieved = bytes_launch / (per_launch_ms / 1e3) / 1e9
+    step_share = ilu["ms"] / ms_step
+    classes = {}
+    for name in ("mgs", "spmv_int", "ilu_fp", "norm2_serial", "residual_fp", "x_update"):
+        if name not in breakdown:
+            continue
+        e = dict(breakdown[name])
+        e["share_of_step"] = round(breakdown[name]["ms"] / ms_step, 4)
+        if name in ab:
+            gbs = ab[name] / (e["ms"] / 1e3) / 1e9
+            e["algorithmic_GB/s"] = round(gbs, 1)
+            e["frac"] = round(gbs / hbm, 4)
+        classes[name] = e
+    if "mgs" in classes and "mgs_actual" in ab:
+        gbs = ab["mgs_actual"] / (breakdown["mgs"]["ms"] / 1e3) / 1e9
+        classes["mgs"]["actual_bytes_GB/s"] = round(gbs, 1)
+        classes["mgs"]["frac_actual_bytes"] = round(gbs / hbm, 4)
+        classes["mgs"]["note"] = ("frac uses the streaming formula (4k+3)Wn (SURVEY 8(d)); k_arnoldi keeps w on "
+                                  "chip and moves (k+2)Wn per step (ncu: 375 MB at j=20, profiles/traffic.json), "
+                                  "frac_actual_bytes divides those")
+    cyc_ms = ms_step / max(1, refinements)
+    cycle = {"bytes_per_cycle": 47.744e9, "ms_per_cycle": round(cyc_ms, 3),
+             "floor_ms": round(47.744e9 / (hbm * 1e9) * 1e3, 3),
+             "frac": round(47.744e9 / (cyc_ms / 1e3) / 1e9 / hbm, 4)}
+    return {"bound": "hbm", "kernel": "k_tri_pencil<int> (ILU(0) substitution, pencil wavefront)",
+            "achieved": round(achieved, 1), "peak": hbm, "peak_source": src, "unit": "GB/s",
+            "frac": round(achieved / hbm, 4), "traffic": measured_traffic("k_tri_pencil_cfg2"),
+            "bytes_per_launch": int(bytes_launch), "us_per_launch": round(per_launch_ms * 1e3, 2),
+            "launches_per_step": ilu["launches"], "share_of_step": round(step_share, 4),
+            "levels": levels, "us_per_level": round(per_launch_ms * 1e3 / levels, 4),
+            "latency_note": "a dependent wavefront of `levels` levels: bounded by per-level latency, "
+                            "not by HBM (the 8(d) bytes are reported for comparability)",
+            "classes": classes, "cycle": cycle,
+            "cfg5_mgs": (micro or {}).get("mgs")}
 
 
 def run_b200(args, ws, rank, local):
@@ -477,12 +566,8 @@ def run_b200(args, ws, rank, local):
             if name in ab:
                 e["GB/s"] = round(ab[name] / (kms[i] / 1e3) / 1e9, 1)
             breakdown[name] = e
-    bw_classes = [k for k in ("mgs", "spmv_int", "vec_div") if k in breakdown]
-    dom = max(bw_classes, key=lambda k: breakdown[k]["ms"])
-    dom_ms = breakdown[dom]["ms"] / breakdown[dom]["launches"]
-    dom_bytes = ab[dom] / breakdown[dom]["launches"]
-    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
-    top = max(breakdown, key=lambda k: breakdown[k]["ms"])
+    roof = roofline_line(breakdown, ab, n, F.levels(False), ms / args.steps, rep.refinements, hbm, src, None)
+    parity = parity_check(d_x, rep, args.grid)
 
     del S, A, F, d_b, d_x, hb, hx
     torch.cuda.empty_cache()
@@ -507,6 +592,8 @@ def run_b200(args, ws, rank, local):
         except Exception as exc:  # the baseline is reported, never required
             cpu = {"value": None, "error": str(exc)}
 
+    if micro and "mgs" in micro:
+        roof["cfg5_mgs"] = micro["mgs"]
     if rank == 0:
         line = {
             "metric": "int-GMRES iters/s", "value": value, "unit": "iters/s", "n_gpus": ws,
@@ -524,7 +611,8 @@ def run_b200(args, ws, rank, local):
             "gpu_launches": int(launches),
             "e2e": {"value": e2e_val, "unit": "iters/s", "h2d_bytes_per_step": int(8 * n),
                     "d2h_bytes_per_step": int(8 * n)},
-            "roofline": roofline_line(micro, dom, achieved, dom_bytes, hbm, src, top, breakdown),
+            "roofline": roof,
+            "parity": parity,
             "kernel_microbench": micro,
             "breakdown": breakdown,
             "clocks": clk.summary(),

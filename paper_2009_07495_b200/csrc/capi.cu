@@ -56,6 +56,8 @@ igm_status guarded(F&& fn) {
     return set_err(f.st, f.msg);
   } catch (const CudaFail& e) {
     return set_err(IGM_CUDA_ERROR, e.what());
+  } catch (const LaunchFail& e) {
+    return set_err(IGM_CUDA_ERROR, e.what());
   } catch (const std::bad_alloc&) {
     return set_err(IGM_CUDA_ERROR, "host allocation failed");
   }

@@ -17,6 +17,8 @@
 #include "../../include/igm.h"
 
 #include <cuda_runtime.h>
+#include <atomic>
+#include <stdexcept>
 
 #include <cstdint>
 #include <string>
@@ -223,6 +225,17 @@ void launch_split_cast(cudaStream_t st, int n, const int* rp, const int* ci, con
                        int* err_row);
 
 int num_sms(int device);
+int cur_device();  // cudaGetDevice
+// once-per-device guard (cudaFuncSetAttribute applies per device)
+struct PerDevice {
+  std::atomic<unsigned long long> bits{0};
+  bool first(int device);
+};
+// a kernel launch failed (configuration error or sticky fault): the C ABI
+// returns IGM_CUDA_ERROR with this message
+struct LaunchFail : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
 void tri_trace_setup(int tile, unsigned long long* buf);
 extern unsigned long long g_launches;  // kernels launched by this library
 

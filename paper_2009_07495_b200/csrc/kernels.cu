@@ -125,9 +125,9 @@ inline int grid_full(long long n, int nt) {
   return static_cast<int>(g < 1 ? 1 : (g > 0x7fffffffLL ? 0x7fffffffLL : g));
 }
 
-inline int grid_for(long long n, int nt, int device = 0) {
+inline int grid_for(long long n, int nt, int device = -1) {
   long long g = (n + nt - 1) / nt;
-  const long long cap = static_cast<long long>(num_sms(device)) * 8;
+  const long long cap = static_cast<long long>(num_sms(device < 0 ? cur_device() : device)) * 8;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return static_cast<int>(g);
@@ -2365,7 +2365,29 @@ __global__ void k_fxupdate(long long n, int dim, const double* __restrict__ basi
 // ---------------------------------------------------------------------------
 // launchers
 
-#define LAUNCH_CHECK() ++g_launches
+// every launch is counted and checked: a launch-configuration error (not
+// reported by a later synchronisation) or a sticky device fault turns into
+// IGM_CUDA_ERROR at the C-ABI boundary instead of stale outputs
+static void launch_check_at(int line) {
+  ++g_launches;
+  const cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw LaunchFail(std::string("kernel launch (kernels.cu:") + std::to_string(line) + "): " + cudaGetErrorString(e));
+  }
+}
+#define LAUNCH_CHECK() launch_check_at(__LINE__)
+
+int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+bool PerDevice::first(int device) {
+  const unsigned long long bit = 1ull << (device & 63);
+  return (bits.fetch_or(bit) & bit) == 0;
+}
 
 void launch_spmv_int(cudaStream_t st, const DevSplit& m, int s, const i64* v, i64* out, u64* cnt,
                      const Ctl* ctl, bool checked) {
@@ -2463,7 +2485,7 @@ void launch_mgs_pass(cudaStream_t st, long long n, int mode, i64* w, const i64* 
                      ShiftsD sh, u64* cnt_axpy, u64* cnt_red, const Ctl* ctl, bool checked) {
   ProfScope prof_(st, KC_MGS);
   const int nt = 512;
-  const int g = static_cast<int>(std::max<long long>(1, std::min<long long>(2LL * num_sms(0), (n / 4 + nt - 1) / nt)));
+  const int g = static_cast<int>(std::max<long long>(1, std::min<long long>(2LL * num_sms(cur_device()), (n / 4 + nt - 1) / nt)));
   // 256-bit accesses when every stream is 32-byte aligned (n % 4 == 0 and
   // aligned bases); scalar otherwise
   auto al32 = [](const void* p) { return (reinterpret_cast<size_t>(p) & 31) == 0; };
@@ -2498,7 +2520,8 @@ void launch_fx_red(cudaStream_t st, long long n, int mode, const i64* v, const i
                    int b2, u64* acc, u64* abs_out, u64* cnt, bool checked) {
   ProfScope prof_(st, KC_MGS);
   const int nt = 512;
-  const int g = grid_for(n, nt) > 2 * num_sms(0) ? 2 * num_sms(0) : grid_for(n, nt);
+  const int sms = num_sms(cur_device());
+  const int g = grid_for(n, nt) > 2 * sms ? 2 * sms : grid_for(n, nt);
   if (checked)
     k_fx_red<true><<<g, nt, 0, st>>>(n, mode, v, w, b1, b2, acc, abs_out, cnt);
   else
@@ -2578,13 +2601,13 @@ void launch_arnoldi(cudaStream_t st, long long n, int j, long long S, const i64*
                     u64* absj, u64* nacc, u64* nabs, int f, ShiftsD sh, u64* cstep, i64* hess, int ld, i64* g,
                     i64* cs, i64* sn, i64* gabs, Ctl* ctl, unsigned gbase, bool checked, u64* vmx) {
   ProfScope prof_(st, KC_MGS);
-  const int G = num_sms(0);
+  const int dev = cur_device();
+  const int G = num_sms(dev);
   const size_t smem = static_cast<size_t>(S) * 16;
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;  // the attribute is per device
+  if (attr.first(dev)) {
     cudaFuncSetAttribute(k_arnoldi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kArnSmemMax));
     cudaFuncSetAttribute(k_arnoldi<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kArnSmemMax));
-    attr = true;
   }
   void* args[] = {&n, &j, &S, &w, &basis, &accj, &absj, &nacc, &nabs, &f, &sh, &cstep,
                   &hess, &ld, &g, &cs, &sn, &gabs, &ctl, &gbase, &vmx};
@@ -2660,10 +2683,11 @@ static void tri_launch_one(cudaStream_t st, const DevTri& t, const T* y, T* out,
     while (L > 1 && lay.total > kBudget) lay = tri_smem_layout<D, CP>(t.tile_cap, seg_cap, --L, t.max_seg_ext);
   }
   const size_t sm = lay.total;
-  static size_t done = 0;
-  if (sm > done) {
+  static size_t done[64] = {0};  // per device
+  const int dev = cur_device() & 63;
+  if (sm > done[dev]) {
     cudaFuncSetAttribute(k_tri<T, B, D, CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    done = sm;
+    done[dev] = sm;
   }
   TriArgs args = tri_args(t);
   {  // per-launch tag: splitmix64 of a counter (never 0, the words' initial tag)
@@ -2724,11 +2748,10 @@ static void pen_launch(cudaStream_t st, const DevTri& t, bool backward, const vo
                        bool checked, const double* prescale) {
   constexpr int D = 4, R = 16;
   const size_t sm = pencil_smem_bytes(R, D);
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;  // the attribute is per device
+  if (attr.first(cur_device())) {
     cudaFuncSetAttribute(k_tri_pencil<D, true, FP>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
     cudaFuncSetAttribute(k_tri_pencil<D, false, FP>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-    attr = true;
   }
   PenArgs a;
   a.gx = t.pen_gx;
@@ -2772,7 +2795,11 @@ int pencil27_max_resident(int device) {
   return std::min(std::min(a, b), c) * num_sms(device);
 }
 
-static void pen27_launch(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out, const Ctl* ctl,
+// k_tri27's bricks wait on each other in both directions, so they must all
+// be resident: a cooperative launch guarantees that (or fails, e.g. when
+// another context's kernels occupy the SMs).  Returns false when the launch
+// was refused; the caller then runs the generic wavefront.
+static bool pen27_launch(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out, const Ctl* ctl,
                          bool checked, bool fp = false, const double* prescale = nullptr) {
   P27Args a;
   a.gx = t.p27_gx;
@@ -2788,12 +2815,19 @@ static void pen27_launch(cudaStream_t st, const DevTri& t, bool backward, const 
   const int* stop = ctl ? &ctl->stop : nullptr;
   const int* err = ctl ? &ctl->err : nullptr;
   const size_t sm = pencil27_smem_bytes();
-  if (fp)
-    k_tri27<false, true><<<t.p27_nbricks, kP27Threads, sm, st>>>(a, y, out, stop, err, prescale);
-  else if (checked)
-    k_tri27<true><<<t.p27_nbricks, kP27Threads, sm, st>>>(a, y, out, stop, err, nullptr);
-  else
-    k_tri27<false><<<t.p27_nbricks, kP27Threads, sm, st>>>(a, y, out, stop, err, nullptr);
+  static PerDevice attr;  // the attribute is per device
+  if (attr.first(cur_device())) pencil27_max_resident(cur_device());
+  const double* ps = fp ? prescale : nullptr;
+  void* args[] = {&a, &y, &out, &stop, &err, &ps};
+  const void* fn = fp ? reinterpret_cast<const void*>(k_tri27<false, true>)
+                      : (checked ? reinterpret_cast<const void*>(k_tri27<true>)
+                                 : reinterpret_cast<const void*>(k_tri27<false>));
+  const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(t.p27_nbricks), dim3(kP27Threads), args, sm, st);
+  if (e == cudaErrorCooperativeLaunchTooLarge) {
+    cudaGetLastError();
+    return false;
+  }
+  return true;  // any other error is reported by LAUNCH_CHECK
 }
 
 void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out,
@@ -2804,8 +2838,8 @@ void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* 
   {
     ProfScope prof_(st, KC_TRI_INT);
     if (t.pen) pen_launch<false>(st, t, backward, y, out, ctl, checked, nullptr);
-    else if (t.pen27) pen27_launch(st, t, backward, y, out, ctl, checked);
-    else if (backward) tri_dispatch<i64, true>(st, t, y, out, ctl, nullptr);
+    else if (t.pen27 && pen27_launch(st, t, backward, y, out, ctl, checked)) {
+    } else if (backward) tri_dispatch<i64, true>(st, t, y, out, ctl, nullptr);
     else tri_dispatch<i64, false>(st, t, y, out, ctl, nullptr);
   }
   LAUNCH_CHECK();
@@ -2823,10 +2857,10 @@ void launch_tri_fp(cudaStream_t st, const DevTri& t, bool backward, const double
   if (!(t.pen && t.pen_blk_fp)) cudaMemsetAsync(t.ticket, 0, sizeof(int), st);
   ProfScope prof_(st, KC_TRI_FP);
   if (t.pen && t.pen_blk_fp) pen_launch<true>(st, t, backward, y, out, ctl, false, prescale);
-  else if (t.pen27 && t.p27_rec_fp)
-    pen27_launch(st, t, backward, reinterpret_cast<const i64*>(y), reinterpret_cast<i64*>(out), ctl, false, true,
-                 prescale);
-  else if (backward) tri_dispatch<double, true>(st, t, y, out, ctl, prescale);
+  else if (t.pen27 && t.p27_rec_fp &&
+           pen27_launch(st, t, backward, reinterpret_cast<const i64*>(y), reinterpret_cast<i64*>(out), ctl, false,
+                        true, prescale)) {
+  } else if (backward) tri_dispatch<double, true>(st, t, y, out, ctl, prescale);
   else tri_dispatch<double, false>(st, t, y, out, ctl, prescale);
   LAUNCH_CHECK();
 }

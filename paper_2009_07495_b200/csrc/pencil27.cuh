@@ -11,8 +11,9 @@
 //
 // Unlike the 7-point case the bricks depend on each other in both directions
 // (row (i,j,k) reads (i+1,j+1,k-1) of the +x / +y brick), so every brick of a
-// launch must be resident at once; the launcher checks the occupancy and
-// falls back to the generic wavefront otherwise.  Inside a brick every row
+// launch must be resident at once: the launcher uses a cooperative launch
+// (co-residency guaranteed or the launch fails) and falls back to the generic
+// wavefront when it fails.  Inside a brick every row
 // value goes through a shared-memory ring of R planes; brick-boundary rows are
 // also exported as tagged words (value, tag ^ value) in global memory, which
 // the neighbour bricks read.  A word of another launch / plane or a torn word
@@ -32,6 +33,7 @@ constexpr int kP27B = 16;                 // brick: 16 x 16 pencils
 constexpr int kP27Threads = kP27B * kP27B;  // one per pencil (8 warps of 16 x 2)
 constexpr int kP27R = 8;                  // ring planes
 constexpr int kP27Rec = 64;               // stream bytes per row: 13 x int32 factor, int32 info, u64 reciprocal
+constexpr int kP27Lag = 24;               // max steps a warp may lead its neighbour warps (ring of kP27R planes)
 
 // the 13 dependency offsets (di, dj, dk)
 __host__ __device__ constexpr int p27_di(int q) { return q < 9 ? q % 3 - 1 : (q < 12 ? q - 10 : -1); }
@@ -129,8 +131,10 @@ __global__ void __launch_bounds__(kP27Threads, 2) k_tri27(P27Args a, const i64* 
                                                           const int* stop, const int* err,
                                                           const double* prescale = nullptr) {
   extern __shared__ __align__(16) unsigned char p27_smem[];
+  __shared__ volatile int s_prog[kP27Threads / 32];  // steps completed per warp (ring back-pressure)
   if (stop != nullptr && (*stop | *err) != 0) return;
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31, xl = lane & 15, jl = 2 * w + (lane >> 4);
+  if (lane == 0) s_prog[w] = 0;
   const int bx = blockIdx.x % a.nbx, by = blockIdx.x / a.nbx;
   const int i = bx * kP27B + xl, j = by * kP27B + jl;
   const bool ing = i < a.gx && j < a.gy;
@@ -175,9 +179,24 @@ __global__ void __launch_bounds__(kP27Threads, 2) k_tri27(P27Args a, const i64* 
   // step-synchronous: at step s the lanes with (s - off) % 4 == 0 handle row
   // (s - off) / 4 (8 lanes per warp); the warp reconverges every step
   const int Smax = kP27B - 1 + 2 * (kP27B - 1) + 4 * gz;
+  int seen = 0;  // min progress of warps w-1 / w+1 last observed
 #pragma unroll 1
   for (int s = 0; s < Smax; ++s) {
     __syncwarp();
+    if (lane == 0) s_prog[w] = s;
+    // Step s overwrites ring slot k & 7, which held plane k - 8; its last
+    // readers (warps w-1, w, w+1: dependency offsets |dj| <= 1) read it at
+    // their step s - 25 at the latest (plane k - 7 with a dk = -1 entry,
+    // lane offset <= off + 3).  A factor with the full 27-point pattern keeps
+    // the warps within a step of each other; a subset pattern (no coupling
+    // back to warp w+1) could otherwise let warp w lap its consumers.
+    if (s - kP27Lag > seen) {
+      do {
+        const int a0 = w > 0 ? s_prog[w - 1] : 0x3fffffff;
+        const int a1 = w + 1 < kP27Threads / 32 ? s_prog[w + 1] : 0x3fffffff;
+        seen = a0 < a1 ? a0 : a1;
+      } while (s - kP27Lag > seen);
+    }
     const int dd = s - off;
     if (!ing || dd < 0 || (dd & 3) != 0 || (dd >> 2) >= gz) continue;
     const int k = dd >> 2;
@@ -273,6 +292,8 @@ __global__ void __launch_bounds__(kP27Threads, 2) k_tri27(P27Args a, const i64* 
       }
     }
   }
+  __syncwarp();
+  if (lane == 0) s_prog[w] = 0x3fffffff;  // done: never a consumer again
   if (CHECKED && !FP && a.stats != nullptr) {
     if (ymx) atomicMax(a.stats, static_cast<unsigned long long>(ymx + 1));
     if (zmx) atomicMax(a.stats + 1, static_cast<unsigned long long>(zmx + 1));
