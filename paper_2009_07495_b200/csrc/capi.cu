@@ -432,8 +432,16 @@ void build_tri(igm_ctx* c, DevTri& t, int n, const int* rp, const int* ci, const
   t.ticket = dalloc<int>(2);  // [tickets taken, CTAs finished]
   ck(cudaMemsetAsync(t.ticket, 0, 2 * sizeof(int), st), "ticket");
   if (S.grid[0] > 0 && env_int("IGM_PENCIL", 1) != 0) {  // structured 7-point: the pencil wavefront
-    const PencilStream P = build_pencil_stream(n, rp, ci, vals, dpos, upper, S.grid[0], S.grid[1], S.grid[2]);
+    // bricks are coupled through DSMEM in clusters along y (tri_pencil2.cuh):
+    // the largest power of two <= 8 that the brick rows fill
+    const int nby = (S.grid[1] + kPenY - 1) / kPenY;
+    int cy = nby >= 8 ? 8 : nby >= 4 ? 4 : nby >= 2 ? 2 : 1;
+    cy = env_int("IGM_PEN_CY", cy);
+    if (cy != 1 && cy != 2 && cy != 4 && cy != 8) cy = 1;
+    const PencilStream P = build_pencil_stream(n, rp, ci, vals, dpos, upper, S.grid[0], S.grid[1], S.grid[2], 16,
+                                               false, cy);
     if (P.ok) {
+      t.pen_cy = P.cy;
       t.pen = true;
       t.pen_gx = P.gx;
       t.pen_gy = P.gy;
@@ -444,7 +452,8 @@ void build_tri(igm_ctx* c, DevTri& t, int n, const int* rp, const int* ci, const
       t.pen_S = P.S;
       t.pen_pad = P.pad;
       t.pen_blk = dupload(P.blk.data(), P.blk.size(), st);
-      const PencilStream Q = build_pencil_stream(n, rp, ci, vals, dpos, upper, S.grid[0], S.grid[1], S.grid[2], 16, true);
+      const PencilStream Q =
+          build_pencil_stream(n, rp, ci, vals, dpos, upper, S.grid[0], S.grid[1], S.grid[2], 16, true, cy);
       if (Q.ok) t.pen_blk_fp = dupload(Q.blk.data(), Q.blk.size(), st);
       t.pen_bot = dupload(P.brick_of_ticket.data(), P.brick_of_ticket.size(), st);
     }

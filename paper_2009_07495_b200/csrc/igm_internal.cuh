@@ -114,6 +114,7 @@ struct DevTri {
   void* p27_rec_fp = nullptr;  // the FP64 substitution's stream (diagonal as a double)
   void* pen_blk_fp = nullptr;  // the FP64 substitution's stream (diagonal as a double)
   int* pen_bot = nullptr;
+  int pen_cy = 1;  // bricks per thread-block cluster along y in the stream's ticket order (tri_pencil2.cuh)
   int* ticket = nullptr;  // 1
 };
 

@@ -9,6 +9,7 @@
 // without host round trips.
 #include "igm_internal.cuh"
 #include "tri_pencil.cuh"
+#include "tri_pencil2.cuh"
 #include "pencil27.cuh"
 
 #include <algorithm>
@@ -2741,8 +2742,54 @@ static u64 pen_epoch() {
   return (z ^ (z >> 31)) | 1ull;
 }
 
-// pencil wavefront (tri_pencil.cuh) of a structured 7-point factor: integer
-// (FP = false) or FP64 (apply_inverse_fp) substitution
+// warp-specialised pencil wavefront (tri_pencil2.cuh), bricks coupled in
+// thread-block clusters of t.pen_cy along y.  Any ticket order the stream
+// builder produces is valid for every cluster size (a brick waits only on
+// bricks of earlier tickets), so a cluster launch that cannot be scheduled
+// (e.g. SMs taken by another context) falls back to single-brick CTAs.
+template <bool CHECKED, bool FP, int CY>
+static bool pen2_launch_cy(cudaStream_t st, const DevTri& t, const PenArgs& a, const i64* y, i64* out,
+                           const int* stop, const int* err, const double* prescale) {
+  static PerDevice attr;  // the attributes are per device
+  if (attr.first(cur_device())) {
+    cudaFuncSetAttribute(k_tri_pencil2<CHECKED, FP, CY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kP2Smem));
+  }
+  if constexpr (CY == 1) {
+    k_tri_pencil2<CHECKED, FP, 1><<<t.pen_nbricks, kP2Threads, kP2Smem, st>>>(a, y, out, stop, err, prescale);
+    return true;
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(t.pen_nbricks));
+    cfg.blockDim = dim3(kP2Threads);
+    cfg.dynamicSmemBytes = kP2Smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CY;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, k_tri_pencil2<CHECKED, FP, CY>, a, y, out, stop, err, prescale) == cudaSuccess)
+      return true;
+    cudaGetLastError();  // not launchable as clusters: fall back
+    return false;
+  }
+}
+
+template <bool CHECKED, bool FP>
+static void pen2_launch(cudaStream_t st, const DevTri& t, const PenArgs& a, const i64* y, i64* out, const int* stop,
+                        const int* err, const double* prescale) {
+  bool ok = false;
+  if (t.pen_cy == 8) ok = pen2_launch_cy<CHECKED, FP, 8>(st, t, a, y, out, stop, err, prescale);
+  else if (t.pen_cy == 4) ok = pen2_launch_cy<CHECKED, FP, 4>(st, t, a, y, out, stop, err, prescale);
+  else if (t.pen_cy == 2) ok = pen2_launch_cy<CHECKED, FP, 2>(st, t, a, y, out, stop, err, prescale);
+  if (!ok) pen2_launch_cy<CHECKED, FP, 1>(st, t, a, y, out, stop, err, prescale);
+}
+
+// pencil wavefront (tri_pencil.cuh / tri_pencil2.cuh) of a structured 7-point
+// factor: integer (FP = false) or FP64 (apply_inverse_fp) substitution
 template <bool FP>
 static void pen_launch(cudaStream_t st, const DevTri& t, bool backward, const void* y, void* out, const Ctl* ctl,
                        bool checked, const double* prescale) {
@@ -2774,6 +2821,15 @@ static void pen_launch(cudaStream_t st, const DevTri& t, bool backward, const vo
   const int* err = ctl ? &ctl->err : nullptr;
   const i64* yi = static_cast<const i64*>(y);
   i64* oi = static_cast<i64*>(out);
+  static const bool v2 = [] {  // IGM_PENCIL2=0 selects the single-warp-role kernel (A/B timing)
+    const char* e = std::getenv("IGM_PENCIL2");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  if (v2) {
+    if (checked && !FP) pen2_launch<true, FP>(st, t, a, yi, oi, stop, err, prescale);
+    else pen2_launch<false, FP>(st, t, a, yi, oi, stop, err, prescale);
+    return;
+  }
   if (checked && !FP)
     k_tri_pencil<D, true, FP><<<t.pen_nbricks, kPenThreads, sm, st>>>(a, yi, oi, stop, err, prescale);
   else

@@ -34,6 +34,7 @@ constexpr int kPenSkew = kPenX;            // max (i mod 16) + (j mod 2): steps 
 struct PencilStream {
   bool ok = false;
   int gx = 0, gy = 0, gz = 0, nbx = 0, nby = 0, nbricks = 0, S = 0;  // S = steps per warp
+  int cy = 1;   // bricks per thread-block cluster along y (tri_pencil2.cuh)
   int pad = 0;  // idle blocks after each warp's S steps (the kernel's prefetch runs ahead)
   // [ticket][warp][step] blocks of 768 B: 32 lanes x {f_x, f_y, f_z, info}
   // (int32), then 32 lanes x the exact reciprocal of |diag| (u64)
@@ -52,7 +53,7 @@ inline std::int32_t pencil_info(const SDivMagic& g, bool active, int present = 0
 // row has a duplicate column: the generic wavefront handles those.
 inline PencilStream build_pencil_stream(int n, const int* rp, const int* ci, const std::int64_t* vals,
                                         const int* dpos, bool upper, int gx, int gy, int gz, int pad = 16,
-                                        bool fp = false) {
+                                        bool fp = false, int cy = 1) {
   PencilStream P;
   if (gx < 2 || gy < 2 || gz < 1 || static_cast<long long>(gx) * gy * gz != n || gx > 0xffff * kPenX ||
       gy > 0x7fff * kPenY)
@@ -95,15 +96,23 @@ inline PencilStream build_pencil_stream(int n, const int* rp, const int* ci, con
   P.gz = gz;
   P.nbx = (gx + kPenX - 1) / kPenX;
   P.nby = (gy + kPenY - 1) / kPenY;
-  P.nbricks = P.nbx * P.nby;
+  // tickets: clusters of cy bricks stacked along y (cy = 1: single bricks) in
+  // wavefront order (cbx + cby, then cbx), a cluster's bricks at consecutive
+  // tickets by rank; the y extent is padded to whole clusters with idle bricks
+  const int ncy = (P.nby + cy - 1) / cy;
+  P.cy = cy;
+  P.nbricks = P.nbx * ncy * cy;
   P.S = gz + kPenSkew;
   P.pad = pad;
   const int SB = P.S + pad;  // blocks per warp
-  for (int b = 0; b < P.nbricks; ++b) P.brick_of_ticket.push_back(((b / P.nbx) << 16) | (b % P.nbx));
-  std::stable_sort(P.brick_of_ticket.begin(), P.brick_of_ticket.end(), [](int a, int b) {
+  std::vector<int> clusters;
+  for (int c = 0; c < P.nbx * ncy; ++c) clusters.push_back(((c / P.nbx) << 16) | (c % P.nbx));
+  std::stable_sort(clusters.begin(), clusters.end(), [](int a, int b) {
     const int sa = (a & 0xffff) + (a >> 16), sb = (b & 0xffff) + (b >> 16);
     return sa != sb ? sa < sb : (a & 0xffff) < (b & 0xffff);
   });
+  for (int c : clusters)
+    for (int r = 0; r < cy; ++r) P.brick_of_ticket.push_back((((c >> 16) * cy + r) << 16) | (c & 0xffff));
   const size_t blocks = static_cast<size_t>(P.nbricks) * kPenWarps * SB;
   P.blk.assign(blocks * 96, 0);
   const SDivMagic one = make_sdiv(1);
