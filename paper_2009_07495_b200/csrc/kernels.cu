@@ -1353,7 +1353,7 @@ __device__ __forceinline__ u64 grid_barrier(Ctl* ctl, unsigned target, const u64
 }
 
 // CTA-wide wrapping sums of (s0, s1, s2) -> one atomic each (s1, s2 when CHECKED)
-template <bool CHECKED>
+template <bool CHECKED, int NT = kArnThreads>
 __device__ __forceinline__ void cta_reduce_add(u64 s0, u64 s1, u64 s2, u64* out0, u64* out12, u64 (*red)[32]) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -1372,7 +1372,7 @@ __device__ __forceinline__ void cta_reduce_add(u64 s0, u64 s1, u64 s2, u64* out0
   __syncthreads();
   if (threadIdx.x == 0) {
     u64 a = 0, b = 0, c = 0;
-    for (int i = 0; i < kArnThreads / 32; ++i) {
+    for (int i = 0; i < NT / 32; ++i) {
       a += red[0][i];
       b += red[1][i];
       c += red[2][i];
@@ -1681,6 +1681,7 @@ __global__ void __launch_bounds__(kArnThreads, 1)
   }
 }
 
+
 __global__ void k_cycle_init(Ctl* ctl, i64* g, int f) {
   ctl->gbar = 0;
   ctl->stop = 0;
@@ -1859,6 +1860,337 @@ __device__ __forceinline__ i64 lds64(unsigned a) {
 __device__ __forceinline__ void sts64(unsigned a, i64 v) {
   asm volatile("st.shared.s64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
 }
+
+// K2-K5, register-resident variant (config 2 sizes): the same passes, step
+// order and overflow accounting as k_arnoldi, but w lives in registers (512
+// threads x kArn2Q quads of 4 rows each), the two shared-memory buffers hold
+// v_{i-1} and v_i, and each next basis vector's slice arrives by one bulk
+// copy (TMA, cp.async.bulk + mbarrier) issued as soon as its buffer is free
+// -- so the HBM stream of the basis overlaps each pass's reduction and grid
+// barrier instead of following it.
+constexpr int kArn2Threads = 512;
+constexpr int kArn2Q = 7;  // quads per thread: up to 4 * 512 * 7 = 14336 rows per CTA
+
+template <bool CHECKED>
+__global__ void __launch_bounds__(kArn2Threads, 1)
+    k_arnoldi2(long long n, int j, long long S, const i64* __restrict__ win, i64* basis, u64* accj, u64* absj,
+               u64* nacc, u64* nabs, int f, ShiftsD sh, u64* cstep, i64* hess, int ld, i64* g, i64* cs, i64* sn,
+               i64* gabs, Ctl* ctl, unsigned gbase, u64* vmx) {
+  extern __shared__ __align__(16) i64 arn_sm[];
+  __shared__ u64 red[3][32];
+  __shared__ u64 s_word;
+  __shared__ int s_vd[6];
+  __shared__ __align__(8) unsigned long long s_bar[2];
+  __shared__ u64 s_mx[2];
+  if (cycle_over(ctl)) return;  // uniform: ctl is not written before the first barrier
+  constexpr int T = kArn2Threads, Q = kArn2Q;
+  const unsigned G = gridDim.x;
+  unsigned nbar = gbase;
+  const long long lo = static_cast<long long>(blockIdx.x) * S;
+  const long long cnt = max(0LL, min(n, lo + S) - lo);  // a multiple of 4 (n, S are)
+  const int nq = static_cast<int>(cnt >> 2);
+  const int tid = threadIdx.x;
+  i64* buf[2] = {arn_sm, arn_sm + S};
+  const unsigned bar0 = smem_u32(&s_bar[0]);
+  if (tid == 0) {
+    mbar_init_s(bar0, 1);
+    mbar_init_s(bar0 + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  unsigned ph[2] = {0, 0};
+  // thread 0: this CTA's slice of basis vector `v` into buffer b
+  auto fetch = [&](int b, const i64* v) {
+    const unsigned bar = bar0 + 8u * b;
+    if (cnt > 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_expect_tx_s(bar, static_cast<unsigned>(cnt * 8));
+      bulk_g2s_s(smem_u32(buf[b]), v + lo, static_cast<unsigned>(cnt * 8), bar);
+    } else {
+      mbar_arrive_s(bar);
+    }
+  };
+  auto wait_buf = [&](int b) {
+    mbar_wait_s(bar0 + 8u * b, ph[b]);
+    ph[b] ^= 1u;
+  };
+  if (tid == 0) {
+    fetch(0, basis);
+    if (j >= 1) fetch(1, basis + n);
+  }
+  u64 *cA = cstep + K_AXPY * OP_COUNT, *cD = cstep + K_DOT * OP_COUNT, *cN = cstep + K_NORM * OP_COUNT;
+  const int post = f - sh.axpy_b1;
+  auto dot_term = [&](i64 wl, i64 c, ArnAcc& A, auto ovf) {
+    const i64 a = asr(wl, sh.dot_b1), b = asr(c, sh.dot_b2);
+    const i64 t = wmul(a, b);
+    A.sum += static_cast<u64>(t);
+    if (CHECKED) {
+      if (decltype(ovf)::value) A.n3 += mul_ovf(a, b);
+      A.abs_add(t);
+    }
+  };
+  auto axpy_term = [&](i64 hs, i64 vp, i64& wl, ArnAcc& A, auto ovf) {
+    const i64 d = asr(wmul(hs, vp), post);
+    if (CHECKED && decltype(ovf)::value) {
+      A.n1 += mul_ovf(hs, vp);
+      A.n2 += sub_ovf(wl, d);
+    }
+    wl = wsub(wl, d);
+  };
+  // magnitude bounds (checked mode), exactly as in k_arnoldi
+  constexpr u64 kLim = 1ull << 63;
+  auto absu = [](i64 v) -> u64 { return v < 0 ? u64{0} - static_cast<u64>(v) : static_cast<u64>(v); };
+  auto mul_lt = [&](u64 x, u64 y2) { return __umul64hi(x, y2) == 0 && x * y2 < kLim; };
+  auto shb = [](u64 v, int s2) { return (s2 >= 63 ? 0ull : (v >> (s2 < 0 ? 0 : s2))) + 1; };
+  const int vst = ld + 1;
+  u64* vmx_me = vmx + static_cast<size_t>(blockIdx.x) * vst;
+  u64 Wb = 0, V0 = 0;
+  auto cta_max2 = [&](u64 m0, u64 m1) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      m0 = max(m0, static_cast<u64>(__shfl_down_sync(0xffffffffu, m0, o)));
+      m1 = max(m1, static_cast<u64>(__shfl_down_sync(0xffffffffu, m1, o)));
+    }
+    if (tid == 0) s_mx[0] = s_mx[1] = 0;
+    __syncthreads();
+    if ((tid & 31) == 0) {
+      atomicMax(reinterpret_cast<unsigned long long*>(&s_mx[0]), static_cast<unsigned long long>(m0));
+      atomicMax(reinterpret_cast<unsigned long long*>(&s_mx[1]), static_cast<unsigned long long>(m1));
+    }
+    __syncthreads();
+  };
+  auto certify = [&](u64 ahs, u64 Vp, int qs1, u64 Qb, bool has_axpy) {
+    bool ok = true;
+    u64 W2 = Wb;
+    if (has_axpy) {
+      ok = post >= 0 && mul_lt(ahs, Vp);
+      const u64 dmax = ok ? ((ahs * Vp) >> post) + 1 : kLim;
+      ok = ok && W2 < kLim && dmax < kLim - W2;
+      W2 = ok ? W2 + dmax : kLim;
+    }
+    ok = ok && mul_lt(shb(W2, qs1), Qb);
+    Wb = W2;
+    return ok;
+  };
+  i64 wr[Q][4];  // this thread's rows of w: quads tid + m * T
+  // ---- pass 0: w -> registers, dot_0 = <w, v_0>
+  {
+    wait_buf(0);
+    ArnAcc A;
+#pragma unroll
+    for (int m = 0; m < Q; ++m) {
+      const int q = tid + m * T;
+      if (q < nq) {
+        i64 cq[4];
+        ld_v4_nc(win + lo + 4 * q, wr[m]);
+        lds_q(buf[0] + 4 * q, cq);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          dot_term(wr[m][e], cq[e], A, std::true_type{});
+          if (CHECKED) {
+            Wb = max(Wb, absu(wr[m][e]));
+            V0 = max(V0, absu(cq[e]));
+          }
+        }
+      }
+    }
+    if (CHECKED) bump(cD, OP_MUL, A.n3);
+    cta_reduce_add<CHECKED, T>(A.sum, A.ahi, A.alo, accj + 0, absj + 0, red);
+    if (CHECKED) {
+      cta_max2(Wb, V0);
+      Wb = s_mx[0];
+      V0 = s_mx[1];
+    }
+  }
+  const int e0 = f - sh.dot_b1 - sh.dot_b2;
+  auto h_of = [&](u64 acc) {
+    const i64 a = static_cast<i64>(acc);
+    const i64 h = e0 >= 0 ? asr(a, e0) : wrap_shl(a, -e0);
+    return asr(h, sh.axpy_b1);
+  };
+  // ---- passes 1..j: axpy_{i-1} (v_{i-1} in buf[(i-1)&1]), dot_i (v_i in buf[i&1])
+  for (int i = 1; i <= j; ++i) {
+    const i64 hs = h_of(grid_barrier(ctl, (++nbar) * G, accj + i - 1, &s_word));
+    wait_buf(i & 1);
+    const i64* vp = buf[(i - 1) & 1];
+    const i64* vc = buf[i & 1];
+    ArnAcc A;
+    auto pass = [&](auto ovf) {
+#pragma unroll
+      for (int m = 0; m < Q; ++m) {
+        const int q = tid + m * T;
+        if (q < nq) {
+          i64 pq[4], cq[4];
+          lds_q(vp + 4 * q, pq);
+          lds_q(vc + 4 * q, cq);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            axpy_term(hs, pq[e], wr[m][e], A, ovf);
+            dot_term(wr[m][e], cq[e], A, ovf);
+          }
+        }
+      }
+    };
+    if (CHECKED && certify(absu(hs), i == 1 ? V0 : vmx_me[i - 1], sh.dot_b1, shb(vmx_me[i], sh.dot_b2), true))
+      pass(std::false_type{});
+    else
+      pass(std::true_type{});
+    if (CHECKED) {
+      bump(cA, OP_MUL, A.n1);
+      bump(cA, OP_SUB, A.n2);
+      bump(cD, OP_MUL, A.n3);
+    }
+    cta_reduce_add<CHECKED, T>(A.sum, A.ahi, A.alo, accj + i, absj + 2 * i, red);
+    // every thread is past its reads of v_{i-1}: its buffer takes v_{i+1}
+    if (tid == 0 && i + 1 <= j) fetch((i + 1) & 1, basis + static_cast<long long>(i + 1) * n);
+  }
+  // ---- axpy_j (v_j in buf[j&1]), then the norm sum of the orthogonalised w
+  {
+    const i64 hs = h_of(grid_barrier(ctl, (++nbar) * G, accj + j, &s_word));
+    const i64* vp = buf[j & 1];
+    ArnAcc A;
+    auto pass = [&](auto ovf) {
+#pragma unroll
+      for (int m = 0; m < Q; ++m) {
+        const int q = tid + m * T;
+        if (q < nq) {
+          i64 pq[4];
+          lds_q(vp + 4 * q, pq);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            axpy_term(hs, pq[e], wr[m][e], A, ovf);
+            const i64 sq = asr(wr[m][e], sh.norm_b1);
+            const i64 t = wmul(sq, sq);
+            A.sum += static_cast<u64>(t);
+            if (CHECKED) {
+              if (decltype(ovf)::value) A.n3 += mul_ovf(sq, sq);
+              A.abs_add(t);
+            }
+          }
+        }
+      }
+    };
+    bool fast = false;
+    if (CHECKED) {
+      const u64 Vp = j == 0 ? V0 : vmx_me[j];
+      fast = certify(absu(hs), Vp, 0, 1, true);
+      fast = fast && mul_lt(shb(Wb, sh.norm_b1), shb(Wb, sh.norm_b1));
+    }
+    if (fast)
+      pass(std::false_type{});
+    else
+      pass(std::true_type{});
+    if (CHECKED) {
+      bump(cA, OP_MUL, A.n1);
+      bump(cA, OP_SUB, A.n2);
+      bump(cN, OP_MUL, A.n3);
+    }
+    cta_reduce_add<CHECKED, T>(A.sum, A.ahi, A.alo, nacc, nabs, red);
+  }
+  // ---- per-step scalar work (one thread), then v_{j+1} = w / h_{j+1,j}
+  grid_barrier(ctl, (++nbar) * G, nullptr, nullptr);
+  if (blockIdx.x == 0 && 6LL * (j + 2) > 2 * S) {  // too small a slice to stage in: straight from global memory
+    if (tid == 0) {
+      __threadfence();
+      i64* w0 = reinterpret_cast<i64*>(&s_word);
+      *w0 = nq > 0 ? wr[0][0] : 0;
+      step_scalar_dev(j, f, sh, accj, 1, absj, 2, nacc, nabs, cstep + K_NORM * OP_COUNT + OP_MUL, hess, ld, g, cs,
+                      sn, gabs, w0, cstep, ctl, CHECKED ? 1 : 0);
+    }
+  } else if (blockIdx.x == 0) {
+    // the scalar step is a dependent chain of small reads and writes: stage
+    // its operands (reduced accumulators, certificates, the Hessenberg
+    // column, the stored rotations) in shared memory with all threads (the
+    // v buffers are free now), run it on one thread there, write back
+    u64* s_acc = reinterpret_cast<u64*>(buf[0]);
+    u64* s_abs = s_acc + (j + 1);
+    i64* s_col = reinterpret_cast<i64*>(s_abs + 2 * (j + 1));
+    i64* s_cs = s_col + (j + 2);
+    i64* s_sn = s_cs + (j + 1);
+    i64* col = hess + static_cast<long long>(j) * ld;
+    for (int q = tid; q <= j; q += T) {
+      s_acc[q] = ld_cg_u64(accj + q);  // L2: the atomics' results
+      s_abs[2 * q] = ld_cg_u64(absj + 2 * q);
+      s_abs[2 * q + 1] = ld_cg_u64(absj + 2 * q + 1);
+      s_col[q] = col[q];
+      if (q < j) {
+        s_cs[q] = cs[q];
+        s_sn[q] = sn[q];
+      }
+    }
+    if (tid == 0) s_col[j + 1] = col[j + 1];
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();  // this SM's L1 holds no stale copy of the reduced words
+      // w is only dereferenced for an error diagnostic: row 0 (this thread's first)
+      i64* w0 = s_sn + (j + 1);
+      *w0 = nq > 0 ? wr[0][0] : 0;
+      step_scalar_dev(j, f, sh, s_acc, 1, s_abs, 2, nacc, nabs, cstep + K_NORM * OP_COUNT + OP_MUL,
+                      s_col - static_cast<long long>(j) * ld, ld, g, s_cs, s_sn, gabs, w0, cstep, ctl,
+                      CHECKED ? 1 : 0);
+    }
+    __syncthreads();
+    for (int q = tid; q <= j + 1; q += T) col[q] = s_col[q];
+    if (tid == 0) {
+      cs[j] = s_cs[j];
+      sn[j] = s_sn[j];
+    }
+  }
+  const u64 dm = grid_barrier(ctl, (++nbar) * G, &ctl->div_m, &s_word);
+  if (tid == 0) {
+    volatile const int* c = &ctl->do_vecdiv;
+    s_vd[0] = c[0];
+    s_vd[1] = *static_cast<volatile int*>(&ctl->div_sh1);
+    s_vd[2] = *static_cast<volatile int*>(&ctl->div_sh2);
+    s_vd[3] = *static_cast<volatile int*>(&ctl->div_neg);
+    s_vd[4] = *static_cast<volatile int*>(&ctl->div_m1);
+  }
+  __syncthreads();
+  if (!s_vd[0]) return;
+  {
+    SDivMagic gm;
+    gm.u.m = dm;
+    gm.u.sh1 = s_vd[1];
+    gm.u.sh2 = s_vd[2];
+    gm.den_neg = s_vd[3];
+    gm.den_is_m1 = s_vd[4];
+    const int b1 = sh.div_b1, ee = f - sh.div_b1 - sh.div_b2;
+    i64* out = basis + static_cast<long long>(j + 1) * n + lo;
+    u64 nshl = 0, ndiv = 0, vmax = 0;
+#pragma unroll
+    for (int m = 0; m < Q; ++m) {
+      const int q = tid + m * T;
+      if (q < nq) {
+        i64 vq[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const i64 a = wr[m][e];
+          const i64 num = wrap_shl(a, b1);
+          const i64 qq = sdiv(num, gm);
+          if (ee >= 0) {
+            vq[e] = wrap_shl(qq, ee);
+            if (CHECKED) nshl += shl_ovf(qq, ee);
+          } else {
+            vq[e] = asr(qq, -ee);
+          }
+          if (CHECKED) {
+            nshl += shl_ovf(a, b1);
+            ndiv += sdiv_ovf(num, gm);
+            vmax = max(vmax, absu(vq[e]));
+          }
+        }
+        st_v4(out + 4 * q, vq);
+      }
+    }
+    if (CHECKED) {
+      bump(cstep + K_VEC_DIV * OP_COUNT, OP_SHL, nshl);
+      bump(cstep + K_VEC_DIV * OP_COUNT, OP_DIV, ndiv);
+      cta_max2(vmax, 0);
+      if (tid == 0) vmx_me[j + 1] = s_mx[0];
+    }
+  }
+}
+
 __device__ __forceinline__ int4 lds128i(unsigned a) {
   int4 v;
   asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
@@ -2612,6 +2944,22 @@ void launch_arnoldi(cudaStream_t st, long long n, int j, long long S, const i64*
   }
   void* args[] = {&n, &j, &S, &w, &basis, &accj, &absj, &nacc, &nabs, &f, &sh, &cstep,
                   &hess, &ld, &g, &cs, &sn, &gabs, &ctl, &gbase, &vmx};
+  static const bool v2 = [] {  // IGM_ARNOLDI2=0: the shared-memory-resident k_arnoldi (A/B timing)
+    const char* e = std::getenv("IGM_ARNOLDI2");
+    return e == nullptr || e[0] != '0';
+  }();
+  if (v2 && S <= 4LL * kArn2Threads * kArn2Q) {  // w fits the registers: k_arnoldi2
+    static PerDevice attr2;
+    if (attr2.first(dev)) {
+      cudaFuncSetAttribute(k_arnoldi2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kArnSmemMax));
+      cudaFuncSetAttribute(k_arnoldi2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kArnSmemMax));
+    }
+    const void* fn2 =
+        checked ? reinterpret_cast<const void*>(k_arnoldi2<true>) : reinterpret_cast<const void*>(k_arnoldi2<false>);
+    cudaLaunchCooperativeKernel(fn2, dim3(G), dim3(kArn2Threads), args, smem, st);
+    LAUNCH_CHECK();
+    return;
+  }
   const void* fn = checked ? reinterpret_cast<const void*>(k_arnoldi<true>) : reinterpret_cast<const void*>(k_arnoldi<false>);
   cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kArnThreads), args, smem, st);
   LAUNCH_CHECK();
