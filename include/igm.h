@@ -247,6 +247,38 @@ igm_status igm_solve(igm_ctx* ctx, const igm_split* m, const igm_csrf* a_fp,
                      const igm_ilu* precond, double* x_out, igm_report* rep,
                      igm_trace* external_trace);
 
+/* ---- config 3's WL = 32 variant ----------------------------------------- */
+/* The int-GMRES cycle with 32-bit words (BASELINE.json config 3, "WL=32 fixed
+ * point").  The reference has no WL != 64 code (fxp.hpp:22, a SPEC.md:149
+ * non-goal), so these entries replace no reference function: they are the
+ * reference's unpreconditioned run_cycle / solve (gmres_int.cpp:42-196,
+ * refine.cpp:21-106) with every word an int32 and every wrap mod 2^32, checked
+ * against the CPU restatement oracle/igm_oracle32.c (parity unpinned).  One
+ * departure from the WL = 64 ShiftPlan rules: rot_b may be > 0 (two Q.f words
+ * of magnitude ~1 multiply to 2^(2f), which needs rot_b >= f - 15). */
+typedef struct igm_split32 igm_split32;
+/* the int64 components of an uploaded split narrowed to int32 (the CSR
+ * pattern is shared); IGM_OVERFLOW_ERROR if a value does not fit */
+igm_status igm_split32_from_split(igm_ctx* ctx, const igm_split* m, igm_split32** out);
+void igm_split32_free(igm_split32* m);
+typedef struct {
+  int m, frac_bits, s, checked;
+  igm_shifts shifts;
+} igm_cycle32_cfg;
+/* the builder's WL = 32 shift plan for n rows, matrix scaling alpha_a (the
+ * split's) and frac_bits: each shift keeps its operands and sums inside 31
+ * bits with the headroom of a sum of n terms */
+igm_status igm_shifts32_plan(long long n, int alpha_a, int frac_bits, igm_shifts* out);
+/* one cycle from x0 = 0; any output may be NULL: basis ((m+1)*n), hess
+ * ((m+1)*m, column-major), g (m+1), cos_raw / sin_raw (m) */
+igm_status igm_run_cycle32(igm_ctx* ctx, const igm_split32* m, const igm_cycle32_cfg* cfg, const double* b,
+                           double* x_out, int* dim, double* r0_norm, int32_t* basis, int* n_basis, int32_t* hess,
+                           int32_t* g, int32_t* cos_raw, int32_t* sin_raw, uint64_t* overflows);
+/* the refinement loop (refine.cpp:21-106) around the WL = 32 cycle; report
+ * arrays as in igm_solve (overflow_exact = 0 when a reduction may have wrapped) */
+igm_status igm_solve32(igm_ctx* ctx, const igm_split32* m, const igm_csrf* a_fp, const double* b, double tol,
+                       int max_refinements, const igm_cycle32_cfg* cfg, double* x_out, igm_report* rep);
+
 /* replaces intgmres::fp_cycle (refsolve.hpp:26-29, refsolve.cpp:9-105): one
  * FP64 GMRES(m) cycle from x0 on a, with an optional LEFT preconditioner
  * given as a host callback (in/out host buffers of n doubles; returns 0 on

@@ -365,6 +365,77 @@ class Oracle(_Backend):
         return comp[:nc.value].copy(), [int(a) for a in al[:nc.value]], bool(ex.value)
 
 
+class Cycle32Cfg(C.Structure):
+    _fields_ = [("m", C.c_int), ("f", C.c_int), ("s", C.c_int), ("checked", C.c_int), ("sh", Shifts)]
+
+
+class Oracle32:
+    """WL = 32 restatement (igm_oracle32.c): PARITY UNPINNED -- the reference
+    has no WL != 64 code (fxp.hpp:22)."""
+
+    def __init__(self):
+        ensure_built()
+        self.lib = C.CDLL(str(ORACLE_SO))
+        self.lib.ora32_last_error.restype = C.c_char_p
+
+    def _rc(self, rc):
+        if rc:
+            raise RuntimeError(f"oracle32 error {rc}: {self.lib.ora32_last_error().decode()}")
+
+    @staticmethod
+    def _split(rp, ci, comp32, alphas):
+        rp = np.ascontiguousarray(rp, np.int32); ci = np.ascontiguousarray(ci, np.int32)
+        comp32 = np.ascontiguousarray(np.atleast_2d(comp32), np.int32)
+        al = np.ascontiguousarray(alphas, np.int32)
+        return rp, ci, comp32, al
+
+    def spmv(self, rp, ci, comp32, alphas, s, v):
+        rp, ci, cv, al = self._split(rp, ci, comp32, alphas)
+        v = np.ascontiguousarray(v, np.int32)
+        out = np.zeros(len(rp) - 1, np.int32)
+        ov = C.c_uint64()
+        self._rc(self.lib.ora32_spmv(len(rp) - 1, _p(rp, i32p), _p(ci, i32p), _p(cv, i32p), cv.shape[1], cv.shape[0],
+                                     _p(al, i32p), s, _p(v, i32p), _p(out, i32p), C.byref(ov)))
+        return out, int(ov.value)
+
+    def run_cycle(self, rp, ci, comp32, alphas, m, f, s, shifts, b, checked=True):
+        rp, ci, cv, al = self._split(rp, ci, comp32, alphas)
+        n = len(rp) - 1
+        b = np.ascontiguousarray(b, np.float64)
+        x = np.zeros(n)
+        basis = np.zeros((m + 1) * n, np.int32)
+        hess = np.zeros((m + 1) * m, np.int32)
+        g = np.zeros(m + 1, np.int32)
+        cs = np.zeros(m, np.int32); sn = np.zeros(m, np.int32)
+        dim = C.c_int(); nb = C.c_int(); r0 = C.c_double(); ov = C.c_uint64()
+        cfg = Cycle32Cfg(m, f, s, int(checked), shifts)
+        self._rc(self.lib.ora32_run_cycle(n, _p(rp, i32p), _p(ci, i32p), _p(cv, i32p), cv.shape[1], cv.shape[0],
+                                          _p(al, i32p), C.byref(cfg), _p(b, f64p), _p(x, f64p), C.byref(dim),
+                                          C.byref(r0), _p(basis, i32p), C.byref(nb), _p(hess, i32p), _p(g, i32p),
+                                          _p(cs, i32p), _p(sn, i32p), C.byref(ov)))
+        return dict(dim=dim.value, r0_norm=r0.value, basis=basis[:nb.value * n].copy(), n_basis=nb.value,
+                    hess=hess, g=g, cos_raw=cs, sin_raw=sn, x=x, overflows=int(ov.value))
+
+    def solve(self, rp, ci, comp32, alphas, a_vals, b, tol, max_ref, m, f, s, shifts, checked=True):
+        rp, ci, cv, al = self._split(rp, ci, comp32, alphas)
+        n = len(rp) - 1
+        av = np.ascontiguousarray(a_vals, np.float64)
+        a = Csrf(n, _p(rp, i32p), _p(ci, i32p), _p(av, f64p))
+        b = np.ascontiguousarray(b, np.float64)
+        x = np.zeros(n)
+        rel = np.zeros(max_ref + 1); gam = np.zeros(max(max_ref, 1)); dims = np.zeros(max(max_ref, 1), np.int32)
+        nref = C.c_int(); conv = C.c_int(); ov = C.c_uint64()
+        cfg = Cycle32Cfg(m, f, s, int(checked), shifts)
+        self._rc(self.lib.ora32_solve(n, _p(rp, i32p), _p(ci, i32p), _p(cv, i32p), cv.shape[1], cv.shape[0],
+                                      _p(al, i32p), C.byref(a), _p(b, f64p), C.c_double(tol), max_ref, C.byref(cfg),
+                                      _p(x, f64p), _p(rel, f64p), _p(gam, f64p), _p(dims, i32p), C.byref(nref),
+                                      C.byref(conv), C.byref(ov)))
+        k = nref.value
+        return x, dict(refinements=k, relres_history=[float(v) for v in rel[:k + 1]],
+                       gamma_history=[float(v) for v in gam[:k]], inner_dims=[int(v) for v in dims[:k]],
+                       converged=bool(conv.value), overflow_total=int(ov.value))
+
+
 class Reference(_Backend):
     """The unmodified reference library (oracle/_ref); only where it was built."""
     prefix = "ref_"

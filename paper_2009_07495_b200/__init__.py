@@ -254,6 +254,10 @@ class ShiftPlan:
         return _capi.Shifts(self.dot_b1, self.dot_b2, self.axpy_b1, self.norm_b1, self.div_b1,
                             self.div_b2, self.givens_b2, self.rot_b)
 
+    def astuple(self) -> tuple:
+        return (self.dot_b1, self.dot_b2, self.axpy_b1, self.norm_b1, self.div_b1, self.div_b2,
+                self.givens_b2, self.rot_b)
+
 
 class FxTrace:
     """FxTrace (fxp.hpp:51-103) backed by an igm_trace."""
@@ -526,6 +530,79 @@ def solve(m: SplitMatrix, a_fp: CsrMatrixF, b, cfg: RefineConfig, precond: Optio
         overflow_total=int(rep.overflow_total), wall_time_sec=rep.wall_time_sec,
         overflow_exact=bool(rep.overflow_exact))
     return x, report
+
+
+# ------------------------------------------------- config 3's WL = 32 variant
+class SplitMatrix32:
+    """A SplitMatrix's components narrowed to int32 words (igm_split32_from_split).
+    WL = 32 has no reference implementation (fxp.hpp:22): parity is against
+    oracle/igm_oracle32.c only (unpinned)."""
+
+    def __init__(self, m: SplitMatrix):
+        self.dev, self.n, self.ncomp, self.alphas = m.dev, m.n, m.ncomp, m.alphas
+        self._src = m  # the CSR pattern is shared
+        h = C.c_void_p()
+        _check(lib().igm_split32_from_split(self.dev.h, m.h, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            lib().igm_split32_free(self.h)
+        except Exception:
+            pass
+
+
+def shifts32_plan(n: int, alpha_a: int, frac_bits: int) -> "ShiftPlan":
+    """The builder's WL = 32 shift plan (igm_shifts32_plan)."""
+    sh = _capi.Shifts()
+    _check(lib().igm_shifts32_plan(int(n), alpha_a, frac_bits, C.byref(sh)))
+    return ShiftPlan(sh.dot_b1, sh.dot_b2, sh.axpy_b1, sh.norm_b1, sh.div_b1, sh.div_b2, sh.givens_b2, sh.rot_b)
+
+
+def run_cycle32(m: SplitMatrix32, m_steps: int, frac_bits: int, s: int, shifts: "ShiftPlan", b, checked=True):
+    n = m.n
+    cfg = _capi.Cycle32Cfg(m_steps, frac_bits, s, 1 if checked else 0, shifts.c())
+    x = np.zeros(n)
+    basis = np.zeros((m_steps + 1) * n, dtype=np.int32)
+    hess = np.zeros((m_steps + 1) * m_steps, dtype=np.int32)
+    g = np.zeros(m_steps + 1, dtype=np.int32)
+    cs = np.zeros(m_steps, dtype=np.int32)
+    sn = np.zeros(m_steps, dtype=np.int32)
+    dim, nb, r0, ov = C.c_int(), C.c_int(), C.c_double(), C.c_uint64()
+    pb, k1 = _ptr(b, np.float64)
+    p = lambda a: C.c_void_p(a.ctypes.data)
+    _check(lib().igm_run_cycle32(m.dev.h, m.h, C.byref(cfg), pb, p(x), C.byref(dim), C.byref(r0), p(basis),
+                                 C.byref(nb), p(hess), p(g), p(cs), p(sn), C.byref(ov)))
+    return dict(dim=dim.value, r0_norm=r0.value, basis=basis[:nb.value * n].copy(), n_basis=nb.value, hess=hess,
+                g=g, cos_raw=cs, sin_raw=sn, x=x, overflows=int(ov.value))
+
+
+def solve32(m: SplitMatrix32, a_fp: "CsrMatrixF", b, tol: float, max_refinements: int, m_steps: int, frac_bits: int,
+            s: int, shifts: "ShiftPlan", checked=True, x_out=None):
+    """The refinement loop around the WL = 32 cycle (igm_solve32)."""
+    R = max(max_refinements, 0)
+    dims = np.zeros(R + 1, dtype=np.int32)
+    rel = np.zeros(R + 2)
+    gam = np.zeros(R + 1)
+    ovf = np.zeros(R + 1, dtype=np.uint64)
+    rep = _capi.Report()
+    rep.inner_dims = dims.ctypes.data_as(_capi.i32p)
+    rep.relres_history = rel.ctypes.data_as(_capi.f64p)
+    rep.gamma_history = gam.ctypes.data_as(_capi.f64p)
+    rep.overflow_per_restart = ovf.ctypes.data_as(_capi.u64p)
+    cfg = _capi.Cycle32Cfg(m_steps, frac_bits, s, 1 if checked else 0, shifts.c())
+    x = x_out if x_out is not None else _out_like(b, m.n, np.float64)
+    pb, k1 = _ptr(b, np.float64)
+    px, k2 = _ptr(x, np.float64)
+    _check(lib().igm_solve32(m.dev.h, m.h, a_fp.h, pb, C.c_double(tol), max_refinements, C.byref(cfg), px,
+                             C.byref(rep)))
+    k = rep.refinements
+    return x, SolveReport(
+        converged=bool(rep.converged), refinements=k, total_inner_iterations=int(rep.total_inner_iterations),
+        inner_dims=[int(v) for v in dims[:k]], relres_history=[float(v) for v in rel[:rep.n_relres]],
+        gamma_history=[float(v) for v in gam[:k]], overflow_per_restart=[int(v) for v in ovf[:k]],
+        overflow_total=int(rep.overflow_total), wall_time_sec=rep.wall_time_sec,
+        overflow_exact=bool(rep.overflow_exact))
 
 
 def spmv_mgs(m: SplitMatrix, s: int, v_in, basis, k: int, f: int, dot_b1: int, dot_b2: int,

@@ -67,6 +67,10 @@ class CycleOut(C.Structure):
     ]
 
 
+class Cycle32Cfg(C.Structure):
+    _fields_ = [("m", C.c_int), ("frac_bits", C.c_int), ("s", C.c_int), ("checked", C.c_int), ("shifts", Shifts)]
+
+
 class DcInfo(C.Structure):
     _fields_ = [("dim", C.c_int), ("stop", C.c_int), ("nbasis", C.c_int), ("add_inexact", C.c_int),
                 ("r0_norm", C.c_double), ("relnorm", C.c_double), ("nb", C.c_double), ("nr", C.c_double),
@@ -174,6 +178,15 @@ SIGNATURES = [
                                  C.POINTER(Shifts), C.c_int]),
     ("igm_dc_finish", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int64, C.c_void_p, C.c_void_p]),
     ("igm_dc_fetch", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    # config 3's WL = 32 variant
+    ("igm_split32_from_split", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
+    ("igm_split32_free", None, [C.c_void_p]),
+    ("igm_shifts32_plan", C.c_int, [C.c_longlong, C.c_int, C.c_int, C.POINTER(Shifts)]),
+    ("igm_run_cycle32", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(Cycle32Cfg), C.c_void_p, C.c_void_p,
+                                  C.POINTER(C.c_int), C.POINTER(C.c_double), C.c_void_p, C.POINTER(C.c_int),
+                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]),
+    ("igm_solve32", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int,
+                              C.POINTER(Cycle32Cfg), C.c_void_p, C.POINTER(Report)]),
     ("igm_row_scale_dev", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
                                     C.c_void_p]),
     ("igm_build_split_dev", C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p,

@@ -2026,3 +2026,268 @@ igm_status igm_mgs_pass(igm_ctx* c, int64_t n, int mode, int64_t* w, const int64
 }
 
 }  // extern "C"
+
+// ===========================================================================
+// Config 3's WL = 32 variant (wl32.cu).  No reference function: the
+// reference's unpreconditioned cycle / solve with int32 words (see igm.h).
+struct igm_split32 : igm::Dev32Split {
+  Wl32Work ws;  // per-handle cycle buffers (sized on first use)
+};
+
+namespace {
+
+void ws32_ensure(igm_split32* m, int M) {
+  Wl32Work& w = m->ws;
+  const long long n = m->n;
+  if (w.n == n && w.M >= M) return;
+  dfree(w.basis);
+  dfree(w.w);
+  dfree(w.small);
+  dfree(w.y);
+  dfree(w.wts);
+  w = Wl32Work{};
+  w.n = n;
+  w.M = M;
+  w.basis = dalloc<int32_t>(static_cast<size_t>(M + 1) * n + 1);
+  w.w = dalloc<int32_t>(static_cast<size_t>(n) + 1);
+  const size_t na = static_cast<size_t>(M) * (M + 1);
+  const size_t cnt = static_cast<size_t>(M) * K_COUNT * OP_COUNT;
+  // u64 arrays first (alignment), then the 32-bit ones
+  const size_t bytes = 8 * (na + M + cnt) + 4 * (na + M + static_cast<size_t>(M + 1) * M + (M + 1) + 2 * M) + 64;
+  w.small = dalloc<unsigned char>(bytes);
+  w.small_bytes = bytes;
+  unsigned char* p = static_cast<unsigned char*>(w.small);
+  w.abs = reinterpret_cast<u64*>(p);
+  w.nabs = w.abs + na;
+  w.cnt = w.nabs + M;
+  uint32_t* q = reinterpret_cast<uint32_t*>(w.cnt + cnt);
+  w.acc = q;
+  w.nacc = w.acc + na;
+  w.hess = reinterpret_cast<int32_t*>(w.nacc + M);
+  w.g = w.hess + static_cast<size_t>(M + 1) * M;
+  w.cs = w.g + (M + 1);
+  w.sn = w.cs + M;
+  w.y = dalloc<double>(M);
+  w.wts = dalloc<double>(M);
+}
+
+void validate_shifts32(const igm_shifts& p, int f) {  // fxp.cpp:106-127 at WL = 32 (rot_b relaxed)
+  if (f < 0 || f > 30) fail(IGM_INVALID_ARGUMENT, "QFormat: frac_bits must be in [0, 30]");
+  auto right = [&](int b, const char* name) {
+    if (b < 0 || (b > 0 && b >= f)) fail(IGM_INVALID_ARGUMENT, std::string("ShiftPlan: ") + name + " must lie in [0, frac_bits)");
+  };
+  right(p.dot_b1, "dot_b1");
+  right(p.dot_b2, "dot_b2");
+  right(p.axpy_b1, "axpy_b1");
+  right(p.norm_b1, "norm_b1");
+  right(p.div_b2, "div_b2");
+  right(p.givens_b2, "givens_b2");
+  if (p.div_b1 < 0 || p.div_b1 > f) fail(IGM_INVALID_ARGUMENT, "ShiftPlan: div_b1 must lie in [0, frac_bits]");
+  if (p.rot_b < 0 || (p.rot_b > 0 && p.rot_b >= f)) fail(IGM_INVALID_ARGUMENT, "ShiftPlan: rot_b must lie in [0, frac_bits)");
+  if (2 * (f - p.norm_b1) > 30)
+    fail(IGM_INVALID_ARGUMENT, "ShiftPlan: norm accumulator needs 2*(frac_bits - norm_b1) <= 30");
+}
+
+// one cycle at WL = 32 from the FP64 right-hand side r0 (device); returns dim
+int cycle32(igm_ctx* c, igm_split32* m, const igm_cycle32_cfg& cfg, const double* r0, int xmode, double* x) {
+  cudaStream_t st = c->stream;
+  const long long n = m->n;
+  ws32_ensure(m, cfg.m);
+  ck(cudaMemsetAsync(m->ws.small, 0, m->ws.small_bytes, st), "wl32 zero");
+  launch_norm2_serial(st, n, r0, nullptr, c->ctl, 3, n2_scratch(c, n));  // r0n (gmres_int.cpp:71-75)
+  enqueue_cycle32(st, m->ws, *m, cfg.m, cfg.frac_bits, cfg.s, to_sd(cfg.shifts), r0, c->ctl, cfg.checked != 0, xmode,
+                  x);
+  ck(cudaMemcpyAsync(c->h_ctl, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st), "ctl");
+  ck(cudaStreamSynchronize(st), "wl32 cycle");
+  raise_device_error(c);
+  return c->h_ctl->dim;
+}
+
+u64 cycle32_overflows(igm_ctx* c, igm_split32* m, int M, bool* inexact) {
+  std::vector<u64> cnt(static_cast<size_t>(M) * K_COUNT * OP_COUNT);
+  ck(cudaMemcpy(cnt.data(), m->ws.cnt, cnt.size() * 8, cudaMemcpyDeviceToHost), "wl32 counters");
+  u64 t = 0;
+  for (u64 v : cnt) t += v;
+  *inexact = c->h_ctl->add_inexact != 0;
+  return t;
+}
+
+}  // namespace
+
+igm_status igm_split32_from_split(igm_ctx* c, const igm_split* m, igm_split32** out) {
+  return guarded([&] {
+    need_ctx(c);
+    if (!m || !out) fail(IGM_INVALID_ARGUMENT, "split32: null argument");
+    auto* s = new igm_split32();
+    s->n = m->n;
+    s->nnz = m->nnz;
+    s->ncomp = m->ncomp;
+    s->row_ptr = m->row_ptr;  // the pattern is shared with the WL = 64 split
+    s->col_idx = m->col_idx;
+    s->own_pattern = false;
+    s->h_alphas = m->h_alphas;
+    s->device = c->device;
+    const long long cnt = static_cast<long long>(m->ncomp) * m->nnz;
+    s->vals = dalloc<int32_t>(static_cast<size_t>(std::max(cnt, 1LL)));
+    s->alphas = dupload(m->h_alphas.data(), m->h_alphas.size(), c->stream);
+    int* bad = dalloc<int>(1);
+    ck(cudaMemsetAsync(bad, 0, sizeof(int), c->stream), "split32");
+    launch_vals_to32(c->stream, cnt, m->vals, s->vals, bad);
+    int hb = 0;
+    ck(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "split32");
+    ck(cudaStreamSynchronize(c->stream), "split32");
+    dfree(bad);
+    if (hb) {
+      dfree(s->vals);
+      dfree(s->alphas);
+      delete s;
+      fail(IGM_OVERFLOW_ERROR, "split32: a component value does not fit in int32");
+    }
+    *out = s;
+  });
+}
+
+void igm_split32_free(igm_split32* m) {
+  if (!m) return;
+  cudaDeviceSynchronize();
+  dfree(m->vals);
+  dfree(m->alphas);
+  if (m->own_pattern) {
+    dfree(m->row_ptr);
+    dfree(m->col_idx);
+  }
+  dfree(m->ws.basis);
+  dfree(m->ws.w);
+  dfree(m->ws.small);
+  dfree(m->ws.y);
+  dfree(m->ws.wts);
+  delete m;
+}
+
+// The builder's plan.  Magnitudes in bits,
+// worst case: a basis word may be O(1) (later Krylov vectors of config 3
+// concentrate on few rows), v < 2^f; w = A v ~ 2^(alpha + 2) v; h ~ |w| 2^f ~
+// 2^(f + alpha + 1); a sum of n terms needs L = log2(n)/2 bits of headroom.
+igm_status igm_shifts32_plan(long long n, int alpha_a, int f, igm_shifts* out) {
+  return guarded([&] {
+    if (!out || n < 1) fail(IGM_INVALID_ARGUMENT, "shifts32_plan: bad argument");
+    const double L = std::log2(static_cast<double>(n)) / 2;
+    const double bv = f, bw = bv + alpha_a + 2, bh = f + alpha_a + 1;
+    auto clampf = [&](double v, int hi) { return static_cast<int>(std::max(0.0, std::min(static_cast<double>(hi), v))); };
+    const double need = bw + bv + L + 2 - 30;  // a sum of n dot terms in 30 bits
+    const int b2 = clampf(std::floor(std::ceil(need - (bw - bv)) / 2), f - 1);
+    const int b1 = clampf(std::ceil(need - b2), f - 1);
+    igm_shifts p{};
+    p.dot_b1 = b1;
+    p.dot_b2 = b2;
+    p.axpy_b1 = clampf(std::ceil(bh + bv - 30), f - 1);                    // (h >> b1) v in 30 bits
+    p.norm_b1 = clampf(std::max(static_cast<double>(f - 15), std::ceil(f - (29 - 2.0 * (alpha_a + 1)) / 2)), f - 1);
+    p.div_b1 = clampf(30 - bh, f);                                          // Givens: h << b1 in 30 bits
+    p.div_b2 = clampf(std::min(static_cast<double>(f - p.div_b1), bh - 16), f - 1);  // 16 bits of divisor
+    p.givens_b2 = clampf(std::ceil(bh + f + 1 - 30), f - 1);               // c (h >> b2) in 31 bits
+    p.rot_b = std::max(0, f - 15);                                         // c g, s g in 30 bits
+    *out = p;
+  });
+}
+
+igm_status igm_run_cycle32(igm_ctx* c, const igm_split32* mc, const igm_cycle32_cfg* cfg, const double* b,
+                           double* x_out, int* dim, double* r0_norm, int32_t* basis, int* n_basis, int32_t* hess,
+                           int32_t* g, int32_t* cos_raw, int32_t* sin_raw, uint64_t* overflows) {
+  return guarded([&] {
+    need_ctx(c);
+    if (!mc || !cfg || !b) fail(IGM_INVALID_ARGUMENT, "run_cycle32: null argument");
+    if (cfg->m < 1) fail(IGM_INVALID_ARGUMENT, "run_cycle: m must be >= 1");
+    if (cfg->s < 0 || cfg->s > mc->ncomp - 1) fail(IGM_INVALID_ARGUMENT, "run_cycle: splitting depth out of range");
+    validate_shifts32(cfg->shifts, cfg->frac_bits);
+    auto* m = const_cast<igm_split32*>(mc);
+    const long long n = m->n;
+    const int M = cfg->m;
+    ws_ensure(c, n, 1);
+    cudaStream_t st = c->stream;
+    In<double> db(b, n, st, c->ws.b);
+    reset_ctl(c);
+    const int d = cycle32(c, m, *cfg, db.d, 0, c->ws.x);
+    if (dim) *dim = d;
+    if (r0_norm) *r0_norm = c->h_ctl->r0n;
+    if (n_basis) *n_basis = c->h_ctl->r0n == 0.0 ? 0 : c->h_ctl->nbasis;
+    if (x_out) {
+      if (d > 0) ck(cudaMemcpyAsync(x_out, c->ws.x, sizeof(double) * n, cudaMemcpyDefault, st), "x");
+      else ck(cudaMemsetAsync(x_out, 0, 0, st), "x");  // x0 = 0: nothing to add
+    }
+    const int nb = c->h_ctl->r0n == 0.0 ? 0 : c->h_ctl->nbasis;
+    if (basis && nb) ck(cudaMemcpyAsync(basis, m->ws.basis, sizeof(int32_t) * nb * n, cudaMemcpyDefault, st), "basis");
+    if (hess) ck(cudaMemcpyAsync(hess, m->ws.hess, sizeof(int32_t) * (M + 1) * M, cudaMemcpyDefault, st), "hess");
+    if (g) ck(cudaMemcpyAsync(g, m->ws.g, sizeof(int32_t) * (M + 1), cudaMemcpyDefault, st), "g");
+    if (cos_raw) ck(cudaMemcpyAsync(cos_raw, m->ws.cs, sizeof(int32_t) * M, cudaMemcpyDefault, st), "cos");
+    if (sin_raw) ck(cudaMemcpyAsync(sin_raw, m->ws.sn, sizeof(int32_t) * M, cudaMemcpyDefault, st), "sin");
+    ck(cudaStreamSynchronize(st), "sync");
+    if (x_out && d == 0 && !is_device_ptr(x_out)) std::fill(x_out, x_out + n, 0.0);
+    bool inexact = false;
+    const u64 ov = cycle32_overflows(c, m, M, &inexact);
+    if (overflows) *overflows = ov;
+  });
+}
+
+igm_status igm_solve32(igm_ctx* c, const igm_split32* mc, const igm_csrf* a_fp, const double* b, double tol,
+                       int max_refinements, const igm_cycle32_cfg* cfg, double* x_out, igm_report* rep) {
+  return guarded([&] {
+    need_ctx(c);
+    if (!mc || !a_fp || !b || !cfg || !rep) fail(IGM_INVALID_ARGUMENT, "solve32: null argument");
+    if (a_fp->n != mc->n) fail(IGM_INVALID_ARGUMENT, "solve: dimension mismatch");
+    if (max_refinements < 0) fail(IGM_INVALID_ARGUMENT, "solve: max_refinements must be >= 0");
+    if (cfg->m < 1) fail(IGM_INVALID_ARGUMENT, "run_cycle: m must be >= 1");
+    if (cfg->s < 0 || cfg->s > mc->ncomp - 1) fail(IGM_INVALID_ARGUMENT, "run_cycle: splitting depth out of range");
+    validate_shifts32(cfg->shifts, cfg->frac_bits);
+    auto* m = const_cast<igm_split32*>(mc);
+    const auto t0 = std::chrono::steady_clock::now();
+    const long long n = m->n;
+    ws_ensure(c, n, 1);
+    Work& w = c->ws;
+    cudaStream_t st = c->stream;
+    rep->converged = 0;
+    rep->refinements = 0;
+    rep->total_inner_iterations = 0;
+    rep->n_relres = 0;
+    rep->overflow_total = 0;
+    rep->overflow_exact = 1;
+    In<double> db(b, n, st, w.b);
+    ck(cudaMemsetAsync(w.x, 0, sizeof(double) * n, st), "x=0");
+    reset_ctl(c);
+    launch_norm2_serial(st, n, db.d, nullptr, c->ctl, 1, n2_scratch(c, n));  // ||b||
+    launch_residual(st, *a_fp, w.x, db.d, w.r, c->ctl, true);
+    launch_norm2_serial(st, n, w.r, nullptr, c->ctl, 2, n2_scratch(c, n));
+    ck(cudaMemcpyAsync(c->h_ctl, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st), "ctl");
+    ck(cudaStreamSynchronize(st), "sync");
+    double relnorm = c->h_ctl->relnorm;
+    rep->relres_history[rep->n_relres++] = relnorm;
+    for (int k = 0; k < max_refinements && relnorm >= tol; ++k) {
+      const u64 rbits = c->h_ctl->rmax_bits;
+      double rmax;
+      std::memcpy(&rmax, &rbits, sizeof rmax);
+      if (rmax == 0.0) break;
+      launch_scale_div(st, n, w.r, w.r0, c->ctl);  // b_k = r / gamma (refine.cpp:53-56)
+      const int dim = cycle32(c, m, *cfg, w.r0, 1, w.x);
+      bool inexact = false;
+      const u64 ov = cycle32_overflows(c, m, cfg->m, &inexact);
+      if (inexact) rep->overflow_exact = 0;
+      if (dim == 0) break;
+      ck(cudaMemsetAsync(&c->ctl->rmax_bits, 0, sizeof(u64), st), "rmax reset");
+      launch_residual(st, *a_fp, w.x, db.d, w.r, c->ctl, true);
+      launch_norm2_serial(st, n, w.r, nullptr, c->ctl, 2, n2_scratch(c, n));
+      ck(cudaMemcpyAsync(c->h_ctl, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st), "ctl");
+      ck(cudaStreamSynchronize(st), "sync");
+      rep->refinements = k + 1;
+      rep->total_inner_iterations += dim;
+      rep->inner_dims[k] = dim;
+      rep->gamma_history[k] = rmax;
+      rep->overflow_per_restart[k] = ov;
+      rep->overflow_total += ov;
+      relnorm = c->h_ctl->relnorm;
+      rep->relres_history[rep->n_relres++] = relnorm;
+    }
+    rep->converged = relnorm < tol;
+    if (x_out) ck(cudaMemcpyAsync(x_out, w.x, sizeof(double) * n, cudaMemcpyDefault, st), "x");
+    ck(cudaStreamSynchronize(st), "sync");
+    rep->wall_time_sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}

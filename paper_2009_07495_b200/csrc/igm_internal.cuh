@@ -118,6 +118,39 @@ struct DevTri {
   int* ticket = nullptr;  // 1
 };
 
+// config 3's WL = 32 variant (wl32.cu): the split's values as int32
+struct Dev32Split {
+  int n = 0, nnz = 0, ncomp = 0;
+  int* row_ptr = nullptr;
+  int* col_idx = nullptr;
+  int32_t* vals = nullptr;  // ncomp * nnz
+  int* alphas = nullptr;    // ncomp (device)
+  std::vector<int> h_alphas;
+  bool own_pattern = true;
+  int device = 0;
+};
+// per-cycle buffers of the WL = 32 cycle; `small` .. small + small_bytes is
+// zeroed before every cycle (accumulators, certificates, counters, H, g, cs, sn)
+struct Wl32Work {
+  long long n = 0;
+  int M = 0;
+  int32_t* basis = nullptr;  // (M+1) * n
+  int32_t* w = nullptr;      // n
+  void* small = nullptr;
+  size_t small_bytes = 0;
+  uint32_t* acc = nullptr;   // M * (M+1): per step j, the j+1 dot accumulators
+  u64* abs = nullptr;        // M * (M+1): their sum |term| certificates
+  uint32_t* nacc = nullptr;  // M norm accumulators
+  u64* nabs = nullptr;       // M
+  int32_t* hess = nullptr;   // (M+1) * M column-major
+  int32_t* g = nullptr;      // M+1
+  int32_t* cs = nullptr;     // M
+  int32_t* sn = nullptr;     // M
+  u64* cnt = nullptr;        // M * K_COUNT * OP_COUNT overflow counters
+  double* y = nullptr;       // M
+  double* wts = nullptr;     // M
+};
+
 struct DevIlu {
   int n = 0;
   DevTri lower, upper;
@@ -205,6 +238,10 @@ void launch_fxupdate(cudaStream_t st, long long n, int dim, const double* basis,
 int fdot_blocks();
 // persistent Arnoldi step (passes + scalar + vec_div in one cooperative launch)
 long long arnoldi_slice(long long n, int device);
+// one WL = 32 cycle (wl32.cu); xmode 0: x = correction, 1: x += gamma * correction
+void enqueue_cycle32(cudaStream_t st, const Wl32Work& b, const Dev32Split& m, int M, int f, int s, ShiftsD sh,
+                     const double* r0, Ctl* ctl, bool checked, int xmode, double* x);
+void launch_vals_to32(cudaStream_t st, long long cnt, const i64* in, int32_t* out, int* bad);
 int arnoldi_barriers(int j);
 void launch_arnoldi(cudaStream_t st, long long n, int j, long long S, const i64* w, i64* basis, u64* accj,
                     u64* absj, u64* nacc, u64* nabs, int f, ShiftsD sh, u64* cstep, i64* hess, int ld, i64* g,
