@@ -10,7 +10,12 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -fmad=false -Iinclu
 CXXFLAGS:= -O2 -std=c++20 -fPIC -ffp-contract=off -fno-fast-math -Wall -Iinclude
 HDRS    := $(wildcard $(PKG)/csrc/*.cuh) $(PKG)/csrc/schedule.hpp $(PKG)/csrc/pencil.hpp include/igm.h $(wildcard include/intgmres/*.hpp)
 
-all: $(LIB) oracle
+all: $(LIB) $(BUILD)/e2e_cpp oracle
+
+# the drop-in C++ API timed end to end (bench.py's e2e_cpp leg)
+$(BUILD)/e2e_cpp: scripts/e2e_cpp.cpp $(LIB) $(wildcard include/intgmres/*.hpp)
+	@mkdir -p $(BUILD)
+	g++ -std=c++20 -O2 -Iinclude scripts/e2e_cpp.cpp -L$(PKG) -ligm_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)' -o $@
 
 $(BUILD)/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	@mkdir -p $(BUILD)

@@ -406,6 +406,47 @@ def run_cfg5_sharded(args, igm, dev, local, rank, ws, g=400, k=30):
     }
 
 
+# ----------------------------------------------------------------- e2e_cpp
+def run_e2e_cpp(args, rp, ci, v, bh):
+    """The drop-in boundary timed as a reference user calls it: build/e2e_cpp
+    (scripts/e2e_cpp.cpp, written against include/intgmres/ and linked to
+    libigm_b200.so) runs intgmres::solve on config 2 with host std::vector
+    containers, b uploaded and x downloaded inside every timed call, the
+    operators reused through the verified operator cache.  Its x is hashed
+    against the reference golden."""
+    import hashlib
+    import subprocess
+    import tempfile
+    exe = os.path.join(ROOT, "build", "e2e_cpp")
+    if not os.path.exists(exe):
+        return {"error": "build/e2e_cpp not built"}
+    with tempfile.TemporaryDirectory() as d:
+        np.ascontiguousarray(rp, np.int32).tofile(os.path.join(d, "rp.bin"))
+        np.ascontiguousarray(ci, np.int32).tofile(os.path.join(d, "ci.bin"))
+        np.ascontiguousarray(v, np.float64).tofile(os.path.join(d, "v.bin"))
+        np.ascontiguousarray(bh, np.float64).tofile(os.path.join(d, "bh.bin"))
+        xo = os.path.join(d, "x.bin")
+        p = subprocess.run([exe, d, str(args.steps), str(max(1, args.warmup)), xo], capture_output=True, text=True,
+                           timeout=1200)
+        try:
+            rec = json.loads(p.stdout.strip().splitlines()[-1])
+        except (ValueError, IndexError):
+            return {"error": (p.stdout + p.stderr)[-400:]}
+        if os.path.exists(xo):
+            x = np.fromfile(xo, dtype=np.float64)
+            xh = hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest()
+            try:
+                with open(os.path.join(ROOT, "tests", "golden", "full_goldens.json")) as f:
+                    gx = json.load(f)["cfg2"]["solve"]["x"]
+                rec["parity"] = bool(xh == gx) if args.grid == 128 else None
+            except (OSError, KeyError, ValueError):
+                rec["parity"] = None
+    rec.update({"value": rec.get("iters_per_s"), "unit": "iters/s",
+                "call": "intgmres::solve(SplitMatrix, CsrMatrixF, std::vector<double> b, RefineConfig, &IluFactors) "
+                        "from C++ (refine.hpp:67-70), host containers in and out"})
+    return rec
+
+
 # ----------------------------------------------------------------- parity
 def parity_check(d_x, rep, grid):
     """The timed solve's x (every word) and report against the reference
@@ -550,6 +591,12 @@ def run_b200(args, ws, rank, local):
     e2e_ms = max_over_ranks(f0.elapsed_time(f1), ws)
     e2e_val = e2e_its * ws / (e2e_ms / 1e3)
 
+    # e2e through the reference's own C++ API (intgmres::solve, host containers)
+    e2e_cpp = None
+    if rank == 0 and not args.no_e2e_cpp:
+        e2e_cpp = run_e2e_cpp(args, rp, ci, v, bh)
+        log(f"[bench] e2e_cpp: {e2e_cpp}")
+
     # instrumented solve: per-kernel-class device time -> roofline
     igm.lib().igm_profile_enable(1)
     _, rp_ = igm.solve(S, A, d_b, cfg, precond=F, x_out=d_x)
@@ -611,6 +658,7 @@ def run_b200(args, ws, rank, local):
             "gpu_launches": int(launches),
             "e2e": {"value": e2e_val, "unit": "iters/s", "h2d_bytes_per_step": int(8 * n),
                     "d2h_bytes_per_step": int(8 * n)},
+            "e2e_cpp": e2e_cpp,
             "roofline": roof,
             "parity": parity,
             "kernel_microbench": micro,
@@ -631,6 +679,7 @@ def main():
     ap.add_argument("--grid", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cfg5", action="store_true", help="skip the config-5 kernel microbench")
+    ap.add_argument("--no-e2e-cpp", action="store_true", help="skip the C++ drop-in API leg")
     ap.add_argument("--only-cfg5", action="store_true", help="run only the config-5 microbench (profiling)")
     ap.add_argument("--cfg5-sharded", action="store_true",
                     help="at 1 GPU, also run the row-block partitioned config-5 driver")
