@@ -508,19 +508,21 @@ def roofline_line(breakdown, ab, n, levels, ms_step, refinements, hbm, src, micr
             e["frac"] = round(gbs / hbm, 4)
         classes[name] = e
     if "mgs" in classes and "mgs_actual" in ab:
+        classes["mgs"]["kernel"] = "k_arnoldi2 (register-resident w, TMA double-buffered basis slices)"
         gbs = ab["mgs_actual"] / (breakdown["mgs"]["ms"] / 1e3) / 1e9
         classes["mgs"]["actual_bytes_GB/s"] = round(gbs, 1)
         classes["mgs"]["frac_actual_bytes"] = round(gbs / hbm, 4)
         classes["mgs"]["note"] = ("frac uses the streaming formula (4k+3)Wn (SURVEY 8(d)); k_arnoldi keeps w on "
-                                  "chip and moves (k+2)Wn per step (ncu: 375 MB at j=20, profiles/traffic.json), "
+                                  "chip and moves (k+2)Wn per step (ncu: 374 MB at j=20 for k_arnoldi2, profiles/traffic.json), "
                                   "frac_actual_bytes divides those")
     cyc_ms = ms_step / max(1, refinements)
     cycle = {"bytes_per_cycle": 47.744e9, "ms_per_cycle": round(cyc_ms, 3),
              "floor_ms": round(47.744e9 / (hbm * 1e9) * 1e3, 3),
              "frac": round(47.744e9 / (cyc_ms / 1e3) / 1e9 / hbm, 4)}
-    return {"bound": "hbm", "kernel": "k_tri_pencil<int> (ILU(0) substitution, pencil wavefront)",
+    return {"bound": "hbm", "kernel": "k_tri_pencil2<checked,int,8> (ILU(0) substitution, warp-specialised pencil "
+                                      "wavefront, bricks in 8-CTA clusters)",
             "achieved": round(achieved, 1), "peak": hbm, "peak_source": src, "unit": "GB/s",
-            "frac": round(achieved / hbm, 4), "traffic": measured_traffic("k_tri_pencil_cfg2"),
+            "frac": round(achieved / hbm, 4), "traffic": measured_traffic("k_tri_pencil2_cfg2"),
             "bytes_per_launch": int(bytes_launch), "us_per_launch": round(per_launch_ms * 1e3, 2),
             "launches_per_step": ilu["launches"], "share_of_step": round(step_share, 4),
             "levels": levels, "us_per_level": round(per_launch_ms * 1e3 / levels, 4),
