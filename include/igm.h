@@ -362,6 +362,30 @@ igm_status igm_dc_tri_fp(igm_ctx* ctx, igm_dstate* d, const igm_ilu* f, int back
                          double* out);
 igm_status igm_dc_tri(igm_ctx* ctx, igm_dstate* d, const igm_ilu* f, int backward, const int64_t* in,
                       int64_t* out, int j, int checked);
+/* ---- pipelined z-slab substitutions (the row-partitioned solve)
+ * The global ILU(0) on z-slabs: instead of handing a whole boundary plane to
+ * the next rank after the substitution finished, every rank's pencil
+ * wavefront streams its last own plane, pencil by pencil, as tagged 16-byte
+ * words (value, epoch + idx; idx = natural j * gx + i) into the neighbour's
+ * import buffer -- a device buffer of the neighbour mapped with CUDA IPC (P2P
+ * over NVLink) -- and imports its own halo plane the same way, so rank p's
+ * wavefront starts as soon as rank p-1's first pencils finish (the critical
+ * path stays the global DAG's, ilu.cpp:122-155).  zimp: this rank's import
+ * buffer (NULL: the halo rows' right-hand sides are in `in`); zexp: the
+ * neighbour's buffer (NULL: nothing exported); kexp: the solve-order plane
+ * exported; epoch: the same value on both ranks for one substitution.
+ * IGM_INVALID_ARGUMENT when the rank-local factor is not a 7-point pencil
+ * factor (the caller then relays whole planes). */
+igm_status igm_dc_tri_piped(igm_ctx* ctx, igm_dstate* d, const igm_ilu* f, int backward, const int64_t* in,
+                            int64_t* out, int j, int checked, const void* zimp, void* zexp, int kexp,
+                            uint64_t epoch);
+/* device buffers shared across processes (CUDA IPC) */
+igm_status igm_dev_alloc(igm_ctx* ctx, uint64_t bytes, void** out);
+void igm_dev_free(void* p);
+igm_status igm_ipc_handle(const void* dptr, unsigned char handle[64]);
+igm_status igm_ipc_open(igm_ctx* ctx, const unsigned char handle[64], void** dptr);
+void igm_ipc_close(void* dptr);
+
 /* v0 = encode(r0 / ||r0||) (gmres_int.cpp:71-81) */
 igm_status igm_dc_encode(igm_ctx* ctx, igm_dstate* d, int64_t n, const double* r0, int64_t* v0,
                          int frac_bits);

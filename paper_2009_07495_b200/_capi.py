@@ -167,6 +167,13 @@ SIGNATURES = [
     ("igm_dc_tri_fp", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
     ("igm_dc_tri", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
                              C.c_int]),
+    ("igm_dc_tri_piped", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                                   C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_uint64]),
+    ("igm_dev_alloc", C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p)]),
+    ("igm_dev_free", None, [C.c_void_p]),
+    ("igm_ipc_handle", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("igm_ipc_open", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
+    ("igm_ipc_close", None, [C.c_void_p]),
     ("igm_dc_encode", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int]),
     ("igm_dc_spmv", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
                               C.c_int]),

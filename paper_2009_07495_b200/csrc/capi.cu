@@ -1927,6 +1927,63 @@ igm_status igm_dc_tri(igm_ctx* c, igm_dstate* d, const igm_ilu* f, int backward,
   });
 }
 
+igm_status igm_dc_tri_piped(igm_ctx* c, igm_dstate* d, const igm_ilu* f, int backward, const int64_t* in,
+                            int64_t* out, int j, int checked, const void* zimp, void* zexp, int kexp,
+                            uint64_t epoch) {
+  return guarded([&] {
+    need_ds(c, d);
+    if (!f) fail(IGM_INVALID_ARGUMENT, "dc_tri_piped: null factors");
+    if (j < 0 || j >= d->m) fail(IGM_INVALID_ARGUMENT, "dc_tri_piped: step out of range");
+    need_dev(in, "dc_tri_piped"); need_dev(out, "dc_tri_piped");
+    PenZ z;
+    z.imp = static_cast<const ulonglong2*>(zimp);
+    z.exp = static_cast<ulonglong2*>(zexp);
+    z.kexp = kexp;
+    z.epoch = epoch;
+    const DevTri& t = backward ? f->upper : f->lower;
+    if (!launch_tri_int_piped(c->stream, t, backward != 0, in, out, d->lcnt + j * kCntStride + K_PRECOND * OP_COUNT,
+                              d->ctl, checked != 0, z))
+      fail(IGM_INVALID_ARGUMENT, "dc_tri_piped: the factor is not a 7-point pencil factor");
+  });
+}
+
+igm_status igm_dev_alloc(igm_ctx* c, uint64_t bytes, void** out) {
+  return guarded([&] {
+    need_ctx(c);
+    if (!out) fail(IGM_INVALID_ARGUMENT, "dev_alloc: null output");
+    void* p = nullptr;
+    ck(cudaMalloc(&p, bytes ? bytes : 16), "dev_alloc");
+    ck(cudaMemset(p, 0, bytes ? bytes : 16), "dev_alloc");
+    *out = p;
+  });
+}
+
+void igm_dev_free(void* p) {
+  if (p) cudaFree(p);
+}
+
+igm_status igm_ipc_handle(const void* dptr, unsigned char handle[64]) {
+  return guarded([&] {
+    cudaIpcMemHandle_t h;
+    ck(cudaIpcGetMemHandle(&h, const_cast<void*>(dptr)), "ipc handle");
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(handle, &h, 64);
+  });
+}
+
+igm_status igm_ipc_open(igm_ctx* c, const unsigned char handle[64], void** dptr) {
+  return guarded([&] {
+    need_ctx(c);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    ck(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess), "ipc open");
+  });
+}
+
+void igm_ipc_close(void* dptr) {
+  if (dptr) cudaIpcCloseMemHandle(dptr);
+}
+
 igm_status igm_dc_mgs_pass(igm_ctx* c, igm_dstate* d, int64_t n, int j, int i, int64_t* w, const int64_t* vprev,
                            const int64_t* vcur, int f, const igm_shifts* sh, int checked) {
   return guarded([&] {

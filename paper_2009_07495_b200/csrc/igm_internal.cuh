@@ -180,6 +180,14 @@ void launch_spmv_fp_split(cudaStream_t st, const DevSplit& m, int s,
 void launch_residual(cudaStream_t st, const DevCsrf& a, const double* x,
                      const double* b, double* r, Ctl* ctl, bool track_max);
 int pencil27_max_resident(int device);  // CTAs of k_tri27 that fit on the GPU at once
+struct PenZ {  // z-slab pipelining of the pencil wavefront (PenArgs::zimp ...)
+  const ulonglong2* imp = nullptr;
+  ulonglong2* exp = nullptr;
+  int kexp = -1;
+  unsigned long long epoch = 0;
+};
+bool launch_tri_int_piped(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out, u64* cnt,
+                          const Ctl* ctl, bool checked, const PenZ& z);
 void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward,
                     const i64* y, i64* out, u64* cnt, const Ctl* ctl,
                     bool checked);

@@ -3140,7 +3140,7 @@ static void pen2_launch(cudaStream_t st, const DevTri& t, const PenArgs& a, cons
 // factor: integer (FP = false) or FP64 (apply_inverse_fp) substitution
 template <bool FP>
 static void pen_launch(cudaStream_t st, const DevTri& t, bool backward, const void* y, void* out, const Ctl* ctl,
-                       bool checked, const double* prescale) {
+                       bool checked, const double* prescale, const PenZ* zp = nullptr) {
   constexpr int D = 4, R = 16;
   const size_t sm = pencil_smem_bytes(R, D);
   static PerDevice attr;  // the attribute is per device
@@ -3165,15 +3165,21 @@ static void pen_launch(cudaStream_t st, const DevTri& t, bool backward, const vo
   a.epoch = pen_epoch();
   a.ticket = t.ticket;
   a.stats = reinterpret_cast<unsigned long long*>(t.stats);
+  if (zp) {
+    a.zimp = zp->imp;
+    a.zexp = zp->exp;
+    a.kexp = zp->kexp;
+    a.zepoch = zp->epoch;
+  }
   const int* stop = ctl ? &ctl->stop : nullptr;
-  const int* err = ctl ? &ctl->err : nullptr;
+  const int* err = ctl && !zp ? &ctl->err : nullptr;  // pipelined: see k_tri_pencil2
   const i64* yi = static_cast<const i64*>(y);
   i64* oi = static_cast<i64*>(out);
   static const bool v2 = [] {  // IGM_PENCIL2=0 selects the single-warp-role kernel (A/B timing)
     const char* e = std::getenv("IGM_PENCIL2");
     return e == nullptr || std::atoi(e) != 0;
   }();
-  if (v2) {
+  if (v2 || zp) {
     if (checked && !FP) pen2_launch<true, FP>(st, t, a, yi, oi, stop, err, prescale);
     else pen2_launch<false, FP>(st, t, a, yi, oi, stop, err, prescale);
     return;
@@ -3232,6 +3238,27 @@ static bool pen27_launch(cudaStream_t st, const DevTri& t, bool backward, const 
     return false;
   }
   return true;  // any other error is reported by LAUNCH_CHECK
+}
+
+// the rank-local substitution of a z-slab with its boundary plane streamed from
+// / to the neighbour ranks (pencil wavefront only); false when the factor is
+// not a 7-point pencil factor
+bool launch_tri_int_piped(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out, u64* cnt,
+                          const Ctl* ctl, bool checked, const PenZ& z) {
+  if (t.n == 0 || !t.pen) return false;
+  if (checked) cudaMemsetAsync(t.stats, 0, 2 * sizeof(u64), st);
+  {
+    ProfScope prof_(st, KC_TRI_INT);
+    pen_launch<false>(st, t, backward, y, out, ctl, checked, nullptr, &z);
+  }
+  LAUNCH_CHECK();
+  if (checked) {
+    ProfScope prof_(st, KC_OTHER);
+    k_tri_count<<<grid_for(t.n, 256), 256, 0, st>>>(t.n, t.c_rp, t.c_ci, t.c_val, t.c_diag, y, out, cnt, ctl,
+                                                      t.stats, static_cast<double>(t.maxabs_l), t.maxd);
+    LAUNCH_CHECK();
+  }
+  return true;
 }
 
 void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out,

@@ -48,6 +48,14 @@ struct PenArgs {
   unsigned long long epoch;         // per launch, hashed, non-zero
   int* ticket;
   unsigned long long* stats;        // [max|y|, max|z|] of this apply (checked mode's bound)
+  // z-slab pipelining (k_tri_pencil2 only; dist.py's row-partitioned solve):
+  // the right-hand sides of solve-order plane 0 come from tagged words
+  // zimp[idx] = (value, zepoch + idx) written by the neighbour rank (idx =
+  // natural j * gx + i), and plane kexp's results go to zexp[idx] likewise
+  const ulonglong2* zimp = nullptr;
+  ulonglong2* zexp = nullptr;
+  int kexp = -1;
+  unsigned long long zepoch = 0;
 };
 
 __device__ __forceinline__ void pen_xz_load(const ulonglong2* p, u64& v, u64& tg) {

@@ -139,8 +139,11 @@ __global__ void __launch_bounds__(kP2Threads, 1)
                   const double* prescale) {
   extern __shared__ __align__(128) unsigned char p2_smem[];
   // the cycle already ended (Ctl::stop / Ctl::err): uniform over the grid, so
-  // every CTA of a cluster returns before any cluster barrier
-  if (stop != nullptr && (*stop | *err) != 0) return;
+  // every CTA of a cluster returns before any cluster barrier.  Pipelined
+  // slabs pass err = nullptr: an error can be rank-local (encode), and the
+  // neighbours' wavefronts wait on this one's words -- only the replicated
+  // stop ends all of them together
+  if (stop != nullptr && (*stop | (err != nullptr ? *err : 0)) != 0) return;
   constexpr int W = kPenWarps, G = kP2G, NS = kP2NS, R = kP2R;
   constexpr unsigned RM = R - 1;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -217,11 +220,29 @@ __global__ void __launch_bounds__(kP2Threads, 1)
         for (int q = 0; q < G; ++q) {
           const int s = g * G + q;
           const bool act = static_cast<unsigned>(s - sa[v]) < static_cast<unsigned>(gz);
+          if (a.zimp != nullptr && act && s == sa[v]) {  // plane 0: the neighbour rank's value (pipelined slabs)
+            const int j = by * kPenY + 2 * v + jj;
+            const long long idx = a.mirror ? static_cast<long long>(a.gy - 1 - j) * a.gx + (a.gx - 1 - i)
+                                           : static_cast<long long>(j) * a.gx + i;
+            u64 zv, zt;
+            unsigned spins = 0;
+            (void)spins;
+            do {
+              asm volatile("{ .reg .b128 t; ld.relaxed.sys.global.b128 t, [%2]; mov.b128 {%0, %1}, t; }"
+                           : "=l"(zv), "=l"(zt)
+                           : "l"(a.zimp + idx)
+                           : "memory");
+              P2_GUARD(7, s, v)
+            } while (zt != a.zepoch + static_cast<u64>(idx));
+            asm volatile("st.shared.u64 [%0], %1;" ::"r"(drhs + q * 256u), "l"(zv) : "memory");
+            continue;
+          }
           const i64* p = act ? yp[v] + static_cast<long long>(s) * ystride : y;
           asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(drhs + q * 256u), "l"(p),
                        "r"(act ? 8 : 0)
                        : "memory");
         }
+        if (a.zimp != nullptr) asm volatile("fence.acq_rel.cta;" ::: "memory");  // imported words stored above
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(fb) : "memory");
       }
     }
@@ -417,6 +438,14 @@ __global__ void __launch_bounds__(kP2Threads, 1)
           else p2_sts_word(ring_prod + rs * 256u, static_cast<u64>(z), k);
         }
         if (act) *op = z;
+        if (a.zexp != nullptr && act && k == a.kexp) {  // the next rank's plane-0 value (pipelined slabs)
+          const long long idx = a.mirror ? static_cast<long long>(a.gy - 1 - j) * a.gx + (a.gx - 1 - i)
+                                         : static_cast<long long>(j) * a.gx + i;
+          const u64 tz = a.zepoch + static_cast<u64>(idx);
+          asm volatile("{ .reg .b128 t; mov.b128 t, {%1, %2}; st.relaxed.sys.global.b128 [%0], t; }" ::"l"(a.zexp + idx),
+                       "l"(static_cast<u64>(z)), "l"(tz)
+                       : "memory");
+        }
         asm volatile(
             "{ .reg .pred p; .reg .b128 t; setp.ne.b32 p, %3, 0; mov.b128 t, {%1, %2};\n"
             "@p st.global.relaxed.gpu.b128 [%0], t; }" ::"l"(ep),

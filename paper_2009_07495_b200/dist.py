@@ -217,6 +217,54 @@ class CudaSlabBackend:
             self._c("igm_dc_tri", st.h, fac.h, 1 if backward else 0, self._p(src), self._p(dst), j,
                     1 if checked else 0)
 
+    # ---- pipelined substitutions: boundary planes streamed over CUDA IPC
+    def pipe_auto(self, dist, group=None) -> bool:
+        """P2P words between ranks need one process per GPU (NCCL ranks);
+        IGM_DIST_PIPE=0 selects the plane relay"""
+        import os
+        if os.environ.get("IGM_DIST_PIPE", "1") == "0" or not hasattr(dist, "get_backend"):
+            return False
+        try:
+            return dist.get_backend(group) == "nccl"
+        except Exception:
+            return False
+
+    def pipe_capable(self, fac, slab) -> bool:
+        """both local factors run the 7-point pencil wavefront on the slab's grid"""
+        if fac is None:
+            return False
+        for bw in (False, True):
+            info = fac.schedule_info(bw)
+            gx, gy, gz = info["grid"]
+            if fac.pencil_bricks(bw) <= 0 or gx * gy != slab.plane or gx * gy * gz != slab.next_:
+                return False
+        return True
+
+    def pipe_alloc(self, nwords):
+        import ctypes as C
+        p = C.c_void_p()
+        self._c("igm_dev_alloc", C.c_uint64(16 * nwords), C.byref(p))
+        return p.value
+
+    def pipe_handle(self, buf):
+        import ctypes as C
+        h = (C.c_ubyte * 64)()
+        self.igm._check(self.igm.lib().igm_ipc_handle(C.c_void_p(buf), h))
+        return np.frombuffer(bytes(h), dtype=np.int64).copy()
+
+    def pipe_open(self, handle):
+        import ctypes as C
+        h = (C.c_ubyte * 64).from_buffer_copy(np.asarray(handle, dtype=np.int64).tobytes())
+        p = C.c_void_p()
+        self._c("igm_ipc_open", h, C.byref(p))
+        return p.value
+
+    def tri_piped(self, st, fac, backward, src, dst, j, checked, zimp, zexp, kexp, epoch):
+        import ctypes as C
+        self._c("igm_dc_tri_piped", st.h, fac.h, 1 if backward else 0, self._p(src), self._p(dst), j,
+                1 if checked else 0, None if zimp is None else C.c_void_p(zimp),
+                None if zexp is None else C.c_void_p(zexp), kexp, C.c_uint64(epoch))
+
     def encode(self, st, r0, v0, f):
         self._c("igm_dc_encode", st.h, int(r0.numel()), self._p(r0), self._p(v0), f)
 
@@ -466,7 +514,71 @@ def _validate_cycle(m: int, f: int, depth: int, ncomp: int, sh) -> None:
         raise ValueError("ShiftPlan: division shifts out of range")
 
 
-def solve_sharded(be, slab: Slab, mats: dict, b_own, cfg, dist, group=None, s_schedule=None):
+class ZPipe:
+    """The rank's side of the pipelined substitutions: the
+    global ILU(0) wavefront crosses a slab boundary pencil by pencil instead
+    of plane by plane.  Rank p owns two import buffers of one plane of
+    16-byte words (value, epoch + natural idx): `fwd` written by rank p-1's
+    forward wavefront as it finishes its last own plane, `bwd` by rank p+1's
+    backward wavefront (its first own plane); the neighbours map them with
+    CUDA IPC and store into them over NVLink.  In the rank-local solve order
+    the import is plane 0 (the lower halo forward, the upper halo backward),
+    the export is plane `kexp_*`.  Epochs are (call count) << 32, identical on
+    every rank, so a word of an earlier substitution never matches.  Reuse of
+    a buffer is ordered by the DAG itself: rank p writes epoch e+1 into
+    p+1's `fwd` only after its own backward of call e, which needed p+1's
+    backward of call e, which ran after p+1's forward of call e read epoch e."""
+
+    def __init__(self, be, slab: Slab, comm):
+        P = slab.plane
+        rank, world = slab.rank, slab.world
+        self.imp_fwd = be.pipe_alloc(P) if rank > 0 else None
+        self.imp_bwd = be.pipe_alloc(P) if rank < world - 1 else None
+        mine = np.zeros((world, 2, 8), dtype=np.int64)
+        if self.imp_fwd is not None:
+            mine[rank, 0] = be.pipe_handle(self.imp_fwd)
+        if self.imp_bwd is not None:
+            mine[rank, 1] = be.pipe_handle(self.imp_bwd)
+        allh = be.host_i64(mine.ravel().tolist())
+        comm.sum_(allh)
+        allh = allh.cpu().numpy().reshape(world, 2, 8)
+        self.exp_fwd = be.pipe_open(allh[rank + 1, 0]) if rank < world - 1 else None
+        self.exp_bwd = be.pipe_open(allh[rank - 1, 1]) if rank > 0 else None
+        self.kexp_fwd, self.kexp_bwd = self.planes(slab)
+        self.calls = 0
+
+    @staticmethod
+    def planes(slab: Slab) -> Tuple[int, int]:
+        """solve-order index of the exported plane, forward and backward (-1: none)"""
+        P, nz = slab.plane, slab.next_ // slab.plane
+        return (slab.own1 // P - 1 if slab.rank < slab.world - 1 else -1,
+                nz - 1 - slab.own0 // P if slab.rank > 0 else -1)
+
+    def next_epoch(self) -> int:
+        self.calls += 1
+        return self.calls << 32
+
+
+def _pipe_for(be, slab: Slab, pre, comm, dist, group, pipe):
+    """The rank's ZPipe (cached on the backend) when every rank can stream
+    its boundary planes, else None (the plane relay)."""
+    if slab.world == 1 or pre is None or pipe is False or not hasattr(be, "tri_piped"):
+        return None
+    if pipe is None and not be.pipe_auto(dist, group):
+        return None
+    bad = be.host_i64([0 if be.pipe_capable(pre, slab) else 1])
+    comm.max_(bad)
+    if int(bad[0]):
+        return None
+    cache = be.__dict__.setdefault("_zpipes", {})
+    key = (slab.rank, slab.world, slab.z0, slab.z1, slab.plane, slab.nplanes)
+    if key not in cache:
+        cache[key] = ZPipe(be, slab, comm)
+    return cache[key]
+
+
+def solve_sharded(be, slab: Slab, mats: dict, b_own, cfg, dist, group=None, s_schedule=None,
+                  pipe=None):
     """solve() (refine.cpp:21-106, fixed-point engine) on this rank's rows.
 
     be:   rank-local backend (CudaSlabBackend: the product's kernels through
@@ -475,6 +587,8 @@ def solve_sharded(be, slab: Slab, mats: dict, b_own, cfg, dist, group=None, s_sc
           A_fp, 'ilu': extended-square local factors or None, 'ncomp': int}
     b_own: the rank's rows of b; cfg: RefineConfig-like (tol,
           max_refinements, m, frac_bits, s, checked, shifts).
+    pipe: stream the integer substitutions' boundary planes pencil by pencil
+          (ZPipe) -- None: when the backend and every rank can, False: relay.
     Returns (x_own, ShardedReport); every rank returns the same report."""
     comm = _Comm(slab, dist, group)
     be.sync()  # inputs produced on other streams are complete
@@ -512,9 +626,19 @@ def solve_sharded(be, slab: Slab, mats: dict, b_own, cfg, dist, group=None, s_sc
             comm.bcast(chain[2:3], world - 1)
             be.norm2(st, v[:0], chain[2:3], None, mode)
 
+    zp = _pipe_for(be, slab, pre, comm, dist, group, pipe)
+
     def tri_pipeline(fac_fp, src_ext, mid_ext, dst_ext, j=0):
         """forward (ranks in order) then backward (reverse order) substitution
-        of the global factors; src_ext's own rows hold the rhs."""
+        of the global factors; src_ext's own rows hold the rhs.  Integer
+        substitutions stream the boundary planes word by word when the ranks
+        can (ZPipe); otherwise, and for the FP64 one, whole planes are relayed."""
+        if zp is not None and not fac_fp:
+            e = zp.next_epoch()
+            with be.stream():
+                be.tri_piped(st, pre, False, src_ext, mid_ext, j, checked, zp.imp_fwd, zp.exp_fwd, zp.kexp_fwd, e)
+                be.tri_piped(st, pre, True, mid_ext, dst_ext, j, checked, zp.imp_bwd, zp.exp_bwd, zp.kexp_bwd, e)
+            return
         with be.stream():
             if rank > 0:
                 comm.recv(src_ext[:o0], rank - 1)

@@ -182,6 +182,87 @@ class OracleSlabBackend:
             if t is not None:
                 st.lcnt[j][1 * 6 + 3] += t.total
 
+    # ---- pipelined substitutions (dist.ZPipe), emulated: the "device
+    # buffers" are shared-memory segments of one plane of (value, tag) words,
+    # the "IPC handle" is the segment name; the import waits for every tag
+    # of the plane, the export writes values then tags -- the CUDA kernel's
+    # word protocol with the plane as the unit
+    pipe_emulate = False
+
+    def pipe_auto(self, dist, group=None):
+        return self.pipe_emulate
+
+    def pipe_capable(self, fac, slab):
+        if fac is None:
+            return False
+        fac.slab = slab
+        return True
+
+    def _pipe_view(self, key):
+        shm = self._shm[key]
+        return np.ndarray((shm.size // 16, 2), dtype=np.int64, buffer=shm.buf)
+
+    def pipe_alloc(self, nwords):
+        from multiprocessing import shared_memory
+        shm = shared_memory.SharedMemory(create=True, size=16 * nwords)
+        self.__dict__.setdefault("_shm", {})
+        self.__dict__.setdefault("_own_shm", []).append(shm)
+        key = len(self._shm) + 1
+        self._shm[key] = shm
+        self._pipe_view(key)[:] = 0
+        return key
+
+    def pipe_handle(self, key):
+        name = self._shm[key].name.encode()
+        assert len(name) <= 64
+        return np.frombuffer(name.ljust(64, b"\0"), dtype=np.int64).copy()
+
+    def pipe_open(self, handle):
+        from multiprocessing import shared_memory
+        name = np.asarray(handle, dtype=np.int64).tobytes().rstrip(b"\0").decode()
+        shm = shared_memory.SharedMemory(name=name)
+        self.__dict__.setdefault("_shm", {})
+        key = len(self._shm) + 1
+        self._shm[key] = shm
+        return key
+
+    def pipe_close(self):
+        for shm in self.__dict__.get("_shm", {}).values():
+            shm.close()
+        for shm in self.__dict__.get("_own_shm", []):
+            shm.unlink()
+        self._shm, self._own_shm = {}, []
+
+    def tri_piped(self, st, fac, backward, src, dst, j, checked, zimp, zexp, kexp, epoch):
+        import time
+        if st.stop and st.err is None:  # the replicated stop (errors can be rank-local: run on)
+            return
+        P, nx = fac.slab.plane, fac.slab.next_
+        y = src.numpy().copy()
+        tags = epoch + np.arange(P, dtype=np.int64)
+        if zimp is not None:
+            buf = self._pipe_view(zimp)
+            t0 = time.time()
+            while not np.array_equal(buf[:, 1], tags):
+                if time.time() - t0 > 120:
+                    raise RuntimeError("tri_piped: import timed out")
+                time.sleep(0.0005)
+            if backward:
+                y[nx - P:] = buf[:, 0]
+            else:
+                y[:P] = buf[:, 0]
+        il = fac.bwd if backward else fac.fwd
+        from oracle.ffi import PyTrace
+        t = PyTrace() if checked else None
+        dst.numpy()[:] = self.O.apply_inverse(il, y, t)
+        if t is not None:
+            st.lcnt[j][1 * 6 + 3] += t.total
+        if zexp is not None:
+            z = (nx // P - 1 - kexp) if backward else kexp
+            buf = self._pipe_view(zexp)
+            buf[:, 0] = dst.numpy()[z * P:(z + 1) * P]
+            buf[:, 1] = tags
+
     def encode(self, st, r0, v0, f):
         if self._over(st):
             return

@@ -124,15 +124,16 @@ def _problem(kind, g, oracle):
         rp, ci, v = gen.upwind_3d(g, 20.0)
     n = len(rp) - 1
     A = oracle.csrf(rp, ci, v)
-    alpha = 32 if kind == "27pt_ilu" else 16
+    ilu = kind.endswith("_ilu")
+    alpha = 32 if ilu else 16
     vals, scale = oracle.row_scale(A, alpha)
-    comp, al, _ = oracle.build_split(vals, alpha, 1 if kind == "27pt_ilu" else 2)
-    fac = oracle.factorize_split_cast(oracle.csrf(rp, ci, vals)) if kind == "27pt_ilu" else None
+    comp, al, _ = oracle.build_split(vals, alpha, 1 if ilu else 2)
+    fac = oracle.factorize_split_cast(oracle.csrf(rp, ci, vals)) if ilu else None
     b = gen.spmv_np(rp, ci, v, gen.uniform(17, n)) / scale
     return rp, ci, vals, comp, al, fac, b
 
 
-def _solve_worker(rank, world, port, kind, g, m, s, q):
+def _solve_worker(rank, world, port, kind, g, m, s, q, pipe=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -143,31 +144,39 @@ def _solve_worker(rank, world, port, kind, g, m, s, q):
         rp, ci, vals, comp, al, fac, b = _problem(kind, g, O)
         sl = D.make_slab(g, g * g, rank, world)
         be = OracleSlabBackend(O)
+        be.pipe_emulate = pipe
         mats = D.shard_problem(be, sl, rp, ci, comp, al, vals, fac)
         g0, g1 = sl.global_rows
         plan = igm.ShiftPlan.default_preconditioned(30) if fac is not None else igm.ShiftPlan.default_unpreconditioned(30)
         cfg = igm.RefineConfig(tol=1e-10, max_refinements=30, m=m, frac_bits=30, s=s, checked=True, shifts=plan)
         x, rep = D.solve_sharded(be, sl, mats, torch.from_numpy(b[g0:g1].copy()), cfg, dist)
+        piped = sum(zp.calls for zp in be.__dict__.get("_zpipes", {}).values())
         parts = [None] * world
-        dist.all_gather_object(parts, (g0, x.numpy().copy(), rep))
+        dist.all_gather_object(parts, (g0, x.numpy().copy(), rep, piped))
+        if pipe:
+            be.pipe_close()
         if rank == 0:
             q.put(sorted(parts, key=lambda t: t[0]))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind,world", [("27pt_ilu", 2), ("27pt_ilu", 3), ("7pt_plain", 2)])
-def test_sharded_solve_matches_oracle(oracle, kind, world):
+@pytest.mark.parametrize("kind,world,pipe", [("27pt_ilu", 2, False), ("27pt_ilu", 3, False), ("7pt_plain", 2, False),
+                                             ("7pt_ilu", 2, True), ("7pt_ilu", 3, True), ("27pt_ilu", 3, True)])
+def test_sharded_solve_matches_oracle(oracle, kind, world, pipe):
     """World 2/3 gloo run of dist.solve_sharded (halo planes, exact u64 pass
     sums, relayed norm2 chain, rank-pipelined global ILU) against the
     single-process oracle solve: every x word, the relative-residual history,
-    the inner dimensions and the gammas bit-identical."""
+    the inner dimensions and the gammas bit-identical.  pipe: the integer
+    substitutions hand the boundary plane over dist.ZPipe's word protocol
+    (tagged one-plane buffers opened by handle, epochs per call; emulated
+    with shared-memory segments) instead of the NCCL/gloo plane relay."""
     g, m = 6, 8
-    s = 0 if kind == "27pt_ilu" else 1
+    s = 0 if kind.endswith("_ilu") else 1
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_solve_worker, args=(r, world, port, kind, g, m, s, q)) for r in range(world)]
+    procs = [ctx.Process(target=_solve_worker, args=(r, world, port, kind, g, m, s, q, pipe)) for r in range(world)]
     for p in procs:
         p.start()
     parts = q.get(timeout=600)
@@ -177,6 +186,10 @@ def test_sharded_solve_matches_oracle(oracle, kind, world):
     x = np.concatenate([p[1] for p in parts])
     rep = parts[0][2]
     assert all(p[2] == rep for p in parts)  # replicated report
+    if pipe:  # every integer substitution pair went through the word protocol
+        assert all(p[3] == parts[0][3] for p in parts) and parts[0][3] == rep.refinements * m  # one per Arnoldi step (the FP64 one is relayed)
+    else:
+        assert all(p[3] == 0 for p in parts)
     from oracle.ffi import Shifts
     from tests.cases import PRE, UNPRE
     rp, ci, vals, comp, al, fac, b = _problem(kind, g, oracle)

@@ -614,7 +614,8 @@ def test_cpp_experiment(gpu, reference, tmp_path):
             assert ours[-1].endswith("converged=yes") and refl[-1].endswith("converged=yes")
 
 
-@pytest.mark.parametrize("kind,g,world", [("27pt_ilu", 12, 1), ("27pt_ilu", 12, 3), ("7pt_plain", 10, 2)])
+@pytest.mark.parametrize("kind,g,world", [("27pt_ilu", 12, 1), ("27pt_ilu", 12, 3), ("7pt_plain", 10, 2),
+                                          ("7pt_ilu", 16, 2)])
 def test_sharded_solve_cuda_backend(gpu, oracle, kind, g, world):
     """dist.solve_sharded through the product kernels (igm_dc_* entries: rank
     local SpMV / MGS passes / replicated scalar step / vec_div / pipelined
@@ -631,7 +632,7 @@ def test_sharded_solve_cuda_backend(gpu, oracle, kind, g, world):
         devs[rank] = gpu.Device(0)
         return D.CudaSlabBackend(gpu, devs[rank])
 
-    m, s = 10, (0 if kind == "27pt_ilu" else 1)
+    m, s = 10, (0 if kind.endswith("_ilu") else 1)
     x, reps, prob = run_sharded_threads(oracle, make_backend, kind, g, m, s, world, to_dev=lambda t: t.cuda())
     check_sharded_vs_oracle(oracle, x, reps, prob, m, s)
 
@@ -865,3 +866,76 @@ def test_ilu_pencil27_wavefront(gpu, oracle, dims):
     assert G.pencil_bricks(False) == 0
     y = gen.uniform_int(33, n, -(1 << 50), 1 << 50)
     assert np.array_equal(gpu.apply_inverse(G, y), gpu.apply_inverse(F, y))
+
+
+@pytest.mark.parametrize("g,world", [(16, 2), (24, 3), (40, 4)])
+def test_piped_substitution_protocol(gpu, oracle, g, world):
+    """igm_dc_tri_piped, the word protocol of the pipelined slab
+    substitutions (dist.ZPipe): rank r's forward wavefront stores its last
+    own plane as tagged words into rank r+1's import buffer and rank r+1's
+    wavefront reads its halo plane from there; backward the same from r+1 to
+    r.  Here the ranks share this GPU, so they run strictly one after the
+    other (each launch completes before the next rank's starts: no kernel ever
+    waits on another); the buffers are plain device pointers instead of IPC
+    mappings.  Concatenated own rows == the global substitution pair of the
+    oracle (ilu.cpp:122-180), bit for bit, over two calls (epochs 1, 2) with
+    different right-hand sides -- a stale word of call 1 must not satisfy
+    call 2."""
+    import ctypes as C
+    import torch
+    from paper_2009_07495_b200 import dist as D
+    from workloads import gen
+    rp, ci, v = gen.upwind_3d(g, 20.0)
+    n = len(rp) - 1
+    vals, _ = oracle.row_scale(oracle.csrf(rp, ci, v), 32)
+    lower, upper = oracle.factorize_split_cast(oracle.csrf(rp, ci, vals))
+    eye = (np.arange(n + 1, dtype=np.int32), np.arange(n, dtype=np.int32), np.ones(n, np.int64),
+           np.arange(n, dtype=np.int32))
+    fwd, bwd = oracle.ilu(lower, eye), oracle.ilu(eye, upper)
+    ranks = []
+    for r in range(world):
+        sl = D.make_slab(g, g * g, r, world)
+        be = D.CudaSlabBackend(gpu, gpu.Device(0))
+        fac = be.upload_factors(D.slab_factor(lower, sl), D.slab_factor(upper, sl))
+        assert be.pipe_capable(fac, sl), fac.schedule_info()
+        st = be.state(1)
+        with be.stream():
+            be.reset(st)
+        ranks.append(dict(sl=sl, be=be, fac=fac, st=st, kf=D.ZPipe.planes(sl),
+                          imp_f=be.pipe_alloc(sl.plane) if r > 0 else None,
+                          imp_b=be.pipe_alloc(sl.plane) if r < world - 1 else None))
+    rng = np.random.default_rng(7)
+    try:
+        for epoch in (1, 2):
+            y = rng.integers(-(1 << 40), 1 << 40, n, dtype=np.int64)
+            want = oracle.apply_inverse(bwd, oracle.apply_inverse(fwd, y))
+            for R in ranks:
+                sl = R["sl"]
+                g0, g1 = sl.global_rows
+                R["y"] = torch.zeros(sl.next_, dtype=torch.int64, device="cuda")
+                R["y"][sl.own0:sl.own1] = torch.from_numpy(y[g0:g1]).cuda()
+                R["mid"] = torch.full((sl.next_,), 7, dtype=torch.int64, device="cuda")
+                R["out"] = torch.full((sl.next_,), 7, dtype=torch.int64, device="cuda")
+            torch.cuda.synchronize()
+            for r in range(world):  # forward: rank order
+                R = ranks[r]
+                nxt = ranks[r + 1]["imp_f"] if r < world - 1 else None
+                R["be"].tri_piped(R["st"], R["fac"], False, R["y"], R["mid"], 0, True, R["imp_f"], nxt,
+                                  R["kf"][0], epoch << 32)
+                R["be"].sync()
+            for r in reversed(range(world)):  # backward: reverse rank order
+                R = ranks[r]
+                prv = ranks[r - 1]["imp_b"] if r > 0 else None
+                R["be"].tri_piped(R["st"], R["fac"], True, R["mid"], R["out"], 0, True, R["imp_b"], prv,
+                                  R["kf"][1], epoch << 32)
+                R["be"].sync()
+            got = np.concatenate([R["out"][R["sl"].own0:R["sl"].own1].cpu().numpy() for R in ranks])
+            assert np.array_equal(got, want), epoch
+            for R in ranks:
+                R["be"].fetch(R["st"])  # raises on a device error
+                assert int(R["st"].view("lcnt", 0).sum()) == 0  # checked mode: no overflow event
+    finally:
+        for R in ranks:
+            for k in ("imp_f", "imp_b"):
+                if R[k] is not None:
+                    gpu.lib().igm_dev_free(C.c_void_p(R[k]))
