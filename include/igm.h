@@ -144,6 +144,14 @@ int igm_debug_pencil27_stream(int n, const int* row_ptr, const int* col_idx, con
                               const int* diag_pos, int upper, int gx, int gy, int gz, long long* out2);
 /* debug: per-segment phase timestamps of one ILU tile (8 u64 per segment) */
 void igm_debug_tri_trace(int tile, unsigned long long* device_buf);
+/* debug: per-CTA phase timestamps (ns) of Arnoldi step j of the register
+ * resident MGS kernel; out == NULL arms, then out reads cap words and disarms;
+ * returns the slots per CTA */
+int igm_debug_arn_ts(int j, unsigned long long* out, int cap);
+/* debug: the device fast paths of the scalar fixed-point helpers on n input
+ * pairs (a_i, b_i): out[4i..4i+3] = isqrt(a), division magic of b,
+ * trunc(a / b) as int64, floor(((a mod b) * 2^64 + (~a ^ b)) / b); 0 = ok */
+int igm_debug_fx_selftest(int n, const uint64_t* a, const uint64_t* b, uint64_t* out);
 
 /* ---- primitives (parity entry points) ---------------------------------- */
 /* replaces intgmres::spmv (split.hpp:48-49, split.cpp:137-157) */

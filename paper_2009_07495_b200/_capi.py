@@ -129,6 +129,8 @@ SIGNATURES = [
     ("igm_debug_pencil27_stream", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                             C.c_int, C.c_int, C.c_int, C.POINTER(C.c_longlong)]),
     ("igm_debug_tri_trace", None, [C.c_int, C.c_void_p]),
+    ("igm_debug_arn_ts", C.c_int, [C.c_int, C.c_void_p, C.c_int]),
+    ("igm_debug_fx_selftest", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("igm_debug_tri_schedule", C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                          C.c_int, i32p]),
     ("igm_spmv", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.POINTER(Trace)]),

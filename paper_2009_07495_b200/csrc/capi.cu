@@ -733,6 +733,12 @@ igm_status igm_set_exact_overflow_counts(igm_ctx* c, int on) {
 void igm_profile_enable(int on) { prof_enable(on != 0); }
 
 // debug hook: per-segment phase timestamps of one ILU tile (4 u64 per segment)
+int igm_debug_arn_ts(int j, unsigned long long* out, int cap) { return debug_arn_ts(j, out, cap); }
+int igm_debug_fx_selftest(int n, const uint64_t* a, const uint64_t* b, uint64_t* out) {
+  return debug_fx_selftest(n, reinterpret_cast<const u64*>(a), reinterpret_cast<const u64*>(b),
+                           reinterpret_cast<u64*>(out));
+}
+
 void igm_debug_tri_trace(int tile, unsigned long long* device_buf) {
   igm::tri_trace_setup(tile, device_buf);
 }

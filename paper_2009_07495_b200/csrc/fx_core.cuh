@@ -72,6 +72,66 @@ FXC int clz64(u64 v) {
 #endif
 }
 
+#if defined(__CUDACC__)
+// Device fast paths for the one-thread scalar chains (the per-step Givens /
+// norm work): the GPU has no integer divider, and its generic 64- and 128-bit
+// division routines are long dependent sequences.  These estimate the
+// quotient in FP64 and correct it with exact 128-bit remainders, so they
+// return the same (unique) floor values.
+//
+// floor((hi * 2^64 + lo) / d), requires hi < d (the quotient fits 64 bits)
+#if defined(__CUDA_ARCH__)
+// 1 / d to ~2^-50 relative: the MUFU single-precision reciprocal refined by
+// two Newton steps in FP64 (the IEEE-exact __ddiv/__drcp sequences are an
+// order of magnitude longer on a one-thread dependent chain)
+__device__ __forceinline__ double recip_approx(double d) {
+  double r = static_cast<double>(__frcp_rn(__double2float_rn(d)));
+  r = __dmul_rn(r, __dsub_rn(2.0, __dmul_rn(d, r)));
+  r = __dmul_rn(r, __dsub_rn(2.0, __dmul_rn(d, r)));
+  return r;
+}
+#endif
+
+__host__ __device__ __forceinline__ u64 udiv128_64_dev(u64 hi, u64 lo, u64 d) {
+#if !defined(__CUDA_ARCH__)
+  return static_cast<u64>(((static_cast<unsigned __int128>(hi) << 64) | lo) / d);
+#else
+  const double dd = __ull2double_rn(d);
+  const double rcp = recip_approx(dd);
+  const double nn = __dadd_rn(__dmul_rn(__ull2double_rn(hi), 18446744073709551616.0), __ull2double_rn(lo));
+  u64 q = __double2ull_rz(__dmul_rn(nn, rcp));  // relative error < 2^-48 (saturates at 2^64 - 1)
+  // remainder num - q d as a two's complement (rhi, rlo) pair: |true value|
+  // < 2^17 d < 2^81, so the difference taken mod 2^128 is exact
+  long long rhi;
+  u64 rlo;
+  auto rem = [&]() {
+    const u64 plo = q * d, phi = __umul64hi(q, d);
+    rlo = lo - plo;
+    rhi = static_cast<long long>(hi - phi - (lo < plo ? 1ull : 0ull));
+  };
+  rem();
+  for (int it = 0; it < 2; ++it) {  // FP64 correction steps
+    const double rd = __dadd_rn(__dmul_rn(__ll2double_rn(rhi), 18446744073709551616.0), __ull2double_rn(rlo));
+    const long long dq = __double2ll_rz(__dmul_rn(rd, rcp));
+    if (dq == 0) break;
+    q += static_cast<u64>(dq);
+    rem();
+  }
+  while (rhi < 0) {  // r < 0: q too large
+    --q;
+    rlo += d;
+    rhi += rlo < d ? 1 : 0;
+  }
+  while (rhi > 0 || rlo >= d) {  // r >= d: q too small
+    ++q;
+    rhi -= rlo < d ? 1 : 0;
+    rlo -= d;
+  }
+  return q;
+#endif
+}
+#endif
+
 // Exact unsigned division by an invariant d >= 1, valid for every n < 2^64.
 struct UDivMagic {
   u64 m;    // round-up reciprocal
@@ -82,10 +142,14 @@ struct UDivMagic {
 FXC UDivMagic make_udiv(u64 d) {
   int l = 64 - clz64(d - 1);  // ceil(log2 d); 0 for d == 1
   if (d == 1) l = 0;
+  UDivMagic r;
+#if defined(__CUDA_ARCH__)
+  r.m = udiv128_64_dev(static_cast<u64>((static_cast<unsigned __int128>(1) << l) - d), 0, d) + 1;
+#else
   const unsigned __int128 num =
       ((static_cast<unsigned __int128>(1) << l) - d) << 64;
-  UDivMagic r;
   r.m = static_cast<u64>(num / d) + 1;
+#endif
   r.sh1 = l < 1 ? l : 1;
   r.sh2 = l > 1 ? l - 1 : 0;
   return r;
@@ -125,11 +189,37 @@ FXC bool sdiv_ovf(i64 num, const SDivMagic& s) {
   return s.den_is_m1 && num == INT64_MIN;
 }
 
+// trunc(num / den) for den != 0 and not (INT64_MIN / -1) (fxp.hpp:145-152)
+FXC i64 sdiv_trunc(i64 num, i64 den) {
+#if defined(__CUDA_ARCH__)
+  const u64 an = num < 0 ? 0ull - static_cast<u64>(num) : static_cast<u64>(num);
+  const u64 ad = den < 0 ? 0ull - static_cast<u64>(den) : static_cast<u64>(den);
+  const u64 q = udiv128_64_dev(0, an, ad);
+  return ((num < 0) != (den < 0)) ? static_cast<i64>(0ull - q) : static_cast<i64>(q);
+#else
+  return num / den;
+#endif
+}
+
 // floor(sqrt(v)) over the full u64 range (fxp.cpp:20-33 computes the same
 // value with Newton's method; floor sqrt is unique so any exact method is
 // bit-identical).
 FXC u64 isqrt_u64(u64 v) {
   if (v == 0) return 0;
+#if defined(__CUDA_ARCH__)
+  // FP64 estimate (within 1 of the root for v < 2^64: MUFU rsqrt refined by
+  // two Newton steps), then exact fix-ups
+  const double vd = __ull2double_rn(v);
+  double r = static_cast<double>(rsqrtf(__double2float_rn(vd)));
+  const double hv = __dmul_rn(0.5, vd);
+  r = __dmul_rn(r, __dsub_rn(1.5, __dmul_rn(hv, __dmul_rn(r, r))));
+  r = __dmul_rn(r, __dsub_rn(1.5, __dmul_rn(hv, __dmul_rn(r, r))));
+  u64 x = __double2ull_rz(__dmul_rn(vd, r));
+  if (x > 0xffffffffull) x = 0xffffffffull;
+  while (x * x > v) --x;  // x <= 2^32 - 1: x * x fits
+  while (x < 0xffffffffull && (x + 1) * (x + 1) <= v) ++x;
+  return x;
+#else
   const int bits = 64 - clz64(v);
   u64 x = u64{1} << ((bits + 1) / 2);
   for (;;) {
@@ -139,6 +229,7 @@ FXC u64 isqrt_u64(u64 v) {
   }
   while (static_cast<unsigned __int128>(x) * x > v) --x;
   return x;
+#endif
 }
 
 // Overflow event kinds and kernel tags, numbered like the oracle / FxTrace.

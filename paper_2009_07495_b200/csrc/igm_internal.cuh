@@ -56,7 +56,11 @@ struct Ctl {
   u64 rmax_bits;  // max |r_i| as IEEE bits (non-negative doubles order as u64)
   double nb, nr, relnorm;
   double scalar;  // scratch result of norm2 kernels
-  unsigned gbar;  // grid-barrier arrivals of the persistent Arnoldi kernel (reset per cycle)
+  // grid-barrier arrivals of the persistent Arnoldi kernel (reset per cycle),
+  // on a cache line of its own: every CTA polls it while CTA 0's scalar step
+  // reads and writes the fields above
+  alignas(128) unsigned gbar;
+  unsigned gbar_pad[31];
 };
 
 struct DevSplit {
@@ -186,6 +190,8 @@ struct PenZ {  // z-slab pipelining of the pencil wavefront (PenArgs::zimp ...)
   int kexp = -1;
   unsigned long long epoch = 0;
 };
+int debug_arn_ts(int j, unsigned long long* out, int cap);
+int debug_fx_selftest(int n, const u64* a, const u64* b, u64* out);
 bool launch_tri_int_piped(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out, u64* cnt,
                           const Ctl* ctl, bool checked, const PenZ& z);
 void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward,

@@ -1133,14 +1133,21 @@ struct Ev {
   }
 };
 
-__device__ i64 d_fx_mul(i64 a, i64 b, int f, int b1, int b2, int of, Ev& ev, int k) {
+// The scalar step runs once per launch, cold in the instruction cache: its
+// time is set by its code size, so the helpers it calls more than once are
+// out-of-line (one copy, warm at the second call).
+__device__ __noinline__ u64 isqrt_nl(u64 v) { return isqrt_u64(v); }
+__device__ __noinline__ i64 sdiv_trunc_nl(i64 a, i64 b) { return sdiv_trunc(a, b); }
+__device__ __noinline__ SDivMagic make_sdiv_nl(i64 d) { return make_sdiv(d); }
+
+__device__ __noinline__ i64 d_fx_mul(i64 a, i64 b, int f, int b1, int b2, int of, Ev& ev, int k) {
   const i64 x = asr(a, b1), y = asr(b, b2);
   if (mul_ovf(x, y)) ev.hit(k, OP_MUL);
   return asr(wmul(x, y), 2 * f - b1 - b2 - of);
 }
 
 // returns false on a zero shifted divisor (domain_error)
-__device__ bool d_fx_div(i64 a, i64 b, int f, int b1, int b2, i64* out, Ev& ev, int k) {
+__device__ __noinline__ bool d_fx_div(i64 a, i64 b, int f, int b1, int b2, i64* out, Ev& ev, int k) {
   const i64 num = wrap_shl(a, b1);
   if (shl_ovf(a, b1)) ev.hit(k, OP_SHL);
   const i64 den = asr(b, b2);
@@ -1150,7 +1157,7 @@ __device__ bool d_fx_div(i64 a, i64 b, int f, int b1, int b2, i64* out, Ev& ev, 
     ev.hit(k, OP_DIV);
     q = num;
   } else {
-    q = num / den;
+    q = sdiv_trunc_nl(num, den);
   }
   const int e = f - b1 - b2;
   if (e >= 0) {
@@ -1183,9 +1190,13 @@ __device__ bool abs_small(const u64* ab) {
 __device__ void step_scalar_dev(int j, int f, ShiftsD sh, const u64* acc_col, int acc_st, const u64* abs_col,
                                 int abs_st, const u64* nacc, const u64* nabs, const u64* norm_mul, i64* hess,
                                 int ld, i64* g, i64* cs, i64* sn, i64* gabs, const i64* w, u64* cnt_step,
-                                Ctl* ctl, int checked) {
+                                Ctl* ctl, int checked, unsigned long long* ts = nullptr) {
+#define SS_TS(k) \
+  if (ts != nullptr) ts[100 + (k)] = clock64();
+  SS_TS(0)
   ctl->do_vecdiv = 0;
   if (cycle_over(ctl)) return;
+  SS_TS(1)
   Ev ev{cnt_step, checked != 0};
   i64* col = hess + static_cast<long long>(j) * ld;
   // h_ij = fx_dot finalisation (fxp.cpp:63-65)
@@ -1200,6 +1211,7 @@ __device__ void step_scalar_dev(int j, int f, ShiftsD sh, const u64* acc_col, in
     }
     if (checked == 1 && !abs_small(abs_col + i * abs_st)) ctl->add_inexact = 1;
   }
+  SS_TS(2)
   // h_{j+1,j} = fx_norm(w) (fxp.cpp:69-86)
   const i64 nsum = static_cast<i64>(*nacc);
   if (checked == 1) {  // (checked == 2: the norm's add events were counted exactly by k_adds_*)
@@ -1217,6 +1229,7 @@ __device__ void step_scalar_dev(int j, int f, ShiftsD sh, const u64* acc_col, in
     set_err(ctl, IGM_DOMAIN_ERROR, EM_NORM_NEG, j);
     return;
   }
+  SS_TS(3)
   i64 hnext;
   {
     const i64 r = static_cast<i64>(isqrt_u64(static_cast<u64>(nsum)));
@@ -1224,6 +1237,7 @@ __device__ void step_scalar_dev(int j, int f, ShiftsD sh, const u64* acc_col, in
     if (shl_ovf(r, es)) ev.hit(K_NORM, OP_SHL);
     hnext = wrap_shl(r, es);
   }
+  SS_TS(4)
   col[j + 1] = hnext;
   ctl->hnext = hnext;
   const bool happy = hnext == 0;
@@ -1243,6 +1257,7 @@ __device__ void step_scalar_dev(int j, int f, ShiftsD sh, const u64* acc_col, in
     ctl->do_vecdiv = 1;
     ctl->nbasis = j + 2;
   }
+  SS_TS(5)
   // apply_stored_rotations (gmres_int.cpp:8-25)
   for (int i = 0; i < j; ++i) {
     const i64 c = cs[i], s = sn[i], hi = col[i], hn = col[i + 1];
@@ -1255,6 +1270,7 @@ __device__ void step_scalar_dev(int j, int f, ShiftsD sh, const u64* acc_col, in
     col[i] = wadd(a, b);
     col[i + 1] = wsub(d, q);
   }
+  SS_TS(6)
   // t_mp = fx_norm((h_jj, h_{j+1,j})) (gmres_int.cpp:133-137)
   i64 tmp;
   {
@@ -1278,12 +1294,14 @@ __device__ void step_scalar_dev(int j, int f, ShiftsD sh, const u64* acc_col, in
     ctl->stop = 1;
     return;
   }
+  SS_TS(7)
   i64 c, s;
   if (!d_fx_div(col[j], tmp, f, sh.div_b1, sh.div_b2, &c, ev, K_GIVENS_DIV) ||
       !d_fx_div(col[j + 1], tmp, f, sh.div_b1, sh.div_b2, &s, ev, K_GIVENS_DIV)) {
     set_err(ctl, IGM_DOMAIN_ERROR, EM_DIV_ZERO, j);
     return;
   }
+  SS_TS(8)
   cs[j] = c;
   sn[j] = s;
   col[j] = tmp;
@@ -1297,14 +1315,209 @@ __device__ void step_scalar_dev(int j, int f, ShiftsD sh, const u64* acc_col, in
   ctl->dim = j + 1;
   gabs[j] = g[j + 1];
   if (happy) ctl->stop = 1;
+  SS_TS(9)
+#undef SS_TS
+}
+
+// step_scalar_dev on one warp (same values, same overflow-event totals): the
+// h_ij finalisations and the chain-independent products of the stored
+// rotations run across the lanes; the rotation chain itself,
+//   x_0 = h_0j,  x_{i+1} = c_i * h_{i+1,j} - s_i * x_i   (d_fx_mul, wsub),
+// runs on every lane at once (redundantly: no broadcast), after which lane i
+// forms rotation i's outputs (h_ij = c_i x_i + s_i h_{i+1,j}, h_{i+1,j} =
+// x_{i+1}) and counts its events.  The norm, t_mp, (c, s) and g updates stay
+// on lane 0.  All 32 lanes of the calling warp must call it.
+__device__ void step_scalar_warp(int j, int f, ShiftsD sh, const u64* acc_col, int acc_st, const u64* abs_col,
+                                 int abs_st, const u64* nacc, const u64* nabs, const u64* norm_mul, i64* hess,
+                                 int ld, i64* g, i64* cs, i64* sn, i64* gabs, const i64* w, u64* cnt_step,
+                                 Ctl* ctl, int checked, unsigned long long* ts = nullptr) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+#define SW_TS(k) \
+  if (ts != nullptr && lane == 0) ts[100 + (k)] = clock64();
+  SW_TS(0)
+  int over = 0;
+  i64 g_old = 0;
+  if (lane == 0) {
+    ctl->do_vecdiv = 0;
+    over = cycle_over(ctl);
+    g_old = g[j];
+  }
+  if (__shfl_sync(FULL, over, 0)) return;
+  SW_TS(1)
+  Ev ev{cnt_step, checked != 0};
+  const bool on = checked != 0;
+  i64* col = hess + static_cast<long long>(j) * ld;
+  // h_ij = fx_dot finalisation (fxp.cpp:63-65), one entry per lane
+  {
+    const int e = f - sh.dot_b1 - sh.dot_b2;
+    unsigned nshl = 0;
+    int inexact = 0;
+    for (int i = lane; i <= j; i += 32) {
+      const i64 acc = static_cast<i64>(acc_col[i * acc_st]);
+      if (e >= 0) {
+        col[i] = asr(acc, e);
+      } else {
+        nshl += shl_ovf(acc, -e);
+        col[i] = wrap_shl(acc, -e);
+      }
+      if (checked == 1 && !abs_small(abs_col + i * abs_st)) inexact = 1;
+    }
+    nshl = __reduce_add_sync(FULL, nshl);
+    inexact = __any_sync(FULL, inexact);
+    if (lane == 0) {
+      if (on && nshl) cnt_step[K_DOT * OP_COUNT + OP_SHL] += nshl;
+      if (inexact) ctl->add_inexact = 1;
+    }
+  }
+  __syncwarp();
+  SW_TS(2)
+  // h_{j+1,j} = fx_norm(w) (fxp.cpp:69-86) and the vec_div reciprocal: lane 0
+  int ret = 0;
+  int happy = 0;
+  if (lane == 0) {
+    const i64 nsum = static_cast<i64>(*nacc);
+    if (checked == 1) {
+      if (*norm_mul == 0) {
+        const unsigned __int128 s2 = (static_cast<unsigned __int128>(nabs[0]) << 32) + nabs[1];
+        const unsigned __int128 wraps = (s2 + (static_cast<unsigned __int128>(1) << 63)) >> 64;
+        cnt_step[K_NORM * OP_COUNT + OP_ADD] += static_cast<u64>(wraps);
+      } else if (!abs_small(nabs)) {
+        ctl->add_inexact = 1;
+      }
+    }
+    SW_TS(6)
+    if (nsum < 0) {
+      set_err(ctl, IGM_DOMAIN_ERROR, EM_NORM_NEG, j);
+      ret = 1;
+    } else {
+      const i64 r = static_cast<i64>(isqrt_nl(static_cast<u64>(nsum)));
+      SW_TS(7)
+      const int es = sh.norm_b1;
+      if (shl_ovf(r, es)) ev.hit(K_NORM, OP_SHL);
+      const i64 hnext = wrap_shl(r, es);
+      col[j + 1] = hnext;
+      ctl->hnext = hnext;
+      happy = hnext == 0;
+      if (!happy) {
+        const i64 den = asr(hnext, sh.div_b2);
+        if (den == 0) {
+          if (shl_ovf(w[0], sh.div_b1)) ev.hit(K_VEC_DIV, OP_SHL);
+          set_err(ctl, IGM_DOMAIN_ERROR, EM_DIV_ZERO, j);
+          ret = 1;
+        } else {
+          const SDivMagic gm = make_sdiv_nl(den);
+          SW_TS(8)
+          ctl->div_m = gm.u.m;
+          ctl->div_sh1 = gm.u.sh1;
+          ctl->div_sh2 = gm.u.sh2;
+          ctl->div_neg = gm.den_neg;
+          ctl->div_m1 = gm.den_is_m1;
+          ctl->do_vecdiv = 1;
+          ctl->nbasis = j + 2;
+        }
+      }
+    }
+  }
+  if (__shfl_sync(FULL, ret, 0)) return;
+  happy = __shfl_sync(FULL, happy, 0);
+  SW_TS(3)
+  // apply_stored_rotations (gmres_int.cpp:8-25)
+  if (j > 0) {
+    const int gb2 = sh.givens_b2, sr = f - gb2;  // d_fx_mul(., ., f, 0, givens_b2, f)
+    auto fxm = [&](i64 a, i64 b) { return asr(wmul(a, asr(b, gb2)), sr); };
+    auto fxm_ovf = [&](i64 a, i64 b) { return mul_ovf(a, asr(b, gb2)) ? 1u : 0u; };
+    unsigned nmul = 0, nadd = 0, nsub = 0;
+    i64 x = col[0];  // x_0: the finalised h_0j
+    for (int base = 0; base < j; base += 32) {
+      const int i = base + lane;
+      const bool act = i < j;
+      const i64 c = act ? cs[i] : 0, sv = act ? sn[i] : 0, h1 = act ? col[i + 1] : 0;
+      const i64 D = fxm(c, h1), B = fxm(sv, h1);
+      __syncwarp();  // every lane has read its h_{i+1,j} before the outputs overwrite them
+      i64 xi = 0;
+      const int cnt = min(32, j - base);
+#pragma unroll 4
+      for (int t = 0; t < cnt; ++t) {  // the chain, on every lane
+        const i64 st = __shfl_sync(FULL, sv, t), Dt = __shfl_sync(FULL, D, t);
+        if (lane == t) xi = x;
+        x = wsub(Dt, fxm(st, x));
+      }
+      if (act) {
+        const i64 a = fxm(c, xi), q = fxm(sv, xi);
+        nmul += fxm_ovf(c, xi) + fxm_ovf(sv, h1) + fxm_ovf(c, h1) + fxm_ovf(sv, xi);
+        nadd += add_ovf(a, B);
+        nsub += sub_ovf(D, q);
+        col[i] = wadd(a, B);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) col[j] = x;  // x_j: the last rotation's h_{j,j}
+    nmul = __reduce_add_sync(FULL, nmul);
+    nadd = __reduce_add_sync(FULL, nadd);
+    nsub = __reduce_add_sync(FULL, nsub);
+    if (lane == 0 && on) {
+      if (nmul) cnt_step[K_GIVENS * OP_COUNT + OP_MUL] += nmul;
+      if (nadd) cnt_step[K_GIVENS * OP_COUNT + OP_ADD] += nadd;
+      if (nsub) cnt_step[K_GIVENS * OP_COUNT + OP_SUB] += nsub;
+    }
+  }
+  __syncwarp();
+  SW_TS(4)
+  if (lane != 0) return;
+  // t_mp = fx_norm((h_jj, h_{j+1,j})) (gmres_int.cpp:133-137)
+  i64 tmp;
+  {
+    const i64 s0 = asr(col[j], sh.norm_b1), s1 = asr(col[j + 1], sh.norm_b1);
+    if (mul_ovf(s0, s0)) ev.hit(K_GIVENS_NORM, OP_MUL);
+    const i64 p0 = wmul(s0, s0);
+    i64 acc = p0;
+    if (mul_ovf(s1, s1)) ev.hit(K_GIVENS_NORM, OP_MUL);
+    const i64 p1 = wmul(s1, s1);
+    if (add_ovf(acc, p1)) ev.hit(K_GIVENS_NORM, OP_ADD);
+    acc = wadd(acc, p1);
+    if (acc < 0) {
+      set_err(ctl, IGM_DOMAIN_ERROR, EM_NORM_NEG, j);
+      return;
+    }
+    const i64 r = static_cast<i64>(isqrt_nl(static_cast<u64>(acc)));
+    if (shl_ovf(r, sh.norm_b1)) ev.hit(K_GIVENS_NORM, OP_SHL);
+    tmp = wrap_shl(r, sh.norm_b1);
+  }
+  SW_TS(9)
+  if (tmp == 0) {
+    ctl->stop = 1;
+    return;
+  }
+  i64 c, sv;
+  if (!d_fx_div(col[j], tmp, f, sh.div_b1, sh.div_b2, &c, ev, K_GIVENS_DIV) ||
+      !d_fx_div(col[j + 1], tmp, f, sh.div_b1, sh.div_b2, &sv, ev, K_GIVENS_DIV)) {
+    set_err(ctl, IGM_DOMAIN_ERROR, EM_DIV_ZERO, j);
+    return;
+  }
+  SW_TS(10)
+  cs[j] = c;
+  sn[j] = sv;
+  col[j] = tmp;
+  col[j + 1] = 0;
+  // residual estimate (gmres_int.cpp:150-153)
+  if (sub_ovf(0, sv)) ev.hit(K_ROT, OP_SUB);
+  const i64 neg_s = wsub(0, sv);
+  g[j + 1] = d_fx_mul(neg_s, g_old, f, sh.rot_b, sh.rot_b, f, ev, K_ROT);
+  g[j] = d_fx_mul(c, g_old, f, sh.rot_b, sh.rot_b, f, ev, K_ROT);
+  ctl->dim = j + 1;
+  gabs[j] = g[j + 1];
+  if (happy) ctl->stop = 1;
+  SW_TS(5)
+#undef SW_TS
 }
 
 __global__ void k_step_scalar(int j, int f, ShiftsD sh, const u64* acc_col, int acc_st, const u64* abs_col,
                               int abs_st, const u64* nacc, const u64* nabs, const u64* norm_mul, i64* hess,
                               int ld, i64* g, i64* cs, i64* sn, i64* gabs, const i64* w, u64* cnt_step,
                               Ctl* ctl, int checked) {
-  step_scalar_dev(j, f, sh, acc_col, acc_st, abs_col, abs_st, nacc, nabs, norm_mul, hess, ld, g, cs, sn, gabs, w,
-                  cnt_step, ctl, checked);
+  step_scalar_warp(j, f, sh, acc_col, acc_st, abs_col, abs_st, nacc, nabs, norm_mul, hess, ld, g, cs, sn, gabs, w,
+                   cnt_step, ctl, checked);
 }
 
 // ---------------------------------------------------------------------------
@@ -1318,7 +1531,7 @@ __global__ void k_step_scalar(int j, int f, ShiftsD sh, const u64* acc_col, int 
 // step is the per-element one of the pass kernels, and reductions are the
 // same wrapping (order-free) u64 sums, so results are bit-identical.
 constexpr int kArnThreads = 1024;
-constexpr size_t kArnSmemMax = 227 * 1024 - 1024;  // dynamic; the static reduction scratch is 768 B
+constexpr size_t kArnSmemMax = 227 * 1024 - 2048;  // dynamic; static + dynamic <= 228 KB per CTA (k_arnoldi2: 2.1 KB static)
 
 // grid barrier: arrival count since the cycle started (Ctl::gbar); barrier
 // number k completes when all G CTAs have arrived k times.  The acquire spin
@@ -1871,6 +2084,18 @@ __device__ __forceinline__ void sts64(unsigned a, i64 v) {
 constexpr int kArn2Threads = 512;
 constexpr int kArn2Q = 7;  // quads per thread: up to 4 * 512 * 7 = 14336 rows per CTA
 
+// debug (igm_debug_arn_ts): per-CTA phase timestamps (globaltimer, ns) of the
+// Arnoldi step j = g_arn_ts_j; slot 4i+0 v_i's buffer ready, +1 pass i
+// computed, +2 CTA sum added, +3 grid barrier passed; 120.. the step tail
+__device__ unsigned long long* g_arn_ts = nullptr;
+__device__ int g_arn_ts_j = -1;
+constexpr int kArnTsSlots = 128;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <bool CHECKED>
 __global__ void __launch_bounds__(kArn2Threads, 1)
     k_arnoldi2(long long n, int j, long long S, const i64* __restrict__ win, i64* basis, u64* accj, u64* absj,
@@ -1883,6 +2108,9 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
   __shared__ __align__(8) unsigned long long s_bar[2];
   __shared__ u64 s_mx[2];
   if (cycle_over(ctl)) return;  // uniform: ctl is not written before the first barrier
+  unsigned long long* ts = (g_arn_ts_j == j && threadIdx.x == 0) ? g_arn_ts + blockIdx.x * kArnTsSlots : nullptr;
+#define ARN_TS(slot) \
+  if (ts != nullptr && (slot) < kArnTsSlots) ts[slot] = gtimer();
   constexpr int T = kArn2Threads, Q = kArn2Q;
   const unsigned G = gridDim.x;
   unsigned nbar = gbase;
@@ -1975,7 +2203,9 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
   i64 wr[Q][4];  // this thread's rows of w: quads tid + m * T
   // ---- pass 0: w -> registers, dot_0 = <w, v_0>
   {
+    ARN_TS(124)
     wait_buf(0);
+    ARN_TS(0)
     ArnAcc A;
 #pragma unroll
     for (int m = 0; m < Q; ++m) {
@@ -1995,7 +2225,9 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
       }
     }
     if (CHECKED) bump(cD, OP_MUL, A.n3);
+    ARN_TS(1)
     cta_reduce_add<CHECKED, T>(A.sum, A.ahi, A.alo, accj + 0, absj + 0, red);
+    ARN_TS(2)
     if (CHECKED) {
       cta_max2(Wb, V0);
       Wb = s_mx[0];
@@ -2011,7 +2243,9 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
   // ---- passes 1..j: axpy_{i-1} (v_{i-1} in buf[(i-1)&1]), dot_i (v_i in buf[i&1])
   for (int i = 1; i <= j; ++i) {
     const i64 hs = h_of(grid_barrier(ctl, (++nbar) * G, accj + i - 1, &s_word));
+    ARN_TS(4 * i - 1)
     wait_buf(i & 1);
+    ARN_TS(4 * i)
     const i64* vp = buf[(i - 1) & 1];
     const i64* vc = buf[i & 1];
     ArnAcc A;
@@ -2040,13 +2274,16 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
       bump(cA, OP_SUB, A.n2);
       bump(cD, OP_MUL, A.n3);
     }
+    ARN_TS(4 * i + 1)
     cta_reduce_add<CHECKED, T>(A.sum, A.ahi, A.alo, accj + i, absj + 2 * i, red);
+    ARN_TS(4 * i + 2)
     // every thread is past its reads of v_{i-1}: its buffer takes v_{i+1}
     if (tid == 0 && i + 1 <= j) fetch((i + 1) & 1, basis + static_cast<long long>(i + 1) * n);
   }
   // ---- axpy_j (v_j in buf[j&1]), then the norm sum of the orthogonalised w
   {
     const i64 hs = h_of(grid_barrier(ctl, (++nbar) * G, accj + j, &s_word));
+    ARN_TS(4 * j + 3)
     const i64* vp = buf[j & 1];
     ArnAcc A;
     auto pass = [&](auto ovf) {
@@ -2085,10 +2322,13 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
       bump(cA, OP_SUB, A.n2);
       bump(cN, OP_MUL, A.n3);
     }
+    ARN_TS(4 * j + 5)
     cta_reduce_add<CHECKED, T>(A.sum, A.ahi, A.alo, nacc, nabs, red);
+    ARN_TS(4 * j + 6)
   }
   // ---- per-step scalar work (one thread), then v_{j+1} = w / h_{j+1,j}
   grid_barrier(ctl, (++nbar) * G, nullptr, nullptr);
+  ARN_TS(120)
   if (blockIdx.x == 0 && 6LL * (j + 2) > 2 * S) {  // too small a slice to stage in: straight from global memory
     if (tid == 0) {
       __threadfence();
@@ -2120,14 +2360,17 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
     }
     if (tid == 0) s_col[j + 1] = col[j + 1];
     __syncthreads();
+    i64* w0 = s_sn + (j + 1);
     if (tid == 0) {
       __threadfence();  // this SM's L1 holds no stale copy of the reduced words
       // w is only dereferenced for an error diagnostic: row 0 (this thread's first)
-      i64* w0 = s_sn + (j + 1);
       *w0 = nq > 0 ? wr[0][0] : 0;
-      step_scalar_dev(j, f, sh, s_acc, 1, s_abs, 2, nacc, nabs, cstep + K_NORM * OP_COUNT + OP_MUL,
-                      s_col - static_cast<long long>(j) * ld, ld, g, s_cs, s_sn, gabs, w0, cstep, ctl,
-                      CHECKED ? 1 : 0);
+    }
+    if (tid < 32) {
+      __syncwarp();
+      step_scalar_warp(j, f, sh, s_acc, 1, s_abs, 2, nacc, nabs, cstep + K_NORM * OP_COUNT + OP_MUL,
+                       s_col - static_cast<long long>(j) * ld, ld, g, s_cs, s_sn, gabs, w0, cstep, ctl,
+                       CHECKED ? 1 : 0, ts);
     }
     __syncthreads();
     for (int q = tid; q <= j + 1; q += T) col[q] = s_col[q];
@@ -2136,7 +2379,9 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
       sn[j] = s_sn[j];
     }
   }
+  ARN_TS(121)
   const u64 dm = grid_barrier(ctl, (++nbar) * G, &ctl->div_m, &s_word);
+  ARN_TS(122)
   if (tid == 0) {
     volatile const int* c = &ctl->do_vecdiv;
     s_vd[0] = c[0];
@@ -2146,6 +2391,7 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
     s_vd[4] = *static_cast<volatile int*>(&ctl->div_m1);
   }
   __syncthreads();
+  ARN_TS(125)
   if (!s_vd[0]) return;
   {
     SDivMagic gm;
@@ -2157,14 +2403,25 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
     const int b1 = sh.div_b1, ee = f - sh.div_b1 - sh.div_b2;
     i64* out = basis + static_cast<long long>(j + 1) * n + lo;
     u64 nshl = 0, ndiv = 0, vmax = 0;
+    // w's registers -> this thread's own slots of the free buffer, then ONE
+    // compact loop over them: this code runs once per launch, so its size
+    // (instruction-cache misses), not its arithmetic, sets its time -- the
+    // fully unrolled loop took 4x longer cold than warm
+    i64* ws = buf[1];
 #pragma unroll
     for (int m = 0; m < Q; ++m) {
       const int q = tid + m * T;
+      if (q < nq) sts_q(ws + 4 * q, wr[m]);
+    }
+#pragma unroll 1
+    for (int m = 0; m < Q; ++m) {
+      const int q = tid + m * T;
       if (q < nq) {
-        i64 vq[4];
+        i64 vq[4], wq[4];
+        lds_q(ws + 4 * q, wq);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const i64 a = wr[m][e];
+          const i64 a = wq[e];
           const i64 num = wrap_shl(a, b1);
           const i64 qq = sdiv(num, gm);
           if (ee >= 0) {
@@ -2182,6 +2439,7 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
         st_v4(out + 4 * q, vq);
       }
     }
+    ARN_TS(126)
     if (CHECKED) {
       bump(cstep + K_VEC_DIV * OP_COUNT, OP_SHL, nshl);
       bump(cstep + K_VEC_DIV * OP_COUNT, OP_DIV, ndiv);
@@ -2189,7 +2447,10 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
       if (tid == 0) vmx_me[j + 1] = s_mx[0];
     }
   }
+  ARN_TS(123)
+#undef ARN_TS
 }
+
 
 __device__ __forceinline__ int4 lds128i(unsigned a) {
   int4 v;
@@ -2621,6 +2882,54 @@ TriArgs tri_args(const DevTri& t) {
 
 }  // namespace
 
+// device fast paths of fx_core.cuh (isqrt, division magic, truncating and
+// 128/64 division) on n input pairs: out[4i..4i+3]
+__global__ void k_fx_selftest(int n, const u64* a, const u64* b, u64* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const u64 x = a[i], y = b[i] ? b[i] : 1;
+  out[4 * i + 0] = isqrt_u64(x);
+  out[4 * i + 1] = make_udiv(y).m;
+  const i64 sx = static_cast<i64>(x), sy = static_cast<i64>(y);
+  out[4 * i + 2] = (sx == INT64_MIN && sy == -1) ? 0 : static_cast<u64>(sdiv_trunc(sx, sy));
+  out[4 * i + 3] = udiv128_64_dev(x % y, ~x ^ y, y);
+}
+
+int debug_fx_selftest(int n, const u64* a, const u64* b, u64* out) {
+  u64 *da, *db, *dout;
+  cudaMalloc(&da, 8 * static_cast<size_t>(n) + 8);
+  cudaMalloc(&db, 8 * static_cast<size_t>(n) + 8);
+  cudaMalloc(&dout, 32 * static_cast<size_t>(n) + 8);
+  cudaMemcpy(da, a, 8 * static_cast<size_t>(n), cudaMemcpyHostToDevice);
+  cudaMemcpy(db, b, 8 * static_cast<size_t>(n), cudaMemcpyHostToDevice);
+  k_fx_selftest<<<(n + 255) / 256, 256>>>(n, da, db, dout);
+  const cudaError_t e = cudaMemcpy(out, dout, 32 * static_cast<size_t>(n), cudaMemcpyDeviceToHost);
+  cudaFree(da);
+  cudaFree(db);
+  cudaFree(dout);
+  return e == cudaSuccess ? 0 : 1;
+}
+
+// arm (out == nullptr: record step j of the following k_arnoldi2 launches) /
+// read and disarm (out: cap words, CTA-major, kArnTsSlots per CTA)
+int debug_arn_ts(int j, unsigned long long* out, int cap) {
+  static unsigned long long* buf = nullptr;
+  constexpr int kMaxCta = 1024;
+  if (out == nullptr) {
+    if (buf == nullptr) cudaMalloc(&buf, sizeof(unsigned long long) * kMaxCta * kArnTsSlots);
+    cudaMemset(buf, 0, sizeof(unsigned long long) * kMaxCta * kArnTsSlots);
+    cudaMemcpyToSymbol(g_arn_ts, &buf, sizeof(buf));
+    cudaMemcpyToSymbol(g_arn_ts_j, &j, sizeof(int));
+    return kArnTsSlots;
+  }
+  cudaDeviceSynchronize();
+  const int n = cap < kMaxCta * kArnTsSlots ? cap : kMaxCta * kArnTsSlots;
+  cudaMemcpy(out, buf, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost);
+  const int off = -1;
+  cudaMemcpyToSymbol(g_arn_ts_j, &off, sizeof(int));
+  return kArnTsSlots;
+}
+
 // ---------------------------------------------------------------------------
 // FP64 engine (Engine::floating_point: refine.cpp:47-86, refsolve.cpp:9-105)
 // reconstruct_fp (split.cpp:177-191): vals[k] = sum_l ldexp(double(c_l[k]), -alpha_l), from 0.0
@@ -2908,7 +3217,7 @@ void launch_step_scalar(cudaStream_t st, int j, int f, ShiftsD sh, const u64* ac
                         int checked, int acc_st, int abs_st, const u64* norm_mul) {
   ProfScope prof_(st, KC_SCALAR);
   if (!norm_mul) norm_mul = cnt_step + K_NORM * OP_COUNT + OP_MUL;
-  k_step_scalar<<<1, 1, 0, st>>>(j, f, sh, acc_col, acc_st, abs_col, abs_st, nacc, nabs, norm_mul, hess, ld, g,
+  k_step_scalar<<<1, 32, 0, st>>>(j, f, sh, acc_col, acc_st, abs_col, abs_st, nacc, nabs, norm_mul, hess, ld, g,
                                  cs, sn, gabs, w, cnt_step, ctl, checked);
   LAUNCH_CHECK();
 }
@@ -3095,16 +3404,16 @@ static u64 pen_epoch() {
 // builder produces is valid for every cluster size (a brick waits only on
 // bricks of earlier tickets), so a cluster launch that cannot be scheduled
 // (e.g. SMs taken by another context) falls back to single-brick CTAs.
-template <bool CHECKED, bool FP, int CY>
+template <bool CHECKED, bool FP, int CY, bool PIPE>
 static bool pen2_launch_cy(cudaStream_t st, const DevTri& t, const PenArgs& a, const i64* y, i64* out,
                            const int* stop, const int* err, const double* prescale) {
   static PerDevice attr;  // the attributes are per device
   if (attr.first(cur_device())) {
-    cudaFuncSetAttribute(k_tri_pencil2<CHECKED, FP, CY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_tri_pencil2<CHECKED, FP, CY, PIPE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kP2Smem));
   }
   if constexpr (CY == 1) {
-    k_tri_pencil2<CHECKED, FP, 1><<<t.pen_nbricks, kP2Threads, kP2Smem, st>>>(a, y, out, stop, err, prescale);
+    k_tri_pencil2<CHECKED, FP, 1, PIPE><<<t.pen_nbricks, kP2Threads, kP2Smem, st>>>(a, y, out, stop, err, prescale);
     return true;
   } else {
     cudaLaunchConfig_t cfg = {};
@@ -3119,21 +3428,21 @@ static bool pen2_launch_cy(cudaStream_t st, const DevTri& t, const PenArgs& a, c
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, k_tri_pencil2<CHECKED, FP, CY>, a, y, out, stop, err, prescale) == cudaSuccess)
+    if (cudaLaunchKernelEx(&cfg, k_tri_pencil2<CHECKED, FP, CY, PIPE>, a, y, out, stop, err, prescale) == cudaSuccess)
       return true;
     cudaGetLastError();  // not launchable as clusters: fall back
     return false;
   }
 }
 
-template <bool CHECKED, bool FP>
+template <bool CHECKED, bool FP, bool PIPE>
 static void pen2_launch(cudaStream_t st, const DevTri& t, const PenArgs& a, const i64* y, i64* out, const int* stop,
                         const int* err, const double* prescale) {
   bool ok = false;
-  if (t.pen_cy == 8) ok = pen2_launch_cy<CHECKED, FP, 8>(st, t, a, y, out, stop, err, prescale);
-  else if (t.pen_cy == 4) ok = pen2_launch_cy<CHECKED, FP, 4>(st, t, a, y, out, stop, err, prescale);
-  else if (t.pen_cy == 2) ok = pen2_launch_cy<CHECKED, FP, 2>(st, t, a, y, out, stop, err, prescale);
-  if (!ok) pen2_launch_cy<CHECKED, FP, 1>(st, t, a, y, out, stop, err, prescale);
+  if (t.pen_cy == 8) ok = pen2_launch_cy<CHECKED, FP, 8, PIPE>(st, t, a, y, out, stop, err, prescale);
+  else if (t.pen_cy == 4) ok = pen2_launch_cy<CHECKED, FP, 4, PIPE>(st, t, a, y, out, stop, err, prescale);
+  else if (t.pen_cy == 2) ok = pen2_launch_cy<CHECKED, FP, 2, PIPE>(st, t, a, y, out, stop, err, prescale);
+  if (!ok) pen2_launch_cy<CHECKED, FP, 1, PIPE>(st, t, a, y, out, stop, err, prescale);
 }
 
 // pencil wavefront (tri_pencil.cuh / tri_pencil2.cuh) of a structured 7-point
@@ -3180,8 +3489,15 @@ static void pen_launch(cudaStream_t st, const DevTri& t, bool backward, const vo
     return e == nullptr || std::atoi(e) != 0;
   }();
   if (v2 || zp) {
-    if (checked && !FP) pen2_launch<true, FP>(st, t, a, yi, oi, stop, err, prescale);
-    else pen2_launch<false, FP>(st, t, a, yi, oi, stop, err, prescale);
+    if constexpr (!FP) {
+      if (zp) {  // pipelined z-slab substitution: the PIPE instantiation
+        if (checked) pen2_launch<true, false, true>(st, t, a, yi, oi, stop, err, prescale);
+        else pen2_launch<false, false, true>(st, t, a, yi, oi, stop, err, prescale);
+        return;
+      }
+    }
+    if (checked && !FP) pen2_launch<true, FP, false>(st, t, a, yi, oi, stop, err, prescale);
+    else pen2_launch<false, FP, false>(st, t, a, yi, oi, stop, err, prescale);
     return;
   }
   if (checked && !FP)

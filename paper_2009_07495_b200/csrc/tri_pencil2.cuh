@@ -133,7 +133,9 @@ __device__ __noinline__ void p2_report(int id, int x, int y) {
 __device__ unsigned long long g_p2_bt[64 * 64 * 16];
 #endif
 
-template <bool CHECKED, bool FP, int CY>
+// PIPE: the z-slab hand-off of a pipelined row partition (PenArgs::zimp /
+// zexp); a separate instantiation so the single-GPU kernel carries none of it
+template <bool CHECKED, bool FP, int CY, bool PIPE = false>
 __global__ void __launch_bounds__(kP2Threads, 1)
     k_tri_pencil2(PenArgs a, const i64* __restrict__ y, i64* __restrict__ out, const int* stop, const int* err,
                   const double* prescale) {
@@ -220,7 +222,7 @@ __global__ void __launch_bounds__(kP2Threads, 1)
         for (int q = 0; q < G; ++q) {
           const int s = g * G + q;
           const bool act = static_cast<unsigned>(s - sa[v]) < static_cast<unsigned>(gz);
-          if (a.zimp != nullptr && act && s == sa[v]) {  // plane 0: the neighbour rank's value (pipelined slabs)
+          if (PIPE && a.zimp != nullptr && act && s == sa[v]) {  // plane 0: the neighbour rank's value (pipelined slabs)
             const int j = by * kPenY + 2 * v + jj;
             const long long idx = a.mirror ? static_cast<long long>(a.gy - 1 - j) * a.gx + (a.gx - 1 - i)
                                            : static_cast<long long>(j) * a.gx + i;
@@ -242,7 +244,7 @@ __global__ void __launch_bounds__(kP2Threads, 1)
                        "r"(act ? 8 : 0)
                        : "memory");
         }
-        if (a.zimp != nullptr) asm volatile("fence.acq_rel.cta;" ::: "memory");  // imported words stored above
+        if (PIPE && a.zimp != nullptr) asm volatile("fence.acq_rel.cta;" ::: "memory");  // imported words stored above
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(fb) : "memory");
       }
     }
@@ -438,7 +440,7 @@ __global__ void __launch_bounds__(kP2Threads, 1)
           else p2_sts_word(ring_prod + rs * 256u, static_cast<u64>(z), k);
         }
         if (act) *op = z;
-        if (a.zexp != nullptr && act && k == a.kexp) {  // the next rank's plane-0 value (pipelined slabs)
+        if (PIPE && a.zexp != nullptr && act && k == a.kexp) {  // the next rank's plane-0 value (pipelined slabs)
           const long long idx = a.mirror ? static_cast<long long>(a.gy - 1 - j) * a.gx + (a.gx - 1 - i)
                                          : static_cast<long long>(j) * a.gx + i;
           const u64 tz = a.zepoch + static_cast<u64>(idx);

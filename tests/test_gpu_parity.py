@@ -939,3 +939,50 @@ def test_piped_substitution_protocol(gpu, oracle, g, world):
             for k in ("imp_f", "imp_b"):
                 if R[k] is not None:
                     gpu.lib().igm_dev_free(C.c_void_p(R[k]))
+
+
+def test_fx_device_fast_paths(gpu):
+    """The device fast paths of the scalar helpers (fx_core.cuh: FP64
+    estimate + exact 128-bit remainder fix-ups) against exact integer
+    arithmetic: floor sqrt (fxp.cpp:20-33), the round-up division magic,
+    truncating int64 division (fxp.hpp:145-152), and 128/64 floor division --
+    on edge values (0, 1, squares +-1, powers of two +-1, 2^63, 2^64 - 1) and
+    random words of every magnitude."""
+    import ctypes as C
+    import math
+    M = (1 << 64) - 1
+    edge = {0, 1, 2, 3, 4, 5, 7, 8, 9, 15, 16, 17, (1 << 32) - 1, 1 << 32, (1 << 32) + 1, (1 << 63) - 1, 1 << 63,
+            (1 << 63) + 1, M, M - 1, ((1 << 32) - 1) ** 2, ((1 << 32) - 1) ** 2 - 1, ((1 << 32) - 1) ** 2 + 1}
+    for k in range(1, 64):
+        edge |= {(1 << k) - 1, 1 << k, ((1 << k) + 1) & M}
+    for r in (3, 1000, 65535, 65536, 94906265, 94906266, 3037000499, 3037000500, 4294967295):
+        edge |= {r * r - 1, r * r, r * r + 1}
+    edge = sorted(e & M for e in edge)
+    rng = np.random.default_rng(11)
+    rand = [int(x) >> int(s) for x, s in zip(rng.integers(0, 1 << 63, 4000, dtype=np.uint64).astype(object) * 2 +
+                                             rng.integers(0, 2, 4000).astype(object),
+                                             rng.integers(0, 64, 4000))]
+    a = [x for x in edge for _ in range(3)] + rand + rand[::-1]
+    b = [edge[(i * 7 + 3) % len(edge)] for i in range(len(edge) * 3)] + rand[::-1] + [max(1, x >> 40) for x in rand]
+    n = len(a)
+    A = np.array(a, dtype=np.uint64)
+    B = np.array(b, dtype=np.uint64)
+    out = np.zeros(4 * n, dtype=np.uint64)
+    assert gpu.lib().igm_debug_fx_selftest(n, A.ctypes.data_as(C.c_void_p), B.ctypes.data_as(C.c_void_p),
+                                           out.ctypes.data_as(C.c_void_p)) == 0
+    out = out.reshape(n, 4)
+    sgn = lambda v: v - (1 << 64) if v >= 1 << 63 else v
+    for i in range(n):
+        x, y = a[i], b[i] if b[i] else 1
+        want_sqrt = math.isqrt(x)
+        l = 0 if y == 1 else (y - 1).bit_length()
+        want_m = ((((1 << l) - y) << 64) // y + 1) & M
+        sx, sy = sgn(x), sgn(y)
+        if sx == -(1 << 63) and sy == -1:
+            want_q = 0
+        else:
+            q = abs(sx) // abs(sy)
+            want_q = (-q if (sx < 0) != (sy < 0) else q) & M
+        want_u = ((((x % y) << 64) | ((~x ^ y) & M)) // y) & M
+        got = [int(v) for v in out[i]]
+        assert got == [want_sqrt, want_m, want_q, want_u], (x, y, got, [want_sqrt, want_m, want_q, want_u])
