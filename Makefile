@@ -25,7 +25,7 @@ $(BUILD)/%.o: $(PKG)/csrc/%.cpp $(HDRS) $(PKG)/csrc/schedule.hpp
 	@mkdir -p $(BUILD)
 	g++ $(CXXFLAGS) -I/usr/local/cuda/include -c $< -o $@
 
-$(LIB): $(BUILD)/kernels.o $(BUILD)/setup.o $(BUILD)/capi.o $(BUILD)/shim.o $(BUILD)/schedule.o $(BUILD)/mm_io.o $(BUILD)/experiment.o $(BUILD)/wl32.o
+$(LIB): $(BUILD)/kernels.o $(BUILD)/setup.o $(BUILD)/capi.o $(BUILD)/shim.o $(BUILD)/schedule.o $(BUILD)/mm_io.o $(BUILD)/experiment.o $(BUILD)/wl32.o $(BUILD)/trace_order.o
 	$(NVCC) $(ARCH) -shared -o $@ $^
 
 oracle:

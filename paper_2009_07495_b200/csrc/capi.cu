@@ -347,6 +347,24 @@ void trace_add(igm_trace* t, int kernel, int op, u64 count, int restart, int ste
   }
 }
 
+// ordered event lists of the primitives (trace_order.cu): the counters give
+// the totals, a locate pass gives the list in the reference's element order
+bool list_room(const igm_trace* t) { return t && t->checked && t->events && t->n_events < t->cap_events; }
+long long list_left(const igm_trace* t) { return static_cast<long long>(t->cap_events) - t->n_events; }
+void list_push(igm_trace* t, int kernel, std::vector<unsigned char>& codes) {
+  for (unsigned char op : codes) {
+    if (t->n_events >= t->cap_events) break;
+    int32_t* e = t->events + 4 * t->n_events;
+    e[0] = kernel; e[1] = op; e[2] = t->restart; e[3] = t->step;
+    t->n_events++;
+  }
+  codes.clear();
+}
+struct Locator {
+  std::unique_ptr<LocateScratch, void (*)(LocateScratch*)> s{locate_scratch_new(), locate_scratch_free};
+  std::vector<unsigned char> codes;
+};
+
 void trace_shift(igm_trace* t, int kernel, int b1, int b2, long long times = 1) {
   if (!t || !t->record_shifts || times <= 0) return;
   for (long long i = 0; i < times; ++i) {
@@ -607,6 +625,199 @@ void fetch_cycle_state(igm_ctx* c) {
      "small D2H");
 }
 
+// The cycle's overflow events in the reference's sequential order
+// (trace_order.cu): the vector calls of every step with events are replayed
+// on the device from the cycle's basis and accumulators and located element
+// by element; the scalar work (fx_dot / fx_sqrt finalisations, the stored
+// rotations, t_mp, (c, s), g) is replayed here in gmres_int.cpp:90-160's
+// order.  Appends to t->events until it is full; t->total is the caller's.
+void ordered_events(igm_ctx* c, const CycleParams& p, igm_trace* t, int restart, long long n, int steps_run) {
+  Work& w = c->ws;
+  cudaStream_t st = c->stream;
+  const u64* cnt = hview<u64>(w, w.cnt);
+  const u64* acc = hview<u64>(w, w.acc);
+  const u64* nacc = hview<u64>(w, w.nacc);
+  const int M = p.M, f = p.f;
+  const igm_shifts& s = p.sh;
+  const size_t cstride = static_cast<size_t>(K_COUNT) * OP_COUNT;
+  auto room = [&]() -> long long { return static_cast<long long>(t->cap_events) - t->n_events; };
+  auto push = [&](int k, int op, int step) {
+    if (t->n_events >= t->cap_events) return;
+    int32_t* e = t->events + 4 * t->n_events;
+    e[0] = k; e[1] = op; e[2] = restart; e[3] = step;
+    t->n_events++;
+  };
+  std::unique_ptr<LocateScratch, void (*)(LocateScratch*)> S(locate_scratch_new(), locate_scratch_free);
+  std::vector<unsigned char> codes;
+  auto flush = [&](int k, int step) {
+    for (unsigned char op : codes) push(k, op, step);
+    codes.clear();
+  };
+  std::vector<i64> g(static_cast<size_t>(M) + 1, 0), hc(static_cast<size_t>(M), 0), hsn(static_cast<size_t>(M), 0);
+  g[0] = static_cast<i64>(1) << f;
+  std::vector<i64> col(static_cast<size_t>(M) + 2);
+  const int gb2 = s.givens_b2;
+  auto fxm_g = [&](i64 a, i64 b, int step) {  // fx_mul(a, b, 0, givens_b2, f) (gmres_int.cpp:18-21)
+    const i64 y = asr(b, gb2);
+    if (mul_ovf(a, y)) push(K_GIVENS, OP_MUL, step);
+    return asr(wmul(a, y), f - gb2);
+  };
+  // fx_div(a, b, div_b1, div_b2) (fxp.hpp:220-235); false when it throws
+  auto fxdiv = [&](i64 a, i64 b, int k, int step, i64* out) {
+    if (shl_ovf(a, s.div_b1)) push(k, OP_SHL, step);
+    const i64 num = wrap_shl(a, s.div_b1);
+    const i64 den = asr(b, s.div_b2);
+    if (den == 0) return false;
+    i64 q;
+    if (num == INT64_MIN && den == -1) {
+      push(k, OP_DIV, step);
+      q = num;
+    } else {
+      q = num / den;
+    }
+    const int e = f - s.div_b1 - s.div_b2;
+    if (e >= 0) {
+      if (shl_ovf(q, e)) push(k, OP_SHL, step);
+      *out = wrap_shl(q, e);
+    } else {
+      *out = asr(q, -e);
+    }
+    return true;
+  };
+  // counts that may miss running-sum adds (add_inexact): locate every call
+  const bool all = c->h_ctl->add_inexact != 0;
+  for (int j = 0; j < steps_run && room() > 0; ++j) {
+    const u64* cj = cnt + static_cast<size_t>(j) * cstride;
+    auto ktot = [&](int k) {
+      u64 v = all ? 1 : 0;
+      for (int op = 1; op < OP_COUNT; ++op) v += cj[k * OP_COUNT + op];
+      return v;
+    };
+    const bool vec = ktot(K_SPMV) + ktot(K_PRECOND) + ktot(K_DOT) + ktot(K_AXPY) + ktot(K_NORM) + ktot(K_VEC_DIV) > 0;
+    const u64* aj = acc + static_cast<size_t>(j) * (M + 1);
+    // ---- w = M^{-1} A v_j (gmres_int.cpp:94-99)
+    if (vec) {
+      const i64* vj = w.basis + static_cast<long long>(j) * n;
+      i64* y = p.pre ? w.z : w.w;
+      launch_spmv_int(st, *p.m, p.s, vj, y, nullptr, nullptr, false);
+      if (ktot(K_SPMV)) {
+        locate_spmv(st, *S, *p.m, p.s, vj, room(), codes);
+        flush(K_SPMV, j);
+      }
+      if (p.pre) {
+        launch_tri_int(st, p.pre->lower, false, w.z, w.vin, nullptr, nullptr, false);
+        launch_tri_int(st, p.pre->upper, true, w.vin, w.w, nullptr, nullptr, false);
+        if (ktot(K_PRECOND)) {
+          locate_tri(st, *S, p.pre->lower, false, w.z, w.vin, room(), codes);
+          flush(K_PRECOND, j);
+          locate_tri(st, *S, p.pre->upper, true, w.vin, w.w, room(), codes);
+          flush(K_PRECOND, j);
+        }
+      }
+    }
+    // ---- modified Gram-Schmidt (gmres_int.cpp:101-110)
+    const int e_dot = f - s.dot_b1 - s.dot_b2;
+    for (int i = 0; i <= j; ++i) {
+      const i64* vi = w.basis + static_cast<long long>(i) * n;
+      if (vec && ktot(K_DOT)) {
+        locate_red(st, *S, n, w.w, vi, s.dot_b1, s.dot_b2, room(), codes);
+        flush(K_DOT, j);
+      }
+      const i64 a = static_cast<i64>(aj[i]);
+      i64 hij;
+      if (e_dot >= 0) {
+        hij = asr(a, e_dot);
+      } else {
+        if (shl_ovf(a, -e_dot)) push(K_DOT, OP_SHL, j);
+        hij = wrap_shl(a, -e_dot);
+      }
+      col[i] = hij;
+      if (vec) {
+        if (ktot(K_AXPY)) {
+          locate_axpy(st, *S, n, w.w, vi, asr(hij, s.axpy_b1), f - s.axpy_b1, room(), codes);
+          flush(K_AXPY, j);
+        }
+        launch_axpy_only(st, n, w.w, hij, vi, f, s.axpy_b1, nullptr, false);
+      }
+    }
+    // ---- h_{j+1,j} = fx_norm(w) (gmres_int.cpp:112-114, fxp.cpp:69-86)
+    if (vec && ktot(K_NORM)) {
+      locate_red(st, *S, n, w.w, nullptr, s.norm_b1, s.norm_b1, room(), codes);
+      flush(K_NORM, j);
+    }
+    const i64 nsum = static_cast<i64>(nacc[j]);
+    if (nsum < 0) break;  // domain_error
+    i64 hnext;
+    {
+      const i64 r = static_cast<i64>(isqrt_u64(static_cast<u64>(nsum)));
+      if (shl_ovf(r, s.norm_b1)) push(K_NORM, OP_SHL, j);
+      hnext = wrap_shl(r, s.norm_b1);
+    }
+    col[j + 1] = hnext;
+    const bool happy = hnext == 0;
+    // ---- v_{j+1} = w / h_{j+1,j} (gmres_int.cpp:116-125)
+    if (!happy) {
+      const i64 den = asr(hnext, s.div_b2);
+      if (den == 0) {  // fx_div of element 0 throws after its shl
+        i64 w0 = 0;
+        ck(cudaMemcpyAsync(&w0, w.w, sizeof(i64), cudaMemcpyDeviceToHost, st), "w0");
+        ck(cudaStreamSynchronize(st), "w0");
+        if (shl_ovf(w0, s.div_b1)) push(K_VEC_DIV, OP_SHL, j);
+        break;
+      }
+      if (vec && ktot(K_VEC_DIV)) {
+        locate_vec_div(st, *S, n, w.w, den, s.div_b1, f - s.div_b1 - s.div_b2, room(), codes);
+        flush(K_VEC_DIV, j);
+      }
+    }
+    // ---- stored rotations (gmres_int.cpp:8-25)
+    for (int i = 0; i < j; ++i) {
+      const i64 ci = hc[i], si = hsn[i], hi = col[i], hn = col[i + 1];
+      const i64 a = fxm_g(ci, hi, j), b = fxm_g(si, hn, j), d = fxm_g(ci, hn, j), e = fxm_g(si, hi, j);
+      if (add_ovf(a, b)) push(K_GIVENS, OP_ADD, j);
+      if (sub_ovf(d, e)) push(K_GIVENS, OP_SUB, j);
+      col[i] = wadd(a, b);
+      col[i + 1] = wsub(d, e);
+    }
+    // ---- t_mp = fx_norm((h_jj, h_{j+1,j})) (gmres_int.cpp:132-137)
+    i64 tmp;
+    {
+      const i64 s0 = asr(col[j], s.norm_b1), s1 = asr(col[j + 1], s.norm_b1);
+      if (mul_ovf(s0, s0)) push(K_GIVENS_NORM, OP_MUL, j);
+      i64 ac = wmul(s0, s0);
+      if (mul_ovf(s1, s1)) push(K_GIVENS_NORM, OP_MUL, j);
+      const i64 p1 = wmul(s1, s1);
+      if (add_ovf(ac, p1)) push(K_GIVENS_NORM, OP_ADD, j);
+      ac = wadd(ac, p1);
+      if (ac < 0) break;  // domain_error
+      const i64 r = static_cast<i64>(isqrt_u64(static_cast<u64>(ac)));
+      if (shl_ovf(r, s.norm_b1)) push(K_GIVENS_NORM, OP_SHL, j);
+      tmp = wrap_shl(r, s.norm_b1);
+    }
+    if (tmp == 0) break;
+    // ---- (c, s) (gmres_int.cpp:139-147)
+    i64 cj_, sj_;
+    if (!fxdiv(col[j], tmp, K_GIVENS_DIV, j, &cj_)) break;
+    if (!fxdiv(col[j + 1], tmp, K_GIVENS_DIV, j, &sj_)) break;
+    hc[j] = cj_;
+    hsn[j] = sj_;
+    // ---- g (gmres_int.cpp:149-153)
+    {
+      const i64 g_old = g[j];
+      if (sub_ovf(0, sj_)) push(K_ROT, OP_SUB, j);
+      const i64 neg_s = wsub(0, sj_);
+      auto fxm_r = [&](i64 a, i64 b) {
+        const i64 x = asr(a, s.rot_b), y = asr(b, s.rot_b);
+        if (mul_ovf(x, y)) push(K_ROT, OP_MUL, j);
+        return asr(wmul(x, y), 2 * f - 2 * s.rot_b - f);
+      };
+      g[j + 1] = fxm_r(neg_s, g_old);
+      g[j] = fxm_r(cj_, g_old);
+    }
+    if (happy) break;
+  }
+}
+
 // Fold one cycle's device counters into the trace; returns the cycle total.
 u64 account_cycle(igm_ctx* c, const CycleParams& p, igm_trace* t, int restart, long long n) {
   const Work& w = c->ws;
@@ -621,22 +832,21 @@ u64 account_cycle(igm_ctx* c, const CycleParams& p, igm_trace* t, int restart, l
   else if (h.nbasis == h.dim) steps_run = h.dim;   // happy breakdown
   else steps_run = std::min(p.M, h.dim + 1);       // t_mp == 0 break
   const size_t cstride = static_cast<size_t>(K_COUNT) * OP_COUNT;
-  for (int j = 0; j < steps_run; ++j) {
-    for (int kk : kKernelOrder) {
-      for (int op = 1; op < OP_COUNT; ++op) {
-        const u64 v = cnt[j * cstride + kk * OP_COUNT + op];
-        if (v) {
-          total += v;
-          trace_add(t, kk, op, v, restart, j);
-        }
-      }
-    }
+  for (int j = 0; j < steps_run; ++j)
+    for (int kk : kKernelOrder)
+      for (int op = 1; op < OP_COUNT; ++op) total += cnt[j * cstride + kk * OP_COUNT + op];
+  if (t && (total || h.add_inexact)) {
+    t->total += total;
+    // the event list in the reference's order (the totals above are exact
+    // whatever the list's room)
+    if (t->events && t->n_events < t->cap_events) ordered_events(c, p, t, restart, n, steps_run);
   }
   if (t) {
     if (h.add_inexact) t->exact = 0;
     // shift records, synthesised in the reference's call order
     if (t->record_shifts) {
       const auto& s = p.sh;
+      const u64* nacc = hview<u64>(w, w.nacc);
       for (int j = 0; j < steps_run; ++j) {
         for (int i = 0; i <= j; ++i) {
           trace_shift(t, K_DOT, s.dot_b1, s.dot_b2);
@@ -644,13 +854,31 @@ u64 account_cycle(igm_ctx* c, const CycleParams& p, igm_trace* t, int restart, l
         }
         trace_shift(t, K_NORM, s.norm_b1, s.norm_b1);
         const bool last = (j == steps_run - 1);
+        // a domain_error of the last step stops the log where the reference
+        // throws: fx_norm of w (after its record), vec_div of element 0 (after
+        // one record), t_mp's fx_norm, or the first Givens fx_div
+        int err_at = 0;  // 1 norm, 2 vec_div, 3 givens_norm, 4 givens_div
+        if (last && h.err) {
+          const i64 nsum = static_cast<i64>(nacc[j]);
+          if (nsum < 0) {
+            err_at = 1;
+          } else {
+            const i64 hnext = wrap_shl(static_cast<i64>(isqrt_u64(static_cast<u64>(nsum))), s.norm_b1);
+            if (hnext != 0 && asr(hnext, s.div_b2) == 0) err_at = 2;
+            else err_at = h.err_msg == EM_NORM_NEG ? 3 : 4;
+          }
+        }
+        if (err_at == 1) break;
         const bool broke_tmp = last && h.stop && !h.err && h.dim == j;  // t_mp == 0
-        const bool vecdiv = !last || h.nbasis == j + 2;
-        if (vecdiv) trace_shift(t, K_VEC_DIV, s.div_b1, s.div_b2, n);
+        const bool vecdiv = err_at == 2 || (err_at == 0 && (!last || h.nbasis == j + 2)) ||
+                            (err_at >= 3 && h.nbasis == j + 2);
+        if (vecdiv) trace_shift(t, K_VEC_DIV, s.div_b1, s.div_b2, err_at == 2 ? 1 : n);
+        if (err_at == 2) break;
         trace_shift(t, K_GIVENS, 0, s.givens_b2, 4LL * j);
         trace_shift(t, K_GIVENS_NORM, s.norm_b1, s.norm_b1);
-        if (broke_tmp) break;
-        trace_shift(t, K_GIVENS_DIV, s.div_b1, s.div_b2, 2);
+        if (broke_tmp || err_at == 3) break;
+        trace_shift(t, K_GIVENS_DIV, s.div_b1, s.div_b2, err_at == 4 ? 1 : 2);
+        if (err_at == 4) break;
         trace_shift(t, K_ROT, s.rot_b, s.rot_b, 2);
       }
     }
@@ -905,8 +1133,13 @@ igm_status igm_spmv(igm_ctx* c, const igm_split* m, int s, const int64_t* v, int
     ck(cudaMemcpyAsync(c->h_red, c->red, sizeof(u64) * (3 + OP_COUNT), cudaMemcpyDeviceToHost, c->stream), "D2H");
     ck(cudaStreamSynchronize(c->stream), "sync");
     if (chk) {
-      trace_add(t, t->kernel, OP_MUL, c->h_red[3 + OP_MUL], t->restart, t->step);
-      trace_add(t, t->kernel, OP_ADD, c->h_red[3 + OP_ADD], t->restart, t->step);
+      const u64 tot = c->h_red[3 + OP_MUL] + c->h_red[3 + OP_ADD];
+      t->total += tot;
+      if (tot && list_room(t)) {  // split.cpp:141-153 order
+        Locator L;
+        locate_spmv(c->stream, *L.s, *m, s, dv.d, list_left(t), L.codes);
+        list_push(t, t->kernel, L.codes);
+      }
     }
   });
 }
@@ -926,8 +1159,17 @@ igm_status igm_apply_inverse(igm_ctx* c, const igm_ilu* f, const int64_t* y, int
     dout.fetch(c->stream);
     ck(cudaMemcpyAsync(c->h_red, c->red, sizeof(u64) * (3 + OP_COUNT), cudaMemcpyDeviceToHost, c->stream), "D2H");
     ck(cudaStreamSynchronize(c->stream), "sync");
-    if (chk)
-      for (int op : {OP_MUL, OP_SUB, OP_DIV}) trace_add(t, t->kernel, op, c->h_red[3 + op], t->restart, t->step);
+    if (chk) {
+      const u64 tot = c->h_red[3 + OP_MUL] + c->h_red[3 + OP_SUB] + c->h_red[3 + OP_DIV];
+      t->total += tot;
+      if (tot && list_room(t)) {  // ilu.cpp:126-153 order: forward rows, then backward rows descending
+        Locator L;
+        locate_tri(c->stream, *L.s, f->lower, false, dy.d, c->ws.z, list_left(t), L.codes);
+        list_push(t, t->kernel, L.codes);
+        locate_tri(c->stream, *L.s, f->upper, true, c->ws.z, dout.d, list_left(t), L.codes);
+        list_push(t, t->kernel, L.codes);
+      }
+    }
   });
 }
 
@@ -945,10 +1187,17 @@ igm_status igm_apply_inverse_fp(igm_ctx* c, const igm_ilu* f, const double* y, d
   });
 }
 
+// list: the caller's trace when its event list has room -- the elements'
+// events in order (fxp.cpp:57-61 / 77-81) are appended after the reduction
 static void fx_red_common(igm_ctx* c, long long n, int mode, const int64_t* v, const int64_t* w,
-                          int b1, int b2, bool chk) {
+                          int b1, int b2, bool chk, igm_trace* list = nullptr) {
   In<i64> dv(v, n, c->stream);
   In<i64> dw(mode == 0 ? w : nullptr, n, c->stream);
+  if (list && n > 0) {
+    Locator L;
+    locate_red(c->stream, *L.s, n, dv.d, mode == 0 ? dw.d : nullptr, b1, b2, list_left(list), L.codes);
+    list_push(list, list->kernel, L.codes);
+  }
   ck(cudaMemsetAsync(c->red, 0, sizeof(u64) * (3 + OP_COUNT), c->stream), "memset");
   if (n > 0) launch_fx_red(c->stream, n, mode, dv.d, dw.d, b1, b2, c->red, c->red + 1, c->red + 3, chk);
   if (n > 0 && chk && c->exact_adds)  // exact running-sum events (no-op under the certificate)
@@ -971,11 +1220,11 @@ igm_status igm_fx_dot(igm_ctx* c, int64_t n, const int64_t* v, const int64_t* w,
     check_shift(b2, "fx_dot");
     if (t) trace_shift(t, t->kernel, b1, b2);
     const bool chk = t && t->checked;
-    fx_red_common(c, n, 0, v, w, b1, b2, chk);
+    fx_red_common(c, n, 0, v, w, b1, b2, chk, list_room(t) ? t : nullptr);
     const i64 acc = static_cast<i64>(c->h_red[0]);
     if (chk) {
-      trace_add(t, t->kernel, OP_MUL, c->h_red[3 + OP_MUL], t->restart, t->step);
-      if (c->exact_adds) trace_add(t, t->kernel, OP_ADD, c->h_red[3 + OP_ADD], t->restart, t->step);
+      t->total += c->h_red[3 + OP_MUL];
+      if (c->exact_adds) t->total += c->h_red[3 + OP_ADD];
       else if (!abs_small_h(c->h_red + 1)) t->exact = 0;
     }
     const int e = f - b1 - b2;
@@ -999,17 +1248,17 @@ igm_status igm_fx_norm(igm_ctx* c, int64_t n, const int64_t* v, int f, int b1, i
            "fx_norm: accumulator format not representable (need 2*(f-b1) in [0, 62])");
     if (t) trace_shift(t, t->kernel, b1, b1);
     const bool chk = t && t->checked;
-    fx_red_common(c, n, 1, v, nullptr, b1, b1, chk);
+    fx_red_common(c, n, 1, v, nullptr, b1, b1, chk, list_room(t) ? t : nullptr);
     const i64 acc = static_cast<i64>(c->h_red[0]);
     if (chk) {
       const u64 nmul = c->h_red[3 + OP_MUL];
-      trace_add(t, t->kernel, OP_MUL, nmul, t->restart, t->step);
+      t->total += nmul;
       if (c->exact_adds) {
-        trace_add(t, t->kernel, OP_ADD, c->h_red[3 + OP_ADD], t->restart, t->step);
+        t->total += c->h_red[3 + OP_ADD];
       } else if (nmul == 0) {
         const unsigned __int128 s = (static_cast<unsigned __int128>(c->h_red[1]) << 32) + c->h_red[2];
         const u64 wraps = static_cast<u64>((s + (static_cast<unsigned __int128>(1) << 63)) >> 64);
-        trace_add(t, t->kernel, OP_ADD, wraps, t->restart, t->step);
+        t->total += wraps;
       } else if (!abs_small_h(c->h_red + 1)) {
         t->exact = 0;
       }
@@ -1044,14 +1293,17 @@ igm_status igm_fx_axpy_sub(igm_ctx* c, int64_t n, int64_t* w, int64_t h, const i
       ck(cudaMemcpyAsync(dw, w, sizeof(i64) * n, cudaMemcpyHostToDevice, c->stream), "H2D");
     }
     ck(cudaMemsetAsync(c->red, 0, sizeof(u64) * (3 + OP_COUNT), c->stream), "memset");
+    Locator L;
+    if (chk && n > 0 && list_room(t))  // fxp.cpp:98-103 order, located on the input w
+      locate_axpy(c->stream, *L.s, n, dw, dv.d, asr(h, b1), f - b1, list_left(t), L.codes);
     if (n > 0) launch_axpy_only(c->stream, n, dw, h, dv.d, f, b1, c->red + 3, chk);
     if (!wdev) ck(cudaMemcpyAsync(w, dw, sizeof(i64) * n, cudaMemcpyDeviceToHost, c->stream), "D2H");
     ck(cudaMemcpyAsync(c->h_red, c->red, sizeof(u64) * (3 + OP_COUNT), cudaMemcpyDeviceToHost, c->stream), "D2H");
     ck(cudaStreamSynchronize(c->stream), "sync");
     dfree(owned);
     if (chk) {
-      trace_add(t, t->kernel, OP_MUL, c->h_red[3 + OP_MUL], t->restart, t->step);
-      trace_add(t, t->kernel, OP_SUB, c->h_red[3 + OP_SUB], t->restart, t->step);
+      t->total += c->h_red[3 + OP_MUL] + c->h_red[3 + OP_SUB];
+      list_push(t, t->kernel, L.codes);
     }
   });
 }

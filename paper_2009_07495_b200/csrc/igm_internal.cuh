@@ -190,6 +190,21 @@ struct PenZ {  // z-slab pipelining of the pencil wavefront (PenArgs::zimp ...)
   int kexp = -1;
   unsigned long long epoch = 0;
 };
+// trace_order.cu: reference-order event lists (locate passes of one call;
+// each appends at most `room` op tags to out and returns the call's total)
+struct LocateScratch;
+LocateScratch* locate_scratch_new();
+void locate_scratch_free(LocateScratch* s);
+long long locate_spmv(cudaStream_t st, LocateScratch& S, const DevSplit& m, int s, const i64* v, long long room,
+                      std::vector<unsigned char>& out);
+long long locate_tri(cudaStream_t st, LocateScratch& S, const DevTri& t, bool backward, const i64* y, const i64* z,
+                     long long room, std::vector<unsigned char>& out);
+long long locate_red(cudaStream_t st, LocateScratch& S, long long n, const i64* w, const i64* v, int b1, int b2,
+                     long long room, std::vector<unsigned char>& out);
+long long locate_axpy(cudaStream_t st, LocateScratch& S, long long n, const i64* w, const i64* v, i64 hs, int post,
+                      long long room, std::vector<unsigned char>& out);
+long long locate_vec_div(cudaStream_t st, LocateScratch& S, long long n, const i64* w, i64 den, int b1, int e,
+                         long long room, std::vector<unsigned char>& out);
 int debug_arn_ts(int j, unsigned long long* out, int cap);
 int debug_fx_selftest(int n, const u64* a, const u64* b, u64* out);
 bool launch_tri_int_piped(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out, u64* cnt,

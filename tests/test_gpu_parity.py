@@ -49,6 +49,7 @@ def test_spmv_bit_exact(gpu, oracle, goldens, name):
             out = gpu.spmv(c["S"], s, v, t1)
             assert np.array_equal(out, oracle.spmv(c["sp"], s, v, t2))
             assert t1.total_overflows() == t2.total  # per-row sequential: exact
+            assert t1.events == t2.events  # split.cpp:141-153 order (trace_order.cu)
         if "spmv" in goldens["cases"][name]:
             assert h(gpu.spmv(c["S"], s, c["v_full"])) == goldens["cases"][name]["spmv"][str(s)]
 
@@ -63,6 +64,7 @@ def test_ilu_apply_bit_exact(gpu, oracle, goldens, name):
         t1, t2 = gpu.FxTrace(), PyTrace()
         assert np.array_equal(gpu.apply_inverse(c["F"], y, t1), oracle.apply_inverse(c["il"], y, t2))
         assert t1.total_overflows() == t2.total
+        assert t1.events == t2.events
     for _ in range(3):  # repeated launches: the spin-wait protocol is re-armed every call
         assert h(gpu.apply_inverse(c["F"], c["y_int"])) == g["apply_inverse"]
 
@@ -111,11 +113,16 @@ def test_vector_kernels_random(gpu, oracle):
         gpu.fx_axpy_sub(ww, hh, v, 30, b1, t1)
         assert np.array_equal(ww, oracle.fx_axpy_sub(w, hh, v, 30, b1, t2))
         assert t1.total_overflows() == t2.total
+        assert t1.events == t2.events
+        t1, t2 = gpu.FxTrace(), PyTrace()
+        assert gpu.fx_dot(v, w, 30, b1, b2, t1) == oracle.fx_dot(v, w, 30, b1, b2, t2)
+        assert t1.events == t2.events  # mul / running-sum add per element (fxp.cpp:57-61), then the shl
         lim = (1 << 40) if n < 10000 else (1 << 33)  # keep sum of squares < 2^63
         u = rng.integers(-lim, lim, n, dtype=np.int64)
         t1, t2 = gpu.FxTrace(), PyTrace()
         assert gpu.fx_norm(u, 30, 16, t1) == oracle.fx_norm(u, 30, 16, t2)
         assert t1.total_overflows() == t2.total  # square wraps are exact
+        assert t1.events == t2.events
         x = rng.uniform(-1, 1, n)
         assert gpu.norm2(x) == oracle.norm2(x)
 
@@ -986,3 +993,111 @@ def test_fx_device_fast_paths(gpu):
         want_u = ((((x % y) << 64) | ((~x ^ y) & M)) // y) & M
         got = [int(v) for v in out[i]]
         assert got == [want_sqrt, want_m, want_q, want_u], (x, y, got, [want_sqrt, want_m, want_q, want_u])
+
+
+# (grid kind, size, row-scale alpha, split depth, plan, ILU): plans that wrap
+# (found with the restatement; event totals per kernel in the comments)
+_ORDER_CASES = {
+    "dot-guard-removed": ("lap", 8, 16, 10, (0, 0, 16, 16, 16, 14, 16, 0), False),  # dot mul/add
+    "ilu-spmv-precond": ("up", 12, 36, 1, (0, 0, 0, 0, 28, 0, 0, 0), True),  # spmv mul/add, precond sub
+    "ilu-capped": ("up", 12, 40, 1, (4, 4, 0, 0, 20, 0, 8, 0), True),  # > 1024 events: the list is capped
+    "mgs-vecdiv-error": ("lap", 8, 33, 1, (4, 4, 0, 0, 20, 0, 8, 0), False),  # dot/axpy/norm/vec_div/givens/rot,
+}                                                                             # then a domain_error
+
+
+def _order_case(gpu, oracle, name):
+    from workloads import gen
+    kind, g, alpha, depth, plan, ilu = _ORDER_CASES[name]
+    rp, ci, v = gen.upwind_2d(g) if kind == "up" else gen.laplacian2d(g)
+    n = len(rp) - 1
+    f = 30
+    vals, scale = gpu.row_scale(rp, ci, v, alpha)
+    comp, al, _ = gpu.build_split(vals, alpha, depth)
+    pre = opre = None
+    if ilu:
+        lo, up = gpu.factorize_split_cast(rp, ci, vals)
+        pre, opre = gpu.IluFactors(lo, up), oracle.ilu(lo, up)
+    b = gen.uniform(31, n) / scale
+    return rp, ci, vals, comp, al, plan, pre, opre, b, f
+
+
+@pytest.mark.parametrize("name", list(_ORDER_CASES))
+def test_overflow_event_order(gpu, oracle, name):
+    """FxTrace::events in the reference's sequential order (fxp.hpp:51-103,
+    refine.cpp:100): plans that wrap products and running sums in spmv,
+    the ILU substitutions, the MGS dots / axpys, the norm, vec_div and the
+    scalar Givens work; the device counts are grouped per (step, kernel, op),
+    the list is rebuilt by trace_order.cu (replayed vector calls + located
+    elements, host-replayed scalar work).  The first 1024 events of one
+    cycle and of a whole solve equal the restatement's, entry for entry."""
+    rp, ci, vals, comp, al, plan, pre, opre, b, f = _order_case(gpu, oracle, name)
+    n = len(rp) - 1
+    S = gpu.SplitMatrix(rp, ci, comp, al)
+    sp = oracle.split(rp, ci, comp, al)
+    s = len(al) - 1
+    # one cycle
+    t = gpu.FxTrace(checked=True)
+    to = PyTrace()
+    from oracle.ffi import CheckerError
+    errs = []
+    try:
+        gpu.run_cycle(S, gpu.CycleConfig(m=8, frac_bits=f, shifts=gpu.ShiftPlan(*plan), s=s, precond=pre), b,
+                      np.zeros(n), trace=t)
+        errs.append(None)
+    except (ArithmeticError, ValueError, OverflowError, RuntimeError) as e:
+        errs.append(type(e).__name__)
+    try:
+        oracle.run_cycle(sp, 8, f, s, Shifts(*plan), b, np.zeros(n), precond=opre, trace=to)
+        errs.append(None)
+    except CheckerError:
+        errs.append("err")
+    assert (errs[0] is None) == (errs[1] is None)
+    assert to.total > 0
+    if t.exact:  # (otherwise the running-sum adds are counted only where certified)
+        assert t.total_overflows() == to.total
+    assert len(t.events) == len(to.events) == min(1024, to.total)
+    assert t.events == to.events
+    # a whole solve: events across restarts
+    A = gpu.CsrMatrixF(rp, ci, vals)
+    t2 = gpu.FxTrace(checked=True)
+    to2 = PyTrace()
+    try:
+        gpu.solve(S, A, b, gpu.RefineConfig(tol=1e-8, max_refinements=3, m=6, frac_bits=f, shifts=gpu.ShiftPlan(*plan),
+                                            s=s), precond=pre, trace=t2)
+    except (ArithmeticError, ValueError, OverflowError, RuntimeError):
+        pass
+    try:
+        oracle.solve(sp, oracle.csrf(rp, ci, vals), b, 1e-8, 3, 6, f, s, Shifts(*plan), precond=opre, trace=to2)
+    except CheckerError:
+        pass
+    assert t2.events == to2.events
+
+
+@pytest.mark.parametrize("name", ["ilu-spmv-precond", "mgs-vecdiv-error"])
+def test_shift_records_match(gpu, oracle, name):
+    """FxTrace::shifts (record_shifts: one (kernel, b1, b2) per shifted
+    multiply / divide / dot / norm call, fxp.cpp:56,77,98 and fxp.hpp:212,228),
+    which the device path synthesises in gmres_int.cpp's call order (one per
+    vec_div element, four per stored rotation, ...): the whole log of one
+    cycle equals the restatement's, including a cycle that ends in a
+    domain_error."""
+    rp, ci, vals, comp, al, plan, pre, opre, b, f = _order_case(gpu, oracle, name)
+    n = len(rp) - 1
+    S = gpu.SplitMatrix(rp, ci, comp, al)
+    sp = oracle.split(rp, ci, comp, al)
+    s = len(al) - 1
+    t = gpu.FxTrace(checked=True, record_shifts=True)
+    to = PyTrace(record_shifts=True)
+    from oracle.ffi import CheckerError
+    try:
+        gpu.run_cycle(S, gpu.CycleConfig(m=8, frac_bits=f, shifts=gpu.ShiftPlan(*plan), s=s, precond=pre), b,
+                      np.zeros(n), trace=t)
+    except (ArithmeticError, ValueError, OverflowError, RuntimeError):
+        pass
+    try:
+        oracle.run_cycle(sp, 8, f, s, Shifts(*plan), b, np.zeros(n), precond=opre, trace=to)
+    except CheckerError:
+        pass
+    assert len(to.shifts) > n  # at least one vec_div sweep
+    assert t.shifts == to.shifts
+    assert t.events == to.events
