@@ -394,6 +394,47 @@ igm_status igm_ipc_handle(const void* dptr, unsigned char handle[64]);
 igm_status igm_ipc_open(igm_ctx* ctx, const unsigned char handle[64], void** dptr);
 void igm_ipc_close(void* dptr);
 
+/* ---- one-shot P2P mailbox reductions -------------------
+ * The partitioned cycle needs, after every MGS / norm pass, the SUM over ranks
+ * of 3 u64 words (fx_dot / fx_norm accumulators, fxp.cpp:49-86: wrapping sums
+ * are exact in any order) before the next pass can derive h_i -- a latency-,
+ * not bandwidth-bound exchange.  A mailbox is a device buffer of
+ * 2 (parity) x world (sender) x max_words 16-byte words; every rank maps all
+ * peers' mailboxes (CUDA IPC between processes, peer access inside one
+ * process).  A reduction is two small kernels on the context stream:
+ *   publish: stores each word as (value, tag ^ value), tag = f(sequence
+ *            number, word index), with one 128-bit store into slot [rank] of
+ *            EVERY rank's mailbox (NVLink P2P stores; no reads cross the link);
+ *   collect: polls this rank's own mailbox until all `world` senders' words
+ *            of this sequence number have arrived (a stale or torn word fails
+ *            the tag check), reduces them (lanes = senders, warp shuffles) and
+ *            overwrites `words` with the result -- identical on every rank.
+ * Ranks issue the same reductions in the same order (the sequence number is
+ * counted per mailbox).  Two parities suffice: rank A can publish sequence
+ * k+2 only after collecting k+1, which needed B's publish of k+1, which B
+ * enqueued after its collect of k.  A sender that never arrives makes the
+ * collect give up after `IGM_MBOX_TIMEOUT_MS` (default 20 000): the error is
+ * reported by igm_mbox_status / the next igm_mbox_allreduce. */
+typedef struct igm_mbox igm_mbox;
+enum { IGM_MBOX_SUM = 0 /* u64 mod 2^64 */, IGM_MBOX_MAX = 1 /* signed int64 */ };
+enum { IGM_MBOX_MAX_WORLD = 32, IGM_MBOX_MAX_WORDS = 4096 };
+igm_status igm_mbox_create(igm_ctx* ctx, int rank, int world, int max_words, igm_mbox** out);
+void igm_mbox_free(igm_mbox* m);
+/* CUDA IPC handle of this rank's mailbox (to be exchanged out of band) */
+igm_status igm_mbox_handle(igm_mbox* m, unsigned char handle[64]);
+/* one process per GPU: handles = world x 64 bytes, rank-major (own entry ignored) */
+igm_status igm_mbox_connect_ipc(igm_mbox* m, const unsigned char* handles);
+/* one process, several contexts / devices: all = the world's mailboxes by
+ * rank (peer access is enabled between their devices) */
+igm_status igm_mbox_connect_local(igm_mbox* m, igm_mbox* const* all);
+/* the two halves, asynchronous on ctx's stream; n <= max_words device words */
+igm_status igm_mbox_publish(igm_ctx* ctx, igm_mbox* m, const uint64_t* words, int n);
+igm_status igm_mbox_collect(igm_ctx* ctx, igm_mbox* m, uint64_t* words, int n, int op);
+/* publish + collect, any n (chunks of max_words) */
+igm_status igm_mbox_allreduce(igm_ctx* ctx, igm_mbox* m, uint64_t* words, int n, int op);
+/* synchronises ctx's stream; IGM_CUDA_ERROR if a collect timed out */
+igm_status igm_mbox_status(igm_ctx* ctx, igm_mbox* m);
+
 /* v0 = encode(r0 / ||r0||) (gmres_int.cpp:71-81) */
 igm_status igm_dc_encode(igm_ctx* ctx, igm_dstate* d, int64_t n, const double* r0, int64_t* v0,
                          int frac_bits);

@@ -176,6 +176,16 @@ SIGNATURES = [
     ("igm_ipc_handle", C.c_int, [C.c_void_p, C.c_void_p]),
     ("igm_ipc_open", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
     ("igm_ipc_close", None, [C.c_void_p]),
+    # one-shot P2P mailbox reductions
+    ("igm_mbox_create", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    ("igm_mbox_free", None, [C.c_void_p]),
+    ("igm_mbox_handle", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("igm_mbox_connect_ipc", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("igm_mbox_connect_local", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    ("igm_mbox_publish", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
+    ("igm_mbox_collect", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
+    ("igm_mbox_allreduce", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
+    ("igm_mbox_status", C.c_int, [C.c_void_p, C.c_void_p]),
     ("igm_dc_encode", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int]),
     ("igm_dc_spmv", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
                               C.c_int]),

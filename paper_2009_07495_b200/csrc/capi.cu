@@ -2242,6 +2242,253 @@ void igm_ipc_close(void* dptr) {
   if (dptr) cudaIpcCloseMemHandle(dptr);
 }
 
+}  // extern "C"
+
+// ---- one-shot P2P mailbox reductions (igm.h: igm_mbox_*) -------------------
+struct igm_mbox {
+  int device = 0, rank = 0, world = 1, max_words = 0;
+  ulonglong2* local = nullptr;  // [2][world][max_words]
+  ulonglong2* peer[IGM_MBOX_MAX_WORLD] = {};
+  bool ipc[IGM_MBOX_MAX_WORLD] = {};
+  bool connected = false;
+  unsigned long long seq = 0;  // reductions issued (identical on every rank)
+  int* d_err = nullptr;        // a collect gave up waiting
+  unsigned long long timeout_ns = 20000ull * 1000000ull;
+};
+
+namespace {
+
+struct MboxPeers {
+  ulonglong2* p[IGM_MBOX_MAX_WORLD];
+};
+
+__device__ __forceinline__ u64 mbox_tag(u64 seq, int i) { return (seq << 16) + static_cast<u64>(i) + 1; }
+
+// thread (p, i): word i into slot [parity][rank] of rank p's mailbox
+__global__ void k_mbox_publish(MboxPeers peers, const u64* __restrict__ words, int n, int rank, int world,
+                               int max_words, u64 seq) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * world) return;
+  const int p = t / n, i = t - p * n;
+  const u64 v = words[i];
+  const u64 tag = mbox_tag(seq, i) ^ v;
+  ulonglong2* dst = peers.p[p] + (static_cast<size_t>((seq & 1) * world + rank) * max_words + i);
+  asm volatile("{ .reg .b128 t; mov.b128 t, {%1, %2}; st.relaxed.sys.global.b128 [%0], t; }" ::"l"(dst), "l"(v),
+               "l"(tag)
+               : "memory");
+}
+
+// one warp per word: lane p polls sender p's slot, then a shuffle reduction
+__global__ void k_mbox_collect(const ulonglong2* __restrict__ local, u64* __restrict__ words, int n, int world,
+                               int max_words, u64 seq, int op, unsigned long long timeout_ns, int* err) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= n) return;
+  u64 v = 0;
+  bool ok = true;
+  if (lane < world) {
+    const ulonglong2* src = local + (static_cast<size_t>((seq & 1) * world + lane) * max_words + i);
+    const u64 want = mbox_tag(seq, i);
+    unsigned long long t0 = 0;
+    unsigned spins = 0;
+    for (;;) {
+      u64 a, b;
+      asm volatile("{ .reg .b128 t; ld.relaxed.sys.global.b128 t, [%2]; mov.b128 {%0, %1}, t; }"
+                   : "=l"(a), "=l"(b)
+                   : "l"(src)
+                   : "memory");
+      if ((b ^ a) == want) {
+        v = a;
+        break;
+      }
+      if ((++spins & 1023u) == 0) {
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > timeout_ns) {
+          ok = false;
+          break;
+        }
+      }
+    }
+  } else if (op == IGM_MBOX_MAX) {
+    v = static_cast<u64>(INT64_MIN);
+  }
+  __syncwarp();
+  if (!__all_sync(0xffffffffu, ok)) {
+    if (lane == 0) atomicExch(err, 1);
+    return;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const u64 o = __shfl_xor_sync(0xffffffffu, v, d);
+    if (op == IGM_MBOX_MAX) v = static_cast<i64>(o) > static_cast<i64>(v) ? o : v;
+    else v += o;
+  }
+  if (lane == 0) words[i] = v;
+}
+
+void mbox_need(igm_ctx* c, igm_mbox* m, const void* words, int n) {
+  need_ctx(c);
+  if (!m) fail(IGM_INVALID_ARGUMENT, "mbox: null mailbox");
+  if (m->device != c->device) fail(IGM_INVALID_ARGUMENT, "mbox: mailbox and context are on different devices");
+  if (!m->connected) fail(IGM_INVALID_ARGUMENT, "mbox: not connected");
+  if (n < 0 || n > m->max_words) fail(IGM_INVALID_ARGUMENT, "mbox: word count out of range");
+  if (n > 0 && (!words || !is_device_ptr(words))) fail(IGM_INVALID_ARGUMENT, "mbox: words must be a device pointer");
+}
+
+void mbox_publish(igm_ctx* c, igm_mbox* m, const u64* words, int n) {
+  ++m->seq;
+  if (n == 0) return;
+  MboxPeers pp;
+  for (int p = 0; p < IGM_MBOX_MAX_WORLD; ++p) pp.p[p] = m->peer[p];
+  const int total = n * m->world;
+  k_mbox_publish<<<(total + 255) / 256, 256, 0, c->stream>>>(pp, words, n, m->rank, m->world, m->max_words, m->seq);
+  ck(cudaPeekAtLastError(), "mbox publish");
+  ++g_launches;
+}
+
+void mbox_collect(igm_ctx* c, igm_mbox* m, u64* words, int n, int op) {
+  if (n == 0) return;
+  k_mbox_collect<<<(n + 7) / 8, 256, 0, c->stream>>>(m->local, words, n, m->world, m->max_words, m->seq, op,
+                                                      m->timeout_ns, m->d_err);
+  ck(cudaPeekAtLastError(), "mbox collect");
+  ++g_launches;
+}
+
+}  // namespace
+
+extern "C" {
+
+igm_status igm_mbox_create(igm_ctx* c, int rank, int world, int max_words, igm_mbox** out) {
+  return guarded([&] {
+    need_ctx(c);
+    if (!out) fail(IGM_INVALID_ARGUMENT, "mbox_create: null out");
+    if (world < 1 || world > IGM_MBOX_MAX_WORLD || rank < 0 || rank >= world)
+      fail(IGM_INVALID_ARGUMENT, "mbox_create: rank / world out of range");
+    if (max_words < 1 || max_words > IGM_MBOX_MAX_WORDS) fail(IGM_INVALID_ARGUMENT, "mbox_create: max_words out of range");
+    auto m = std::make_unique<igm_mbox>();
+    m->device = c->device;
+    m->rank = rank;
+    m->world = world;
+    m->max_words = max_words;
+    const size_t bytes = sizeof(ulonglong2) * 2 * world * max_words;
+    // cudaMalloc (not a pool allocation): the buffer is exported over CUDA IPC
+    ck(cudaMalloc(reinterpret_cast<void**>(&m->local), bytes), "mbox_create");
+    ck(cudaMemset(m->local, 0, bytes), "mbox_create");
+    ck(cudaMalloc(reinterpret_cast<void**>(&m->d_err), sizeof(int)), "mbox_create");
+    ck(cudaMemset(m->d_err, 0, sizeof(int)), "mbox_create");
+    m->peer[rank] = m->local;
+    m->connected = world == 1;
+    if (const char* e = std::getenv("IGM_MBOX_TIMEOUT_MS")) {
+      const long long ms = std::atoll(e);
+      if (ms > 0) m->timeout_ns = static_cast<unsigned long long>(ms) * 1000000ull;
+    }
+    *out = m.release();
+  });
+}
+
+void igm_mbox_free(igm_mbox* m) {
+  if (!m) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(m->device);
+  for (int p = 0; p < m->world; ++p)
+    if (m->ipc[p] && m->peer[p]) cudaIpcCloseMemHandle(m->peer[p]);
+  cudaFree(m->local);
+  cudaFree(m->d_err);
+  cudaSetDevice(prev);
+  delete m;
+}
+
+igm_status igm_mbox_handle(igm_mbox* m, unsigned char handle[64]) {
+  return guarded([&] {
+    if (!m || !handle) fail(IGM_INVALID_ARGUMENT, "mbox_handle: null argument");
+    cudaIpcMemHandle_t h;
+    ck(cudaIpcGetMemHandle(&h, m->local), "mbox_handle");
+    std::memcpy(handle, &h, 64);
+  });
+}
+
+igm_status igm_mbox_connect_ipc(igm_mbox* m, const unsigned char* handles) {
+  return guarded([&] {
+    if (!m || !handles) fail(IGM_INVALID_ARGUMENT, "mbox_connect_ipc: null argument");
+    ck(cudaSetDevice(m->device), "cudaSetDevice");
+    for (int p = 0; p < m->world; ++p) {
+      if (p == m->rank || m->peer[p]) continue;
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, handles + 64 * static_cast<size_t>(p), 64);
+      void* q = nullptr;
+      ck(cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess), "mbox_connect_ipc");
+      m->peer[p] = static_cast<ulonglong2*>(q);
+      m->ipc[p] = true;
+    }
+    m->connected = true;
+  });
+}
+
+igm_status igm_mbox_connect_local(igm_mbox* m, igm_mbox* const* all) {
+  return guarded([&] {
+    if (!m || !all) fail(IGM_INVALID_ARGUMENT, "mbox_connect_local: null argument");
+    ck(cudaSetDevice(m->device), "cudaSetDevice");
+    for (int p = 0; p < m->world; ++p) {
+      const igm_mbox* o = all[p];
+      if (!o || o->world != m->world || o->rank != p || o->max_words != m->max_words)
+        fail(IGM_INVALID_ARGUMENT, "mbox_connect_local: mailbox list does not match the world");
+      if (o->device != m->device) {
+        int can = 0;
+        ck(cudaDeviceCanAccessPeer(&can, m->device, o->device), "peer access");
+        if (!can) fail(IGM_CUDA_ERROR, "mbox_connect_local: no peer access between the devices");
+        const cudaError_t e = cudaDeviceEnablePeerAccess(o->device, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else ck(e, "peer access");
+      }
+      m->peer[p] = o->local;
+    }
+    m->connected = true;
+  });
+}
+
+igm_status igm_mbox_publish(igm_ctx* c, igm_mbox* m, const uint64_t* words, int n) {
+  return guarded([&] {
+    mbox_need(c, m, words, n);
+    mbox_publish(c, m, words, n);
+  });
+}
+
+igm_status igm_mbox_collect(igm_ctx* c, igm_mbox* m, uint64_t* words, int n, int op) {
+  return guarded([&] {
+    mbox_need(c, m, words, n);
+    if (op != IGM_MBOX_SUM && op != IGM_MBOX_MAX) fail(IGM_INVALID_ARGUMENT, "mbox: unknown reduction");
+    mbox_collect(c, m, words, n, op);
+  });
+}
+
+igm_status igm_mbox_allreduce(igm_ctx* c, igm_mbox* m, uint64_t* words, int n, int op) {
+  return guarded([&] {
+    mbox_need(c, m, words, std::min(n, m ? m->max_words : 0));
+    if (n < 0) fail(IGM_INVALID_ARGUMENT, "mbox: word count out of range");
+    if (op != IGM_MBOX_SUM && op != IGM_MBOX_MAX) fail(IGM_INVALID_ARGUMENT, "mbox: unknown reduction");
+    if (m->world == 1) return;
+    for (int o = 0; o < n; o += m->max_words) {
+      const int k = std::min(m->max_words, n - o);
+      mbox_publish(c, m, words + o, k);
+      mbox_collect(c, m, words + o, k, op);
+    }
+  });
+}
+
+igm_status igm_mbox_status(igm_ctx* c, igm_mbox* m) {
+  return guarded([&] {
+    need_ctx(c);
+    if (!m) fail(IGM_INVALID_ARGUMENT, "mbox: null mailbox");
+    ck(cudaStreamSynchronize(c->stream), "mbox_status");
+    int e = 0;
+    ck(cudaMemcpy(&e, m->d_err, sizeof(int), cudaMemcpyDeviceToHost), "mbox_status");
+    if (e) fail(IGM_CUDA_ERROR, "mbox: a reduction timed out waiting for a peer rank");
+  });
+}
+
 igm_status igm_dc_mgs_pass(igm_ctx* c, igm_dstate* d, int64_t n, int j, int i, int64_t* w, const int64_t* vprev,
                            const int64_t* vcur, int f, const igm_shifts* sh, int checked) {
   return guarded([&] {

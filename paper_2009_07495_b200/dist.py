@@ -265,6 +265,45 @@ class CudaSlabBackend:
                 1 if checked else 0, None if zimp is None else C.c_void_p(zimp),
                 None if zexp is None else C.c_void_p(zexp), kexp, C.c_uint64(epoch))
 
+    # ---- one-shot P2P mailbox reductions (igm_mbox_*): the per-pass sums
+    def mbox_auto(self, dist, group=None) -> bool:
+        """mailboxes are mapped between processes with CUDA IPC: one process
+        per GPU (NCCL ranks); IGM_DIST_MBOX=0 keeps torch.distributed"""
+        import os
+        if os.environ.get("IGM_DIST_MBOX", "1") == "0" or not hasattr(dist, "get_backend"):
+            return False
+        try:
+            return dist.get_backend(group) == "nccl"
+        except Exception:
+            return False
+
+    def mbox_for(self, slab, comm, max_words=2048):
+        """this rank's connected mailbox (cached): the IPC handles travel in
+        one all_reduce of a zero-padded (world, 8) int64 table"""
+        import ctypes as C
+        cache = self.__dict__.setdefault("_mboxes", {})
+        key = (slab.rank, slab.world, max_words)
+        if key in cache:
+            return cache[key]
+        mb = C.c_void_p()
+        self._c("igm_mbox_create", slab.rank, slab.world, max_words, C.byref(mb))
+        h = (C.c_ubyte * 64)()
+        self.igm._check(self.igm.lib().igm_mbox_handle(mb, h))
+        mine = np.zeros((slab.world, 8), dtype=np.int64)
+        mine[slab.rank] = np.frombuffer(bytes(h), dtype=np.int64)
+        allh = self.host_i64(mine.ravel().tolist())
+        comm.d.all_reduce(allh, op=comm.d.ReduceOp.SUM, group=comm.g)
+        raw = allh.cpu().numpy().astype(np.int64).tobytes()
+        self.igm._check(self.igm.lib().igm_mbox_connect_ipc(mb, (C.c_ubyte * len(raw)).from_buffer_copy(raw)))
+        cache[key] = mb
+        return mb
+
+    def mbox_allreduce(self, mb, t, op):
+        self._c("igm_mbox_allreduce", mb, self._p(t), int(t.numel()), op)
+
+    def mbox_status(self, mb):
+        self._c("igm_mbox_status", mb)
+
     def encode(self, st, r0, v0, f):
         self._c("igm_dc_encode", st.h, int(r0.numel()), self._p(r0), self._p(v0), f)
 
@@ -464,17 +503,39 @@ class ShardedReport:
 class _Comm:
     """The rank's exchanges (torch.distributed: NCCL on GPUs, gloo on CPU)."""
 
-    def __init__(self, slab: Slab, dist, group=None):
+    def __init__(self, slab: Slab, dist, group=None, be=None, mbox=None):
+        """mbox: reduce the small int64 sums through the library's P2P
+        mailboxes (igm_mbox_*) instead of torch.distributed -- None: when
+        the backend can (one process per GPU), False: never."""
         self.s, self.d, self.g = slab, dist, group
         self.rank, self.world = slab.rank, slab.world
+        self.be, self.mb = be, None
+        if (self.world > 1 and mbox is not False and be is not None and hasattr(be, "mbox_for")
+                and (mbox is True or be.mbox_auto(dist, group))):
+            self.mb = be.mbox_for(slab, self)
+
+    def _native(self, t) -> bool:
+        return (self.mb is not None and getattr(t, "is_cuda", False) and t.dtype == self.be._torch.int64
+                and t.is_contiguous())
 
     def sum_(self, t):
         if self.world > 1:
-            self.d.all_reduce(t, op=self.d.ReduceOp.SUM, group=self.g)
+            if self._native(t):
+                self.be.mbox_allreduce(self.mb, t, 0)
+            else:
+                self.d.all_reduce(t, op=self.d.ReduceOp.SUM, group=self.g)
 
     def max_(self, t):
         if self.world > 1:
-            self.d.all_reduce(t, op=self.d.ReduceOp.MAX, group=self.g)
+            if self._native(t):
+                self.be.mbox_allreduce(self.mb, t, 1)
+            else:
+                self.d.all_reduce(t, op=self.d.ReduceOp.MAX, group=self.g)
+
+    def check(self):
+        """raises when a mailbox reduction gave up waiting for a peer"""
+        if self.mb is not None:
+            self.be.mbox_status(self.mb)
 
     def send(self, t, dst):
         self.d.send(t.contiguous(), dst, group=self.g)
@@ -539,9 +600,10 @@ class ZPipe:
             mine[rank, 0] = be.pipe_handle(self.imp_fwd)
         if self.imp_bwd is not None:
             mine[rank, 1] = be.pipe_handle(self.imp_bwd)
-        allh = be.host_i64(mine.ravel().tolist())
-        comm.sum_(allh)
-        allh = allh.cpu().numpy().reshape(world, 2, 8)
+        with be.stream():
+            allh = be.host_i64(mine.ravel().tolist())
+            comm.sum_(allh)
+            allh = allh.cpu().numpy().reshape(world, 2, 8)
         self.exp_fwd = be.pipe_open(allh[rank + 1, 0]) if rank < world - 1 else None
         self.exp_bwd = be.pipe_open(allh[rank - 1, 1]) if rank > 0 else None
         self.kexp_fwd, self.kexp_bwd = self.planes(slab)
@@ -566,10 +628,11 @@ def _pipe_for(be, slab: Slab, pre, comm, dist, group, pipe):
         return None
     if pipe is None and not be.pipe_auto(dist, group):
         return None
-    bad = be.host_i64([0 if be.pipe_capable(pre, slab) else 1])
-    comm.max_(bad)
-    if int(bad[0]):
-        return None
+    with be.stream():
+        bad = be.host_i64([0 if be.pipe_capable(pre, slab) else 1])
+        comm.max_(bad)
+        if int(bad[0]):
+            return None
     cache = be.__dict__.setdefault("_zpipes", {})
     key = (slab.rank, slab.world, slab.z0, slab.z1, slab.plane, slab.nplanes)
     if key not in cache:
@@ -578,7 +641,7 @@ def _pipe_for(be, slab: Slab, pre, comm, dist, group, pipe):
 
 
 def solve_sharded(be, slab: Slab, mats: dict, b_own, cfg, dist, group=None, s_schedule=None,
-                  pipe=None):
+                  pipe=None, mbox=None):
     """solve() (refine.cpp:21-106, fixed-point engine) on this rank's rows.
 
     be:   rank-local backend (CudaSlabBackend: the product's kernels through
@@ -589,8 +652,11 @@ def solve_sharded(be, slab: Slab, mats: dict, b_own, cfg, dist, group=None, s_sc
           max_refinements, m, frac_bits, s, checked, shifts).
     pipe: stream the integer substitutions' boundary planes pencil by pencil
           (ZPipe) -- None: when the backend and every rank can, False: relay.
+    mbox: sum the per-pass accumulators / counters through the library's P2P
+          mailboxes (igm_mbox_*) -- None: when one process drives each GPU
+          (NCCL ranks), False: torch.distributed all_reduce.
     Returns (x_own, ShardedReport); every rank returns the same report."""
-    comm = _Comm(slab, dist, group)
+    comm = _Comm(slab, dist, group, be, mbox)
     be.sync()  # inputs produced on other streams are complete
     n, nx, P = slab.n_own, slab.next_, slab.plane
     o0, o1 = slab.own0, slab.own1
@@ -657,9 +723,11 @@ def solve_sharded(be, slab: Slab, mats: dict, b_own, cfg, dist, group=None, s_sc
             info = be.fetch(st)
         except (ArithmeticError, ValueError, RuntimeError, OverflowError) as e:
             err, info = e, None
-        code = be.host_i64([0 if err is None else _err_code(err)])
-        comm.max_(code)
-        c = int(code[0])
+        with be.stream():
+            code = be.host_i64([0 if err is None else _err_code(err)])
+            comm.max_(code)
+            c = int(code[0])
+        comm.check()
         if c:
             if err is not None:
                 raise err

@@ -948,6 +948,96 @@ def test_piped_substitution_protocol(gpu, oracle, g, world):
                     gpu.lib().igm_dev_free(C.c_void_p(R[k]))
 
 
+@pytest.mark.parametrize("world,nwords", [(2, 3), (3, 40), (8, 3), (5, 1200)])
+def test_mailbox_allreduce_protocol(gpu, world, nwords):
+    """igm_mbox_*: the one-shot P2P mailbox reduction of the partitioned
+    solve's per-pass accumulators (fx_dot / fx_norm wrapping sums,
+    fxp.cpp:49-86).  The ranks share this GPU (mailboxes
+    connected as same-process peers), so each reduction is run as its two
+    halves -- every rank publishes, then every rank collects -- and no kernel
+    ever waits on another.  Result on every rank == the wrapping u64 sum /
+    the signed int64 max over ranks, over several sequence numbers (a stale
+    word of reduction k-2 in the same parity slot must not satisfy k) and
+    through the chunked igm_mbox_allreduce of a single-rank world."""
+    import ctypes as C
+    import torch
+    L = gpu.lib()
+    devs = [gpu.Device(0) for _ in range(world)]
+    max_words = 512
+    boxes = []
+    for r in range(world):
+        mb = C.c_void_p()
+        gpu._check(L.igm_mbox_create(devs[r].h, r, world, max_words, C.byref(mb)))
+        boxes.append(mb)
+    try:
+        arr = (C.c_void_p * world)(*[b.value for b in boxes])
+        for r in range(world):
+            gpu._check(L.igm_mbox_connect_local(boxes[r], arr))
+        rng = np.random.default_rng(world * 1000 + nwords)
+        for it in range(5):
+            op = it % 2  # SUM, MAX, SUM, ...
+            host = rng.integers(-(1 << 63), (1 << 63) - 1, (world, nwords), dtype=np.int64, endpoint=True)
+            if it == 3:
+                host[:] = host[0]  # equal words from every rank (torn-word check must still pass)
+            want = host.view(np.uint64).sum(axis=0, dtype=np.uint64).view(np.int64) if op == 0 else host.max(axis=0)
+            t = [torch.from_numpy(host[r].copy()).cuda() for r in range(world)]
+            torch.cuda.synchronize()
+            for o in range(0, nwords, max_words):  # the chunks igm_mbox_allreduce would issue
+                k = min(max_words, nwords - o)
+                for r in range(world):
+                    gpu._check(L.igm_mbox_publish(devs[r].h, boxes[r], C.c_void_p(t[r][o:].data_ptr()), k))
+                for r in range(world):
+                    devs[r].synchronize()
+                for r in range(world):
+                    gpu._check(L.igm_mbox_collect(devs[r].h, boxes[r], C.c_void_p(t[r][o:].data_ptr()), k, op))
+            for r in range(world):
+                gpu._check(L.igm_mbox_status(devs[r].h, boxes[r]))
+                assert np.array_equal(t[r].cpu().numpy(), want), (it, r)
+        # a world of one: allreduce is the identity, any n
+        one = C.c_void_p()
+        gpu._check(L.igm_mbox_create(devs[0].h, 0, 1, 4, C.byref(one)))
+        x = torch.arange(10, dtype=torch.int64, device="cuda")
+        torch.cuda.synchronize()
+        gpu._check(L.igm_mbox_allreduce(devs[0].h, one, C.c_void_p(x.data_ptr()), 10, 0))
+        gpu._check(L.igm_mbox_status(devs[0].h, one))
+        assert x.cpu().tolist() == list(range(10))
+        L.igm_mbox_free(one)
+        # argument errors
+        assert L.igm_mbox_publish(devs[0].h, boxes[0], C.c_void_p(t[0].data_ptr()), max_words + 1) == 1
+        assert L.igm_mbox_collect(devs[0].h, boxes[0], C.c_void_p(t[0].data_ptr()), 1, 7) == 1
+    finally:
+        for b in boxes:
+            L.igm_mbox_free(b)
+
+
+def test_mailbox_timeout_reports(gpu, monkeypatch):
+    """a collect whose peer never publishes gives up and igm_mbox_status
+    reports IGM_CUDA_ERROR instead of hanging the stream"""
+    import ctypes as C
+    import torch
+    monkeypatch.setenv("IGM_MBOX_TIMEOUT_MS", "50")
+    L = gpu.lib()
+    devs = [gpu.Device(0) for _ in range(2)]
+    boxes = []
+    for r in range(2):
+        mb = C.c_void_p()
+        gpu._check(L.igm_mbox_create(devs[r].h, r, 2, 8, C.byref(mb)))
+        boxes.append(mb)
+    try:
+        arr = (C.c_void_p * 2)(*[b.value for b in boxes])
+        for r in range(2):
+            gpu._check(L.igm_mbox_connect_local(boxes[r], arr))
+        t = torch.ones(3, dtype=torch.int64, device="cuda")
+        torch.cuda.synchronize()
+        gpu._check(L.igm_mbox_publish(devs[0].h, boxes[0], C.c_void_p(t.data_ptr()), 3))
+        gpu._check(L.igm_mbox_collect(devs[0].h, boxes[0], C.c_void_p(t.data_ptr()), 3, 0))  # rank 1 silent
+        assert L.igm_mbox_status(devs[0].h, boxes[0]) == 6  # IGM_CUDA_ERROR
+        assert b"timed out" in L.igm_last_error()
+    finally:
+        for b in boxes:
+            L.igm_mbox_free(b)
+
+
 def test_fx_device_fast_paths(gpu):
     """The device fast paths of the scalar helpers (fx_core.cuh: FP64
     estimate + exact 128-bit remainder fix-ups) against exact integer
