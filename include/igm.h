@@ -479,6 +479,15 @@ igm_status igm_factorize_split_cast(int n, const int* row_ptr,
                                     int* u_row_ptr, int* u_col_idx,
                                     int64_t* u_vals, int* u_diag_pos);
 
+/* the same, also returning the merged L, U values of ilu.cpp:29-49 on A's
+ * pattern (lu_out: nnz doubles, may be NULL).  A z-slab rank factorises its
+ * own planes from the previous rank's last plane of merged U rows and hands
+ * its own last plane on (dist.slab_ilu_local). */
+igm_status igm_factorize_split_cast_lu(int n, const int* row_ptr, const int* col_idx, const double* vals,
+                                       int* l_row_ptr, int* l_col_idx, int64_t* l_vals, int* l_diag_pos,
+                                       int* u_row_ptr, int* u_col_idx, int64_t* u_vals, int* u_diag_pos,
+                                       double* lu_out);
+
 /* ---- device-side setup -------------------------- *
  * The same three functions on the GPU, bit-identical to the host versions
  * above (per-row / per-entry IEEE sequences in the reference's order; the
@@ -498,6 +507,12 @@ igm_status igm_factorize_split_cast_dev(igm_ctx* ctx, int n, const int* row_ptr,
                                         const double* vals, int* l_row_ptr, int* l_col_idx, int64_t* l_vals,
                                         int* l_diag_pos, int* u_row_ptr, int* u_col_idx, int64_t* u_vals,
                                         int* u_diag_pos);
+
+/* igm_factorize_split_cast_lu on the device (lu_out: host or device, may be NULL) */
+igm_status igm_factorize_split_cast_dev_lu(igm_ctx* ctx, int n, const int* row_ptr, const int* col_idx,
+                                           const double* vals, int* l_row_ptr, int* l_col_idx, int64_t* l_vals,
+                                           int* l_diag_pos, int* u_row_ptr, int* u_col_idx, int64_t* u_vals,
+                                           int* u_diag_pos, double* lu_out);
 
 #ifdef __cplusplus
 }

@@ -651,8 +651,9 @@ def build_split(vals, alpha_a: int, max_components: int):
     return comp[:nc.value].copy(), [int(a) for a in alphas[:nc.value]], bool(ex.value)
 
 
-def factorize_split_cast(row_ptr, col_idx, vals):
-    """split_cast(factorize_ilu0(A)) -> (lower, upper) tuples of (row_ptr, col_idx, vals, diag_pos)."""
+def factorize_split_cast(row_ptr, col_idx, vals, return_lu: bool = False):
+    """split_cast(factorize_ilu0(A)) -> (lower, upper) tuples of (row_ptr, col_idx, vals, diag_pos);
+    return_lu: also the merged L, U values on A's pattern (ilu.cpp:29-49)."""
     row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int32)
     col_idx = np.ascontiguousarray(col_idx, dtype=np.int32)
     vals = np.ascontiguousarray(vals, dtype=np.float64)
@@ -663,10 +664,12 @@ def factorize_split_cast(row_ptr, col_idx, vals):
     lv = np.zeros(nnz, np.int64); uv = np.zeros(nnz, np.int64)
     ldp = np.zeros(n, np.int32); udp = np.zeros(n, np.int32)
     p = lambda a: C.c_void_p(a.ctypes.data)
-    _check(lib().igm_factorize_split_cast(n, p(row_ptr), p(col_idx), p(vals), p(lrp), p(lci), p(lv), p(ldp),
-                                          p(urp), p(uci), p(uv), p(udp)))
+    lu = np.zeros(nnz, np.float64) if return_lu else None
+    _check(lib().igm_factorize_split_cast_lu(n, p(row_ptr), p(col_idx), p(vals), p(lrp), p(lci), p(lv), p(ldp),
+                                             p(urp), p(uci), p(uv), p(udp), p(lu) if return_lu else None))
     nl, nu = int(lrp[-1]), int(urp[-1])
-    return (lrp, lci[:nl].copy(), lv[:nl].copy(), ldp), (urp, uci[:nu].copy(), uv[:nu].copy(), udp)
+    out = (lrp, lci[:nl].copy(), lv[:nl].copy(), ldp), (urp, uci[:nu].copy(), uv[:nu].copy(), udp)
+    return out + (lu,) if return_lu else out
 
 
 # ---------------------------------------------------------------- device setup
@@ -713,9 +716,10 @@ def build_split_device(vals, alpha_a: int, max_components: int, device: Optional
     return comp[:k * nnz].reshape(k, nnz), [int(a) for a in alphas[:k]], bool(ex.value)
 
 
-def factorize_split_cast_device(row_ptr, col_idx, vals, device: Optional[Device] = None):
+def factorize_split_cast_device(row_ptr, col_idx, vals, device: Optional[Device] = None, return_lu: bool = False):
     """split_cast(factorize_ilu0(A)) on the device -> (lower, upper) tuples of
-    (row_ptr, col_idx, vals, diag_pos), trimmed to the factors' sizes."""
+    (row_ptr, col_idx, vals, diag_pos), trimmed to the factors' sizes;
+    return_lu: also the merged L, U values on A's pattern."""
     dev = _dev(device)
     n = (row_ptr.numel() if _is_torch(row_ptr) else len(row_ptr)) - 1
     nnz = col_idx.numel() if _is_torch(col_idx) else len(col_idx)
@@ -727,7 +731,11 @@ def factorize_split_cast_device(row_ptr, col_idx, vals, device: Optional[Device]
     rp, k1 = _vp(row_ptr, np.int32)
     ci, k2 = _vp(col_idx, np.int32)
     v, k3 = _vp(vals, np.float64)
-    _check(lib().igm_factorize_split_cast_dev(dev.h, n, rp, ci, v, *ptrs))
+    lu = _alloc_like(vals, nnz, np.float64) if return_lu else None
+    plu = None if lu is None else (C.c_void_p(lu.ctypes.data) if isinstance(lu, np.ndarray)
+                                   else C.c_void_p(lu.data_ptr()))
+    _check(lib().igm_factorize_split_cast_dev_lu(dev.h, n, rp, ci, v, *ptrs, plu))
     lrp, lci, lv, ldp, urp, uci, uv, udp = bufs
     nl, nu = int(lrp[-1]), int(urp[-1])
-    return (lrp, lci[:nl], lv[:nl], ldp), (urp, uci[:nu], uv[:nu], udp)
+    out = (lrp, lci[:nl], lv[:nl], ldp), (urp, uci[:nu], uv[:nu], udp)
+    return out + (lu,) if return_lu else out

@@ -216,6 +216,8 @@ SIGNATURES = [
     ("igm_build_split", C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
                                   C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("igm_factorize_split_cast", C.c_int, [C.c_int] + [C.c_void_p] * 11),
+    ("igm_factorize_split_cast_lu", C.c_int, [C.c_int] + [C.c_void_p] * 12),
+    ("igm_factorize_split_cast_dev_lu", C.c_int, [C.c_void_p, C.c_int] + [C.c_void_p] * 12),
 ]
 
 _lib = None

@@ -1898,6 +1898,13 @@ igm_status igm_build_split_dev(igm_ctx* c, int nnz, const double* vals, int alph
 igm_status igm_factorize_split_cast_dev(igm_ctx* c, int n, const int* rp_, const int* ci_, const double* vals,
                                         int* lrp_o, int* lci_o, int64_t* lv_o, int* ldp_o, int* urp_o, int* uci_o,
                                         int64_t* uv_o, int* udp_o) {
+  return igm_factorize_split_cast_dev_lu(c, n, rp_, ci_, vals, lrp_o, lci_o, lv_o, ldp_o, urp_o, uci_o, uv_o, udp_o,
+                                         nullptr);
+}
+
+igm_status igm_factorize_split_cast_dev_lu(igm_ctx* c, int n, const int* rp_, const int* ci_, const double* vals,
+                                           int* lrp_o, int* lci_o, int64_t* lv_o, int* ldp_o, int* urp_o, int* uci_o,
+                                           int64_t* uv_o, int* udp_o, double* lu_o) {
   return guarded([&] {
     need_ctx(c);
     if (n < 0 || !rp_) fail(IGM_INVALID_ARGUMENT, "factorize_ilu0: bad arguments");
@@ -1965,6 +1972,8 @@ igm_status igm_factorize_split_cast_dev(igm_ctx* c, int n, const int* rp_, const
     ErrRow e(st);
     launch_split_cast(st, n, rp.d, ci.d, diag, lu, lrp.d, urp.d, lci.d, lv.d, ldp.d, uci.d, uv.d, udp.d, e.d);
     const int bad = e.get(st);
+    if (lu_o && nnz)  // the merged factors (cudaMemcpyDefault: lu_o may be host or device)
+      ck(cudaMemcpy(lu_o, lu, sizeof(double) * nnz, cudaMemcpyDefault), "lu out");
     cleanup();
     if (bad != INT_MAX)
       fail(IGM_RUNTIME_ERROR, "split_cast: diagonal entry of row " + std::to_string(bad) +

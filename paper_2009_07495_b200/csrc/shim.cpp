@@ -576,7 +576,16 @@ CsrMatrixF reconstruct_fp(const SplitMatrix& m, int s) {
 // ===========================================================================
 // ilu (ilu.hpp): factorisation on the host, substitutions on the GPU
 
-FpIluFactors factorize_ilu0(const CsrMatrixF& a) {
+namespace {
+FpIluFactors ilu0_impl(const CsrMatrixF& a, double* merged_out);
+}
+FpIluFactors factorize_ilu0(const CsrMatrixF& a) { return ilu0_impl(a, nullptr); }
+
+namespace {
+// merged_out (nnz doubles, may be null): the merged L\U values on A's pattern
+// before the split below (a z-slab rank hands its last plane's U rows to the
+// next rank, dist.slab_ilu_local)
+FpIluFactors ilu0_impl(const CsrMatrixF& a, double* merged_out) {
   const int n = a.n;
   std::vector<int> dpos(static_cast<std::size_t>(n), -1);
   for (int i = 0; i < n; ++i)
@@ -602,6 +611,7 @@ FpIluFactors factorize_ilu0(const CsrMatrixF& a) {
     if (lu[dpos[i]] == 0.0) throw std::runtime_error("factorize_ilu0: zero pivot in row " + std::to_string(i));
     for (int k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) slot[a.col_idx[k]] = -1;
   }
+  if (merged_out) std::copy(lu.begin(), lu.end(), merged_out);
   FpIluFactors f;
   f.diag.resize(static_cast<std::size_t>(n));
   f.lower.n = f.upper.n = n;
@@ -626,6 +636,7 @@ FpIluFactors factorize_ilu0(const CsrMatrixF& a) {
   }
   return f;
 }
+}  // namespace
 
 IluFactors split_cast(const FpIluFactors& f) {
   const int n = f.lower.n;
@@ -905,13 +916,19 @@ igm_status setup_guard(F&& fn) {
 extern "C" igm_status igm_factorize_split_cast(int n, const int* rp, const int* ci, const double* vals,
                                                int* lrp, int* lci, int64_t* lv, int* ldp, int* urp,
                                                int* uci, int64_t* uv, int* udp) {
+  return igm_factorize_split_cast_lu(n, rp, ci, vals, lrp, lci, lv, ldp, urp, uci, uv, udp, nullptr);
+}
+
+extern "C" igm_status igm_factorize_split_cast_lu(int n, const int* rp, const int* ci, const double* vals,
+                                                  int* lrp, int* lci, int64_t* lv, int* ldp, int* urp,
+                                                  int* uci, int64_t* uv, int* udp, double* lu_out) {
   return setup_guard([&] {
     intgmres::CsrMatrixF a;
     a.n = n;
     a.row_ptr.assign(rp, rp + n + 1);
     a.col_idx.assign(ci, ci + rp[n]);
     a.vals.assign(vals, vals + rp[n]);
-    const intgmres::IluFactors g = intgmres::split_cast(intgmres::factorize_ilu0(a));
+    const intgmres::IluFactors g = intgmres::split_cast(intgmres::ilu0_impl(a, lu_out));
     std::copy(g.lower.row_ptr.begin(), g.lower.row_ptr.end(), lrp);
     std::copy(g.lower.col_idx.begin(), g.lower.col_idx.end(), lci);
     std::copy(g.lower.vals.begin(), g.lower.vals.end(), lv);

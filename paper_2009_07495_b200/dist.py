@@ -173,6 +173,22 @@ class CudaSlabBackend:
     def host_i64(self, vals):
         return self._torch.tensor(vals, dtype=self._torch.int64, device=f"cuda:{self.dev.index}")
 
+    def from_np(self, a):
+        return self._torch.from_numpy(a).to(f"cuda:{self.dev.index}")
+
+    def to_np(self, t):
+        return t.cpu().numpy()
+
+    # slab-local setup on the device (igm_*_dev: bit-identical to the host versions)
+    def row_scale(self, rp, ci, v, alpha_a):
+        return self.igm.row_scale_device(rp, ci, v, alpha_a, device=self.dev)
+
+    def build_split(self, vals, alpha_a, max_components):
+        return self.igm.build_split_device(vals, alpha_a, max_components, device=self.dev)
+
+    def factorize(self, rp, ci, vals):
+        return self.igm.factorize_split_cast_device(rp, ci, vals, device=self.dev, return_lu=True)
+
     def upload_rows(self, rp, ci, comp, alphas, fp_vals):
         """own rows x extended columns: SplitMatrix + CsrMatrixF (shared pattern)"""
         return (self.igm.SplitMatrix(rp, ci, comp, alphas, device=self.dev),
@@ -486,6 +502,120 @@ def shard_problem(be, slab: Slab, row_ptr, col_idx, comp, alphas, a_fp_vals, fac
     return dict(split=sp, csrf=af, ilu=ilu, ncomp=len(comp))
 
 
+# ---- slab-local setup ("generate and factorise slab-locally") --
+# A rank builds its rows, their scaling and the splitting's truncation layer
+# from its own planes alone.  ILU(0) (ilu.cpp:25-120) eliminates row i with
+# the rows j < i of its pattern, all within one plane below: the factors of a
+# slab need the finished U rows (merged values, diagonal included) of the
+# previous rank's last plane and nothing else.  So the factorisation is a
+# rank-ordered relay of one plane of doubles, and every rank runs the
+# unmodified factorisation on an extended matrix whose lower halo rows are
+# those finished U rows (no entry left of the diagonal: nothing to eliminate,
+# they pass through unchanged) and whose upper halo rows are unit rows.
+def _u_part(rp, ci, row0):
+    """mask of the entries on or right of the diagonal; rows are row0 + local index"""
+    rows = np.repeat(np.arange(len(rp) - 1, dtype=np.int64) + row0, np.diff(rp))
+    return np.asarray(ci, dtype=np.int64) >= rows
+
+
+def slab_ilu_local(slab: Slab, own, halo_pattern, lu_in, factorize):
+    """The rank's extended-square local integer factors -- array for array
+    what slab_factor() cuts out of the global split_cast(factorize_ilu0(A))
+    -- from its own rows only.
+
+    own:          (row_ptr, col_idx GLOBAL, scaled vals) of the rank's rows
+    halo_pattern: (row_ptr, col_idx GLOBAL) of plane z0-1's rows (None on rank 0)
+    lu_in:        merged factor values of that plane's U part (diagonal
+                  included), CSR order, from rank-1 (None on rank 0)
+    factorize:    (row_ptr, col_idx, vals) -> (lower, upper, merged values)
+    Returns (lower, upper, lu_out); lu_out = this rank's last plane in the
+    same form for rank+1 (None on the last rank)."""
+    P, o0, o1, nl = slab.plane, slab.own0, slab.own1, slab.next_
+    g0, _ = slab.global_rows
+    rp_o, ci_o, v_o = (np.asarray(a) for a in own)
+    cnt = np.ones(nl, dtype=np.int64)
+    cnt[o0:o1] = np.diff(rp_o)
+    if o0:
+        hrp, hci = (np.asarray(a) for a in halo_pattern)
+        keep = _u_part(hrp, hci, g0 - P)
+        cnt[:o0] = np.add.reduceat(keep.astype(np.int64), hrp[:-1].astype(np.int64))
+        if lu_in is None or len(lu_in) != int(keep.sum()):
+            raise ValueError("slab_ilu_local: the received plane does not match the pattern of plane z0-1")
+    rp = np.zeros(nl + 1, dtype=np.int64)
+    np.cumsum(cnt, out=rp[1:])
+    nnz = int(rp[-1])
+    ci = np.empty(nnz, dtype=np.int32)
+    v = np.empty(nnz, dtype=np.float64)
+    a, b = int(rp[o0]), int(rp[o1])
+    if o0:
+        ci[:a] = (hci[keep].astype(np.int64) - slab.h0).astype(np.int32)
+        v[:a] = lu_in
+    ci[a:b] = (ci_o.astype(np.int64) - slab.h0).astype(np.int32)
+    v[a:b] = v_o
+    up = np.arange(o1, nl, dtype=np.int64)
+    ci[b:] = up.astype(np.int32)
+    v[b:] = 1.0
+    lower, upper, lu = factorize(rp.astype(np.int32), ci, v)
+    lower, upper = [np.asarray(x) for x in lower], [np.asarray(x) for x in upper]
+    lu = np.asarray(lu)
+    lu_out = None
+    if slab.rank < slab.world - 1:
+        r0 = o1 - P
+        k0, k1 = int(rp[r0]), int(rp[o1])
+        lu_out = lu[k0:k1][_u_part(rp[r0:o1 + 1] - k0, ci[k0:k1], r0)].copy()
+    # halo rows become unit rows (what slab_factor stores): L's already hold
+    # the diagonal only; U's lower halo rows lose their off-diagonal entries
+    lrp, lci, lv, ldp = lower
+    lv = lv.copy()
+    lv[lrp[:o0]] = 1
+    urp, uci, uv, udp = (x.astype(np.int64) for x in upper)
+    if o0:
+        cut = int(urp[o0])
+        urp2 = np.concatenate([np.arange(o0, dtype=np.int64), urp[o0:] - cut + o0])
+        uci2 = np.concatenate([np.arange(o0, dtype=np.int64), uci[cut:]])
+        uv2 = np.concatenate([np.ones(o0, dtype=np.int64), uv[cut:]])
+        udp2 = np.concatenate([np.arange(o0, dtype=np.int64), udp[o0:] - cut + o0])
+        upper = (urp2.astype(np.int32), uci2.astype(np.int32), uv2.astype(np.int64), udp2.astype(np.int32))
+    else:
+        upper = (urp.astype(np.int32), uci.astype(np.int32), uv.astype(np.int64), udp.astype(np.int32))
+    return (lrp, lci, lv, ldp), upper, lu_out
+
+
+def setup_slab_local(be, slab: Slab, rows_fn, alpha_a: int, comm, ilu: bool = True) -> dict:
+    """solve_sharded's inputs built from the rank's own planes (no global
+    array on any rank): row_scale (split.cpp:61-79) and the truncation layer
+    of build_split (split.cpp:90-135; depth-0 splittings -- a deeper layer's
+    scale is a global max) are row local; split_cast(factorize_ilu0(A))
+    through the plane relay of slab_ilu_local.
+
+    rows_fn(z0, z1) -> (row_ptr, col_idx GLOBAL, vals) of planes [z0, z1)
+    be: backend with row_scale / build_split / factorize (device setup for
+        CudaSlabBackend) and the upload methods; comm: send_np / recv_np.
+    Returns solve_sharded's `mats` plus 'scale' (the own rows' row scaling,
+    for scale_rhs) and 'rows' (row_ptr, local col_idx, scaled vals)."""
+    rp, ci, v = rows_fn(slab.z0, slab.z1)
+    vals, scale = be.row_scale(rp, ci, v, alpha_a)
+    del v
+    comp, alphas, _ = be.build_split(vals, alpha_a, 1)
+    ci_loc = (np.asarray(ci, dtype=np.int64) - slab.h0).astype(np.int32)
+    if ci_loc.size and (ci_loc.min() < 0 or ci_loc.max() >= slab.next_):
+        raise ValueError("setup_slab_local: a row reaches beyond the one-plane halo")
+    sp, af = be.upload_rows(rp, ci_loc, np.atleast_2d(comp), alphas, vals)
+    fac = None
+    if ilu:
+        halo, lu_in = None, None
+        if slab.rank > 0:
+            hrp, hci, _ = rows_fn(slab.z0 - 1, slab.z0)
+            halo = (hrp, hci)
+            lu_in = comm.recv_np(int(_u_part(np.asarray(hrp), np.asarray(hci), (slab.z0 - 1) * slab.plane).sum()),
+                                 slab.rank - 1)
+        lower, upper, lu_out = slab_ilu_local(slab, (rp, ci, vals), halo, lu_in, be.factorize)
+        if lu_out is not None:
+            comm.send_np(lu_out, slab.rank + 1)
+        fac = be.upload_factors(lower, upper)
+    return dict(split=sp, csrf=af, ilu=fac, ncomp=1, scale=np.asarray(scale), rows=(rp, ci_loc, vals))
+
+
 @dataclass
 class ShardedReport:
     """SolveReport (refine.hpp:36-47) of a partitioned solve (identical on every rank)."""
@@ -549,6 +679,15 @@ class _Comm:
 
     def halo(self, own, ext):
         halo_exchange(self.s, own, ext, self.d, self.g)
+
+    def send_np(self, a, dst):
+        """a float64 host array to rank dst (setup relay)"""
+        self.d.send(self.be.from_np(np.ascontiguousarray(a, dtype=np.float64)), dst, group=self.g)
+
+    def recv_np(self, count, src):
+        t = self.be.zeros(count, "f64")
+        self.d.recv(t, src, group=self.g)
+        return self.be.to_np(t)
 
 
 def _validate_cycle(m: int, f: int, depth: int, ncomp: int, sh) -> None:

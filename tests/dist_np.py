@@ -92,6 +92,24 @@ class OracleSlabBackend:
     def host_i64(self, vals):
         return torch.tensor(vals, dtype=torch.int64)
 
+    def from_np(self, a):
+        return torch.from_numpy(a)
+
+    def to_np(self, t):
+        return t.numpy()
+
+    # slab-local setup: the oracle's row_scale / build_split; the factorisation
+    # with its merged values is the product's HOST setup function (no GPU)
+    def row_scale(self, rp, ci, v, alpha_a):
+        return self.O.row_scale(self.O.csrf(rp, ci, v), alpha_a)
+
+    def build_split(self, vals, alpha_a, max_components):
+        return self.O.build_split(vals, alpha_a, max_components)
+
+    def factorize(self, rp, ci, vals):
+        import paper_2009_07495_b200 as igm
+        return igm.factorize_split_cast(rp, ci, vals, return_lu=True)
+
     def upload_rows(self, rp, ci, comp, alphas, fp_vals):
         return (SimpleNamespace(sp=self.O.split(rp, ci, comp, alphas), ncomp=len(comp)),
                 self.O.csrf(rp, ci, fp_vals))

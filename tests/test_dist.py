@@ -133,7 +133,60 @@ def _problem(kind, g, oracle):
     return rp, ci, vals, comp, al, fac, b
 
 
-def _solve_worker(rank, world, port, kind, g, m, s, q, pipe=False):
+def _rows_fn(kind, g):
+    from workloads import gen
+    if kind == "27pt_ilu":
+        return lambda z0, z1: gen.stencil27_rows(g, 5, z0, z1)
+    return lambda z0, z1: gen.upwind_3d_rows(g, 20.0, z0, z1)
+
+
+def _local_problem(be, sl, kind, g, comm):
+    """the rank's inputs from its own planes only (dist.setup_slab_local)"""
+    from workloads import gen
+    mats = D.setup_slab_local(be, sl, _rows_fn(kind, g), 32, comm, ilu=True)
+    rp, ci_loc, _ = mats["rows"]
+    xs = gen.uniform(17, g ** 3)[sl.h0:sl.h0 + sl.next_]
+    _, _, v = _rows_fn(kind, g)(sl.z0, sl.z1)
+    return mats, gen.spmv_np(rp, ci_loc, v, xs) / mats["scale"]
+
+
+@pytest.mark.parametrize("kind,g", [("7pt_ilu", 7), ("27pt_ilu", 6)])
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+def test_slab_local_ilu_equals_global_cut(oracle, kind, g, world):
+    """dist.slab_ilu_local: every rank factorises its own planes from the
+    previous rank's last plane of merged U rows (a relay of one plane of
+    doubles) -- its extended-square integer factors are, array for array,
+    what slab_factor cuts out of the oracle's global
+    split_cast(factorize_ilu0(A)) (ilu.cpp:25-120); the own rows' scaling
+    and truncation layer equal the global ones' slices."""
+    from tests.dist_np import OracleSlabBackend
+    rp, ci, vals, comp, al, fac, b = _problem(kind, g, oracle)
+    be = OracleSlabBackend(oracle)
+    rows = _rows_fn(kind, g)
+    lu = None
+    for r in range(world):
+        sl = D.make_slab(g, g * g, r, world)
+        g0, g1 = sl.global_rows
+        a, e = int(rp[g0]), int(rp[g1])
+        orp, oci, ov = rows(sl.z0, sl.z1)
+        sv, sc = be.row_scale(orp, oci, ov, 32)
+        assert np.array_equal(sv, vals[a:e])
+        c1, a1, _ = be.build_split(sv, 32, 1)
+        assert np.array_equal(np.atleast_2d(c1)[0], np.atleast_2d(comp)[0][a:e]) and list(a1) == list(al)
+        halo = rows(sl.z0 - 1, sl.z0)[:2] if r > 0 else None
+        lower, upper, lu = D.slab_ilu_local(sl, (orp, oci, sv), halo, lu, be.factorize)
+        for got, want in ((lower, D.slab_factor(fac[0], sl)), (upper, D.slab_factor(fac[1], sl))):
+            for x, y in zip(got, want):
+                assert np.array_equal(np.asarray(x), np.asarray(y))
+        assert (lu is None) == (r == world - 1)
+    with pytest.raises(ValueError, match="does not match the pattern"):
+        sl = D.make_slab(g, g * g, 1, 2)
+        orp, oci, ov = rows(sl.z0, sl.z1)
+        D.slab_ilu_local(sl, (orp, oci, be.row_scale(orp, oci, ov, 32)[0]), rows(sl.z0 - 1, sl.z0)[:2],
+                         np.zeros(3), be.factorize)
+
+
+def _solve_worker(rank, world, port, kind, g, m, s, q, pipe=False, local=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -145,11 +198,14 @@ def _solve_worker(rank, world, port, kind, g, m, s, q, pipe=False):
         sl = D.make_slab(g, g * g, rank, world)
         be = OracleSlabBackend(O)
         be.pipe_emulate = pipe
-        mats = D.shard_problem(be, sl, rp, ci, comp, al, vals, fac)
         g0, g1 = sl.global_rows
+        if local:  # nothing global on any rank: the planes, their scaling, the ILU relay
+            mats, b_own = _local_problem(be, sl, kind, g, D._Comm(sl, dist, be=be))
+        else:
+            mats, b_own = D.shard_problem(be, sl, rp, ci, comp, al, vals, fac), b[g0:g1].copy()
         plan = igm.ShiftPlan.default_preconditioned(30) if fac is not None else igm.ShiftPlan.default_unpreconditioned(30)
         cfg = igm.RefineConfig(tol=1e-10, max_refinements=30, m=m, frac_bits=30, s=s, checked=True, shifts=plan)
-        x, rep = D.solve_sharded(be, sl, mats, torch.from_numpy(b[g0:g1].copy()), cfg, dist)
+        x, rep = D.solve_sharded(be, sl, mats, torch.from_numpy(b_own), cfg, dist)
         piped = sum(zp.calls for zp in be.__dict__.get("_zpipes", {}).values())
         parts = [None] * world
         dist.all_gather_object(parts, (g0, x.numpy().copy(), rep, piped))
@@ -161,22 +217,28 @@ def _solve_worker(rank, world, port, kind, g, m, s, q, pipe=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind,world,pipe", [("27pt_ilu", 2, False), ("27pt_ilu", 3, False), ("7pt_plain", 2, False),
-                                             ("7pt_ilu", 2, True), ("7pt_ilu", 3, True), ("27pt_ilu", 3, True)])
-def test_sharded_solve_matches_oracle(oracle, kind, world, pipe):
+@pytest.mark.parametrize("kind,world,pipe,local", [
+    ("27pt_ilu", 2, False, False), ("27pt_ilu", 3, False, False), ("7pt_plain", 2, False, False),
+    ("7pt_ilu", 2, True, False), ("7pt_ilu", 3, True, False), ("27pt_ilu", 3, True, False),
+    ("27pt_ilu", 3, False, True), ("7pt_ilu", 2, True, True)])
+def test_sharded_solve_matches_oracle(oracle, kind, world, pipe, local):
     """World 2/3 gloo run of dist.solve_sharded (halo planes, exact u64 pass
     sums, relayed norm2 chain, rank-pipelined global ILU) against the
     single-process oracle solve: every x word, the relative-residual history,
     the inner dimensions and the gammas bit-identical.  pipe: the integer
     substitutions hand the boundary plane over dist.ZPipe's word protocol
     (tagged one-plane buffers opened by handle, epochs per call; emulated
-    with shared-memory segments) instead of the NCCL/gloo plane relay."""
+    with shared-memory segments) instead of the NCCL/gloo plane relay.
+    local: every rank builds its inputs from its own planes
+    (dist.setup_slab_local: plane-range generator, local scaling, the ILU(0)
+    relay of one plane of merged U rows) instead of cutting global arrays."""
     g, m = 6, 8
     s = 0 if kind.endswith("_ilu") else 1
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_solve_worker, args=(r, world, port, kind, g, m, s, q, pipe)) for r in range(world)]
+    procs = [ctx.Process(target=_solve_worker, args=(r, world, port, kind, g, m, s, q, pipe, local))
+             for r in range(world)]
     for p in procs:
         p.start()
     parts = q.get(timeout=600)
@@ -204,7 +266,7 @@ def test_sharded_solve_matches_oracle(oracle, kind, world, pipe):
     assert np.array_equal(x, xo)
 
 
-def run_sharded_threads(oracle, make_backend, kind, g, m, s, world, to_dev=lambda t: t):
+def run_sharded_threads(oracle, make_backend, kind, g, m, s, world, to_dev=lambda t: t, local=False):
     """dist.solve_sharded on `world` in-process ranks (tests/thread_comm.py);
     returns (x, reports, problem)."""
     from tests.thread_comm import run_ranks
@@ -217,9 +279,12 @@ def run_sharded_threads(oracle, make_backend, kind, g, m, s, world, to_dev=lambd
     def rank_fn(rank, comm):
         be = make_backend(rank)
         sl = D.make_slab(g, g * g, rank, world)
-        mats = D.shard_problem(be, sl, rp, ci, comp, al, vals, fac)
         g0, g1 = sl.global_rows
-        x, rep = D.solve_sharded(be, sl, mats, to_dev(torch.from_numpy(b[g0:g1].copy())), cfg, comm)
+        if local:
+            mats, b_own = _local_problem(be, sl, kind, g, D._Comm(sl, comm, be=be, mbox=False))
+        else:
+            mats, b_own = D.shard_problem(be, sl, rp, ci, comp, al, vals, fac), b[g0:g1].copy()
+        x, rep = D.solve_sharded(be, sl, mats, to_dev(torch.from_numpy(b_own)), cfg, comm)
         return g0, x.cpu().numpy().copy(), rep
 
     parts = sorted(run_ranks(world, rank_fn), key=lambda t: t[0])

@@ -621,15 +621,19 @@ def test_cpp_experiment(gpu, reference, tmp_path):
             assert ours[-1].endswith("converged=yes") and refl[-1].endswith("converged=yes")
 
 
-@pytest.mark.parametrize("kind,g,world", [("27pt_ilu", 12, 1), ("27pt_ilu", 12, 3), ("7pt_plain", 10, 2),
-                                          ("7pt_ilu", 16, 2)])
-def test_sharded_solve_cuda_backend(gpu, oracle, kind, g, world):
+@pytest.mark.parametrize("kind,g,world,local", [("27pt_ilu", 12, 1, False), ("27pt_ilu", 12, 3, False),
+                                                ("7pt_plain", 10, 2, False), ("7pt_ilu", 16, 2, False),
+                                                ("27pt_ilu", 12, 3, True), ("7pt_ilu", 16, 2, True)])
+def test_sharded_solve_cuda_backend(gpu, oracle, kind, g, world, local):
     """dist.solve_sharded through the product kernels (igm_dc_* entries: rank
     local SpMV / MGS passes / replicated scalar step / vec_div / pipelined
     global ILU / relayed norm2 / residual) on `world` ranks sharing this GPU
     as threads with their own contexts and streams (exchanges are host copies:
     no kernel waits on another rank) == the single-process oracle solve, bit
-    for bit.  Multi-process gloo runs of the same driver: tests/test_dist.py."""
+    for bit.  Multi-process gloo runs of the same driver: tests/test_dist.py.
+    local: the ranks' inputs come from dist.setup_slab_local (own planes
+    only; device row_scale / build_split, the ILU(0) plane relay through
+    igm_factorize_split_cast_dev_lu)."""
     import torch
     from tests.test_dist import run_sharded_threads, check_sharded_vs_oracle
     from paper_2009_07495_b200 import dist as D
@@ -640,7 +644,8 @@ def test_sharded_solve_cuda_backend(gpu, oracle, kind, g, world):
         return D.CudaSlabBackend(gpu, devs[rank])
 
     m, s = 10, (0 if kind.endswith("_ilu") else 1)
-    x, reps, prob = run_sharded_threads(oracle, make_backend, kind, g, m, s, world, to_dev=lambda t: t.cuda())
+    x, reps, prob = run_sharded_threads(oracle, make_backend, kind, g, m, s, world, to_dev=lambda t: t.cuda(),
+                                        local=local)
     check_sharded_vs_oracle(oracle, x, reps, prob, m, s)
 
 

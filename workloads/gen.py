@@ -365,3 +365,66 @@ def random_band_fast(n: int, seed: int, band: int = 2, extra: int = 10):
     rs = np.bincount(rr, weights=np.abs(offd), minlength=n)
     offd[diag] = 1.2 * rs
     return rp, ci, offd
+
+
+# ---------------------------------------------------------------- plane-range generators
+# Rows of whole z-planes [z0, z1) of the global matrices, with GLOBAL column
+# indices, entry for entry equal to the rows of the whole-matrix generators: a
+# z-slab rank builds only its own rows (dist.setup_slab_local).
+def upwind_3d_rows(g: int, beta: float, z0: int, z1: int):
+    """rows of planes [z0, z1) of upwind_3d(g, beta): (row_ptr, col (global), val)"""
+    rp, ci, v, h0, own0, own1 = upwind_3d_slab(g, beta, z0, z1)
+    a = int(rp[own0])
+    return (rp[own0:own1 + 1] - a).astype(np.int32), (ci.astype(np.int64) + h0).astype(np.int32), v
+
+
+def stencil27_rows(g: int, seed: int, z0: int, z1: int):
+    """rows of planes [z0, z1) of stencil27(g, seed): (row_ptr, col (global), val).
+    The per-offset uniform streams are indexed by global row (SplitMix64 is
+    counter based), the diagonal's row sum accumulates in offset order as in
+    stencil27_lean."""
+    n, p = g ** 3, g * g
+    r = np.arange(z0 * p, z1 * p, dtype=np.int64)
+    no = len(r)
+    i, j, k = r % g, (r // g) % g, r // p
+    offs = [(di, dj, dk) for dk in (-1, 0, 1) for dj in (-1, 0, 1) for di in (-1, 0, 1)]
+
+    def ok(di, dj, dk):
+        m = np.ones(no, dtype=bool)
+        for c, d in ((i, di), (j, dj), (k, dk)):
+            if d < 0:
+                m &= c > 0
+            elif d > 0:
+                m &= c < g - 1
+        return m
+
+    counts = np.zeros(no, dtype=np.int64)
+    for o in offs:
+        counts += ok(*o)
+    row_ptr = np.zeros(no + 1, dtype=np.int64)
+    np.cumsum(counts, out=row_ptr[1:])
+    nnz = int(row_ptr[-1])
+    col = np.empty(nnz, dtype=np.int32)
+    val = np.empty(nnz, dtype=np.float64)
+    cur = row_ptr[:-1].copy()
+    rs = np.zeros(no)
+    dpos = None
+    for o, (di, dj, dk) in enumerate(offs):
+        idx = np.nonzero(ok(di, dj, dk))[0]
+        pos = cur[idx]
+        col[pos] = (r[idx] + (dk * p + dj * g + di)).astype(np.int32)
+        if (di, dj, dk) == (0, 0, 0):
+            val[pos] = 0.0
+            dpos = pos
+        else:
+            s = di + dj + dk
+            sig = 1.0 if s < 0 else (-1.0 if s > 0 else 0.0)
+            u = uniform(seed, no, 0.0, 1.0, offset=o * n + z0 * p)
+            v = -u[idx] * (1.0 + 0.1 * sig)
+            val[pos] = v
+            a = np.zeros(no)
+            a[idx] = np.abs(v)
+            rs += a
+        cur[idx] += 1
+    val[dpos] = 1.05 * rs
+    return row_ptr.astype(np.int32), col, val
