@@ -17,9 +17,15 @@ checked mode (the reference's default).  One step = one full solve from x = 0.
               /root/reference) on this host, one refinement cycle, 1 thread
 
 ``--impl reference`` times the reference's own CPU solver on the same config
-(one refinement cycle = 30 iterations per step).  For N > 1 (torchrun) every
-rank solves its own replica of the system (the refinement loop does not shard
-at this size: see DESIGN.md), scaling = weak, value = sum over ranks.
+(one refinement cycle = 30 iterations per step).
+
+For N > 1 (torchrun) the bench runs the PARTITIONED configs instead of
+replicas: value = iterations/s of ONE BASELINE config-4 solve (256^3 27-point
++ ILU(0)) row-block partitioned over the N GPUs (dist.solve_sharded: slab-
+local setup, halo planes over NCCL P2P, per-pass sums through the library's
+P2P mailboxes, global ILU hand-offs, x hashed against the reference golden),
+scaling = strong, and kernel_microbench = the config-5 call on N GPUs.  The
+1-GPU figure of that workload: `--gpus 1 --cfg4-sharded`.
 """
 from __future__ import annotations
 
@@ -406,6 +412,165 @@ def run_cfg5_sharded(args, igm, dev, local, rank, ws, g=400, k=30):
     }
 
 
+def run_cfg4_sharded(args, igm, dev, local, rank, ws, g=256, m=30):
+    """BASELINE config 4 (g^3 27-point + integer ILU(0), GMRES(30), refinement
+    to 1e-10, checked) as ONE solve row-block partitioned over the ws GPUs
+    (dist.solve_sharded): every rank builds its own planes only
+    (plane-range generator, device row scaling / truncation layer, the ILU(0)
+    plane relay -- dist.setup_slab_local), per step the halo planes move over
+    NCCL P2P, the MGS / norm accumulators are summed through the library's
+    P2P mailboxes (igm_mbox_*), the integer substitutions of the GLOBAL
+    factors hand their boundary planes on as whole planes (27-point factors;
+    7-point ones stream them pencil by pencil, dist.ZPipe), norm2 is one
+    rank-ordered FP64 chain.  Strong scaling: the global problem is the 1-GPU
+    config, and the gathered x (every word) is hashed against the reference
+    library's whole-solve golden at g = 256."""
+    import hashlib
+    import torch
+    import torch.distributed as dist
+    from paper_2009_07495_b200 import dist as D
+    t0 = time.time()
+    dvc = f"cuda:{local}"
+    sl = D.make_slab(g, g * g, rank, ws)
+    be = D.CudaSlabBackend(igm, dev)
+    comm = D._Comm(sl, dist, be=be)
+    seed = gen.SEED_BASE ^ 4
+    rows_fn = lambda z0, z1: gen.stencil27_rows(g, seed, z0, z1)
+    mats = D.setup_slab_local(be, sl, rows_fn, 32, comm, ilu=True)
+    rp, ci_loc, _ = mats["rows"]
+    _, _, v_own = rows_fn(sl.z0, sl.z1)  # unscaled rows: b = (A x*) / scale, the goldens' order
+    n = g ** 3
+    xs = gen.uniform(gen.SEED_BASE ^ 104, sl.next_, offset=sl.h0)
+    b_own = gen.spmv_np(rp, ci_loc, v_own, xs) / mats["scale"]
+    nnz_local = int(rp[-1])
+    del v_own, xs
+    mats.pop("rows")
+    hb = torch.from_numpy(b_own).pin_memory()
+    d_b = hb.to(dvc)
+    cfg = igm.RefineConfig(tol=1e-10, max_refinements=100, m=m, frac_bits=30,
+                           shifts=igm.ShiftPlan.default_preconditioned(30), checked=True)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+    x, rep = None, None
+    for _ in range(max(args.warmup, 1)):
+        x, rep = D.solve_sharded(be, sl, mats, d_b, cfg, dist)
+    stream = torch.cuda.ExternalStream(dev.stream, device=dvc)
+    torch.cuda.synchronize()
+    barrier(ws)
+    l0 = dev.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    its = 0
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            x, rep = D.solve_sharded(be, sl, mats, d_b, cfg, dist)
+            its += rep.total_inner_iterations
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = dev.launches - l0
+    ms = max_over_ranks(e0.elapsed_time(e1), ws)
+    # e2e: the rank's rows of b from pinned host memory in, its rows of x out, per step
+    hx = torch.empty(sl.n_own, dtype=torch.float64).pin_memory()
+    barrier(ws)
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_its = 0
+    f0.record(stream)
+    for _ in range(args.steps):
+        with be.stream():
+            d_b.copy_(hb, non_blocking=True)
+        x, r2 = D.solve_sharded(be, sl, mats, d_b, cfg, dist)
+        with be.stream():
+            hx.copy_(x, non_blocking=True)
+        e2e_its += r2.total_inner_iterations
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(f0.elapsed_time(f1), ws)
+    # the global x on rank 0, hashed against the reference's whole solve
+    x_own = x.contiguous()
+    parity = {"parity": None}
+    if ws > 1:
+        if rank == 0:
+            parts = [x_own.cpu().numpy()]
+            for r in range(1, ws):
+                z0, z1 = D.plane_split(g, ws)[r]
+                t = torch.empty((z1 - z0) * g * g, dtype=torch.float64, device=dvc)
+                dist.recv(t, r)
+                parts.append(t.cpu().numpy())
+            xg = np.concatenate(parts)
+        else:
+            dist.send(x_own, 0)
+            xg = None
+    else:
+        xg = x_own.cpu().numpy()
+    if xg is not None:
+        xh = hashlib.sha256(np.ascontiguousarray(xg).tobytes()).hexdigest()
+        parity = {"parity": None, "x_sha256": xh[:16], "why": "goldens exist for g = 256 only"}
+        try:
+            with open(os.path.join(ROOT, "tests", "golden", "full_goldens.json")) as f:
+                gold = json.load(f)["cfg4"]
+            if g == gold["g"]:
+                r = gold["solve"]["report"]
+                same = (rep.inner_dims == r["inner_dims"] and rep.relres_history == r["relres_history"]
+                        and rep.gamma_history == r["gamma_history"] and rep.overflow_total == r["overflow_total"])
+                parity = {"parity": bool(xh == gold["solve"]["x"] and same), "x_sha256": xh[:16],
+                          "golden_x_sha256": gold["solve"]["x"][:16], "report_equal": bool(same),
+                          "against": "reference library whole solve (tests/golden/full_goldens.json cfg4)"}
+        except (OSError, KeyError, ValueError) as exc:
+            parity["why"] = f"no golden: {exc}"
+    del mats, d_b
+    torch.cuda.empty_cache()
+    return {
+        "workload": f"cfg4: 3D 27-pt {g}^3 (n={n}), integer ILU(0), GMRES({m}), FP64 refinement to 1e-10, Q33.30, "
+                    f"checked; one solve on z-slabs over {ws} GPU(s) ({sl.z1 - sl.z0} planes on rank {rank})",
+        "parallelism": f"z-slab x{ws}", "scaling": "strong",
+        "value": its / (ms / 1e3), "unit": "iters/s", "ms_per_solve": ms / args.steps,
+        "iterations_per_solve": rep.total_inner_iterations, "refinements": rep.refinements,
+        "final_relres": rep.relres_history[-1], "overflows": rep.overflow_total,
+        "e2e": {"value": e2e_its / (e2e_ms / 1e3), "unit": "iters/s", "h2d_bytes_per_step": int(8 * n),
+                "d2h_bytes_per_step": int(8 * n)},
+        "gpu_launches": int(launches), "parity": parity, "clocks": clk.summary(),
+        "reductions": "igm_mbox (P2P mailboxes)" if comm.mb is not None else
+                      ("none (1 GPU)" if ws == 1 else "torch.distributed all_reduce"),
+        "rank0_local_nnz": nnz_local, "setup_s": round(setup_s, 1),
+    }
+
+
+def run_b200_sharded(args, ws, rank, local):
+    """--gpus N > 1: the partitioned configs (BASELINE configs 4 and 5), not
+    replicas of the 1-GPU config: value = iterations/s of ONE config-4 solve
+    on N GPUs (strong scaling), kernel_microbench = the config-5 call on N
+    GPUs.  The 1-GPU figure of the same workload: `--gpus 1 --cfg4-sharded`."""
+    import paper_2009_07495_b200 as igm
+    dev = igm.Device(local)
+    igm.Device._default = dev
+    c4 = run_cfg4_sharded(args, igm, dev, local, rank, ws, g=args.cfg4_grid)
+    log(f"[bench] cfg4 sharded: {c4}")
+    micro = None
+    if not args.no_cfg5:
+        try:
+            micro = run_cfg5_sharded(args, igm, dev, local, rank, ws)
+        except Exception as exc:
+            micro = {"error": repr(exc)}
+    if rank == 0:
+        line = {
+            "metric": "int-GMRES iters/s", "value": c4["value"], "unit": "iters/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": c4["ms_per_solve"],
+            "time_to_solution_s": c4["ms_per_solve"] / 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic (seeded SplitMix64 matrix and x*, b = A x*)",
+            "config": {"workload": c4["workload"], "refinements": c4["refinements"],
+                       "iterations_per_solve": c4["iterations_per_solve"], "final_relres": c4["final_relres"],
+                       "overflows": c4["overflows"], "parallelism": c4["parallelism"],
+                       "reductions": c4["reductions"],
+                       "l2": "inputs larger than L2 (matrix + ILU + basis ~ 19 GB over the ranks)",
+                       "note": "N > 1 runs BASELINE config 4 (the partitioned config); the N = 1 default is "
+                               "config 2, whose 1-GPU config-4 figure is `--gpus 1 --cfg4-sharded`"},
+            "gpu_launches": c4["gpu_launches"], "e2e": c4["e2e"], "parity": c4["parity"],
+            "kernel_microbench": micro, "clocks": c4["clocks"],
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
 # ----------------------------------------------------------------- e2e_cpp
 def run_e2e_cpp(args, rp, ci, v, bh):
     """The drop-in boundary timed as a reference user calls it: build/e2e_cpp
@@ -628,6 +793,14 @@ def run_b200(args, ws, rank, local):
         except Exception as exc:
             micro = {"error": repr(exc)}
         log(f"[bench] cfg5 microbench: {micro}")
+    if args.cfg4_sharded and ws == 1:
+        try:
+            c4 = run_cfg4_sharded(args, igm, dev, local, rank, ws, g=args.cfg4_grid)
+        except Exception as exc:
+            c4 = {"error": repr(exc)}
+        log(f"[bench] cfg4 through the sharded driver at 1 GPU: {c4}")
+        micro = micro if isinstance(micro, dict) else {}
+        micro["cfg4_sharded_driver_1gpu"] = c4
     if args.cfg5_sharded and ws == 1 and not args.no_cfg5:
         try:
             micro["sharded_driver_1gpu"] = run_cfg5_sharded(args, igm, dev, local, rank, ws)
@@ -683,6 +856,9 @@ def main():
     ap.add_argument("--no-cfg5", action="store_true", help="skip the config-5 kernel microbench")
     ap.add_argument("--no-e2e-cpp", action="store_true", help="skip the C++ drop-in API leg")
     ap.add_argument("--only-cfg5", action="store_true", help="run only the config-5 microbench (profiling)")
+    ap.add_argument("--cfg4-sharded", action="store_true",
+                    help="at 1 GPU, also run config 4 through the row-block partitioned solve driver")
+    ap.add_argument("--cfg4-grid", type=int, default=256, help="grid of the partitioned config-4 solve")
     ap.add_argument("--cfg5-sharded", action="store_true",
                     help="at 1 GPU, also run the row-block partitioned config-5 driver")
     args = ap.parse_args()
@@ -696,6 +872,8 @@ def main():
         igm.Device._default = dev
         print(json.dumps(run_cfg5(args, igm, dev, local)), flush=True)
         return 0
+    if ws > 1:
+        return run_b200_sharded(args, ws, rank, local)
     return run_b200(args, ws, rank, local)
 
 
