@@ -382,8 +382,9 @@ igm_status igm_dc_tri(igm_ctx* ctx, igm_dstate* d, const igm_ilu* f, int backwar
  * buffer (NULL: the halo rows' right-hand sides are in `in`); zexp: the
  * neighbour's buffer (NULL: nothing exported); kexp: the solve-order plane
  * exported; epoch: the same value on both ranks for one substitution.
- * IGM_INVALID_ARGUMENT when the rank-local factor is not a 7-point pencil
- * factor (the caller then relays whole planes). */
+ * Both pencil wavefronts stream: the 7-point one (k_tri_pencil2) and the
+ * 27-point one (k_tri27; BASELINE config 4).  IGM_INVALID_ARGUMENT when the
+ * rank-local factor is neither (the caller then relays whole planes). */
 igm_status igm_dc_tri_piped(igm_ctx* ctx, igm_dstate* d, const igm_ilu* f, int backward, const int64_t* in,
                             int64_t* out, int j, int checked, const void* zimp, void* zexp, int kexp,
                             uint64_t epoch);

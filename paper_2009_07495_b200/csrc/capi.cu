@@ -2210,7 +2210,7 @@ igm_status igm_dc_tri_piped(igm_ctx* c, igm_dstate* d, const igm_ilu* f, int bac
     const DevTri& t = backward ? f->upper : f->lower;
     if (!launch_tri_int_piped(c->stream, t, backward != 0, in, out, d->lcnt + j * kCntStride + K_PRECOND * OP_COUNT,
                               d->ctl, checked != 0, z))
-      fail(IGM_INVALID_ARGUMENT, "dc_tri_piped: the factor is not a 7-point pencil factor");
+      fail(IGM_INVALID_ARGUMENT, "dc_tri_piped: the factor is not a 7-point / 27-point pencil factor");
   });
 }
 

@@ -3511,14 +3511,17 @@ int pencil27_max_resident(int device) {
   cudaFuncSetAttribute(k_tri27<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
   cudaFuncSetAttribute(k_tri27<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
   cudaFuncSetAttribute(k_tri27<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-  int a = 0, b = 0, c = 0;
+  cudaFuncSetAttribute(k_tri27<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+  cudaFuncSetAttribute(k_tri27<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+  int a = 0, b = 0, c = 0, d = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_tri27<true>, kP27Threads, sm) != cudaSuccess ||
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_tri27<false>, kP27Threads, sm) != cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_tri27<false, true>, kP27Threads, sm) != cudaSuccess) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_tri27<false, true>, kP27Threads, sm) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d, k_tri27<true, false, true>, kP27Threads, sm) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
-  return std::min(std::min(a, b), c) * num_sms(device);
+  return std::min(std::min(a, b), std::min(c, d)) * num_sms(device);
 }
 
 // k_tri27's bricks wait on each other in both directions, so they must all
@@ -3526,7 +3529,7 @@ int pencil27_max_resident(int device) {
 // another context's kernels occupy the SMs).  Returns false when the launch
 // was refused; the caller then runs the generic wavefront.
 static bool pen27_launch(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out, const Ctl* ctl,
-                         bool checked, bool fp = false, const double* prescale = nullptr) {
+                         bool checked, bool fp = false, const double* prescale = nullptr, const PenZ* zp = nullptr) {
   P27Args a;
   a.gx = t.p27_gx;
   a.gy = t.p27_gy;
@@ -3548,6 +3551,14 @@ static bool pen27_launch(cudaStream_t st, const DevTri& t, bool backward, const 
   const void* fn = fp ? reinterpret_cast<const void*>(k_tri27<false, true>)
                       : (checked ? reinterpret_cast<const void*>(k_tri27<true>)
                                  : reinterpret_cast<const void*>(k_tri27<false>));
+  if (zp != nullptr && !fp) {  // z-slab hand-off: a separate instantiation
+    a.zimp = zp->imp;
+    a.zexp = zp->exp;
+    a.kexp = zp->kexp;
+    a.zepoch = zp->epoch;
+    fn = checked ? reinterpret_cast<const void*>(k_tri27<true, false, true>)
+                 : reinterpret_cast<const void*>(k_tri27<false, false, true>);
+  }
   const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(t.p27_nbricks), dim3(kP27Threads), args, sm, st);
   if (e == cudaErrorCooperativeLaunchTooLarge) {
     cudaGetLastError();
@@ -3557,15 +3568,17 @@ static bool pen27_launch(cudaStream_t st, const DevTri& t, bool backward, const 
 }
 
 // the rank-local substitution of a z-slab with its boundary plane streamed from
-// / to the neighbour ranks (pencil wavefront only); false when the factor is
-// not a 7-point pencil factor
+// / to the neighbour ranks (pencil wavefronts only); false when the factor is
+// neither a 7-point nor a 27-point pencil factor (or the 27-point kernel's
+// bricks cannot all be resident)
 bool launch_tri_int_piped(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out, u64* cnt,
                           const Ctl* ctl, bool checked, const PenZ& z) {
-  if (t.n == 0 || !t.pen) return false;
+  if (t.n == 0 || (!t.pen && !t.pen27)) return false;
   if (checked) cudaMemsetAsync(t.stats, 0, 2 * sizeof(u64), st);
   {
     ProfScope prof_(st, KC_TRI_INT);
-    pen_launch<false>(st, t, backward, y, out, ctl, checked, nullptr, &z);
+    if (t.pen) pen_launch<false>(st, t, backward, y, out, ctl, checked, nullptr, &z);
+    else if (!pen27_launch(st, t, backward, y, out, ctl, checked, false, nullptr, &z)) return false;
   }
   LAUNCH_CHECK();
   if (checked) {

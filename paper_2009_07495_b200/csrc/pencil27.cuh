@@ -109,6 +109,13 @@ struct P27Args {
   ulonglong2* xz;           // exported boundary values by solve-order row
   unsigned long long epoch;
   unsigned long long* stats;  // [max|y|, max|z|] bounds (checked mode)
+  // z-slab pipelining (PIPE instantiation; igm_dc_tri_piped, dist.ZPipe):
+  // plane 0's values arrive as (value, zepoch + natural idx) words in zimp,
+  // plane kexp's leave the same way into the neighbour rank's buffer zexp
+  const ulonglong2* zimp = nullptr;
+  ulonglong2* zexp = nullptr;
+  int kexp = -1;
+  unsigned long long zepoch = 0;
 };
 
 __device__ __forceinline__ void p27_ldg16(const ulonglong2* p, u64& v, u64& t) {
@@ -126,7 +133,7 @@ __device__ __forceinline__ void p27_lds16(unsigned a, u64& v, u64& t) {
 // entries in CSR order -- dependencies 0..12 for the lower factor, 12..0 for
 // the mirrored upper one -- every operation rounded on its own, absent
 // entries skipped, then acc / diag (the stream holds the diagonal as a double)
-template <bool CHECKED, bool FP = false>
+template <bool CHECKED, bool FP = false, bool PIPE = false>
 __global__ void __launch_bounds__(kP27Threads, 2) k_tri27(P27Args a, const i64* __restrict__ y, i64* __restrict__ out,
                                                           const int* stop, const int* err,
                                                           const double* prescale = nullptr) {
@@ -220,6 +227,17 @@ __global__ void __launch_bounds__(kP27Threads, 2) k_tri27(P27Args a, const i64* 
         f[12] = q3.x; info = q3.y;
       }
       if (k + 1 < gz) issue(k + 1);
+      if (PIPE && k == 0 && a.zimp != nullptr) {  // a unit halo row: its value is the neighbour rank's
+        const long long idx = a.mirror ? static_cast<long long>(a.gy - 1 - j) * a.gx + (a.gx - 1 - i)
+                                       : static_cast<long long>(j) * a.gx + i;
+        u64 zt;
+        do {
+          asm volatile("{ .reg .b128 x; ld.relaxed.sys.global.b128 x, [%2]; mov.b128 {%0, %1}, x; }"
+                       : "=l"(yv), "=l"(zt)
+                       : "l"(a.zimp + idx)
+                       : "memory");
+        } while (zt != a.zepoch + static_cast<u64>(idx));
+      }
       const u64 w0 = epoch ^ (static_cast<u64>(k + 1) * C), w1 = epoch ^ (static_cast<u64>(k) * C);  // tags of planes k, k-1
       const long long r = rb + k * plane;
       const int mask = info >> 9;
@@ -286,6 +304,13 @@ __global__ void __launch_bounds__(kP27Threads, 2) k_tri27(P27Args a, const i64* 
                      "l"(a.xz + r)
                      : "memory");
       out[a.mirror ? a.n - 1 - r : r] = z;
+      if (PIPE && k == a.kexp && a.zexp != nullptr) {  // the next rank's plane-0 value
+        const long long idx = a.mirror ? static_cast<long long>(a.gy - 1 - j) * a.gx + (a.gx - 1 - i)
+                                       : static_cast<long long>(j) * a.gx + i;
+        asm volatile("{ .reg .b128 x; mov.b128 x, {%1, %2}; st.relaxed.sys.global.b128 [%0], x; }" ::"l"(a.zexp + idx),
+                     "l"(static_cast<u64>(z)), "l"(a.zepoch + static_cast<u64>(idx))
+                     : "memory");
+      }
       if (CHECKED && !FP) {
         ymx |= yv ^ static_cast<u64>(static_cast<i64>(yv) >> 63);
         zmx |= static_cast<u64>(z ^ (z >> 63));

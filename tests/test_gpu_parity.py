@@ -880,13 +880,15 @@ def test_ilu_pencil27_wavefront(gpu, oracle, dims):
     assert np.array_equal(gpu.apply_inverse(G, y), gpu.apply_inverse(F, y))
 
 
-@pytest.mark.parametrize("g,world", [(16, 2), (24, 3), (40, 4)])
-def test_piped_substitution_protocol(gpu, oracle, g, world):
+@pytest.mark.parametrize("kind,g,world", [("7pt", 16, 2), ("7pt", 24, 3), ("7pt", 40, 4), ("27pt", 12, 2),
+                                          ("27pt", 20, 3), ("27pt", 33, 4)])
+def test_piped_substitution_protocol(gpu, oracle, kind, g, world):
     """igm_dc_tri_piped, the word protocol of the pipelined slab
     substitutions (dist.ZPipe): rank r's forward wavefront stores its last
     own plane as tagged words into rank r+1's import buffer and rank r+1's
     wavefront reads its halo plane from there; backward the same from r+1 to
-    r.  Here the ranks share this GPU, so they run strictly one after the
+    r; both pencil wavefronts (7-point k_tri_pencil2, 27-point k_tri27:
+    BASELINE config 4's factors).  Here the ranks share this GPU, so they run strictly one after the
     other (each launch completes before the next rank's starts: no kernel ever
     waits on another); the buffers are plain device pointers instead of IPC
     mappings.  Concatenated own rows == the global substitution pair of the
@@ -897,7 +899,7 @@ def test_piped_substitution_protocol(gpu, oracle, g, world):
     import torch
     from paper_2009_07495_b200 import dist as D
     from workloads import gen
-    rp, ci, v = gen.upwind_3d(g, 20.0)
+    rp, ci, v = gen.upwind_3d(g, 20.0) if kind == "7pt" else gen.stencil27(g, 5)
     n = len(rp) - 1
     vals, _ = oracle.row_scale(oracle.csrf(rp, ci, v), 32)
     lower, upper = oracle.factorize_split_cast(oracle.csrf(rp, ci, vals))
