@@ -1547,9 +1547,14 @@ __device__ __forceinline__ u64 ld_cg_u64(const u64* p) {
 // CTA instead of one per warp on a single hot line
 // pre: an optional [pre, pre + pre_bytes) range (this CTA's slice of the next
 // pass's basis vector) prefetched into L2 while the barrier is pending
+// SYNC_IN = false: the caller's threads have already met at a CTA barrier
+// after their last work of the phase (cta_reduce_add's), so thread 0 goes
+// straight to the arrival while the other warps are free until the closing
+// barrier (k_arnoldi2 issues the next basis slice's bulk copy there)
+template <bool SYNC_IN = true>
 __device__ __forceinline__ u64 grid_barrier(Ctl* ctl, unsigned target, const u64* fetch, u64* s_word,
                                             const void* pre = nullptr, unsigned pre_bytes = 0) {
-  __syncthreads();
+  if (SYNC_IN) __syncthreads();
   if (threadIdx.x == 0) {
     unsigned* p = &ctl->gbar;
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
@@ -2106,6 +2111,7 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
   __shared__ u64 s_word;
   __shared__ int s_vd[6];
   __shared__ __align__(8) unsigned long long s_bar[2];
+  __shared__ __align__(8) unsigned long long s_cbar[kArn2Q];  // chunk m of v_{i-1} consumed by every warp
   __shared__ u64 s_mx[2];
   if (cycle_over(ctl)) return;  // uniform: ctl is not written before the first barrier
   unsigned long long* ts = (g_arn_ts_j == j && threadIdx.x == 0) ? g_arn_ts + blockIdx.x * kArnTsSlots : nullptr;
@@ -2120,9 +2126,12 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
   const int tid = threadIdx.x;
   i64* buf[2] = {arn_sm, arn_sm + S};
   const unsigned bar0 = smem_u32(&s_bar[0]);
+  const unsigned cbar0 = smem_u32(&s_cbar[0]);
   if (tid == 0) {
     mbar_init_s(bar0, 1);
     mbar_init_s(bar0 + 8, 1);
+#pragma unroll
+    for (int m = 0; m < Q; ++m) mbar_init_s(cbar0 + 8u * m, T / 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -2141,6 +2150,36 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
   auto wait_buf = [&](int b) {
     mbar_wait_s(bar0 + 8u * b, ph[b]);
     ph[b] ^= 1u;
+  };
+  // Streaming refill: during pass i the slice of v_{i-1} is consumed chunk by
+  // chunk (chunk m = the quads [m T, (m+1) T), 16 KB: iteration m of every
+  // thread), and chunk m of v_{i+1} is copied into its place once every warp
+  // has arrived on the chunk's mbarrier -- the HBM stream of the basis then
+  // runs under the pass's arithmetic, not only under the grid barrier that
+  // follows (whose round trips it delays: 4.2 vs ~2 us, scripts/arn_ts.py).
+  // The issuing lane never sleeps on a chunk barrier inside the pass: it
+  // TESTS it and issues whatever is free; the rest goes out after the pass.
+  constexpr int kIssuer = T - 32;  // lane 0 of the last warp
+  auto chunk_free = [&](int c, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(cbar0 + 8u * c), "r"(parity)
+        : "memory");
+    return ok != 0;
+  };
+  auto issue_chunk = [&](int c, int b, const i64* v) {
+    // (no proxy fence: the chunk was only READ through the generic proxy, and
+    // those reads are ordered before this point by the warps' arrivals)
+    if (c == 0) {
+      if (cnt > 0) mbar_arrive_expect_tx_s(bar0 + 8u * b, static_cast<unsigned>(cnt * 8));
+      else mbar_arrive_s(bar0 + 8u * b);
+    }
+    const int q0 = c * T;
+    if (q0 < nq)
+      bulk_g2s_s(smem_u32(buf[b] + 4 * q0), v + lo + 4 * q0, static_cast<unsigned>(min(T, nq - q0)) * 32u,
+                 bar0 + 8u * b);
   };
   if (tid == 0) {
     fetch(0, basis);
@@ -2242,12 +2281,16 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
   };
   // ---- passes 1..j: axpy_{i-1} (v_{i-1} in buf[(i-1)&1]), dot_i (v_i in buf[i&1])
   for (int i = 1; i <= j; ++i) {
-    const i64 hs = h_of(grid_barrier(ctl, (++nbar) * G, accj + i - 1, &s_word));
+    const i64 hs = h_of(grid_barrier<false>(ctl, (++nbar) * G, accj + i - 1, &s_word));
     ARN_TS(4 * i - 1)
     wait_buf(i & 1);
     ARN_TS(4 * i)
     const i64* vp = buf[(i - 1) & 1];
     const i64* vc = buf[i & 1];
+    const bool refill = i + 1 <= j;  // v_{i+1} takes v_{i-1}'s place, chunk by chunk
+    const i64* vnext = basis + static_cast<long long>(i + 1) * n;
+    const unsigned cpar = static_cast<unsigned>(i - 1) & 1u;
+    int issued = 0;  // (issuer lane) chunks of v_{i+1} on their way
     ArnAcc A;
     auto pass = [&](auto ovf) {
 #pragma unroll
@@ -2263,6 +2306,10 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
             dot_term(wr[m][e], cq[e], A, ovf);
           }
         }
+        __syncwarp();  // the warp's reads of chunk m have been consumed
+        if ((tid & 31) == 0) mbar_arrive_s(cbar0 + 8u * m);
+        if (tid == kIssuer && refill)
+          while (issued < m && chunk_free(issued, cpar)) issue_chunk(issued++, (i - 1) & 1, vnext);
       }
     };
     if (CHECKED && certify(absu(hs), i == 1 ? V0 : vmx_me[i - 1], sh.dot_b1, shb(vmx_me[i], sh.dot_b2), true))
@@ -2277,12 +2324,20 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
     ARN_TS(4 * i + 1)
     cta_reduce_add<CHECKED, T>(A.sum, A.ahi, A.alo, accj + i, absj + 2 * i, red);
     ARN_TS(4 * i + 2)
-    // every thread is past its reads of v_{i-1}: its buffer takes v_{i+1}
-    if (tid == 0 && i + 1 <= j) fetch((i + 1) & 1, basis + static_cast<long long>(i + 1) * n);
+    // every thread is past its reads of v_{i-1} (the reduction's CTA barrier):
+    // its buffer takes v_{i+1}.  Issued by warp 1 while thread 0 runs the grid
+    // barrier: the issuing thread stays blocked ~2.3 us behind the bulk copy
+    // (scripts/arn_ts.py: 4.2 us per barrier with the copy issued on thread
+    // 0's path against 1.5-2.1 us without one), so it must not be the thread
+    // the barrier's arrival waits for.
+    // The chunks still held back go out here, after the reduction's CTA
+    // barrier (every chunk is free), while thread 0 runs the grid barrier.
+    if (tid == kIssuer && refill)
+      for (; issued < Q; ++issued) issue_chunk(issued, (i - 1) & 1, vnext);
   }
   // ---- axpy_j (v_j in buf[j&1]), then the norm sum of the orthogonalised w
   {
-    const i64 hs = h_of(grid_barrier(ctl, (++nbar) * G, accj + j, &s_word));
+    const i64 hs = h_of(grid_barrier<false>(ctl, (++nbar) * G, accj + j, &s_word));
     ARN_TS(4 * j + 3)
     const i64* vp = buf[j & 1];
     ArnAcc A;
