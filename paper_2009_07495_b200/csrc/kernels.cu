@@ -2243,6 +2243,12 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
   // ---- pass 0: w -> registers, dot_0 = <w, v_0>
   {
     ARN_TS(124)
+    // w's loads go out before the wait for v_0's slice: both arrive together
+#pragma unroll
+    for (int m = 0; m < Q; ++m) {
+      const int q = tid + m * T;
+      if (q < nq) ld_v4_nc(win + lo + 4 * q, wr[m]);
+    }
     wait_buf(0);
     ARN_TS(0)
     ArnAcc A;
@@ -2251,7 +2257,6 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
       const int q = tid + m * T;
       if (q < nq) {
         i64 cq[4];
-        ld_v4_nc(win + lo + 4 * q, wr[m]);
         lds_q(buf[0] + 4 * q, cq);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
