@@ -995,6 +995,7 @@ igm_status igm_upload_split(igm_ctx* c, int n, int nnz, const int* row_ptr, cons
     m->vals = dupload(comp_vals, static_cast<size_t>(ncomp) * nnz, c->stream);
     m->alphas = dupload(alphas, ncomp, c->stream);
     m->h_alphas = is_device_ptr(alphas) ? to_host(alphas, ncomp) : std::vector<int>(alphas, alphas + ncomp);
+    m->max_row = device_max_row(c->stream, n, m->row_ptr);
     ck(cudaStreamSynchronize(c->stream), "upload sync");
     *out = m.release();
   });

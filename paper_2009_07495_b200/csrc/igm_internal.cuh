@@ -72,6 +72,7 @@ struct DevSplit {
   std::vector<int> h_alphas;
   std::vector<int> h_row_ptr_hash;  // not used for identity, kept small
   int device = 0;
+  int max_row = 0;  // longest row (selects the staged SpMV for long rows)
 };
 
 struct DevCsrf {
@@ -176,6 +177,7 @@ struct ShiftsD {
   int dot_b1, dot_b2, axpy_b1, norm_b1, div_b1, div_b2, givens_b2, rot_b;
 };
 
+int device_max_row(cudaStream_t st, int n, const int* rp);
 void launch_spmv_int(cudaStream_t st, const DevSplit& m, int s, const i64* v,
                      i64* out, u64* cnt, const Ctl* ctl, bool checked);
 void launch_spmv_fp_split(cudaStream_t st, const DevSplit& m, int s,

@@ -174,6 +174,75 @@ __global__ void __launch_bounds__(256) k_spmv_int(int n, const int* __restrict__
   }
 }
 
+// K1, staged variant for long rows (27-point stencils: 324 B per row).  One
+// thread per row makes a warp touch 32 distant row segments per load, which
+// the L1 cannot hold until they are consumed (config 4: 0.45 of HBM).  Here a
+// warp owns a tile of 32 consecutive rows = one contiguous run of entries:
+// it loads the run's (value, column) pairs coalesced, multiplies, parks the
+// products in shared memory, and every lane then sums ITS row's products in
+// CSR order -- the reference's per-row order (split.cpp:137-157), so the
+// add-overflow events are the reference's too (wrapping sums are order-free,
+// the events are not).
+constexpr int kSpRows = 32, kSpMaxRow = 32, kSpWarps = 4;
+template <bool CHECKED>
+__global__ void __launch_bounds__(kSpWarps * 32) k_spmv_int_staged(int n, const int* __restrict__ rp,
+                                                                   const int* __restrict__ ci,
+                                                                   const i64* __restrict__ vals, long long nnz,
+                                                                   const int* __restrict__ alphas, int s,
+                                                                   const i64* __restrict__ v, i64* __restrict__ out,
+                                                                   u64* cnt, const Ctl* ctl) {
+  __shared__ i64 sm[kSpWarps][kSpRows * kSpMaxRow];
+  if (cycle_over(ctl)) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  i64* prod = sm[w];
+  u64 nmul = 0, nadd = 0;
+  const int ntiles = (n + kSpRows - 1) / kSpRows;
+  for (int tile = blockIdx.x * kSpWarps + w; tile < ntiles; tile += gridDim.x * kSpWarps) {
+    const int row = tile * kSpRows + lane;
+    const bool live = row < n;
+    const int b = live ? rp[row] : 0, e = live ? rp[row + 1] : 0;
+    const int tb = __shfl_sync(0xffffffffu, b, 0);
+    const int te = __shfl_sync(0xffffffffu, e, min(kSpRows - 1, n - 1 - tile * kSpRows));
+    i64 o = 0;
+    for (int l = 0; l <= s; ++l) {
+      const i64* cv = vals + static_cast<long long>(l) * nnz;
+#pragma unroll 4
+      for (int k = tb + lane; k < te; k += 32) {
+        // the matrix streams through once: keep it out of the L1 lines the
+        // gathered vector entries (reused ~27 times) live in
+        const i64 a = __ldcs(cv + k);
+        const i64 x = __ldg(v + __ldcs(ci + k));
+        if (CHECKED) nmul += mul_ovf(a, x);
+        prod[k - tb] = wmul(a, x);
+      }
+      __syncwarp();
+      i64 acc = 0;
+      for (int k = b; k < e; ++k) {
+        const i64 p = prod[k - tb];
+        if (CHECKED) nadd += add_ovf(acc, p);
+        acc = wadd(acc, p);
+      }
+      const i64 d = asr(acc, alphas[l]);
+      if (CHECKED) nadd += add_ovf(o, d);
+      o = wadd(o, d);
+      __syncwarp();
+    }
+    if (live) out[row] = o;
+  }
+  if (CHECKED) {
+    bump(cnt, OP_MUL, nmul);
+    bump(cnt, OP_ADD, nadd);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_max_row(int n, const int* __restrict__ rp, int* out) {
+  int m = 0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) m = max(m, rp[r + 1] - rp[r]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
 // spmv_fp(SplitMatrix) (split.cpp:159-175) fused with r0 = b - A x0
 // (gmres_int.cpp:63-68); if b == nullptr, y = A x.
 __global__ void __launch_bounds__(256) k_spmv_fp_split(int n, const int* __restrict__ rp,
@@ -3094,6 +3163,23 @@ bool PerDevice::first(int device) {
 void launch_spmv_int(cudaStream_t st, const DevSplit& m, int s, const i64* v, i64* out, u64* cnt,
                      const Ctl* ctl, bool checked) {
   ProfScope prof_(st, KC_SPMV);
+  // long rows (mean >= 16, max <= 32 entries: 27-point stencils): the staged kernel
+  static const bool staged_on = [] {
+    const char* e = std::getenv("IGM_SPMV_STAGED");
+    return !(e && e[0] == '0');
+  }();
+  if (staged_on && m.max_row > 0 && m.max_row <= kSpMaxRow && static_cast<long long>(m.nnz) >= 16LL * m.n) {
+    const int tiles = (m.n + kSpRows - 1) / kSpRows;
+    const int g = std::max(1, std::min((tiles + kSpWarps - 1) / kSpWarps, num_sms(cur_device()) * 12));
+    if (checked)
+      k_spmv_int_staged<true><<<g, kSpWarps * 32, 0, st>>>(m.n, m.row_ptr, m.col_idx, m.vals, m.nnz, m.alphas, s, v,
+                                                           out, cnt, ctl);
+    else
+      k_spmv_int_staged<false><<<g, kSpWarps * 32, 0, st>>>(m.n, m.row_ptr, m.col_idx, m.vals, m.nnz, m.alphas, s, v,
+                                                            out, cnt, ctl);
+    LAUNCH_CHECK();
+    return;
+  }
   const int nt = 256;
   const int g = static_cast<int>((m.n + nt - 1) / nt > 0 ? (m.n + nt - 1) / nt : 1);
   if (checked)
@@ -3101,6 +3187,20 @@ void launch_spmv_int(cudaStream_t st, const DevSplit& m, int s, const i64* v, i6
   else
     k_spmv_int<false><<<g, nt, 0, st>>>(m.n, m.row_ptr, m.col_idx, m.vals, m.nnz, m.alphas, s, v, out, cnt, ctl);
   LAUNCH_CHECK();
+}
+
+int device_max_row(cudaStream_t st, int n, const int* rp) {
+  if (n <= 0) return 0;
+  int* d = nullptr;
+  if (cudaMalloc(reinterpret_cast<void**>(&d), sizeof(int)) != cudaSuccess) return 0;
+  cudaMemsetAsync(d, 0, sizeof(int), st);
+  k_max_row<<<grid_for(n, 256), 256, 0, st>>>(n, rp, d);
+  LAUNCH_CHECK();
+  int h = 0;
+  cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  cudaFree(d);
+  return h;
 }
 
 void launch_spmv_fp_split(cudaStream_t st, const DevSplit& m, int s, const double* x,
