@@ -440,7 +440,8 @@ void build_tri(igm_ctx* c, DevTri& t, int n, const int* rp, const int* ci, const
   t.xz = dalloc<ulonglong2>(static_cast<size_t>(std::max(n, 1)));
   ck(cudaMemsetAsync(t.xz, 0, sizeof(ulonglong2) * std::max(n, 1), st), "xz");
   t.yperm = dalloc<i64>(static_cast<size_t>(n) + 2);
-  t.stats = dalloc<u64>(2);
+  t.stats = dalloc<u64>(4);  // [max|y|, max|z|, recount CTAs done, pad]
+  ck(cudaMemset(t.stats, 0, 4 * sizeof(u64)), "stats");
   t.maxabs_l = 0;
   for (const i64 v : S.c_val) {
     const u64 a = v < 0 ? 0ull - static_cast<u64>(v) : static_cast<u64>(v);
@@ -576,8 +577,13 @@ void enqueue_cycle(igm_ctx* c, const CycleParams& p, CycleMode mode, const doubl
     i64* vj = w.basis + static_cast<long long>(j) * n;
     if (p.pre) {
       launch_spmv_int(st, *p.m, p.s, vj, w.z, cstep + K_SPMV * OP_COUNT, ctl, p.checked);
-      launch_tri_int(st, p.pre->lower, false, w.z, w.vin, cstep + K_PRECOND * OP_COUNT, ctl, p.checked);
-      launch_tri_int(st, p.pre->upper, true, w.vin, w.w, cstep + K_PRECOND * OP_COUNT, ctl, p.checked);
+      // checked mode: one recount launch for the pair (w.z, w.vin and w.w all
+      // outlive it), no stats memsets
+      const bool pair = p.checked && p.pre->lower.n == p.pre->upper.n;
+      launch_tri_int(st, p.pre->lower, false, w.z, w.vin, cstep + K_PRECOND * OP_COUNT, ctl, p.checked, pair);
+      launch_tri_int(st, p.pre->upper, true, w.vin, w.w, cstep + K_PRECOND * OP_COUNT, ctl, p.checked, pair);
+      if (pair)
+        launch_tri_count_pair(st, p.pre->lower, p.pre->upper, w.z, w.vin, w.w, cstep + K_PRECOND * OP_COUNT, ctl);
     } else {
       launch_spmv_int(st, *p.m, p.s, vj, w.w, cstep + K_SPMV * OP_COUNT, ctl, p.checked);
     }

@@ -213,7 +213,9 @@ bool launch_tri_int_piped(cudaStream_t st, const DevTri& t, bool backward, const
                           const Ctl* ctl, bool checked, const PenZ& z);
 void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward,
                     const i64* y, i64* out, u64* cnt, const Ctl* ctl,
-                    bool checked);
+                    bool checked, bool defer_count = false);
+void launch_tri_count_pair(cudaStream_t st, const DevTri& lo, const DevTri& up, const i64* y, const i64* mid,
+                           const i64* z, u64* cnt, const Ctl* ctl);
 void launch_tri_fp(cudaStream_t st, const DevTri& t, bool backward,
                    const double* y, double* out, const Ctl* ctl,
                    const double* prescale /* divide y by *prescale or null */);

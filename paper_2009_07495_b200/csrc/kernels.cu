@@ -2986,6 +2986,70 @@ __global__ void __launch_bounds__(256) k_tri_count(int n, const int* __restrict_
   bump(cnt, OP_DIV, ndiv);
 }
 
+// The two recounts of one preconditioner application (forward: y -> mid,
+// backward: mid -> z) in ONE launch on a small grid: in a configured run both
+// magnitude bounds hold and every CTA returns at once, so the cost per
+// Arnoldi step is one short launch instead of two memsets and two launches
+// on a full grid.  The last CTA to finish clears both factors' [max|y|,
+// max|z|] words for the next application (no memset nodes).
+struct TriCnt {
+  int n;
+  const int* rp;
+  const int* ci;
+  const i64* val;
+  const i64* diag;
+  u64* stats;  // [max|y|, max|z|, CTAs done]
+  double maxl;
+  int maxd;
+};
+__device__ __forceinline__ void tri_recount(const TriCnt& t, const i64* __restrict__ y, const i64* __restrict__ z,
+                                            u64& nmul, u64& nsub, u64& ndiv) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < t.n; i += gridDim.x * blockDim.x) {
+    i64 acc = y[i];
+    for (int k = t.rp[i]; k < t.rp[i + 1]; ++k) {
+      const i64 l = t.val[k], zj = z[t.ci[k]];
+      const i64 p = wmul(l, zj);
+      nmul += mul_ovf(l, zj);
+      nsub += sub_ovf(acc, p);
+      acc = wsub(acc, p);
+    }
+    ndiv += (acc == INT64_MIN && t.diag[i] == -1);
+  }
+}
+__global__ void __launch_bounds__(256) k_tri_count_pair(TriCnt lo, TriCnt up, const i64* __restrict__ y,
+                                                        const i64* __restrict__ mid, const i64* __restrict__ z,
+                                                        u64* cnt, const Ctl* ctl) {
+  __shared__ int s_skip[2];
+  if (threadIdx.x == 0) {
+    auto holds = [](const TriCnt& t) {
+      const double b = __dadd_rn(static_cast<double>(ld_cg_u64(t.stats)),
+                                 static_cast<double>(t.maxd) * t.maxl * static_cast<double>(ld_cg_u64(t.stats + 1)));
+      return b < 4611686018427387904.0;  // 2^62, as in k_tri_count
+    };
+    const bool over = cycle_over(ctl);
+    s_skip[0] = over || holds(lo);
+    s_skip[1] = over || holds(up);
+  }
+  __syncthreads();
+  if (!s_skip[0] || !s_skip[1]) {
+    u64 nmul = 0, nsub = 0, ndiv = 0;
+    if (!s_skip[0]) tri_recount(lo, y, mid, nmul, nsub, ndiv);
+    if (!s_skip[1]) tri_recount(up, mid, z, nmul, nsub, ndiv);
+    bump(cnt, OP_MUL, nmul);
+    bump(cnt, OP_SUB, nsub);
+    bump(cnt, OP_DIV, ndiv);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(reinterpret_cast<unsigned long long*>(lo.stats + 2), 1ull) == gridDim.x - 1) {
+      lo.stats[0] = lo.stats[1] = lo.stats[2] = 0;
+      up.stats[0] = up.stats[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
 TriArgs tri_args(const DevTri& t) {
   TriArgs a;
   a.n = t.n;
@@ -3750,10 +3814,35 @@ bool launch_tri_int_piped(cudaStream_t st, const DevTri& t, bool backward, const
   return true;
 }
 
+void launch_tri_count_pair(cudaStream_t st, const DevTri& lo, const DevTri& up, const i64* y, const i64* mid,
+                           const i64* z, u64* cnt, const Ctl* ctl) {
+  if (lo.n == 0) return;
+  auto mk = [](const DevTri& t) {
+    return TriCnt{t.n, t.c_rp, t.c_ci, t.c_val, t.c_diag, t.stats, static_cast<double>(t.maxabs_l), t.maxd};
+  };
+  ProfScope prof_(st, KC_OTHER);
+  const int g = std::max(1, std::min((lo.n + 255) / 256, 2 * num_sms(cur_device())));
+  k_tri_count_pair<<<g, 256, 0, st>>>(mk(lo), mk(up), y, mid, z, cnt, ctl);
+  LAUNCH_CHECK();
+}
+
+// defer_count: checked mode without the stats memset and the recount launch --
+// the caller runs launch_tri_count_pair after the forward / backward pair
 void launch_tri_int(cudaStream_t st, const DevTri& t, bool backward, const i64* y, i64* out,
-                    u64* cnt, const Ctl* ctl, bool checked) {
+                    u64* cnt, const Ctl* ctl, bool checked, bool defer_count) {
   if (t.n == 0) return;
   if (!t.pen) cudaMemsetAsync(t.ticket, 0, sizeof(int), st);  // the pencil kernel's last CTA resets it
+  if (checked && defer_count) {
+    {
+      ProfScope prof_(st, KC_TRI_INT);
+      if (t.pen) pen_launch<false>(st, t, backward, y, out, ctl, checked, nullptr);
+      else if (t.pen27 && pen27_launch(st, t, backward, y, out, ctl, checked)) {
+      } else if (backward) tri_dispatch<i64, true>(st, t, y, out, ctl, nullptr);
+      else tri_dispatch<i64, false>(st, t, y, out, ctl, nullptr);
+    }
+    LAUNCH_CHECK();
+    return;
+  }
   if (checked) cudaMemsetAsync(t.stats, 0, 2 * sizeof(u64), st);
   {
     ProfScope prof_(st, KC_TRI_INT);
