@@ -218,7 +218,7 @@ void ws_ensure(igm_ctx* c, long long n, int m) {
   w.x = dalloc<double>(nn);
   w.b = dalloc<double>(nn);
   w.x0 = dalloc<double>(nn);
-  w.vmx = dalloc<u64>(static_cast<size_t>(1024) * (mm + 2));
+  w.vmx = dalloc<u64>(static_cast<size_t>(kVmxRows) * (mm + 2));
   // small arrays
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes); return o; };
@@ -571,12 +571,18 @@ void enqueue_cycle(igm_ctx* c, const CycleParams& p, CycleMode mode, const doubl
   const bool exact = p.checked && c->exact_adds;
   void* adds = exact ? adds_scratch(c, n) : nullptr;
   const long long arn_S = exact ? 0 : arnoldi_slice(n, c->device);
+  if (p.checked && arn_S > 0)  // the all-CTA maxima of this cycle's basis vectors (atomicMax targets)
+    ck(cudaMemsetAsync(w.vmx + static_cast<size_t>(kVmxRows - 1) * (ld + 1), 0, sizeof(u64) * (ld + 1), st), "vmx");
   unsigned gbase = 0;  // grid-barrier arrivals so far in this cycle (Ctl::gbar reset by cycle_init)
   for (int j = 0; j < M; ++j) {
     u64* cstep = w.cnt + static_cast<size_t>(j) * cstride;
     i64* vj = w.basis + static_cast<long long>(j) * n;
+    // v_j's magnitude bound for the SpMV's certificate: the per-CTA maxima the
+    // persistent Arnoldi kernel of step j-1 recorded when it wrote v_j
+    const bool vb_ok = p.checked && arn_S > 0 && j > 0;
+    const u64* vb = vb_ok ? w.vmx + static_cast<size_t>(kVmxRows - 1) * (ld + 1) + j : nullptr;
     if (p.pre) {
-      launch_spmv_int(st, *p.m, p.s, vj, w.z, cstep + K_SPMV * OP_COUNT, ctl, p.checked);
+      launch_spmv_int(st, *p.m, p.s, vj, w.z, cstep + K_SPMV * OP_COUNT, ctl, p.checked, vb);
       // checked mode: one recount launch for the pair (w.z, w.vin and w.w all
       // outlive it), no stats memsets
       const bool pair = p.checked && p.pre->lower.n == p.pre->upper.n;
@@ -585,7 +591,7 @@ void enqueue_cycle(igm_ctx* c, const CycleParams& p, CycleMode mode, const doubl
       if (pair)
         launch_tri_count_pair(st, p.pre->lower, p.pre->upper, w.z, w.vin, w.w, cstep + K_PRECOND * OP_COUNT, ctl);
     } else {
-      launch_spmv_int(st, *p.m, p.s, vj, w.w, cstep + K_SPMV * OP_COUNT, ctl, p.checked);
+      launch_spmv_int(st, *p.m, p.s, vj, w.w, cstep + K_SPMV * OP_COUNT, ctl, p.checked, vb);
     }
     u64* accj = w.acc + static_cast<size_t>(j) * (M + 1);
     u64* absj = w.absacc + static_cast<size_t>(j) * (M + 1) * 2;
@@ -1002,6 +1008,7 @@ igm_status igm_upload_split(igm_ctx* c, int n, int nnz, const int* row_ptr, cons
     m->alphas = dupload(alphas, ncomp, c->stream);
     m->h_alphas = is_device_ptr(alphas) ? to_host(alphas, ncomp) : std::vector<int>(alphas, alphas + ncomp);
     m->max_row = device_max_row(c->stream, n, m->row_ptr);
+    m->max_abs0 = device_max_abs(c->stream, nnz, m->vals);
     ck(cudaStreamSynchronize(c->stream), "upload sync");
     *out = m.release();
   });

@@ -73,6 +73,7 @@ struct DevSplit {
   std::vector<int> h_row_ptr_hash;  // not used for identity, kept small
   int device = 0;
   int max_row = 0;  // longest row (selects the staged SpMV for long rows)
+  u64 max_abs0 = ~0ull;  // max |value| of component 0 (the SpMV's magnitude certificate)
 };
 
 struct DevCsrf {
@@ -178,8 +179,13 @@ struct ShiftsD {
 };
 
 int device_max_row(cudaStream_t st, int n, const int* rp);
+u64 device_max_abs(cudaStream_t st, long long n, const i64* a);
 void launch_spmv_int(cudaStream_t st, const DevSplit& m, int s, const i64* v,
-                     i64* out, u64* cnt, const Ctl* ctl, bool checked);
+                     i64* out, u64* cnt, const Ctl* ctl, bool checked,
+                     const u64* vb = nullptr);
+// Work::vmx: kVmxRows rows of (m + 2) words -- row c < grid: CTA c's max |v_i|
+// per basis vector; the last row: the maximum over all CTAs (atomicMax)
+constexpr int kVmxRows = 1024;
 void launch_spmv_fp_split(cudaStream_t st, const DevSplit& m, int s,
                           const double* x, const double* b, double* y,
                           const Ctl* ctl);

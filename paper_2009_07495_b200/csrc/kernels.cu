@@ -174,6 +174,75 @@ __global__ void __launch_bounds__(256) k_spmv_int(int n, const int* __restrict__
   }
 }
 
+// K1, short rows (<= 8 entries: 7-point stencils), split depth 0: one thread
+// per row as above, but the row's (value, column) pairs are all loaded before
+// the first gather and the gathers before the first product, so a thread
+// keeps up to 24 loads in flight instead of 2-3 (the loop above is a chain
+// of dependent loads per entry: ncu shows long-scoreboard stalls at DRAM
+// traffic equal to the algorithmic bytes).  Sums stay in CSR order.
+template <bool CHECKED>
+__global__ void __launch_bounds__(128) k_spmv_int_r8(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                     const i64* __restrict__ vals, int alpha0,
+                                                     const i64* __restrict__ v, i64* __restrict__ out, u64* cnt,
+                                                     const Ctl* ctl, u64 amax, const u64* __restrict__ vb) {
+  if (cycle_over(ctl)) return;
+  // |v| <= V: the maximum the Arnoldi kernel recorded while writing v (one
+  // word, loaded with the row's other operands)
+  const u64 V = (CHECKED && vb != nullptr) ? static_cast<u64>(__ldcg(reinterpret_cast<const unsigned long long*>(vb)))
+                                           : ~0ull;
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = row < n;
+  const int b = live ? rp[row] : 0, len = live ? rp[row + 1] - b : 0;
+  int c[8];
+  i64 a[8], x[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    c[u] = u < len ? ci[b + u] : 0;
+    a[u] = u < len ? vals[b + u] : 0;
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) x[u] = u < len ? __ldg(v + c[u]) : 0;
+  // magnitude certificate: with |a| <= amax, 8 * amax * V < 2^63 rules out
+  // every product and running-sum overflow of a row of <= 8 entries -- the
+  // exact event count is zero and the per-product tests are skipped
+  const bool safe = CHECKED && vb != nullptr && __umul64hi(amax, V) == 0 && amax * V < (1ull << 60);
+  u64 nmul = 0, nadd = 0;
+  i64 acc = 0;
+  if (!CHECKED || safe) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (u < len) acc = wadd(acc, wmul(a[u], x[u]));
+  } else {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (u < len) {
+        const i64 p = wmul(a[u], x[u]);
+        nmul += mul_ovf(a[u], x[u]);
+        nadd += add_ovf(acc, p);
+        acc = wadd(acc, p);
+      }
+    }
+  }
+  if (live) out[row] = asr(acc, alpha0);
+  if (CHECKED && !safe) {
+    bump(cnt, OP_MUL, nmul);
+    bump(cnt, OP_ADD, nadd);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_max_abs(long long n, const i64* __restrict__ a, unsigned long long* out) {
+  u64 m = 0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const i64 x = a[i];
+    const u64 ax = x < 0 ? u64{0} - static_cast<u64>(x) : static_cast<u64>(x);
+    m = ax > m ? ax : m;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, static_cast<u64>(__shfl_down_sync(0xffffffffu, m, o)));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, static_cast<unsigned long long>(m));
+}
+
 // K1, staged variant for long rows (27-point stencils: 324 B per row).  One
 // thread per row makes a warp touch 32 distant row segments per load, which
 // the L1 cannot hold until they are consumed (config 4: 0.45 of HBM).  Here a
@@ -1963,7 +2032,11 @@ __global__ void __launch_bounds__(kArnThreads, 1)
       bump(cstep + K_VEC_DIV * OP_COUNT, OP_SHL, nshl);
       bump(cstep + K_VEC_DIV * OP_COUNT, OP_DIV, ndiv);
       cta_max2(vmax, 0);
-      if (threadIdx.x == 0) vmx_me[j + 1] = s_mx[0];  // read by this CTA in later steps of the cycle
+      if (threadIdx.x == 0) {
+        vmx_me[j + 1] = s_mx[0];  // read by this CTA in later steps of the cycle
+        atomicMax(reinterpret_cast<unsigned long long*>(vmx + static_cast<size_t>(kVmxRows - 1) * vst + j + 1),
+                  static_cast<unsigned long long>(s_mx[0]));  // all CTAs: the SpMV's certificate
+      }
     }
   }
 }
@@ -2573,7 +2646,11 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
       bump(cstep + K_VEC_DIV * OP_COUNT, OP_SHL, nshl);
       bump(cstep + K_VEC_DIV * OP_COUNT, OP_DIV, ndiv);
       cta_max2(vmax, 0);
-      if (tid == 0) vmx_me[j + 1] = s_mx[0];
+      if (tid == 0) {
+        vmx_me[j + 1] = s_mx[0];
+        atomicMax(reinterpret_cast<unsigned long long*>(vmx + static_cast<size_t>(kVmxRows - 1) * vst + j + 1),
+                  static_cast<unsigned long long>(s_mx[0]));  // all CTAs: the SpMV's certificate
+      }
     }
   }
   ARN_TS(123)
@@ -3224,14 +3301,30 @@ bool PerDevice::first(int device) {
   return (bits.fetch_or(bit) & bit) == 0;
 }
 
+// vb (checked mode, may be null): a device word that bounds |v| (the maximum
+// k_arnoldi recorded over all CTAs when it wrote this basis vector)
 void launch_spmv_int(cudaStream_t st, const DevSplit& m, int s, const i64* v, i64* out, u64* cnt,
-                     const Ctl* ctl, bool checked) {
+                     const Ctl* ctl, bool checked, const u64* vb) {
   ProfScope prof_(st, KC_SPMV);
   // long rows (mean >= 16, max <= 32 entries: 27-point stencils): the staged kernel
   static const bool staged_on = [] {
     const char* e = std::getenv("IGM_SPMV_STAGED");
     return !(e && e[0] == '0');
   }();
+  static const bool r8_on = [] {
+    const char* e = std::getenv("IGM_SPMV_R8");
+    return !(e && e[0] == '0');
+  }();
+  if (r8_on && s == 0 && m.max_row > 0 && m.max_row <= 8) {
+    const int g = std::max(1, (m.n + 127) / 128);
+    const int a0 = m.h_alphas.empty() ? 0 : m.h_alphas[0];
+    if (checked)
+      k_spmv_int_r8<true><<<g, 128, 0, st>>>(m.n, m.row_ptr, m.col_idx, m.vals, a0, v, out, cnt, ctl, m.max_abs0, vb);
+    else
+      k_spmv_int_r8<false><<<g, 128, 0, st>>>(m.n, m.row_ptr, m.col_idx, m.vals, a0, v, out, cnt, ctl, 0, nullptr);
+    LAUNCH_CHECK();
+    return;
+  }
   if (staged_on && m.max_row > 0 && m.max_row <= kSpMaxRow && static_cast<long long>(m.nnz) >= 16LL * m.n) {
     const int tiles = (m.n + kSpRows - 1) / kSpRows;
     const int g = std::max(1, std::min((tiles + kSpWarps - 1) / kSpWarps, num_sms(cur_device()) * 12));
@@ -3251,6 +3344,20 @@ void launch_spmv_int(cudaStream_t st, const DevSplit& m, int s, const i64* v, i6
   else
     k_spmv_int<false><<<g, nt, 0, st>>>(m.n, m.row_ptr, m.col_idx, m.vals, m.nnz, m.alphas, s, v, out, cnt, ctl);
   LAUNCH_CHECK();
+}
+
+u64 device_max_abs(cudaStream_t st, long long n, const i64* a) {
+  if (n <= 0) return 0;
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(reinterpret_cast<void**>(&d), sizeof(unsigned long long)) != cudaSuccess) return ~0ull;
+  cudaMemsetAsync(d, 0, sizeof(unsigned long long), st);
+  k_max_abs<<<grid_for(n, 256), 256, 0, st>>>(n, a, d);
+  LAUNCH_CHECK();
+  unsigned long long h = 0;
+  cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  cudaFree(d);
+  return h;
 }
 
 int device_max_row(cudaStream_t st, int n, const int* rp) {
