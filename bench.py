@@ -420,9 +420,9 @@ def run_cfg4_sharded(args, igm, dev, local, rank, ws, g=256, m=30):
     plane relay -- dist.setup_slab_local), per step the halo planes move over
     NCCL P2P, the MGS / norm accumulators are summed through the library's
     P2P mailboxes (igm_mbox_*), the integer substitutions of the GLOBAL
-    factors hand their boundary planes on as whole planes (27-point factors;
-    7-point ones stream them pencil by pencil, dist.ZPipe), norm2 is one
-    rank-ordered FP64 chain.  Strong scaling: the global problem is the 1-GPU
+    factors stream their boundary planes to the next rank pencil by pencil
+    (dist.ZPipe, igm_dc_tri_piped: the 27-point wavefront's PIPE variant),
+    norm2 is one rank-ordered FP64 chain.  Strong scaling: the global problem is the 1-GPU
     config, and the gathered x (every word) is hashed against the reference
     library's whole-solve golden at g = 256."""
     import hashlib
