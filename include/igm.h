@@ -129,8 +129,11 @@ void igm_ilu_schedule_info(const igm_ilu* f, int backward, int* out8);
 int igm_debug_tri_schedule(int n, const int* row_ptr, const int* col_idx,
                            const int64_t* vals, const int* diag_pos, int upper,
                            int num_sms, int* out8);
-/* bricks of the pencil wavefront (structured 7-point factor, csrc/pencil.hpp)
- * that apply_inverse uses for this substitution; 0 = the generic wavefront */
+/* bricks of the pencil wavefront that apply_inverse uses for this
+ * substitution: the 7-point one (csrc/pencil.hpp, tri_pencil2.cuh) or, for
+ * factors of a 27-point stencil, the 27-point one (csrc/pencil27.cuh: selected
+ * only when all of its bricks can be resident at once, launched
+ * cooperatively); 0 = the generic wavefront */
 int igm_ilu_pencil(const igm_ilu* f, int backward);
 /* CPU-only: build the pencil record stream of one factor on a gx*gy*gz grid
  * (host arrays); returns 1 if the factor has the 7-point structure, then
