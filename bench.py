@@ -693,6 +693,13 @@ def roofline_line(breakdown, ab, n, levels, ms_step, refinements, hbm, src, micr
             "levels": levels, "us_per_level": round(per_launch_ms * 1e3 / levels, 4),
             "latency_note": "a dependent wavefront of `levels` levels: bounded by per-level latency, "
                             "not by HBM (the 8(d) bytes are reported for comparability)",
+            # the bound that does apply: `levels` dependent steps of the row recurrence (two 64-bit
+            # shuffles -> three wrapping products -> exact reciprocal division), 240 cycles per step
+            # alone in a warp (scripts/step_chain_bench.cu on this GPU) at the SM clock
+            "latency_roofline": {"chain_cycles_per_level": 240, "sm_mhz": 1965,
+                                 "floor_us": round(levels * 240 / 1965.0, 1),
+                                 "achieved_us": round(per_launch_ms * 1e3, 2),
+                                 "frac": round(levels * 240 / 1965.0 / (per_launch_ms * 1e3), 4)},
             "classes": classes, "cycle": cycle,
             "cfg5_mgs": (micro or {}).get("mgs")}
 
