@@ -844,6 +844,58 @@ def test_arnoldi_overflow_certificate(gpu, plan):
         assert outs[0]["total"] > 0
 
 
+_SPMV_CERT_SCRIPT = r"""
+import sys, json
+import numpy as np
+import paper_2009_07495_b200 as gpu
+from workloads import gen
+alpha, f = int(sys.argv[1]), int(sys.argv[2])
+rp, ci, v = gen.upwind_3d(16, 20.0)
+n = len(rp) - 1
+vals, scale = gpu.row_scale(rp, ci, v, alpha)
+comp, al, _ = gpu.build_split(vals, alpha, 1)
+S = gpu.SplitMatrix(rp, ci, comp, al)
+b = gen.uniform(31, n) / scale
+t = gpu.FxTrace(checked=True)
+try:
+    r = gpu.run_cycle(S, gpu.CycleConfig(m=6, frac_bits=f, shifts=gpu.ShiftPlan(16, 0, 16, 16, 16, 14, 16, 0)), b,
+                      np.zeros(n), trace=t)
+    st = [int(r.dim), int(np.bitwise_xor.reduce(r.basis.view(np.uint64))), int(np.bitwise_xor.reduce(r.hess.view(np.uint64)))]
+except Exception as e:
+    st = type(e).__name__
+ev = sorted(map(list, t.events))
+print(json.dumps({"state": st, "total": t.total_overflows(), "exact": t.exact, "events": ev,
+                  "spmv_events": sum(1 for e in ev if e[0] == "spmv")}))
+"""
+
+
+@pytest.mark.parametrize("alpha,f,wraps", [(16, 30, False), (40, 44, True)], ids=["configured", "products-wrap"])
+def test_spmv_magnitude_certificate(gpu, alpha, f, wraps):
+    """k_spmv_int_r8 (7-point rows, the persistent cycle of n = 4096) skips its
+    per-product overflow tests only under the magnitude certificate
+    8 * max|a| * max|v_j| < 2^63 (max|v_j| recorded by the Arnoldi kernel).
+    Its checked-mode trace and cycle state equal those of the generic
+    one-thread-per-row kernel that tests every product (IGM_SPMV_R8=0) and of
+    the separate pass kernels, which pass no bound (IGM_ARNOLDI=0) -- on a
+    configured run (no events) and with alpha_a = 40, Q19.44, where the
+    products of split.cpp:137-157 wrap and the certificate must fail."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env in ({}, {"IGM_SPMV_R8": "0"}, {"IGM_ARNOLDI": "0"}):
+        r = subprocess.run([sys.executable, "-c", _SPMV_CERT_SCRIPT, str(alpha), str(f)], cwd=root,
+                           capture_output=True, text=True, env={**os.environ, **env}, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0] == outs[1] == outs[2]
+    if wraps:
+        assert outs[0]["spmv_events"] > 0 or outs[0]["total"] > 1024
+    else:
+        assert outs[0]["total"] == 0
+
+
 _P27_SHAPES = [(12, 12, 12), (17, 35, 9), (33, 20, 7), (2, 2, 30), (40, 3, 5)]
 
 
