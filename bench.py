@@ -202,9 +202,9 @@ def ref_setup(B, rp, ci, v, bh, alpha=32):
     return sp, As, b, il
 
 
-def ref_cycle(B, sp, As, b, il, max_ref=1):
+def ref_cycle(B, sp, As, b, il, max_ref=1, m=30):
     from oracle.ffi import Shifts
-    x, rep = B.solve(sp, As, b, 1e-10, max_ref, 30, 30, 0, Shifts(0, 0, 0, 0, 30, 0, 0, 0), checked=True,
+    x, rep = B.solve(sp, As, b, 1e-10, max_ref, m, 30, 0, Shifts(0, 0, 0, 0, 30, 0, 0, 0), checked=True,
                      precond=il)
     return rep
 
@@ -249,9 +249,52 @@ def cpu_sample(rp, ci, v, bh):
                       f"threading); {rep['wall_time_sec']:.2f} s"}
 
 
+def run_reference_cfg4(args):
+    """The reference arm of `--gpus N > 1`: the B200 arm then runs config 4
+    (run_b200_sharded), so the reference's own CPU solver is timed on the same
+    system.  A whole config-4 solve takes the reference ~220 s, so each step
+    is a bounded sample: one refinement cycle of GMRES(4) (4 inner iterations:
+    SpMV + ILU(0) apply + MGS each; the MGS share is smaller than in a
+    GMRES(30) cycle, which flatters the reference by ~15 %)."""
+    g = args.cfg4_grid
+    t0 = time.time()
+    rp, ci, v = gen.stencil27_lean(g, gen.SEED_BASE ^ 4)
+    n = len(rp) - 1
+    bh = gen.spmv_np(rp, ci, v, gen.uniform(gen.SEED_BASE ^ 104, n))
+    B, kind = reference_solver()
+    sp, As, b, il = ref_setup(B, rp, ci, v, bh)
+    del v, bh
+    log(f"[bench] reference arm, config 4 at {g}^3: setup {time.time() - t0:.0f} s")
+    m = 4
+    for _ in range(args.warmup):
+        ref_cycle(B, sp, As, b, il, 1, m)
+    t, its = 0.0, 0
+    for _ in range(args.steps):
+        rep = ref_cycle(B, sp, As, b, il, 1, m)
+        t += rep["wall_time_sec"]
+        its += rep["total_inner_iterations"]
+    val = its / t
+    line = {"impl": "reference", "metric": "int-GMRES iters/s", "value": val, "unit": "iters/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic (seeded SplitMix64)",
+            "config": {"workload": f"cfg4: 3D 27-pt {g}^3 (n={n}), integer ILU(0), GMRES(30), FP64 refinement to "
+                                   f"1e-10, Q33.30, checked",
+                       "step": f"one refinement cycle of GMRES({m}) ({m} inner iterations) of the reference solver"},
+            "cpu_baseline": {"value": val, "unit": "iters/s", "cores": 1, "kind": kind,
+                             "host_cpu": host_cpu()[0], "host_cores_total": host_cpu()[1],
+                             "sample": f"each step = 1 refinement cycle of GMRES({m}) on the config-4 system; the "
+                                       f"reference is single-threaded (no threads / OpenMP in proj/core)"},
+            "e2e": {"value": val, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_reference(args, ws, rank):
     if rank != 0:
         return 0
+    if ws > 1:
+        return run_reference_cfg4(args)
     rp, ci, v, bh = config2(args.grid)
     B, kind = reference_solver()
     sp, As, b, il = ref_setup(B, rp, ci, v, bh)
