@@ -22,6 +22,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <future>
 #include <memory>
 #include <string>
 #include <thread>
@@ -261,21 +262,42 @@ bool opcache_on() {
   return on;
 }
 
-// the cached upload of `obj` (one entry per operator type and host thread)
+// the cached upload of `obj` (one entry per operator type and host thread).
+// When the addresses and sizes match the cached entry, the upload is handed
+// out at once and `pending` receives the fingerprint job: the caller runs its
+// GPU work on the cached copy while host threads verify the content, and
+// repeats the work on a fresh upload if the verification fails (solve()).
+struct PendingCheck {
+  std::vector<Span> data;
+  std::uint64_t want = 0;
+  bool active = false;
+};
+template <class Up>
+struct CacheEntry {
+  std::vector<Span> key;
+  std::uint64_t fp = 0;
+  std::unique_ptr<Up> up;
+};
+template <class Up>
+CacheEntry<Up>& cache_entry() {
+  thread_local CacheEntry<Up> e;
+  return e;
+}
 template <class Up, class Obj>
-Up& cached_upload(const Obj& obj, std::unique_ptr<Up>& fresh) {
-  struct Entry {
-    std::vector<Span> key;
-    std::uint64_t fp = 0;
-    std::unique_ptr<Up> up;
-  };
-  thread_local Entry e;
+Up& cached_upload(const Obj& obj, std::unique_ptr<Up>& fresh, PendingCheck* pending = nullptr) {
+  CacheEntry<Up>& e = cache_entry<Up>();
   if (!opcache_on()) {
     fresh = std::make_unique<Up>(obj);
     return *fresh;
   }
   std::vector<Span> key = spans_of(obj);
   std::vector<Span> data(key.begin() + 1, key.end());  // the n pseudo-span carries no bytes
+  if (pending != nullptr && e.up && e.key == key) {  // same arrays: verify the content concurrently
+    pending->data = std::move(data);
+    pending->want = e.fp;
+    pending->active = true;
+    return *e.up;
+  }
   const std::uint64_t fp = fingerprint(data);
   if (!e.up || !(e.key == key) || e.fp != fp) {
     e.up.reset();  // free the old upload first
@@ -284,6 +306,13 @@ Up& cached_upload(const Obj& obj, std::unique_ptr<Up>& fresh) {
     e.fp = fp;
   }
   return *e.up;
+}
+// a failed verification: the entry no longer describes the host arrays
+template <class Up>
+void cache_drop() {
+  CacheEntry<Up>& e = cache_entry<Up>();
+  e.up.reset();
+  e.key.clear();
 }
 
 inline double absmax_update(double acc, double v) {
@@ -833,9 +862,22 @@ SolveResult solve(const SplitMatrix& m, const CsrMatrixF& a_fp, const std::vecto
   std::unique_ptr<SplitUp> up_own;
   std::unique_ptr<CsrfUp> af_own;
   std::unique_ptr<IluUp> pre_own;
-  SplitUp& up = cached_upload(m, up_own);
-  CsrfUp& af = cached_upload(a_fp, af_own);
-  IluUp* pre = precond ? &cached_upload(*precond, pre_own) : nullptr;
+  // Operators whose arrays sit where the cached upload's did are used at once;
+  // their content fingerprints are checked on host threads while the GPU
+  // solves, and a mismatch (arrays mutated in place) repeats the solve on a
+  // fresh upload before anything is returned or thrown.
+  PendingCheck chk[3];
+  SplitUp* up = &cached_upload(m, up_own, &chk[0]);
+  CsrfUp* af = &cached_upload(a_fp, af_own, &chk[1]);
+  IluUp* pre = precond ? &cached_upload(*precond, pre_own, &chk[2]) : nullptr;
+  std::future<bool> verified;
+  if (chk[0].active || chk[1].active || chk[2].active)
+    verified = std::async(std::launch::async, [&chk] {
+      bool same = true;
+      for (const PendingCheck& c : chk)
+        if (c.active && fingerprint(c.data) != c.want) same = false;
+      return same;
+    });
   const int R = cfg.max_refinements;
   igm_refine_cfg rc{};
   rc.tol = cfg.tol;
@@ -862,12 +904,30 @@ SolveResult solve(const SplitMatrix& m, const CsrMatrixF& a_fp, const std::vecto
       trace->records_shifts()
           ? static_cast<std::size_t>(R) * cfg.m * (2 * (cfg.m + 1) + static_cast<std::size_t>(n) + 4 * cfg.m + 8)
           : 0;
-  TraceBridge tb(trace, std::min<std::size_t>(shift_cap, 1u << 26));
   SolveResult res;
   res.x.resize(static_cast<std::size_t>(n));
-  const igm_status st =
-      igm_solve(ctx(), up.h, af.h, b.data(), &rc, pre ? pre->h : nullptr, res.x.data(), &rep, tb.ptr());
-  tb.flush();
+  std::unique_ptr<TraceBridge> tb = std::make_unique<TraceBridge>(trace, std::min<std::size_t>(shift_cap, 1u << 26));
+  igm_status st =
+      igm_solve(ctx(), up->h, af->h, b.data(), &rc, pre ? pre->h : nullptr, res.x.data(), &rep, tb->ptr());
+  if (verified.valid() && !verified.get()) {
+    // some operator changed under an unchanged address: drop the stale
+    // uploads, upload again (fingerprinted synchronously) and solve again;
+    // the first run touched neither the caller's trace nor anything returned
+    if (chk[0].active) cache_drop<SplitUp>();
+    if (chk[1].active) cache_drop<CsrfUp>();
+    if (chk[2].active) cache_drop<IluUp>();
+    up = &cached_upload(m, up_own);
+    af = &cached_upload(a_fp, af_own);
+    pre = precond ? &cached_upload(*precond, pre_own) : nullptr;
+    rep = igm_report{};
+    rep.inner_dims = dims.data();
+    rep.relres_history = relres.data();
+    rep.gamma_history = gam.data();
+    rep.overflow_per_restart = ovf.data();
+    tb = std::make_unique<TraceBridge>(trace, std::min<std::size_t>(shift_cap, 1u << 26));
+    st = igm_solve(ctx(), up->h, af->h, b.data(), &rc, pre ? pre->h : nullptr, res.x.data(), &rep, tb->ptr());
+  }
+  tb->flush();
   ok(st);
   SolveReport& r = res.report;
   r.converged = rep.converged != 0;

@@ -512,6 +512,23 @@ def test_cpp_dropin_solve(gpu, oracle, tmp_path):
         assert np.array_equal(np.array([float.fromhex(t) for t in g["x"]]), x)
 
 
+def test_cpp_dropin_operator_cache(gpu, tmp_path):
+    """The C++ drop-in's verified operator cache (shim.cpp): a repeated
+    intgmres::solve on unchanged containers reuses the upload and returns the
+    same bits; operators overwritten IN PLACE (same addresses and sizes) are
+    detected by the content fingerprint, which is checked on host threads
+    while the GPU already solves on the cached copy, and the solve is repeated
+    on a fresh upload -- its result equals the one from separate containers."""
+    import subprocess
+    from tests.test_capi import build_cpp_dropin
+    exe = build_cpp_dropin(tmp_path)
+    out = subprocess.run([str(exe), "24", "cache"], check=True, capture_output=True, text=True, timeout=300).stdout
+    line = [ln for ln in out.splitlines() if ln.startswith("cache ")]
+    assert line, out
+    assert line[0].split() == ["cache", "repeat_same", "1", "inplace", "1", "mutated_detected", "1",
+                               "differs_from_first", "1"], out
+
+
 @pytest.mark.parametrize("name", ["cfg1", "cfg2_16"])
 def test_fp64_engine_vs_reference(gpu, oracle, reference, name):
     """Engine::floating_point (refsolve.cpp via refine.cpp:74-82) on the
