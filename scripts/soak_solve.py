@@ -1,0 +1,35 @@
+"""Soak: N whole config-2 solves (and M config-1-size solves with a wrapping
+plan) back to back, every x hashed against the first one / the reference
+golden -- a race in the persistent Arnoldi kernel's streaming refill, the
+pair recount or the SpMV certificate would show up as a differing word.
+
+    python scripts/soak_solve.py [n_solves]
+"""
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+import paper_2009_07495_b200 as igm  # noqa: E402
+
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+rp, ci, v, bh = bench.config2(128)
+S, A, F, b, lower, upper, _ = bench.setup_b200(rp, ci, v, bh)
+cfg = bench.solve_cfg(igm)
+with open(os.path.join(bench.ROOT, "tests", "golden", "full_goldens.json")) as f:
+    gold = json.load(f)["cfg2"]["solve"]["x"]
+t0 = time.time()
+bad = 0
+for i in range(N):
+    x, rep = igm.solve(S, A, b, cfg, precond=F)
+    h = hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest()
+    if h != gold or rep.total_inner_iterations != 150:
+        bad += 1
+        print(f"solve {i}: x differs from the reference golden ({h[:16]}), {rep.total_inner_iterations} iterations")
+print(f"{N} config-2 solves in {time.time() - t0:.1f} s, {bad} differing from the reference golden")
+sys.exit(1 if bad else 0)
