@@ -136,6 +136,7 @@ struct Work {
   unsigned char* small = nullptr;
   size_t small_bytes = 0;
   u64 *acc = nullptr, *absacc = nullptr, *nacc = nullptr, *nabs = nullptr, *cnt = nullptr;
+  u64* snap = nullptr;  // k_arnoldi2's pass snapshot slots {accumulator, arrivals} per (step, pass)
   u64* vmx = nullptr;  // per CTA and basis vector: max |v_i| over the CTA's rows (k_arnoldi certificates)
   i64 *hess = nullptr, *g = nullptr, *cs = nullptr, *sn = nullptr, *gabs = nullptr;
   int* steprec = nullptr;
@@ -224,6 +225,7 @@ void ws_ensure(igm_ctx* c, long long n, int m) {
   auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes); return o; };
   const size_t o_acc = take(sizeof(u64) * mm * (mm + 1));
   const size_t o_abs = take(sizeof(u64) * mm * (mm + 1) * 2);
+  const size_t o_snap = take(sizeof(u64) * mm * (mm + 1) * 2);
   const size_t o_nacc = take(sizeof(u64) * mm);
   const size_t o_nabs = take(sizeof(u64) * mm * 2);
   const size_t o_cnt = take(sizeof(u64) * mm * K_COUNT * OP_COUNT);
@@ -241,6 +243,7 @@ void ws_ensure(igm_ctx* c, long long n, int m) {
   ck(cudaMallocHost(reinterpret_cast<void**>(&w.h_small), off), "cudaMallocHost");
   w.acc = reinterpret_cast<u64*>(w.small + o_acc);
   w.absacc = reinterpret_cast<u64*>(w.small + o_abs);
+  w.snap = reinterpret_cast<u64*>(w.small + o_snap);
   w.nacc = reinterpret_cast<u64*>(w.small + o_nacc);
   w.nabs = reinterpret_cast<u64*>(w.small + o_nabs);
   w.cnt = reinterpret_cast<u64*>(w.small + o_cnt);
@@ -597,8 +600,9 @@ void enqueue_cycle(igm_ctx* c, const CycleParams& p, CycleMode mode, const doubl
     u64* absj = w.absacc + static_cast<size_t>(j) * (M + 1) * 2;
     if (arn_S > 0) {  // one persistent launch: passes, scalar work and vec_div
       launch_arnoldi(st, n, j, arn_S, w.w, w.basis, accj, absj, w.nacc + j, w.nabs + 2 * j, f, sh, cstep, w.hess, ld,
-                     w.g, w.cs, w.sn, w.gabs, ctl, gbase, p.checked, w.vmx);
-      gbase += static_cast<unsigned>(arnoldi_barriers(j));
+                     w.g, w.cs, w.sn, w.gabs, ctl, gbase, p.checked, w.vmx,
+                     w.snap + static_cast<size_t>(j) * (M + 1) * 2);
+      gbase += static_cast<unsigned>(arnoldi_barriers(j, arn_S));
       continue;
     }
     for (int i = 0; i <= j; ++i) {

@@ -281,10 +281,10 @@ long long arnoldi_slice(long long n, int device);
 void enqueue_cycle32(cudaStream_t st, const Wl32Work& b, const Dev32Split& m, int M, int f, int s, ShiftsD sh,
                      const double* r0, Ctl* ctl, bool checked, int xmode, double* x);
 void launch_vals_to32(cudaStream_t st, long long cnt, const i64* in, int32_t* out, int* bad);
-int arnoldi_barriers(int j);
+int arnoldi_barriers(int j, long long S);
 void launch_arnoldi(cudaStream_t st, long long n, int j, long long S, const i64* w, i64* basis, u64* accj,
                     u64* absj, u64* nacc, u64* nabs, int f, ShiftsD sh, u64* cstep, i64* hess, int ld, i64* g,
-                    i64* cs, i64* sn, i64* gabs, Ctl* ctl, unsigned gbase, bool checked, u64* vmx);
+                    i64* cs, i64* sn, i64* gabs, Ctl* ctl, unsigned gbase, bool checked, u64* vmx, u64* snapj);
 void launch_basis_norms(cudaStream_t st, long long n, int nb, int f,
                         const i64* basis, void* scratch, double* out, Ctl* ctl);
 

@@ -1742,6 +1742,65 @@ __device__ __forceinline__ void cta_reduce_add(u64 s0, u64 s1, u64 s2, u64* out0
   __syncthreads();
 }
 
+// Pass reduction and grid barrier of k_arnoldi2 in one hand-off: the CTA's
+// wrapping sum is added to the pass's SNAPSHOT slot {accumulator, arrivals}
+// (one aligned 16-byte pair, zeroed per cycle) and its arrival is counted in
+// the same slot with release semantics, so a waiter's single 128-bit load
+// returns the arrival count AND the accumulator as the L2 held them at one
+// instant -- arrivals == grid means every CTA's sum is in (each CTA's add
+// precedes its arrival).  That saves the barrier's second round trip (the
+// separate load of the accumulator after the counter was seen, ~0.7 us).
+template <bool CHECKED, int NT>
+__device__ __forceinline__ void cta_reduce_post(u64 s0, u64 s1, u64 s2, u64* snap, u64* out12, u64 (*red)[32]) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_down_sync(0xffffffffu, s0, o);
+    if (CHECKED) {
+      s1 += __shfl_down_sync(0xffffffffu, s1, o);
+      s2 += __shfl_down_sync(0xffffffffu, s2, o);
+    }
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][wid] = s0;
+    red[1][wid] = s1;
+    red[2][wid] = s2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u64 a = 0, b = 0, c = 0;
+    for (int i = 0; i < NT / 32; ++i) {
+      a += red[0][i];
+      b += red[1][i];
+      c += red[2][i];
+    }
+    atomicAdd(reinterpret_cast<unsigned long long*>(snap), static_cast<unsigned long long>(a));
+    if (CHECKED) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(out12), static_cast<unsigned long long>(b));
+      atomicAdd(reinterpret_cast<unsigned long long*>(out12 + 1), static_cast<unsigned long long>(c));
+    }
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(snap + 1) : "memory");
+  }
+}
+// waits for the pass's snapshot slot to show `grid` arrivals; returns the
+// accumulator to every thread; CTA 0 also files it in the step's accumulator
+// array (the scalar step, the host and the trace replay read it there)
+__device__ __forceinline__ u64 snap_wait(const u64* snap, unsigned grid, u64* acc_out, u64* s_word) {
+  if (threadIdx.x == 0) {
+    u64 a, c;
+    do {
+      asm volatile("{ .reg .b128 t; ld.relaxed.gpu.global.b128 t, [%2]; mov.b128 {%0, %1}, t; }"
+                   : "=l"(a), "=l"(c)
+                   : "l"(snap)
+                   : "memory");
+    } while (c < grid);
+    *s_word = a;
+    if (blockIdx.x == 0) *acc_out = a;
+  }
+  __syncthreads();
+  return *s_word;
+}
+
 // per-element pieces of the passes (identical to k_mgs / k_vec_div)
 struct ArnAcc {
   u64 sum = 0, ahi = 0, alo = 0, n1 = 0, n2 = 0, n3 = 0;
@@ -2247,7 +2306,7 @@ template <bool CHECKED>
 __global__ void __launch_bounds__(kArn2Threads, 1)
     k_arnoldi2(long long n, int j, long long S, const i64* __restrict__ win, i64* basis, u64* accj, u64* absj,
                u64* nacc, u64* nabs, int f, ShiftsD sh, u64* cstep, i64* hess, int ld, i64* g, i64* cs, i64* sn,
-               i64* gabs, Ctl* ctl, unsigned gbase, u64* vmx) {
+               i64* gabs, Ctl* ctl, unsigned gbase, u64* vmx, u64* snapj) {
   extern __shared__ __align__(16) i64 arn_sm[];
   __shared__ u64 red[3][32];
   __shared__ u64 s_word;
@@ -2412,7 +2471,7 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
     }
     if (CHECKED) bump(cD, OP_MUL, A.n3);
     ARN_TS(1)
-    cta_reduce_add<CHECKED, T>(A.sum, A.ahi, A.alo, accj + 0, absj + 0, red);
+    cta_reduce_post<CHECKED, T>(A.sum, A.ahi, A.alo, snapj + 0, absj + 0, red);
     ARN_TS(2)
     if (CHECKED) {
       cta_max2(Wb, V0);
@@ -2428,7 +2487,7 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
   };
   // ---- passes 1..j: axpy_{i-1} (v_{i-1} in buf[(i-1)&1]), dot_i (v_i in buf[i&1])
   for (int i = 1; i <= j; ++i) {
-    const i64 hs = h_of(grid_barrier<false>(ctl, (++nbar) * G, accj + i - 1, &s_word));
+    const i64 hs = h_of(snap_wait(snapj + 2 * (i - 1), G, accj + i - 1, &s_word));
     ARN_TS(4 * i - 1)
     wait_buf(i & 1);
     ARN_TS(4 * i)
@@ -2469,7 +2528,7 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
       bump(cD, OP_MUL, A.n3);
     }
     ARN_TS(4 * i + 1)
-    cta_reduce_add<CHECKED, T>(A.sum, A.ahi, A.alo, accj + i, absj + 2 * i, red);
+    cta_reduce_post<CHECKED, T>(A.sum, A.ahi, A.alo, snapj + 2 * i, absj + 2 * i, red);
     ARN_TS(4 * i + 2)
     // every thread is past its reads of v_{i-1} (the reduction's CTA barrier):
     // its buffer takes v_{i+1}.  Issued by warp 1 while thread 0 runs the grid
@@ -2484,7 +2543,7 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
   }
   // ---- axpy_j (v_j in buf[j&1]), then the norm sum of the orthogonalised w
   {
-    const i64 hs = h_of(grid_barrier<false>(ctl, (++nbar) * G, accj + j, &s_word));
+    const i64 hs = h_of(snap_wait(snapj + 2 * j, G, accj + j, &s_word));
     ARN_TS(4 * j + 3)
     const i64* vp = buf[j & 1];
     ArnAcc A;
@@ -3568,11 +3627,21 @@ long long arnoldi_slice(long long n, int device) {
   return S;
 }
 
-int arnoldi_barriers(int j) { return j + 3; }
+// counted grid-barrier arrivals per CTA of one step's launch: k_arnoldi counts
+// every pass barrier (j + 1) plus two; k_arnoldi2's pass barriers live in the
+// snapshot slots, only the two around the scalar step use the counter
+static bool arnoldi_v2(long long S) {
+  static const bool v2 = [] {
+    const char* e = std::getenv("IGM_ARNOLDI2");
+    return e == nullptr || e[0] != '0';
+  }();
+  return v2 && S <= 4LL * kArn2Threads * kArn2Q;
+}
+int arnoldi_barriers(int j, long long S) { return arnoldi_v2(S) ? 2 : j + 3; }
 
 void launch_arnoldi(cudaStream_t st, long long n, int j, long long S, const i64* w, i64* basis, u64* accj,
                     u64* absj, u64* nacc, u64* nabs, int f, ShiftsD sh, u64* cstep, i64* hess, int ld, i64* g,
-                    i64* cs, i64* sn, i64* gabs, Ctl* ctl, unsigned gbase, bool checked, u64* vmx) {
+                    i64* cs, i64* sn, i64* gabs, Ctl* ctl, unsigned gbase, bool checked, u64* vmx, u64* snapj) {
   ProfScope prof_(st, KC_MGS);
   const int dev = cur_device();
   const int G = num_sms(dev);
@@ -3589,6 +3658,8 @@ void launch_arnoldi(cudaStream_t st, long long n, int j, long long S, const i64*
     return e == nullptr || e[0] != '0';
   }();
   if (v2 && S <= 4LL * kArn2Threads * kArn2Q) {  // w fits the registers: k_arnoldi2
+    void* args2[] = {&n, &j, &S, &w, &basis, &accj, &absj, &nacc, &nabs, &f, &sh, &cstep,
+                     &hess, &ld, &g, &cs, &sn, &gabs, &ctl, &gbase, &vmx, &snapj};
     static PerDevice attr2;
     if (attr2.first(dev)) {
       cudaFuncSetAttribute(k_arnoldi2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kArnSmemMax));
@@ -3596,7 +3667,7 @@ void launch_arnoldi(cudaStream_t st, long long n, int j, long long S, const i64*
     }
     const void* fn2 =
         checked ? reinterpret_cast<const void*>(k_arnoldi2<true>) : reinterpret_cast<const void*>(k_arnoldi2<false>);
-    cudaLaunchCooperativeKernel(fn2, dim3(G), dim3(kArn2Threads), args, smem, st);
+    cudaLaunchCooperativeKernel(fn2, dim3(G), dim3(kArn2Threads), args2, smem, st);
     LAUNCH_CHECK();
     return;
   }
