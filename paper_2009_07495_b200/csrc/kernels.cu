@@ -1751,7 +1751,8 @@ __device__ __forceinline__ void cta_reduce_add(u64 s0, u64 s1, u64 s2, u64* out0
 // precedes its arrival).  That saves the barrier's second round trip (the
 // separate load of the accumulator after the counter was seen, ~0.7 us).
 template <bool CHECKED, int NT>
-__device__ __forceinline__ void cta_reduce_post(u64 s0, u64 s1, u64 s2, u64* snap, u64* out12, u64 (*red)[32]) {
+__device__ __forceinline__ void cta_reduce_post(u64 s0, u64 s1, u64 s2, u64* snap, u64* out12, u64 (*red)[32],
+                                                u64 zmask) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     s0 += __shfl_down_sync(0xffffffffu, s0, o);
@@ -1774,12 +1775,19 @@ __device__ __forceinline__ void cta_reduce_post(u64 s0, u64 s1, u64 s2, u64* sna
       b += red[1][i];
       c += red[2][i];
     }
-    atomicAdd(reinterpret_cast<unsigned long long*>(snap), static_cast<unsigned long long>(a));
-    if (CHECKED) {
+    if (CHECKED) {  // the certificate words: read after the step's later (release / acquire) barriers
       atomicAdd(reinterpret_cast<unsigned long long*>(out12), static_cast<unsigned long long>(b));
       atomicAdd(reinterpret_cast<unsigned long long*>(out12 + 1), static_cast<unsigned long long>(c));
     }
-    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(snap + 1) : "memory");
+    // The arrival must follow the sum in the slot.  Instead of a release
+    // fence (a membar over all of the thread's outstanding atomics), the sum
+    // is a RETURNING atomic and the arrival's operand depends on its result:
+    // the add has been performed at the L2 before the arrival is even issued,
+    // and both target the same 16-byte slot.  (`zmask` is 0 at run time.)
+    const unsigned long long old =
+        atomicAdd(reinterpret_cast<unsigned long long*>(snap), static_cast<unsigned long long>(a));
+    const unsigned long long inc = 1ull + (old & zmask);
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(snap + 1), "l"(inc) : "memory");
   }
 }
 // waits for the pass's snapshot slot to show `grid` arrivals; returns the
@@ -2320,6 +2328,7 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
   if (ts != nullptr && (slot) < kArnTsSlots) ts[slot] = gtimer();
   constexpr int T = kArn2Threads, Q = kArn2Q;
   const unsigned G = gridDim.x;
+  const u64 zmask = static_cast<u64>(n) >> 62;  // 0 (n < 2^62), unknown to the compiler: see cta_reduce_post
   unsigned nbar = gbase;
   const long long lo = static_cast<long long>(blockIdx.x) * S;
   const long long cnt = max(0LL, min(n, lo + S) - lo);  // a multiple of 4 (n, S are)
@@ -2471,7 +2480,7 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
     }
     if (CHECKED) bump(cD, OP_MUL, A.n3);
     ARN_TS(1)
-    cta_reduce_post<CHECKED, T>(A.sum, A.ahi, A.alo, snapj + 0, absj + 0, red);
+    cta_reduce_post<CHECKED, T>(A.sum, A.ahi, A.alo, snapj + 0, absj + 0, red, zmask);
     ARN_TS(2)
     if (CHECKED) {
       cta_max2(Wb, V0);
@@ -2528,7 +2537,7 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
       bump(cD, OP_MUL, A.n3);
     }
     ARN_TS(4 * i + 1)
-    cta_reduce_post<CHECKED, T>(A.sum, A.ahi, A.alo, snapj + 2 * i, absj + 2 * i, red);
+    cta_reduce_post<CHECKED, T>(A.sum, A.ahi, A.alo, snapj + 2 * i, absj + 2 * i, red, zmask);
     ARN_TS(4 * i + 2)
     // every thread is past its reads of v_{i-1} (the reduction's CTA barrier):
     // its buffer takes v_{i+1}.  Issued by warp 1 while thread 0 runs the grid
