@@ -2631,8 +2631,9 @@ __global__ void __launch_bounds__(kArn2Threads, 1)
     if (tid == 0) s_col[j + 1] = col[j + 1];
     __syncthreads();
     i64* w0 = s_sn + (j + 1);
+    // (no fence here: the grid barrier above acquired at gpu scope and dropped
+    // the L1's lines, and the reduced words were loaded with ld.cg)
     if (tid == 0) {
-      __threadfence();  // this SM's L1 holds no stale copy of the reduced words
       // w is only dereferenced for an error diagnostic: row 0 (this thread's first)
       *w0 = nq > 0 ? wr[0][0] : 0;
     }
