@@ -310,7 +310,20 @@ class CudaSlabBackend:
         allh = self.host_i64(mine.ravel().tolist())
         comm.d.all_reduce(allh, op=comm.d.ReduceOp.SUM, group=comm.g)
         raw = allh.cpu().numpy().astype(np.int64).tobytes()
-        self.igm._check(self.igm.lib().igm_mbox_connect_ipc(mb, (C.c_ubyte * len(raw)).from_buffer_copy(raw)))
+        # mapping a peer's buffer can fail (no P2P path between two devices):
+        # the ranks agree on the outcome, and fall back to all_reduce together
+        ok = 1
+        try:
+            self.igm._check(self.igm.lib().igm_mbox_connect_ipc(mb, (C.c_ubyte * len(raw)).from_buffer_copy(raw)))
+        except Exception as exc:  # noqa: BLE001 -- any failure disables the mailboxes on every rank
+            ok = 0
+            import warnings
+            warnings.warn(f"igm_mbox: cannot map the peers' mailboxes ({exc}); using torch.distributed all_reduce")
+        flag = self.host_i64([ok])
+        comm.d.all_reduce(flag, op=comm.d.ReduceOp.MIN, group=comm.g)
+        if int(flag[0]) == 0:
+            self.igm.lib().igm_mbox_free(mb)
+            mb = None
         cache[key] = mb
         return mb
 
