@@ -756,8 +756,17 @@ class ZPipe:
             allh = be.host_i64(mine.ravel().tolist())
             comm.sum_(allh)
             allh = allh.cpu().numpy().reshape(world, 2, 8)
-        self.exp_fwd = be.pipe_open(allh[rank + 1, 0]) if rank < world - 1 else None
-        self.exp_bwd = be.pipe_open(allh[rank - 1, 1]) if rank > 0 else None
+        # mapping a neighbour's buffer can fail (no P2P path): the ranks agree
+        # on the outcome in _pipe_for and relay whole planes together instead
+        self.ok = True
+        self.exp_fwd = self.exp_bwd = None
+        try:
+            self.exp_fwd = be.pipe_open(allh[rank + 1, 0]) if rank < world - 1 else None
+            self.exp_bwd = be.pipe_open(allh[rank - 1, 1]) if rank > 0 else None
+        except Exception as exc:  # noqa: BLE001
+            self.ok = False
+            import warnings
+            warnings.warn(f"ZPipe: cannot map the neighbour's import buffer ({exc}); relaying whole planes")
         self.kexp_fwd, self.kexp_bwd = self.planes(slab)
         self.calls = 0
 
@@ -788,7 +797,11 @@ def _pipe_for(be, slab: Slab, pre, comm, dist, group, pipe):
     cache = be.__dict__.setdefault("_zpipes", {})
     key = (slab.rank, slab.world, slab.z0, slab.z1, slab.plane, slab.nplanes)
     if key not in cache:
-        cache[key] = ZPipe(be, slab, comm)
+        zp = ZPipe(be, slab, comm)
+        with be.stream():
+            bad = be.host_i64([0 if getattr(zp, "ok", True) else 1])
+            comm.max_(bad)
+            cache[key] = None if int(bad[0]) else zp
     return cache[key]
 
 
