@@ -529,6 +529,8 @@ struct N2State {
   long long pos;  // next term
   int tail;       // the sum became non-finite at pos-1: finish serially
   double tailv;
+  int win;        // terms the next pass of n2_advance looks at (adaptive)
+  long long last_exit;  // position of the last term that left its binade
 };
 
 __device__ __forceinline__ double n2_term(long long i, const double* __restrict__ v, const i64* __restrict__ raw,
@@ -549,24 +551,39 @@ __device__ void n2_advance(long long hi, const double* __restrict__ v, const i64
     const int E = S.E;
     const u64 M0 = S.M;
     if (pos >= hi || S.tail) break;
-    const long long lim = min(hi, pos + kN2Chunk);
+    // Adaptive window: a pass costs the whole CTA ~9 us when all 8192 terms
+    // are classified and scanned, and the passes right after a binade exit
+    // usually end a few terms later (a sum that starts at 0 leaves a binade
+    // after 1, 2, 4, ... terms).  So a pass after an exit looks at 256 terms
+    // (one warp's worth) and the window doubles with every pass that ends
+    // without an exit; warps outside the window skip the classification.
+    const int win = S.win;
+    const long long lim = min(hi, pos + win);
     const long long base = pos + static_cast<long long>(tid) * kN2Per;
     u64 a[kN2Per];
     int cls[kN2Per];
     Aut mine{0, 0};
+    if (base < lim) {  // (warp-uniform up to the window's last warp)
 #pragma unroll
-    for (int g = 0; g < kN2Per; ++g) {
-      const long long idx = base + g;
-      if (idx < lim) {
-        cls[g] = n2_classify(n2_term(idx, v, raw, scale), E, a[g]);
-      } else {
+      for (int g = 0; g < kN2Per; ++g) {
+        const long long idx = base + g;
+        if (idx < lim) {
+          cls[g] = n2_classify(n2_term(idx, v, raw, scale), E, a[g]);
+        } else {
+          cls[g] = N2_DOWN;
+          a[g] = 0;
+        }
+        Aut e;
+        e.d0 = n2_inc(a[g], cls[g] == N2_EXIT ? N2_DOWN : cls[g], 0);
+        e.d1 = n2_inc(a[g], cls[g] == N2_EXIT ? N2_DOWN : cls[g], 1);
+        mine = aut_then(mine, e);
+      }
+    } else {
+#pragma unroll
+      for (int g = 0; g < kN2Per; ++g) {
         cls[g] = N2_DOWN;
         a[g] = 0;
       }
-      Aut e;
-      e.d0 = n2_inc(a[g], cls[g] == N2_EXIT ? N2_DOWN : cls[g], 0);
-      e.d1 = n2_inc(a[g], cls[g] == N2_EXIT ? N2_DOWN : cls[g], 1);
-      mine = aut_then(mine, e);
     }
     // exclusive block scan of the automata (sequence order = thread order)
     Aut inc = mine;
@@ -628,7 +645,17 @@ __device__ void n2_advance(long long hi, const double* __restrict__ v, const i64
       if (xe == INT_MAX) {
         S.M = M0 + ((M0 & 1) ? total.d1 : total.d0);
         S.pos = lim;
+        S.win = min(2 * win, kN2Chunk);
       } else {
+        // the next exit tends to be about as far from this one as this one
+        // was from the one before (a sum growing from 0 leaves its binade
+        // after 1, 2, 4, ... terms; an isolated crossing much later gets the
+        // full window back)
+        const long long gap = pos + xe - S.last_exit;
+        int wn = 256;
+        while (wn < 2 * gap && wn < kN2Chunk) wn *= 2;
+        S.win = wn;
+        S.last_exit = pos + xe;
         // replay the term that leaves the binade with the real FP64 add
         const long long idx = pos + xe;
         const double sp = ldexp(static_cast<double>(S.mprev), E - 52);
@@ -689,6 +716,8 @@ __device__ __forceinline__ void n2_init(N2State& S, const double* start) {
   S.M = 0;
   S.pos = 0;
   S.tail = 0;
+  S.win = 256;
+  S.last_exit = -1;
   const double s0 = start ? *start : 0.0;
   if (s0 != 0.0) {
     const u64 bits = static_cast<u64>(__double_as_longlong(s0));
@@ -858,6 +887,8 @@ __global__ void __launch_bounds__(kN2Threads) k_n2_walk(long long n, int nblk, c
       __syncthreads();
       b = s_fast;
       if (b >= np || S.tail) break;
+      if (threadIdx.x == 0) S.win = kN2Chunk;  // a later block: one exit at most is the rule
+      __syncthreads();
       n2_advance(min(n, static_cast<long long>(p0 + b + 1) * kN2Chunk), v, raw, scale, S);  // replay block b
       ++b;
     }
