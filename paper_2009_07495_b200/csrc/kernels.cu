@@ -180,7 +180,10 @@ __global__ void __launch_bounds__(256) k_spmv_int(int n, const int* __restrict__
 // keeps up to 24 loads in flight instead of 2-3 (the loop above is a chain
 // of dependent loads per entry: ncu shows long-scoreboard stalls at DRAM
 // traffic equal to the algorithmic bytes).  Sums stay in CSR order.
-template <bool CHECKED>
+// R = 8 (7-point stencils) or 16 (config 3's band + 10 random columns: the
+// random gathers make the dependent-load chain of the generic kernel twice as
+// costly there)
+template <bool CHECKED, int R = 8>
 __global__ void __launch_bounds__(128) k_spmv_int_r8(int n, const int* __restrict__ rp, const int* __restrict__ ci,
                                                      const i64* __restrict__ vals, int alpha0,
                                                      const i64* __restrict__ v, i64* __restrict__ out, u64* cnt,
@@ -193,28 +196,28 @@ __global__ void __launch_bounds__(128) k_spmv_int_r8(int n, const int* __restric
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = row < n;
   const int b = live ? rp[row] : 0, len = live ? rp[row + 1] - b : 0;
-  int c[8];
-  i64 a[8], x[8];
+  int c[R];
+  i64 a[R], x[R];
 #pragma unroll
-  for (int u = 0; u < 8; ++u) {
+  for (int u = 0; u < R; ++u) {
     c[u] = u < len ? ci[b + u] : 0;
     a[u] = u < len ? vals[b + u] : 0;
   }
 #pragma unroll
-  for (int u = 0; u < 8; ++u) x[u] = u < len ? __ldg(v + c[u]) : 0;
-  // magnitude certificate: with |a| <= amax, 8 * amax * V < 2^63 rules out
-  // every product and running-sum overflow of a row of <= 8 entries -- the
+  for (int u = 0; u < R; ++u) x[u] = u < len ? __ldg(v + c[u]) : 0;
+  // magnitude certificate: with |a| <= amax, R * amax * V < 2^63 rules out
+  // every product and running-sum overflow of a row of <= R entries -- the
   // exact event count is zero and the per-product tests are skipped
-  const bool safe = CHECKED && vb != nullptr && __umul64hi(amax, V) == 0 && amax * V < (1ull << 60);
+  const bool safe = CHECKED && vb != nullptr && __umul64hi(amax, V) == 0 && amax * V < (1ull << 63) / R;
   u64 nmul = 0, nadd = 0;
   i64 acc = 0;
   if (!CHECKED || safe) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < R; ++u)
       if (u < len) acc = wadd(acc, wmul(a[u], x[u]));
   } else {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < R; ++u) {
       if (u < len) {
         const i64 p = wmul(a[u], x[u]);
         nmul += mul_ovf(a[u], x[u]);
@@ -3415,13 +3418,22 @@ void launch_spmv_int(cudaStream_t st, const DevSplit& m, int s, const i64* v, i6
     const char* e = std::getenv("IGM_SPMV_R8");
     return !(e && e[0] == '0');
   }();
-  if (r8_on && s == 0 && m.max_row > 0 && m.max_row <= 8) {
+  if (r8_on && s == 0 && m.max_row > 0 && m.max_row <= 16) {
     const int g = std::max(1, (m.n + 127) / 128);
     const int a0 = m.h_alphas.empty() ? 0 : m.h_alphas[0];
-    if (checked)
-      k_spmv_int_r8<true><<<g, 128, 0, st>>>(m.n, m.row_ptr, m.col_idx, m.vals, a0, v, out, cnt, ctl, m.max_abs0, vb);
-    else
-      k_spmv_int_r8<false><<<g, 128, 0, st>>>(m.n, m.row_ptr, m.col_idx, m.vals, a0, v, out, cnt, ctl, 0, nullptr);
+    if (m.max_row <= 8) {
+      if (checked)
+        k_spmv_int_r8<true><<<g, 128, 0, st>>>(m.n, m.row_ptr, m.col_idx, m.vals, a0, v, out, cnt, ctl, m.max_abs0, vb);
+      else
+        k_spmv_int_r8<false><<<g, 128, 0, st>>>(m.n, m.row_ptr, m.col_idx, m.vals, a0, v, out, cnt, ctl, 0, nullptr);
+    } else {
+      if (checked)
+        k_spmv_int_r8<true, 16><<<g, 128, 0, st>>>(m.n, m.row_ptr, m.col_idx, m.vals, a0, v, out, cnt, ctl,
+                                                   m.max_abs0, vb);
+      else
+        k_spmv_int_r8<false, 16><<<g, 128, 0, st>>>(m.n, m.row_ptr, m.col_idx, m.vals, a0, v, out, cnt, ctl, 0,
+                                                    nullptr);
+    }
     LAUNCH_CHECK();
     return;
   }
