@@ -2714,6 +2714,7 @@ igm_status igm_split32_from_split(igm_ctx* c, const igm_split* m, igm_split32** 
     s->row_ptr = m->row_ptr;  // the pattern is shared with the WL = 64 split
     s->col_idx = m->col_idx;
     s->own_pattern = false;
+    s->max_row = m->max_row;
     s->h_alphas = m->h_alphas;
     s->device = c->device;
     const long long cnt = static_cast<long long>(m->ncomp) * m->nnz;

@@ -134,6 +134,7 @@ struct Dev32Split {
   std::vector<int> h_alphas;
   bool own_pattern = true;
   int device = 0;
+  int max_row = 0;  // longest row (rows of <= 16 entries use the register-batched SpMV)
 };
 // per-cycle buffers of the WL = 32 cycle; `small` .. small + small_bytes is
 // zeroed before every cycle (accumulators, certificates, counters, H, g, cs, sn)

@@ -168,6 +168,47 @@ __global__ void __launch_bounds__(kT) k32_spmv(int n, const int* __restrict__ rp
   }
 }
 
+// the same at depth 0 for rows of <= 16 entries: every (value, column) pair of
+// the row is loaded before the first gather and every gather before the first
+// product (as k_spmv_int_r8 does at WL = 64: the loop above chains a column
+// load, a gather and a product per entry); sums stay in CSR order
+__global__ void __launch_bounds__(128) k32_spmv_r16(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                    const int32_t* __restrict__ vals, int alpha0,
+                                                    const int32_t* __restrict__ v, int32_t* __restrict__ out, u64* cnt,
+                                                    const Ctl* ctl, int checked) {
+  if (over32(ctl)) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int k0 = __ldg(rp + i), len = __ldg(rp + i + 1) - k0;
+  int c[16];
+  int32_t a[16], x[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    c[u] = u < len ? __ldg(ci + k0 + u) : 0;
+    a[u] = u < len ? __ldg(vals + k0 + u) : 0;
+  }
+#pragma unroll
+  for (int u = 0; u < 16; ++u) x[u] = u < len ? __ldg(v + c[u]) : 0;
+  u64 nm = 0, na = 0;
+  int32_t acc = 0;
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    if (u < len) {
+      const int32_t p = mulw(a[u], x[u]);
+      if (checked) {
+        nm += mul_ovf32(a[u], x[u]);
+        na += add_ovf32(acc, p);
+      }
+      acc = static_cast<int32_t>(static_cast<uint32_t>(acc) + static_cast<uint32_t>(p));
+    }
+  }
+  out[i] = asr32(acc, alpha0);  // o = 0 + t: never an add event
+  if (checked) {
+    if (nm) atomicAdd(reinterpret_cast<unsigned long long*>(cnt + K_SPMV * OP_COUNT + OP_MUL), nm);
+    if (na) atomicAdd(reinterpret_cast<unsigned long long*>(cnt + K_SPMV * OP_COUNT + OP_ADD), na);
+  }
+}
+
 // h from a dot accumulator (fxp.cpp:63-65 at WL = 32)
 __device__ __forceinline__ int32_t h_of32(uint32_t acc, int e) {
   const int32_t a = static_cast<int32_t>(acc);
@@ -447,8 +488,12 @@ void enqueue_cycle32(cudaStream_t st, const Wl32Work& b, const Dev32Split& m, in
   for (int j = 0; j < M; ++j) {
     u64* cstep = b.cnt + static_cast<size_t>(j) * cstride;
     const int32_t* vj = b.basis + static_cast<long long>(j) * n;
-    k32_spmv<<<grid32(n), kT, 0, st>>>(m.n, m.row_ptr, m.col_idx, m.vals, m.nnz, m.alphas, s, vj, b.w, cstep, ctl,
-                                        checked ? 1 : 0);
+    if (s == 0 && m.max_row > 0 && m.max_row <= 16 && !m.h_alphas.empty())
+      k32_spmv_r16<<<(m.n + 127) / 128, 128, 0, st>>>(m.n, m.row_ptr, m.col_idx, m.vals, m.h_alphas[0], vj, b.w, cstep,
+                                                      ctl, checked ? 1 : 0);
+    else
+      k32_spmv<<<grid32(n), kT, 0, st>>>(m.n, m.row_ptr, m.col_idx, m.vals, m.nnz, m.alphas, s, vj, b.w, cstep, ctl,
+                                          checked ? 1 : 0);
     uint32_t* accj = b.acc + static_cast<size_t>(j) * (M + 1);
     u64* absj = b.abs + static_cast<size_t>(j) * (M + 1);
     for (int i = 0; i <= j; ++i) {
