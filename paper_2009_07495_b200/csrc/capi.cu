@@ -574,7 +574,7 @@ void enqueue_cycle(igm_ctx* c, const CycleParams& p, CycleMode mode, const doubl
   const bool exact = p.checked && c->exact_adds;
   void* adds = exact ? adds_scratch(c, n) : nullptr;
   const long long arn_S = exact ? 0 : arnoldi_slice(n, c->device);
-  if (p.checked && arn_S > 0)  // the all-CTA maxima of this cycle's basis vectors (atomicMax targets)
+  if (p.checked)  // the maxima over all rows of this cycle's basis vectors (atomicMax targets)
     ck(cudaMemsetAsync(w.vmx + static_cast<size_t>(kVmxRows - 1) * (ld + 1), 0, sizeof(u64) * (ld + 1), st), "vmx");
   unsigned gbase = 0;  // grid-barrier arrivals so far in this cycle (Ctl::gbar reset by cycle_init)
   for (int j = 0; j < M; ++j) {
@@ -582,7 +582,7 @@ void enqueue_cycle(igm_ctx* c, const CycleParams& p, CycleMode mode, const doubl
     i64* vj = w.basis + static_cast<long long>(j) * n;
     // v_j's magnitude bound for the SpMV's certificate: the per-CTA maxima the
     // persistent Arnoldi kernel of step j-1 recorded when it wrote v_j
-    const bool vb_ok = p.checked && arn_S > 0 && j > 0;
+    const bool vb_ok = p.checked && j > 0;  // (k_arnoldi* and k_vec_div both record it)
     const u64* vb = vb_ok ? w.vmx + static_cast<size_t>(kVmxRows - 1) * (ld + 1) + j : nullptr;
     if (p.pre) {
       launch_spmv_int(st, *p.m, p.s, vj, w.z, cstep + K_SPMV * OP_COUNT, ctl, p.checked, vb);
@@ -623,7 +623,8 @@ void enqueue_cycle(igm_ctx* c, const CycleParams& p, CycleMode mode, const doubl
     launch_step_scalar(st, j, f, sh, accj, absj, w.nacc + j, w.nabs + 2 * j, w.hess, ld, w.g, w.cs,
                        w.sn, w.gabs, w.w, cstep, ctl, exact ? 2 : (p.checked ? 1 : 0));
     launch_vec_div(st, n, w.w, w.basis + static_cast<long long>(j + 1) * n, f, sh,
-                   cstep + K_VEC_DIV * OP_COUNT, ctl, p.checked);
+                   cstep + K_VEC_DIV * OP_COUNT, ctl, p.checked,
+                   p.checked ? w.vmx + static_cast<size_t>(kVmxRows - 1) * (ld + 1) + j + 1 : nullptr);
   }
   // ---- least squares and update (gmres_int.cpp:163-180)
   launch_cycle_finish(st, M, f, w.hess, w.g, w.y, w.wts, ctl);
@@ -1013,6 +1014,22 @@ igm_status igm_upload_split(igm_ctx* c, int n, int nnz, const int* row_ptr, cons
     m->h_alphas = is_device_ptr(alphas) ? to_host(alphas, ncomp) : std::vector<int>(alphas, alphas + ncomp);
     m->max_row = device_max_row(c->stream, n, m->row_ptr);
     m->max_abs0 = device_max_abs(c->stream, nnz, m->vals);
+    if (m->max_row > 16 && m->max_row <= 32 && n >= 4096 && env_int("IGM_SPMV_SELL", 1) != 0) {
+      // sliced-ELL copy of component 0 (SpMV of 27-point rows, kernels.cu k_spmv_int_sell)
+      const size_t slots = (static_cast<size_t>(n) + 31) / 32 * 32 * static_cast<size_t>(m->max_row);
+      void *sv = nullptr, *sc = nullptr;
+      if (cudaMalloc(&sv, slots * sizeof(i64)) == cudaSuccess && cudaMalloc(&sc, slots * sizeof(int)) == cudaSuccess) {
+        m->sell_vals = static_cast<i64*>(sv);
+        m->sell_cols = static_cast<int*>(sc);
+        m->sell_w = m->max_row;
+        ck(cudaMemsetAsync(sv, 0, slots * sizeof(i64), c->stream), "sell");
+        ck(cudaMemsetAsync(sc, 0, slots * sizeof(int), c->stream), "sell");
+        launch_build_sell(c->stream, n, m->sell_w, m->row_ptr, m->col_idx, m->vals, m->sell_vals, m->sell_cols);
+      } else {  // no room for the second copy: the CSR kernels serve
+        cudaGetLastError();
+        if (sv) cudaFree(sv);
+      }
+    }
     ck(cudaStreamSynchronize(c->stream), "upload sync");
     *out = m.release();
   });
@@ -1022,6 +1039,7 @@ void igm_split_free(igm_split* m) {
   if (!m) return;
   cudaSetDevice(m->device);
   dfree(m->row_ptr); dfree(m->col_idx); dfree(m->vals); dfree(m->alphas);
+  dfree(m->sell_vals); dfree(m->sell_cols);
   delete m;
 }
 

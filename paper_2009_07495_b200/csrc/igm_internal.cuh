@@ -74,6 +74,12 @@ struct DevSplit {
   int device = 0;
   int max_row = 0;  // longest row (selects the staged SpMV for long rows)
   u64 max_abs0 = ~0ull;  // max |value| of component 0 (the SpMV's magnitude certificate)
+  // long rows (17..32 entries: 27-point stencils): component 0 once more in a
+  // sliced-ELL layout (32-row slices, slot-major, sell_w slots per row, zero
+  // padded) for coalesced matrix AND vector loads with one thread per row
+  i64* sell_vals = nullptr;
+  int* sell_cols = nullptr;
+  int sell_w = 0;
 };
 
 struct DevCsrf {
@@ -181,6 +187,7 @@ struct ShiftsD {
 
 int device_max_row(cudaStream_t st, int n, const int* rp);
 u64 device_max_abs(cudaStream_t st, long long n, const i64* a);
+void launch_build_sell(cudaStream_t st, int n, int w, const int* rp, const int* ci, const i64* vals, i64* sv, int* sc);
 void launch_spmv_int(cudaStream_t st, const DevSplit& m, int s, const i64* v,
                      i64* out, u64* cnt, const Ctl* ctl, bool checked,
                      const u64* vb = nullptr);
@@ -240,7 +247,7 @@ void launch_mgs_pass(cudaStream_t st, long long n, int mode, i64* w,
                      bool checked);
 void launch_vec_div(cudaStream_t st, long long n, const i64* w, i64* out,
                     int f, ShiftsD sh, u64* cnt, const Ctl* ctl,
-                    bool checked);
+                    bool checked, u64* vmax_out = nullptr);
 void launch_step_scalar(cudaStream_t st, int j, int f, ShiftsD sh,
                         const u64* acc_col, const u64* abs_col, const u64* nacc,
                         const u64* nabs, i64* hess, int ld, i64* g, i64* cs,

@@ -307,6 +307,75 @@ __global__ void __launch_bounds__(kSpWarps * 32) k_spmv_int_staged(int n, const 
   }
 }
 
+// K1 for long rows (17..32 entries: 27-point stencils), depth 0: sliced ELL.
+// Component 0 is kept a second time in 32-row slices, slot-major (slot u of
+// the slice's 32 rows is one contiguous run; rows shorter than the width are
+// padded with value 0 / column 0), so with one thread per row every matrix
+// load is one coalesced 256-byte (values) / 128-byte (columns) access AND
+// slot u of 32 consecutive rows gathers 32 consecutive vector words; the loads
+// of 9 slots are issued before their products.  Slot order is CSR order: the
+// running sums and their overflow events are the reference's
+// (split.cpp:137-157).  CSR keeps a 27-point warp at 32 distant row segments
+// per load (L1-wavefront bound, 0.44 of HBM); the staged kernel above pays
+// ~11 sectors per gather.
+template <bool CHECKED>
+__global__ void __launch_bounds__(128) k_spmv_int_sell(int n, int w, const i64* __restrict__ sv,
+                                                       const int* __restrict__ sc, int alpha0,
+                                                       const i64* __restrict__ v, i64* __restrict__ out, u64* cnt,
+                                                       const Ctl* ctl, u64 amax, const u64* __restrict__ vb) {
+  if (cycle_over(ctl)) return;
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 V = (CHECKED && vb != nullptr) ? static_cast<u64>(__ldcg(reinterpret_cast<const unsigned long long*>(vb)))
+                                           : ~0ull;
+  const size_t base = static_cast<size_t>(row >> 5) * w * 32 + (row & 31);
+  // magnitude certificate as in k_spmv_int_r8, for rows of <= 32 entries
+  const bool safe = CHECKED && vb != nullptr && __umul64hi(amax, V) == 0 && amax * V < (1ull << 58);
+  u64 nmul = 0, nadd = 0;
+  i64 acc = 0;
+  constexpr int B = 9;
+  for (int u0 = 0; u0 < w; u0 += B) {
+    i64 a[B], x[B];
+    int c[B];
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      const bool ok = u0 + q < w;
+      a[q] = ok ? __ldcs(sv + base + static_cast<size_t>(u0 + q) * 32) : 0;
+      c[q] = ok ? __ldcs(sc + base + static_cast<size_t>(u0 + q) * 32) : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < B; ++q) x[q] = __ldg(v + c[q]);
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      if (u0 + q < w) {
+        const i64 p = wmul(a[q], x[q]);
+        if (CHECKED && !safe) {
+          nmul += mul_ovf(a[q], x[q]);
+          nadd += add_ovf(acc, p);
+        }
+        acc = wadd(acc, p);
+      }
+    }
+  }
+  if (row < n) out[row] = asr(acc, alpha0);
+  if (CHECKED && !safe) {
+    bump(cnt, OP_MUL, nmul);
+    bump(cnt, OP_ADD, nadd);
+  }
+}
+
+__global__ void __launch_bounds__(128) k_build_sell(int n, int w, const int* __restrict__ rp,
+                                                    const int* __restrict__ ci, const i64* __restrict__ vals,
+                                                    i64* __restrict__ sv, int* __restrict__ sc) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n) return;
+  const int b = rp[row], len = rp[row + 1] - b;
+  const size_t base = static_cast<size_t>(row >> 5) * w * 32 + (row & 31);
+  for (int u = 0; u < len && u < w; ++u) {
+    sv[base + static_cast<size_t>(u) * 32] = vals[b + u];
+    sc[base + static_cast<size_t>(u) * 32] = ci[b + u];
+  }
+}
+
 __global__ void __launch_bounds__(256) k_max_row(int n, const int* __restrict__ rp, int* out) {
   int m = 0;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) m = max(m, rp[r + 1] - rp[r]);
@@ -1159,7 +1228,7 @@ __global__ void __launch_bounds__(512) k_axpy(long long n, i64* __restrict__ w, 
 template <bool CHECKED>
 __global__ void __launch_bounds__(512) k_vec_div(long long n, const i64* __restrict__ w,
                                                  i64* __restrict__ out, int f, int b1, int b2,
-                                                 u64* cnt, const Ctl* ctl) {
+                                                 u64* cnt, const Ctl* ctl, u64* vmax_out) {
   if (!ctl->do_vecdiv) return;
   SDivMagic g;
   g.u.m = ctl->div_m;
@@ -1168,7 +1237,7 @@ __global__ void __launch_bounds__(512) k_vec_div(long long n, const i64* __restr
   g.den_neg = ctl->div_neg;
   g.den_is_m1 = ctl->div_m1;
   const int e = f - b1 - b2;
-  u64 nshl = 0, ndiv = 0;
+  u64 nshl = 0, ndiv = 0, vmax = 0;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   for (long long l = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; l < n; l += stride) {
     const i64 a = w[l];
@@ -1184,12 +1253,24 @@ __global__ void __launch_bounds__(512) k_vec_div(long long n, const i64* __restr
     if (CHECKED) {
       nshl += shl_ovf(a, b1);
       ndiv += sdiv_ovf(num, g);
+      const u64 ar = r < 0 ? u64{0} - static_cast<u64>(r) : static_cast<u64>(r);
+      vmax = ar > vmax ? ar : vmax;
     }
     out[l] = r;
   }
   if (CHECKED) {
     bump(cnt, OP_SHL, nshl);
     bump(cnt, OP_DIV, ndiv);
+    // max |v_{j+1}| over all rows: the next SpMV's magnitude certificate
+    if (vmax_out != nullptr) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const u64 t = __shfl_down_sync(0xffffffffu, vmax, o);
+        vmax = t > vmax ? t : vmax;
+      }
+      if ((threadIdx.x & 31) == 0 && vmax)
+        atomicMax(reinterpret_cast<unsigned long long*>(vmax_out), static_cast<unsigned long long>(vmax));
+    }
   }
 }
 
@@ -3437,6 +3518,18 @@ void launch_spmv_int(cudaStream_t st, const DevSplit& m, int s, const i64* v, i6
     LAUNCH_CHECK();
     return;
   }
+  if (s == 0 && m.sell_vals != nullptr) {
+    const int g = std::max(1, ((m.n + 31) / 32 * 32 + 127) / 128);
+    const int a0 = m.h_alphas.empty() ? 0 : m.h_alphas[0];
+    if (checked)
+      k_spmv_int_sell<true><<<g, 128, 0, st>>>(m.n, m.sell_w, m.sell_vals, m.sell_cols, a0, v, out, cnt, ctl,
+                                               m.max_abs0, vb);
+    else
+      k_spmv_int_sell<false><<<g, 128, 0, st>>>(m.n, m.sell_w, m.sell_vals, m.sell_cols, a0, v, out, cnt, ctl, 0,
+                                                nullptr);
+    LAUNCH_CHECK();
+    return;
+  }
   if (staged_on && m.max_row > 0 && m.max_row <= kSpMaxRow && static_cast<long long>(m.nnz) >= 16LL * m.n) {
     const int tiles = (m.n + kSpRows - 1) / kSpRows;
     const int g = std::max(1, std::min((tiles + kSpWarps - 1) / kSpWarps, num_sms(cur_device()) * 12));
@@ -3470,6 +3563,13 @@ u64 device_max_abs(cudaStream_t st, long long n, const i64* a) {
   cudaStreamSynchronize(st);
   cudaFree(d);
   return h;
+}
+
+void launch_build_sell(cudaStream_t st, int n, int w, const int* rp, const int* ci, const i64* vals, i64* sv,
+                       int* sc) {
+  if (n <= 0) return;
+  k_build_sell<<<(n + 127) / 128, 128, 0, st>>>(n, w, rp, ci, vals, sv, sc);
+  LAUNCH_CHECK();
 }
 
 int device_max_row(cudaStream_t st, int n, const int* rp) {
@@ -3643,14 +3743,14 @@ void launch_axpy_only(cudaStream_t st, long long n, i64* w, i64 h, const i64* v,
 }
 
 void launch_vec_div(cudaStream_t st, long long n, const i64* w, i64* out, int f, ShiftsD sh,
-                    u64* cnt, const Ctl* ctl, bool checked) {
+                    u64* cnt, const Ctl* ctl, bool checked, u64* vmax_out) {
   ProfScope prof_(st, KC_VEC_DIV);
   const int nt = 512;
   const int g = grid_for(n, nt);
   if (checked)
-    k_vec_div<true><<<g, nt, 0, st>>>(n, w, out, f, sh.div_b1, sh.div_b2, cnt, ctl);
+    k_vec_div<true><<<g, nt, 0, st>>>(n, w, out, f, sh.div_b1, sh.div_b2, cnt, ctl, vmax_out);
   else
-    k_vec_div<false><<<g, nt, 0, st>>>(n, w, out, f, sh.div_b1, sh.div_b2, cnt, ctl);
+    k_vec_div<false><<<g, nt, 0, st>>>(n, w, out, f, sh.div_b1, sh.div_b2, cnt, ctl, nullptr);
   LAUNCH_CHECK();
 }
 

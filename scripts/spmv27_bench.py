@@ -1,6 +1,6 @@
 """Integer SpMV variants on a 27-point (config-4 family) or 7-point (config-2
-family) matrix: one thread per row against the staged long-row kernel
-(IGM_SPMV_STAGED), timed with CUDA events through the Python call (adds ~30 us
+family) matrix: one thread per row over CSR, the staged long-row kernel and
+the sliced-ELL kernel (IGM_SPMV_STAGED / IGM_SPMV_SELL), timed with CUDA events through the Python call (adds ~30 us
 per call), outputs compared by hash.
 
     python scripts/spmv27_bench.py [grid] [checked] [27|7]
@@ -39,13 +39,13 @@ if len(sys.argv) > 4:  # child: one mode
     ms = e0.elapsed_time(e1) / reps
     b = 12 * nnz + 4 * (n + 1) + 16 * n
     import hashlib
-    print(f"staged={os.environ.get('IGM_SPMV_STAGED', '1')} "
+    print(f"sell={os.environ.get('IGM_SPMV_SELL', '1')} staged={os.environ.get('IGM_SPMV_STAGED', '1')} "
           f"{sys.argv[3]}-pt g={g} checked={checked}: {ms * 1e3:.1f} us, "
           f"{b / ms / 1e6:.0f} GB/s, sha {hashlib.sha256(out.cpu().numpy().tobytes()).hexdigest()[:16]}")
 else:
     g = sys.argv[1] if len(sys.argv) > 1 else "160"
     chk = sys.argv[2] if len(sys.argv) > 2 else "1"
     kind = sys.argv[3] if len(sys.argv) > 3 else "27"
-    for staged in ("0", "1"):
+    for sell, staged in (("0", "0"), ("0", "1"), ("1", "1")):
         subprocess.run([sys.executable, __file__, g, chk, kind, "child"],
-                       env=dict(os.environ, IGM_SPMV_STAGED=staged), check=True)
+                       env=dict(os.environ, IGM_SPMV_SELL=sell, IGM_SPMV_STAGED=staged), check=True)
