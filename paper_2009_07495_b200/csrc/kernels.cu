@@ -3499,7 +3499,7 @@ void launch_spmv_int(cudaStream_t st, const DevSplit& m, int s, const i64* v, i6
     const char* e = std::getenv("IGM_SPMV_R8");
     return !(e && e[0] == '0');
   }();
-  if (r8_on && s == 0 && m.max_row > 0 && m.max_row <= 16) {
+  if (r8_on && s == 0 && m.max_row > 0 && m.max_row <= 16 && m.sell_vals == nullptr) {
     const int g = std::max(1, (m.n + 127) / 128);
     const int a0 = m.h_alphas.empty() ? 0 : m.h_alphas[0];
     if (m.max_row <= 8) {
