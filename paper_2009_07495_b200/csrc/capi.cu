@@ -1017,8 +1017,11 @@ igm_status igm_upload_split(igm_ctx* c, int n, int nnz, const int* row_ptr, cons
     // sliced-ELL copy of component 0 (kernels.cu k_spmv_int_sell) for rows of 9..32 entries.
     // Measured: config 3 (15 entries) 75 -> 58 us per call, config 4 (27) 1.96 -> 1.2 ms; 7-point
     // rows stay on the register-batched CSR kernel (config 2: 43.9 us against 46.2 us with SELL)
-    if (m->max_row >= env_int("IGM_SPMV_SELL_MIN", 9) && m->max_row <= 32 && n >= 4096 &&
-        env_int("IGM_SPMV_SELL", 1) != 0) {
+    // ... except on very long vectors (config 5, n = 64M: 1.10 -> 0.91 ms per call), where the
+    // thread-contiguous CSR loads no longer merge in the L1 as well
+    const bool sell_rows = m->max_row >= env_int("IGM_SPMV_SELL_MIN", 9) ||
+                           (m->max_row > 0 && n >= env_int("IGM_SPMV_SELL_BIGN", 8 << 20));
+    if (sell_rows && m->max_row <= 32 && n >= 4096 && env_int("IGM_SPMV_SELL", 1) != 0) {
       const size_t slots = (static_cast<size_t>(n) + 31) / 32 * 32 * static_cast<size_t>(m->max_row);
       void *sv = nullptr, *sc = nullptr;
       if (cudaMalloc(&sv, slots * sizeof(i64)) == cudaSuccess && cudaMalloc(&sc, slots * sizeof(int)) == cudaSuccess) {
