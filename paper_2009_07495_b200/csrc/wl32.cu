@@ -27,6 +27,9 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <cstring>
+
 namespace igm {
 
 namespace {
@@ -477,8 +480,85 @@ void launch_vals_to32(cudaStream_t st, long long cnt, const i64* in, int32_t* ou
 // One cycle at WL = 32 (gmres_int.cpp:42-196, unpreconditioned), enqueued on st.
 // r0: the cycle's right-hand side in FP64 (device); ctl->r0n holds its norm
 // (launch_norm2_serial mode 3 before this).  Buffers: see Wl32Work.
+static void enqueue_cycle32_launches(cudaStream_t st, const Wl32Work& b, const Dev32Split& m, int M, int f, int s,
+                                     ShiftsD sh, const double* r0, Ctl* ctl, bool checked, int xmode, double* x);
+
+// The cycle is ~M^2 / 2 short launches (1525 at M = 50) over vectors that sit
+// in the L2: launch-bound.  The sequence and every argument are fixed for a
+// given (buffers, M, shifts, ...), so it is captured once into a CUDA graph
+// and replayed per cycle (IGM_WL32_GRAPH=0: plain launches).
+namespace {
+struct Cyc32Key {
+  const void *small, *basis, *vals, *rp, *r0, *ctl, *x;
+  long long n;
+  int M, f, s, checked, xmode, max_row;
+  ShiftsD sh;
+  bool operator==(const Cyc32Key& o) const { return std::memcmp(this, &o, sizeof(Cyc32Key)) == 0; }
+};
+struct Cyc32Graph {
+  Cyc32Key key;
+  cudaGraphExec_t exec = nullptr;
+};
+}  // namespace
+
 void enqueue_cycle32(cudaStream_t st, const Wl32Work& b, const Dev32Split& m, int M, int f, int s, ShiftsD sh,
                      const double* r0, Ctl* ctl, bool checked, int xmode, double* x) {
+  static const bool use_graph = [] {
+    const char* e = std::getenv("IGM_WL32_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  if (!use_graph) {
+    enqueue_cycle32_launches(st, b, m, M, f, s, sh, r0, ctl, checked, xmode, x);
+    return;
+  }
+  Cyc32Key key;
+  std::memset(&key, 0, sizeof(key));  // (padding bytes take part in the comparison)
+  key.small = b.small;
+  key.basis = b.basis;
+  key.vals = m.vals;
+  key.rp = m.row_ptr;
+  key.r0 = r0;
+  key.ctl = ctl;
+  key.x = x;
+  key.n = m.n;
+  key.M = M;
+  key.f = f;
+  key.s = s;
+  key.checked = checked ? 1 : 0;
+  key.xmode = xmode;
+  key.max_row = m.max_row;
+  key.sh = sh;
+  thread_local Cyc32Graph cache;  // one context (stream) per host thread drives a cycle at a time
+  if (cache.exec == nullptr || !(cache.key == key)) {
+    if (cache.exec) {
+      cudaGraphExecDestroy(cache.exec);
+      cache.exec = nullptr;
+    }
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+      enqueue_cycle32_launches(st, b, m, M, f, s, sh, r0, ctl, checked, xmode, x);
+      if (cudaStreamEndCapture(st, &g) == cudaSuccess && g != nullptr &&
+          cudaGraphInstantiate(&cache.exec, g, 0) == cudaSuccess) {
+        cache.key = key;
+      } else {
+        cache.exec = nullptr;
+      }
+      if (g) cudaGraphDestroy(g);
+    }
+    if (cache.exec == nullptr) {  // capture unavailable: plain launches
+      cudaGetLastError();
+      enqueue_cycle32_launches(st, b, m, M, f, s, sh, r0, ctl, checked, xmode, x);
+      return;
+    }
+  }
+  if (cudaGraphLaunch(cache.exec, st) != cudaSuccess) {
+    cudaGetLastError();
+    enqueue_cycle32_launches(st, b, m, M, f, s, sh, r0, ctl, checked, xmode, x);
+  }
+}
+
+static void enqueue_cycle32_launches(cudaStream_t st, const Wl32Work& b, const Dev32Split& m, int M, int f, int s,
+                                     ShiftsD sh, const double* r0, Ctl* ctl, bool checked, int xmode, double* x) {
   const long long n = m.n;
   const int ld = M + 1;
   const int gr = grid32(n);
