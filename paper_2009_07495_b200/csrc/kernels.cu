@@ -325,6 +325,7 @@ __global__ void __launch_bounds__(128) k_spmv_int_sell(int n, int w, const i64* 
                                                        const Ctl* ctl, u64 amax, const u64* __restrict__ vb) {
   if (cycle_over(ctl)) return;
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= ((n + 31) & ~31)) return;  // past the last (zero-padded) slice
   const u64 V = (CHECKED && vb != nullptr) ? static_cast<u64>(__ldcg(reinterpret_cast<const unsigned long long*>(vb)))
                                            : ~0ull;
   const size_t base = static_cast<size_t>(row >> 5) * w * 32 + (row & 31);

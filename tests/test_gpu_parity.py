@@ -54,6 +54,44 @@ def test_spmv_bit_exact(gpu, oracle, goldens, name):
             assert h(gpu.spmv(c["S"], s, c["v_full"])) == goldens["cases"][name]["spmv"][str(s)]
 
 
+@pytest.mark.parametrize("kind", ["27pt_18", "band_6000", "7pt_17"])
+def test_spmv_layout_variants_bit_exact(gpu, oracle, kind, monkeypatch):
+    """The integer SpMV kernels that re-lay the matrix or its loads out --
+    k_spmv_int_sell (sliced ELL: rows of 9..32 entries), k_spmv_int_r8
+    (register-batched: short rows), k_spmv_int_staged (IGM_SPMV_SELL=0 on long
+    rows) -- against the oracle's split.cpp:137-157 on matrices of n >= 4096:
+    every output word, the checked-mode event totals and the ordered event
+    lists, on full-range vectors (products and running sums wrap) and on
+    small ones."""
+    from workloads import gen
+    if kind == "27pt_18":
+        rp, ci, v = gen.stencil27(18, 3)
+    elif kind == "band_6000":
+        rp, ci, v = gen.random_band_fast(6000, 9)
+    else:
+        rp, ci, v = gen.upwind_3d(17, 20.0)
+    n = len(rp) - 1
+    vals, _ = oracle.row_scale(oracle.csrf(rp, ci, v), 32)
+    comp, al, _ = oracle.build_split(vals, 32, 1)
+    sp = oracle.split(rp, ci, comp, al)
+    rng = np.random.default_rng(5)
+    vecs = (rng.integers(-(1 << 63), (1 << 63) - 1, n, dtype=np.int64),
+            rng.integers(-(1 << 28), 1 << 28, n, dtype=np.int64))
+    for env in ({}, {"IGM_SPMV_SELL": "0"}):
+        for k, val in env.items():
+            monkeypatch.setenv(k, val)
+        S = gpu.SplitMatrix(rp, ci, comp, al)  # (the sliced copy is decided at upload)
+        for vec in vecs:
+            t1, t2 = gpu.FxTrace(), PyTrace()
+            out = gpu.spmv(S, 0, vec, t1)
+            assert np.array_equal(out, oracle.spmv(sp, 0, vec, t2)), (kind, env)
+            assert t1.total_overflows() == t2.total
+            assert t1.events == t2.events
+            assert np.array_equal(gpu.spmv(S, 0, vec), out)  # unchecked path
+        for k in env:
+            monkeypatch.delenv(k)
+
+
 @pytest.mark.parametrize("name", ["cfg2_16", "cfg4_12", "ilu_random"])
 def test_ilu_apply_bit_exact(gpu, oracle, goldens, name):
     c = product_case(gpu, oracle, name)
