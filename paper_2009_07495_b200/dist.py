@@ -694,13 +694,18 @@ class _Comm:
         halo_exchange(self.s, own, ext, self.d, self.g)
 
     def send_np(self, a, dst):
-        """a float64 host array to rank dst (setup relay)"""
-        self.d.send(self.be.from_np(np.ascontiguousarray(a, dtype=np.float64)), dst, group=self.g)
+        """a float64 host array to rank dst (setup relay); buffer, transfer
+        and host copy all ordered on the backend's stream"""
+        with self.be.stream():
+            t = self.be.from_np(np.ascontiguousarray(a, dtype=np.float64))
+            self.d.send(t, dst, group=self.g)
+            self.be.sync()
 
     def recv_np(self, count, src):
-        t = self.be.zeros(count, "f64")
-        self.d.recv(t, src, group=self.g)
-        return self.be.to_np(t)
+        with self.be.stream():
+            t = self.be.zeros(count, "f64")
+            self.d.recv(t, src, group=self.g)
+            return self.be.to_np(t)
 
 
 def _validate_cycle(m: int, f: int, depth: int, ncomp: int, sh) -> None:
